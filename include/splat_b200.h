@@ -1,0 +1,138 @@
+/* libsplat_b200.so — C-ABI of the B200 (sm_100a) LiteGS training hot path.
+ *
+ * The reference (tinysplat, a NumPy package) has no FFI: its boundary is the
+ * Python API re-exported by pkg/src/tinysplat/__init__.py:8-25.  Each entry
+ * point below replaces the reference function cited beside it; the Python
+ * package paper_2503_01199_b200 binds them with ctypes and re-exposes the
+ * reference's names, argument order and exceptions.
+ *
+ * Conventions:
+ *   - every pointer is caller-owned DEVICE memory unless stated otherwise;
+ *   - the library never allocates device memory, never synchronises the
+ *     stream and keeps no global state; scratch comes from a caller-provided
+ *     workspace whose size is queried with the matching *_workspace_bytes();
+ *   - each call returns 0 on success or a negative SB_E* code, and sets a
+ *     thread-local message readable with sb_last_error();
+ *   - `stream` is a cudaStream_t passed as an opaque pointer (NULL = legacy
+ *     default stream).
+ *
+ * Data layout in HBM:
+ *   params  (N, 16) float32 rows: position 3 | log_scale 3 | rotation 4 (wxyz)
+ *           | color 3 | opacity_logit 1 | pad 2  (64 B, four 128-bit loads)
+ *   recs    (N_c,) 48-byte compact raster records (x, y, conic a b c, opacity,
+ *           rgb, depth, radius, flags)
+ *   sgrad   (N_c,) sb_screen_grad, 64 B
+ */
+#ifndef SPLAT_B200_H
+#define SPLAT_B200_H
+#include <stddef.h>
+#include <stdint.h>
+#include "splat_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* sb_stream_t;
+
+enum {
+    SB_OK = 0,
+    SB_EINVAL = -1,        /* bad argument (ValueError / ShapeMismatchError)   */
+    SB_ECUDA = -2,         /* CUDA launch / runtime error                      */
+    SB_EWORKSPACE = -3,    /* workspace too small                              */
+    SB_ENODEVICE = -4,     /* no sm_100 device                                 */
+};
+
+const char* sb_last_error(void);
+int sb_version(void);
+int sb_record_bytes(void);        /* sizeof compact raster record (48)          */
+int sb_screen_grad_bytes(void);   /* sizeof(sb_screen_grad) (64)                */
+
+/* ---- Morton sort (ccc.py:79-90) ------------------------------------------ */
+/* scene.py:256-260 + ccc.py:48-66: bounds -> lohi[6] (float64, device) and
+ * 63-bit Morton keys; vals = iota.  *bad_index (device int) receives the
+ * smallest index of a non-finite position, or a value >= n (0x7F7F7F7F). */
+size_t sb_morton_keys_workspace_bytes(int64_t n);
+int sb_morton_keys(const float* params, int64_t n, uint64_t* keys, uint32_t* vals, double* lohi,
+                   int32_t* bad_index, void* ws, size_t ws_bytes, sb_stream_t stream);
+
+/* ccc.py:88 np.argsort(kind="stable"): stable LSD radix sort of (key, value)
+ * pairs over key bits [0, bits).  *result_in_alt (host int) is set to 1 when
+ * the sorted data ended in keys_alt/vals_alt. */
+size_t sb_sort_workspace_bytes(int64_t n);
+int sb_radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
+                            int bits, int* result_in_alt, void* ws, size_t ws_bytes, sb_stream_t stream);
+
+/* scene.py:207-218 SceneSoA._apply(permute): dst[k][i] = src[k][perm[i]] for
+ * `count` (<= 16) arrays of row_bytes[k] bytes per row.  src/dst/row_bytes
+ * are HOST arrays of device pointers. */
+int sb_permute_rows(const uint32_t* perm, int64_t n, int count, const void* const* src, void* const* dst,
+                    const int32_t* row_bytes, sb_stream_t stream);
+
+/* ---- forward: project + cull + compact + bin (forward.py:258-290) -------- */
+/* projection.py:130-190 + ccc.py:112-194 + tiles.py:50-91 (counting).
+ * Outputs: recs[N] (first N_c used), compact_map[N] (int32, first N_c used),
+ * cluster_offset[K] (compact start of each visible cluster, -1 if culled),
+ * cluster_vis[K], tile_counts[tiles] (must be ZEROED by the caller),
+ * counters[4] (must be ZEROED): visible clusters, N_c, n_degenerate. */
+size_t sb_project_workspace_bytes(int64_t n);
+int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
+                            void* recs, int32_t* compact_map, int32_t* cluster_offset, uint8_t* cluster_vis,
+                            int32_t* tile_counts, int32_t* counters, void* ws, size_t ws_bytes, sb_stream_t stream);
+
+/* tiles.py:92-106: exclusive scan of tile_counts -> tile_offsets[ntiles + 1]
+ * (tile_offsets[ntiles] = P, the number of (tile, primitive) pairs). */
+int sb_bin_offsets(const int32_t* tile_counts, int32_t ntiles, int32_t* tile_offsets, sb_stream_t stream);
+
+/* tiles.py:75-91: emit one 64-bit key (depth_bits << 32 | compact slot) per
+ * (tile, primitive) hit into the tile's segment of pair_keys[P]. */
+size_t sb_bin_emit_workspace_bytes(int32_t ntiles);
+int sb_bin_emit(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam,
+                const int32_t* tile_offsets, uint64_t* pair_keys, void* ws, size_t ws_bytes, sb_stream_t stream);
+
+/* tiles.py:92-106 per-tile depth sort (depth asc, index tie-break):
+ * tile_prims[P] = compact slots in per-tile order.  scratch: P u64. */
+int sb_tile_sort(const int32_t* tile_offsets, int32_t ntiles, uint64_t* pair_keys, uint64_t* scratch,
+                 int32_t* tile_prims, sb_stream_t stream);
+
+/* forward.py:161-191 + 240-255: color (H,W,3), transmittance (H,W),
+ * frag_count (H,W) and last[(H,W)] = 1 + list position of each pixel's last
+ * contributing fragment (consumed by the backward). */
+int sb_raster_fwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
+                  const sb_raster_cfg* cfg, float* color, float* transmittance, int32_t* frag_count, int32_t* last,
+                  sb_stream_t stream);
+
+/* ---- backward (backward.py:205-279) --------------------------------------- */
+/* backward.py:112-267: screen-space gradients + S/M/C per compact primitive.
+ * sgrad[n_cap] is zeroed by the call. */
+int sb_raster_bwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
+                  const sb_raster_cfg* cfg, const float* dL_dI, const float* transmittance, const int32_t* last,
+                  sb_screen_grad* sgrad, int64_t n_cap, sb_stream_t stream);
+
+/* backward.py:272-278 (_chain_projection 384-516 + scatter_grads
+ * ccc.py:197-216 + stats np.add.at): grads (N, 16) float32 for every row
+ * (zero for culled clusters); S, M (float64) and C (int32) accumulated in
+ * place when non-NULL. */
+int sb_chain_projection_bwd(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
+                            const int32_t* cluster_offset, const sb_screen_grad* sgrad, float* grads, double* S,
+                            double* M, int32_t* C, sb_stream_t stream);
+
+/* ---- optimiser / densification ------------------------------------------- */
+/* optim.py:69-98: Adam (0.9, 0.999, 1e-15) on rows of true-masked clusters;
+ * params/grads/m/v (N, 16) float32, step (N,) int32, lr[5] per channel (HOST). */
+int sb_adam_sparse(float* params, const float* grads, float* m, float* v, int32_t* step,
+                   const uint8_t* cluster_mask, int64_t n, const double* lr, sb_stream_t stream);
+
+/* densify.py:57-63: max(S - M^2 / C, 0), 0 where C == 0. */
+int sb_variance_score(const double* S, const double* M, const int32_t* C, int64_t n, double* out,
+                      sb_stream_t stream);
+
+/* reduction.py:21-58 on `groups` groups of 32 float32 values:
+ * mode 0 = lane_group_reduce (float32 butterfly), 1 = exp_aligned_reduce
+ * (result cast to float32), 2 = lane_group_reduce in float64 (out_d). */
+int sb_lane_reduce(const float* values, int64_t groups, int mode, float* out_f, double* out_d, sb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,33 @@
+"""paper_2503_01199_b200: a B200-native (sm_100a) implementation of the LiteGS
+3D Gaussian Splatting training hot path, drop-in for the reference package's
+Python API (pkg/src/tinysplat/__init__.py:8-25).
+
+Morton sort, cluster-cull-compact, projection, tile binning and per-tile
+depth sort, the warp-per-tile rasterizer (forward + backward with warp
+reductions), the opacity-gradient statistics and the cluster-sparse Adam
+step run as hand-written CUDA kernels in libsplat_b200.so, called through
+its C-ABI (include/splat_b200.h).  There is no CPU fallback.
+"""
+from .backward import BackwardResult, DensifyStats, SceneGrads, backward
+from .camera import CameraView, build_frustum, look_at
+from .ccc import morton_sort
+from .densify import DensifyConfig, densify_step, opacity_decay, prune, variance_score
+from .errors import ShapeMismatchError, StaleSceneError, TrainingDiverged, ValidationError
+from .forward import RasterConfig, RenderContext, RenderOutput, forward, render
+from .metrics import loss_and_grad, psnr, ssim
+from .optim import AdamState, LearningRates, adam_step
+from .reduction import exp_aligned_reduce, lane_group_reduce
+from .scene import SceneSoA
+from .train import TrainConfig, TrainResult, train
+
+__all__ = [
+    "BackwardResult", "DensifyStats", "SceneGrads", "backward",
+    "CameraView", "build_frustum", "look_at", "morton_sort",
+    "DensifyConfig", "densify_step", "opacity_decay", "prune", "variance_score",
+    "ShapeMismatchError", "StaleSceneError", "TrainingDiverged", "ValidationError",
+    "RasterConfig", "RenderContext", "RenderOutput", "forward", "render",
+    "loss_and_grad", "psnr", "ssim", "AdamState", "LearningRates", "adam_step",
+    "exp_aligned_reduce", "lane_group_reduce", "SceneSoA", "TrainConfig", "TrainResult", "train",
+]
+
+__version__ = "0.1.0"

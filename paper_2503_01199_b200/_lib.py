@@ -1,0 +1,133 @@
+"""ctypes binding of libsplat_b200.so (include/splat_b200.h).
+
+The product path has no CPU fallback: if the library or a CUDA device is
+missing, every entry point raises `RuntimeError` naming what is absent.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import torch
+
+from .errors import ShapeMismatchError, ValidationError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsplat_b200.so")
+
+SB_OK, SB_EINVAL, SB_ECUDA, SB_EWORKSPACE, SB_ENODEVICE = 0, -1, -2, -3, -4
+
+# exported symbols and their argtypes (all pointers are c_void_p)
+VP, I64, I32, SZ = C.c_void_p, C.c_int64, C.c_int32, C.c_size_t
+SIGNATURES = {
+    "sb_last_error": ([], C.c_char_p),
+    "sb_version": ([], C.c_int),
+    "sb_record_bytes": ([], C.c_int),
+    "sb_screen_grad_bytes": ([], C.c_int),
+    "sb_morton_keys_workspace_bytes": ([I64], SZ),
+    "sb_morton_keys": ([VP, I64, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_sort_workspace_bytes": ([I64], SZ),
+    "sb_radix_sort_pairs_u64": ([VP, VP, VP, VP, I64, C.c_int, VP, VP, SZ, VP], C.c_int),
+    "sb_permute_rows": ([VP, I64, C.c_int, VP, VP, VP, VP], C.c_int),
+    "sb_project_workspace_bytes": ([I64], SZ),
+    "sb_project_cull_compact": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_bin_offsets": ([VP, I32, VP, VP], C.c_int),
+    "sb_bin_emit_workspace_bytes": ([I32], SZ),
+    "sb_bin_emit": ([VP, VP, I64, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_tile_sort": ([VP, I32, VP, VP, VP, VP], C.c_int),
+    "sb_raster_fwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP], C.c_int),
+    "sb_raster_bwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, VP], C.c_int),
+    "sb_chain_projection_bwd": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP], C.c_int),
+    "sb_adam_sparse": ([VP, VP, VP, VP, VP, VP, I64, VP, VP], C.c_int),
+    "sb_variance_score": ([VP, VP, VP, I64, VP, VP], C.c_int),
+    "sb_lane_reduce": ([VP, I64, C.c_int, VP, VP, VP], C.c_int),
+}
+
+
+class SbCamera(C.Structure):
+    _fields_ = [("w2c", C.c_double * 16), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("near_plane", C.c_double),
+                ("far_plane", C.c_double), ("planes", C.c_double * 24),
+                ("width", C.c_int32), ("height", C.c_int32), ("pad_", C.c_int32 * 2)]
+
+
+class SbRasterCfg(C.Structure):
+    _fields_ = [("alpha_min", C.c_float), ("alpha_max", C.c_float), ("t_stop", C.c_float),
+                ("background", C.c_float * 3), ("low_pass", C.c_float),
+                ("use_culling", C.c_int32), ("conic_reduce", C.c_int32), ("half_state", C.c_int32)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load the library (raises RuntimeError if it is not built)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise RuntimeError(
+                        f"libsplat_b200.so not found at {LIB_PATH}: build it with "
+                        "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+                lib = C.CDLL(LIB_PATH)
+                for name, (args, res) in SIGNATURES.items():
+                    f = getattr(lib, name)
+                    f.argtypes = args
+                    f.restype = res
+                _lib = lib
+    return _lib
+
+
+def exported_symbols():
+    return sorted(SIGNATURES)
+
+
+def require_cuda(t: torch.Tensor | None = None):
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2503_01199_b200 needs a CUDA device (B200, sm_100a); none is available")
+    if t is not None and not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+
+
+def stream_ptr(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())
+
+
+def call(name: str, *args):
+    """Call an sb_* entry point and map its status to the reference's
+    exception conventions (errors.py:6-32)."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != SB_OK:
+        msg = (lib.sb_last_error() or b"").decode()
+        if rc == SB_EINVAL:
+            raise ValueError(f"{name}: {msg}")
+        raise RuntimeError(f"{name} failed ({rc}): {msg}")
+    return rc
+
+
+# ---------------------------------------------------------------------------
+# workspace arena: one growable byte buffer per (purpose, device)
+_arena: dict = {}
+
+
+def workspace(purpose: str, nbytes: int, device) -> torch.Tensor:
+    key = (purpose, str(device))
+    buf = _arena.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes * 1.25), 256), dtype=torch.uint8, device=device)
+        _arena[key] = buf
+    return buf
+
+
+__all__ = ["load", "call", "ptr", "stream_ptr", "workspace", "SbCamera", "SbRasterCfg", "require_cuda",
+           "ShapeMismatchError", "ValidationError", "exported_symbols"]

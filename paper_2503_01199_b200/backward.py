@@ -1,0 +1,134 @@
+"""Backward: raster replay + warp reductions + projection chain, on device.
+
+Reference API: pkg/src/tinysplat/backward.py:37-92 (SceneGrads,
+DensifyStats, BackwardResult) and 205-279 (backward).  Two launches:
+
+  sb_raster_bwd            backward.py:112-267: back-to-front tile replay,
+                           per-fragment dL/dalpha, scanline fold, one warp
+                           reduction per channel, one atomic per (primitive,
+                           tile, channel), S/M/C opacity-gradient statistics
+  sb_chain_projection_bwd  backward.py:272-278: float64 chain to the raw
+                           channels + scatter_grads + stats accumulation
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .errors import ShapeMismatchError, StaleSceneError
+from .forward import RenderContext
+from .scene import CHANNEL_COLS, RAW_CHANNELS, SceneSoA
+
+GRAD_CHANNELS = RAW_CHANNELS
+SGRAD_BYTES = 64
+
+
+class SceneGrads:
+    """Per-channel gradient views over one (N, 16) float32 buffer (the
+    optimiser consumes the packed rows directly)."""
+
+    def __init__(self, packed: torch.Tensor):
+        self.packed = packed
+
+    def _col(self, name):
+        a, b = CHANNEL_COLS[name]
+        return self.packed[:, a] if b - a == 1 else self.packed[:, a:b]
+
+    position = property(lambda s: s._col("position"))
+    log_scale = property(lambda s: s._col("log_scale"))
+    rotation = property(lambda s: s._col("rotation"))
+    color = property(lambda s: s._col("color"))
+    opacity_logit = property(lambda s: s._col("opacity_logit"))
+
+    def as_dict(self):
+        return {k: self._col(k) for k in GRAD_CHANNELS}
+
+    @classmethod
+    def zeros(cls, n, device="cuda"):
+        return cls(torch.zeros((n, 16), dtype=torch.float32, device=device))
+
+    @classmethod
+    def from_dict(cls, d, n, device="cuda"):
+        out = cls.zeros(n, device)
+        for k, (a, b) in CHANNEL_COLS.items():
+            out.packed[:, a:b] = torch.as_tensor(d[k], device=device).to(torch.float32).reshape(n, b - a)
+        return out
+
+
+@dataclass
+class DensifyStats:
+    """backward.py:59-86: S = sum f^2, M = sum f (float64), C = contributing
+    fragment count (int32 on the device), per primitive."""
+    S: torch.Tensor
+    M: torch.Tensor
+    C: torch.Tensor
+
+    @classmethod
+    def zeros(cls, n, device="cuda"):
+        return cls(S=torch.zeros(n, dtype=torch.float64, device=device),
+                   M=torch.zeros(n, dtype=torch.float64, device=device),
+                   C=torch.zeros(n, dtype=torch.int32, device=device))
+
+    def reset(self):
+        self.S.zero_()
+        self.M.zero_()
+        self.C.zero_()
+
+    def attach(self, scene: SceneSoA):
+        scene.register_extra("densify_S", self.S)
+        scene.register_extra("densify_M", self.M)
+        scene.register_extra("densify_C", self.C)
+
+    @classmethod
+    def from_scene(cls, scene: SceneSoA):
+        return cls(S=scene.extras["densify_S"], M=scene.extras["densify_M"], C=scene.extras["densify_C"])
+
+
+@dataclass
+class BackwardResult:
+    grads: SceneGrads
+    stats: DensifyStats
+    cluster_mask: torch.Tensor   # (K,) bool: clusters eligible for the optimiser
+
+
+def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | None = None,
+             trace=None) -> BackwardResult:
+    """backward.py:205-279.  dL_dI is (H, W, 3) (any float dtype / device;
+    cast to float32 on the scene's device)."""
+    if trace is not None:
+        raise ValueError("per-fragment traces are a CPU-oracle debug feature")
+    if ctx.generation != scene.generation:
+        raise StaleSceneError(
+            f"render context generation {ctx.generation} != scene generation {scene.generation}")
+    W, H = ctx.camera.resolution
+    dI = torch.as_tensor(dL_dI)
+    if tuple(dI.shape) != (H, W, 3):
+        raise ShapeMismatchError(f"dL_dI shape {tuple(dI.shape)} != {(H, W, 3)}")
+    dev = scene.device
+    dI = dI.to(device=dev, dtype=torch.float32).contiguous()
+    if stats is None:
+        stats = DensifyStats.from_scene(scene) if "densify_S" in scene.extras else DensifyStats.zeros(scene.n, dev)
+    n = scene.n
+    cam_s = ctx.camera.struct()
+    cfg_s = ctx.config.struct()
+    stream = C.c_void_p(_lib.stream_ptr(dev))
+    nc = max(ctx.n_compact, 1)
+    sgrad = _lib.workspace("sgrad", nc * SGRAD_BYTES, dev)
+    _lib.call("sb_raster_bwd", _lib.ptr(ctx.recs), _lib.ptr(ctx.tile_offsets), _lib.ptr(ctx.tile_prims),
+              C.byref(cam_s), C.byref(cfg_s), _lib.ptr(dI), _lib.ptr(ctx.transmittance), _lib.ptr(ctx.last),
+              _lib.ptr(sgrad), ctx.n_compact, stream)
+    grads = torch.empty((n, 16), dtype=torch.float32, device=dev)
+    _lib.call("sb_chain_projection_bwd", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s),
+              _lib.ptr(ctx.cluster_offset), _lib.ptr(sgrad), _lib.ptr(grads), _lib.ptr(stats.S),
+              _lib.ptr(stats.M), _lib.ptr(stats.C), stream)
+    return BackwardResult(grads=SceneGrads(grads), stats=stats, cluster_mask=ctx.cluster_vis.bool())
+
+
+def screen_grads(ctx: RenderContext) -> torch.Tensor:
+    """The last backward's compact screen-space records as (N_c, 16) float32
+    view: a b c u v o r g b | C(int) | S(f64) | M(f64) (debug / parity)."""
+    buf = _lib._arena[("sgrad", str(ctx.recs.device))]
+    return buf[: ctx.n_compact * SGRAD_BYTES].view(torch.float32).reshape(ctx.n_compact, 16)

@@ -1,0 +1,104 @@
+"""Cluster-Cull-Compact host API: Morton keys / sort on the device.
+
+Reference: pkg/src/tinysplat/ccc.py.  Culling and compaction themselves run
+fused inside the forward (sb_project_cull_compact); this module exposes the
+Morton re-sort (ccc.py:59-90) and the small index helpers.
+
+  morton_encode  -> sb_morton_keys (bounds + float64 quantise + bit interleave)
+  morton_sort    -> sb_morton_keys + sb_radix_sort_pairs_u64 (63-bit keys,
+                    8 stable LSD passes) + sb_permute_rows over the parameter
+                    rows and every registered extra
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from .errors import ValidationError
+from .scene import SceneSoA
+
+CLUSTER_SIZE = 128
+MORTON_BITS = 21
+
+
+def cluster_count(n: int, cluster_size: int = CLUSTER_SIZE) -> int:
+    return (n + cluster_size - 1) // cluster_size
+
+
+def _keys(rows: torch.Tensor, n: int):
+    dev = rows.device
+    stream = C.c_void_p(_lib.stream_ptr(dev))
+    keys = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    vals = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    lohi = torch.empty(6, dtype=torch.float64, device=dev)
+    bad = torch.empty(1, dtype=torch.int32, device=dev)
+    ws = _lib.workspace("morton", _lib.load().sb_morton_keys_workspace_bytes(n), dev)
+    _lib.call("sb_morton_keys", _lib.ptr(rows), n, _lib.ptr(keys), _lib.ptr(vals), _lib.ptr(lohi), _lib.ptr(bad),
+              _lib.ptr(ws), ws.numel(), stream)
+    return keys, vals, lohi, bad
+
+
+def morton_encode_scene(scene: SceneSoA):
+    """(keys uint64-as-int64, lo, hi) for the scene's own bounds."""
+    _lib.require_cuda(scene.data)
+    keys, _, lohi, bad = _keys(scene.data, scene.n)
+    b = int(bad.item())
+    if b < scene.n:
+        raise ValidationError("position", b, "non-finite position")
+    return keys[: scene.n], lohi[:3], lohi[3:]
+
+
+def morton_sort(scene: SceneSoA) -> torch.Tensor:
+    """Stable in-place sort of the scene and all extras by Morton key
+    (ccc.py:79-90).  Returns the applied permutation (int64); bumps
+    generation even when the order was already sorted."""
+    n = scene.n
+    if n == 0:
+        scene.generation += 1
+        return torch.zeros(0, dtype=torch.int64, device=scene.device)
+    _lib.require_cuda(scene.data)
+    dev = scene.device
+    keys, vals, _, bad = _keys(scene.data, n)
+    keys_alt = torch.empty_like(keys)
+    vals_alt = torch.empty_like(vals)
+    ws = _lib.workspace("sort", _lib.load().sb_sort_workspace_bytes(n), dev)
+    flip = C.c_int(0)
+    _lib.call("sb_radix_sort_pairs_u64", _lib.ptr(keys), _lib.ptr(vals), _lib.ptr(keys_alt), _lib.ptr(vals_alt), n,
+              63, C.byref(flip), _lib.ptr(ws), ws.numel(), C.c_void_p(_lib.stream_ptr(dev)))
+    b = int(bad.item())
+    if b < n:
+        raise ValidationError("position", b, "non-finite position")
+    perm = (vals_alt if flip.value else vals)[:n]
+    scene.permute(perm)
+    return perm.to(torch.int64)
+
+
+def sort_pairs(keys: torch.Tensor, vals: torch.Tensor, bits: int = 64):
+    """Stable (key, value) sort with the hand-written LSD radix sort; keys are
+    uint64 carried in int64 tensors (unsigned order)."""
+    n = keys.numel()
+    dev = keys.device
+    k = keys.contiguous().clone()
+    v = vals.to(torch.int32).contiguous().clone()
+    ka, va = torch.empty_like(k), torch.empty_like(v)
+    ws = _lib.workspace("sort", _lib.load().sb_sort_workspace_bytes(n), dev)
+    flip = C.c_int(0)
+    _lib.call("sb_radix_sort_pairs_u64", _lib.ptr(k), _lib.ptr(v), _lib.ptr(ka), _lib.ptr(va), n, bits,
+              C.byref(flip), _lib.ptr(ws), ws.numel(), C.c_void_p(_lib.stream_ptr(dev)))
+    return (ka, va) if flip.value else (k, v)
+
+
+def scatter_grads(compact_grads: torch.Tensor, compact_map: torch.Tensor, n: int,
+                  cluster_size: int = CLUSTER_SIZE):
+    """ccc.py:197-216 for a (N_c, ...) tensor: full-length rows (zeros
+    elsewhere) and the per-cluster update mask."""
+    out = torch.zeros((n,) + tuple(compact_grads.shape[1:]), dtype=compact_grads.dtype,
+                      device=compact_grads.device)
+    idx = compact_map.long()
+    out[idx] = compact_grads
+    mask = torch.zeros(cluster_count(n, cluster_size), dtype=torch.bool, device=compact_grads.device)
+    if idx.numel():
+        mask[idx // cluster_size] = True
+    return out, mask

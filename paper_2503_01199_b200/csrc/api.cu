@@ -1,0 +1,248 @@
+// extern "C" surface of libsplat_b200.so (include/splat_b200.h).
+#include <climits>
+#include <cstdio>
+#include <string>
+#include "common.cuh"
+#include "../../include/splat_b200.h"
+
+// launchers (one per kernel family)
+void sb_launch_project_cull_compact(const float*, int, const CamDev&, int, RasterRec*, int32_t*, int32_t*, uint8_t*,
+                                    int32_t*, int32_t*, unsigned long long*, unsigned int*, cudaStream_t);
+int sb_project_blocks(int n);
+void sb_launch_tile_offsets(const int32_t*, int, int32_t*, cudaStream_t);
+void sb_launch_emit_pairs(const RasterRec*, const int32_t*, int, const int32_t*, int32_t*, unsigned long long*, int,
+                          int, int, int, cudaStream_t);
+void sb_launch_tile_sort(const int32_t*, int, unsigned long long*, unsigned long long*, int32_t*, cudaStream_t);
+void sb_launch_raster_fwd(const RasterRec*, const int32_t*, const int32_t*, int, int, int, int, const sb_raster_cfg&,
+                          float*, float*, int32_t*, int32_t*, cudaStream_t);
+void sb_launch_raster_bwd(const RasterRec*, const int32_t*, const int32_t*, int, int, int, int, const sb_raster_cfg&,
+                          const float*, const float*, const int32_t*, sb_screen_grad*, cudaStream_t);
+void sb_launch_lane_reduce(const float*, int, int, float*, double*, cudaStream_t);
+void sb_launch_chain(const float*, int, const CamDev&, const int32_t*, const sb_screen_grad*, float*, double*,
+                     double*, int32_t*, cudaStream_t);
+void sb_launch_adam(float*, const float*, float*, float*, int32_t*, const uint8_t*, int, const double[5],
+                    cudaStream_t);
+void sb_launch_variance(const double*, const double*, const int32_t*, int, double*, cudaStream_t);
+void sb_launch_bounds(const float*, int, float*, double*, cudaStream_t);
+int sb_bounds_partial_floats();
+void sb_launch_morton_keys(const float*, int, const double*, unsigned long long*, uint32_t*, int*, cudaStream_t);
+int sb_scan_blocks(int n);
+int sb_radix_blocks(int n);
+int sb_launch_radix_sort(unsigned long long*, uint32_t*, unsigned long long*, uint32_t*, int, int, uint32_t*,
+                         uint32_t*, unsigned long long*, unsigned int*, cudaStream_t);
+void sb_launch_permute(const uint32_t*, int, int, const void* const*, void* const*, const int*, cudaStream_t);
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+static int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    g_err.clear();
+    return SB_OK;
+}
+
+static inline cudaStream_t S(sb_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static CamDev make_cam(const sb_camera* c, const sb_raster_cfg* cfg) {
+    CamDev d;
+    for (int i = 0; i < 3; i++) {
+        for (int j = 0; j < 3; j++) {
+            d.R[3 * i + j] = (float)c->w2c[4 * i + j];
+            d.Rd[3 * i + j] = c->w2c[4 * i + j];
+        }
+        d.t[i] = (float)c->w2c[4 * i + 3];
+    }
+    d.fx = (float)c->fx; d.fy = (float)c->fy; d.cx = (float)c->cx; d.cy = (float)c->cy;
+    d.nearf = (float)c->near_plane; d.farf = (float)c->far_plane;
+    d.Wm1 = (float)(c->width - 1); d.Hm1 = (float)(c->height - 1);
+    d.low_pass = cfg ? cfg->low_pass : 0.3f;
+    d.W = c->width; d.H = c->height;
+    d.tiles_x = (c->width + SB_TILE_W - 1) / SB_TILE_W;
+    d.tiles_y = (c->height + SB_TILE_H - 1) / SB_TILE_H;
+    d.fxd = c->fx; d.fyd = c->fy;
+    for (int i = 0; i < 24; i++) d.planes[i] = c->planes[i];
+    return d;
+}
+
+static int check_cam(const sb_camera* c) {
+    if (!c) return fail(SB_EINVAL, "camera is NULL");
+    if (c->width <= 0 || c->height <= 0) return fail(SB_EINVAL, "resolution must be positive");
+    if (!(0.0 < c->near_plane && c->near_plane < c->far_plane)) return fail(SB_EINVAL, "need 0 < near < far");
+    return SB_OK;
+}
+
+extern "C" {
+
+const char* sb_last_error(void) { return g_err.c_str(); }
+int sb_version(void) { return 1; }
+int sb_record_bytes(void) { return (int)sizeof(RasterRec); }
+int sb_screen_grad_bytes(void) { return (int)sizeof(sb_screen_grad); }
+
+size_t sb_morton_keys_workspace_bytes(int64_t n) {
+    (void)n;
+    return align256(sizeof(float) * sb_bounds_partial_floats());
+}
+
+int sb_morton_keys(const float* params, int64_t n, uint64_t* keys, uint32_t* vals, double* lohi, int32_t* bad_index,
+                   void* ws, size_t ws_bytes, sb_stream_t stream) {
+    if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
+    if (ws_bytes < sb_morton_keys_workspace_bytes(n)) return fail(SB_EWORKSPACE, "morton workspace too small");
+    cudaMemsetAsync(bad_index, 0x7F, sizeof(int32_t), S(stream));   // 0x7F7F7F7F: no bad index
+    sb_launch_bounds(params, (int)n, static_cast<float*>(ws), lohi, S(stream));
+    sb_launch_morton_keys(params, (int)n, lohi, reinterpret_cast<unsigned long long*>(keys), vals, bad_index,
+                          S(stream));
+    return check_launch("sb_morton_keys");
+}
+
+size_t sb_sort_workspace_bytes(int64_t n) {
+    const int nb = sb_radix_blocks((int)n);
+    const size_t ncount = 256 * (size_t)nb;
+    const int sb = sb_scan_blocks((int)ncount);
+    return 2 * align256(sizeof(uint32_t) * ncount) + align256(sizeof(unsigned long long) * sb + 16);
+}
+
+int sb_radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
+                            int bits, int* result_in_alt, void* ws, size_t ws_bytes, sb_stream_t stream) {
+    if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
+    if (bits < 0 || bits > 64) return fail(SB_EINVAL, "bits out of range");
+    if (ws_bytes < sb_sort_workspace_bytes(n)) return fail(SB_EWORKSPACE, "sort workspace too small");
+    const int nb = sb_radix_blocks((int)n);
+    const size_t ncount = 256 * (size_t)nb;
+    char* w = static_cast<char*>(ws);
+    uint32_t* counts = reinterpret_cast<uint32_t*>(w);
+    w += align256(sizeof(uint32_t) * ncount);
+    uint32_t* scanned = reinterpret_cast<uint32_t*>(w);
+    w += align256(sizeof(uint32_t) * ncount);
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(w);
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(status + sb_scan_blocks((int)ncount));
+    const int flip = sb_launch_radix_sort(reinterpret_cast<unsigned long long*>(keys), vals,
+                                          reinterpret_cast<unsigned long long*>(keys_alt), vals_alt, (int)n, bits,
+                                          counts, scanned, status, ticket, S(stream));
+    if (result_in_alt) *result_in_alt = flip;
+    return check_launch("sb_radix_sort_pairs_u64");
+}
+
+int sb_permute_rows(const uint32_t* perm, int64_t n, int count, const void* const* src, void* const* dst,
+                    const int32_t* row_bytes, sb_stream_t stream) {
+    if (count < 0 || count > 16) return fail(SB_EINVAL, "at most 16 arrays per permute call");
+    if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
+    for (int k = 0; k < count; k++)
+        if (row_bytes[k] <= 0) return fail(SB_EINVAL, "row_bytes must be positive");
+    sb_launch_permute(perm, (int)n, count, src, dst, row_bytes, S(stream));
+    return check_launch("sb_permute_rows");
+}
+
+size_t sb_project_workspace_bytes(int64_t n) {
+    return align256(sizeof(unsigned long long) * (sb_project_blocks((int)n) + 1) + 16);
+}
+
+int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
+                            void* recs, int32_t* compact_map, int32_t* cluster_offset, uint8_t* cluster_vis,
+                            int32_t* tile_counts, int32_t* counters, void* ws, size_t ws_bytes, sb_stream_t stream) {
+    if (int r = check_cam(cam)) return r;
+    if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
+    if (n < 0 || n > INT32_MAX - 256) return fail(SB_EINVAL, "n out of range");
+    if (ws_bytes < sb_project_workspace_bytes(n)) return fail(SB_EWORKSPACE, "project workspace too small");
+    if (n == 0) { g_err.clear(); return SB_OK; }
+    const int blocks = sb_project_blocks((int)n);
+    unsigned long long* status = static_cast<unsigned long long*>(ws);
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(status + blocks);
+    cudaMemsetAsync(ws, 0, sizeof(unsigned long long) * blocks + 16, S(stream));
+    const CamDev d = make_cam(cam, cfg);
+    sb_launch_project_cull_compact(params, (int)n, d, cfg->use_culling, static_cast<RasterRec*>(recs), compact_map,
+                                   cluster_offset, cluster_vis, tile_counts, counters, status, ticket, S(stream));
+    return check_launch("sb_project_cull_compact");
+}
+
+int sb_bin_offsets(const int32_t* tile_counts, int32_t ntiles, int32_t* tile_offsets, sb_stream_t stream) {
+    if (ntiles <= 0) return fail(SB_EINVAL, "ntiles must be positive");
+    sb_launch_tile_offsets(tile_counts, ntiles, tile_offsets, S(stream));
+    return check_launch("sb_bin_offsets");
+}
+
+size_t sb_bin_emit_workspace_bytes(int32_t ntiles) { return align256(sizeof(int32_t) * (size_t)ntiles); }
+
+int sb_bin_emit(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam,
+                const int32_t* tile_offsets, uint64_t* pair_keys, void* ws, size_t ws_bytes, sb_stream_t stream) {
+    if (int r = check_cam(cam)) return r;
+    const CamDev d = make_cam(cam, nullptr);
+    const int ntiles = d.tiles_x * d.tiles_y;
+    if (ws_bytes < sb_bin_emit_workspace_bytes(ntiles)) return fail(SB_EWORKSPACE, "emit workspace too small");
+    cudaMemsetAsync(ws, 0, sizeof(int32_t) * ntiles, S(stream));
+    sb_launch_emit_pairs(static_cast<const RasterRec*>(recs), counters, (int)n_cap, tile_offsets,
+                         static_cast<int32_t*>(ws), reinterpret_cast<unsigned long long*>(pair_keys), d.tiles_x,
+                         d.tiles_y, d.W, d.H, S(stream));
+    return check_launch("sb_bin_emit");
+}
+
+int sb_tile_sort(const int32_t* tile_offsets, int32_t ntiles, uint64_t* pair_keys, uint64_t* scratch,
+                 int32_t* tile_prims, sb_stream_t stream) {
+    sb_launch_tile_sort(tile_offsets, ntiles, reinterpret_cast<unsigned long long*>(pair_keys),
+                        reinterpret_cast<unsigned long long*>(scratch), tile_prims, S(stream));
+    return check_launch("sb_tile_sort");
+}
+
+int sb_raster_fwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
+                  const sb_raster_cfg* cfg, float* color, float* transmittance, int32_t* frag_count, int32_t* last,
+                  sb_stream_t stream) {
+    if (int r = check_cam(cam)) return r;
+    if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
+    if (cfg->half_state) return fail(SB_EINVAL, "half_state forward is not built in this version");
+    const CamDev d = make_cam(cam, cfg);
+    sb_launch_raster_fwd(static_cast<const RasterRec*>(recs), tile_offsets, tile_prims, d.W, d.H, d.tiles_x,
+                         d.tiles_x * d.tiles_y, *cfg, color, transmittance, frag_count, last, S(stream));
+    return check_launch("sb_raster_fwd");
+}
+
+int sb_raster_bwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
+                  const sb_raster_cfg* cfg, const float* dL_dI, const float* transmittance, const int32_t* last,
+                  sb_screen_grad* sgrad, int64_t n_cap, sb_stream_t stream) {
+    if (int r = check_cam(cam)) return r;
+    if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
+    const CamDev d = make_cam(cam, cfg);
+    if (n_cap > 0) cudaMemsetAsync(sgrad, 0, sizeof(sb_screen_grad) * (size_t)n_cap, S(stream));
+    sb_launch_raster_bwd(static_cast<const RasterRec*>(recs), tile_offsets, tile_prims, d.W, d.H, d.tiles_x,
+                         d.tiles_x * d.tiles_y, *cfg, dL_dI, transmittance, last, sgrad, S(stream));
+    return check_launch("sb_raster_bwd");
+}
+
+int sb_chain_projection_bwd(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
+                            const int32_t* cluster_offset, const sb_screen_grad* sgrad, float* grads, double* S_,
+                            double* M_, int32_t* C_, sb_stream_t stream) {
+    if (int r = check_cam(cam)) return r;
+    if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
+    const CamDev d = make_cam(cam, cfg);
+    sb_launch_chain(params, (int)n, d, cluster_offset, sgrad, grads, S_, M_, C_, S(stream));
+    return check_launch("sb_chain_projection_bwd");
+}
+
+int sb_adam_sparse(float* params, const float* grads, float* m, float* v, int32_t* step, const uint8_t* cluster_mask,
+                   int64_t n, const double* lr, sb_stream_t stream) {
+    if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
+    if (!lr) return fail(SB_EINVAL, "learning rates are NULL");
+    double l5[5] = {lr[0], lr[1], lr[2], lr[3], lr[4]};
+    sb_launch_adam(params, grads, m, v, step, cluster_mask, (int)n, l5, S(stream));
+    return check_launch("sb_adam_sparse");
+}
+
+int sb_variance_score(const double* S_, const double* M_, const int32_t* C_, int64_t n, double* out,
+                      sb_stream_t stream) {
+    if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
+    sb_launch_variance(S_, M_, C_, (int)n, out, S(stream));
+    return check_launch("sb_variance_score");
+}
+
+int sb_lane_reduce(const float* values, int64_t groups, int mode, float* out_f, double* out_d, sb_stream_t stream) {
+    if (mode < 0 || mode > 2) return fail(SB_EINVAL, "mode must be 0, 1 or 2");
+    if (groups < 0 || groups > INT32_MAX / 32) return fail(SB_EINVAL, "groups out of range");
+    sb_launch_lane_reduce(values, (int)groups, mode, out_f, out_d, S(stream));
+    return check_launch("sb_lane_reduce");
+}
+
+}  // extern "C"

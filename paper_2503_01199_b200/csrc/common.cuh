@@ -1,0 +1,221 @@
+// Shared device code for libsplat_b200.so (sm_100a).
+//
+// Exact-rounding discipline: every projection / binning operation that the
+// reference performs as a separately rounded numpy op is written with the
+// explicit _rn intrinsics (never contracted into FMA); the reference's
+// k-order FMA matmul chains are written with __fmaf_rn / __fma_rn.  This is
+// what makes xy/depth/conic/radius, cull masks, compact maps and tile lists
+// bit-exact with pkg/src/tinysplat/projection.py:130-190 and tiles.py:50-107.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/splat_types.h"
+
+#define SB_INLINE __device__ __forceinline__
+
+// float32, separately rounded
+#define FMUL(a, b) __fmul_rn((a), (b))
+#define FADD(a, b) __fadd_rn((a), (b))
+#define FSUB(a, b) __fsub_rn((a), (b))
+#define FDIV(a, b) __fdiv_rn((a), (b))
+#define FFMA(a, b, c) __fmaf_rn((a), (b), (c))
+// float64, separately rounded
+#define DMUL(a, b) __dmul_rn((a), (b))
+#define DADD(a, b) __dadd_rn((a), (b))
+#define DSUB(a, b) __dsub_rn((a), (b))
+#define DDIV(a, b) __ddiv_rn((a), (b))
+#define DFMA(a, b, c) __fma_rn((a), (b), (c))
+
+// Packed parameter row (64 B): the reference's five raw channels
+// (scene.py:27-28, SceneSoA) stored as one 16-float row so one Gaussian is
+// four 128-bit loads:  [px py pz | s0 s1 s2 | qw qx qy qz | r g b | o | pad pad]
+#define SB_ROW 16
+#define SB_COL_POS 0
+#define SB_COL_LS 3
+#define SB_COL_ROT 6
+#define SB_COL_COL 10
+#define SB_COL_OPA 13
+
+// Device-side camera constants, prepared on the host from sb_camera with the
+// same float64 -> float32 casts numpy's astype performs.
+struct CamDev {
+    float R[9];          // rotation (row-major), float32
+    float t[3];
+    float fx, fy, cx, cy;
+    float nearf, farf;   // NEP 50: Python scalars compared in float32
+    float Wm1, Hm1;      // (W - 1), (H - 1) as float32
+    float low_pass;
+    int W, H;
+    int tiles_x, tiles_y;
+    double Rd[9];        // float64 rotation (projection chain, backward.py:450)
+    double fxd, fyd;
+    double planes[24];   // frustum planes (projection.py:38-65)
+};
+
+// Compact raster record (48 B): written by the fused project/cull/compact
+// kernel, gathered by binning and the rasterizer.
+struct __align__(16) RasterRec {
+    float x, y, a, b;        // screen mean, conic a, b
+    float c, o, r, g;        // conic c, opacity, colour r, g
+    float bl, depth, radius; // colour b, camera depth, 3-sigma radius
+    uint32_t flags;          // bit0 valid, bit1 in_image
+};
+
+SB_INLINE double sb_sigmoid(double x) {
+    // scene.py:31-38
+    if (x >= 0) return DDIV(1.0, DADD(1.0, exp(-x)));
+    double ex = exp(x);
+    return DDIV(ex, DADD(1.0, ex));
+}
+
+SB_INLINE void sb_quat_to_rotmat(double w, double x, double y, double z, double R[3][3]) {
+    // scene.py:46-59
+    R[0][0] = DSUB(1.0, DMUL(2.0, DADD(DMUL(y, y), DMUL(z, z))));
+    R[0][1] = DMUL(2.0, DSUB(DMUL(x, y), DMUL(w, z)));
+    R[0][2] = DMUL(2.0, DADD(DMUL(x, z), DMUL(w, y)));
+    R[1][0] = DMUL(2.0, DADD(DMUL(x, y), DMUL(w, z)));
+    R[1][1] = DSUB(1.0, DMUL(2.0, DADD(DMUL(x, x), DMUL(z, z))));
+    R[1][2] = DMUL(2.0, DSUB(DMUL(y, z), DMUL(w, x)));
+    R[2][0] = DMUL(2.0, DSUB(DMUL(x, z), DMUL(w, y)));
+    R[2][1] = DMUL(2.0, DADD(DMUL(y, z), DMUL(w, x)));
+    R[2][2] = DSUB(1.0, DMUL(2.0, DADD(DMUL(x, x), DMUL(y, y))));
+}
+
+// Full float32 projection of one Gaussian (projection.py:130-190 with
+// compose_cov3d scene.py:62-73).  Also returns the backward intermediates.
+struct ProjOut {
+    float x, y, depth, ca, cb, cc, radius;
+    float col[3], op;
+    float t[3], M[2][3], cov[3][3], sa, sb, sc;
+    float s[3], q[4];
+    bool valid, in_image, degenerate;
+};
+
+SB_INLINE void sb_project(const float* __restrict__ p, const CamDev& cam, ProjOut& o) {
+    // activations in float64, then rounded (projection.py:134-138)
+    float pos[3] = {p[0], p[1], p[2]};
+    for (int k = 0; k < 3; k++) o.s[k] = (float)exp((double)p[SB_COL_LS + k]);
+    double q0 = p[SB_COL_ROT], q1 = p[SB_COL_ROT + 1], q2 = p[SB_COL_ROT + 2], q3 = p[SB_COL_ROT + 3];
+    double qn = __dsqrt_rn(DADD(DADD(DADD(DMUL(q0, q0), DMUL(q1, q1)), DMUL(q2, q2)), DMUL(q3, q3)));
+    o.q[0] = (float)DDIV(q0, qn);
+    o.q[1] = (float)DDIV(q1, qn);
+    o.q[2] = (float)DDIV(q2, qn);
+    o.q[3] = (float)DDIV(q3, qn);
+    for (int k = 0; k < 3; k++) o.col[k] = (float)sb_sigmoid((double)p[SB_COL_COL + k]);
+    o.op = (float)sb_sigmoid((double)p[SB_COL_OPA]);
+
+    // t = pos @ R.T + trans: k-order FMA chain (numpy/OpenBLAS sgemm), then add
+    for (int j = 0; j < 3; j++)
+        o.t[j] = FADD(FFMA(pos[2], cam.R[3 * j + 2], FFMA(pos[1], cam.R[3 * j + 1], FMUL(pos[0], cam.R[3 * j]))),
+                      cam.t[j]);
+    const float tz = o.t[2];
+    const bool in_depth = (tz > cam.nearf) && (tz < cam.farf);
+    const float tzs = in_depth ? tz : 1.0f;
+    o.x = FADD(FDIV(FMUL(cam.fx, o.t[0]), tzs), cam.cx);
+    o.y = FADD(FDIV(FMUL(cam.fy, o.t[1]), tzs), cam.cy);
+    o.depth = tz;
+
+    // compose_cov3d in float64 from the float32-rounded scale / quaternion
+    {
+        double R[3][3], RD[3][3], C[3][3];
+        sb_quat_to_rotmat((double)o.q[0], (double)o.q[1], (double)o.q[2], (double)o.q[3], R);
+        double ss[3];
+        for (int j = 0; j < 3; j++) ss[j] = DMUL((double)o.s[j], (double)o.s[j]);
+        for (int i = 0; i < 3; i++)
+            for (int j = 0; j < 3; j++) RD[i][j] = DMUL(R[i][j], ss[j]);
+        for (int i = 0; i < 3; i++)
+            for (int j = 0; j < 3; j++)
+                C[i][j] = DFMA(RD[i][2], R[j][2], DFMA(RD[i][1], R[j][1], DMUL(RD[i][0], R[j][0])));
+        for (int i = 0; i < 3; i++)
+            for (int j = 0; j < 3; j++) o.cov[i][j] = (float)DMUL(0.5, DADD(C[i][j], C[j][i]));
+    }
+    const float tzz = FMUL(tzs, tzs);
+    float J[2][3];
+    J[0][0] = FDIV(cam.fx, tzs); J[0][1] = 0.0f; J[0][2] = FDIV(FMUL(-cam.fx, o.t[0]), tzz);
+    J[1][0] = 0.0f; J[1][1] = FDIV(cam.fy, tzs); J[1][2] = FDIV(FMUL(-cam.fy, o.t[1]), tzz);
+    float A[2][3], S[2][2];
+    for (int i = 0; i < 2; i++)
+        for (int j = 0; j < 3; j++)
+            o.M[i][j] = FFMA(J[i][2], cam.R[6 + j], FFMA(J[i][1], cam.R[3 + j], FMUL(J[i][0], cam.R[j])));
+    for (int i = 0; i < 2; i++)
+        for (int j = 0; j < 3; j++)
+            A[i][j] = FFMA(o.M[i][2], o.cov[2][j], FFMA(o.M[i][1], o.cov[1][j], FMUL(o.M[i][0], o.cov[0][j])));
+    for (int i = 0; i < 2; i++)
+        for (int j = 0; j < 2; j++)
+            S[i][j] = FFMA(A[i][2], o.M[j][2], FFMA(A[i][1], o.M[j][1], FMUL(A[i][0], o.M[j][0])));
+    o.sa = FADD(S[0][0], cam.low_pass);
+    o.sb = S[0][1];
+    o.sc = FADD(S[1][1], cam.low_pass);
+    const float det = FSUB(FMUL(o.sa, o.sc), FMUL(o.sb, o.sb));
+    const bool nondeg = det > 0.0f;
+    o.degenerate = in_depth && !nondeg;
+    const float dets = nondeg ? det : 1.0f;
+    o.ca = FDIV(o.sc, dets);
+    o.cb = FDIV(-o.sb, dets);
+    o.cc = FDIV(o.sa, dets);
+    const float mid = FMUL(0.5f, FADD(o.sa, o.sc));
+    float disc = FSUB(FMUL(mid, mid), dets);
+    if (!(disc >= 0.0f)) disc = (disc != disc) ? disc : 0.0f;  // np.maximum propagates NaN
+    const float lam = FADD(mid, __fsqrt_rn(disc));
+    o.radius = FMUL(3.0f, __fsqrt_rn(lam));
+    o.valid = in_depth && nondeg;
+    o.in_image = o.valid && (FADD(o.x, o.radius) >= 0.0f) && (FSUB(o.x, o.radius) <= cam.Wm1) &&
+                 (FADD(o.y, o.radius) >= 0.0f) && (FSUB(o.y, o.radius) <= cam.Hm1);
+}
+
+// np.clip(np.floor(v).astype(int64), 0, hi) (tiles.py:70-73)
+SB_INLINE int sb_clip_floor(float v, int hi) {
+    float f = floorf(v);
+    if (!(f >= 0.0f)) return 0;
+    if (f > (float)hi) return hi;
+    return (int)f;
+}
+
+// Candidate tile rectangle of a footprint disc (tiles.py:70-73), float32
+SB_INLINE void sb_tile_range(float cx, float cy, float r, int txn, int tyn, int& tx0, int& tx1, int& ty0,
+                             int& ty1) {
+    tx0 = sb_clip_floor(FDIV(FSUB(cx, r), (float)SB_TILE_W), txn - 1);
+    tx1 = sb_clip_floor(FDIV(FADD(cx, r), (float)SB_TILE_W), txn - 1);
+    ty0 = sb_clip_floor(FDIV(FSUB(cy, r), (float)SB_TILE_H), tyn - 1);
+    ty1 = sb_clip_floor(FDIV(FADD(cy, r), (float)SB_TILE_H), tyn - 1);
+}
+
+// Exact disc/rect test (tiles.py:43-47): dx, dy in float64 (int64 - float32
+// promotes), r*r rounded in float32 before the float64 compare.
+SB_INLINE bool sb_disc_hits(float cx, float cy, float r, int tx, int ty, int W, int H) {
+    int rx0 = tx * SB_TILE_W, ry0 = ty * SB_TILE_H;
+    int rx1 = min(rx0 + SB_TILE_W - 1, W - 1), ry1 = min(ry0 + SB_TILE_H - 1, H - 1);
+    double dcx = (double)cx, dcy = (double)cy;
+    double dx = fmax(fmax(DSUB((double)rx0, dcx), DSUB(dcx, (double)rx1)), 0.0);
+    double dy = fmax(fmax(DSUB((double)ry0, dcy), DSUB(dcy, (double)ry1)), 0.0);
+    float rr = FMUL(r, r);
+    return DADD(DMUL(dx, dx), DMUL(dy, dy)) <= (double)rr;
+}
+
+// ---------------------------------------------------------------------------
+// decoupled look-back (single-pass chained scan) over uint32 block aggregates.
+// status[i] packs (flag << 32 | value); flag 1 = aggregate, 2 = inclusive.
+// Must be called by ONE thread per block, in ticket order (block index
+// obtained from an atomic counter so predecessors are resident).
+SB_INLINE uint32_t sb_lookback_exclusive(unsigned long long* status, int bid, uint32_t agg) {
+    if (bid == 0) {
+        atomicExch(&status[0], (2ull << 32) | agg);
+        return 0;
+    }
+    atomicExch(&status[bid], (1ull << 32) | agg);
+    uint32_t excl = 0;
+    int j = bid - 1;
+    while (true) {
+        unsigned long long s;
+        do {
+            s = atomicAdd(&status[j], 0ull);
+        } while ((s >> 32) == 0);
+        excl += (uint32_t)(s & 0xffffffffu);
+        if ((s >> 32) == 2) break;
+        j--;
+    }
+    atomicExch(&status[bid], (2ull << 32) | (excl + agg));
+    return excl;
+}
+
+SB_INLINE unsigned lane_id() { return threadIdx.x & 31; }

@@ -1,0 +1,183 @@
+// K5: fused projection + cluster AABB + frustum cull + stream compaction +
+// per-tile hit counting, one warp per 128-primitive cluster.
+//
+// Replaces (pkg/src/tinysplat):
+//   projection.py:130-190  project_scene           (bit-exact float32 mirror)
+//   ccc.py:112-131         build_clusters          (float64 AABB, 3 * max scale)
+//   ccc.py:134-146         cull_clusters           (p-vertex test)
+//   ccc.py:149-164         cluster_visibility      (| any(in_image) widening)
+//   ccc.py:171-194         compact_arrays          (contiguous visible ranges)
+//   tiles.py:50-91         bin_tiles, counting half (exact disc test)
+//
+// One pass over the 64-byte parameter rows (four 128-bit loads per lane per
+// Gaussian, 2 KB contiguous per warp), records staged in shared memory, the
+// compact offset of each cluster from a decoupled look-back over blocks, then
+// coalesced 128-bit stores of the 48-byte compact records.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kWarps = 8;                      // clusters per block
+constexpr int kThreads = kWarps * 32;
+
+struct WarpStage {
+    RasterRec rec[SB_CLUSTER_SIZE];
+};
+
+SB_INLINE double warp_min_d(double v) {
+    for (int s = 16; s >= 1; s >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, s));
+    return v;
+}
+SB_INLINE double warp_max_d(double v) {
+    for (int s = 16; s >= 1; s >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, s));
+    return v;
+}
+
+__global__ void __launch_bounds__(kThreads)
+project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clusters, CamDev cam,
+                            int use_culling, RasterRec* __restrict__ rec_out, int32_t* __restrict__ compact_map,
+                            int32_t* __restrict__ cluster_offset, uint8_t* __restrict__ cluster_vis,
+                            int32_t* __restrict__ tile_counts, int32_t* __restrict__ counters,
+                            unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpStage* stage = reinterpret_cast<WarpStage*>(smem_raw);
+    __shared__ int s_bid;
+    __shared__ uint32_t s_prefix;
+    __shared__ uint32_t s_warp_vis[kWarps];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_bid = (int)atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int bid = s_bid;
+    const int cl = bid * kWarps + warp;
+    RasterRec* st = stage[warp].rec;
+
+    bool any_in = false;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    int ndeg = 0;
+    if (cl < n_clusters) {
+#pragma unroll 1
+        for (int j = 0; j < 4; j++) {
+            const int slot = j * 32 + lane;
+            const int g = cl * SB_CLUSTER_SIZE + slot;
+            RasterRec r;
+            r.flags = 0;
+            if (g < n) {
+                float p[16];
+                const float4* row = params + (size_t)g * 4;
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    float4 v = __ldg(row + k);
+                    p[4 * k] = v.x; p[4 * k + 1] = v.y; p[4 * k + 2] = v.z; p[4 * k + 3] = v.w;
+                }
+                ProjOut o;
+                sb_project(p, cam, o);
+                r.x = o.x; r.y = o.y; r.a = o.ca; r.b = o.cb; r.c = o.cc; r.o = o.op;
+                r.r = o.col[0]; r.g = o.col[1]; r.bl = o.col[2]; r.depth = o.depth; r.radius = o.radius;
+                r.flags = (o.valid ? 1u : 0u) | (o.in_image ? 2u : 0u);
+                any_in |= o.in_image;
+                ndeg += o.degenerate ? 1 : 0;
+                // cluster AABB: p -+ 3 * max(exp(log_scale)) in float64 (ccc.py:125-130)
+                double m = exp((double)p[SB_COL_LS]);
+                m = fmax(m, exp((double)p[SB_COL_LS + 1]));
+                m = fmax(m, exp((double)p[SB_COL_LS + 2]));
+                const double reach = DMUL(3.0, m);
+                for (int k = 0; k < 3; k++) {
+                    lo[k] = fmin(lo[k], DSUB((double)p[k], reach));
+                    hi[k] = fmax(hi[k], DADD((double)p[k], reach));
+                }
+                // tile-hit counting for fragment-generating primitives
+                if (o.in_image) {
+                    int tx0, tx1, ty0, ty1;
+                    sb_tile_range(o.x, o.y, o.radius, cam.tiles_x, cam.tiles_y, tx0, tx1, ty0, ty1);
+                    for (int ty = ty0; ty <= ty1; ty++)
+                        for (int tx = tx0; tx <= tx1; tx++)
+                            if (sb_disc_hits(o.x, o.y, o.radius, tx, ty, cam.W, cam.H))
+                                atomicAdd(&tile_counts[ty * cam.tiles_x + tx], 1);
+                }
+            }
+            st[slot] = r;
+        }
+    }
+    // cluster visibility (p-vertex test, einsum order (c0 n0 + c2 n2) + c1 n1)
+    bool vis = false;
+    if (cl < n_clusters) {
+        const bool any_ii = __any_sync(0xffffffffu, any_in);
+        if (use_culling) {
+            for (int k = 0; k < 3; k++) {
+                lo[k] = warp_min_d(lo[k]);
+                hi[k] = warp_max_d(hi[k]);
+            }
+            bool inside = true;
+            for (int pl = 0; pl < 6; pl++) {
+                const double* P = cam.planes + 4 * pl;
+                double c0 = P[0] >= 0.0 ? hi[0] : lo[0];
+                double c1 = P[1] >= 0.0 ? hi[1] : lo[1];
+                double c2 = P[2] >= 0.0 ? hi[2] : lo[2];
+                double dist = DADD(DADD(DADD(DMUL(c0, P[0]), DMUL(c2, P[2])), DMUL(c1, P[1])), P[3]);
+                inside = inside && (dist >= 0.0);
+            }
+            vis = inside || any_ii;
+        } else {
+            vis = true;
+        }
+        int nd = __reduce_add_sync(0xffffffffu, ndeg);
+        if (lane == 0 && nd) atomicAdd(&counters[2], nd);
+    }
+    if (lane == 0) s_warp_vis[warp] = vis ? 1u : 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t agg = 0;
+        for (int w = 0; w < kWarps; w++) agg += s_warp_vis[w];
+        s_prefix = sb_lookback_exclusive(status, bid, agg);
+    }
+    __syncthreads();
+    if (cl >= n_clusters) return;
+    uint32_t before = s_prefix;
+    for (int w = 0; w < warp; w++) before += s_warp_vis[w];
+    if (lane == 0) {
+        cluster_vis[cl] = vis ? 1 : 0;
+        cluster_offset[cl] = vis ? (int32_t)(before * SB_CLUSTER_SIZE) : -1;
+    }
+    if (!vis) return;
+    const int members = min(SB_CLUSTER_SIZE, n - cl * SB_CLUSTER_SIZE);
+    if (lane == 0) {
+        atomicAdd(&counters[0], 1);
+        atomicAdd(&counters[1], members);
+    }
+    __syncwarp();
+    // coalesced copy of the staged records: 128 x 48 B = 384 float4
+    const size_t base = (size_t)before * SB_CLUSTER_SIZE;
+    const float4* src = reinterpret_cast<const float4*>(st);
+    float4* dst = reinterpret_cast<float4*>(rec_out + base);
+    const int nvec = members * 3;
+    for (int v = lane; v < nvec; v += 32) dst[v] = src[v];
+    for (int s = lane; s < members; s += 32) compact_map[base + s] = cl * SB_CLUSTER_SIZE + s;
+}
+
+}  // namespace
+
+void sb_launch_project_cull_compact(const float* params, int n, const CamDev& cam, int use_culling,
+                                    RasterRec* rec_out, int32_t* compact_map, int32_t* cluster_offset,
+                                    uint8_t* cluster_vis, int32_t* tile_counts, int32_t* counters,
+                                    unsigned long long* status, unsigned int* ticket, cudaStream_t stream)
+{
+    const int k = (n + SB_CLUSTER_SIZE - 1) / SB_CLUSTER_SIZE;
+    const int blocks = (k + kWarps - 1) / kWarps;
+    if (blocks == 0) return;
+    const size_t smem = sizeof(WarpStage) * kWarps;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(project_cull_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    project_cull_compact_kernel<<<blocks, kThreads, smem, stream>>>(
+        reinterpret_cast<const float4*>(params), n, k, cam, use_culling, rec_out, compact_map, cluster_offset,
+        cluster_vis, tile_counts, counters, status, ticket);
+}
+
+int sb_project_blocks(int n) {
+    const int k = (n + SB_CLUSTER_SIZE - 1) / SB_CLUSTER_SIZE;
+    return (k + kWarps - 1) / kWarps;
+}

@@ -1,0 +1,199 @@
+"""Forward render: project -> cluster cull -> compact -> bin -> per-tile
+depth sort -> warp-per-tile raster, all on the device.
+
+Reference API: pkg/src/tinysplat/forward.py:56-94 (RasterConfig,
+RenderOutput, RenderContext) and 258-308 (forward, render).  The call chain
+per view is five launches through the C-ABI (include/splat_b200.h):
+
+  sb_project_cull_compact  projection.py:130-190 + ccc.py:112-194 + tile counts
+  sb_bin_offsets           per-tile exclusive scan (-> P)
+  sb_bin_emit              tiles.py:75-91 exact disc test, 64-bit keys
+  sb_tile_sort             tiles.py:92-106 per-tile (depth, index) sort
+  sb_raster_fwd            forward.py:161-191 blend + 240-255 assembly
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .camera import CameraView
+from .scene import SceneSoA
+
+TILE_W, TILE_H, LANES, PIXELS_PER_LANE = 16, 8, 32, 4
+CLUSTER_SIZE = 128
+REC_FLOATS = 12  # 48-byte compact record
+
+
+@dataclass
+class RasterConfig:
+    """forward.py:56-71 fields.  The device path computes in float32 (the
+    reference default); float64 is the CPU oracle's numeric mode only."""
+    dtype: str = "float32"
+    kernel: str = "scanline"
+    alpha_min: float = 1.0 / 255.0
+    alpha_max: float = 0.99
+    t_stop: float = 1e-4
+    background: tuple = (0.0, 0.0, 0.0)
+    low_pass: float = 0.3
+    use_culling: bool = True
+    conic_reduce: str = "exp_aligned"   # backward: "exp_aligned" | "tree"
+
+    def struct(self, half: bool = False) -> _lib.SbRasterCfg:
+        if self.dtype != "float32":
+            raise ValueError("the B200 path rasterizes in float32 (dtype='float32'); "
+                             "float64 exists only in the CPU oracle")
+        if self.kernel != "scanline":
+            raise ValueError("only the scanline kernel is implemented on the device")
+        if self.conic_reduce not in ("exp_aligned", "tree"):
+            raise ValueError(f"unknown conic_reduce {self.conic_reduce!r}")
+        s = _lib.SbRasterCfg()
+        s.alpha_min, s.alpha_max, s.t_stop = self.alpha_min, self.alpha_max, self.t_stop
+        s.background[:] = [float(b) for b in self.background]
+        s.low_pass = self.low_pass
+        s.use_culling = int(bool(self.use_culling))
+        s.conic_reduce = 0 if self.conic_reduce == "exp_aligned" else 1
+        s.half_state = int(bool(half))
+        return s
+
+
+@dataclass
+class RenderOutput:
+    color: torch.Tensor          # (H, W, 3) float32
+    transmittance: torch.Tensor  # (H, W) float32
+    frag_count: torch.Tensor     # (H, W) int32
+
+
+@dataclass
+class TileWorkload:
+    """tiles.py:30-35, materialised on demand from the device lists."""
+    tile_x: int
+    tile_y: int
+    origin: tuple
+    primitives: np.ndarray
+
+
+@dataclass
+class RenderContext:
+    """forward.py:80-94: what the backward replays, pinned to a generation.
+    Device buffers stay resident; host views are built lazily."""
+    generation: int
+    camera: CameraView
+    config: RasterConfig
+    n_total: int
+    n_clusters: int
+    n_compact: int
+    n_pairs: int
+    visible_clusters: int
+    culled_clusters: int
+    recs: torch.Tensor            # (N, 12) float32 compact records (first n_compact rows)
+    compact_map_full: torch.Tensor  # (N,) int32
+    cluster_offset: torch.Tensor  # (K,) int32
+    cluster_vis: torch.Tensor     # (K,) uint8
+    tile_offsets: torch.Tensor    # (T + 1,) int32
+    tile_prims: torch.Tensor      # (P,) int32 compact slots, per-tile depth order
+    transmittance: torch.Tensor   # (H, W)
+    last: torch.Tensor            # (H, W) int32
+    n_degenerate: int = 0
+    _tiles: list | None = field(default=None, repr=False)
+
+    @property
+    def compact_map(self) -> torch.Tensor:
+        return self.compact_map_full[: self.n_compact]
+
+    @property
+    def tiles(self) -> list:
+        """Non-empty tiles in tile-id order (the reference's ctx.tiles)."""
+        if self._tiles is None:
+            offs = self.tile_offsets.cpu().numpy()
+            prims = self.tile_prims.cpu().numpy()
+            tx_n = self.camera.tiles[0]
+            out = []
+            for t in np.flatnonzero(np.diff(offs) > 0):
+                ty, tx = divmod(int(t), tx_n)
+                out.append(TileWorkload(tile_x=tx, tile_y=ty, origin=(tx * TILE_W, ty * TILE_H),
+                                        primitives=prims[offs[t]:offs[t + 1]].astype(np.int64)))
+            self._tiles = out
+        return self._tiles
+
+    @property
+    def projected(self) -> dict:
+        """Compact projected arrays decoded from the device records."""
+        r = self.recs[: self.n_compact]
+        flags = r[:, 11].contiguous().view(torch.int32)
+        return {
+            "xy": r[:, 0:2], "conic": torch.stack([r[:, 2], r[:, 3], r[:, 4]], 1), "opacity": r[:, 5],
+            "color": r[:, 6:9], "depth": r[:, 9], "radius": r[:, 10],
+            "valid": (flags & 1) != 0, "in_image": (flags & 2) != 0,
+        }
+
+
+def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, half: bool):
+    _lib.require_cuda(scene.data)
+    dev = scene.device
+    n = scene.n
+    W, H = camera.resolution
+    tx_n, ty_n = camera.tiles
+    ntiles = tx_n * ty_n
+    K = (n + CLUSTER_SIZE - 1) // CLUSTER_SIZE
+    cam_s = camera.struct()
+    cfg_s = config.struct(half)
+    stream = C.c_void_p(_lib.stream_ptr(dev))
+
+    recs = torch.empty((max(n, 1), REC_FLOATS), dtype=torch.float32, device=dev)
+    cmap = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    coff = torch.empty(max(K, 1), dtype=torch.int32, device=dev)
+    cvis = torch.zeros(max(K, 1), dtype=torch.uint8, device=dev)
+    tile_counts = torch.zeros(ntiles, dtype=torch.int32, device=dev)
+    counters = torch.zeros(4, dtype=torch.int32, device=dev)
+    tile_offsets = torch.empty(ntiles + 1, dtype=torch.int32, device=dev)
+    ws_n = _lib.load().sb_project_workspace_bytes(n)
+    ws = _lib.workspace("project", ws_n, dev)
+    _lib.call("sb_project_cull_compact", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s), _lib.ptr(recs),
+              _lib.ptr(cmap), _lib.ptr(coff), _lib.ptr(cvis), _lib.ptr(tile_counts), _lib.ptr(counters),
+              _lib.ptr(ws), ws.numel(), stream)
+    _lib.call("sb_bin_offsets", _lib.ptr(tile_counts), ntiles, _lib.ptr(tile_offsets), stream)
+    hdr = torch.cat([tile_offsets[ntiles:], counters[:3]]).cpu().tolist()   # one D2H read: P, vis, N_c, ndeg
+    P, vis, nc, ndeg = (int(v) for v in hdr)
+    keys = torch.empty(max(P, 1), dtype=torch.int64, device=dev)
+    scratch = torch.empty(max(P, 1), dtype=torch.int64, device=dev)
+    prims = torch.empty(max(P, 1), dtype=torch.int32, device=dev)
+    ws_e = _lib.workspace("emit", _lib.load().sb_bin_emit_workspace_bytes(ntiles), dev)
+    _lib.call("sb_bin_emit", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), _lib.ptr(tile_offsets),
+              _lib.ptr(keys), _lib.ptr(ws_e), ws_e.numel(), stream)
+    _lib.call("sb_tile_sort", _lib.ptr(tile_offsets), ntiles, _lib.ptr(keys), _lib.ptr(scratch), _lib.ptr(prims),
+              stream)
+    color = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+    T = torch.empty((H, W), dtype=torch.float32, device=dev)
+    frags = torch.empty((H, W), dtype=torch.int32, device=dev)
+    last = torch.empty((H, W), dtype=torch.int32, device=dev)
+    _lib.call("sb_raster_fwd", _lib.ptr(recs), _lib.ptr(tile_offsets), _lib.ptr(prims), C.byref(cam_s),
+              C.byref(cfg_s), _lib.ptr(color), _lib.ptr(T), _lib.ptr(frags), _lib.ptr(last), stream)
+    out = RenderOutput(color=color, transmittance=T, frag_count=frags)
+    ctx = RenderContext(generation=scene.generation, camera=camera, config=config, n_total=n, n_clusters=K,
+                        n_compact=nc, n_pairs=P, visible_clusters=vis, culled_clusters=K - vis, recs=recs,
+                        compact_map_full=cmap, cluster_offset=coff[:K], cluster_vis=cvis[:K],
+                        tile_offsets=tile_offsets, tile_prims=prims[:P], transmittance=T, last=last,
+                        n_degenerate=ndeg)
+    return out, ctx
+
+
+def forward(scene: SceneSoA, camera, config: RasterConfig | None = None, counter=None, half: bool = False):
+    """Render `scene` from `camera`; returns (RenderOutput, RenderContext).
+
+    forward.py:258-304.  `counter` (the reference's CPU op tally) is not
+    applicable on the device and must be None; use ncu counters instead."""
+    if counter is not None:
+        raise ValueError("OpCounter instrumentation is CPU-only; profile the device path with ncu")
+    config = config or RasterConfig()
+    camera = CameraView.from_any(camera)
+    if half:
+        raise NotImplementedError("fp16 blending state (half_path_blend) is not built yet")
+    return _launch_forward(scene, camera, config, half)
+
+
+def render(scene: SceneSoA, camera, config: RasterConfig | None = None) -> RenderOutput:
+    return forward(scene, camera, config)[0]

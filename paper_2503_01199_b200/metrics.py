@@ -1,0 +1,112 @@
+"""Training loss on the device: (1 - lambda) L1 + lambda (1 - SSIM) and its
+analytic image gradient, plus PSNR.
+
+Reference: pkg/src/tinysplat/metrics.py:18-132 (float64 with scipy's
+correlate1d, 11x11 Gaussian window sigma 1.5, valid interior, adjoint by
+zero-embedding).  Here: the same formulas as separable torch conv2d in
+float32 on the rendered image's device (a fused CUDA
+kernel is the next step).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+import torch.nn.functional as F
+
+SSIM_WINDOW = 11
+SSIM_SIGMA = 1.5
+C1 = 0.01 ** 2
+C2 = 0.03 ** 2
+
+_win_cache: dict = {}
+
+
+def gaussian_window(size: int = SSIM_WINDOW, sigma: float = SSIM_SIGMA, device="cpu", dtype=torch.float64):
+    x = torch.arange(size, dtype=torch.float64) - (size - 1) / 2.0
+    w = torch.exp(-0.5 * (x / sigma) ** 2)
+    return (w / w.sum()).to(device=device, dtype=dtype)
+
+
+def _win(device, dtype):
+    key = (str(device), dtype)
+    if key not in _win_cache:
+        w = gaussian_window(device=device, dtype=dtype)
+        _win_cache[key] = (w.view(1, 1, -1, 1), w.view(1, 1, 1, -1))
+    return _win_cache[key]
+
+
+def _filter_valid(img, wc, wr):
+    """(B, 1, H, W) -> (B, 1, H-10, W-10): correlate along rows then columns."""
+    return F.conv2d(F.conv2d(img, wc), wr)
+
+
+def _filter_transpose(field, wc, wr):
+    """Adjoint of _filter_valid: embed the interior and correlate with zero padding."""
+    r = wc.shape[2] // 2
+    return F.conv2d(F.conv2d(F.pad(field, (r, r, r, r)), wc, padding=(r, 0)), wr, padding=(0, r))
+
+
+def _ssim_terms(x, y, need_grad):
+    wc, wr = _win(x.device, x.dtype)
+    mu_x = _filter_valid(x, wc, wr)
+    mu_y = _filter_valid(y, wc, wr)
+    xx = _filter_valid(x * x, wc, wr)
+    yy = _filter_valid(y * y, wc, wr)
+    xy = _filter_valid(x * y, wc, wr)
+    var_x, var_y, cov = xx - mu_x * mu_x, yy - mu_y * mu_y, xy - mu_x * mu_y
+    A1 = 2.0 * mu_x * mu_y + C1
+    A2 = 2.0 * cov + C2
+    B1 = mu_x * mu_x + mu_y * mu_y + C1
+    B2 = var_x + var_y + C2
+    S = (A1 * A2) / (B1 * B2)
+    per_ch = S.mean(dim=(1, 2, 3))
+    if not need_grad:
+        return per_ch, None
+    n = S[0].numel()
+    dA1 = A2 / (B1 * B2)
+    dA2 = A1 / (B1 * B2)
+    dB1 = -S / B1
+    dB2 = -S / B2
+    g_mu = 2.0 * mu_y * dA1 - 2.0 * mu_y * dA2 + 2.0 * mu_x * dB1 - 2.0 * mu_x * dB2
+    grad = _filter_transpose(g_mu, wc, wr)
+    grad = grad + _filter_transpose(2.0 * dA2, wc, wr) * y
+    grad = grad + _filter_transpose(dB2, wc, wr) * (2.0 * x)
+    return per_ch, grad / n
+
+
+def _chw(img):
+    return img.permute(2, 0, 1).unsqueeze(1)   # (H, W, C) -> (C, 1, H, W)
+
+
+def ssim(a, b) -> float:
+    a = torch.as_tensor(a)
+    b = torch.as_tensor(b, device=a.device, dtype=a.dtype)
+    if a.dim() == 2:
+        a, b = a[..., None], b[..., None]
+    vals, _ = _ssim_terms(_chw(a), _chw(b), False)
+    return float(vals.mean())
+
+
+def psnr(a, b) -> float:
+    a = torch.as_tensor(a).double()
+    b = torch.as_tensor(b, device=a.device).double()
+    mse = float(((a - b) ** 2).mean())
+    return math.inf if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
+
+
+def loss_and_grad(rendered: torch.Tensor, target: torch.Tensor, lam: float, return_tensor: bool = False):
+    """(loss, dL/d rendered) for (H, W, 3) images (metrics.py:118-132).
+    With return_tensor=True the loss stays a 0-d device tensor (no sync)."""
+    x = rendered.float()
+    y = torch.as_tensor(target, device=x.device).float()
+    diff = x - y
+    nel = diff.numel()
+    loss = (1.0 - lam) * diff.abs().mean()
+    grad = torch.sign(diff) * ((1.0 - lam) / nel)
+    if lam != 0.0:
+        nch = x.shape[-1]
+        vals, g = _ssim_terms(_chw(x), _chw(y), True)
+        loss = loss + lam * (1.0 - vals.mean())
+        grad = grad - lam * (g[:, 0].permute(1, 2, 0) / nch)
+    return (loss if return_tensor else float(loss)), grad.contiguous()

@@ -1,0 +1,289 @@
+"""Parity of the CUDA path (through the C-ABI) with the reference's own
+outputs (tests/golden, made from /root/reference) and with the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  bit-exact  Morton keys / sort order, cull masks, compact maps, tile lists,
+             projected xy/depth/conic/radius/colour/opacity
+  1e-3       rendered image max abs (fp32 accumulation)
+  1e-2       per-Gaussian gradients and S/M/variance, floored relative
+             |g - g_ref| <= 1e-2 * max(|g_ref|, 1e-3 * max|g_ref|) per channel,
+             with an allowance only where the reference's own fp32 path is
+             equally far from its fp64 path (ill-conditioned rows)
+"""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from tests import goldens as G
+
+pytestmark = pytest.mark.gpu
+
+CH_SLICES = ((0, 3), (3, 6), (6, 10), (10, 13), (13, 14))
+
+
+def _sb():
+    import paper_2503_01199_b200 as sb
+    return sb
+
+
+def _scene(d, prefix=""):
+    sb = _sb()
+    sc = G.scene(d, prefix)
+    return sb.SceneSoA(*[sc[k] for k in G.CH], device="cuda")
+
+
+def _cfg(d, prefix=""):
+    sb = _sb()
+    return sb.RasterConfig(background=tuple(float(b) for b in d[f"{prefix}cfg_bg"]),
+                           use_culling=bool(d[f"{prefix}cfg_cull"]),
+                           conic_reduce="tree" if int(d[f"{prefix}cfg_tree"]) else "exp_aligned")
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("fname,prefix", G.CASES)
+def test_forward_bit_exact_stages_and_image(fname, prefix):
+    sb = _sb()
+    d = G.load(fname)
+    scene, cam, cfg = _scene(d, prefix), G.camera(d, prefix), _cfg(d, prefix)
+    out, ctx = sb.forward(scene, cam, cfg)
+    cmap = ctx.compact_map.cpu().numpy()
+    assert np.array_equal(cmap, d[f"{prefix}compact_map"])
+    assert np.array_equal(ctx.tile_offsets.cpu().numpy(), d[f"{prefix}tile_offsets"])
+    assert np.array_equal(ctx.tile_prims.cpu().numpy(), d[f"{prefix}tile_prims"])
+    if int(d[f"{prefix}cfg_cull"]) and len(cmap):
+        vis = d[f"{prefix}vis_mask"]
+        assert np.array_equal(ctx.cluster_vis.cpu().numpy().astype(bool), vis)
+    p = {k: v.cpu().numpy() for k, v in ctx.projected.items()}
+    valid = d[f"{prefix}proj_valid"][cmap]
+    assert np.array_equal(p["valid"], valid)
+    assert np.array_equal(p["in_image"], d[f"{prefix}proj_in_image"][cmap])
+    for k in ("xy", "depth", "conic", "radius", "color", "opacity"):
+        ref = d[f"{prefix}proj_{k}"][cmap]
+        assert np.array_equal(p[k][valid].view(np.uint32), ref[valid].view(np.uint32)), k
+    color = out.color.cpu().numpy()
+    assert np.abs(color - d[f"{prefix}fwd_color"]).max() <= 1e-3
+    assert np.abs(out.transmittance.cpu().numpy() - d[f"{prefix}fwd_T"]).max() <= 1e-3
+    # frag counts: exact except alpha / T threshold flips
+    assert (out.frag_count.cpu().numpy() != d[f"{prefix}fwd_frags"]).sum() <= 2
+    if f"{prefix}fwd64_color" in d:
+        assert np.abs(color - d[f"{prefix}fwd64_color"]).max() <= 1e-3
+
+
+@pytest.mark.parametrize("fname,prefix", G.CASES)
+def test_backward_vs_reference(fname, prefix):
+    sb = _sb()
+    d = G.load(fname)
+    scene, cam, cfg = _scene(d, prefix), G.camera(d, prefix), _cfg(d, prefix)
+    n = scene.n
+    out, ctx = sb.forward(scene, cam, cfg)
+    stats = sb.DensifyStats.zeros(n)
+    res = sb.backward(scene, ctx, torch.from_numpy(d[f"{prefix}dL_dI"]), stats)
+    g = res.grads.packed[:, :14].double().cpu().numpy()
+    g32 = d[f"{prefix}grads"].astype(np.float64)
+    g64 = d.get(f"{prefix}grads64")
+    for lo, hi in CH_SLICES:
+        if g64 is None:
+            assert G.floored_rel(g[:, lo:hi], g32[:, lo:hi]) <= 1e-2, (lo, hi)
+        else:
+            assert G.conditioned_rel_excess(g[:, lo:hi], g32[:, lo:hi], g64[:, lo:hi].astype(np.float64),
+                                            1e-2) <= 1.0, (lo, hi)
+    C = stats.C.cpu().numpy()
+    assert (C != d[f"{prefix}stat_C"]).sum() <= 2
+    assert G.floored_rel(stats.S.cpu().numpy(), d[f"{prefix}stat_S"]) <= 1e-2
+    assert G.floored_rel(stats.M.cpu().numpy(), d[f"{prefix}stat_M"]) <= 1e-2
+    assert np.array_equal(res.cluster_mask.cpu().numpy(), d[f"{prefix}upd_mask"])
+    score = sb.variance_score(stats).cpu().numpy()
+    assert G.floored_rel(score, d[f"{prefix}score"]) <= 1e-2
+
+
+@pytest.mark.parametrize("fname,prefix", [c for c in G.CASES if c[1] in ("", "e1_")])
+def test_backward_vs_float64_oracle(fname, prefix):
+    """Against the reference's float64 path: the back-to-front fp32 replay is
+    closer to fp64 than the reference's own fp32 path."""
+    sb = _sb()
+    d = G.load(fname)
+    scene, cam, cfg = _scene(d, prefix), G.camera(d, prefix), _cfg(d, prefix)
+    out, ctx = sb.forward(scene, cam, cfg)
+    res = sb.backward(scene, ctx, torch.from_numpy(d[f"{prefix}dL_dI"]), sb.DensifyStats.zeros(scene.n))
+    g = res.grads.packed[:, :14].double().cpu().numpy()
+    g64 = d[f"{prefix}grads64"].astype(np.float64)
+    for lo, hi in CH_SLICES:
+        assert G.floored_rel(g[:, lo:hi], g64[:, lo:hi]) <= 1e-2, (lo, hi)
+
+
+def test_morton_keys_and_sort_bit_exact():
+    sb = _sb()
+    from paper_2503_01199_b200.ccc import morton_encode_scene
+    for fname, prefix in (("golden_A.npz", ""), ("golden_edge.npz", "e4_")):
+        d = G.load(fname)
+        scene = _scene(d, prefix)
+        keys, lo, hi = morton_encode_scene(scene)
+        assert np.array_equal(keys.cpu().numpy().view(np.uint64), d[f"{prefix}morton_keys"])
+        sc2 = scene.copy()
+        perm = sb.morton_sort(sc2)
+        assert np.array_equal(perm.cpu().numpy(), d[f"{prefix}morton_perm"])
+        assert torch.equal(sc2.data, scene.data[perm])
+        assert sc2.generation == scene.generation + 1
+    d = G.load("golden_edge.npz")
+    pos = d["mort_pos"]
+    z = np.zeros((len(pos), 3))
+    scene = sb.SceneSoA(pos, z, np.tile([1.0, 0, 0, 0], (len(pos), 1)), z, np.zeros(len(pos)), device="cuda")
+    # mort_pos is float64 data not representable in fp32; compare with the
+    # oracle on the fp32-rounded positions instead of the fixture
+    keys, perm = O.morton_perm(pos.astype(np.float32).astype(np.float64))
+    got, _, _ = morton_encode_scene(scene)
+    assert np.array_equal(got.cpu().numpy().view(np.uint64), keys)
+    assert np.array_equal(sb.morton_sort(scene.copy()).cpu().numpy(), perm)
+
+
+def test_radix_sort_random_keys_stable():
+    from paper_2503_01199_b200.ccc import sort_pairs
+    rng = np.random.default_rng(3)
+    for n in (1, 7, 4096, 4097, 100_003):
+        k = rng.integers(0, 1 << 20, n, dtype=np.uint64) << np.uint64(30)   # many duplicates
+        kt = torch.from_numpy(k.view(np.int64)).cuda()
+        vt = torch.arange(n, dtype=torch.int32, device="cuda")
+        ks, vs = sort_pairs(kt, vt, bits=64)
+        ref = np.argsort(k, kind="stable")
+        assert np.array_equal(vs.cpu().numpy(), ref)
+        assert np.array_equal(ks.cpu().numpy().view(np.uint64), k[ref])
+
+
+def test_lane_reductions_bit_exact():
+    sb = _sb()
+    d = G.load("golden_edge.npz")
+    v = torch.from_numpy(d["red_in"]).cuda()
+    assert np.array_equal(sb.lane_group_reduce(v).cpu().numpy(), d["red_tree"])
+    assert np.array_equal(sb.lane_group_reduce(v, float64=True).cpu().numpy(), d["red_tree64"])
+    assert np.array_equal(sb.exp_aligned_reduce(v).cpu().numpy(), d["red_exp"].astype(np.float32))
+
+
+def test_adam_vs_reference():
+    sb = _sb()
+    d = G.load("golden_edge.npz")
+    n = len(d["adam_in_position"])
+    scene = sb.SceneSoA(*[d[f"adam_in_{c}"] for c in G.CH], device="cuda")
+    st = sb.AdamState(scene)
+    lrs = dict(zip(G.CH, d["adam_lrs"]))
+    for k in range(3):
+        g = d[f"adam_g{k}"]
+        grads = sb.SceneGrads.from_dict({c: g[:, a:b] for c, (a, b) in zip(G.CH, CH_SLICES)}, n)
+        sb.adam_step(scene, grads, st, torch.from_numpy(d[f"adam_mask{k}"]), lrs)
+    got = scene.data[:, :14].double().cpu().numpy()
+    # fp32 state vs the reference's fp64: ~1e-7 relative; Adam steps are ~lr
+    np.testing.assert_allclose(got, d["adam_out"], rtol=2e-6, atol=2e-7)
+    np.testing.assert_allclose(st.m_rows[:, :14].double().cpu().numpy(), d["adam_m"], rtol=1e-6, atol=1e-30)
+    np.testing.assert_allclose(st.v_rows[:, :14].double().cpu().numpy(), d["adam_v"], rtol=1e-6, atol=1e-30)
+    assert np.array_equal(st.step.cpu().numpy(), d["adam_step"])
+
+
+def test_variance_score_exact():
+    sb = _sb()
+    d = G.load("golden_edge.npz")
+    stats = sb.DensifyStats(S=torch.from_numpy(d["var_S"]).cuda(), M=torch.from_numpy(d["var_M"]).cuda(),
+                            C=torch.from_numpy(d["var_C"].astype(np.int32)).cuda())
+    assert np.array_equal(sb.variance_score(stats).cpu().numpy(), d["var_score"])
+
+
+def test_empty_scene_and_errors():
+    sb = _sb()
+    d = G.load("golden_edge.npz")
+    cam = G.camera(d, "e5_")
+    scene = sb.SceneSoA.empty(device="cuda")
+    out, ctx = sb.forward(scene, cam, sb.RasterConfig(background=(0.1, 0.2, 0.3)))
+    assert np.array_equal(out.color.cpu().numpy(), d["e5_fwd_color"])
+    res = sb.backward(scene, ctx, torch.zeros(cam.resolution[1], cam.resolution[0], 3))
+    assert res.grads.packed.shape == (0, 16)
+    # staleness and shape errors (backward.py:213-218)
+    d = G.load("golden_A.npz")
+    scene = _scene(d)
+    out, ctx = sb.forward(scene, G.camera(d))
+    with pytest.raises(sb.ShapeMismatchError):
+        sb.backward(scene, ctx, torch.zeros(3, 3, 3))
+    sb.morton_sort(scene)
+    with pytest.raises(sb.StaleSceneError):
+        sb.backward(scene, ctx, torch.zeros(128, 128, 3))
+
+
+def test_forward_deterministic_and_culling_invisible():
+    sb = _sb()
+    d = G.load("golden_A.npz")
+    scene, cam = _scene(d), G.camera(d)
+    a, _ = sb.forward(scene, cam)
+    b, _ = sb.forward(scene, cam)
+    c, _ = sb.forward(scene, cam, sb.RasterConfig(use_culling=False))
+    assert torch.equal(a.color, b.color) and torch.equal(a.frag_count, b.frag_count)
+    assert torch.equal(a.color, c.color) and torch.equal(a.frag_count, c.frag_count)
+
+
+@pytest.mark.parametrize("n,res,seed", [(50_000, (256, 192), 11), (200_000, (640, 360), 5)])
+def test_seeded_vs_oracle(n, res, seed):
+    """Size-scaled scenes against the oracle run here."""
+    sb = _sb()
+    from paper_2503_01199_b200.synthetic import SyntheticSceneSpec, camera_ring, scaled_scene_arrays
+    arr = scaled_scene_arrays(n, seed, res)
+    cam = camera_ring(SyntheticSceneSpec(n_gaussians=n, n_views=3, view_resolution=res, seed=seed))[2]
+    scene = sb.SceneSoA(*[arr[k] for k in G.CH], device="cuda")
+    sb.morton_sort(scene)
+    arr = {k: v for k, v in zip(G.CH, [None] * 5)}
+    h = scene.data.cpu().numpy().astype(np.float64)
+    arr = {"position": h[:, 0:3], "log_scale": h[:, 3:6], "rotation": h[:, 6:10], "color": h[:, 10:13],
+           "opacity_logit": h[:, 13]}
+    out, ctx = sb.forward(scene, cam)
+    col, T, frags, octx = O.forward(arr, cam, O.RasterConfig())
+    assert np.array_equal(ctx.compact_map.cpu().numpy(), octx.compact_map)
+    assert np.array_equal(ctx.tile_offsets.cpu().numpy().astype(np.int64), octx.tile_offsets)
+    assert np.array_equal(ctx.tile_prims.cpu().numpy().astype(np.int64), octx.prims)
+    assert np.abs(out.color.cpu().numpy() - col).max() <= 1e-3
+    assert (out.frag_count.cpu().numpy() != frags).sum() <= 5
+    rng = np.random.default_rng(seed)
+    _, dI = O.loss_and_grad(col, rng.uniform(0, 1, col.shape), 0.2)
+    dI = dI.astype(np.float32)
+    res_ = sb.backward(scene, ctx, torch.from_numpy(dI), sb.DensifyStats.zeros(scene.n))
+    ob = O.backward(arr, octx, dI)
+    g = res_.grads.packed[:, :14].double().cpu().numpy()
+    for lo, hi in CH_SLICES:
+        assert G.floored_rel(g[:, lo:hi], ob["grads"][:, lo:hi]) <= 1e-2, (lo, hi)
+    st = res_.stats
+    assert G.floored_rel(st.S.cpu().numpy(), ob["S"]) <= 1e-2
+    assert G.floored_rel(st.M.cpu().numpy(), ob["M"]) <= 1e-2
+    assert (st.C.cpu().numpy() != ob["C"]).sum() <= 5
+
+
+@pytest.mark.parametrize("name", ["B", "C", "E"])
+def test_big_configs_bit_exact_hashes(name):
+    """Configs B/C/E at full size: Morton order, projection, cull masks,
+    compact map and tile lists hash-identical to the reference's."""
+    sb = _sb()
+    from paper_2503_01199_b200.synthetic import SyntheticSceneSpec, camera_ring, scaled_scene_arrays
+    gb = G.load("golden_big.json")[name]
+    n, res = gb["n"], tuple(gb["res"])
+    arr = scaled_scene_arrays(n, 7, res)
+    for c in G.CH:
+        assert _sha(arr[c].astype(np.float32)) == gb["scene_sha"][c], c
+    scene = sb.SceneSoA(*[arr[k] for k in G.CH], device="cuda")
+    from paper_2503_01199_b200.ccc import morton_encode_scene
+    keys, _, _ = morton_encode_scene(scene)
+    assert _sha(keys.cpu().numpy().view(np.uint64)) == gb["morton_keys_sha"]
+    perm = sb.morton_sort(scene)
+    assert _sha(perm.cpu().numpy()) == gb["morton_perm_sha"]
+    cam = camera_ring(SyntheticSceneSpec(n_gaussians=n, n_views=1, view_resolution=res, seed=7))[0]
+    out, ctx = sb.forward(scene, cam)
+    assert ctx.n_compact == gb["n_compact"] and ctx.visible_clusters == gb["visible_clusters"]
+    assert _sha(ctx.cluster_vis.cpu().numpy().astype(np.uint8)) == gb["vis_mask_sha"]
+    assert _sha(ctx.compact_map.cpu().numpy().astype(np.int64)) == gb["compact_map_sha"]
+    assert ctx.n_pairs == gb["P"]
+    assert _sha(ctx.tile_offsets.cpu().numpy().astype(np.int64)) == gb["tile_offsets_sha"]
+    assert _sha(ctx.tile_prims.cpu().numpy().astype(np.int64)) == gb["tile_prims_sha"]
+    if "fwd_sample_pix" in gb:
+        pix = np.array(gb["fwd_sample_pix"])
+        col = out.color.reshape(-1, 3).cpu().numpy()[pix]
+        assert np.abs(col - np.array(gb["fwd_sample_color"])).max() <= 1e-3
+        fr = out.frag_count.reshape(-1).cpu().numpy()[pix]
+        assert (fr != np.array(gb["fwd_sample_frags"])).sum() <= 5
