@@ -1,0 +1,380 @@
+"""Benchmark: LiteGS training iteration on B200 (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload ("config B"): 1,000,000 synthetic Gaussians (reference generator,
+seed 7, footprints shrunk by (N/512)^(1/3) per SURVEY 8(d)), Morton-sorted,
+1920x1080 views on the reference's camera ring.  One step = one full training
+iteration per GPU: project + cluster cull + compact + bin + per-tile sort +
+raster forward + L1/D-SSIM loss + raster backward + projection chain +
+(NCCL all-reduce of grads and statistics when N > 1) + cluster-sparse Adam.
+Each rank rasterises its own view against replicated Gaussians (weak scaling).
+
+`value`  whole-job views/s with inputs resident in HBM, device-timed with CUDA
+         events over K steps, max over ranks.
+`e2e`    the same through the public API with host buffers: every step copies
+         its target image (uint8, pinned) host->device and reads the loss back.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "raster fwd+bwd ms/view & train iters/s @1M Gaussians 1080p; HBM roofline frac"
+N_GAUSS = 1_000_000
+RES = (1920, 1080)
+N_VIEWS = 8
+CH = ("position", "log_scale", "rotation", "color", "opacity_logit")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def setup_dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def build_workload(device):
+    import paper_2503_01199_b200 as sb
+    from paper_2503_01199_b200.synthetic import SyntheticSceneSpec, camera_ring, scaled_scene_arrays
+    arr = scaled_scene_arrays(N_GAUSS, 7, RES)
+    scene = sb.SceneSoA(*[arr[k] for k in CH], device=device)
+    state = sb.AdamState(scene)
+    sb.DensifyStats.zeros(scene.n, device).attach(scene)
+    sb.morton_sort(scene)
+    views = camera_ring(SyntheticSceneSpec(n_gaussians=N_GAUSS, n_views=N_VIEWS, view_resolution=RES, seed=7))
+    rng = np.random.default_rng(1234)
+    W, H = RES
+    targets_host = [torch.from_numpy(rng.integers(0, 256, (H, W, 3), dtype=np.uint8)).pin_memory()
+                    for _ in range(N_VIEWS)]
+    return scene, state, views, targets_host
+
+
+class Trainer:
+    """One training iteration through the public API (train.py:95-104)."""
+
+    def __init__(self, scene, state, views, ws, rank):
+        import paper_2503_01199_b200 as sb
+        self.sb = sb
+        self.scene, self.state, self.views = scene, state, views
+        self.ws, self.rank = ws, rank
+        self.lrs = sb.LearningRates().at(0.0, position_scale=3.2)
+        self.stats_step = sb.DensifyStats.zeros(scene.n, scene.device)
+
+    def step(self, it, target):
+        sb = self.sb
+        cam = self.views[(it * self.ws + self.rank) % len(self.views)]
+        out, ctx = sb.forward(self.scene, cam)
+        loss, dI = sb.loss_and_grad(out.color, target, 0.2, return_tensor=True)
+        stats = self.stats_step
+        if self.ws > 1:
+            stats.reset()
+        else:
+            stats = sb.DensifyStats.from_scene(self.scene)
+        res = sb.backward(self.scene, ctx, dI, stats)
+        mask = res.cluster_mask
+        if self.ws > 1:
+            dist.all_reduce(res.grads.packed)
+            sm = torch.stack([stats.S, stats.M])
+            dist.all_reduce(sm)
+            dist.all_reduce(stats.C)
+            m8 = mask.to(torch.uint8)
+            dist.all_reduce(m8, op=dist.ReduceOp.MAX)
+            mask = m8.bool()
+            run = sb.DensifyStats.from_scene(self.scene)
+            run.S += sm[0]
+            run.M += sm[1]
+            run.C += stats.C
+        sb.adam_step(self.scene, res.grads, self.state, mask, self.lrs)
+        return loss, ctx
+
+
+def timed(fn, steps, ws):
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    t0 = time.perf_counter()
+    fn()
+    b.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    if ws > 1:
+        dist.barrier()
+    ms = a.elapsed_time(b)
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, wall
+
+
+# algorithmic bytes per launch; P pairs, Nc compact, Npix pixels
+def algorithmic_bytes(name, n, nc, P, npix):
+    return {
+        "sb_project_cull_compact": 56 * n + 48 * nc,
+        "sb_bin_emit": 12 * nc + 8 * P,
+        "sb_tile_sort": 8 * P + 4 * P,
+        "sb_raster_fwd": 40 * P + 20 * npix,
+        "sb_raster_bwd": 96 * P + 20 * npix,
+        "sb_chain_projection_bwd": 188 * nc,
+        "sb_adam_sparse": 400 * nc,
+    }.get(name)
+
+
+def cpu_baseline_oracle(sample_iters=1):
+    """The CPU oracle (C port of the reference, all host threads) on config B."""
+    from oracle import oracle as O
+    from paper_2503_01199_b200.synthetic import SyntheticSceneSpec, camera_ring, scaled_scene_arrays
+    arr = scaled_scene_arrays(N_GAUSS, 7, RES)
+    _, perm = O.morton_perm(arr["position"])
+    arr = {k: np.ascontiguousarray(v[perm]) for k, v in arr.items()}
+    views = camera_ring(SyntheticSceneSpec(n_gaussians=N_GAUSS, n_views=N_VIEWS, view_resolution=RES, seed=7))
+    rng = np.random.default_rng(1234)
+    p14 = np.ascontiguousarray(O.pack14(arr))
+    m = np.zeros_like(p14); v = np.zeros_like(p14); st = np.zeros(len(p14), np.int64)
+    lr = [1.6e-4 * 3.2, 5e-3, 1e-3, 2.5e-3, 5e-2]
+    times = []
+    for it in range(sample_iters):
+        target = rng.integers(0, 256, (RES[1], RES[0], 3)).astype(np.float64) / 255.0
+        t0 = time.perf_counter()
+        col, T, fr, ctx = O.forward(arr, views[it % N_VIEWS])
+        _, dI = O.loss_and_grad(col, target, 0.2)
+        b = O.backward(arr, ctx, dI.astype(np.float32))
+        O.adam_step(p14, np.ascontiguousarray(b["grads"]), m, v, st, b["cluster_mask"], lr)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.build() if not os.path.exists(O.LIB_PATH) else None
+    cores = os.cpu_count()
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    w = min(args.warmup, 1)
+    k = max(1, min(args.steps, 4))
+    cpu_baseline_oracle(w) if w else None
+    times = cpu_baseline_oracle(k)
+    ms = 1e3 * sum(times) / len(times)
+    val = 1e3 / ms
+    sample = (f"{k} full config-B iterations (1M Gaussians, 1920x1080: project, cull, compact, bin, forward, "
+              f"fp64 L1+SSIM loss, backward, Adam) of the C oracle port, OpenMP over tiles")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "iters/s", "n_gpus": ws, "steps": k,
+        "warmup": w, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32+f64", "data": "synthetic",
+        "config": {"workload": "config B: 1M Gaussians, 1920x1080, full train iteration", "n_gaussians": N_GAUSS,
+                   "resolution": list(RES)},
+        "cpu_baseline": {"value": val, "unit": "iters/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = setup_dist()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        if ws > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    args.warmup = max(args.warmup, 3)
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    import paper_2503_01199_b200 as sb
+    from paper_2503_01199_b200 import _lib
+    scene, state, views, targets_host = build_workload(device)
+    trainer = Trainer(scene, state, views, ws, rank)
+    targets_dev = [t.to(device).float().div_(255.0) for t in targets_host]
+
+    it = {"i": 0}
+
+    def run(k):
+        for _ in range(k):
+            i = it["i"]
+            trainer.step(i, targets_dev[(i * ws + rank) % N_VIEWS])
+            it["i"] += 1
+
+    run(args.warmup)
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _lib.launch_count["n"]
+    ms, wall = timed(lambda: run(args.steps), args.steps, ws)
+    launches = _lib.launch_count["n"] - launches0
+    clk = clocks.stop()
+    ms_step = ms / args.steps
+    value = ws * args.steps / (ms / 1e3)
+
+    # e2e: public API with host buffers (H2D target per step, D2H loss per step)
+    W, H = RES
+    h2d = H * W * 3
+    losses = []
+
+    def run_e2e(k):
+        for _ in range(k):
+            i = it["i"]
+            host = targets_host[(i * ws + rank) % N_VIEWS]
+            tgt = host.to(device, non_blocking=True).float().div_(255.0)
+            loss, _ = trainer.step(i, tgt)
+            losses.append(float(loss.item()))
+            it["i"] += 1
+
+    run_e2e(2)
+    e2e_ms, _ = timed(lambda: run_e2e(args.steps), args.steps, ws)
+    e2e_val = ws * args.steps / (e2e_ms / 1e3)
+
+    # per-kernel durations (CUDA events on the launching stream, separate pass)
+    _lib.enable_call_timing(True)
+    ctxs = []
+    for _ in range(3):
+        _, ctx = trainer.step(it["i"], targets_dev[0])
+        ctxs.append(ctx)
+        it["i"] += 1
+    torch.cuda.synchronize()
+    tim = _lib.call_timings()
+    _lib.enable_call_timing(False)
+    ctx = ctxs[-1]
+    n, nc, P, npix = scene.n, ctx.n_compact, ctx.n_pairs, W * H
+    stages = {k: statistics.mean(v) for k, v in tim.items()}
+    dominant = max(stages, key=stages.get)
+    peak, peak_kind = peaks()
+    ab = algorithmic_bytes(dominant, n, nc, P, npix)
+    achieved = ab / (stages[dominant] * 1e-3) / 1e9 if ab else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dominant)
+        except Exception:
+            traffic = None
+    raster_ms = stages.get("sb_raster_fwd", 0.0) + stages.get("sb_raster_bwd", 0.0)
+    raster_bytes = algorithmic_bytes("sb_raster_fwd", n, nc, P, npix) + algorithmic_bytes("sb_raster_bwd", n, nc, P,
+                                                                                          npix)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            t = cpu_baseline_oracle(1)
+            cpu = {"value": 1.0 / t[0], "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": "1 full config-B iteration of the C oracle port (OpenMP over tiles, all host threads)"}
+        except Exception as e:  # the baseline must not take down the bench line
+            cpu = {"value": None, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generator, seed 7, N-scaled)",
+            "config": {"workload": "config B: 1M Gaussians, 1920x1080, full train iteration per view per GPU",
+                       "n_gaussians": N_GAUSS, "resolution": list(RES), "views_per_gpu_per_step": 1,
+                       "parallelism": f"view-parallel dp{ws}" if ws > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (params 64 MB + pairs ~165 MB + records 45 MB per view)",
+                       "P_pairs": P, "n_compact": nc},
+            "raster_fwd_bwd_ms_per_view": raster_ms,
+            "raster_fwd_bwd_roofline_frac": (raster_bytes / (raster_ms * 1e-3) / 1e9) / peak if raster_ms else None,
+            "stages_ms": stages,
+            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if achieved else None, "traffic": traffic,
+                         "algorithmic_bytes": ab, "peak_kind": peak_kind},
+            "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -102,11 +102,46 @@ def ptr(t: torch.Tensor | None):
     return C.c_void_p(t.data_ptr())
 
 
+# kernel launches issued by each entry point (for bench.py's gpu_launches);
+# the radix sort issues 3 per 8-bit pass and is counted by the caller.
+KERNELS_PER_CALL = {
+    "sb_morton_keys": 3, "sb_permute_rows": 1, "sb_project_cull_compact": 1, "sb_bin_offsets": 1,
+    "sb_bin_emit": 1, "sb_tile_sort": 1, "sb_raster_fwd": 1, "sb_raster_bwd": 1,
+    "sb_chain_projection_bwd": 1, "sb_adam_sparse": 1, "sb_variance_score": 1, "sb_lane_reduce": 1,
+    "sb_loss_fwd_bwd": 1,
+}
+launch_count = {"n": 0}
+# optional per-call CUDA-event timing: {name: [(start_event, end_event), ...]}
+_timing: dict | None = None
+
+
+def enable_call_timing(on: bool = True):
+    """Record CUDA events around every sb_* call on the current stream."""
+    global _timing
+    _timing = {} if on else None
+
+
+def call_timings() -> dict:
+    """{name: [ms, ...]} for the calls recorded since enable_call_timing()."""
+    if _timing is None:
+        return {}
+    return {k: [a.elapsed_time(b) for a, b in v] for k, v in _timing.items()}
+
+
 def call(name: str, *args):
     """Call an sb_* entry point and map its status to the reference's
     exception conventions (errors.py:6-32)."""
     lib = load()
-    rc = getattr(lib, name)(*args)
+    launch_count["n"] += KERNELS_PER_CALL.get(name, 0)
+    if _timing is not None:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        rc = getattr(lib, name)(*args)
+        b.record()
+        _timing.setdefault(name, []).append((a, b))
+    else:
+        rc = getattr(lib, name)(*args)
     if rc != SB_OK:
         msg = (lib.sb_last_error() or b"").decode()
         if rc == SB_EINVAL:

@@ -178,8 +178,11 @@ def test_adam_vs_reference():
     got = scene.data[:, :14].double().cpu().numpy()
     # fp32 state vs the reference's fp64: ~1e-7 relative; Adam steps are ~lr
     np.testing.assert_allclose(got, d["adam_out"], rtol=2e-6, atol=2e-7)
-    np.testing.assert_allclose(st.m_rows[:, :14].double().cpu().numpy(), d["adam_m"], rtol=1e-6, atol=1e-30)
-    np.testing.assert_allclose(st.v_rows[:, :14].double().cpu().numpy(), d["adam_v"], rtol=1e-6, atol=1e-30)
+    # moments are float32 state: identical grads in, float64 arithmetic, one
+    # rounding per step (cancellation in 0.9 m + 0.1 g needs the floor)
+    for lo, hi in CH_SLICES:
+        assert G.floored_rel(st.m_rows[:, lo:hi].double().cpu().numpy(), d["adam_m"][:, lo:hi]) <= 1e-5
+        assert G.floored_rel(st.v_rows[:, lo:hi].double().cpu().numpy(), d["adam_v"][:, lo:hi]) <= 1e-5
     assert np.array_equal(st.step.cpu().numpy(), d["adam_step"])
 
 

@@ -212,8 +212,8 @@ def make_edge():
            "opacity_logit": 5e-2}
     d["adam_lrs"] = np.array([lrs[c] for c in CH])
     for k in range(3):
-        g = {c: rng.normal(size=getattr(base, c).shape).astype(np.float32).astype(np.float64)
-             * (10.0 ** rng.uniform(-6, 0)) for c in CH}
+        g = {c: (rng.normal(size=getattr(base, c).shape) * (10.0 ** rng.uniform(-6, 0)))
+             .astype(np.float32).astype(np.float64) for c in CH}
         mask = rng.uniform(size=(n + 127) // 128) < 0.7
         d[f"adam_g{k}"] = np.concatenate([g[c].reshape(n, -1) for c in CH], axis=1)
         d[f"adam_mask{k}"] = mask
