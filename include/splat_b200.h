@@ -98,16 +98,17 @@ int sb_tile_sort(const int32_t* tile_offsets, int32_t ntiles, uint64_t* pair_key
 /* forward.py:161-191 + 240-255: color (H,W,3), transmittance (H,W),
  * frag_count (H,W) and last[(H,W)] = 1 + list position of each pixel's last
  * contributing fragment (consumed by the backward). */
+size_t sb_raster_workspace_bytes(void);
 int sb_raster_fwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
                   const sb_raster_cfg* cfg, float* color, float* transmittance, int32_t* frag_count, int32_t* last,
-                  sb_stream_t stream);
+                  void* ws, size_t ws_bytes, sb_stream_t stream);
 
 /* ---- backward (backward.py:205-279) --------------------------------------- */
 /* backward.py:112-267: screen-space gradients + S/M/C per compact primitive.
  * sgrad[n_cap] is zeroed by the call. */
 int sb_raster_bwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
                   const sb_raster_cfg* cfg, const float* dL_dI, const float* transmittance, const int32_t* last,
-                  sb_screen_grad* sgrad, int64_t n_cap, sb_stream_t stream);
+                  sb_screen_grad* sgrad, int64_t n_cap, void* ws, size_t ws_bytes, sb_stream_t stream);
 
 /* backward.py:272-278 (_chain_projection 384-516 + scatter_grads
  * ccc.py:197-216 + stats np.add.at): grads (N, 16) float32 for every row
@@ -127,9 +128,18 @@ int sb_adam_sparse(float* params, const float* grads, float* m, float* v, int32_
 int sb_variance_score(const double* S, const double* M, const int32_t* C, int64_t n, double* out,
                       sb_stream_t stream);
 
+/* metrics.py:118-132 loss_and_grad, fused: (1 - lam) L1 + lam (1 - SSIM)
+ * over (H, W, 3) float32 images and dL/d rendered.  target is float32, or
+ * uint8 (value / 255) when target_u8 != NULL.  loss[0] (float64, device) is
+ * written on the stream; accum: 2 float64 scratch. */
+int sb_loss_fwd_bwd(const float* rendered, const float* target, const uint8_t* target_u8, int32_t width,
+                    int32_t height, float lam, float* grad, double* accum, double* loss, sb_stream_t stream);
+
 /* reduction.py:21-58 on `groups` groups of 32 float32 values:
  * mode 0 = lane_group_reduce (float32 butterfly), 1 = exp_aligned_reduce
- * (result cast to float32), 2 = lane_group_reduce in float64 (out_d). */
+ * (result cast to float32), 2 = lane_group_reduce in float64 (out_d),
+ * 3 / 4 = the raster backward's register row reductions (tree /
+ * exponent-aligned) on the same 32 values. */
 int sb_lane_reduce(const float* values, int64_t groups, int mode, float* out_f, double* out_d, sb_stream_t stream);
 
 #ifdef __cplusplus

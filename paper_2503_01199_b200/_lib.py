@@ -36,12 +36,14 @@ SIGNATURES = {
     "sb_bin_emit_workspace_bytes": ([I32], SZ),
     "sb_bin_emit": ([VP, VP, I64, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_tile_sort": ([VP, I32, VP, VP, VP, VP], C.c_int),
-    "sb_raster_fwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP], C.c_int),
-    "sb_raster_bwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, VP], C.c_int),
+    "sb_raster_workspace_bytes": ([], SZ),
+    "sb_raster_fwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_raster_bwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, VP, SZ, VP], C.c_int),
     "sb_chain_projection_bwd": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP], C.c_int),
     "sb_adam_sparse": ([VP, VP, VP, VP, VP, VP, I64, VP, VP], C.c_int),
     "sb_variance_score": ([VP, VP, VP, I64, VP, VP], C.c_int),
     "sb_lane_reduce": ([VP, I64, C.c_int, VP, VP, VP], C.c_int),
+    "sb_loss_fwd_bwd": ([VP, VP, VP, I32, I32, C.c_float, VP, VP, VP, VP], C.c_int),
 }
 
 
@@ -108,7 +110,7 @@ KERNELS_PER_CALL = {
     "sb_morton_keys": 3, "sb_permute_rows": 1, "sb_project_cull_compact": 1, "sb_bin_offsets": 1,
     "sb_bin_emit": 1, "sb_tile_sort": 1, "sb_raster_fwd": 1, "sb_raster_bwd": 1,
     "sb_chain_projection_bwd": 1, "sb_adam_sparse": 1, "sb_variance_score": 1, "sb_lane_reduce": 1,
-    "sb_loss_fwd_bwd": 1,
+    "sb_loss_fwd_bwd": 2,
 }
 launch_count = {"n": 0}
 # optional per-call CUDA-event timing: {name: [(start_event, end_event), ...]}

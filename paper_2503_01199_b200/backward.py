@@ -117,9 +117,10 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
     stream = C.c_void_p(_lib.stream_ptr(dev))
     nc = max(ctx.n_compact, 1)
     sgrad = _lib.workspace("sgrad", nc * SGRAD_BYTES, dev)
+    ws_r = _lib.workspace("raster_bwd", _lib.load().sb_raster_workspace_bytes(), dev)
     _lib.call("sb_raster_bwd", _lib.ptr(ctx.recs), _lib.ptr(ctx.tile_offsets), _lib.ptr(ctx.tile_prims),
               C.byref(cam_s), C.byref(cfg_s), _lib.ptr(dI), _lib.ptr(ctx.transmittance), _lib.ptr(ctx.last),
-              _lib.ptr(sgrad), ctx.n_compact, stream)
+              _lib.ptr(sgrad), ctx.n_compact, _lib.ptr(ws_r), ws_r.numel(), stream)
     grads = torch.empty((n, 16), dtype=torch.float32, device=dev)
     _lib.call("sb_chain_projection_bwd", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s),
               _lib.ptr(ctx.cluster_offset), _lib.ptr(sgrad), _lib.ptr(grads), _lib.ptr(stats.S),

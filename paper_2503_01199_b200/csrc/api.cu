@@ -14,13 +14,15 @@ void sb_launch_emit_pairs(const RasterRec*, const int32_t*, int, const int32_t*,
                           int, int, int, cudaStream_t);
 void sb_launch_tile_sort(const int32_t*, int, unsigned long long*, unsigned long long*, int32_t*, cudaStream_t);
 void sb_launch_raster_fwd(const RasterRec*, const int32_t*, const int32_t*, int, int, int, int, const sb_raster_cfg&,
-                          float*, float*, int32_t*, int32_t*, cudaStream_t);
+                          int*, float*, float*, int32_t*, int32_t*, cudaStream_t);
 void sb_launch_raster_bwd(const RasterRec*, const int32_t*, const int32_t*, int, int, int, int, const sb_raster_cfg&,
-                          const float*, const float*, const int32_t*, sb_screen_grad*, cudaStream_t);
+                          int*, const float*, const float*, const int32_t*, sb_screen_grad*, cudaStream_t);
 void sb_launch_lane_reduce(const float*, int, int, float*, double*, cudaStream_t);
 void sb_launch_chain(const float*, int, const CamDev&, const int32_t*, const sb_screen_grad*, float*, double*,
                      double*, int32_t*, cudaStream_t);
 void sb_launch_adam(float*, const float*, float*, float*, int32_t*, const uint8_t*, int, const double[5],
+                    cudaStream_t);
+void sb_launch_loss(const float*, const float*, const uint8_t*, int, int, float, float*, double*, double*,
                     cudaStream_t);
 void sb_launch_variance(const double*, const double*, const int32_t*, int, double*, cudaStream_t);
 void sb_launch_bounds(const float*, int, float*, double*, cudaStream_t);
@@ -188,27 +190,35 @@ int sb_tile_sort(const int32_t* tile_offsets, int32_t ntiles, uint64_t* pair_key
     return check_launch("sb_tile_sort");
 }
 
+size_t sb_raster_workspace_bytes(void) { return 256; }
+
 int sb_raster_fwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
                   const sb_raster_cfg* cfg, float* color, float* transmittance, int32_t* frag_count, int32_t* last,
-                  sb_stream_t stream) {
+                  void* ws, size_t ws_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
     if (cfg->half_state) return fail(SB_EINVAL, "half_state forward is not built in this version");
+    if (ws_bytes < sb_raster_workspace_bytes()) return fail(SB_EWORKSPACE, "raster workspace too small");
     const CamDev d = make_cam(cam, cfg);
+    cudaMemsetAsync(ws, 0, sizeof(int), S(stream));
     sb_launch_raster_fwd(static_cast<const RasterRec*>(recs), tile_offsets, tile_prims, d.W, d.H, d.tiles_x,
-                         d.tiles_x * d.tiles_y, *cfg, color, transmittance, frag_count, last, S(stream));
+                         d.tiles_x * d.tiles_y, *cfg, static_cast<int*>(ws), color, transmittance, frag_count, last,
+                         S(stream));
     return check_launch("sb_raster_fwd");
 }
 
 int sb_raster_bwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
                   const sb_raster_cfg* cfg, const float* dL_dI, const float* transmittance, const int32_t* last,
-                  sb_screen_grad* sgrad, int64_t n_cap, sb_stream_t stream) {
+                  sb_screen_grad* sgrad, int64_t n_cap, void* ws, size_t ws_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
+    if (ws_bytes < sb_raster_workspace_bytes()) return fail(SB_EWORKSPACE, "raster workspace too small");
     const CamDev d = make_cam(cam, cfg);
     if (n_cap > 0) cudaMemsetAsync(sgrad, 0, sizeof(sb_screen_grad) * (size_t)n_cap, S(stream));
+    cudaMemsetAsync(ws, 0, sizeof(int), S(stream));
     sb_launch_raster_bwd(static_cast<const RasterRec*>(recs), tile_offsets, tile_prims, d.W, d.H, d.tiles_x,
-                         d.tiles_x * d.tiles_y, *cfg, dL_dI, transmittance, last, sgrad, S(stream));
+                         d.tiles_x * d.tiles_y, *cfg, static_cast<int*>(ws), dL_dI, transmittance, last, sgrad,
+                         S(stream));
     return check_launch("sb_raster_bwd");
 }
 
@@ -238,8 +248,16 @@ int sb_variance_score(const double* S_, const double* M_, const int32_t* C_, int
     return check_launch("sb_variance_score");
 }
 
+int sb_loss_fwd_bwd(const float* rendered, const float* target, const uint8_t* target_u8, int32_t width,
+                    int32_t height, float lam, float* grad, double* accum, double* loss, sb_stream_t stream) {
+    if (width <= 0 || height <= 0) return fail(SB_EINVAL, "resolution must be positive");
+    if (!target && !target_u8) return fail(SB_EINVAL, "target is NULL");
+    sb_launch_loss(rendered, target, target_u8, width, height, lam, grad, accum, loss, S(stream));
+    return check_launch("sb_loss_fwd_bwd");
+}
+
 int sb_lane_reduce(const float* values, int64_t groups, int mode, float* out_f, double* out_d, sb_stream_t stream) {
-    if (mode < 0 || mode > 2) return fail(SB_EINVAL, "mode must be 0, 1 or 2");
+    if (mode < 0 || mode > 4) return fail(SB_EINVAL, "mode must be 0..4");
     if (groups < 0 || groups > INT32_MAX / 32) return fail(SB_EINVAL, "groups out of range");
     sb_launch_lane_reduce(values, (int)groups, mode, out_f, out_d, S(stream));
     return check_launch("sb_lane_reduce");

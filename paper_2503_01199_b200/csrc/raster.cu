@@ -15,18 +15,28 @@
 // T_final and last-contributor index, T recovered by division and the suffix
 // (sum_{j>k} w_j c_j + T_final bg) kept as a running sum; per-fragment
 // dL/dalpha, f = dL/do, u = dL/dG; scanline fold to per-lane (a,b,c,u,v)
-// partials; ONE warp reduction per channel (conic via the exponent-aligned
-// integer sum with REDUX max/add, the rest via the __shfl_xor butterfly, S/M in
-// float64) and ONE atomic per (primitive, tile, channel).
+// partials; then ONE 32-lane reduction per channel and ONE atomic per
+// (primitive, tile, channel).  Contributing fragments are batched 8 at a
+// time: every lane stores its 10 channel partials (a b c u v o r g b S) into a
+// bank-swizzled warp-private shared-memory batch, then each lane reduces whole
+// (fragment, channel) rows in registers:
+//   conic a,b,c  exponent-aligned integer sum (reduction.py:35-58): max
+//                exponent, integer round-half-even alignment, exact int sum;
+//   the rest     the reference's pairing tree v[:s] + v[s:2s], s = 16..1
+//                (reduction.py:21-32), bit-identical to a __shfl_xor butterfly.
+// This replaces per-fragment shuffle / REDUX chains with independent,
+// latency-tolerant register work (the kernel was dependency- and
+// branch-stall bound).  The warp-shuffle reductions remain for the
+// standalone reduction entry point (sb_lane_reduce).
 //
-// Records for 32 list entries at a time are gathered into a warp-private
-// shared-memory slab (lane l fetches entry l's 48-byte record with three
-// 128-bit loads) and then broadcast-read by all lanes.
+// Scheduling: warps pull tiles from an atomic counter (persistent grid), and
+// the 48-byte records of the next 32 list entries are fetched into registers
+// while the current 32 are consumed from a warp-private shared-memory slab.
 #include "common.cuh"
 
 namespace {
 
-constexpr int kWarpsPerBlock = 8;
+constexpr int kWarpsPerBlock = 4;
 constexpr int kThreads = kWarpsPerBlock * 32;
 
 struct __align__(16) SRec {
@@ -36,33 +46,35 @@ struct __align__(16) SRec {
     int32_t slot;
 };
 
-struct FwdParams {
-    const RasterRec* recs;
-    const int32_t* offsets;
-    const int32_t* prims;
-    int W, H, tiles_x, ntiles;
-    float amin, amax, tstop;
-    float bg[3];
-    float* out_color;   // (H, W, 3)
-    float* out_T;       // (H, W)
-    int32_t* out_frags; // (H, W)
-    int32_t* out_last;  // (H, W): 1 + list position of the last contributing fragment
+struct Prefetch {
+    float4 a, b;
+    float bl;
+    int slot;
 };
 
-SB_INLINE void load_chunk(SRec* slab, const RasterRec* __restrict__ recs, const int32_t* __restrict__ prims,
-                          int beg, int k0, int cnt, int lane) {
+SB_INLINE void prefetch_chunk(Prefetch& pf, const RasterRec* __restrict__ recs, const int32_t* __restrict__ prims,
+                              int beg, int k0, int cnt, int lane) {
     if (lane < cnt) {
         const int slot = __ldg(prims + beg + k0 + lane);
         const float4* r4 = reinterpret_cast<const float4*>(recs + slot);
-        const float4 a = __ldg(r4), b = __ldg(r4 + 1), c = __ldg(r4 + 2);
-        float4* d = reinterpret_cast<float4*>(slab + lane);
-        d[0] = a;
-        d[1] = b;
-        d[2] = make_float4(c.x, 0.f, 0.f, __int_as_float(slot));
+        pf.a = __ldg(r4);
+        pf.b = __ldg(r4 + 1);
+        pf.bl = __ldg(reinterpret_cast<const float*>(r4 + 2));
+        pf.slot = slot;
     }
 }
 
-// scanline exponent (forward.py:97-108) with numpy's operation order
+SB_INLINE void commit_chunk(SRec* slab, const Prefetch& pf, int cnt, int lane) {
+    if (lane < cnt) {
+        float4* d = reinterpret_cast<float4*>(slab + lane);
+        d[0] = pf.a;
+        d[1] = pf.b;
+        d[2] = make_float4(pf.bl, 0.f, 0.f, __int_as_float(pf.slot));
+    }
+}
+
+// scanline exponent (forward.py:97-108) with numpy's operation order; the
+// forward and backward share it so both see bit-identical alphas
 SB_INLINE void lane_G(const SRec& r, float px, float py0, float G[4], float& dx, float& dy) {
     dx = FSUB(r.x, px);
     dy = FSUB(r.y, py0);
@@ -77,72 +89,95 @@ SB_INLINE void lane_G(const SRec& r, float px, float py0, float G[4], float& dx,
     }
 }
 
+SB_INLINE int next_tile(int* counter, int lane) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(counter, 1);
+    return __shfl_sync(0xffffffffu, t, 0);
+}
+
+struct FwdParams {
+    const RasterRec* recs;
+    const int32_t* offsets;
+    const int32_t* prims;
+    int W, H, tiles_x, ntiles;
+    float amin, amax, tstop;
+    float bg[3];
+    int* tile_counter;
+    float* out_color;   // (H, W, 3)
+    float* out_T;       // (H, W)
+    int32_t* out_frags; // (H, W)
+    int32_t* out_last;  // (H, W): 1 + list position of the last contributing fragment
+};
+
 __global__ void __launch_bounds__(kThreads)
 raster_fwd_kernel(FwdParams p)
 {
     __shared__ SRec slabs[kWarpsPerBlock][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t = blockIdx.x * kWarpsPerBlock + warp;
-    if (t >= p.ntiles) return;
     SRec* slab = slabs[warp];
-    const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
-    const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
-    const float px = (float)pxi, py0 = (float)py0i;
-    bool valid[4];
-    float T[4], rgb[4][3];
-    int frags[4], last[4];
+    for (int t = next_tile(p.tile_counter, lane); t < p.ntiles; t = next_tile(p.tile_counter, lane)) {
+        const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
+        const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
+        const float px = (float)pxi, py0 = (float)py0i;
+        bool valid[4];
+        float T[4], rgb[4][3];
+        int frags[4], last[4];
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-        valid[i] = pxi < p.W && py0i + i < p.H;
-        T[i] = 1.0f;
-        rgb[i][0] = rgb[i][1] = rgb[i][2] = 0.0f;
-        frags[i] = 0;
-        last[i] = 0;
-    }
-    const int beg = p.offsets[t], end = p.offsets[t + 1];
-    bool warp_done = false;
-    for (int k0 = 0; beg + k0 < end && !warp_done; k0 += 32) {
-        const int cnt = min(32, end - beg - k0);
-        __syncwarp();
-        load_chunk(slab, p.recs, p.prims, beg, k0, cnt, lane);
-        __syncwarp();
-        for (int j = 0; j < cnt; j++) {
-            bool live = false;
+        for (int i = 0; i < 4; i++) {
+            valid[i] = pxi < p.W && py0i + i < p.H;
+            T[i] = 1.0f;
+            rgb[i][0] = rgb[i][1] = rgb[i][2] = 0.0f;
+            frags[i] = 0;
+            last[i] = 0;
+        }
+        const int beg = p.offsets[t], n = p.offsets[t + 1] - beg;
+        Prefetch pf;
+        if (n > 0) prefetch_chunk(pf, p.recs, p.prims, beg, 0, min(32, n), lane);
+        bool done = false;
+        for (int k0 = 0; k0 < n && !done; k0 += 32) {
+            const int cnt = min(32, n - k0);
+            __syncwarp();
+            commit_chunk(slab, pf, cnt, lane);
+            __syncwarp();
+            if (k0 + 32 < n) prefetch_chunk(pf, p.recs, p.prims, beg, k0 + 32, min(32, n - k0 - 32), lane);
+            for (int j = 0; j < cnt; j++) {
+                bool live = false;
 #pragma unroll
-            for (int i = 0; i < 4; i++) live |= valid[i] && T[i] >= p.tstop;
-            if (!__any_sync(0xffffffffu, live)) {
-                warp_done = true;
-                break;
-            }
-            if (!live) continue;
-            const SRec r = slab[j];
-            float G[4], dx, dy;
-            lane_G(r, px, py0, G, dx, dy);
+                for (int i = 0; i < 4; i++) live |= valid[i] && T[i] >= p.tstop;
+                if (!__any_sync(0xffffffffu, live)) {
+                    done = true;
+                    break;
+                }
+                if (!live) continue;
+                const SRec r = slab[j];
+                float G[4], dx, dy;
+                lane_G(r, px, py0, G, dx, dy);
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
-                float alpha = fminf(FMUL(r.o, G[i]), p.amax);
-                if (valid[i] && T[i] >= p.tstop && alpha >= p.amin) {
-                    const float w = FMUL(T[i], alpha);
-                    rgb[i][0] = FADD(rgb[i][0], FMUL(w, r.r));
-                    rgb[i][1] = FADD(rgb[i][1], FMUL(w, r.g));
-                    rgb[i][2] = FADD(rgb[i][2], FMUL(w, r.bl));
-                    T[i] = FMUL(T[i], FSUB(1.0f, alpha));
-                    frags[i]++;
-                    last[i] = k0 + j + 1;
+                for (int i = 0; i < 4; i++) {
+                    const float alpha = fminf(FMUL(r.o, G[i]), p.amax);
+                    if (valid[i] && T[i] >= p.tstop && alpha >= p.amin) {
+                        const float w = FMUL(T[i], alpha);
+                        rgb[i][0] = FADD(rgb[i][0], FMUL(w, r.r));
+                        rgb[i][1] = FADD(rgb[i][1], FMUL(w, r.g));
+                        rgb[i][2] = FADD(rgb[i][2], FMUL(w, r.bl));
+                        T[i] = FMUL(T[i], FSUB(1.0f, alpha));
+                        frags[i]++;
+                        last[i] = k0 + j + 1;
+                    }
                 }
             }
         }
-    }
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-        if (!valid[i]) continue;
-        const size_t pix = (size_t)(py0i + i) * p.W + pxi;
-        p.out_color[3 * pix + 0] = FADD(rgb[i][0], FMUL(T[i], p.bg[0]));
-        p.out_color[3 * pix + 1] = FADD(rgb[i][1], FMUL(T[i], p.bg[1]));
-        p.out_color[3 * pix + 2] = FADD(rgb[i][2], FMUL(T[i], p.bg[2]));
-        p.out_T[pix] = T[i];
-        p.out_frags[pix] = frags[i];
-        p.out_last[pix] = last[i];
+        for (int i = 0; i < 4; i++) {
+            if (!valid[i]) continue;
+            const size_t pix = (size_t)(py0i + i) * p.W + pxi;
+            p.out_color[3 * pix + 0] = FADD(rgb[i][0], FMUL(T[i], p.bg[0]));
+            p.out_color[3 * pix + 1] = FADD(rgb[i][1], FMUL(T[i], p.bg[1]));
+            p.out_color[3 * pix + 2] = FADD(rgb[i][2], FMUL(T[i], p.bg[2]));
+            p.out_T[pix] = T[i];
+            p.out_frags[pix] = frags[i];
+            p.out_last[pix] = last[i];
+        }
     }
 }
 
@@ -154,6 +189,7 @@ struct BwdParams {
     float amin, amax, tstop;
     float bg[3];
     int conic_tree;
+    int* tile_counter;
     const float* dL_dI;     // (H, W, 3)
     const float* T_final;   // (H, W)
     const int32_t* last;    // (H, W)
@@ -172,170 +208,281 @@ SB_INLINE double warp_tree_d(double v) {
     return v;
 }
 
-// reduction.py:35-58 exponent-aligned integer sum (bit-exact given identical
-// lane inputs): e = floor(log2|v|) of nonzeros, e_max by REDUX.MAX, mantissas
-// rint(v * 2^(23 - e_max)) summed exactly by REDUX.SUM, result cast to float32.
-SB_INLINE float warp_exp_aligned(float v) {
-    const uint32_t bits = __float_as_uint(v);
+// floor(log2|v|) of a float32 (frexp exponent - 1); INT_MIN for zero
+SB_INLINE int f32_exponent(uint32_t bits) {
     const uint32_t ef = (bits >> 23) & 0xffu, mant = bits & 0x7fffffu;
-    int e;
-    if ((bits & 0x7fffffffu) == 0) e = INT_MIN;
-    else if (ef == 0) e = (31 - __clz((int)mant)) - 149;
-    else e = (int)ef - 127;
-    const int emax = __reduce_max_sync(0xffffffffu, e);
-    if (emax == INT_MIN) return 0.0f;
-    const int shift = 23 - emax;
-    const int m = (int)__double2ll_rn(ldexp((double)v, shift));
-    const int total = __reduce_add_sync(0xffffffffu, m);
-    return (float)ldexp((double)total, -shift);
+    if ((bits & 0x7fffffffu) == 0) return INT_MIN;
+    if (ef == 0) return (31 - __clz((int)mant)) - 149;
+    return (int)ef - 127;
 }
 
-__global__ void __launch_bounds__(kThreads)
+// rint(v * 2^(23 - emax)) in pure integer arithmetic (round half to even)
+SB_INLINE int aligned_mantissa(uint32_t bits, int emax) {
+    if ((bits & 0x7fffffffu) == 0) return 0;
+    const uint32_t ef = (bits >> 23) & 0xffu;
+    uint32_t M;
+    int E;
+    if (ef == 0) { M = bits & 0x7fffffu; E = -149; }
+    else { M = (bits & 0x7fffffu) | 0x800000u; E = (int)ef - 150; }
+    const int sh = emax - 23 - E;
+    int m;
+    if (sh <= 0) {
+        m = (int)(M << (-sh));
+    } else if (sh >= 32) {
+        m = 0;
+    } else {
+        const uint32_t q = M >> sh, rem = M & ((1u << sh) - 1u), half = 1u << (sh - 1);
+        m = (int)(q + ((rem > half || (rem == half && (q & 1u))) ? 1u : 0u));
+    }
+    return (bits >> 31) ? -m : m;
+}
+
+// reduction.py:35-58 exponent-aligned integer sum; bit-exact given identical
+// lane inputs; result rounded once to float32 (the reference's astype)
+SB_INLINE float warp_exp_aligned(float v) {
+    const uint32_t bits = __float_as_uint(v);
+    const int emax = __reduce_max_sync(0xffffffffu, f32_exponent(bits));
+    if (emax == INT_MIN) return 0.0f;
+    const int total = __reduce_add_sync(0xffffffffu, aligned_mantissa(bits, emax));
+    const double scale = __longlong_as_double((long long)(emax - 23 + 1023) << 52);
+    return __double2float_rn((double)total * scale);
+}
+
+SB_INLINE float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Batched transpose for the backward: contributing fragments append their
+// per-lane partials (10 channels) to a warp-private shared-memory batch; a
+// full batch is reduced row-wise (one (fragment, channel) row of 32 lane
+// values per lane at a time) and flushed with one atomic per row.
+constexpr int kBatch = 8;
+constexpr int kCh = 10;            // a b c | u v o r g bl | S
+constexpr int kRows = kBatch * kCh;
+
+struct BwdWarpSmem {
+    SRec slab[32];
+    float part[kRows * 32];        // row r holds lane l at ((l + 4 * (r & 7)) & 31)
+    int slot[kBatch];
+    int count[kBatch];
+};
+
+SB_INLINE void put_part(float* part, int row, int lane, float v) {
+    part[row * 32 + ((lane + 4 * (row & 7)) & 31)] = v;
+}
+
+// exact v * 2^s for float32 v with |v * 2^s| < 2^24 (power-of-two scaling is
+// exact unless the result is subnormal, and then |result| < 0.5 rounds to 0)
+SB_INLINE float scale_pow2(float v, int s) {
+    if (s > 126) {
+        v *= __int_as_float((127 + 64) << 23);
+        s -= 64;
+    }
+    if (s < -126) return 0.0f;
+    return v * __int_as_float((127 + s) << 23);
+}
+
+// reduction.py:35-58 over one row of 32 lane values held in registers:
+// max exponent, exact integer alignment (round half to even), exact int sum,
+// one rounding to float32
+SB_INLINE float row_exp_aligned(const float v[32]) {
+    uint32_t mx = 0;
+#pragma unroll
+    for (int l = 0; l < 32; l++) mx = max(mx, __float_as_uint(v[l]) & 0x7fffffffu);
+    if (mx == 0) return 0.0f;
+    const int emax = f32_exponent(mx);
+    const int sh = 23 - emax;
+    int total = 0;
+#pragma unroll
+    for (int l = 0; l < 32; l++) total += __float2int_rn(scale_pow2(v[l], sh));
+    const double scale = __longlong_as_double((long long)(emax - 23 + 1023) << 52);
+    return __double2float_rn((double)total * scale);
+}
+
+// reduction.py:21-32 tree v[:s] + v[s:2s], s = 16..1, in registers
+SB_INLINE float row_tree(float v[32]) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1)
+#pragma unroll
+        for (int l = 0; l < s; l++) v[l] = v[l] + v[l + s];
+    return v[0];
+}
+
+// rows of a batch: conic rows first (3 per fragment) so lanes of one
+// iteration take the same reduction path, then the 7 tree rows per fragment
+SB_INLINE int conic_row(int b, int c) { return b * 3 + c; }
+SB_INLINE int tree_row(int b, int c) { return kBatch * 3 + b * 7 + (c - 3); }
+
+SB_INLINE void flush_batch(BwdWarpSmem& ws, int nb, int lane, int conic_tree, sb_screen_grad* grads) {
+    __syncwarp();
+    const int n_conic = nb * 3;
+    for (int i = lane; i < n_conic + nb * 7; i += 32) {
+        int row, b, c;
+        if (i < n_conic) {
+            b = i / 3; c = i - 3 * b; row = conic_row(b, c);
+        } else {
+            const int t = i - n_conic;
+            b = t / 7; c = 3 + (t - 7 * b); row = tree_row(b, c);
+        }
+        float v[32];
+        const float* base = ws.part + row * 32;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const float4 x = *reinterpret_cast<const float4*>(base + 4 * ((q + (row & 7)) & 7));
+            v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+        }
+        const float out = (c < 3 && !conic_tree) ? row_exp_aligned(v) : row_tree(v);
+        sb_screen_grad* gr = grads + ws.slot[b];
+        if (c < 9) {
+            atomicAdd(reinterpret_cast<float*>(gr) + c, out);
+            if (c == 5) atomicAdd(&gr->M, (double)out);       // M = sum of dL/do over the tile
+            if (c == 0) atomicAdd(&gr->C, ws.count[b]);
+        } else {
+            atomicAdd(&gr->S, (double)out);
+        }
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
 raster_bwd_kernel(BwdParams p)
 {
-    __shared__ SRec slabs[kWarpsPerBlock][32];
+    __shared__ BwdWarpSmem wsm[kWarpsPerBlock];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t = blockIdx.x * kWarpsPerBlock + warp;
-    if (t >= p.ntiles) return;
-    const int beg = p.offsets[t], end = p.offsets[t + 1];
-    if (beg == end) return;
-    SRec* slab = slabs[warp];
-    const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
-    const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
-    const float px = (float)pxi, py0 = (float)py0i;
-    float T[4], suf[4][3], dI[4][3];
-    int last[4];
-    int kmax = 0;
+    BwdWarpSmem& ws = wsm[warp];
+    for (int t = next_tile(p.tile_counter, lane); t < p.ntiles; t = next_tile(p.tile_counter, lane)) {
+        const int beg = p.offsets[t];
+        if (p.offsets[t + 1] == beg) continue;
+        const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
+        const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
+        const float px = (float)pxi, py0 = (float)py0i;
+        float T[4], suf[4][3], dI[4][3];
+        int last[4];
+        int lane_max = 0;
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-        const bool v = pxi < p.W && py0i + i < p.H;
-        const size_t pix = (size_t)(py0i + i) * p.W + pxi;
-        T[i] = v ? p.T_final[pix] : 1.0f;
-        last[i] = v ? p.last[pix] : 0;
-        for (int ch = 0; ch < 3; ch++) {
-            dI[i][ch] = v ? p.dL_dI[3 * pix + ch] : 0.0f;
-            suf[i][ch] = FMUL(T[i], p.bg[ch]);
+        for (int i = 0; i < 4; i++) {
+            const bool v = pxi < p.W && py0i + i < p.H;
+            const size_t pix = (size_t)(py0i + i) * p.W + pxi;
+            T[i] = v ? p.T_final[pix] : 1.0f;
+            last[i] = v ? p.last[pix] : 0;
+#pragma unroll
+            for (int ch = 0; ch < 3; ch++) {
+                dI[i][ch] = v ? p.dL_dI[3 * pix + ch] : 0.0f;
+                suf[i][ch] = T[i] * p.bg[ch];
+            }
+            lane_max = max(lane_max, last[i]);
         }
-        kmax = max(kmax, last[i]);
-    }
-    kmax = __reduce_max_sync(0xffffffffu, kmax);
-    for (int k1 = kmax; k1 > 0; k1 -= 32) {
-        const int k0 = max(0, k1 - 32), cnt = k1 - k0;
-        __syncwarp();
-        load_chunk(slab, p.recs, p.prims, beg, k0, cnt, lane);
-        __syncwarp();
-        for (int j = cnt - 1; j >= 0; j--) {
-            const int k = k0 + j;
-            const SRec r = slab[j];
-            float G[4], dx, dy;
-            bool any = false;
+        const int kmax = __reduce_max_sync(0xffffffffu, lane_max);
+        Prefetch pf;
+        if (kmax > 0) prefetch_chunk(pf, p.recs, p.prims, beg, max(0, kmax - 32), kmax - max(0, kmax - 32), lane);
+        int nb = 0;
+        for (int k1 = kmax; k1 > 0; k1 -= 32) {
+            const int k0 = max(0, k1 - 32), cnt = k1 - k0;
+            __syncwarp();
+            commit_chunk(ws.slab, pf, cnt, lane);
+            __syncwarp();
+            if (k0 > 0) prefetch_chunk(pf, p.recs, p.prims, beg, max(0, k0 - 32), k0 - max(0, k0 - 32), lane);
+            for (int j = cnt - 1; j >= 0; j--) {
+                const int k = k0 + j;
+                const bool act = k < lane_max;
+                if (!__any_sync(0xffffffffu, act)) continue;
+                const SRec& r = ws.slab[j];
+                float f[4], uG[4], w[4];
+                float dx = 0.f, dy = 0.f;
+                int cnt_l = 0;
+                {
+                    float G[4];
+                    lane_G(r, px, py0, G, dx, dy);
 #pragma unroll
-            for (int i = 0; i < 4; i++) any |= k < last[i];
-            float f[4], u[4], w[4];
-            int cnt_l = 0;
-            if (any) {
-                lane_G(r, px, py0, G, dx, dy);
-#pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    f[i] = u[i] = w[i] = 0.0f;
-                    const float araw = FMUL(r.o, G[i]);
-                    const float alpha = fminf(araw, p.amax);
-                    if (k < last[i] && alpha >= p.amin) {
-                        // contributing fragment: every fragment before the last
-                        // contributor is active (T is non-increasing)
-                        const float om = FSUB(1.0f, alpha);
-                        const float Tb = FDIV(T[i], om);
-                        w[i] = FMUL(Tb, alpha);
-                        float da = FMUL(dI[i][0], FSUB(FMUL(Tb, r.r), FDIV(suf[i][0], om)));
-                        da = FADD(da, FMUL(dI[i][1], FSUB(FMUL(Tb, r.g), FDIV(suf[i][1], om))));
-                        da = FADD(da, FMUL(dI[i][2], FSUB(FMUL(Tb, r.bl), FDIV(suf[i][2], om))));
-                        const float dpre = araw < p.amax ? da : 0.0f;
-                        f[i] = FMUL(dpre, G[i]);
-                        u[i] = FMUL(dpre, r.o);
-                        suf[i][0] = FADD(suf[i][0], FMUL(w[i], r.r));
-                        suf[i][1] = FADD(suf[i][1], FMUL(w[i], r.g));
-                        suf[i][2] = FADD(suf[i][2], FMUL(w[i], r.bl));
-                        T[i] = Tb;
-                        cnt_l++;
+                    for (int i = 0; i < 4; i++) {
+                        const float araw = FMUL(r.o, G[i]);
+                        const float alpha = fminf(araw, p.amax);
+                        // contributing: before this pixel's last contributor and usable
+                        const bool ci = (k < last[i]) && (alpha >= p.amin);
+                        const float inv = rcp_approx(1.0f - alpha);
+                        const float Tb = T[i] * inv;
+                        const float wi = Tb * alpha;
+                        float da = dI[i][0] * (Tb * r.r - suf[i][0] * inv);
+                        da += dI[i][1] * (Tb * r.g - suf[i][1] * inv);
+                        da += dI[i][2] * (Tb * r.bl - suf[i][2] * inv);
+                        const float dpre = (ci && araw < p.amax) ? da : 0.0f;
+                        f[i] = dpre * G[i];
+                        uG[i] = dpre * r.o * G[i];
+                        w[i] = ci ? wi : 0.0f;
+                        suf[i][0] += w[i] * r.r;
+                        suf[i][1] += w[i] * r.g;
+                        suf[i][2] += w[i] * r.bl;
+                        T[i] = ci ? Tb : T[i];
+                        cnt_l += ci ? 1 : 0;
                     }
                 }
-            }
-            if (!__any_sync(0xffffffffu, cnt_l > 0)) continue;
-            float ch9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-            double s2 = 0.0, s1 = 0.0;
-            if (cnt_l > 0) {
-                // scanline_grad_fold (backward.py:175-196)
-                float uG[4];
-#pragma unroll
-                for (int i = 0; i < 4; i++) uG[i] = FMUL(u[i], G[i]);
-                const float gb = FADD(FADD(FADD(uG[0], uG[1]), uG[2]), uG[3]);
-                const float gl = FADD(FADD(uG[1], FMUL(uG[2], 2.0f)), FMUL(uG[3], 3.0f));
-                const float gq = FADD(FADD(uG[1], FMUL(uG[2], 4.0f)), FMUL(uG[3], 9.0f));
-                ch9[0] = FMUL(gb, FMUL(FMUL(-0.5f, dx), dx));
-                ch9[1] = FADD(FMUL(gb, FMUL(-dx, dy)), FMUL(gl, dx));
-                ch9[2] = FADD(FADD(FMUL(gb, FMUL(FMUL(-0.5f, dy), dy)), FMUL(gl, dy)), FMUL(gq, -0.5f));
-                ch9[3] = FADD(FMUL(gb, -FADD(FMUL(r.a, dx), FMUL(r.b, dy))), FMUL(gl, r.b));
-                ch9[4] = FADD(FMUL(gb, -FADD(FMUL(r.b, dx), FMUL(r.c, dy))), FMUL(gl, r.c));
-                ch9[5] = FADD(FADD(FADD(f[0], f[1]), f[2]), f[3]);
-                ch9[6] = FADD(FADD(FADD(FMUL(w[0], dI[0][0]), FMUL(w[1], dI[1][0])), FMUL(w[2], dI[2][0])),
-                              FMUL(w[3], dI[3][0]));
-                ch9[7] = FADD(FADD(FADD(FMUL(w[0], dI[0][1]), FMUL(w[1], dI[1][1])), FMUL(w[2], dI[2][1])),
-                              FMUL(w[3], dI[3][1]));
-                ch9[8] = FADD(FADD(FADD(FMUL(w[0], dI[0][2]), FMUL(w[1], dI[1][2])), FMUL(w[2], dI[2][2])),
-                              FMUL(w[3], dI[3][2]));
-#pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const double fd = (double)f[i];
-                    s2 = DADD(s2, DMUL(fd, fd));
-                    s1 = DADD(s1, fd);
+                const bool contrib = cnt_l > 0;
+                if (!__any_sync(0xffffffffu, contrib)) continue;
+                // scanline_grad_fold (backward.py:175-196) + per-lane partials
+                const float gb = ((uG[0] + uG[1]) + uG[2]) + uG[3];
+                const float gl = (uG[1] + uG[2] * 2.0f) + uG[3] * 3.0f;
+                const float gq = (uG[1] + uG[2] * 4.0f) + uG[3] * 9.0f;
+                put_part(ws.part, conic_row(nb, 0), lane, gb * (-0.5f * dx * dx));
+                put_part(ws.part, conic_row(nb, 1), lane, gb * (-dx * dy) + gl * dx);
+                put_part(ws.part, conic_row(nb, 2), lane, (gb * (-0.5f * dy * dy) + gl * dy) + gq * -0.5f);
+                put_part(ws.part, tree_row(nb, 3), lane, gb * -(r.a * dx + r.b * dy) + gl * r.b);
+                put_part(ws.part, tree_row(nb, 4), lane, gb * -(r.b * dx + r.c * dy) + gl * r.c);
+                put_part(ws.part, tree_row(nb, 5), lane, ((f[0] + f[1]) + f[2]) + f[3]);
+                put_part(ws.part, tree_row(nb, 6), lane,
+                         ((w[0] * dI[0][0] + w[1] * dI[1][0]) + w[2] * dI[2][0]) + w[3] * dI[3][0]);
+                put_part(ws.part, tree_row(nb, 7), lane,
+                         ((w[0] * dI[0][1] + w[1] * dI[1][1]) + w[2] * dI[2][1]) + w[3] * dI[3][1]);
+                put_part(ws.part, tree_row(nb, 8), lane,
+                         ((w[0] * dI[0][2] + w[1] * dI[1][2]) + w[2] * dI[2][2]) + w[3] * dI[3][2]);
+                put_part(ws.part, tree_row(nb, 9), lane, ((f[0] * f[0] + f[1] * f[1]) + f[2] * f[2]) + f[3] * f[3]);
+                const int C = __reduce_add_sync(0xffffffffu, cnt_l);
+                if (lane == 0) {
+                    ws.slot[nb] = r.slot;
+                    ws.count[nb] = C;
+                }
+                if (++nb == kBatch) {
+                    flush_batch(ws, nb, lane, p.conic_tree, p.grads);
+                    nb = 0;
                 }
             }
-            float red[9];
-            if (p.conic_tree) {
-                red[0] = warp_tree_f(ch9[0]);
-                red[1] = warp_tree_f(ch9[1]);
-                red[2] = warp_tree_f(ch9[2]);
-            } else {
-                red[0] = warp_exp_aligned(ch9[0]);
-                red[1] = warp_exp_aligned(ch9[1]);
-                red[2] = warp_exp_aligned(ch9[2]);
-            }
-#pragma unroll
-            for (int q = 3; q < 9; q++) red[q] = warp_tree_f(ch9[q]);
-            const double S = warp_tree_d(s2), M = warp_tree_d(s1);
-            const int C = __reduce_add_sync(0xffffffffu, cnt_l);
-            // one atomic per (primitive, tile, channel): lane q owns channel q
-            sb_screen_grad* gr = p.grads + r.slot;
-            float mine = 0.0f;
-#pragma unroll
-            for (int q = 0; q < 9; q++)
-                if (lane == q) mine = red[q];
-            if (lane < 9) atomicAdd(reinterpret_cast<float*>(gr) + lane, mine);
-            else if (lane == 9) atomicAdd(&gr->C, C);
-            else if (lane == 10) atomicAdd(&gr->S, S);
-            else if (lane == 11) atomicAdd(&gr->M, M);
         }
+        if (nb) flush_batch(ws, nb, lane, p.conic_tree, p.grads);
     }
 }
 
 }  // namespace
 
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
 void sb_launch_raster_fwd(const RasterRec* recs, const int32_t* offsets, const int32_t* prims, int W, int H,
-                          int tiles_x, int ntiles, const sb_raster_cfg& cfg, float* color, float* T,
-                          int32_t* frags, int32_t* last, cudaStream_t stream)
+                          int tiles_x, int ntiles, const sb_raster_cfg& cfg, int* tile_counter, float* color,
+                          float* T, int32_t* frags, int32_t* last, cudaStream_t stream)
 {
     FwdParams p;
     p.recs = recs; p.offsets = offsets; p.prims = prims;
     p.W = W; p.H = H; p.tiles_x = tiles_x; p.ntiles = ntiles;
     p.amin = cfg.alpha_min; p.amax = cfg.alpha_max; p.tstop = cfg.t_stop;
     for (int c = 0; c < 3; c++) p.bg[c] = cfg.background[c];
+    p.tile_counter = tile_counter;
     p.out_color = color; p.out_T = T; p.out_frags = frags; p.out_last = last;
-    const int blocks = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int want = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int blocks = min(want, sm_count() * 8);
     if (blocks) raster_fwd_kernel<<<blocks, kThreads, 0, stream>>>(p);
 }
 
 void sb_launch_raster_bwd(const RasterRec* recs, const int32_t* offsets, const int32_t* prims, int W, int H,
-                          int tiles_x, int ntiles, const sb_raster_cfg& cfg, const float* dL_dI,
+                          int tiles_x, int ntiles, const sb_raster_cfg& cfg, int* tile_counter, const float* dL_dI,
                           const float* T_final, const int32_t* last, sb_screen_grad* grads, cudaStream_t stream)
 {
     BwdParams p;
@@ -344,8 +491,10 @@ void sb_launch_raster_bwd(const RasterRec* recs, const int32_t* offsets, const i
     p.amin = cfg.alpha_min; p.amax = cfg.alpha_max; p.tstop = cfg.t_stop;
     for (int c = 0; c < 3; c++) p.bg[c] = cfg.background[c];
     p.conic_tree = cfg.conic_reduce == 1;
+    p.tile_counter = tile_counter;
     p.dL_dI = dL_dI; p.T_final = T_final; p.last = last; p.grads = grads;
-    const int blocks = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int want = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int blocks = min(want, sm_count() * 4);
     if (blocks) raster_bwd_kernel<<<blocks, kThreads, 0, stream>>>(p);
 }
 
@@ -364,9 +513,15 @@ __global__ void lane_reduce_kernel(const float* __restrict__ v, int groups, int 
     } else if (mode == 1) {
         const float r = warp_exp_aligned(x);
         if (lane == 0) out_f[gw] = r;
-    } else {
+    } else if (mode == 2) {
         const double r = warp_tree_d((double)x);
         if (lane == 0) out_d[gw] = r;
+    } else if (lane == 0) {
+        // modes 3 / 4: the backward's register row reductions (tree /
+        // exponent-aligned) on the same 32 values
+        float row[32];
+        for (int l = 0; l < 32; l++) row[l] = v[(size_t)gw * 32 + l];
+        out_f[gw] = mode == 3 ? row_tree(row) : row_exp_aligned(row);
     }
 }
 }  // namespace

@@ -170,8 +170,10 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     T = torch.empty((H, W), dtype=torch.float32, device=dev)
     frags = torch.empty((H, W), dtype=torch.int32, device=dev)
     last = torch.empty((H, W), dtype=torch.int32, device=dev)
+    ws_r = _lib.workspace("raster_fwd", _lib.load().sb_raster_workspace_bytes(), dev)
     _lib.call("sb_raster_fwd", _lib.ptr(recs), _lib.ptr(tile_offsets), _lib.ptr(prims), C.byref(cam_s),
-              C.byref(cfg_s), _lib.ptr(color), _lib.ptr(T), _lib.ptr(frags), _lib.ptr(last), stream)
+              C.byref(cfg_s), _lib.ptr(color), _lib.ptr(T), _lib.ptr(frags), _lib.ptr(last), _lib.ptr(ws_r),
+              ws_r.numel(), stream)
     out = RenderOutput(color=color, transmittance=T, frag_count=frags)
     ctx = RenderContext(generation=scene.generation, camera=camera, config=config, n_total=n, n_clusters=K,
                         n_compact=nc, n_pairs=P, visible_clusters=vis, culled_clusters=K - vis, recs=recs,

@@ -1,11 +1,11 @@
 """Training loss on the device: (1 - lambda) L1 + lambda (1 - SSIM) and its
-analytic image gradient, plus PSNR.
+analytic image gradient, plus PSNR / SSIM.
 
 Reference: pkg/src/tinysplat/metrics.py:18-132 (float64 with scipy's
 correlate1d, 11x11 Gaussian window sigma 1.5, valid interior, adjoint by
-zero-embedding).  Here: the same formulas as separable torch conv2d in
-float32 on the rendered image's device (a fused CUDA
-kernel is the next step).
+zero-embedding).  `loss_and_grad` runs the fused CUDA kernel
+(sb_loss_fwd_bwd, one pass over the image); the separable torch conv2d
+restatement below (`loss_and_grad_torch`) is kept as an independent check.
 """
 from __future__ import annotations
 
@@ -95,9 +95,37 @@ def psnr(a, b) -> float:
     return math.inf if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
 
 
-def loss_and_grad(rendered: torch.Tensor, target: torch.Tensor, lam: float, return_tensor: bool = False):
-    """(loss, dL/d rendered) for (H, W, 3) images (metrics.py:118-132).
-    With return_tensor=True the loss stays a 0-d device tensor (no sync)."""
+def loss_and_grad(rendered: torch.Tensor, target, lam: float, return_tensor: bool = False):
+    """(loss, dL/d rendered) for (H, W, 3) images (metrics.py:118-132), fused
+    kernel.  `target` may be float (any dtype) or uint8 (value / 255).  With
+    return_tensor=True the loss stays a 0-d float64 device tensor (no sync)."""
+    import ctypes as C
+    from . import _lib
+    from .errors import ShapeMismatchError
+    _lib.require_cuda(rendered)
+    x = rendered.float().contiguous()
+    H, W, nch = x.shape
+    if nch != 3:
+        raise ShapeMismatchError(f"expected (H, W, 3) images, got {tuple(x.shape)}")
+    y = torch.as_tensor(target, device=x.device)
+    if tuple(y.shape) != tuple(x.shape):
+        raise ShapeMismatchError(f"loss shapes {tuple(x.shape)} vs {tuple(y.shape)}")
+    y8 = None
+    if y.dtype == torch.uint8:
+        y8, y = y.contiguous(), None
+    else:
+        y = y.float().contiguous()
+    grad = torch.empty_like(x)
+    acc = torch.empty(3, dtype=torch.float64, device=x.device)
+    _lib.call("sb_loss_fwd_bwd", _lib.ptr(x), _lib.ptr(y), _lib.ptr(y8), W, H, float(lam), _lib.ptr(grad),
+              _lib.ptr(acc), _lib.ptr(acc[2:]), C.c_void_p(_lib.stream_ptr(x.device)))
+    loss = acc[2]
+    return (loss if return_tensor else float(loss)), grad
+
+
+def loss_and_grad_torch(rendered: torch.Tensor, target: torch.Tensor, lam: float, return_tensor: bool = False):
+    """Separable-conv2d restatement of metrics.py:118-132 (independent check
+    of the fused kernel)."""
     x = rendered.float()
     y = torch.as_tensor(target, device=x.device).float()
     diff = x - y

@@ -36,6 +36,12 @@ def _run(values, mode):
     return (out_d if mode == 2 else out_f)[:g].reshape(lead)
 
 
+def backward_row_reduce(values, exp_aligned: bool = False):
+    """The raster backward's in-register row reductions (test hook): must
+    equal lane_group_reduce / exp_aligned_reduce bit for bit."""
+    return _run(torch.as_tensor(values), 4 if exp_aligned else 3)
+
+
 def lane_group_reduce(values, axis: int = -1, float64: bool = False):
     v = torch.as_tensor(values)
     v = torch.movedim(v, axis, -1)

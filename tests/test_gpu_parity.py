@@ -290,3 +290,38 @@ def test_big_configs_bit_exact_hashes(name):
         assert np.abs(col - np.array(gb["fwd_sample_color"])).max() <= 1e-3
         fr = out.frag_count.reshape(-1).cpu().numpy()[pix]
         assert (fr != np.array(gb["fwd_sample_frags"])).sum() <= 5
+
+
+def test_backward_row_reductions_bit_exact():
+    """The register row reductions the raster backward actually uses."""
+    from paper_2503_01199_b200.reduction import backward_row_reduce
+    d = G.load("golden_edge.npz")
+    v = torch.from_numpy(d["red_in"]).cuda()
+    assert np.array_equal(backward_row_reduce(v).cpu().numpy(), d["red_tree"])
+    assert np.array_equal(backward_row_reduce(v, exp_aligned=True).cpu().numpy(), d["red_exp"].astype(np.float32))
+
+
+@pytest.mark.parametrize("fname,prefix", [("golden_A.npz", ""), ("golden_edge.npz", "e1_")])
+def test_fused_loss_vs_reference(fname, prefix):
+    """metrics.py:118-132: the fused kernel against the reference's float64
+    loss / gradient (fixture) and the torch restatement."""
+    sb = _sb()
+    from paper_2503_01199_b200.metrics import loss_and_grad_torch
+    d = G.load(fname)
+    col = d[f"{prefix}fwd_color"]
+    rng = np.random.default_rng(int(d[f"{prefix}target_seed"]))
+    target = rng.uniform(0.0, 1.0, col.shape)
+    x = torch.from_numpy(col).cuda()
+    y = torch.from_numpy(target).cuda()
+    loss, g = sb.loss_and_grad(x, y, 0.2)
+    assert abs(loss - float(d[f"{prefix}loss"])) <= 1e-5 * abs(float(d[f"{prefix}loss"]))
+    ref = d[f"{prefix}dL_dI"].astype(np.float64)
+    assert np.abs(g.cpu().numpy() - ref).max() <= 1e-4 * np.abs(ref).max()
+    l2, g2 = loss_and_grad_torch(x, y, 0.2)
+    assert abs(loss - l2) <= 1e-5 * abs(l2)
+    # uint8 targets (value / 255)
+    t8 = (target * 255).round().astype(np.uint8)
+    l8, g8 = sb.loss_and_grad(x, torch.from_numpy(t8).cuda(), 0.2)
+    l8r, g8r = O.loss_and_grad(col, t8.astype(np.float64) / 255.0, 0.2)
+    assert abs(l8 - l8r) <= 1e-5 * abs(l8r)
+    assert np.abs(g8.cpu().numpy() - g8r).max() <= 1e-4 * np.abs(g8r).max()
