@@ -56,9 +56,10 @@ size_t sb_morton_keys_workspace_bytes(int64_t n);
 int sb_morton_keys(const float* params, int64_t n, uint64_t* keys, uint32_t* vals, double* lohi,
                    int32_t* bad_index, void* ws, size_t ws_bytes, sb_stream_t stream);
 
-/* ccc.py:88 np.argsort(kind="stable"): stable LSD radix sort of (key, value)
- * pairs over key bits [0, bits).  *result_in_alt (host int) is set to 1 when
- * the sorted data ended in keys_alt/vals_alt. */
+/* ccc.py:88 np.argsort(kind="stable"): stable onesweep LSD radix sort of
+ * (key, value) pairs over key bits [0, bits) (8-bit digits; one kernel per
+ * digit with decoupled look-back).  *result_in_alt (host int) is set to 1
+ * when the sorted data ended in keys_alt/vals_alt. */
 size_t sb_sort_workspace_bytes(int64_t n);
 int sb_radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
                             int bits, int* result_in_alt, void* ws, size_t ws_bytes, sb_stream_t stream);
@@ -70,30 +71,32 @@ int sb_permute_rows(const uint32_t* perm, int64_t n, int count, const void* cons
                     const int32_t* row_bytes, sb_stream_t stream);
 
 /* ---- forward: project + cull + compact + bin (forward.py:258-290) -------- */
-/* projection.py:130-190 + ccc.py:112-194 + tiles.py:50-91 (counting).
- * Outputs: recs[N] (first N_c used), compact_map[N] (int32, first N_c used),
- * cluster_offset[K] (compact start of each visible cluster, -1 if culled),
- * cluster_vis[K], tile_counts[tiles] (must be ZEROED by the caller),
+/* projection.py:130-190 + ccc.py:112-194 + tiles.py:70-91 (hit counting).
+ * Outputs: recs[N] (first N_c used; flags = valid | in_image << 1 |
+ * tile_hits << 2), compact_map[N] (int32, first N_c used), cluster_offset[K]
+ * (compact start of each visible cluster, -1 if culled), cluster_vis[K],
  * counters[4] (must be ZEROED): visible clusters, N_c, n_degenerate. */
 size_t sb_project_workspace_bytes(int64_t n);
 int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
                             void* recs, int32_t* compact_map, int32_t* cluster_offset, uint8_t* cluster_vis,
-                            int32_t* tile_counts, int32_t* counters, void* ws, size_t ws_bytes, sb_stream_t stream);
+                            int32_t* counters, void* ws, size_t ws_bytes, sb_stream_t stream);
 
-/* tiles.py:92-106: exclusive scan of tile_counts -> tile_offsets[ntiles + 1]
- * (tile_offsets[ntiles] = P, the number of (tile, primitive) pairs). */
-int sb_bin_offsets(const int32_t* tile_counts, int32_t ntiles, int32_t* tile_offsets, sb_stream_t stream);
+/* tiles.py:50-107 binning, part 1: stable depth order of the compact
+ * primitives (order[N_c]: compact slots) and the exclusive scan of their
+ * tile-hit counts in that order (pair_offsets[N_c]); *n_pairs (device int)
+ * receives P.  n_cap bounds N_c (read from counters[1] on the device). */
+size_t sb_bin_prepare_workspace_bytes(int64_t n_cap);
+int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, uint32_t* order,
+                   int32_t* pair_offsets, int32_t* n_pairs, void* ws, size_t ws_bytes, sb_stream_t stream);
 
-/* tiles.py:75-91: emit one 64-bit key (depth_bits << 32 | compact slot) per
- * (tile, primitive) hit into the tile's segment of pair_keys[P]. */
-size_t sb_bin_emit_workspace_bytes(int32_t ntiles);
-int sb_bin_emit(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam,
-                const int32_t* tile_offsets, uint64_t* pair_keys, void* ws, size_t ws_bytes, sb_stream_t stream);
-
-/* tiles.py:92-106 per-tile depth sort (depth asc, index tie-break):
- * tile_prims[P] = compact slots in per-tile order.  scratch: P u64. */
-int sb_tile_sort(const int32_t* tile_offsets, int32_t ntiles, uint64_t* pair_keys, uint64_t* scratch,
-                 int32_t* tile_prims, sb_stream_t stream);
+/* tiles.py:50-107 binning, part 2 (P from part 1): emit (tile id, slot)
+ * pairs in depth order, stable sort by tile id, per-tile ranges:
+ * tile_offsets[ntiles + 1], tile_prims[P] (compact slots, per tile in
+ * (depth, index) order == np.lexsort((prim, depth, tile_id))). */
+size_t sb_bin_finish_workspace_bytes(int64_t n_pairs, int32_t ntiles);
+int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, const uint32_t* order,
+                  const int32_t* pair_offsets, const sb_camera* cam, int64_t n_pairs, int32_t* tile_offsets,
+                  int32_t* tile_prims, void* ws, size_t ws_bytes, sb_stream_t stream);
 
 /* forward.py:161-191 + 240-255: color (H,W,3), transmittance (H,W),
  * frag_count (H,W) and last[(H,W)] = 1 + list position of each pixel's last

@@ -7,12 +7,15 @@
 
 // launchers (one per kernel family)
 void sb_launch_project_cull_compact(const float*, int, const CamDev&, int, RasterRec*, int32_t*, int32_t*, uint8_t*,
-                                    int32_t*, int32_t*, unsigned long long*, unsigned int*, cudaStream_t);
+                                    int32_t*, unsigned long long*, unsigned int*, cudaStream_t);
 int sb_project_blocks(int n);
-void sb_launch_tile_offsets(const int32_t*, int, int32_t*, cudaStream_t);
-void sb_launch_emit_pairs(const RasterRec*, const int32_t*, int, const int32_t*, int32_t*, unsigned long long*, int,
-                          int, int, int, cudaStream_t);
-void sb_launch_tile_sort(const int32_t*, int, unsigned long long*, unsigned long long*, int32_t*, cudaStream_t);
+size_t sb_bin_prepare_ws(int n_cap);
+void sb_launch_bin_prepare(const RasterRec*, const int32_t*, int, uint32_t*, int32_t*, int32_t*, void*, cudaStream_t);
+size_t sb_bin_finish_ws(long long n_pairs, int ntiles);
+void sb_launch_bin_finish(const RasterRec*, const int32_t*, int, const uint32_t*, const int32_t*, const CamDev&, int,
+                          int32_t*, int32_t*, void*, cudaStream_t);
+size_t sb_sort_u64_ws(int n, int bits);
+int sb_launch_sort_u64(unsigned long long*, uint32_t*, unsigned long long*, uint32_t*, int, int, void*, cudaStream_t);
 void sb_launch_raster_fwd(const RasterRec*, const int32_t*, const int32_t*, int, int, int, int, const sb_raster_cfg&,
                           int*, float*, float*, int32_t*, int32_t*, cudaStream_t);
 void sb_launch_raster_bwd(const RasterRec*, const int32_t*, const int32_t*, int, int, int, int, const sb_raster_cfg&,
@@ -28,10 +31,6 @@ void sb_launch_variance(const double*, const double*, const int32_t*, int, doubl
 void sb_launch_bounds(const float*, int, float*, double*, cudaStream_t);
 int sb_bounds_partial_floats();
 void sb_launch_morton_keys(const float*, int, const double*, unsigned long long*, uint32_t*, int*, cudaStream_t);
-int sb_scan_blocks(int n);
-int sb_radix_blocks(int n);
-int sb_launch_radix_sort(unsigned long long*, uint32_t*, unsigned long long*, uint32_t*, int, int, uint32_t*,
-                         uint32_t*, unsigned long long*, unsigned int*, cudaStream_t);
 void sb_launch_permute(const uint32_t*, int, int, const void* const*, void* const*, const int*, cudaStream_t);
 
 static thread_local std::string g_err;
@@ -102,30 +101,17 @@ int sb_morton_keys(const float* params, int64_t n, uint64_t* keys, uint32_t* val
     return check_launch("sb_morton_keys");
 }
 
-size_t sb_sort_workspace_bytes(int64_t n) {
-    const int nb = sb_radix_blocks((int)n);
-    const size_t ncount = 256 * (size_t)nb;
-    const int sb = sb_scan_blocks((int)ncount);
-    return 2 * align256(sizeof(uint32_t) * ncount) + align256(sizeof(unsigned long long) * sb + 16);
-}
+size_t sb_sort_workspace_bytes(int64_t n) { return sb_sort_u64_ws((int)n, 64) + 256; }
 
 int sb_radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
                             int bits, int* result_in_alt, void* ws, size_t ws_bytes, sb_stream_t stream) {
-    if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
+    if (n < 0 || n > INT32_MAX / 2) return fail(SB_EINVAL, "n out of range");
     if (bits < 0 || bits > 64) return fail(SB_EINVAL, "bits out of range");
     if (ws_bytes < sb_sort_workspace_bytes(n)) return fail(SB_EWORKSPACE, "sort workspace too small");
-    const int nb = sb_radix_blocks((int)n);
-    const size_t ncount = 256 * (size_t)nb;
-    char* w = static_cast<char*>(ws);
-    uint32_t* counts = reinterpret_cast<uint32_t*>(w);
-    w += align256(sizeof(uint32_t) * ncount);
-    uint32_t* scanned = reinterpret_cast<uint32_t*>(w);
-    w += align256(sizeof(uint32_t) * ncount);
-    unsigned long long* status = reinterpret_cast<unsigned long long*>(w);
-    unsigned int* ticket = reinterpret_cast<unsigned int*>(status + sb_scan_blocks((int)ncount));
-    const int flip = sb_launch_radix_sort(reinterpret_cast<unsigned long long*>(keys), vals,
-                                          reinterpret_cast<unsigned long long*>(keys_alt), vals_alt, (int)n, bits,
-                                          counts, scanned, status, ticket, S(stream));
+    int flip = 0;
+    if (n > 1 && bits > 0)
+        flip = sb_launch_sort_u64(reinterpret_cast<unsigned long long*>(keys), vals,
+                                  reinterpret_cast<unsigned long long*>(keys_alt), vals_alt, (int)n, bits, ws, S(stream));
     if (result_in_alt) *result_in_alt = flip;
     return check_launch("sb_radix_sort_pairs_u64");
 }
@@ -146,7 +132,7 @@ size_t sb_project_workspace_bytes(int64_t n) {
 
 int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
                             void* recs, int32_t* compact_map, int32_t* cluster_offset, uint8_t* cluster_vis,
-                            int32_t* tile_counts, int32_t* counters, void* ws, size_t ws_bytes, sb_stream_t stream) {
+                            int32_t* counters, void* ws, size_t ws_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
     if (n < 0 || n > INT32_MAX - 256) return fail(SB_EINVAL, "n out of range");
@@ -158,36 +144,36 @@ int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam
     cudaMemsetAsync(ws, 0, sizeof(unsigned long long) * blocks + 16, S(stream));
     const CamDev d = make_cam(cam, cfg);
     sb_launch_project_cull_compact(params, (int)n, d, cfg->use_culling, static_cast<RasterRec*>(recs), compact_map,
-                                   cluster_offset, cluster_vis, tile_counts, counters, status, ticket, S(stream));
+                                   cluster_offset, cluster_vis, counters, status, ticket, S(stream));
     return check_launch("sb_project_cull_compact");
 }
 
-int sb_bin_offsets(const int32_t* tile_counts, int32_t ntiles, int32_t* tile_offsets, sb_stream_t stream) {
-    if (ntiles <= 0) return fail(SB_EINVAL, "ntiles must be positive");
-    sb_launch_tile_offsets(tile_counts, ntiles, tile_offsets, S(stream));
-    return check_launch("sb_bin_offsets");
+size_t sb_bin_prepare_workspace_bytes(int64_t n_cap) { return sb_bin_prepare_ws((int)n_cap) + 256; }
+
+int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, uint32_t* order,
+                   int32_t* pair_offsets, int32_t* n_pairs, void* ws, size_t ws_bytes, sb_stream_t stream) {
+    if (n_cap < 0 || n_cap > INT32_MAX / 2) return fail(SB_EINVAL, "n_cap out of range");
+    if (ws_bytes < sb_bin_prepare_workspace_bytes(n_cap)) return fail(SB_EWORKSPACE, "bin prepare workspace too small");
+    sb_launch_bin_prepare(static_cast<const RasterRec*>(recs), counters, (int)n_cap, order, pair_offsets, n_pairs, ws,
+                          S(stream));
+    return check_launch("sb_bin_prepare");
 }
 
-size_t sb_bin_emit_workspace_bytes(int32_t ntiles) { return align256(sizeof(int32_t) * (size_t)ntiles); }
+size_t sb_bin_finish_workspace_bytes(int64_t n_pairs, int32_t ntiles) {
+    return sb_bin_finish_ws((long long)n_pairs, ntiles) + 256;
+}
 
-int sb_bin_emit(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam,
-                const int32_t* tile_offsets, uint64_t* pair_keys, void* ws, size_t ws_bytes, sb_stream_t stream) {
+int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, const uint32_t* order,
+                  const int32_t* pair_offsets, const sb_camera* cam, int64_t n_pairs, int32_t* tile_offsets,
+                  int32_t* tile_prims, void* ws, size_t ws_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
+    if (n_pairs < 0 || n_pairs > INT32_MAX / 2) return fail(SB_EINVAL, "n_pairs out of range");
     const CamDev d = make_cam(cam, nullptr);
-    const int ntiles = d.tiles_x * d.tiles_y;
-    if (ws_bytes < sb_bin_emit_workspace_bytes(ntiles)) return fail(SB_EWORKSPACE, "emit workspace too small");
-    cudaMemsetAsync(ws, 0, sizeof(int32_t) * ntiles, S(stream));
-    sb_launch_emit_pairs(static_cast<const RasterRec*>(recs), counters, (int)n_cap, tile_offsets,
-                         static_cast<int32_t*>(ws), reinterpret_cast<unsigned long long*>(pair_keys), d.tiles_x,
-                         d.tiles_y, d.W, d.H, S(stream));
-    return check_launch("sb_bin_emit");
-}
-
-int sb_tile_sort(const int32_t* tile_offsets, int32_t ntiles, uint64_t* pair_keys, uint64_t* scratch,
-                 int32_t* tile_prims, sb_stream_t stream) {
-    sb_launch_tile_sort(tile_offsets, ntiles, reinterpret_cast<unsigned long long*>(pair_keys),
-                        reinterpret_cast<unsigned long long*>(scratch), tile_prims, S(stream));
-    return check_launch("sb_tile_sort");
+    if (ws_bytes < sb_bin_finish_workspace_bytes(n_pairs, d.tiles_x * d.tiles_y))
+        return fail(SB_EWORKSPACE, "bin finish workspace too small");
+    sb_launch_bin_finish(static_cast<const RasterRec*>(recs), counters, (int)n_cap, order, pair_offsets, d,
+                         (int)n_pairs, tile_offsets, tile_prims, ws, S(stream));
+    return check_launch("sb_bin_finish");
 }
 
 size_t sb_raster_workspace_bytes(void) { return 256; }

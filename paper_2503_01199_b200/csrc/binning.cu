@@ -1,175 +1,208 @@
-// K6/K7: tile binning and the per-tile depth sort (tiles.py:50-107).
+// K6/K7: tile binning with the per-tile depth order (tiles.py:50-107).
 //
-//   offsets : exclusive scan of the per-tile hit counts from K5
-//   emit    : one thread per compact primitive re-runs the exact disc test and
-//             appends 64-bit keys (depth_bits << 32 | compact_slot) into its
-//             tiles' segments (atomic cursor per tile)
-//   sort    : one CTA per tile sorts its segment in shared memory (bitonic on
-//             unique 64-bit keys => depth ascending, slot tie-break, exactly
-//             np.lexsort((prim, depth, tile_id))).  Depth > near > 0, so the
-//             float32 bit pattern is order preserving as uint32.  Segments
-//             larger than the shared-memory capacity are sorted in chunks and
-//             merged in global memory by the same CTA.
-#include "common.cuh"
+// The reference builds (tile, depth, index) triples and lexsorts them.  Here:
+//   prepare  (1) sort the compact primitives by depth (32-bit float bits are
+//                order preserving for depth > near > 0) with the stable
+//                onesweep radix sort, values = compact slots in index order, so
+//                equal depths keep index order;
+//            (2) exclusive scan of the per-primitive tile-hit counts (from
+//                the fused projection kernel) in that depth order -> each
+//                primitive's output range and the pair count P;
+//   finish   (3) emit, in depth order, one (tile id, slot) pair per exact
+//                disc/rect hit (coalesced writes, no atomics);
+//            (4) stable onesweep sort of the pairs by tile id (2 passes at
+//                1080p): within a tile the depth order -- and the index
+//                tie-break -- of step (1) survive, which is exactly
+//                np.lexsort((prim, depth, tile_id));
+//            (5) per-tile [start, end) by binary search of the sorted ids.
+#include "onesweep.cuh"
 
 namespace {
 
-constexpr int kScanThreads = 1024;
-
-__global__ void __launch_bounds__(kScanThreads)
-tile_offsets_kernel(const int32_t* __restrict__ counts, int ntiles, int32_t* __restrict__ offsets)
-{
-    __shared__ int32_t warp_sums[32];
-    const int tid = threadIdx.x;
-    const int per = (ntiles + kScanThreads - 1) / kScanThreads;
-    const int s = tid * per, e = min(s + per, ntiles);
-    int32_t local = 0;
-    for (int i = s; i < e; i++) local += counts[i];
-    // block exclusive scan of the per-thread sums
-    int32_t v = local;
-    const int lane = tid & 31, warp = tid >> 5;
-    for (int o = 1; o < 32; o <<= 1) {
-        int32_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-    }
-    if (lane == 31) warp_sums[warp] = v;
-    __syncthreads();
-    if (warp == 0) {
-        int32_t w = warp_sums[lane];
-        for (int o = 1; o < 32; o <<= 1) {
-            int32_t u = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += u;
-        }
-        warp_sums[lane] = w;
-    }
-    __syncthreads();
-    int32_t run = v - local + (warp > 0 ? warp_sums[warp - 1] : 0);
-    for (int i = s; i < e; i++) {
-        offsets[i] = run;
-        run += counts[i];
-    }
-    if (tid == kScanThreads - 1) offsets[ntiles] = run;
-}
-
 __global__ void __launch_bounds__(256)
-emit_pairs_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ counters, int n_cap,
-                  const int32_t* __restrict__ offsets, int32_t* __restrict__ cursor,
-                  unsigned long long* __restrict__ keys, int tiles_x, int tiles_y, int W, int H)
+depth_keys_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ counters, int n_cap,
+                  uint32_t* __restrict__ keys)
 {
     const int nc = min(counters[1], n_cap);
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nc) return;
+    const float4 c = __ldg(reinterpret_cast<const float4*>(recs + s) + 2);
+    const uint32_t flags = __float_as_uint(c.w);
+    // primitives without hits sort last (their position is irrelevant)
+    keys[s] = (flags & 2u) ? __float_as_uint(c.y) : 0xffffffffu;
+}
+
+// single-pass exclusive scan of nhit[order[i]] with decoupled look-back
+constexpr int kScanT = 256, kScanItems = 8, kScanTile = kScanT * kScanItems;
+
+__global__ void __launch_bounds__(kScanT)
+hit_scan_kernel(const RasterRec* __restrict__ recs, const uint32_t* __restrict__ order,
+                const int32_t* __restrict__ counters, int n_cap, int32_t* __restrict__ offsets,
+                int32_t* __restrict__ total, unsigned long long* __restrict__ status, unsigned* __restrict__ ticket)
+{
+    __shared__ int s_bid;
+    __shared__ uint32_t s_warp[kScanT / 32];
+    __shared__ uint32_t s_prefix;
+    if (threadIdx.x == 0) s_bid = (int)atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int bid = s_bid;
+    const int nc = min(counters[1], n_cap);
+    const int base = bid * kScanTile + threadIdx.x * kScanItems;
+    uint32_t v[kScanItems], sum = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        v[j] = 0;
+        if (base + j < nc) {
+            const uint32_t slot = order[base + j];
+            const uint32_t flags = __float_as_uint(__ldg(reinterpret_cast<const float*>(recs + slot) + 11));
+            v[j] = flags >> 2;
+        }
+        sum += v[j];
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int w = 0; w < kScanT / 32; w++) { const uint32_t t = s_warp[w]; s_warp[w] = run; run += t; }
+        s_prefix = sb_lookback_exclusive(status, bid, run);
+        if (bid == (int)gridDim.x - 1) *total = (int32_t)(s_prefix + run);
+    }
+    __syncthreads();
+    uint32_t run = s_prefix + s_warp[warp] + x - sum;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        if (base + j < nc) offsets[base + j] = (int32_t)run;
+        run += v[j];
+    }
+}
+
+__global__ void __launch_bounds__(256)
+emit_kernel(const RasterRec* __restrict__ recs, const uint32_t* __restrict__ order,
+            const int32_t* __restrict__ offsets, const int32_t* __restrict__ counters, int n_cap,
+            uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ slots, int tiles_x, int tiles_y, int W, int H)
+{
+    const int nc = min(counters[1], n_cap);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nc) return;
+    const uint32_t s = order[i];
     const float4* r4 = reinterpret_cast<const float4*>(recs + s);
     const float4 a = __ldg(r4);
     const float4 c = __ldg(r4 + 2);
     const uint32_t flags = __float_as_uint(c.w);
-    if (!(flags & 2u)) return;
-    const float x = a.x, y = a.y, depth = c.y, r = c.z;
-    const unsigned long long hi = (unsigned long long)__float_as_uint(depth) << 32;
+    if ((flags >> 2) == 0) return;
+    const float x = a.x, y = a.y, r = c.z;
     int tx0, tx1, ty0, ty1;
     sb_tile_range(x, y, r, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+    int pos = offsets[i];
     for (int ty = ty0; ty <= ty1; ty++)
         for (int tx = tx0; tx <= tx1; tx++)
             if (sb_disc_hits(x, y, r, tx, ty, W, H)) {
-                const int t = ty * tiles_x + tx;
-                const int pos = atomicAdd(&cursor[t], 1);
-                keys[(size_t)offsets[t] + pos] = hi | (unsigned)s;
+                tile_keys[pos] = (uint32_t)(ty * tiles_x + tx);
+                slots[pos] = s;
+                pos++;
             }
 }
 
-constexpr int kSortThreads = 256;
-constexpr int kSortCap = 4096;   // keys sorted in shared memory (32 KB)
-
-SB_INLINE void bitonic_smem(unsigned long long* s, int L) {
-    for (int k = 2; k <= L; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < L; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const unsigned long long x = s[i], y = s[ixj];
-                    const bool up = (i & k) == 0;
-                    if ((x > y) == up) {
-                        s[i] = y;
-                        s[ixj] = x;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kSortThreads)
-tile_sort_kernel(const int32_t* __restrict__ offsets, unsigned long long* __restrict__ keys,
-                 unsigned long long* __restrict__ scratch, int32_t* __restrict__ prims)
+__global__ void __launch_bounds__(256)
+tile_ranges_kernel(const uint32_t* __restrict__ sorted_tiles, int P, int ntiles, int32_t* __restrict__ offsets)
 {
-    __shared__ unsigned long long s[kSortCap];
-    const int t = blockIdx.x;
-    const int beg = offsets[t], n = offsets[t + 1] - beg;
-    if (n == 0) return;
-    if (n == 1) {
-        if (threadIdx.x == 0) prims[beg] = (int32_t)(keys[beg] & 0xffffffffu);
-        return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > ntiles) return;
+    int lo = 0, hi = P;
+    while (lo < hi) {   // first index with key >= t
+        const int mid = (lo + hi) >> 1;
+        if (sorted_tiles[mid] < (uint32_t)t) lo = mid + 1; else hi = mid;
     }
-    unsigned long long* seg = keys + beg;
-    if (n <= kSortCap) {
-        int L = 2;
-        while (L < n) L <<= 1;
-        for (int i = threadIdx.x; i < L; i += blockDim.x) s[i] = i < n ? seg[i] : ~0ull;
-        __syncthreads();
-        bitonic_smem(s, L);
-        for (int i = threadIdx.x; i < n; i += blockDim.x) prims[beg + i] = (int32_t)(s[i] & 0xffffffffu);
-        return;
-    }
-    // large segment: sorted runs of kSortCap, then pairwise merges by rank
-    for (int c0 = 0; c0 < n; c0 += kSortCap) {
-        const int m = min(kSortCap, n - c0);
-        for (int i = threadIdx.x; i < kSortCap; i += blockDim.x) s[i] = i < m ? seg[c0 + i] : ~0ull;
-        __syncthreads();
-        bitonic_smem(s, kSortCap);
-        for (int i = threadIdx.x; i < m; i += blockDim.x) seg[c0 + i] = s[i];
-        __syncthreads();
-    }
-    unsigned long long* src = seg;
-    unsigned long long* dst = scratch + beg;
-    for (int w = kSortCap; w < n; w <<= 1) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const int run = i / (2 * w), a0 = run * 2 * w;
-            const int b0 = min(a0 + w, n), b1 = min(a0 + 2 * w, n);
-            const unsigned long long x = src[i];
-            int lo, hi;
-            if (i < b0) { lo = b0; hi = b1; } else { lo = a0; hi = b0; }
-            const int base = lo;
-            while (lo < hi) {  // count of keys < x in the partner run (keys are unique)
-                const int mid = (lo + hi) >> 1;
-                if (src[mid] < x) lo = mid + 1; else hi = mid;
-            }
-            const int rank_other = lo - base;
-            const int own = i < b0 ? i - a0 : i - b0;
-            dst[a0 + own + rank_other] = x;
-        }
-        __syncthreads();
-        unsigned long long* tmp = src; src = dst; dst = tmp;
-    }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) prims[beg + i] = (int32_t)(src[i] & 0xffffffffu);
+    offsets[t] = lo;
 }
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
-void sb_launch_tile_offsets(const int32_t* counts, int ntiles, int32_t* offsets, cudaStream_t stream) {
-    tile_offsets_kernel<<<1, kScanThreads, 0, stream>>>(counts, ntiles, offsets);
+// ---- prepare: depth order + hit-count scan ---------------------------------
+size_t sb_bin_prepare_ws(int n_cap) {
+    const size_t n = (size_t)n_cap;
+    return 3 * align256(n * 4) + align256(onesweep::workspace_bytes(n_cap, 4)) +
+           align256(sizeof(unsigned long long) * ((n + kScanTile - 1) / kScanTile) + 16);
 }
 
-void sb_launch_emit_pairs(const RasterRec* recs, const int32_t* counters, int n_cap, const int32_t* offsets,
-                          int32_t* cursor, unsigned long long* keys, int tiles_x, int tiles_y, int W, int H,
-                          cudaStream_t stream) {
-    if (n_cap <= 0) return;
-    emit_pairs_kernel<<<(n_cap + 255) / 256, 256, 0, stream>>>(recs, counters, n_cap, offsets, cursor, keys,
-                                                               tiles_x, tiles_y, W, H);
+void sb_launch_bin_prepare(const RasterRec* recs, const int32_t* counters, int n_cap, uint32_t* order,
+                           int32_t* pair_offsets, int32_t* n_pairs, void* ws, cudaStream_t stream)
+{
+    if (n_cap <= 0) {
+        cudaMemsetAsync(n_pairs, 0, sizeof(int32_t), stream);
+        return;
+    }
+    char* w = static_cast<char*>(ws);
+    const size_t n = (size_t)n_cap;
+    uint32_t* keys = reinterpret_cast<uint32_t*>(w); w += align256(n * 4);
+    uint32_t* keys_alt = reinterpret_cast<uint32_t*>(w); w += align256(n * 4);
+    uint32_t* vals_alt = reinterpret_cast<uint32_t*>(w); w += align256(n * 4);
+    void* sort_ws = w; w += align256(onesweep::workspace_bytes(n_cap, 4));
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(w);
+    const int scan_blocks = (n_cap + kScanTile - 1) / kScanTile;
+    unsigned* ticket = reinterpret_cast<unsigned*>(status + scan_blocks);
+
+    depth_keys_kernel<<<(n_cap + 255) / 256, 256, 0, stream>>>(recs, counters, n_cap, keys);
+    // 4 passes (even): the sorted slots end in `order`
+    onesweep::sort<uint32_t>(keys, order, keys_alt, vals_alt, counters + 1, n_cap, 4, false, true, sort_ws, stream);
+    cudaMemsetAsync(status, 0, sizeof(unsigned long long) * scan_blocks + 16, stream);
+    hit_scan_kernel<<<scan_blocks, kScanT, 0, stream>>>(recs, order, counters, n_cap, pair_offsets, n_pairs, status,
+                                                        ticket);
 }
 
-void sb_launch_tile_sort(const int32_t* offsets, int ntiles, unsigned long long* keys,
-                         unsigned long long* scratch, int32_t* prims, cudaStream_t stream) {
-    if (ntiles <= 0) return;
-    tile_sort_kernel<<<ntiles, kSortThreads, 0, stream>>>(offsets, keys, scratch, prims);
+// ---- finish: emit + tile sort + ranges -------------------------------------
+static int tile_passes(int ntiles) {
+    int bits = 1;
+    while ((1 << bits) < ntiles) bits++;
+    return (bits + 7) / 8;
+}
+
+size_t sb_bin_finish_ws(long long n_pairs, int ntiles) {
+    const size_t P = (size_t)(n_pairs > 0 ? n_pairs : 1);
+    return 3 * align256(P * 4) + align256(onesweep::workspace_bytes((int)P, tile_passes(ntiles)));
+}
+
+void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_cap, const uint32_t* order,
+                          const int32_t* pair_offsets, const CamDev& cam, int P, int32_t* tile_offsets,
+                          int32_t* tile_prims, void* ws, cudaStream_t stream)
+{
+    const int ntiles = cam.tiles_x * cam.tiles_y;
+    if (P <= 0) {
+        cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (ntiles + 1), stream);
+        return;
+    }
+    char* w = static_cast<char*>(ws);
+    const size_t Ps = (size_t)P;
+    uint32_t* tkeys = reinterpret_cast<uint32_t*>(w); w += align256(Ps * 4);
+    uint32_t* tkeys_alt = reinterpret_cast<uint32_t*>(w); w += align256(Ps * 4);
+    uint32_t* slots_alt = reinterpret_cast<uint32_t*>(w); w += align256(Ps * 4);
+    void* sort_ws = w;
+    const int passes = tile_passes(ntiles);
+    // emit into the buffers the sort ends in when the pass count is even
+    uint32_t* vals = passes % 2 == 0 ? reinterpret_cast<uint32_t*>(tile_prims) : slots_alt;
+    uint32_t* valt = passes % 2 == 0 ? slots_alt : reinterpret_cast<uint32_t*>(tile_prims);
+    emit_kernel<<<(n_cap + 255) / 256, 256, 0, stream>>>(recs, order, pair_offsets, counters, n_cap, tkeys, vals,
+                                                         cam.tiles_x, cam.tiles_y, cam.W, cam.H);
+    const int flip = onesweep::sort<uint32_t>(tkeys, vals, tkeys_alt, valt, nullptr, P, passes, true, false, sort_ws,
+                                              stream);
+    const uint32_t* sorted = flip ? tkeys_alt : tkeys;
+    tile_ranges_kernel<<<(ntiles + 1 + 255) / 256, 256, 0, stream>>>(sorted, P, ntiles, tile_offsets);
+}
+
+// ---- Morton sort (u64 keys) --------------------------------------------------
+size_t sb_sort_u64_ws(int n, int bits) { return onesweep::workspace_bytes(n, (bits + 7) / 8); }
+
+int sb_launch_sort_u64(unsigned long long* keys, uint32_t* vals, unsigned long long* keys_alt, uint32_t* vals_alt,
+                       int n, int bits, void* ws, cudaStream_t stream)
+{
+    return onesweep::sort<unsigned long long>(keys, vals, keys_alt, vals_alt, nullptr, n, (bits + 7) / 8, true, false,
+                                              ws, stream);
 }

@@ -1,6 +1,5 @@
-// K1 scene bounds, K2 Morton keys, K3 stable LSD radix sort of (u64 key,
-// u32 value) pairs, K4 multi-array row permute, plus a single-pass
-// decoupled-look-back exclusive scan.
+// K1 scene bounds, K2 Morton keys, K4 multi-array row permute.  (K3, the
+// stable radix sort of the keys, is the onesweep sort in onesweep.cuh.)
 //
 // Replaces (pkg/src/tinysplat):
 //   scene.py:256-260   SceneSoA.bounds
@@ -102,124 +101,6 @@ morton_keys_kernel(const float4* __restrict__ params, int n, const double* __res
     vals[g] = (uint32_t)g;
 }
 
-// ---- single-pass exclusive scan (uint32) ------------------------------------
-constexpr int kScanT = 256, kScanItems = 16, kScanTile = kScanT * kScanItems;
-
-__global__ void __launch_bounds__(kScanT)
-scan_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int n,
-            unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket)
-{
-    __shared__ int s_bid;
-    __shared__ uint32_t s_warp[kScanT / 32];
-    __shared__ uint32_t s_prefix;
-    if (threadIdx.x == 0) s_bid = (int)atomicAdd(ticket, 1u);
-    __syncthreads();
-    const int bid = s_bid;
-    const int base = bid * kScanTile + threadIdx.x * kScanItems;
-    uint32_t v[kScanItems], sum = 0;
-#pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
-        v[j] = base + j < n ? in[base + j] : 0u;
-        sum += v[j];
-    }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = sum;
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_warp[warp] = x;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (int w = 0; w < kScanT / 32; w++) { const uint32_t t = s_warp[w]; s_warp[w] = run; run += t; }
-        s_prefix = sb_lookback_exclusive(status, bid, run);
-    }
-    __syncthreads();
-    uint32_t run = s_prefix + s_warp[warp] + x - sum;
-#pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
-        if (base + j < n) out[base + j] = run;
-        run += v[j];
-    }
-}
-
-// ---- K3 stable LSD radix sort, 8-bit digits -------------------------------
-constexpr int kSortT = 256, kSortItems = 16, kSortTile = kSortT * kSortItems;
-constexpr int kSortWarps = kSortT / 32, kWarpKeys = kSortTile / kSortWarps;   // 512
-
-__global__ void __launch_bounds__(kSortT)
-radix_upsweep_kernel(const unsigned long long* __restrict__ keys, int n, int shift, int nblocks,
-                     uint32_t* __restrict__ counts)
-{
-    __shared__ uint32_t hist[256];
-    hist[threadIdx.x] = 0;
-    __syncthreads();
-    const int base = blockIdx.x * kSortTile;
-#pragma unroll 4
-    for (int j = 0; j < kSortItems; j++) {
-        const int i = base + j * kSortT + threadIdx.x;
-        if (i < n) atomicAdd(&hist[(keys[i] >> shift) & 0xff], 1u);
-    }
-    __syncthreads();
-    counts[threadIdx.x * nblocks + blockIdx.x] = hist[threadIdx.x];
-}
-
-__global__ void __launch_bounds__(kSortT)
-radix_downsweep_kernel(const unsigned long long* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-                       unsigned long long* __restrict__ keys_out, uint32_t* __restrict__ vals_out, int n,
-                       int shift, int nblocks, const uint32_t* __restrict__ offsets)
-{
-    __shared__ uint32_t wcount[kSortWarps][256];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int d = lane; d < 256; d += 32) wcount[warp][d] = 0;
-    __syncwarp();
-    const int wbase = blockIdx.x * kSortTile + warp * kWarpKeys;
-    unsigned long long k[kSortItems];
-    uint32_t v[kSortItems], rank[kSortItems];
-    int dig[kSortItems];
-    const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int j = 0; j < kSortItems; j++) {
-        const int i = wbase + j * 32 + lane;
-        const bool ok = i < n;
-        const unsigned active = __ballot_sync(0xffffffffu, ok);
-        dig[j] = -1;
-        rank[j] = 0;
-        if (ok) {
-            k[j] = keys_in[i];
-            v[j] = vals_in[i];
-            const int d = (int)((k[j] >> shift) & 0xff);
-            dig[j] = d;
-            const unsigned peers = __match_any_sync(active, d);
-            const uint32_t pre = wcount[warp][d];
-            rank[j] = pre + __popc(peers & lt);
-            __syncwarp(active);
-            if ((peers & lt) == 0) wcount[warp][d] = pre + __popc(peers);
-        }
-        __syncwarp();
-    }
-    __syncthreads();
-    // per digit: exclusive prefix over warps, plus the global offset
-    {
-        const int d = threadIdx.x;
-        uint32_t run = offsets[d * nblocks + blockIdx.x];
-        for (int w = 0; w < kSortWarps; w++) {
-            const uint32_t c = wcount[w][d];
-            wcount[w][d] = run;
-            run += c;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kSortItems; j++) {
-        if (dig[j] < 0) continue;
-        const uint32_t pos = wcount[warp][dig[j]] + rank[j];
-        keys_out[pos] = k[j];
-        vals_out[pos] = v[j];
-    }
-}
-
 // ---- K4 multi-array row permute (gather) -------------------------------------
 struct PermArrays {
     const char* src[16];
@@ -263,44 +144,6 @@ void sb_launch_morton_keys(const float* params, int n, const double* lohi, unsig
     if (n <= 0) return;
     morton_keys_kernel<<<(n + 255) / 256, 256, 0, stream>>>(reinterpret_cast<const float4*>(params), n, lohi, keys,
                                                             vals, bad);
-}
-
-int sb_scan_blocks(int n) { return (n + kScanTile - 1) / kScanTile; }
-
-// status: sb_scan_blocks(n) u64 + ticket, zeroed by the caller
-void sb_launch_scan(const uint32_t* in, uint32_t* out, int n, unsigned long long* status, unsigned int* ticket,
-                    cudaStream_t stream) {
-    const int b = sb_scan_blocks(n);
-    if (b) scan_kernel<<<b, kScanT, 0, stream>>>(in, out, n, status, ticket);
-}
-
-int sb_radix_blocks(int n) { return (n + kSortTile - 1) / kSortTile; }
-
-// Sorts (keys, vals) by the bit range [0, bits) with ceil(bits / 8) passes,
-// ping-ponging between (keys, vals) and (keys_alt, vals_alt).  Returns 1 when
-// the sorted data ended in the *_alt buffers.  Workspace: counts
-// (256 * blocks u32), scanned (same), scan status (scan blocks u64 + 1 u32),
-// all carved by the caller; the scan status is re-zeroed every pass.
-int sb_launch_radix_sort(unsigned long long* keys, uint32_t* vals, unsigned long long* keys_alt, uint32_t* vals_alt,
-                         int n, int bits, uint32_t* counts, uint32_t* scanned, unsigned long long* scan_status,
-                         unsigned int* scan_ticket, cudaStream_t stream) {
-    if (n <= 1) return 0;
-    const int nb = sb_radix_blocks(n);
-    const int ncount = 256 * nb;
-    const int sb = sb_scan_blocks(ncount);
-    int flip = 0;
-    for (int shift = 0; shift < bits; shift += 8) {
-        unsigned long long* ki = flip ? keys_alt : keys;
-        uint32_t* vi = flip ? vals_alt : vals;
-        unsigned long long* ko = flip ? keys : keys_alt;
-        uint32_t* vo = flip ? vals : vals_alt;
-        radix_upsweep_kernel<<<nb, kSortT, 0, stream>>>(ki, n, shift, nb, counts);
-        cudaMemsetAsync(scan_status, 0, sizeof(unsigned long long) * sb + sizeof(unsigned int) * 4, stream);
-        sb_launch_scan(counts, scanned, ncount, scan_status, scan_ticket, stream);
-        radix_downsweep_kernel<<<nb, kSortT, 0, stream>>>(ki, vi, ko, vo, n, shift, nb, scanned);
-        flip ^= 1;
-    }
-    return flip;
 }
 
 void sb_launch_permute(const uint32_t* perm, int n, int count, const void* const* src, void* const* dst,

@@ -1,0 +1,230 @@
+// Stable LSD radix sort, "onesweep" style: one global histogram kernel for
+// all digit passes, then ONE kernel per 8-bit digit pass that ranks a
+// 4096-key tile locally (per-warp match_any ranking, stable), publishes its
+// per-digit counts, obtains its global per-digit prefix by decoupled
+// look-back over the preceding tiles, and scatters through shared memory so
+// the global writes are digit-contiguous runs.
+//
+// Used for np.argsort(kind="stable") (ccc.py:88, 63-bit Morton keys) and for
+// the binning sorts (tiles.py:98: depth, then tile id).
+#pragma once
+#include "common.cuh"
+
+namespace onesweep {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kItems = 16;
+constexpr int kTile = kThreads * kItems;        // 4096 keys per CTA
+constexpr int kWarpKeys = kTile / kWarps;       // 512
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
+
+template <typename K>
+struct Smem {
+    K keys[kTile];
+    uint32_t vals[kTile];
+    uint32_t wcount[kWarps][256];
+    uint32_t block_off[256];
+    uint32_t global_off[256];
+    int bid;
+    int n;
+};
+
+__host__ __device__ __forceinline__ int tile_count(int n) { return (n + kTile - 1) / kTile; }
+
+// hist[p][d] += #keys with digit d in pass p, for p < passes.
+template <typename K>
+__global__ void __launch_bounds__(kThreads)
+hist_kernel(const K* __restrict__ keys, const int* __restrict__ n_dev, int n_cap, int passes,
+            uint32_t* __restrict__ hist)
+{
+    __shared__ uint32_t h[8][256];
+    for (int i = threadIdx.x; i < 8 * 256; i += kThreads) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const int n = n_dev ? min(*n_dev, n_cap) : n_cap;
+    const unsigned lane_lt = (1u << (threadIdx.x & 31)) - 1u;
+    for (int base = blockIdx.x * kThreads; base < n; base += gridDim.x * kThreads) {
+        const int i = base + threadIdx.x;
+        const bool ok = i < n;
+        const unsigned act = __ballot_sync(0xffffffffu, ok);
+        if (!ok) continue;
+        const K k = keys[i];
+        for (int p = 0; p < passes; p++) {
+            const int d = (int)((k >> (8 * p)) & 0xff);
+            const unsigned peers = __match_any_sync(act, d);
+            if ((peers & lane_lt) == 0) atomicAdd(&h[p][d], (uint32_t)__popc(peers));
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * 256; i += kThreads) {
+        const uint32_t c = (&h[0][0])[i];
+        if (c) atomicAdd(&hist[i], c);
+    }
+}
+
+// in place: hist[p][*] -> exclusive prefix over digits
+__global__ void __launch_bounds__(256) scan_hist_kernel(uint32_t* hist, int passes)
+{
+    __shared__ uint32_t s[256];
+    for (int p = 0; p < passes; p++) {
+        const uint32_t v = hist[p * 256 + threadIdx.x];
+        s[threadIdx.x] = v;
+        __syncthreads();
+        for (int o = 1; o < 256; o <<= 1) {
+            const uint32_t t = threadIdx.x >= o ? s[threadIdx.x - o] : 0u;
+            __syncthreads();
+            s[threadIdx.x] += t;
+            __syncthreads();
+        }
+        hist[p * 256 + threadIdx.x] = s[threadIdx.x] - v;
+        __syncthreads();
+    }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kThreads)
+pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
+            uint32_t* __restrict__ vout, const int* __restrict__ n_dev, int n_cap, int shift,
+            const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status, unsigned* __restrict__ ticket)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<K>& sm = *reinterpret_cast<Smem<K>*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        sm.bid = (int)atomicAdd(ticket, 1u);
+        sm.n = n_dev ? min(*n_dev, n_cap) : n_cap;
+    }
+    for (int d = lane; d < 256; d += 32) sm.wcount[warp][d] = 0;
+    __syncthreads();
+    const int bid = sm.bid, n = sm.n;
+    const int tile_base = bid * kTile;
+    const int wbase = tile_base + warp * kWarpKeys;
+    K k[kItems];
+    uint32_t v[kItems], rank[kItems];
+    int dig[kItems];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < kItems; j++) {
+        const int i = wbase + j * 32 + lane;
+        const bool ok = i < n;
+        const unsigned active = __ballot_sync(0xffffffffu, ok);
+        dig[j] = -1;
+        rank[j] = 0;
+        if (ok) {
+            k[j] = kin[i];
+            v[j] = vin ? vin[i] : (uint32_t)i;
+            const int d = (int)((k[j] >> shift) & 0xff);
+            dig[j] = d;
+            const unsigned peers = __match_any_sync(active, d);
+            const uint32_t pre = sm.wcount[warp][d];
+            rank[j] = pre + __popc(peers & lt);
+            __syncwarp(active);
+            if ((peers & lt) == 0) sm.wcount[warp][d] = pre + __popc(peers);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: prefix over warps, tile count, publish the aggregate
+    const int d = threadIdx.x;
+    uint32_t cnt = 0;
+    for (int w = 0; w < kWarps; w++) {
+        const uint32_t c = sm.wcount[w][d];
+        sm.wcount[w][d] = cnt;
+        cnt += c;
+    }
+    volatile uint32_t* st = status;
+    st[(size_t)bid * 256 + d] = (bid == 0 ? kFlagInc : kFlagAgg) | cnt;
+    // exclusive scan of the tile counts over digits -> local digit offsets
+    sm.block_off[d] = cnt;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {
+        const uint32_t t = d >= o ? sm.block_off[d - o] : 0u;
+        __syncthreads();
+        sm.block_off[d] += t;
+        __syncthreads();
+    }
+    const uint32_t local_off = sm.block_off[d] - cnt;
+    // decoupled look-back for this digit
+    uint32_t prefix = 0;
+    if (bid > 0) {
+        int j = bid - 1;
+        while (true) {
+            uint32_t s;
+            do {
+                s = st[(size_t)j * 256 + d];
+            } while ((s & (kFlagAgg | kFlagInc)) == 0);
+            prefix += s & kValMask;
+            if (s & kFlagInc) break;
+            j--;
+        }
+        st[(size_t)bid * 256 + d] = kFlagInc | (prefix + cnt);
+    }
+    __syncthreads();
+    sm.block_off[d] = local_off;
+    sm.global_off[d] = digit_base[d] + prefix;
+    __syncthreads();
+    // stage in digit order (stable), then write digit-contiguous runs
+#pragma unroll
+    for (int j = 0; j < kItems; j++) {
+        if (dig[j] < 0) continue;
+        const uint32_t pos = sm.block_off[dig[j]] + sm.wcount[warp][dig[j]] + rank[j];
+        sm.keys[pos] = k[j];
+        sm.vals[pos] = v[j];
+    }
+    __syncthreads();
+    const int tn = max(0, min(kTile, n - tile_base));
+    for (int i = threadIdx.x; i < tn; i += kThreads) {
+        const K key = sm.keys[i];
+        const int dd = (int)((key >> shift) & 0xff);
+        const uint32_t g = sm.global_off[dd] + (uint32_t)i - sm.block_off[dd];
+        if (kout) kout[g] = key;
+        vout[g] = sm.vals[i];
+    }
+}
+
+// Workspace: hist (passes*256 u32) | status (tiles*256 u32) | ticket (u32).
+inline size_t workspace_bytes(int n_cap, int passes) {
+    const size_t t = (size_t)tile_count(n_cap);
+    return 256 * sizeof(uint32_t) * (size_t)passes + t * 256 * sizeof(uint32_t) + 256;
+}
+
+// Sorts (keys, vals) by bits [0, 8*passes) with ping-pong buffers; with
+// iota the first pass reads value i for key i instead of vals.  Returns 1
+// if the result is in (k_alt, v_alt).  The final pass skips the key write
+// when keep_keys == false.  n_dev (device int, optional) bounds the count
+// below n_cap at run time.
+template <typename K>
+int sort(K* keys, uint32_t* vals, K* k_alt, uint32_t* v_alt, const int* n_dev, int n_cap, int passes,
+         bool keep_keys, bool iota, void* ws, cudaStream_t stream)
+{
+    if (n_cap <= 0 || passes <= 0) return 0;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(pass_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<K>));
+        attr = true;
+    }
+    const int tiles = tile_count(n_cap);
+    uint32_t* hist = static_cast<uint32_t*>(ws);
+    uint32_t* status = hist + 256 * passes;
+    unsigned* ticket = reinterpret_cast<unsigned*>(status + (size_t)tiles * 256);
+    cudaMemsetAsync(hist, 0, 256 * sizeof(uint32_t) * passes, stream);
+    const int hb = min(tiles, 4 * 148);
+    hist_kernel<K><<<hb, kThreads, 0, stream>>>(keys, n_dev, n_cap, passes, hist);
+    scan_hist_kernel<<<1, 256, 0, stream>>>(hist, passes);
+    int flip = 0;
+    for (int p = 0; p < passes; p++) {
+        cudaMemsetAsync(status, 0, (size_t)tiles * 256 * sizeof(uint32_t) + sizeof(unsigned), stream);
+        const K* ki = flip ? k_alt : keys;
+        const uint32_t* vi = flip ? v_alt : vals;
+        K* ko = flip ? keys : k_alt;
+        uint32_t* vo = flip ? vals : v_alt;
+        const bool last = p == passes - 1;
+        pass_kernel<K><<<tiles, kThreads, sizeof(Smem<K>), stream>>>(
+            ki, (p == 0 && iota) ? nullptr : vi, (last && !keep_keys) ? nullptr : ko, vo, n_dev, n_cap,
+            8 * p, hist + 256 * p, status, ticket);
+        flip ^= 1;
+    }
+    return flip;
+}
+
+}  // namespace onesweep

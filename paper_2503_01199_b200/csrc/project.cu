@@ -7,7 +7,7 @@
 //   ccc.py:134-146         cull_clusters           (p-vertex test)
 //   ccc.py:149-164         cluster_visibility      (| any(in_image) widening)
 //   ccc.py:171-194         compact_arrays          (contiguous visible ranges)
-//   tiles.py:50-91         bin_tiles, counting half (exact disc test)
+//   tiles.py:50-91         bin_tiles, per-primitive hit count (exact disc test)
 //
 // One pass over the 64-byte parameter rows (four 128-bit loads per lane per
 // Gaussian, 2 KB contiguous per warp), records staged in shared memory, the
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kThreads)
 project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clusters, CamDev cam,
                             int use_culling, RasterRec* __restrict__ rec_out, int32_t* __restrict__ compact_map,
                             int32_t* __restrict__ cluster_offset, uint8_t* __restrict__ cluster_vis,
-                            int32_t* __restrict__ tile_counts, int32_t* __restrict__ counters,
+                            int32_t* __restrict__ counters,
                             unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -75,7 +75,7 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
                 sb_project(p, cam, o);
                 r.x = o.x; r.y = o.y; r.a = o.ca; r.b = o.cb; r.c = o.cc; r.o = o.op;
                 r.r = o.col[0]; r.g = o.col[1]; r.bl = o.col[2]; r.depth = o.depth; r.radius = o.radius;
-                r.flags = (o.valid ? 1u : 0u) | (o.in_image ? 2u : 0u);
+                uint32_t nhit = 0;
                 any_in |= o.in_image;
                 ndeg += o.degenerate ? 1 : 0;
                 // cluster AABB: p -+ 3 * max(exp(log_scale)) in float64 (ccc.py:125-130)
@@ -87,15 +87,16 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
                     lo[k] = fmin(lo[k], DSUB((double)p[k], reach));
                     hi[k] = fmax(hi[k], DADD((double)p[k], reach));
                 }
-                // tile-hit counting for fragment-generating primitives
+                // tile hits of fragment-generating primitives (exact disc test)
                 if (o.in_image) {
                     int tx0, tx1, ty0, ty1;
                     sb_tile_range(o.x, o.y, o.radius, cam.tiles_x, cam.tiles_y, tx0, tx1, ty0, ty1);
                     for (int ty = ty0; ty <= ty1; ty++)
                         for (int tx = tx0; tx <= tx1; tx++)
-                            if (sb_disc_hits(o.x, o.y, o.radius, tx, ty, cam.W, cam.H))
-                                atomicAdd(&tile_counts[ty * cam.tiles_x + tx], 1);
+                            nhit += sb_disc_hits(o.x, o.y, o.radius, tx, ty, cam.W, cam.H) ? 1u : 0u;
                 }
+                // flags: bit0 valid, bit1 in_image, bits 2.. tile-hit count
+                r.flags = (o.valid ? 1u : 0u) | (o.in_image ? 2u : 0u) | (nhit << 2);
             }
             st[slot] = r;
         }
@@ -160,7 +161,7 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
 
 void sb_launch_project_cull_compact(const float* params, int n, const CamDev& cam, int use_culling,
                                     RasterRec* rec_out, int32_t* compact_map, int32_t* cluster_offset,
-                                    uint8_t* cluster_vis, int32_t* tile_counts, int32_t* counters,
+                                    uint8_t* cluster_vis, int32_t* counters,
                                     unsigned long long* status, unsigned int* ticket, cudaStream_t stream)
 {
     const int k = (n + SB_CLUSTER_SIZE - 1) / SB_CLUSTER_SIZE;
@@ -174,7 +175,7 @@ void sb_launch_project_cull_compact(const float* params, int n, const CamDev& ca
     }
     project_cull_compact_kernel<<<blocks, kThreads, smem, stream>>>(
         reinterpret_cast<const float4*>(params), n, k, cam, use_culling, rec_out, compact_map, cluster_offset,
-        cluster_vis, tile_counts, counters, status, ticket);
+        cluster_vis, counters, status, ticket);
 }
 
 int sb_project_blocks(int n) {

@@ -3,12 +3,12 @@ depth sort -> warp-per-tile raster, all on the device.
 
 Reference API: pkg/src/tinysplat/forward.py:56-94 (RasterConfig,
 RenderOutput, RenderContext) and 258-308 (forward, render).  The call chain
-per view is five launches through the C-ABI (include/splat_b200.h):
+per view is four calls through the C-ABI (include/splat_b200.h):
 
-  sb_project_cull_compact  projection.py:130-190 + ccc.py:112-194 + tile counts
-  sb_bin_offsets           per-tile exclusive scan (-> P)
-  sb_bin_emit              tiles.py:75-91 exact disc test, 64-bit keys
-  sb_tile_sort             tiles.py:92-106 per-tile (depth, index) sort
+  sb_project_cull_compact  projection.py:130-190 + ccc.py:112-194 + tile-hit counts
+  sb_bin_prepare           stable depth order + scan of hit counts (-> P)
+  sb_bin_finish            tiles.py:75-106: emit pairs in depth order, stable
+                           onesweep sort by tile id, per-tile ranges
   sb_raster_fwd            forward.py:161-191 blend + 240-255 assembly
 """
 from __future__ import annotations
@@ -147,25 +147,22 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     cmap = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     coff = torch.empty(max(K, 1), dtype=torch.int32, device=dev)
     cvis = torch.zeros(max(K, 1), dtype=torch.uint8, device=dev)
-    tile_counts = torch.zeros(ntiles, dtype=torch.int32, device=dev)
-    counters = torch.zeros(4, dtype=torch.int32, device=dev)
-    tile_offsets = torch.empty(ntiles + 1, dtype=torch.int32, device=dev)
-    ws_n = _lib.load().sb_project_workspace_bytes(n)
-    ws = _lib.workspace("project", ws_n, dev)
+    counters = torch.zeros(8, dtype=torch.int32, device=dev)   # vis, N_c, ndeg, pad, P
+    order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    pair_offsets = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    ws = _lib.workspace("project", lib.sb_project_workspace_bytes(n), dev)
     _lib.call("sb_project_cull_compact", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s), _lib.ptr(recs),
-              _lib.ptr(cmap), _lib.ptr(coff), _lib.ptr(cvis), _lib.ptr(tile_counts), _lib.ptr(counters),
-              _lib.ptr(ws), ws.numel(), stream)
-    _lib.call("sb_bin_offsets", _lib.ptr(tile_counts), ntiles, _lib.ptr(tile_offsets), stream)
-    hdr = torch.cat([tile_offsets[ntiles:], counters[:3]]).cpu().tolist()   # one D2H read: P, vis, N_c, ndeg
-    P, vis, nc, ndeg = (int(v) for v in hdr)
-    keys = torch.empty(max(P, 1), dtype=torch.int64, device=dev)
-    scratch = torch.empty(max(P, 1), dtype=torch.int64, device=dev)
+              _lib.ptr(cmap), _lib.ptr(coff), _lib.ptr(cvis), _lib.ptr(counters), _lib.ptr(ws), ws.numel(), stream)
+    ws_p = _lib.workspace("bin_prepare", lib.sb_bin_prepare_workspace_bytes(n), dev)
+    _lib.call("sb_bin_prepare", _lib.ptr(recs), _lib.ptr(counters), n, _lib.ptr(order), _lib.ptr(pair_offsets),
+              _lib.ptr(counters[4:]), _lib.ptr(ws_p), ws_p.numel(), stream)
+    vis, nc, ndeg, _, P = (int(v) for v in counters[:5].cpu().tolist())   # one D2H read
+    tile_offsets = torch.empty(ntiles + 1, dtype=torch.int32, device=dev)
     prims = torch.empty(max(P, 1), dtype=torch.int32, device=dev)
-    ws_e = _lib.workspace("emit", _lib.load().sb_bin_emit_workspace_bytes(ntiles), dev)
-    _lib.call("sb_bin_emit", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), _lib.ptr(tile_offsets),
-              _lib.ptr(keys), _lib.ptr(ws_e), ws_e.numel(), stream)
-    _lib.call("sb_tile_sort", _lib.ptr(tile_offsets), ntiles, _lib.ptr(keys), _lib.ptr(scratch), _lib.ptr(prims),
-              stream)
+    ws_f = _lib.workspace("bin_finish", lib.sb_bin_finish_workspace_bytes(P, ntiles), dev)
+    _lib.call("sb_bin_finish", _lib.ptr(recs), _lib.ptr(counters), n, _lib.ptr(order), _lib.ptr(pair_offsets),
+              C.byref(cam_s), P, _lib.ptr(tile_offsets), _lib.ptr(prims), _lib.ptr(ws_f), ws_f.numel(), stream)
     color = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
     T = torch.empty((H, W), dtype=torch.float32, device=dev)
     frags = torch.empty((H, W), dtype=torch.int32, device=dev)
