@@ -82,31 +82,61 @@ hit_scan_kernel(const RasterRec* __restrict__ recs, const uint32_t* __restrict__
     }
 }
 
+// Consecutive depth ranks own consecutive output ranges, so a warp's 32
+// primitives write one contiguous span: stage it in shared memory and store
+// it with coalesced writes (direct writes only when the span overflows).
+constexpr int kEmitStage = 768;   // pairs staged per warp
+
 __global__ void __launch_bounds__(256)
 emit_kernel(const RasterRec* __restrict__ recs, const uint32_t* __restrict__ order,
             const int32_t* __restrict__ offsets, const int32_t* __restrict__ counters, int n_cap,
             uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ slots, int tiles_x, int tiles_y, int W, int H)
 {
+    __shared__ uint2 stage[8][kEmitStage];
     const int nc = min(counters[1], n_cap);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nc) return;
-    const uint32_t s = order[i];
-    const float4* r4 = reinterpret_cast<const float4*>(recs + s);
-    const float4 a = __ldg(r4);
-    const float4 c = __ldg(r4 + 2);
-    const uint32_t flags = __float_as_uint(c.w);
-    if ((flags >> 2) == 0) return;
-    const float x = a.x, y = a.y, r = c.z;
-    int tx0, tx1, ty0, ty1;
-    sb_tile_range(x, y, r, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
-    int pos = offsets[i];
-    for (int ty = ty0; ty <= ty1; ty++)
-        for (int tx = tx0; tx <= tx1; tx++)
-            if (sb_disc_hits(x, y, r, tx, ty, W, H)) {
-                tile_keys[pos] = (uint32_t)(ty * tiles_x + tx);
-                slots[pos] = s;
-                pos++;
-            }
+    const int i0 = i - lane;
+    if (i0 >= nc) return;
+    uint32_t s = 0, nh = 0;
+    float x = 0.f, y = 0.f, r = 0.f;
+    int off = 0;
+    if (i < nc) {
+        s = order[i];
+        const float4* r4 = reinterpret_cast<const float4*>(recs + s);
+        const float4 a = __ldg(r4);
+        const float4 c = __ldg(r4 + 2);
+        nh = __float_as_uint(c.w) >> 2;
+        x = a.x; y = a.y; r = c.z;
+        off = offsets[i];
+    }
+    const int wbeg = __shfl_sync(0xffffffffu, off, 0);
+    const int wend = __reduce_max_sync(0xffffffffu, (unsigned)(nh ? off + (int)nh : wbeg));
+    const bool staged = wend - wbeg <= kEmitStage;
+    if (nh) {
+        int tx0, tx1, ty0, ty1;
+        sb_tile_range(x, y, r, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+        int pos = off;
+        for (int ty = ty0; ty <= ty1; ty++)
+            for (int tx = tx0; tx <= tx1; tx++)
+                if (sb_disc_hits(x, y, r, tx, ty, W, H)) {
+                    const uint32_t t = (uint32_t)(ty * tiles_x + tx);
+                    if (staged) {
+                        stage[warp][pos - wbeg] = make_uint2(t, s);
+                    } else {
+                        tile_keys[pos] = t;
+                        slots[pos] = s;
+                    }
+                    pos++;
+                }
+    }
+    if (!staged) return;
+    __syncwarp();
+    for (int q = lane; q < wend - wbeg; q += 32) {
+        const uint2 e = stage[warp][q];
+        tile_keys[wbeg + q] = e.x;
+        slots[wbeg + q] = e.y;
+    }
 }
 
 __global__ void __launch_bounds__(256)

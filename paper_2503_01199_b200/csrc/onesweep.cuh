@@ -32,7 +32,24 @@ struct Smem {
 
 __host__ __device__ __forceinline__ int tile_count(int n) { return (n + kTile - 1) / kTile; }
 
-// hist[p][d] += #keys with digit d in pass p, for p < passes.
+// lanes of `active` holding the same 8-bit digit as this lane: the
+// intersection of 8 ballots (short-latency VOTEs instead of MATCH.ANY)
+SB_INLINE unsigned digit_peers(unsigned active, int d) {
+    unsigned peers = active;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        const bool bit = (d >> b) & 1;
+        const unsigned m = __ballot_sync(active, bit);
+        peers &= bit ? m : ~m;
+    }
+    return peers;
+}
+
+// hist[p][d] += #keys with digit d in pass p, for p < passes.  Each thread
+// issues all of its loads for a chunk before the (match_any-aggregated)
+// shared-memory counting, so memory latency overlaps.
+constexpr int kHistItems = 8;
+
 template <typename K>
 __global__ void __launch_bounds__(kThreads)
 hist_kernel(const K* __restrict__ keys, const int* __restrict__ n_dev, int n_cap, int passes,
@@ -43,16 +60,24 @@ hist_kernel(const K* __restrict__ keys, const int* __restrict__ n_dev, int n_cap
     __syncthreads();
     const int n = n_dev ? min(*n_dev, n_cap) : n_cap;
     const unsigned lane_lt = (1u << (threadIdx.x & 31)) - 1u;
-    for (int base = blockIdx.x * kThreads; base < n; base += gridDim.x * kThreads) {
-        const int i = base + threadIdx.x;
-        const bool ok = i < n;
-        const unsigned act = __ballot_sync(0xffffffffu, ok);
-        if (!ok) continue;
-        const K k = keys[i];
-        for (int p = 0; p < passes; p++) {
-            const int d = (int)((k >> (8 * p)) & 0xff);
-            const unsigned peers = __match_any_sync(act, d);
-            if ((peers & lane_lt) == 0) atomicAdd(&h[p][d], (uint32_t)__popc(peers));
+    for (int base = blockIdx.x * kThreads * kHistItems; base < n; base += gridDim.x * kThreads * kHistItems) {
+        K k[kHistItems];
+#pragma unroll
+        for (int j = 0; j < kHistItems; j++) {
+            const int i = base + j * kThreads + threadIdx.x;
+            k[j] = i < n ? keys[i] : K(0);
+        }
+#pragma unroll
+        for (int j = 0; j < kHistItems; j++) {
+            const int i = base + j * kThreads + threadIdx.x;
+            const bool ok = i < n;
+            const unsigned act = __ballot_sync(0xffffffffu, ok);
+            if (!ok) continue;
+            for (int p = 0; p < passes; p++) {
+                const int d = (int)((k[j] >> (8 * p)) & 0xff);
+                const unsigned peers = digit_peers(act, d);
+                if ((peers & lane_lt) == 0) atomicAdd(&h[p][d], (uint32_t)__popc(peers));
+            }
         }
     }
     __syncthreads();
@@ -100,24 +125,27 @@ pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
     const int tile_base = bid * kTile;
     const int wbase = tile_base + warp * kWarpKeys;
     K k[kItems];
-    uint32_t v[kItems], rank[kItems];
-    int dig[kItems];
+    uint32_t v[kItems], dr[kItems];   // dr = digit << 16 | rank within the warp (0xffffffff: none)
     const unsigned lt = (1u << lane) - 1u;
+    // all loads first so their latency overlaps
+#pragma unroll
+    for (int j = 0; j < kItems; j++) {
+        const int i = wbase + j * 32 + lane;
+        const bool ok = i < n;
+        k[j] = ok ? kin[i] : K(0);
+        v[j] = ok ? (vin ? vin[i] : (uint32_t)i) : 0u;
+    }
 #pragma unroll
     for (int j = 0; j < kItems; j++) {
         const int i = wbase + j * 32 + lane;
         const bool ok = i < n;
         const unsigned active = __ballot_sync(0xffffffffu, ok);
-        dig[j] = -1;
-        rank[j] = 0;
+        dr[j] = 0xffffffffu;
         if (ok) {
-            k[j] = kin[i];
-            v[j] = vin ? vin[i] : (uint32_t)i;
             const int d = (int)((k[j] >> shift) & 0xff);
-            dig[j] = d;
-            const unsigned peers = __match_any_sync(active, d);
+            const unsigned peers = digit_peers(active, d);
             const uint32_t pre = sm.wcount[warp][d];
-            rank[j] = pre + __popc(peers & lt);
+            dr[j] = ((uint32_t)d << 16) | (pre + __popc(peers & lt));
             __syncwarp(active);
             if ((peers & lt) == 0) sm.wcount[warp][d] = pre + __popc(peers);
         }
@@ -166,8 +194,9 @@ pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
     // stage in digit order (stable), then write digit-contiguous runs
 #pragma unroll
     for (int j = 0; j < kItems; j++) {
-        if (dig[j] < 0) continue;
-        const uint32_t pos = sm.block_off[dig[j]] + sm.wcount[warp][dig[j]] + rank[j];
+        if (dr[j] == 0xffffffffu) continue;
+        const uint32_t dj = dr[j] >> 16;
+        const uint32_t pos = sm.block_off[dj] + sm.wcount[warp][dj] + (dr[j] & 0xffffu);
         sm.keys[pos] = k[j];
         sm.vals[pos] = v[j];
     }
@@ -208,7 +237,7 @@ int sort(K* keys, uint32_t* vals, K* k_alt, uint32_t* v_alt, const int* n_dev, i
     uint32_t* status = hist + 256 * passes;
     unsigned* ticket = reinterpret_cast<unsigned*>(status + (size_t)tiles * 256);
     cudaMemsetAsync(hist, 0, 256 * sizeof(uint32_t) * passes, stream);
-    const int hb = min(tiles, 4 * 148);
+    const int hb = min((n_cap + kThreads * kHistItems - 1) / (kThreads * kHistItems), 8 * 148);
     hist_kernel<K><<<hb, kThreads, 0, stream>>>(keys, n_dev, n_cap, passes, hist);
     scan_hist_kernel<<<1, 256, 0, stream>>>(hist, passes);
     int flip = 0;

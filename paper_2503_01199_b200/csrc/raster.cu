@@ -358,7 +358,10 @@ raster_bwd_kernel(BwdParams p)
         const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
         const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
         const float px = (float)pxi, py0 = (float)py0i;
-        float T[4], suf[4][3], dI[4][3];
+        // per pixel: T (recovered back to front), dI, and Sd = dI . suffix where
+        // suffix = sum_{j>k} w_j c_j + T_final bg (backward.py:155-159), so
+        // dL/dalpha = T (dI . c) - Sd / (1 - alpha)
+        float T[4], Sd[4], dI[4][3];
         int last[4];
         int lane_max = 0;
 #pragma unroll
@@ -368,10 +371,8 @@ raster_bwd_kernel(BwdParams p)
             T[i] = v ? p.T_final[pix] : 1.0f;
             last[i] = v ? p.last[pix] : 0;
 #pragma unroll
-            for (int ch = 0; ch < 3; ch++) {
-                dI[i][ch] = v ? p.dL_dI[3 * pix + ch] : 0.0f;
-                suf[i][ch] = T[i] * p.bg[ch];
-            }
+            for (int ch = 0; ch < 3; ch++) dI[i][ch] = v ? p.dL_dI[3 * pix + ch] : 0.0f;
+            Sd[i] = T[i] * (dI[i][0] * p.bg[0] + dI[i][1] * p.bg[1] + dI[i][2] * p.bg[2]);
             lane_max = max(lane_max, last[i]);
         }
         const int kmax = __reduce_max_sync(0xffffffffu, lane_max);
@@ -404,16 +405,13 @@ raster_bwd_kernel(BwdParams p)
                         const float inv = rcp_approx(1.0f - alpha);
                         const float Tb = T[i] * inv;
                         const float wi = Tb * alpha;
-                        float da = dI[i][0] * (Tb * r.r - suf[i][0] * inv);
-                        da += dI[i][1] * (Tb * r.g - suf[i][1] * inv);
-                        da += dI[i][2] * (Tb * r.bl - suf[i][2] * inv);
+                        const float dc = dI[i][0] * r.r + dI[i][1] * r.g + dI[i][2] * r.bl;
+                        const float da = Tb * dc - Sd[i] * inv;
                         const float dpre = (ci && araw < p.amax) ? da : 0.0f;
                         f[i] = dpre * G[i];
                         uG[i] = dpre * r.o * G[i];
                         w[i] = ci ? wi : 0.0f;
-                        suf[i][0] += w[i] * r.r;
-                        suf[i][1] += w[i] * r.g;
-                        suf[i][2] += w[i] * r.bl;
+                        Sd[i] += w[i] * dc;
                         T[i] = ci ? Tb : T[i];
                         cnt_l += ci ? 1 : 0;
                     }
