@@ -135,8 +135,10 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
     for (int k = 0; k < 4; k++) dst[k] = make_float4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
 }
 
-// optim.py:69-98: rows of true-masked clusters; per-row step counters; float64
-// arithmetic on float32 state.
+// optim.py:69-98: rows of true-masked clusters, per-row step counters.
+// Per row the bias corrections are formed in float64 (beta^t = exp2(t *
+// log2 beta)) and folded into two scalars per channel; the per-element
+// moment and parameter updates run in float32 on the float32 state.
 __global__ void __launch_bounds__(256)
 adam_kernel(float4* __restrict__ params, const float4* __restrict__ grads, float4* __restrict__ m,
             float4* __restrict__ v, int32_t* __restrict__ step, const uint8_t* __restrict__ cluster_mask, int n,
@@ -147,27 +149,39 @@ adam_kernel(float4* __restrict__ params, const float4* __restrict__ grads, float
     const int s = step[g] + 1;
     step[g] = s;
     const double t = (double)s;
-    const double bc1 = 1.0 - pow(0.9, t), bc2 = 1.0 - pow(0.999, t);
-    const double lrc[5] = {lr0, lr1, lr2, lr3, lr4};
+    const double bc1 = 1.0 - exp2(t * -0.15200309344504997);    // log2(0.9)
+    const double bc2 = 1.0 - exp2(t * -0.0014434168696687937);  // log2(0.999)
+    // p -= lr * (m / bc1) / (sqrt(v / bc2) + eps) = a * m / (sqrt(v) * b + eps)
+    const float b = (float)(1.0 / sqrt(bc2));
+    const double inv1 = 1.0 / bc1;
+    const float a[5] = {(float)(lr0 * inv1), (float)(lr1 * inv1), (float)(lr2 * inv1), (float)(lr3 * inv1),
+                        (float)(lr4 * inv1)};
     const int col_ch[16] = {0, 0, 0, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, -1, -1};
+    float4 P[4], G[4], M[4], V[4];
 #pragma unroll
     for (int k = 0; k < 4; k++) {
         const size_t i = (size_t)g * 4 + k;
-        float4 P = params[i], Gr = __ldg(grads + i), Mm = m[i], V = v[i];
-        float* pp = &P.x; const float* gg = &Gr.x; float* mm = &Mm.x; float* vv = &V.x;
+        P[k] = params[i]; G[k] = __ldg(grads + i); M[k] = m[i]; V[k] = v[i];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        float* pp = &P[k].x; const float* gg = &G[k].x; float* mm = &M[k].x; float* vv = &V[k].x;
 #pragma unroll
         for (int e = 0; e < 4; e++) {
             const int col = 4 * k + e;
             if (col_ch[col] < 0) continue;
-            const double gr = gg[e];
-            const double mn = 0.9 * (double)mm[e] + (1.0 - 0.9) * gr;
-            const double vn = 0.999 * (double)vv[e] + (1.0 - 0.999) * gr * gr;
-            const double mh = mn / bc1, vh = vn / bc2;
-            pp[e] = (float)((double)pp[e] - lrc[col_ch[col]] * mh / (sqrt(vh) + 1e-15));
-            mm[e] = (float)mn;
-            vv[e] = (float)vn;
+            const float gr = gg[e];
+            const float mn = 0.9f * mm[e] + 0.1f * gr;
+            const float vn = 0.999f * vv[e] + 0.001f * gr * gr;
+            pp[e] -= a[col_ch[col]] * mn / (sqrtf(vn) * b + 1e-15f);
+            mm[e] = mn;
+            vv[e] = vn;
         }
-        params[i] = P; m[i] = Mm; v[i] = V;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const size_t i = (size_t)g * 4 + k;
+        params[i] = P[k]; m[i] = M[k]; v[i] = V[k];
     }
 }
 

@@ -5,8 +5,9 @@
 // (sigma 1.5), K1 0.01, K2 0.03, per-channel SSIM over the valid interior,
 // gradient by the adjoint filter (zero-embed the interior field, correlate).
 //
-// One CTA per (64 x 32 output tile, channel): x and y are staged with a
-// 10-pixel halo; the five moment maps are filtered separably on the tile + 5
+// One CTA per 64 x 32 output tile: x and y (all three channels, so the
+// interleaved RGB rows load contiguously) are staged with a 10-pixel halo;
+// then per channel the five moment maps are filtered separably on the tile + 5
 // halo, the three gradient fields (g_mu, 2 dA2, dB2) are formed there,
 // filtered back (adjoint) onto the tile and combined with the L1 sign term.
 // Every separable pass is a register sliding window: a thread owns a short
@@ -26,7 +27,7 @@ constexpr int kThreads = 512;
 struct Win { float w[NT]; };
 
 struct Smem {
-    float sx[IH][IW], sy[IH][IW];
+    float sx[3][IH][IW], sy[3][IH][IW];
     float vm[5][FH][IW];          // vertical moments; later reused for the adjoint vertical pass
     float fl[3][FH][FW];          // g_mu, g_xy (= 2 dA2), g_xx (= dB2)
     double red[2][kThreads / 32];
@@ -38,7 +39,6 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    const int ch = blockIdx.z;
     const int ox = blockIdx.x * TW, oy = blockIdx.y * TH;
     const int tid = threadIdx.x;
     const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
@@ -46,40 +46,48 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
 #pragma unroll
     for (int k = 0; k < NT; k++) w[k] = win.w[k];
 
-    // (1) stage x, y with a 10-pixel halo (zero outside the image)
-    for (int i = tid; i < IH * IW; i += kThreads) {
-        const int r = i / IW, c = i - r * IW;
+    // (1) stage x, y (3 channels) with a 10-pixel halo, zero outside the
+    //     image; consecutive threads read consecutive interleaved floats
+    for (int i = tid; i < IH * IW * 3; i += kThreads) {
+        const int r = i / (IW * 3), rem = i - r * (IW * 3), c = rem / 3, cc = rem - 3 * c;
         const int gy = oy - 2 * R + r, gx = ox - 2 * R + c;
         float xv = 0.f, yv = 0.f;
         if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
-            const size_t idx = ((size_t)gy * W + gx) * 3 + ch;
+            const size_t idx = ((size_t)gy * W + gx) * 3 + cc;
             xv = x_img[idx];
             yv = y_u8 ? (float)y_u8[idx] * (1.0f / 255.0f) : y_img[idx];
         }
-        sm.sx[r][c] = xv;
-        sm.sy[r][c] = yv;
+        sm.sx[cc][r][c] = xv;
+        sm.sy[cc][r][c] = yv;
     }
     __syncthreads();
+    double s_sum = 0.0, l1_sum = 0.0;
+    for (int ch = 0; ch < 3; ch++) {
 
     // (2) vertical moments on rows [oy-5, oy+TH+5): column c, runs of 7 rows
     {
         constexpr int RUN = 7, NRUN = FH / RUN;          // 6 runs x 84 columns = 504 threads
         if (tid < NRUN * IW) {
             const int c = tid % IW, r0 = (tid / IW) * RUN;
-            float xs[RUN + NT - 1], ys[RUN + NT - 1];
+            float xs[RUN + NT - 1], ys[RUN + NT - 1], xx[RUN + NT - 1], yy[RUN + NT - 1], xy[RUN + NT - 1];
 #pragma unroll
-            for (int k = 0; k < RUN + NT - 1; k++) { xs[k] = sm.sx[r0 + k][c]; ys[k] = sm.sy[r0 + k][c]; }
+            for (int k = 0; k < RUN + NT - 1; k++) {
+                xs[k] = sm.sx[ch][r0 + k][c];
+                ys[k] = sm.sy[ch][r0 + k][c];
+                xx[k] = xs[k] * xs[k];
+                yy[k] = ys[k] * ys[k];
+                xy[k] = xs[k] * ys[k];
+            }
 #pragma unroll
             for (int o = 0; o < RUN; o++) {
                 float a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
 #pragma unroll
                 for (int k = 0; k < NT; k++) {
-                    const float xv = xs[o + k], yv = ys[o + k];
-                    a0 += w[k] * xv;
-                    a1 += w[k] * yv;
-                    a2 += w[k] * xv * xv;
-                    a3 += w[k] * yv * yv;
-                    a4 += w[k] * xv * yv;
+                    a0 += w[k] * xs[o + k];
+                    a1 += w[k] * ys[o + k];
+                    a2 += w[k] * xx[o + k];
+                    a3 += w[k] * yy[o + k];
+                    a4 += w[k] * xy[o + k];
                 }
                 sm.vm[0][r0 + o][c] = a0; sm.vm[1][r0 + o][c] = a1; sm.vm[2][r0 + o][c] = a2;
                 sm.vm[3][r0 + o][c] = a3; sm.vm[4][r0 + o][c] = a4;
@@ -89,7 +97,6 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
     __syncthreads();
 
     // (3) horizontal pass -> moments on the field region -> SSIM + gradient fields
-    double s_sum = 0.0;
     {
         constexpr int RUN = 7, NRUN = (FW + RUN - 1) / RUN;   // 11 runs x 42 rows = 462 threads
         if (tid < NRUN * FH) {
@@ -158,7 +165,6 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
     __syncthreads();
 
     // (5) adjoint horizontal pass + combination with the L1 term
-    double l1_sum = 0.0;
     {
         const int ni_w = W - 2 * R, ni_h = H - 2 * R;
         const float n_int = (float)ni_w * (float)ni_h;
@@ -185,7 +191,7 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
         for (int o = 0; o < RUN; o++) {
             const int gx = ox + c0 + o;
             if (gy >= H || gx >= W) continue;
-            const float xv = sm.sx[r + 2 * R][c0 + o + 2 * R], yv = sm.sy[r + 2 * R][c0 + o + 2 * R];
+            const float xv = sm.sx[ch][r + 2 * R][c0 + o + 2 * R], yv = sm.sy[ch][r + 2 * R][c0 + o + 2 * R];
             const float g_ssim = t[0][o] + t[1][o] * yv + t[2][o] * (2.f * xv);
             const float diff = xv - yv;
             const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
@@ -193,6 +199,8 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
             l1_sum += (double)fabsf(diff);
         }
     }
+    __syncthreads();   // vm / fl are reused by the next channel
+    }  // channel loop
     // block reduction of the two loss partials
     const int lane = tid & 31, warp = tid >> 5;
     for (int o = 16; o >= 1; o >>= 1) {
@@ -237,7 +245,7 @@ void sb_launch_loss(const float* x, const float* y, const uint8_t* y_u8, int W, 
         attr = true;
     }
     cudaMemsetAsync(accum, 0, 2 * sizeof(double), stream);
-    dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, 3);
+    dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, 1);
     loss_kernel<<<grid, kThreads, sizeof(Smem), stream>>>(x, y, y_u8, W, H, lam, win, grad, accum);
     loss_finalize_kernel<<<1, 1, 0, stream>>>(accum, W, H, lam, loss);
 }

@@ -396,24 +396,31 @@ raster_bwd_kernel(BwdParams p)
                 {
                     float G[4];
                     lane_G(r, px, py0, G, dx, dy);
+                    float araw[4], alpha[4];
+                    bool ci[4];
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
-                        const float araw = FMUL(r.o, G[i]);
-                        const float alpha = fminf(araw, p.amax);
+                        araw[i] = FMUL(r.o, G[i]);
+                        alpha[i] = fminf(araw[i], p.amax);
                         // contributing: before this pixel's last contributor and usable
-                        const bool ci = (k < last[i]) && (alpha >= p.amin);
-                        const float inv = rcp_approx(1.0f - alpha);
-                        const float Tb = T[i] * inv;
-                        const float wi = Tb * alpha;
-                        const float dc = dI[i][0] * r.r + dI[i][1] * r.g + dI[i][2] * r.bl;
-                        const float da = Tb * dc - Sd[i] * inv;
-                        const float dpre = (ci && araw < p.amax) ? da : 0.0f;
-                        f[i] = dpre * G[i];
-                        uG[i] = dpre * r.o * G[i];
-                        w[i] = ci ? wi : 0.0f;
-                        Sd[i] += w[i] * dc;
-                        T[i] = ci ? Tb : T[i];
-                        cnt_l += ci ? 1 : 0;
+                        ci[i] = (k < last[i]) && (alpha[i] >= p.amin);
+                        cnt_l += ci[i] ? 1 : 0;
+                        f[i] = uG[i] = w[i] = 0.0f;
+                    }
+                    if (cnt_l > 0) {
+#pragma unroll
+                        for (int i = 0; i < 4; i++) {
+                            const float inv = rcp_approx(1.0f - alpha[i]);
+                            const float Tb = T[i] * inv;
+                            const float dc = dI[i][0] * r.r + dI[i][1] * r.g + dI[i][2] * r.bl;
+                            const float da = Tb * dc - Sd[i] * inv;
+                            const float dpre = (ci[i] && araw[i] < p.amax) ? da : 0.0f;
+                            f[i] = dpre * G[i];
+                            uG[i] = dpre * r.o * G[i];
+                            w[i] = ci[i] ? Tb * alpha[i] : 0.0f;
+                            Sd[i] += w[i] * dc;
+                            T[i] = ci[i] ? Tb : T[i];
+                        }
                     }
                 }
                 const bool contrib = cnt_l > 0;
