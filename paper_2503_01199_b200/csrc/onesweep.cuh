@@ -55,11 +55,13 @@ __global__ void __launch_bounds__(kThreads)
 hist_kernel(const K* __restrict__ keys, const int* __restrict__ n_dev, int n_cap, int passes,
             uint32_t* __restrict__ hist)
 {
-    __shared__ uint32_t h[8][256];
-    for (int i = threadIdx.x; i < 8 * 256; i += kThreads) (&h[0][0])[i] = 0;
+    // two copies per pass (even / odd warps) to halve cross-warp contention;
+    // same-bin lanes of one warp are serialised by the hardware
+    __shared__ uint32_t h[2][8][256];
+    for (int i = threadIdx.x; i < 2 * 8 * 256; i += kThreads) (&h[0][0][0])[i] = 0;
     __syncthreads();
     const int n = n_dev ? min(*n_dev, n_cap) : n_cap;
-    const unsigned lane_lt = (1u << (threadIdx.x & 31)) - 1u;
+    const int copy = (threadIdx.x >> 5) & 1;
     for (int base = blockIdx.x * kThreads * kHistItems; base < n; base += gridDim.x * kThreads * kHistItems) {
         K k[kHistItems];
 #pragma unroll
@@ -69,20 +71,13 @@ hist_kernel(const K* __restrict__ keys, const int* __restrict__ n_dev, int n_cap
         }
 #pragma unroll
         for (int j = 0; j < kHistItems; j++) {
-            const int i = base + j * kThreads + threadIdx.x;
-            const bool ok = i < n;
-            const unsigned act = __ballot_sync(0xffffffffu, ok);
-            if (!ok) continue;
-            for (int p = 0; p < passes; p++) {
-                const int d = (int)((k[j] >> (8 * p)) & 0xff);
-                const unsigned peers = digit_peers(act, d);
-                if ((peers & lane_lt) == 0) atomicAdd(&h[p][d], (uint32_t)__popc(peers));
-            }
+            if (base + j * kThreads + threadIdx.x >= n) continue;
+            for (int p = 0; p < passes; p++) atomicAdd(&h[copy][p][(int)((k[j] >> (8 * p)) & 0xff)], 1u);
         }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * 256; i += kThreads) {
-        const uint32_t c = (&h[0][0])[i];
+        const uint32_t c = (&h[0][0][0])[i] + (&h[1][0][0])[i];
         if (c) atomicAdd(&hist[i], c);
     }
 }
@@ -135,19 +130,30 @@ pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
         k[j] = ok ? kin[i] : K(0);
         v[j] = ok ? (vin ? vin[i] : (uint32_t)i) : 0u;
     }
+    // peer masks for all items first (independent MATCHes pipeline), then
+    // the dependent per-warp digit counters
+    unsigned peers[kItems];
 #pragma unroll
     for (int j = 0; j < kItems; j++) {
         const int i = wbase + j * 32 + lane;
         const bool ok = i < n;
         const unsigned active = __ballot_sync(0xffffffffu, ok);
+        peers[j] = 0u;
         dr[j] = 0xffffffffu;
         if (ok) {
             const int d = (int)((k[j] >> shift) & 0xff);
-            const unsigned peers = digit_peers(active, d);
+            dr[j] = (uint32_t)d << 16;
+            peers[j] = __match_any_sync(active, d);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kItems; j++) {
+        if (dr[j] != 0xffffffffu) {
+            const uint32_t d = dr[j] >> 16;
             const uint32_t pre = sm.wcount[warp][d];
-            dr[j] = ((uint32_t)d << 16) | (pre + __popc(peers & lt));
-            __syncwarp(active);
-            if ((peers & lt) == 0) sm.wcount[warp][d] = pre + __popc(peers);
+            dr[j] |= pre + __popc(peers[j] & lt);
+            __syncwarp(__activemask());
+            if ((peers[j] & lt) == 0) sm.wcount[warp][d] = pre + __popc(peers[j]);
         }
         __syncwarp();
     }
@@ -175,15 +181,20 @@ pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
     // decoupled look-back for this digit
     uint32_t prefix = 0;
     if (bid > 0) {
+        // walk back 8 tiles per round trip; stop at the first not-ready entry
         int j = bid - 1;
-        while (true) {
-            uint32_t s;
-            do {
-                s = st[(size_t)j * 256 + d];
-            } while ((s & (kFlagAgg | kFlagInc)) == 0);
-            prefix += s & kValMask;
-            if (s & kFlagInc) break;
-            j--;
+        bool done = false;
+        while (!done) {
+            uint32_t sv[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) sv[q] = j - q >= 0 ? st[(size_t)(j - q) * 256 + d] : (uint32_t)(2u << 30);
+            int q = 0;
+            for (; q < 8; q++) {
+                if ((sv[q] & (kFlagAgg | kFlagInc)) == 0) break;
+                prefix += sv[q] & kValMask;
+                if (sv[q] & kFlagInc) { done = true; break; }
+            }
+            j -= q;
         }
         st[(size_t)bid * 256 + d] = kFlagInc | (prefix + cnt);
     }

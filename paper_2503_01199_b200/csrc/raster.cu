@@ -74,7 +74,10 @@ SB_INLINE void commit_chunk(SRec* slab, const Prefetch& pf, int cnt, int lane) {
 }
 
 // scanline exponent (forward.py:97-108) with numpy's operation order; the
-// forward and backward share it so both see bit-identical alphas
+// forward and backward share it so both see bit-identical alphas.
+// expo_i = (basic + linear*i) + quad*(i*i): for i = 0 the products are exact
+// zeros, and for i = 2 the scalings by 2 and 4 are exact, so fusing them
+// (FMA of an exact product = one rounding) is bit-identical to numpy.
 SB_INLINE void lane_G(const SRec& r, float px, float py0, float G[4], float& dx, float& dy) {
     dx = FSUB(r.x, px);
     dy = FSUB(r.y, py0);
@@ -82,11 +85,10 @@ SB_INLINE void lane_G(const SRec& r, float px, float py0, float G[4], float& dx,
                                          FMUL(FMUL(r.c, dy), dy)));
     const float linear = FADD(FMUL(r.b, dx), FMUL(r.c, dy));
     const float quad = FMUL(-0.5f, r.c);
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-        const float fi = (float)i;
-        G[i] = expf(FADD(FADD(basic, FMUL(linear, fi)), FMUL(quad, (float)(i * i))));
-    }
+    G[0] = expf(basic);
+    G[1] = expf(FADD(FADD(basic, linear), quad));
+    G[2] = expf(FFMA(quad, 4.0f, FFMA(linear, 2.0f, basic)));
+    G[3] = expf(FADD(FADD(basic, FMUL(linear, 3.0f)), FMUL(quad, 9.0f)));
 }
 
 SB_INLINE int next_tile(int* counter, int lane) {
@@ -156,10 +158,12 @@ raster_fwd_kernel(FwdParams p)
                 for (int i = 0; i < 4; i++) {
                     const float alpha = fminf(FMUL(r.o, G[i]), p.amax);
                     if (valid[i] && T[i] >= p.tstop && alpha >= p.amin) {
+                        // T (which decides termination / frag counts) keeps
+                        // numpy's rounding; the colour sum may fuse
                         const float w = FMUL(T[i], alpha);
-                        rgb[i][0] = FADD(rgb[i][0], FMUL(w, r.r));
-                        rgb[i][1] = FADD(rgb[i][1], FMUL(w, r.g));
-                        rgb[i][2] = FADD(rgb[i][2], FMUL(w, r.bl));
+                        rgb[i][0] = fmaf(w, r.r, rgb[i][0]);
+                        rgb[i][1] = fmaf(w, r.g, rgb[i][1]);
+                        rgb[i][2] = fmaf(w, r.bl, rgb[i][2]);
                         T[i] = FMUL(T[i], FSUB(1.0f, alpha));
                         frags[i]++;
                         last[i] = k0 + j + 1;
