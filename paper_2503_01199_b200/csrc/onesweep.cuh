@@ -32,15 +32,17 @@ struct Smem {
 
 __host__ __device__ __forceinline__ int tile_count(int n) { return (n + kTile - 1) / kTile; }
 
-// lanes of `active` holding the same 8-bit digit as this lane: the
-// intersection of 8 ballots (short-latency VOTEs instead of MATCH.ANY)
-SB_INLINE unsigned digit_peers(unsigned active, int d) {
-    unsigned peers = active;
+// lanes of the (full) warp holding the same digit value as this lane, for
+// values < 2^nbits: the intersection of nbits ballots (VOTE + one LOP3 per
+// bit; MATCH.ANY has too little throughput on this part)
+template <int NBITS>
+SB_INLINE unsigned digit_peers(unsigned d) {
+    unsigned peers = 0xffffffffu;
 #pragma unroll
-    for (int b = 0; b < 8; b++) {
-        const bool bit = (d >> b) & 1;
-        const unsigned m = __ballot_sync(active, bit);
-        peers &= bit ? m : ~m;
+    for (int b = 0; b < NBITS; b++) {
+        const unsigned m = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        const unsigned sel = 0u - ((d >> b) & 1u);
+        peers &= ~(m ^ sel);
     }
     return peers;
 }
@@ -132,19 +134,16 @@ pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
     }
     // peer masks for all items first (independent MATCHes pipeline), then
     // the dependent per-warp digit counters
+    // (branch-free; lanes past the end carry value 256 + lane: 9-bit values
+    // with bit 8 set, so they match no real digit)
     unsigned peers[kItems];
 #pragma unroll
     for (int j = 0; j < kItems; j++) {
-        const int i = wbase + j * 32 + lane;
-        const bool ok = i < n;
-        const unsigned active = __ballot_sync(0xffffffffu, ok);
-        peers[j] = 0u;
-        dr[j] = 0xffffffffu;
-        if (ok) {
-            const int d = (int)((k[j] >> shift) & 0xff);
-            dr[j] = (uint32_t)d << 16;
-            peers[j] = __match_any_sync(active, d);
-        }
+        const bool ok = wbase + j * 32 + lane < n;
+        const unsigned d = ok ? (unsigned)((k[j] >> shift) & 0xff) : 256u + lane;
+        dr[j] = ok ? d << 16 : 0xffffffffu;
+        const unsigned pm = digit_peers<9>(d);   // all lanes vote (full mask)
+        peers[j] = ok ? pm : 0u;
     }
 #pragma unroll
     for (int j = 0; j < kItems; j++) {
