@@ -180,15 +180,16 @@ pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
     // decoupled look-back for this digit
     uint32_t prefix = 0;
     if (bid > 0) {
-        // walk back 8 tiles per round trip; stop at the first not-ready entry
+        // walk back 16 tiles per round trip (independent loads in flight);
+        // stop at the first not-ready entry and re-poll from there
         int j = bid - 1;
         bool done = false;
         while (!done) {
-            uint32_t sv[8];
+            uint32_t sv[16];
 #pragma unroll
-            for (int q = 0; q < 8; q++) sv[q] = j - q >= 0 ? st[(size_t)(j - q) * 256 + d] : (uint32_t)(2u << 30);
+            for (int q = 0; q < 16; q++) sv[q] = j - q >= 0 ? st[(size_t)(j - q) * 256 + d] : (uint32_t)(2u << 30);
             int q = 0;
-            for (; q < 8; q++) {
+            for (; q < 16; q++) {
                 if ((sv[q] & (kFlagAgg | kFlagInc)) == 0) break;
                 prefix += sv[q] & kValMask;
                 if (sv[q] & kFlagInc) { done = true; break; }
