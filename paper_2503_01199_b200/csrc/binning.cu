@@ -67,11 +67,16 @@ hit_scan_kernel(const RasterRec* __restrict__ recs, const uint32_t* __restrict__
     }
     if (lane == 31) s_warp[warp] = x;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
         uint32_t run = 0;
-        for (int w = 0; w < kScanT / 32; w++) { const uint32_t t = s_warp[w]; s_warp[w] = run; run += t; }
-        s_prefix = sb_lookback_exclusive(status, bid, run);
-        if (bid == (int)gridDim.x - 1) *total = (int32_t)(s_prefix + run);
+        for (int w = 0; w < kScanT / 32; w++) run += s_warp[w];
+        const uint32_t pre = sb_lookback_warp(status, bid, run);
+        if (lane == 0) {
+            uint32_t r2 = 0;
+            for (int w = 0; w < kScanT / 32; w++) { const uint32_t t = s_warp[w]; s_warp[w] = r2; r2 += t; }
+            s_prefix = pre;
+            if (bid == (int)gridDim.x - 1) *total = (int32_t)(pre + run);
+        }
     }
     __syncthreads();
     uint32_t run = s_prefix + s_warp[warp] + x - sum;

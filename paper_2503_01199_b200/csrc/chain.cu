@@ -23,7 +23,7 @@ SB_INLINE void rotmat_grad_to_quat(const double d[3][3], const double q[4], doub
                     y * d[1][2]) + x * d[2][0]) + y * d[2][1]);
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t* __restrict__ cluster_offset,
              const sb_screen_grad* __restrict__ sg, float4* __restrict__ grads, double* __restrict__ stat_S,
              double* __restrict__ stat_M, int32_t* __restrict__ stat_C)
@@ -136,53 +136,48 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
 }
 
 // optim.py:69-98: rows of true-masked clusters, per-row step counters.
-// Per row the bias corrections are formed in float64 (beta^t = exp2(t *
-// log2 beta)) and folded into two scalars per channel; the per-element
-// moment and parameter updates run in float32 on the float32 state.
+// Four threads per row, one 16-byte column chunk each (full occupancy, four
+// independent 128-bit loads per thread).  Per row the bias corrections are
+// formed in float64 (beta^t = exp2(t log2 beta)) and folded into two scalars
+// per channel; the moment and parameter updates run in float32 on the
+// float32 state.
 __global__ void __launch_bounds__(256)
 adam_kernel(float4* __restrict__ params, const float4* __restrict__ grads, float4* __restrict__ m,
             float4* __restrict__ v, int32_t* __restrict__ step, const uint8_t* __restrict__ cluster_mask, int n,
             double lr0, double lr1, double lr2, double lr3, double lr4)
 {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int g = tid >> 2, kq = tid & 3;
     if (g >= n || !cluster_mask[g / SB_CLUSTER_SIZE]) return;
+    const size_t i = (size_t)g * 4 + kq;
+    float4 P = params[i], M = m[i], V = v[i];
+    const float4 Gr = __ldg(grads + i);
     const int s = step[g] + 1;
-    step[g] = s;
+    if (kq == 0) step[g] = s;
     const double t = (double)s;
     const double bc1 = 1.0 - exp2(t * -0.15200309344504997);    // log2(0.9)
     const double bc2 = 1.0 - exp2(t * -0.0014434168696687937);  // log2(0.999)
     // p -= lr * (m / bc1) / (sqrt(v / bc2) + eps) = a * m / (sqrt(v) * b + eps)
     const float b = (float)(1.0 / sqrt(bc2));
     const double inv1 = 1.0 / bc1;
-    const float a[5] = {(float)(lr0 * inv1), (float)(lr1 * inv1), (float)(lr2 * inv1), (float)(lr3 * inv1),
-                        (float)(lr4 * inv1)};
-    const int col_ch[16] = {0, 0, 0, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, -1, -1};
-    float4 P[4], G[4], M[4], V[4];
+    const float a0 = (float)(lr0 * inv1), a1 = (float)(lr1 * inv1), a2 = (float)(lr2 * inv1);
+    const float a3 = (float)(lr3 * inv1), a4 = (float)(lr4 * inv1);
+    float* pp = &P.x; const float* gg = &Gr.x; float* mm = &M.x; float* vv = &V.x;
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const size_t i = (size_t)g * 4 + k;
-        P[k] = params[i]; G[k] = __ldg(grads + i); M[k] = m[i]; V[k] = v[i];
+    for (int e = 0; e < 4; e++) {
+        // column -> channel: position 0-2, log_scale 3-5, rotation 6-9,
+        // colour 10-12, opacity 13, padding 14-15
+        const int col = 4 * kq + e;
+        if (col >= 14) continue;
+        const float a = col < 3 ? a0 : col < 6 ? a1 : col < 10 ? a2 : col < 13 ? a3 : a4;
+        const float gr = gg[e];
+        const float mn = 0.9f * mm[e] + 0.1f * gr;
+        const float vn = 0.999f * vv[e] + 0.001f * gr * gr;
+        pp[e] -= a * mn / (sqrtf(vn) * b + 1e-15f);
+        mm[e] = mn;
+        vv[e] = vn;
     }
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        float* pp = &P[k].x; const float* gg = &G[k].x; float* mm = &M[k].x; float* vv = &V[k].x;
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-            const int col = 4 * k + e;
-            if (col_ch[col] < 0) continue;
-            const float gr = gg[e];
-            const float mn = 0.9f * mm[e] + 0.1f * gr;
-            const float vn = 0.999f * vv[e] + 0.001f * gr * gr;
-            pp[e] -= a[col_ch[col]] * mn / (sqrtf(vn) * b + 1e-15f);
-            mm[e] = mn;
-            vv[e] = vn;
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const size_t i = (size_t)g * 4 + k;
-        params[i] = P[k]; m[i] = M[k]; v[i] = V[k];
-    }
+    params[i] = P; m[i] = M; v[i] = V;
 }
 
 // densify.py:57-63
@@ -210,7 +205,7 @@ void sb_launch_adam(float* params, const float* grads, float* m, float* v, int32
                     int n, const double lr5[5], cudaStream_t stream)
 {
     if (n <= 0) return;
-    adam_kernel<<<(n + 255) / 256, 256, 0, stream>>>(
+    adam_kernel<<<(4 * n + 255) / 256, 256, 0, stream>>>(
         reinterpret_cast<float4*>(params), reinterpret_cast<const float4*>(grads), reinterpret_cast<float4*>(m),
         reinterpret_cast<float4*>(v), step, mask, n, lr5[0], lr5[1], lr5[2], lr5[3], lr5[4]);
 }

@@ -128,10 +128,11 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
     }
     if (lane == 0) s_warp_vis[warp] = vis ? 1u : 0u;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
         uint32_t agg = 0;
         for (int w = 0; w < kWarps; w++) agg += s_warp_vis[w];
-        s_prefix = sb_lookback_exclusive(status, bid, agg);
+        const uint32_t pre = sb_lookback_warp(status, bid, agg);
+        if (lane == 0) s_prefix = pre;
     }
     __syncthreads();
     if (cl >= n_clusters) return;
