@@ -100,7 +100,8 @@ int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, cons
 
 /* forward.py:161-191 + 240-255: color (H,W,3), transmittance (H,W),
  * frag_count (H,W) and last[(H,W)] = 1 + list position of each pixel's last
- * contributing fragment (consumed by the backward). */
+ * contributing fragment (consumed by the backward).  cfg->half_state = 1
+ * selects the fp16 blending-state path (forward.py:194-230, half=True). */
 size_t sb_raster_workspace_bytes(void);
 int sb_raster_fwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
                   const sb_raster_cfg* cfg, float* color, float* transmittance, int32_t* frag_count, int32_t* last,

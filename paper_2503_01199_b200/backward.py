@@ -116,10 +116,22 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
     cfg_s = ctx.config.struct()
     stream = C.c_void_p(_lib.stream_ptr(dev))
     nc = max(ctx.n_compact, 1)
+    T_final, last = ctx.transmittance, ctx.last
+    if ctx.half:
+        # the reference's backward replays in float32 regardless of the
+        # forward's blending precision: recover float32 T_final / last
+        T_final = torch.empty_like(ctx.transmittance)
+        last = torch.empty_like(ctx.last)
+        scratch = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+        frags = torch.empty_like(ctx.last)
+        ws_f = _lib.workspace("raster_fwd", _lib.load().sb_raster_workspace_bytes(), dev)
+        _lib.call("sb_raster_fwd", _lib.ptr(ctx.recs), _lib.ptr(ctx.tile_offsets), _lib.ptr(ctx.tile_prims),
+                  C.byref(cam_s), C.byref(cfg_s), _lib.ptr(scratch), _lib.ptr(T_final), _lib.ptr(frags),
+                  _lib.ptr(last), _lib.ptr(ws_f), ws_f.numel(), stream)
     sgrad = _lib.workspace("sgrad", nc * SGRAD_BYTES, dev)
     ws_r = _lib.workspace("raster_bwd", _lib.load().sb_raster_workspace_bytes(), dev)
     _lib.call("sb_raster_bwd", _lib.ptr(ctx.recs), _lib.ptr(ctx.tile_offsets), _lib.ptr(ctx.tile_prims),
-              C.byref(cam_s), C.byref(cfg_s), _lib.ptr(dI), _lib.ptr(ctx.transmittance), _lib.ptr(ctx.last),
+              C.byref(cam_s), C.byref(cfg_s), _lib.ptr(dI), _lib.ptr(T_final), _lib.ptr(last),
               _lib.ptr(sgrad), ctx.n_compact, _lib.ptr(ws_r), ws_r.numel(), stream)
     grads = torch.empty((n, 16), dtype=torch.float32, device=dev)
     _lib.call("sb_chain_projection_bwd", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s),

@@ -183,7 +183,6 @@ int sb_raster_fwd(const void* recs, const int32_t* tile_offsets, const int32_t* 
                   void* ws, size_t ws_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
-    if (cfg->half_state) return fail(SB_EINVAL, "half_state forward is not built in this version");
     if (ws_bytes < sb_raster_workspace_bytes()) return fail(SB_EWORKSPACE, "raster workspace too small");
     const CamDev d = make_cam(cam, cfg);
     cudaMemsetAsync(ws, 0, sizeof(int), S(stream));

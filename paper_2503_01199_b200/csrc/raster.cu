@@ -32,6 +32,7 @@
 // Scheduling: warps pull tiles from an atomic counter (persistent grid), and
 // the 48-byte records of the next 32 list entries are fetched into registers
 // while the current 32 are consumed from a warp-private shared-memory slab.
+#include <cuda_fp16.h>
 #include "common.cuh"
 
 namespace {
@@ -193,6 +194,87 @@ raster_fwd_kernel(FwdParams p)
             p.out_color[3 * pix + 1] = FADD(rgb[i][1], FMUL(T[i], p.bg[1]));
             p.out_color[3 * pix + 2] = FADD(rgb[i][2], FMUL(T[i], p.bg[2]));
             p.out_T[pix] = T[i];
+            p.out_frags[pix] = frags[i];
+            p.out_last[pix] = last[i];
+        }
+    }
+}
+
+// forward.py:194-230 (half_path_blend): the exponent and G in float32 (the
+// shared lane_G), then G, opacity, colour, alpha, T and every accumulation
+// in IEEE binary16 (__half ops round once per op, like numpy's float16).
+__global__ void __launch_bounds__(kThreads)
+raster_fwd_half_kernel(FwdParams p)
+{
+    __shared__ SRec slabs[kWarpsPerBlock][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    SRec* slab = slabs[warp];
+    const __half amin = __float2half_rn(p.amin), amax = __float2half_rn(p.amax), tstop = __float2half_rn(p.tstop);
+    const __half one = __float2half_rn(1.0f), zero = __float2half_rn(0.0f);
+    for (int t = next_tile(p.tile_counter, lane); t < p.ntiles; t = next_tile(p.tile_counter, lane)) {
+        const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
+        const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
+        const float px = (float)pxi, py0 = (float)py0i;
+        bool valid[4];
+        __half T[4], rgb[4][3];
+        int frags[4], last[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            valid[i] = pxi < p.W && py0i + i < p.H;
+            T[i] = one;
+            rgb[i][0] = rgb[i][1] = rgb[i][2] = zero;
+            frags[i] = 0;
+            last[i] = 0;
+        }
+        const int beg = p.offsets[t], n = p.offsets[t + 1] - beg;
+        Prefetch pf;
+        if (n > 0) prefetch_chunk(pf, p.recs, p.prims, beg, 0, min(32, n), lane);
+        bool done = false;
+        for (int k0 = 0; k0 < n && !done; k0 += 32) {
+            const int cnt = min(32, n - k0);
+            __syncwarp();
+            commit_chunk(slab, pf, cnt, lane);
+            __syncwarp();
+            if (k0 + 32 < n) prefetch_chunk(pf, p.recs, p.prims, beg, k0 + 32, min(32, n - k0 - 32), lane);
+            for (int j = 0; j < cnt; j++) {
+                bool live = false;
+#pragma unroll
+                for (int i = 0; i < 4; i++) live |= valid[i] && __hge(T[i], tstop);
+                if (!__any_sync(0xffffffffu, live)) {
+                    done = true;
+                    break;
+                }
+                if (!live) continue;
+                const SRec r = slab[j];
+                float G[4], dx, dy;
+                lane_G(r, px, py0, G, dx, dy);
+                const __half o = __float2half_rn(r.o);
+                const __half c[3] = {__float2half_rn(r.r), __float2half_rn(r.g), __float2half_rn(r.bl)};
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    __half alpha = __hmul(o, __float2half_rn(G[i]));
+                    if (__hgt(alpha, amax)) alpha = amax;
+                    if (valid[i] && __hge(T[i], tstop) && __hge(alpha, amin)) {
+                        const __half w = __hmul(T[i], alpha);
+                        rgb[i][0] = __hadd(rgb[i][0], __hmul(w, c[0]));
+                        rgb[i][1] = __hadd(rgb[i][1], __hmul(w, c[1]));
+                        rgb[i][2] = __hadd(rgb[i][2], __hmul(w, c[2]));
+                        T[i] = __hmul(T[i], __hsub(one, alpha));
+                        frags[i]++;
+                        last[i] = k0 + j + 1;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            if (!valid[i]) continue;
+            const size_t pix = (size_t)(py0i + i) * p.W + pxi;
+#pragma unroll
+            for (int ch = 0; ch < 3; ch++)
+                p.out_color[3 * pix + ch] =
+                    __half2float(__hadd(rgb[i][ch], __hmul(T[i], __float2half_rn(p.bg[ch]))));
+            p.out_T[pix] = __half2float(T[i]);
             p.out_frags[pix] = frags[i];
             p.out_last[pix] = last[i];
         }
@@ -501,7 +583,9 @@ void sb_launch_raster_fwd(const RasterRec* recs, const int32_t* offsets, const i
     p.out_color = color; p.out_T = T; p.out_frags = frags; p.out_last = last;
     const int want = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const int blocks = min(want, sm_count() * 8);
-    if (blocks) raster_fwd_kernel<<<blocks, kThreads, 0, stream>>>(p);
+    if (!blocks) return;
+    if (cfg.half_state) raster_fwd_half_kernel<<<blocks, kThreads, 0, stream>>>(p);
+    else raster_fwd_kernel<<<blocks, kThreads, 0, stream>>>(p);
 }
 
 void sb_launch_raster_bwd(const RasterRec* recs, const int32_t* offsets, const int32_t* prims, int W, int H,

@@ -98,6 +98,7 @@ class RenderContext:
     transmittance: torch.Tensor   # (H, W)
     last: torch.Tensor            # (H, W) int32
     n_degenerate: int = 0
+    half: bool = False            # produced by the fp16 blending-state path
     _tiles: list | None = field(default=None, repr=False)
 
     @property
@@ -176,21 +177,21 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
                         n_compact=nc, n_pairs=P, visible_clusters=vis, culled_clusters=K - vis, recs=recs,
                         compact_map_full=cmap, cluster_offset=coff[:K], cluster_vis=cvis[:K],
                         tile_offsets=tile_offsets, tile_prims=prims[:P], transmittance=T, last=last,
-                        n_degenerate=ndeg)
+                        n_degenerate=ndeg, half=half)
     return out, ctx
 
 
 def forward(scene: SceneSoA, camera, config: RasterConfig | None = None, counter=None, half: bool = False):
     """Render `scene` from `camera`; returns (RenderOutput, RenderContext).
 
-    forward.py:258-304.  `counter` (the reference's CPU op tally) is not
+    forward.py:258-304.  half=True renders with fp16 blending state
+    (forward.py:194-230); the backward then replays in float32 as the
+    reference does.  `counter` (the reference's CPU op tally) is not
     applicable on the device and must be None; use ncu counters instead."""
     if counter is not None:
         raise ValueError("OpCounter instrumentation is CPU-only; profile the device path with ncu")
     config = config or RasterConfig()
     camera = CameraView.from_any(camera)
-    if half:
-        raise NotImplementedError("fp16 blending state (half_path_blend) is not built yet")
     return _launch_forward(scene, camera, config, half)
 
 

@@ -148,3 +148,19 @@ def test_morton_edge_cases():
     keys, perm = O.morton_perm(d["mort_pos"])
     assert np.array_equal(keys, d["mort_keys"])
     assert np.array_equal(perm, d["mort_perm"])
+
+
+@pytest.mark.parametrize("fname,prefix", G.CASES)
+def test_half_path_vs_reference(fname, prefix):
+    """forward.py:194-230: fp16 blending state; numpy's float16 ops round
+    once per op like the oracle's _Float16 casts (G comes from different
+    float32 exp implementations, so allow one binary16 ulp-scale slack)."""
+    d = G.load(fname)
+    sc, cam = G.scene(d, prefix), G.camera(d, prefix)
+    color, T, frags, _ = O.forward(sc, cam, G.raster_cfg(d, prefix), half=True)
+    assert np.abs(color - d[f"{prefix}fwdh_color"]).max() <= 2e-3
+    assert np.abs(T - d[f"{prefix}fwdh_T"]).max() <= 2e-3
+    assert (frags != d[f"{prefix}fwdh_frags"]).sum() <= 0.002 * frags.size + 2
+    ref32 = d[f"{prefix}fwd_color"].astype(np.float64)
+    mse = ((color.astype(np.float64) - ref32) ** 2).mean()
+    assert mse == 0 or 10 * np.log10(1 / mse) >= 58.0

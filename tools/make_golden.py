@@ -136,6 +136,11 @@ def full_case(prefix, sc, cam, cfg, target_seed, with_f64=True):
     d[f"{prefix}stat_C"] = stats.C.astype(np.int32)
     d[f"{prefix}score"] = variance_score(stats)
     d[f"{prefix}upd_mask"] = res.cluster_mask
+    # fp16 blending state (forward.py:194-230)
+    outh, _ = ts.forward(sc, cam, cfg, half=True)
+    d[f"{prefix}fwdh_color"] = outh.color
+    d[f"{prefix}fwdh_T"] = outh.transmittance
+    d[f"{prefix}fwdh_frags"] = outh.frag_count
     if with_f64:
         cfg64 = ts.RasterConfig(**{**cfg.__dict__, "dtype": "float64"})
         out64, ctx64 = ts.forward(sc, cam, cfg64)
@@ -236,6 +241,28 @@ def make_edge():
     lo, hi = p.min(0), p.max(0)
     d["mort_keys"] = ccc.morton_encode(p, lo, hi)
     d["mort_perm"] = np.argsort(d["mort_keys"], kind="stable").astype(np.int32)
+    # densification (densify.py:57-187): selection, growth, prune, re-sort
+    from tinysplat.densify import DensifyConfig, densify_step, select_and_grow
+    rng = np.random.default_rng(21)
+    nd = 2000
+    spd = SyntheticSceneSpec(n_gaussians=nd, n_views=1, view_resolution=(64, 64), seed=21)
+    scd = random_scene(spd)
+    scd.opacity_logit[:40] = -8.0          # prune candidates (sigmoid < 0.005)
+    scd.log_scale[80:] -= 1.6             # small primitives -> clone; 40:80 stay large -> split
+    scd = SceneSoA(*[getattr(scd, c).astype(np.float32).astype(np.float64) for c in CH])
+    std = DensifyStats(S=rng.uniform(0, 1, nd), M=rng.normal(0, 0.3, nd), C=rng.integers(0, 30, nd))
+    std.S[::17] = 0.0
+    std.attach(scd)
+    d.update({f"dens_in_{c}": getattr(scd, c).copy() for c in CH})
+    d["dens_S"], d["dens_M"], d["dens_C"] = std.S.copy(), std.M.copy(), std.C.copy()
+    cfgd = DensifyConfig(start_epoch=1, densify_interval_epochs=1, budget=2600)
+    scores = variance_score(std)
+    thr = cfgd.resolve_split_threshold(scd)
+    ci, si = select_and_grow(scd, scores, cfgd.budget, thr)
+    d["dens_clone"], d["dens_split"], d["dens_thr"] = ci, si, np.array(thr)
+    row = densify_step(scd, std, cfgd, epoch=1)
+    d.update({f"dens_out_{c}": getattr(scd, c).copy() for c in CH})
+    d["dens_row"] = np.array([row.n_before, row.n_after, row.n_split, row.n_clone, row.n_pruned])
     np.savez_compressed(os.path.join(OUT, "golden_edge.npz"), **d)
     print(f"golden_edge: {time.time() - t:.1f}s")
 
