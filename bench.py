@@ -102,13 +102,22 @@ class ClockSampler:
 
 
 def setup_dist():
+    """One process per GPU over NCCL.  If ranks outnumber the visible GPUs
+    (a functional check of the multi-rank path on a 1-GPU box), ranks share
+    devices and exchange over gloo instead -- never used for timing claims."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ndev = max(torch.cuda.device_count(), 1)
+        if ws <= ndev:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            local = local % ndev
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
     return ws, rank, local
 
 
@@ -133,35 +142,35 @@ class Trainer:
 
     def __init__(self, scene, state, views, ws, rank):
         import paper_2503_01199_b200 as sb
+        from paper_2503_01199_b200.parallel import ViewParallel
         self.sb = sb
         self.scene, self.state, self.views = scene, state, views
         self.ws, self.rank = ws, rank
+        self.vp = ViewParallel()
         self.lrs = sb.LearningRates().at(0.0, position_scale=3.2)
         self.stats_step = sb.DensifyStats.zeros(scene.n, scene.device)
 
+    def view_index(self, it):
+        return self.vp.views_for_step(it, len(self.views))[0]
+
     def step(self, it, target):
         sb = self.sb
-        cam = self.views[(it * self.ws + self.rank) % len(self.views)]
+        cam = self.views[self.view_index(it)]
         out, ctx = sb.forward(self.scene, cam)
         loss, dI = sb.loss_and_grad(out.color, target, 0.2, return_tensor=True)
-        stats = self.stats_step
         if self.ws > 1:
+            stats = self.stats_step
             stats.reset()
         else:
             stats = sb.DensifyStats.from_scene(self.scene)
         res = sb.backward(self.scene, ctx, dI, stats)
         mask = res.cluster_mask
         if self.ws > 1:
-            dist.all_reduce(res.grads.packed)
-            sm = torch.stack([stats.S, stats.M])
-            dist.all_reduce(sm)
-            dist.all_reduce(stats.C)
-            m8 = mask.to(torch.uint8)
-            dist.all_reduce(m8, op=dist.ReduceOp.MAX)
-            mask = m8.bool()
+            # sum grads / stats over the views of this step, OR masks
+            mask = self.vp.reduce(res.grads.packed, stats.S, stats.M, stats.C, mask)
             run = sb.DensifyStats.from_scene(self.scene)
-            run.S += sm[0]
-            run.M += sm[1]
+            run.S += stats.S
+            run.M += stats.M
             run.C += stats.C
         sb.adam_step(self.scene, res.grads, self.state, mask, self.lrs)
         return loss, ctx
@@ -280,7 +289,7 @@ def main():
     def run(k):
         for _ in range(k):
             i = it["i"]
-            trainer.step(i, targets_dev[(i * ws + rank) % N_VIEWS])
+            trainer.step(i, targets_dev[trainer.view_index(i)])
             it["i"] += 1
 
     run(args.warmup)
@@ -301,7 +310,7 @@ def main():
     def run_e2e(k):
         for _ in range(k):
             i = it["i"]
-            host = targets_host[(i * ws + rank) % N_VIEWS]
+            host = targets_host[trainer.view_index(i)]
             tgt = host.to(device, non_blocking=True).float().div_(255.0)
             loss, _ = trainer.step(i, tgt)
             losses.append(float(loss.item()))

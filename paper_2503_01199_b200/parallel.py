@@ -1,0 +1,55 @@
+"""View-sharded data parallelism across GPUs.
+
+The reference trains one view at a time (train.py:95-104) and has no
+distributed code.  Views are independent given replicated
+Gaussians, so each rank rasterises its own views; the only exchange per
+optimiser step is a SUM of the per-view results:
+
+  grads (N, 16) float32      ->  one float32 all-reduce
+  S, M (float64), C (int32),
+  cluster mask (K, uint8)    ->  one float64 all-reduce over [S | M | C | mask]
+                                 (C and the mask are exact in float64; the
+                                 mask is OR-ed as "sum > 0")
+
+followed by one identical cluster-sparse Adam step on every rank.  Multi-view
+semantics are SUM_v backward(scene, ctx_v, dI_v) plus summed statistics and
+OR-ed masks, then a single adam_step -- the SURVEY 8(e) definition.
+Works with any torch.distributed backend (NCCL over NVLink on the GPU box,
+gloo for the CPU tests).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+class ViewParallel:
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+
+    def views_for_step(self, step: int, n_views: int, views_per_rank: int = 1) -> list:
+        """Indices of the views this rank renders at `step` (round robin)."""
+        base = (step * self.world + self.rank) * views_per_rank
+        return [(base + j) % n_views for j in range(views_per_rank)]
+
+    def reduce(self, grads: torch.Tensor, S: torch.Tensor, M: torch.Tensor, C: torch.Tensor,
+               cluster_mask: torch.Tensor):
+        """In place: grads, S, M, C become the sums over ranks; returns the
+        OR-ed cluster mask (bool)."""
+        if self.world == 1:
+            return cluster_mask.bool()
+        n, k = S.numel(), cluster_mask.numel()
+        flat = torch.empty(2 * n + n + k, dtype=torch.float64, device=S.device)
+        flat[:n] = S
+        flat[n:2 * n] = M
+        flat[2 * n:3 * n] = C.to(torch.float64)
+        flat[3 * n:] = cluster_mask.to(torch.float64)
+        w1 = dist.all_reduce(grads, group=self.group, async_op=True)
+        dist.all_reduce(flat, group=self.group)
+        w1.wait()
+        S.copy_(flat[:n])
+        M.copy_(flat[n:2 * n])
+        C.copy_(flat[2 * n:3 * n].round().to(C.dtype))
+        return flat[3 * n:] > 0
