@@ -237,10 +237,11 @@ def cpu_baseline_oracle(sample_iters=1):
 def run_reference(args, ws, rank):
     if rank != 0:
         return
+    cores = os.cpu_count()
+    # torchrun pre-sets OMP_NUM_THREADS=1; the baseline uses every host thread
+    os.environ["OMP_NUM_THREADS"] = str(cores)
     from oracle import oracle as O
     O.build() if not os.path.exists(O.LIB_PATH) else None
-    cores = os.cpu_count()
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     w = min(args.warmup, 1)
     k = max(1, min(args.steps, 4))
     cpu_baseline_oracle(w) if w else None
@@ -350,6 +351,7 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
         try:
             t = cpu_baseline_oracle(1)
             cpu = {"value": 1.0 / t[0], "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",

@@ -122,18 +122,20 @@ emit_kernel(const RasterRec* __restrict__ recs, const uint32_t* __restrict__ ord
         int tx0, tx1, ty0, ty1;
         sb_tile_range(x, y, r, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
         int pos = off;
-        for (int ty = ty0; ty <= ty1; ty++)
-            for (int tx = tx0; tx <= tx1; tx++)
-                if (sb_disc_hits(x, y, r, tx, ty, W, H)) {
-                    const uint32_t t = (uint32_t)(ty * tiles_x + tx);
-                    if (staged) {
-                        stage[warp][pos - wbeg] = make_uint2(t, s);
-                    } else {
-                        tile_keys[pos] = t;
-                        slots[pos] = s;
-                    }
-                    pos++;
+        for (int ty = ty0; ty <= ty1; ty++) {
+            int a, b;
+            if (!sb_row_hits(x, y, r, ty, tx0, tx1, W, H, a, b)) continue;
+            for (int tx = a; tx <= b; tx++) {
+                const uint32_t t = (uint32_t)(ty * tiles_x + tx);
+                if (staged) {
+                    stage[warp][pos - wbeg] = make_uint2(t, s);
+                } else {
+                    tile_keys[pos] = t;
+                    slots[pos] = s;
                 }
+                pos++;
+            }
+        }
     }
     if (!staged) return;
     __syncwarp();

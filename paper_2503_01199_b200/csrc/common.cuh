@@ -91,10 +91,14 @@ struct ProjOut {
     bool valid, in_image, degenerate;
 };
 
-SB_INLINE void sb_project(const float* __restrict__ p, const CamDev& cam, ProjOut& o) {
+SB_INLINE void sb_project(const float* __restrict__ p, const CamDev& cam, ProjOut& o, double* s64 = nullptr) {
     // activations in float64, then rounded (projection.py:134-138)
     float pos[3] = {p[0], p[1], p[2]};
-    for (int k = 0; k < 3; k++) o.s[k] = (float)exp((double)p[SB_COL_LS + k]);
+    for (int k = 0; k < 3; k++) {
+        const double e = exp((double)p[SB_COL_LS + k]);
+        if (s64) s64[k] = e;
+        o.s[k] = (float)e;
+    }
     double q0 = p[SB_COL_ROT], q1 = p[SB_COL_ROT + 1], q2 = p[SB_COL_ROT + 2], q3 = p[SB_COL_ROT + 3];
     double qn = __dsqrt_rn(DADD(DADD(DADD(DMUL(q0, q0), DMUL(q1, q1)), DMUL(q2, q2)), DMUL(q3, q3)));
     o.q[0] = (float)DDIV(q0, qn);
@@ -190,6 +194,19 @@ SB_INLINE bool sb_disc_hits(float cx, float cy, float r, int tx, int ty, int W, 
     double dy = fmax(fmax(DSUB((double)ry0, dcy), DSUB(dcy, (double)ry1)), 0.0);
     float rr = FMUL(r, r);
     return DADD(DMUL(dx, dx), DMUL(dy, dy)) <= (double)rr;
+}
+
+// Hits of one tile row ty: the exact disc test is monotone in |dx| (the
+// float64 differences of an integer and a float32 are exact and rounding is
+// monotone), so the hit set in a row is one contiguous interval [*a, *b];
+// find it by scanning in from both ends.  Returns b - a + 1 (0 if empty).
+SB_INLINE int sb_row_hits(float cx, float cy, float r, int ty, int tx0, int tx1, int W, int H, int& a, int& b) {
+    a = tx0;
+    while (a <= tx1 && !sb_disc_hits(cx, cy, r, a, ty, W, H)) a++;
+    if (a > tx1) return 0;
+    b = tx1;
+    while (b > a && !sb_disc_hits(cx, cy, r, b, ty, W, H)) b--;
+    return b - a + 1;
 }
 
 // ---------------------------------------------------------------------------

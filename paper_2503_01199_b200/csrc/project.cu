@@ -33,7 +33,7 @@ SB_INLINE double warp_max_d(double v) {
     return v;
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
 project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clusters, CamDev cam,
                             int use_culling, RasterRec* __restrict__ rec_out, int32_t* __restrict__ compact_map,
                             int32_t* __restrict__ cluster_offset, uint8_t* __restrict__ cluster_vis,
@@ -72,16 +72,15 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
                     p[4 * k] = v.x; p[4 * k + 1] = v.y; p[4 * k + 2] = v.z; p[4 * k + 3] = v.w;
                 }
                 ProjOut o;
-                sb_project(p, cam, o);
+                double s64[3];
+                sb_project(p, cam, o, s64);
                 r.x = o.x; r.y = o.y; r.a = o.ca; r.b = o.cb; r.c = o.cc; r.o = o.op;
                 r.r = o.col[0]; r.g = o.col[1]; r.bl = o.col[2]; r.depth = o.depth; r.radius = o.radius;
                 uint32_t nhit = 0;
                 any_in |= o.in_image;
                 ndeg += o.degenerate ? 1 : 0;
                 // cluster AABB: p -+ 3 * max(exp(log_scale)) in float64 (ccc.py:125-130)
-                double m = exp((double)p[SB_COL_LS]);
-                m = fmax(m, exp((double)p[SB_COL_LS + 1]));
-                m = fmax(m, exp((double)p[SB_COL_LS + 2]));
+                const double m = fmax(fmax(s64[0], s64[1]), s64[2]);
                 const double reach = DMUL(3.0, m);
                 for (int k = 0; k < 3; k++) {
                     lo[k] = fmin(lo[k], DSUB((double)p[k], reach));
@@ -91,9 +90,10 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
                 if (o.in_image) {
                     int tx0, tx1, ty0, ty1;
                     sb_tile_range(o.x, o.y, o.radius, cam.tiles_x, cam.tiles_y, tx0, tx1, ty0, ty1);
-                    for (int ty = ty0; ty <= ty1; ty++)
-                        for (int tx = tx0; tx <= tx1; tx++)
-                            nhit += sb_disc_hits(o.x, o.y, o.radius, tx, ty, cam.W, cam.H) ? 1u : 0u;
+                    for (int ty = ty0; ty <= ty1; ty++) {
+                        int a, b;
+                        nhit += (uint32_t)sb_row_hits(o.x, o.y, o.radius, ty, tx0, tx1, cam.W, cam.H, a, b);
+                    }
                 }
                 // flags: bit0 valid, bit1 in_image, bits 2.. tile-hit count
                 r.flags = (o.valid ? 1u : 0u) | (o.in_image ? 2u : 0u) | (nhit << 2);

@@ -364,14 +364,10 @@ constexpr int kRows = kBatch * kCh;
 
 struct BwdWarpSmem {
     SRec slab[32];
-    float part[kRows * 32];        // row r holds lane l at ((l + 4 * (r & 7)) & 31)
+    float part[kRows * 32];        // row r = channel * kBatch + slot; lane l at ((l + 4 * (r & 7)) & 31)
     int slot[kBatch];
     int count[kBatch];
 };
-
-SB_INLINE void put_part(float* part, int row, int lane, float v) {
-    part[row * 32 + ((lane + 4 * (row & 7)) & 31)] = v;
-}
 
 // exact v * 2^s for float32 v with |v * 2^s| < 2^24 (power-of-two scaling is
 // exact unless the result is subnormal, and then |result| < 0.5 rounds to 0)
@@ -410,22 +406,15 @@ SB_INLINE float row_tree(float v[32]) {
     return v[0];
 }
 
-// rows of a batch: conic rows first (3 per fragment) so lanes of one
-// iteration take the same reduction path, then the 7 tree rows per fragment
-SB_INLINE int conic_row(int b, int c) { return b * 3 + c; }
-SB_INLINE int tree_row(int b, int c) { return kBatch * 3 + b * 7 + (c - 3); }
+// rows of a batch: row = channel * kBatch + slot, so the 3 conic channels
+// come first (lanes of one flush iteration take the same reduction path)
+// and all 10 stores of one fragment share the swizzle (row & 7) == slot.
+static_assert(kBatch == 8, "row swizzle assumes 8 slots");
 
 SB_INLINE void flush_batch(BwdWarpSmem& ws, int nb, int lane, int conic_tree, sb_screen_grad* grads) {
     __syncwarp();
-    const int n_conic = nb * 3;
-    for (int i = lane; i < n_conic + nb * 7; i += 32) {
-        int row, b, c;
-        if (i < n_conic) {
-            b = i / 3; c = i - 3 * b; row = conic_row(b, c);
-        } else {
-            const int t = i - n_conic;
-            b = t / 7; c = 3 + (t - 7 * b); row = tree_row(b, c);
-        }
+    for (int i = lane; i < nb * kCh; i += 32) {
+        const int c = i / nb, b = i - c * nb, row = c * kBatch + b;
         float v[32];
         const float* base = ws.part + row * 32;
 #pragma unroll
@@ -529,19 +518,17 @@ raster_bwd_kernel(BwdParams p)
                 const float gb = ((uG[0] + uG[1]) + uG[2]) + uG[3];
                 const float gl = (uG[1] + uG[2] * 2.0f) + uG[3] * 3.0f;
                 const float gq = (uG[1] + uG[2] * 4.0f) + uG[3] * 9.0f;
-                put_part(ws.part, conic_row(nb, 0), lane, gb * (-0.5f * dx * dx));
-                put_part(ws.part, conic_row(nb, 1), lane, gb * (-dx * dy) + gl * dx);
-                put_part(ws.part, conic_row(nb, 2), lane, (gb * (-0.5f * dy * dy) + gl * dy) + gq * -0.5f);
-                put_part(ws.part, tree_row(nb, 3), lane, gb * -(r.a * dx + r.b * dy) + gl * r.b);
-                put_part(ws.part, tree_row(nb, 4), lane, gb * -(r.b * dx + r.c * dy) + gl * r.c);
-                put_part(ws.part, tree_row(nb, 5), lane, ((f[0] + f[1]) + f[2]) + f[3]);
-                put_part(ws.part, tree_row(nb, 6), lane,
-                         ((w[0] * dI[0][0] + w[1] * dI[1][0]) + w[2] * dI[2][0]) + w[3] * dI[3][0]);
-                put_part(ws.part, tree_row(nb, 7), lane,
-                         ((w[0] * dI[0][1] + w[1] * dI[1][1]) + w[2] * dI[2][1]) + w[3] * dI[3][1]);
-                put_part(ws.part, tree_row(nb, 8), lane,
-                         ((w[0] * dI[0][2] + w[1] * dI[1][2]) + w[2] * dI[2][2]) + w[3] * dI[3][2]);
-                put_part(ws.part, tree_row(nb, 9), lane, ((f[0] * f[0] + f[1] * f[1]) + f[2] * f[2]) + f[3] * f[3]);
+                float* pp = ws.part + nb * 32 + ((lane + 4 * nb) & 31);   // channel c at pp[c * 256]
+                pp[0 * 256] = gb * (-0.5f * dx * dx);
+                pp[1 * 256] = gb * (-dx * dy) + gl * dx;
+                pp[2 * 256] = (gb * (-0.5f * dy * dy) + gl * dy) + gq * -0.5f;
+                pp[3 * 256] = gb * -(r.a * dx + r.b * dy) + gl * r.b;
+                pp[4 * 256] = gb * -(r.b * dx + r.c * dy) + gl * r.c;
+                pp[5 * 256] = ((f[0] + f[1]) + f[2]) + f[3];
+                pp[6 * 256] = ((w[0] * dI[0][0] + w[1] * dI[1][0]) + w[2] * dI[2][0]) + w[3] * dI[3][0];
+                pp[7 * 256] = ((w[0] * dI[0][1] + w[1] * dI[1][1]) + w[2] * dI[2][1]) + w[3] * dI[3][1];
+                pp[8 * 256] = ((w[0] * dI[0][2] + w[1] * dI[1][2]) + w[2] * dI[2][2]) + w[3] * dI[3][2];
+                pp[9 * 256] = ((f[0] * f[0] + f[1] * f[1]) + f[2] * f[2]) + f[3] * f[3];
                 const int C = __reduce_add_sync(0xffffffffu, cnt_l);
                 if (lane == 0) {
                     ws.slot[nb] = r.slot;
