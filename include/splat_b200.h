@@ -75,28 +75,32 @@ int sb_permute_rows(const uint32_t* perm, int64_t n, int count, const void* cons
  * Outputs: recs[N] (first N_c used; flags = valid | in_image << 1 |
  * tile_hits << 2), compact_map[N] (int32, first N_c used), cluster_offset[K]
  * (compact start of each visible cluster, -1 if culled), cluster_vis[K],
- * counters[4] (must be ZEROED): visible clusters, N_c, n_degenerate. */
+ * counters[4] (must be ZEROED): visible clusters, N_c, n_degenerate.
+ * Replaces project_scene + build_clusters + cull_clusters +
+ * cluster_visibility + compact_arrays (projection.py:130, ccc.py:112/134/149/171). */
 size_t sb_project_workspace_bytes(int64_t n);
 int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
                             void* recs, int32_t* compact_map, int32_t* cluster_offset, uint8_t* cluster_vis,
                             int32_t* counters, void* ws, size_t ws_bytes, sb_stream_t stream);
 
-/* tiles.py:50-107 binning, part 1: stable depth order of the compact
- * primitives (order[N_c]: compact slots) and the exclusive scan of their
- * tile-hit counts in that order (pair_offsets[N_c]); *n_pairs (device int)
- * receives P.  n_cap bounds N_c (read from counters[1] on the device). */
-size_t sb_bin_prepare_workspace_bytes(int64_t n_cap);
-int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, uint32_t* order,
-                   int32_t* pair_offsets, int32_t* n_pairs, void* ws, size_t ws_bytes, sb_stream_t stream);
+/* tiles.py:50-107 binning, part 1: enumerate the exact disc/rect hits
+ * (tiles.py:75-91), count them per tile and scan the counts ->
+ * tile_offsets[ntiles + 1]; *n_pairs (device int) receives P.  The per-row
+ * hit intervals are kept in `state` (sb_bin_state_workspace_bytes(n_cap)
+ * bytes, caller-owned) for part 2.  n_cap bounds N_c (read from counters[1]
+ * on the device). */
+size_t sb_bin_state_workspace_bytes(int64_t n_cap);
+int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam,
+                   int32_t* tile_offsets, int32_t* n_pairs, void* state, size_t state_bytes, sb_stream_t stream);
 
-/* tiles.py:50-107 binning, part 2 (P from part 1): emit (tile id, slot)
- * pairs in depth order, stable sort by tile id, per-tile ranges:
- * tile_offsets[ntiles + 1], tile_prims[P] (compact slots, per tile in
- * (depth, index) order == np.lexsort((prim, depth, tile_id))). */
+/* tiles.py:50-107 binning, part 2 (P from part 1, `state` as part 1 left
+ * it): scatter every hit into its tile's range, then sort each tile by
+ * (depth, compact slot): tile_prims[P] (compact slots, per tile in
+ * (depth, index) order == np.lexsort((prim, depth, tile_id)) of tiles.py:98). */
 size_t sb_bin_finish_workspace_bytes(int64_t n_pairs, int32_t ntiles);
-int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, const uint32_t* order,
-                  const int32_t* pair_offsets, const sb_camera* cam, int64_t n_pairs, int32_t* tile_offsets,
-                  int32_t* tile_prims, void* ws, size_t ws_bytes, sb_stream_t stream);
+int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam, int64_t n_pairs,
+                  const int32_t* tile_offsets, const void* state, int32_t* tile_prims, void* ws, size_t ws_bytes,
+                  sb_stream_t stream);
 
 /* forward.py:161-191 + 240-255: color (H,W,3), transmittance (H,W),
  * frag_count (H,W) and last[(H,W)] = 1 + list position of each pixel's last

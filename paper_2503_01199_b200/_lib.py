@@ -32,10 +32,10 @@ SIGNATURES = {
     "sb_permute_rows": ([VP, I64, C.c_int, VP, VP, VP, VP], C.c_int),
     "sb_project_workspace_bytes": ([I64], SZ),
     "sb_project_cull_compact": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
-    "sb_bin_prepare_workspace_bytes": ([I64], SZ),
+    "sb_bin_state_workspace_bytes": ([I64], SZ),
     "sb_bin_prepare": ([VP, VP, I64, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_bin_finish_workspace_bytes": ([I64, I32], SZ),
-    "sb_bin_finish": ([VP, VP, I64, VP, VP, VP, I64, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_bin_finish": ([VP, VP, I64, VP, I64, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_raster_workspace_bytes": ([], SZ),
     "sb_raster_fwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_raster_bwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, VP, SZ, VP], C.c_int),
@@ -107,8 +107,8 @@ def ptr(t: torch.Tensor | None):
 # kernel launches issued by each entry point (for bench.py's gpu_launches);
 # the radix sort issues 3 per 8-bit pass and is counted by the caller.
 KERNELS_PER_CALL = {
-    "sb_morton_keys": 3, "sb_permute_rows": 1, "sb_project_cull_compact": 1, "sb_bin_prepare": 8,
-    "sb_bin_finish": 6, "sb_raster_fwd": 1, "sb_raster_bwd": 1, "sb_radix_sort_pairs_u64": 10,
+    "sb_morton_keys": 3, "sb_permute_rows": 1, "sb_project_cull_compact": 1, "sb_bin_prepare": 2,
+    "sb_bin_finish": 2, "sb_raster_fwd": 1, "sb_raster_bwd": 1, "sb_radix_sort_pairs_u64": 10,
     "sb_chain_projection_bwd": 1, "sb_adam_sparse": 1, "sb_variance_score": 1, "sb_lane_reduce": 1,
     "sb_loss_fwd_bwd": 2,
 }

@@ -9,11 +9,12 @@
 void sb_launch_project_cull_compact(const float*, int, const CamDev&, int, RasterRec*, int32_t*, int32_t*, uint8_t*,
                                     int32_t*, unsigned long long*, unsigned int*, cudaStream_t);
 int sb_project_blocks(int n);
-size_t sb_bin_prepare_ws(int n_cap);
-void sb_launch_bin_prepare(const RasterRec*, const int32_t*, int, uint32_t*, int32_t*, int32_t*, void*, cudaStream_t);
+size_t sb_bin_state_bytes(int n_cap);
+void sb_launch_bin_prepare(const RasterRec*, const int32_t*, int, const CamDev&, int32_t*, int32_t*, void*,
+                           cudaStream_t);
 size_t sb_bin_finish_ws(long long n_pairs, int ntiles);
-void sb_launch_bin_finish(const RasterRec*, const int32_t*, int, const uint32_t*, const int32_t*, const CamDev&, int,
-                          int32_t*, int32_t*, void*, cudaStream_t);
+void sb_launch_bin_finish(const RasterRec*, const int32_t*, int, const CamDev&, int, const int32_t*, const void*,
+                          int32_t*, void*, cudaStream_t);
 size_t sb_sort_u64_ws(int n, int bits);
 int sb_launch_sort_u64(unsigned long long*, uint32_t*, unsigned long long*, uint32_t*, int, int, void*, cudaStream_t);
 void sb_launch_raster_fwd(const RasterRec*, const int32_t*, const int32_t*, int, int, int, int, const sb_raster_cfg&,
@@ -148,13 +149,16 @@ int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam
     return check_launch("sb_project_cull_compact");
 }
 
-size_t sb_bin_prepare_workspace_bytes(int64_t n_cap) { return sb_bin_prepare_ws((int)n_cap) + 256; }
+size_t sb_bin_state_workspace_bytes(int64_t n_cap) { return sb_bin_state_bytes((int)n_cap) + 256; }
 
-int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, uint32_t* order,
-                   int32_t* pair_offsets, int32_t* n_pairs, void* ws, size_t ws_bytes, sb_stream_t stream) {
+int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam,
+                   int32_t* tile_offsets, int32_t* n_pairs, void* state, size_t state_bytes, sb_stream_t stream) {
+    if (int r = check_cam(cam)) return r;
     if (n_cap < 0 || n_cap > INT32_MAX / 2) return fail(SB_EINVAL, "n_cap out of range");
-    if (ws_bytes < sb_bin_prepare_workspace_bytes(n_cap)) return fail(SB_EWORKSPACE, "bin prepare workspace too small");
-    sb_launch_bin_prepare(static_cast<const RasterRec*>(recs), counters, (int)n_cap, order, pair_offsets, n_pairs, ws,
+    if (!tile_offsets || !n_pairs) return fail(SB_EINVAL, "NULL buffer");
+    if (state_bytes < sb_bin_state_workspace_bytes(n_cap)) return fail(SB_EWORKSPACE, "bin state too small");
+    const CamDev d = make_cam(cam, nullptr);
+    sb_launch_bin_prepare(static_cast<const RasterRec*>(recs), counters, (int)n_cap, d, tile_offsets, n_pairs, state,
                           S(stream));
     return check_launch("sb_bin_prepare");
 }
@@ -163,16 +167,17 @@ size_t sb_bin_finish_workspace_bytes(int64_t n_pairs, int32_t ntiles) {
     return sb_bin_finish_ws((long long)n_pairs, ntiles) + 256;
 }
 
-int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, const uint32_t* order,
-                  const int32_t* pair_offsets, const sb_camera* cam, int64_t n_pairs, int32_t* tile_offsets,
-                  int32_t* tile_prims, void* ws, size_t ws_bytes, sb_stream_t stream) {
+int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam, int64_t n_pairs,
+                  const int32_t* tile_offsets, const void* state, int32_t* tile_prims, void* ws, size_t ws_bytes,
+                  sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (n_pairs < 0 || n_pairs > INT32_MAX / 2) return fail(SB_EINVAL, "n_pairs out of range");
+    if (n_cap < 0 || n_cap > INT32_MAX / 2) return fail(SB_EINVAL, "n_cap out of range");
     const CamDev d = make_cam(cam, nullptr);
     if (ws_bytes < sb_bin_finish_workspace_bytes(n_pairs, d.tiles_x * d.tiles_y))
         return fail(SB_EWORKSPACE, "bin finish workspace too small");
-    sb_launch_bin_finish(static_cast<const RasterRec*>(recs), counters, (int)n_cap, order, pair_offsets, d,
-                         (int)n_pairs, tile_offsets, tile_prims, ws, S(stream));
+    sb_launch_bin_finish(static_cast<const RasterRec*>(recs), counters, (int)n_cap, d, (int)n_pairs, tile_offsets,
+                         state, tile_prims, ws, S(stream));
     return check_launch("sb_bin_finish");
 }
 

@@ -1,245 +1,495 @@
 // K6/K7: tile binning with the per-tile depth order (tiles.py:50-107).
 //
-// The reference builds (tile, depth, index) triples and lexsorts them.  Here:
-//   prepare  (1) sort the compact primitives by depth (32-bit float bits are
-//                order preserving for depth > near > 0) with the stable
-//                onesweep radix sort, values = compact slots in index order, so
-//                equal depths keep index order;
-//            (2) exclusive scan of the per-primitive tile-hit counts (from
-//                the fused projection kernel) in that depth order -> each
-//                primitive's output range and the pair count P;
-//   finish   (3) emit, in depth order, one (tile id, slot) pair per exact
-//                disc/rect hit (coalesced writes, no atomics);
-//            (4) stable onesweep sort of the pairs by tile id (2 passes at
-//                1080p): within a tile the depth order -- and the index
-//                tie-break -- of step (1) survive, which is exactly
-//                np.lexsort((prim, depth, tile_id));
-//            (5) per-tile [start, end) by binary search of the sorted ids.
-#include "onesweep.cuh"
+// The reference builds (tile, depth, index) triples for every exact
+// disc/rect hit and lexsorts them (tiles.py:94-106).  No global sort here:
+//
+//   prepare  (1) count: each CTA takes 256 consecutive compact slots (Morton
+//                order, so their footprints cluster on screen).  Each thread
+//                enumerates its primitive's exact hits once, row by row
+//                (tiles.py:75-91; float32-filtered float64 disc test), and
+//                stores the per-row hit intervals ("spans", 16 rows x 2 bytes
+//                relative to the bounding tile rectangle).  The CTA counts
+//                the hits per tile in a shared-memory window over its tile
+//                bounding box with two atomics per span (row difference
+//                array, then a row prefix sum) and adds each touched tile's
+//                count to the global counts once;
+//            (2) one CTA: exclusive scan of the counts -> tile_offsets and P;
+//   finish   (1) scatter: the same CTAs rebuild their window counts from the
+//                stored spans, reserve each touched tile's sub-range with ONE
+//                global atomic, and place their 64-bit keys (depth bits << 32
+//                | compact slot) through shared-memory cursors (order inside
+//                a tile is arbitrary at this point);
+//            (2) per-tile sort, one CTA per tile, in shared memory: keys are
+//                distributed over up to 1024 buckets by a monotone map of the
+//                key (float-rounded offset from the tile's minimum), and each
+//                key's final position is its bucket start plus the number of
+//                smaller keys in its bucket.  Lists longer than the shared
+//                capacity sort capacity-sized chunks and merge them in global
+//                scratch (merge position by binary search).
+// Primitives whose bounding rectangle exceeds the span format (more than 16
+// tile rows or 255 tile columns), and CTAs whose window exceeds the shared
+// counters, take a direct path (re-enumeration, one global atomic per hit).
+//
+// Depth > near > 0, so the float32 bit pattern orders depths; ties fall
+// back to the compact slot.  The result is exactly np.lexsort((prim, depth,
+// tile_id)) restricted to each tile.
+#include "common.cuh"
 
 namespace {
 
-__global__ void __launch_bounds__(256)
-depth_keys_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ counters, int n_cap,
-                  uint32_t* __restrict__ keys)
-{
-    const int nc = min(counters[1], n_cap);
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= nc) return;
-    const float4 c = __ldg(reinterpret_cast<const float4*>(recs + s) + 2);
-    const uint32_t flags = __float_as_uint(c.w);
-    // primitives without hits sort last (their position is irrelevant)
-    keys[s] = (flags & 2u) ? __float_as_uint(c.y) : 0xffffffffu;
+constexpr int kBinThreads = 256;
+constexpr int kWin = 6144;          // shared-memory tile counters per CTA
+constexpr int kSpanRows = 16;       // rows per primitive in the span format
+constexpr uint32_t kEmptySpan = 0x00ffu;   // a > b
+
+struct WinSmem {
+    int32_t cnt[kWin];              // (w + 1) x h row-difference / count / cursor window
+    uint16_t span[kBinThreads][kSpanRows];
+    int x0, y0, w, h;
+    int red[4][kBinThreads / 32];
+};
+
+struct Prim {
+    float x, y, r;
+    int tx0, tx1, ty0, ty1;
+    unsigned long long key;
+    bool hit;       // has a non-empty tile rectangle
+    bool spans;     // fits the span format
+};
+
+SB_INLINE Prim load_prim(const RasterRec* __restrict__ recs, int s, int nc, int tiles_x, int tiles_y) {
+    Prim q;
+    q.hit = q.spans = false;
+    q.tx0 = q.ty0 = 0x7fffffff;
+    q.tx1 = q.ty1 = -1;
+    if (s < nc) {
+        const float4* r4 = reinterpret_cast<const float4*>(recs + s);
+        const float4 c = __ldg(r4 + 2);
+        const uint32_t flags = __float_as_uint(c.w);
+        if (flags & 2u) {   // in_image: the only fragment-generating primitives (forward.py:279)
+            const float4 a = __ldg(r4);
+            q.x = a.x; q.y = a.y; q.r = c.z;
+            q.key = ((unsigned long long)__float_as_uint(c.y) << 32) | (uint32_t)s;
+            sb_tile_range(q.x, q.y, q.r, tiles_x, tiles_y, q.tx0, q.tx1, q.ty0, q.ty1);
+            q.hit = true;
+            q.spans = (q.ty1 - q.ty0 < kSpanRows) && (q.tx1 - q.tx0 < 255);
+        }
+    }
+    return q;
 }
 
-// single-pass exclusive scan of nhit[order[i]] with decoupled look-back
-constexpr int kScanT = 256, kScanItems = 8, kScanTile = kScanT * kScanItems;
-
-__global__ void __launch_bounds__(kScanT)
-hit_scan_kernel(const RasterRec* __restrict__ recs, const uint32_t* __restrict__ order,
-                const int32_t* __restrict__ counters, int n_cap, int32_t* __restrict__ offsets,
-                int32_t* __restrict__ total, unsigned long long* __restrict__ status, unsigned* __restrict__ ticket)
-{
-    __shared__ int s_bid;
-    __shared__ uint32_t s_warp[kScanT / 32];
-    __shared__ uint32_t s_prefix;
-    if (threadIdx.x == 0) s_bid = (int)atomicAdd(ticket, 1u);
-    __syncthreads();
-    const int bid = s_bid;
-    const int nc = min(counters[1], n_cap);
-    const int base = bid * kScanTile + threadIdx.x * kScanItems;
-    uint32_t v[kScanItems], sum = 0;
-#pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
-        v[j] = 0;
-        if (base + j < nc) {
-            const uint32_t slot = order[base + j];
-            const uint32_t flags = __float_as_uint(__ldg(reinterpret_cast<const float*>(recs + slot) + 11));
-            v[j] = flags >> 2;
-        }
-        sum += v[j];
-    }
+// CTA tile window = bounding box of the span-format primitives' rectangles;
+// returns true when its (w + 1) x h difference array fits (and is zeroed)
+SB_INLINE bool setup_window(WinSmem& sm, const Prim& q) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = sum;
+    int v[4] = {0x7fffffff, 1, 0x7fffffff, 1};
+    if (q.spans) { v[0] = q.tx0; v[1] = -q.tx1; v[2] = q.ty0; v[3] = -q.ty1; }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        v[k] = __reduce_min_sync(0xffffffffu, v[k]);
+        if (lane == 0) sm.red[k][warp] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int m[4];
+        for (int k = 0; k < 4; k++) {
+            m[k] = sm.red[k][0];
+            for (int w = 1; w < kBinThreads / 32; w++) m[k] = min(m[k], sm.red[k][w]);
+        }
+        sm.x0 = m[0]; sm.w = -m[1] - m[0] + 1;
+        sm.y0 = m[2]; sm.h = -m[3] - m[2] + 1;
+        if (sm.w <= 0 || sm.h <= 0) sm.w = sm.h = 0;
+    }
+    __syncthreads();
+    const int area = (sm.w + 1) * sm.h;
+    const bool fits = area <= kWin;
+    if (fits)
+        for (int i = threadIdx.x; i < area; i += kBinThreads) sm.cnt[i] = 0;
+    __syncthreads();
+    return fits;
+}
+
+// row difference of this thread's spans into the window: +1 at a, -1 past b
+SB_INLINE void window_add_spans(WinSmem& sm, const Prim& q) {
+    const int ww = sm.w + 1;
+    for (int k = 0; k <= q.ty1 - q.ty0; k++) {
+        const uint32_t sp = sm.span[threadIdx.x][k];
+        const int a = sp & 0xff, b = sp >> 8;
+        if (a > b) continue;
+        int32_t* row = sm.cnt + (q.ty0 + k - sm.y0) * ww + (q.tx0 - sm.x0);
+        atomicAdd(row + a, 1);
+        atomicAdd(row + b + 1, -1);
+    }
+}
+
+// window rows: difference array -> per-tile counts (inclusive prefix, one
+// warp per row), then f(count, tile id, cell) for every window tile
+template <typename F>
+SB_INLINE void window_counts(WinSmem& sm, int tiles_x, F&& f) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ww = sm.w + 1;
+    for (int row = warp; row < sm.h; row += kBinThreads / 32) {
+        int carry = 0;
+        for (int c0 = 0; c0 < sm.w; c0 += 32) {
+            const int c = c0 + lane;
+            int v = c < sm.w ? sm.cnt[row * ww + c] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += y;
+            }
+            v += carry;
+            carry = __shfl_sync(0xffffffffu, v, 31);
+            if (c < sm.w) f(v, (sm.y0 + row) * tiles_x + sm.x0 + c, sm.cnt[row * ww + c]);
+        }
+    }
+}
+
+// ---- prepare (1): spans + per-tile counts ------------------------------------
+__global__ void __launch_bounds__(kBinThreads)
+tile_count_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ counters, int n_cap, int tiles_x,
+                  int tiles_y, int W, int H, uint4* __restrict__ spans_out, int32_t* __restrict__ counts)
+{
+    __shared__ WinSmem sm;
+    const int nc = min(counters[1], n_cap);
+    const int s = blockIdx.x * kBinThreads + threadIdx.x;
+    if (blockIdx.x * kBinThreads >= nc) return;
+    const Prim q = load_prim(recs, s, nc, tiles_x, tiles_y);
+    if (q.spans) {
+        // tiles.py:75-91, one exact row interval per tile row
+        for (int k = 0; k <= q.ty1 - q.ty0; k++) {
+            int a, b;
+            const int n = sb_row_hits(q.x, q.y, q.r, q.ty0 + k, q.tx0, q.tx1, W, H, a, b);
+            sm.span[threadIdx.x][k] = n ? (uint16_t)((a - q.tx0) | ((b - q.tx0) << 8)) : (uint16_t)kEmptySpan;
+        }
+        for (int k = q.ty1 - q.ty0 + 1; k < kSpanRows; k++) sm.span[threadIdx.x][k] = (uint16_t)kEmptySpan;
+        const uint4* sp = reinterpret_cast<const uint4*>(sm.span[threadIdx.x]);
+        spans_out[2 * s] = sp[0];
+        spans_out[2 * s + 1] = sp[1];
+    } else if (q.hit) {
+        for (int ty = q.ty0; ty <= q.ty1; ty++) {
+            int a, b;
+            if (!sb_row_hits(q.x, q.y, q.r, ty, q.tx0, q.tx1, W, H, a, b)) continue;
+            for (int tx = a; tx <= b; tx++) atomicAdd(&counts[ty * tiles_x + tx], 1);
+        }
+    }
+    const bool fits = setup_window(sm, q);
+    if (fits) {
+        if (q.spans) window_add_spans(sm, q);
+        __syncthreads();
+        window_counts(sm, tiles_x, [&](int c, int t, int32_t&) {
+            if (c) atomicAdd(&counts[t], c);
+        });
+    } else if (q.spans) {
+        for (int k = 0; k <= q.ty1 - q.ty0; k++) {
+            const uint32_t sp = sm.span[threadIdx.x][k];
+            for (int tx = q.tx0 + (int)(sp & 0xff); tx <= q.tx0 + (int)(sp >> 8); tx++)
+                atomicAdd(&counts[(q.ty0 + k) * tiles_x + tx], 1);
+        }
+    }
+}
+
+// ---- prepare (2): counts -> exclusive offsets, in place ------------------------
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 16;   // per thread and round
+
+__global__ void __launch_bounds__(kScanThreads)
+tile_scan_kernel(int32_t* __restrict__ offsets, int ntiles, int32_t* __restrict__ n_pairs)
+{
+    __shared__ uint32_t s_warp[kScanThreads / 32];
+    __shared__ uint32_t s_carry;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int base = 0; base < ntiles; base += kScanThreads * kScanItems) {
+        // each thread: kScanItems consecutive counts (all loads in flight)
+        const int beg = base + threadIdx.x * kScanItems;
+        uint32_t v[kScanItems], sum = 0;
+#pragma unroll
+        for (int j = 0; j < kScanItems; j++) {
+            v[j] = beg + j < ntiles ? (uint32_t)offsets[beg + j] : 0u;
+            sum += v[j];
+        }
+        uint32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = s_warp[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            s_warp[lane] = w;   // inclusive over warps
+        }
+        __syncthreads();
+        uint32_t run = s_carry + (warp ? s_warp[warp - 1] : 0u) + x - sum;
+#pragma unroll
+        for (int j = 0; j < kScanItems; j++) {
+            if (beg + j < ntiles) offsets[beg + j] = (int32_t)run;
+            run += v[j];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += s_warp[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        offsets[ntiles] = (int32_t)s_carry;
+        *n_pairs = (int32_t)s_carry;
+    }
+}
+
+// ---- finish (1): scatter keys into tile ranges ------------------------------
+__global__ void __launch_bounds__(kBinThreads)
+scatter_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ counters, int n_cap, int tiles_x,
+               int tiles_y, int W, int H, const uint4* __restrict__ spans_in, int32_t* __restrict__ cursor,
+               unsigned long long* __restrict__ keys)
+{
+    __shared__ WinSmem sm;
+    const int nc = min(counters[1], n_cap);
+    const int s = blockIdx.x * kBinThreads + threadIdx.x;
+    if (blockIdx.x * kBinThreads >= nc) return;
+    const Prim q = load_prim(recs, s, nc, tiles_x, tiles_y);
+    if (q.spans) {
+        uint4* sp = reinterpret_cast<uint4*>(sm.span[threadIdx.x]);
+        sp[0] = spans_in[2 * s];
+        sp[1] = spans_in[2 * s + 1];
+    } else if (q.hit) {
+        for (int ty = q.ty0; ty <= q.ty1; ty++) {
+            int a, b;
+            if (!sb_row_hits(q.x, q.y, q.r, ty, q.tx0, q.tx1, W, H, a, b)) continue;
+            for (int tx = a; tx <= b; tx++) keys[atomicAdd(&cursor[ty * tiles_x + tx], 1)] = q.key;
+        }
+    }
+    const bool fits = setup_window(sm, q);
+    if (fits) {
+        if (q.spans) window_add_spans(sm, q);
+        __syncthreads();
+        // reserve each touched tile's sub-range: the cell becomes its cursor
+        window_counts(sm, tiles_x, [&](int c, int t, int32_t& cell) {
+            cell = c ? atomicAdd(&cursor[t], c) : 0;
+        });
+        __syncthreads();
+        if (q.spans) {
+            const int ww = sm.w + 1;
+            for (int k = 0; k <= q.ty1 - q.ty0; k++) {
+                const uint32_t sp = sm.span[threadIdx.x][k];
+                int32_t* row = sm.cnt + (q.ty0 + k - sm.y0) * ww + (q.tx0 - sm.x0);
+                for (int c = (int)(sp & 0xff); c <= (int)(sp >> 8); c++) keys[atomicAdd(row + c, 1)] = q.key;
+            }
+        }
+    } else if (q.spans) {
+        for (int k = 0; k <= q.ty1 - q.ty0; k++) {
+            const uint32_t sp = sm.span[threadIdx.x][k];
+            for (int tx = q.tx0 + (int)(sp & 0xff); tx <= q.tx0 + (int)(sp >> 8); tx++)
+                keys[atomicAdd(&cursor[(q.ty0 + k) * tiles_x + tx], 1)] = q.key;
+        }
+    }
+}
+
+// ---- finish (2): per-tile sort, one CTA per tile ----------------------------
+constexpr int kSortThreads = 256;
+constexpr int kCap = 4096;       // keys sorted in shared memory at once
+constexpr int kBuckets = 1024;
+
+struct SortSmem {
+    unsigned long long a[kCap];
+    uint16_t b[kCap];            // bucket-distributed positions into a
+    uint32_t cnt[kBuckets];
+    uint32_t cur[kBuckets];
+    unsigned long long red[2][kSortThreads / 32];
+    uint32_t wsum[kSortThreads / 32];
+};
+
+SB_INLINE unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t < v ? t : v;
+    }
+    return v;
+}
+SB_INLINE unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+// monotone (non-decreasing) map of a key onto [0, nb)
+SB_INLINE int bucket_of(unsigned long long k, unsigned long long kmin, float scale, int nb) {
+    const int b = (int)__fmul_rn(__ull2float_rn(k - kmin), scale);
+    return min(b, nb - 1);
+}
+
+// sorts sm.a[0, n) ascending (n <= kCap, keys distinct) and hands the key of
+// rank i to out(i, key).  Whole CTA.
+template <typename Out>
+__device__ __forceinline__ void cta_sort(SortSmem& sm, int n, Out&& out)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int i = tid; i < n; i += kSortThreads) {
+        const unsigned long long k = sm.a[i];
+        lo = k < lo ? k : lo;
+        hi = k > hi ? k : hi;
+    }
+    lo = warp_min_u64(lo);
+    hi = warp_max_u64(hi);
+    // about one key per bucket: nb = smallest power of two >= n, <= kBuckets
+    const int nb = min(kBuckets, 1 << (32 - __clz(max(n - 1, 1))));
+    for (int i = tid; i < nb; i += kSortThreads) sm.cnt[i] = 0;
+    if (lane == 0) { sm.red[0][warp] = lo; sm.red[1][warp] = hi; }
+    __syncthreads();
+    lo = sm.red[0][0];
+    hi = sm.red[1][0];
+#pragma unroll
+    for (int w = 1; w < kSortThreads / 32; w++) {
+        lo = sm.red[0][w] < lo ? sm.red[0][w] : lo;
+        hi = sm.red[1][w] > hi ? sm.red[1][w] : hi;
+    }
+    const float scale = (float)nb / __fadd_rn(__ull2float_rn(hi - lo), 1.0f);
+    for (int i = tid; i < n; i += kSortThreads) atomicAdd(&sm.cnt[bucket_of(sm.a[i], lo, scale, nb)], 1u);
+    __syncthreads();
+    // exclusive scan of the bucket counts: 4 consecutive buckets per thread
+    static_assert(kBuckets == 4 * kSortThreads, "scan layout");
+    uint32_t c[4], s = 0;
+#pragma unroll
+    for (int q = 0; q < 4; q++) { c[q] = 4 * tid + q < nb ? sm.cnt[4 * tid + q] : 0u; s += c[q]; }
+    uint32_t x = s;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
-    if (lane == 31) s_warp[warp] = x;
+    if (lane == 31) sm.wsum[warp] = x;
     __syncthreads();
-    if (warp == 0) {
-        uint32_t run = 0;
-        for (int w = 0; w < kScanT / 32; w++) run += s_warp[w];
-        const uint32_t pre = sb_lookback_warp(status, bid, run);
-        if (lane == 0) {
-            uint32_t r2 = 0;
-            for (int w = 0; w < kScanT / 32; w++) { const uint32_t t = s_warp[w]; s_warp[w] = r2; r2 += t; }
-            s_prefix = pre;
-            if (bid == (int)gridDim.x - 1) *total = (int32_t)(pre + run);
-        }
-    }
-    __syncthreads();
-    uint32_t run = s_prefix + s_warp[warp] + x - sum;
+    uint32_t run = x - s;
+    for (int w = 0; w < warp; w++) run += sm.wsum[w];
 #pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
-        if (base + j < nc) offsets[base + j] = (int32_t)run;
-        run += v[j];
+    for (int q = 0; q < 4; q++) {
+        if (4 * tid + q < nb) sm.cur[4 * tid + q] = run;
+        run += c[q];
     }
+    __syncthreads();
+    for (int i = tid; i < n; i += kSortThreads) {
+        const uint32_t p = atomicAdd(&sm.cur[bucket_of(sm.a[i], lo, scale, nb)], 1u);
+        sm.b[p] = (uint16_t)i;
+    }
+    __syncthreads();
+    // rank = bucket start + number of smaller keys in the bucket (cur = end now)
+    for (int i = tid; i < n; i += kSortThreads) {
+        const unsigned long long k = sm.a[sm.b[i]];
+        const int bk = bucket_of(k, lo, scale, nb);
+        const uint32_t end = sm.cur[bk], beg = end - sm.cnt[bk];
+        uint32_t r = 0;
+        for (uint32_t j = beg; j < end; j++) r += sm.a[sm.b[j]] < k ? 1u : 0u;
+        out(beg + r, k);
+    }
+    __syncthreads();
 }
 
-// Consecutive depth ranks own consecutive output ranges, so a warp's 32
-// primitives write one contiguous span: stage it in shared memory and store
-// it with coalesced writes (direct writes only when the span overflows).
-constexpr int kEmitStage = 768;   // pairs staged per warp
-
-__global__ void __launch_bounds__(256)
-emit_kernel(const RasterRec* __restrict__ recs, const uint32_t* __restrict__ order,
-            const int32_t* __restrict__ offsets, const int32_t* __restrict__ counters, int n_cap,
-            uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ slots, int tiles_x, int tiles_y, int W, int H)
-{
-    __shared__ uint2 stage[8][kEmitStage];
-    const int nc = min(counters[1], n_cap);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int i0 = i - lane;
-    if (i0 >= nc) return;
-    uint32_t s = 0, nh = 0;
-    float x = 0.f, y = 0.f, r = 0.f;
-    int off = 0;
-    if (i < nc) {
-        s = order[i];
-        const float4* r4 = reinterpret_cast<const float4*>(recs + s);
-        const float4 a = __ldg(r4);
-        const float4 c = __ldg(r4 + 2);
-        nh = __float_as_uint(c.w) >> 2;
-        x = a.x; y = a.y; r = c.z;
-        off = offsets[i];
-    }
-    const int wbeg = __shfl_sync(0xffffffffu, off, 0);
-    const int wend = __reduce_max_sync(0xffffffffu, (unsigned)(nh ? off + (int)nh : wbeg));
-    const bool staged = wend - wbeg <= kEmitStage;
-    if (nh) {
-        int tx0, tx1, ty0, ty1;
-        sb_tile_range(x, y, r, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
-        int pos = off;
-        for (int ty = ty0; ty <= ty1; ty++) {
-            int a, b;
-            if (!sb_row_hits(x, y, r, ty, tx0, tx1, W, H, a, b)) continue;
-            for (int tx = a; tx <= b; tx++) {
-                const uint32_t t = (uint32_t)(ty * tiles_x + tx);
-                if (staged) {
-                    stage[warp][pos - wbeg] = make_uint2(t, s);
-                } else {
-                    tile_keys[pos] = t;
-                    slots[pos] = s;
-                }
-                pos++;
-            }
-        }
-    }
-    if (!staged) return;
-    __syncwarp();
-    for (int q = lane; q < wend - wbeg; q += 32) {
-        const uint2 e = stage[warp][q];
-        tile_keys[wbeg + q] = e.x;
-        slots[wbeg + q] = e.y;
-    }
-}
-
-__global__ void __launch_bounds__(256)
-tile_ranges_kernel(const uint32_t* __restrict__ sorted_tiles, int P, int ntiles, int32_t* __restrict__ offsets)
-{
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t > ntiles) return;
-    int lo = 0, hi = P;
-    while (lo < hi) {   // first index with key >= t
+// number of keys in sorted src[0, n) smaller than k
+SB_INLINE int lower_bound_u64(const unsigned long long* src, int n, unsigned long long k) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (sorted_tiles[mid] < (uint32_t)t) lo = mid + 1; else hi = mid;
+        if (src[mid] < k) lo = mid + 1; else hi = mid;
     }
-    offsets[t] = lo;
+    return lo;
+}
+
+__global__ void __launch_bounds__(kSortThreads)
+tile_sort_kernel(const int32_t* __restrict__ offsets, unsigned long long* __restrict__ keys,
+                 unsigned long long* __restrict__ scratch, int32_t* __restrict__ prims)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
+    const int t = blockIdx.x, tid = threadIdx.x;
+    const int off = offsets[t], L = offsets[t + 1] - off;
+    if (L <= 1) {
+        if (L == 1 && tid == 0) prims[off] = (int32_t)(uint32_t)keys[off];
+        return;
+    }
+    if (L <= kCap) {
+        for (int i = tid; i < L; i += kSortThreads) sm.a[i] = keys[off + i];
+        __syncthreads();
+        cta_sort(sm, L, [&](int pos, unsigned long long k) { prims[off + pos] = (int32_t)(uint32_t)k; });
+        return;
+    }
+    // long list: sorted chunks of kCap into scratch, then pairwise merges
+    unsigned long long* src = scratch + off;
+    unsigned long long* dst = keys + off;
+    for (int c0 = 0; c0 < L; c0 += kCap) {
+        const int n = min(kCap, L - c0);
+        for (int i = tid; i < n; i += kSortThreads) sm.a[i] = keys[off + c0 + i];
+        __syncthreads();
+        cta_sort(sm, n, [&](int pos, unsigned long long k) { src[c0 + pos] = k; });
+    }
+    for (int width = kCap; width < L; width *= 2) {
+        const bool final_pass = 2 * width >= L;
+        for (int i = tid; i < L; i += kSortThreads) {
+            const int run = i / width, rs = run * width, ps = (run ^ 1) * width;
+            const int pl = max(0, min(width, L - ps));
+            const unsigned long long k = src[i];
+            const int pos = min(rs, ps) + (i - rs) + (pl > 0 ? lower_bound_u64(src + ps, pl, k) : 0);
+            if (final_pass) prims[off + pos] = (int32_t)(uint32_t)k;
+            else dst[pos] = k;
+        }
+        __syncthreads();
+        unsigned long long* tmp = src; src = dst; dst = tmp;
+    }
 }
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
-// ---- prepare: depth order + hit-count scan ---------------------------------
-size_t sb_bin_prepare_ws(int n_cap) {
-    const size_t n = (size_t)n_cap;
-    return 3 * align256(n * 4) + align256(onesweep::workspace_bytes(n_cap, 4)) +
-           align256(sizeof(unsigned long long) * ((n + kScanTile - 1) / kScanTile) + 16);
-}
+// ---- prepare -------------------------------------------------------------------
+size_t sb_bin_state_bytes(int n_cap) { return align256((size_t)(n_cap > 0 ? n_cap : 1) * 32); }
 
-void sb_launch_bin_prepare(const RasterRec* recs, const int32_t* counters, int n_cap, uint32_t* order,
-                           int32_t* pair_offsets, int32_t* n_pairs, void* ws, cudaStream_t stream)
-{
-    if (n_cap <= 0) {
-        cudaMemsetAsync(n_pairs, 0, sizeof(int32_t), stream);
-        return;
-    }
-    char* w = static_cast<char*>(ws);
-    const size_t n = (size_t)n_cap;
-    uint32_t* keys = reinterpret_cast<uint32_t*>(w); w += align256(n * 4);
-    uint32_t* keys_alt = reinterpret_cast<uint32_t*>(w); w += align256(n * 4);
-    uint32_t* vals_alt = reinterpret_cast<uint32_t*>(w); w += align256(n * 4);
-    void* sort_ws = w; w += align256(onesweep::workspace_bytes(n_cap, 4));
-    unsigned long long* status = reinterpret_cast<unsigned long long*>(w);
-    const int scan_blocks = (n_cap + kScanTile - 1) / kScanTile;
-    unsigned* ticket = reinterpret_cast<unsigned*>(status + scan_blocks);
-
-    depth_keys_kernel<<<(n_cap + 255) / 256, 256, 0, stream>>>(recs, counters, n_cap, keys);
-    // 4 passes (even): the sorted slots end in `order`
-    onesweep::sort<uint32_t>(keys, order, keys_alt, vals_alt, counters + 1, n_cap, 4, false, true, sort_ws, stream);
-    cudaMemsetAsync(status, 0, sizeof(unsigned long long) * scan_blocks + 16, stream);
-    hit_scan_kernel<<<scan_blocks, kScanT, 0, stream>>>(recs, order, counters, n_cap, pair_offsets, n_pairs, status,
-                                                        ticket);
-}
-
-// ---- finish: emit + tile sort + ranges -------------------------------------
-static int tile_passes(int ntiles) {
-    int bits = 1;
-    while ((1 << bits) < ntiles) bits++;
-    return (bits + 7) / 8;
-}
-
-size_t sb_bin_finish_ws(long long n_pairs, int ntiles) {
-    const size_t P = (size_t)(n_pairs > 0 ? n_pairs : 1);
-    return 3 * align256(P * 4) + align256(onesweep::workspace_bytes((int)P, tile_passes(ntiles)));
-}
-
-void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_cap, const uint32_t* order,
-                          const int32_t* pair_offsets, const CamDev& cam, int P, int32_t* tile_offsets,
-                          int32_t* tile_prims, void* ws, cudaStream_t stream)
+void sb_launch_bin_prepare(const RasterRec* recs, const int32_t* counters, int n_cap, const CamDev& cam,
+                           int32_t* tile_offsets, int32_t* n_pairs, void* state, cudaStream_t stream)
 {
     const int ntiles = cam.tiles_x * cam.tiles_y;
-    if (P <= 0) {
-        cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (ntiles + 1), stream);
-        return;
-    }
-    char* w = static_cast<char*>(ws);
-    const size_t Ps = (size_t)P;
-    uint32_t* tkeys = reinterpret_cast<uint32_t*>(w); w += align256(Ps * 4);
-    uint32_t* tkeys_alt = reinterpret_cast<uint32_t*>(w); w += align256(Ps * 4);
-    uint32_t* slots_alt = reinterpret_cast<uint32_t*>(w); w += align256(Ps * 4);
-    void* sort_ws = w;
-    const int passes = tile_passes(ntiles);
-    // emit into the buffers the sort ends in when the pass count is even
-    uint32_t* vals = passes % 2 == 0 ? reinterpret_cast<uint32_t*>(tile_prims) : slots_alt;
-    uint32_t* valt = passes % 2 == 0 ? slots_alt : reinterpret_cast<uint32_t*>(tile_prims);
-    emit_kernel<<<(n_cap + 255) / 256, 256, 0, stream>>>(recs, order, pair_offsets, counters, n_cap, tkeys, vals,
-                                                         cam.tiles_x, cam.tiles_y, cam.W, cam.H);
-    const int flip = onesweep::sort<uint32_t>(tkeys, vals, tkeys_alt, valt, nullptr, P, passes, true, false, sort_ws,
-                                              stream);
-    const uint32_t* sorted = flip ? tkeys_alt : tkeys;
-    tile_ranges_kernel<<<(ntiles + 1 + 255) / 256, 256, 0, stream>>>(sorted, P, ntiles, tile_offsets);
+    cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (ntiles + 1), stream);
+    if (n_cap > 0)
+        tile_count_kernel<<<(n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream>>>(
+            recs, counters, n_cap, cam.tiles_x, cam.tiles_y, cam.W, cam.H, static_cast<uint4*>(state), tile_offsets);
+    tile_scan_kernel<<<1, kScanThreads, 0, stream>>>(tile_offsets, ntiles, n_pairs);
 }
 
-// ---- Morton sort (u64 keys) --------------------------------------------------
-size_t sb_sort_u64_ws(int n, int bits) { return onesweep::workspace_bytes(n, (bits + 7) / 8); }
+// ---- finish --------------------------------------------------------------------
+size_t sb_bin_finish_ws(long long n_pairs, int ntiles) {
+    const size_t P = (size_t)(n_pairs > 0 ? n_pairs : 1);
+    return 2 * align256(P * 8) + align256((size_t)ntiles * 4);
+}
 
-int sb_launch_sort_u64(unsigned long long* keys, uint32_t* vals, unsigned long long* keys_alt, uint32_t* vals_alt,
-                       int n, int bits, void* ws, cudaStream_t stream)
+void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_cap, const CamDev& cam, int P,
+                          const int32_t* tile_offsets, const void* state, int32_t* tile_prims, void* ws,
+                          cudaStream_t stream)
 {
-    return onesweep::sort<unsigned long long>(keys, vals, keys_alt, vals_alt, nullptr, n, (bits + 7) / 8, true, false,
-                                              ws, stream);
+    const int ntiles = cam.tiles_x * cam.tiles_y;
+    if (P <= 0 || n_cap <= 0) return;
+    char* w = static_cast<char*>(ws);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)P * 8);
+    unsigned long long* scratch = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)P * 8);
+    int32_t* cursor = reinterpret_cast<int32_t*>(w);
+    cudaMemcpyAsync(cursor, tile_offsets, sizeof(int32_t) * ntiles, cudaMemcpyDeviceToDevice, stream);
+    scatter_kernel<<<(n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream>>>(
+        recs, counters, n_cap, cam.tiles_x, cam.tiles_y, cam.W, cam.H, static_cast<const uint4*>(state), cursor,
+        keys);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem));
+        attr = true;
+    }
+    tile_sort_kernel<<<ntiles, kSortThreads, sizeof(SortSmem), stream>>>(tile_offsets, keys, scratch, tile_prims);
 }

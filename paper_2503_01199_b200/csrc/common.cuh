@@ -196,16 +196,35 @@ SB_INLINE bool sb_disc_hits(float cx, float cy, float r, int tx, int ty, int W, 
     return DADD(DMUL(dx, dx), DMUL(dy, dy)) <= (double)rr;
 }
 
+// The same decision with a float32 filter.  Each float32 difference of an
+// integer <= W (or H) and cx (cy) is within E = (|cx| + |cy| + W + H) 2^-23
+// of the exact one, so |q32 - Q64| <= 2 (dx + dy + E) E + 2^-22 (q + rr).
+// Outside that margin the float32 verdict is the float64 verdict; inside it,
+// the float64 test decides.
+SB_INLINE bool sb_disc_hits_fast(float cx, float cy, float r, int tx, int ty, int W, int H) {
+    const int rx0 = tx * SB_TILE_W, ry0 = ty * SB_TILE_H;
+    const int rx1 = min(rx0 + SB_TILE_W - 1, W - 1), ry1 = min(ry0 + SB_TILE_H - 1, H - 1);
+    const float dx = fmaxf(fmaxf((float)rx0 - cx, cx - (float)rx1), 0.0f);
+    const float dy = fmaxf(fmaxf((float)ry0 - cy, cy - (float)ry1), 0.0f);
+    const float rr = FMUL(r, r);
+    const float q = fmaf(dx, dx, dy * dy);
+    const float E = (fabsf(cx) + fabsf(cy) + (float)(W + H)) * 1.1920929e-7f;
+    const float m = fmaf(2.0f * (dx + dy + E), E, (q + rr) * 2.384185791e-7f) + 1e-30f;
+    if (q < rr - m) return true;
+    if (q > rr + m) return false;
+    return sb_disc_hits(cx, cy, r, tx, ty, W, H);
+}
+
 // Hits of one tile row ty: the exact disc test is monotone in |dx| (the
 // float64 differences of an integer and a float32 are exact and rounding is
 // monotone), so the hit set in a row is one contiguous interval [*a, *b];
 // find it by scanning in from both ends.  Returns b - a + 1 (0 if empty).
 SB_INLINE int sb_row_hits(float cx, float cy, float r, int ty, int tx0, int tx1, int W, int H, int& a, int& b) {
     a = tx0;
-    while (a <= tx1 && !sb_disc_hits(cx, cy, r, a, ty, W, H)) a++;
+    while (a <= tx1 && !sb_disc_hits_fast(cx, cy, r, a, ty, W, H)) a++;
     if (a > tx1) return 0;
     b = tx1;
-    while (b > a && !sb_disc_hits(cx, cy, r, b, ty, W, H)) b--;
+    while (b > a && !sb_disc_hits_fast(cx, cy, r, b, ty, W, H)) b--;
     return b - a + 1;
 }
 

@@ -158,3 +158,15 @@ void sb_launch_permute(const uint32_t* perm, int n, int count, const void* const
     }
     permute_kernel<<<(n + 255) / 256, 256, 0, stream>>>(perm, n, a);
 }
+
+// ---- Morton sort (u64 keys): stable onesweep LSD radix sort -----------------
+#include "onesweep.cuh"
+
+size_t sb_sort_u64_ws(int n, int bits) { return onesweep::workspace_bytes(n, (bits + 7) / 8); }
+
+int sb_launch_sort_u64(unsigned long long* keys, uint32_t* vals, unsigned long long* keys_alt, uint32_t* vals_alt,
+                       int n, int bits, void* ws, cudaStream_t stream)
+{
+    return onesweep::sort<unsigned long long>(keys, vals, keys_alt, vals_alt, nullptr, n, (bits + 7) / 8, true, false,
+                                              ws, stream);
+}

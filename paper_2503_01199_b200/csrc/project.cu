@@ -1,5 +1,5 @@
-// K5: fused projection + cluster AABB + frustum cull + stream compaction +
-// per-tile hit counting, one warp per 128-primitive cluster.
+// K5: fused projection + cluster AABB + frustum cull + stream compaction,
+// one warp per 128-primitive cluster.
 //
 // Replaces (pkg/src/tinysplat):
 //   projection.py:130-190  project_scene           (bit-exact float32 mirror)
@@ -7,7 +7,6 @@
 //   ccc.py:134-146         cull_clusters           (p-vertex test)
 //   ccc.py:149-164         cluster_visibility      (| any(in_image) widening)
 //   ccc.py:171-194         compact_arrays          (contiguous visible ranges)
-//   tiles.py:50-91         bin_tiles, per-primitive hit count (exact disc test)
 //
 // One pass over the 64-byte parameter rows (four 128-bit loads per lane per
 // Gaussian, 2 KB contiguous per warp), records staged in shared memory, the
@@ -76,7 +75,6 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
                 sb_project(p, cam, o, s64);
                 r.x = o.x; r.y = o.y; r.a = o.ca; r.b = o.cb; r.c = o.cc; r.o = o.op;
                 r.r = o.col[0]; r.g = o.col[1]; r.bl = o.col[2]; r.depth = o.depth; r.radius = o.radius;
-                uint32_t nhit = 0;
                 any_in |= o.in_image;
                 ndeg += o.degenerate ? 1 : 0;
                 // cluster AABB: p -+ 3 * max(exp(log_scale)) in float64 (ccc.py:125-130)
@@ -86,17 +84,8 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
                     lo[k] = fmin(lo[k], DSUB((double)p[k], reach));
                     hi[k] = fmax(hi[k], DADD((double)p[k], reach));
                 }
-                // tile hits of fragment-generating primitives (exact disc test)
-                if (o.in_image) {
-                    int tx0, tx1, ty0, ty1;
-                    sb_tile_range(o.x, o.y, o.radius, cam.tiles_x, cam.tiles_y, tx0, tx1, ty0, ty1);
-                    for (int ty = ty0; ty <= ty1; ty++) {
-                        int a, b;
-                        nhit += (uint32_t)sb_row_hits(o.x, o.y, o.radius, ty, tx0, tx1, cam.W, cam.H, a, b);
-                    }
-                }
-                // flags: bit0 valid, bit1 in_image, bits 2.. tile-hit count
-                r.flags = (o.valid ? 1u : 0u) | (o.in_image ? 2u : 0u) | (nhit << 2);
+                // flags: bit0 valid, bit1 in_image (tile hits: binning.cu)
+                r.flags = (o.valid ? 1u : 0u) | (o.in_image ? 2u : 0u);
             }
             st[slot] = r;
         }

@@ -4,7 +4,13 @@
 // vertical run starting at row 4 * (l / 16) (tiles.py:18-27).  The footprint
 // exponent is expanded along the run as basic + linear*i + quad*i^2
 // (forward.py:97-108, 130-158): the full quadratic form once per (primitive,
-// lane), two multiply-adds per extra pixel.
+// lane), two multiply-adds per extra pixel.  The exponent is formed directly
+// in log2 units from per-primitive coefficients computed once when a chunk of
+// records is staged (A = -log2(e)/2 a, B = -log2(e) b, Cq = -log2(e)/2 c), so
+// G = ex2(e) is one MUFU per pixel.  G therefore differs from numpy's float32
+// np.exp of its own float32 exponent by a few ulp (the reference's exp is
+// itself ~2.5 ulp); the forward and the backward share this function, so
+// they always agree on alpha.
 //
 // Forward (forward.py:161-191, 240-255): front-to-back blend, alpha =
 // min(o*G, alpha_max), skip alpha < alpha_min, blend while T_before >= t_stop
@@ -25,8 +31,7 @@
 //   the rest     the reference's pairing tree v[:s] + v[s:2s], s = 16..1
 //                (reduction.py:21-32), bit-identical to a __shfl_xor butterfly.
 // This replaces per-fragment shuffle / REDUX chains with independent,
-// latency-tolerant register work (the kernel was dependency- and
-// branch-stall bound).  The warp-shuffle reductions remain for the
+// latency-tolerant register work.  The warp-shuffle reductions remain for the
 // standalone reduction entry point (sb_lane_reduce).
 //
 // Scheduling: warps pull tiles from an atomic counter (persistent grid), and
@@ -40,10 +45,13 @@ namespace {
 constexpr int kWarpsPerBlock = 4;
 constexpr int kThreads = kWarpsPerBlock * 32;
 
+// staged record: raw conic (for the backward fold) plus the log2-domain
+// exponent coefficients
 struct __align__(16) SRec {
-    float x, y, a, b;
-    float c, o, r, g;
-    float bl, pad0, pad1;
+    float x, y, A, B;        // A = -log2e/2 a, B = -log2e b
+    float Cq, o, r, g;       // Cq = -log2e/2 c
+    float bl, nB, nC2, pad;  // nB = -B, nC2 = -2 Cq
+    float a, b, c;
     int32_t slot;
 };
 
@@ -65,45 +73,37 @@ SB_INLINE void prefetch_chunk(Prefetch& pf, const RasterRec* __restrict__ recs, 
     }
 }
 
+constexpr float kHalfLog2e = -0.72134752044448170f;   // -log2(e) / 2
+constexpr float kLog2e = -1.44269504088896341f;       // -log2(e)
+
 SB_INLINE void commit_chunk(SRec* slab, const Prefetch& pf, int cnt, int lane) {
     if (lane < cnt) {
+        const float A = kHalfLog2e * pf.a.z, B = kLog2e * pf.a.w, Cq = kHalfLog2e * pf.b.x;
         float4* d = reinterpret_cast<float4*>(slab + lane);
-        d[0] = pf.a;
-        d[1] = pf.b;
-        d[2] = make_float4(pf.bl, 0.f, 0.f, __int_as_float(pf.slot));
+        d[0] = make_float4(pf.a.x, pf.a.y, A, B);
+        d[1] = make_float4(Cq, pf.b.y, pf.b.z, pf.b.w);
+        d[2] = make_float4(pf.bl, -B, -2.0f * Cq, 0.f);
+        d[3] = make_float4(pf.a.z, pf.a.w, pf.b.x, __int_as_float(pf.slot));
     }
 }
 
-// scanline exponent (forward.py:97-108) with numpy's operation order; the
-// forward and backward share it so both see bit-identical alphas.
-// expo_i = (basic + linear*i) + quad*(i*i): for i = 0 the products are exact
-// zeros, and for i = 2 the scalings by 2 and 4 are exact, so fusing them
-// (FMA of an exact product = one rounding) is bit-identical to numpy.
-#ifdef SB_FAST_EXP
-// exp(x) = 2^(x log2 e) with the product split so its rounding error does not
-// grow with |x| (hi + lo), then MUFU.EX2; max error ~2-3 ulp
-SB_INLINE float g_exp(float x) {
-    const float hi = x * 1.44269502f;
-    const float lo = fmaf(x, 1.44269502f, -hi) + x * 1.9259630e-8f;
-    float e;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(hi));
-    return fmaf(e, lo * 0.69314718f, e);
+SB_INLINE float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
-#else
-SB_INLINE float g_exp(float x) { return expf(x); }
-#endif
 
+// G at the lane's 4 run pixels: e0 = A dx^2 + B dx dy + Cq dy^2 (log2
+// units), e_i = e0 + l2 i + Cq i^2 with l2 = -(B dx + 2 Cq dy)
 SB_INLINE void lane_G(const SRec& r, float px, float py0, float G[4], float& dx, float& dy) {
-    dx = FSUB(r.x, px);
-    dy = FSUB(r.y, py0);
-    const float basic = FMUL(-0.5f, FADD(FADD(FMUL(FMUL(r.a, dx), dx), FMUL(FMUL(FMUL(2.0f, r.b), dx), dy)),
-                                         FMUL(FMUL(r.c, dy), dy)));
-    const float linear = FADD(FMUL(r.b, dx), FMUL(r.c, dy));
-    const float quad = FMUL(-0.5f, r.c);
-    G[0] = g_exp(basic);
-    G[1] = g_exp(FADD(FADD(basic, linear), quad));
-    G[2] = g_exp(FFMA(quad, 4.0f, FFMA(linear, 2.0f, basic)));
-    G[3] = g_exp(FADD(FADD(basic, FMUL(linear, 3.0f)), FMUL(quad, 9.0f)));
+    dx = r.x - px;
+    dy = r.y - py0;
+    const float e0 = fmaf(fmaf(r.A, dx, r.B * dy), dx, (r.Cq * dy) * dy);
+    const float l2 = fmaf(r.nB, dx, r.nC2 * dy);
+    G[0] = ex2(e0);
+    G[1] = ex2(e0 + (l2 + r.Cq));
+    G[2] = ex2(fmaf(4.0f, r.Cq, fmaf(2.0f, l2, e0)));
+    G[3] = ex2(fmaf(9.0f, r.Cq, fmaf(3.0f, l2, e0)));
 }
 
 SB_INLINE int next_tile(int* counter, int lane) {
@@ -136,13 +136,13 @@ raster_fwd_kernel(FwdParams p)
         const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
         const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
         const float px = (float)pxi, py0 = (float)py0i;
-        bool valid[4];
+        // out-of-image pixels start terminated (T = 0 < t_stop): they never
+        // blend and are never written
         float T[4], rgb[4][3];
         int frags[4], last[4];
 #pragma unroll
         for (int i = 0; i < 4; i++) {
-            valid[i] = pxi < p.W && py0i + i < p.H;
-            T[i] = 1.0f;
+            T[i] = (pxi < p.W && py0i + i < p.H) ? 1.0f : 0.0f;
             rgb[i][0] = rgb[i][1] = rgb[i][2] = 0.0f;
             frags[i] = 0;
             last[i] = 0;
@@ -158,24 +158,22 @@ raster_fwd_kernel(FwdParams p)
             __syncwarp();
             if (k0 + 32 < n) prefetch_chunk(pf, p.recs, p.prims, beg, k0 + 32, min(32, n - k0 - 32), lane);
             for (int j = 0; j < cnt; j++) {
-                bool live = false;
-#pragma unroll
-                for (int i = 0; i < 4; i++) live |= valid[i] && T[i] >= p.tstop;
+                const bool live = fmaxf(fmaxf(T[0], T[1]), fmaxf(T[2], T[3])) >= p.tstop;
                 if (!__any_sync(0xffffffffu, live)) {
                     done = true;
                     break;
                 }
                 if (!live) continue;
-                const SRec r = slab[j];
+                const SRec& r = slab[j];
                 float G[4], dx, dy;
                 lane_G(r, px, py0, G, dx, dy);
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
-                    const float alpha = fminf(FMUL(r.o, G[i]), p.amax);
-                    if (valid[i] && T[i] >= p.tstop && alpha >= p.amin) {
+                    const float alpha = fminf(r.o * G[i], p.amax);
+                    if (T[i] >= p.tstop && alpha >= p.amin) {
                         // T (which decides termination / frag counts) keeps
                         // numpy's rounding; the colour sum may fuse
-                        const float w = FMUL(T[i], alpha);
+                        const float w = T[i] * alpha;
                         rgb[i][0] = fmaf(w, r.r, rgb[i][0]);
                         rgb[i][1] = fmaf(w, r.g, rgb[i][1]);
                         rgb[i][2] = fmaf(w, r.bl, rgb[i][2]);
@@ -188,7 +186,7 @@ raster_fwd_kernel(FwdParams p)
         }
 #pragma unroll
         for (int i = 0; i < 4; i++) {
-            if (!valid[i]) continue;
+            if (!(pxi < p.W && py0i + i < p.H)) continue;
             const size_t pix = (size_t)(py0i + i) * p.W + pxi;
             p.out_color[3 * pix + 0] = FADD(rgb[i][0], FMUL(T[i], p.bg[0]));
             p.out_color[3 * pix + 1] = FADD(rgb[i][1], FMUL(T[i], p.bg[1]));
@@ -245,7 +243,7 @@ raster_fwd_half_kernel(FwdParams p)
                     break;
                 }
                 if (!live) continue;
-                const SRec r = slab[j];
+                const SRec& r = slab[j];
                 float G[4], dx, dy;
                 lane_G(r, px, py0, G, dx, dy);
                 const __half o = __float2half_rn(r.o);
@@ -369,32 +367,29 @@ struct BwdWarpSmem {
     int count[kBatch];
 };
 
-// exact v * 2^s for float32 v with |v * 2^s| < 2^24 (power-of-two scaling is
-// exact unless the result is subnormal, and then |result| < 0.5 rounds to 0)
-SB_INLINE float scale_pow2(float v, int s) {
-    if (s > 126) {
-        v *= __int_as_float((127 + 64) << 23);
-        s -= 64;
-    }
-    if (s < -126) return 0.0f;
-    return v * __int_as_float((127 + s) << 23);
-}
-
 // reduction.py:35-58 over one row of 32 lane values held in registers:
 // max exponent, exact integer alignment (round half to even), exact int sum,
-// one rounding to float32
+// one rounding to float32.  v * 2^(23 - emax) is a power-of-two scaling: exact
+// unless the product is subnormal, and then |product| < 0.5 rounds to 0
+// either way, so one (row-uniform) multiply replaces the integer alignment.
 SB_INLINE float row_exp_aligned(const float v[32]) {
-    uint32_t mx = 0;
+    float mx = 0.0f;
 #pragma unroll
-    for (int l = 0; l < 32; l++) mx = max(mx, __float_as_uint(v[l]) & 0x7fffffffu);
-    if (mx == 0) return 0.0f;
-    const int emax = f32_exponent(mx);
-    const int sh = 23 - emax;
+    for (int l = 0; l < 32; l++) mx = fmaxf(mx, fabsf(v[l]));
+    if (mx == 0.0f) return 0.0f;
+    const int emax = f32_exponent(__float_as_uint(mx));
+    int sh = 23 - emax;               // in [-104, 172]
+    float pre = 1.0f;
+    if (sh > 126) {                   // all values below 2^-103: two steps
+        pre = __int_as_float((127 + 64) << 23);
+        sh -= 64;
+    }
+    const float scale = __int_as_float((127 + sh) << 23);
     int total = 0;
 #pragma unroll
-    for (int l = 0; l < 32; l++) total += __float2int_rn(scale_pow2(v[l], sh));
-    const double scale = __longlong_as_double((long long)(emax - 23 + 1023) << 52);
-    return __double2float_rn((double)total * scale);
+    for (int l = 0; l < 32; l++) total += __float2int_rn((v[l] * pre) * scale);
+    const double out = __longlong_as_double((long long)(emax - 23 + 1023) << 52);
+    return __double2float_rn((double)total * out);
 }
 
 // reduction.py:21-32 tree v[:s] + v[s:2s], s = 16..1, in registers
@@ -407,30 +402,49 @@ SB_INLINE float row_tree(float v[32]) {
 }
 
 // rows of a batch: row = channel * kBatch + slot, so the 3 conic channels
-// come first (lanes of one flush iteration take the same reduction path)
-// and all 10 stores of one fragment share the swizzle (row & 7) == slot.
+// come first and all 10 stores of one fragment share the swizzle
+// (row & 7) == slot.
 static_assert(kBatch == 8, "row swizzle assumes 8 slots");
 
+SB_INLINE void load_row(const BwdWarpSmem& ws, int row, float v[32]) {
+    const float* base = ws.part + row * 32;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        const float4 x = *reinterpret_cast<const float4*>(base + 4 * ((q + (row & 7)) & 7));
+        v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+    }
+}
+
+SB_INLINE void emit_row(const BwdWarpSmem& ws, int c, int b, float out, sb_screen_grad* grads) {
+    sb_screen_grad* gr = grads + ws.slot[b];
+    if (c < 9) {
+        atomicAdd(reinterpret_cast<float*>(gr) + c, out);
+        if (c == 5) atomicAdd(&gr->M, (double)out);       // M = sum of dL/do over the tile
+        if (c == 0) atomicAdd(&gr->C, ws.count[b]);
+    } else {
+        atomicAdd(&gr->S, (double)out);
+    }
+}
+
+// conic rows (exponent-aligned) and tree rows in separate, lane-uniform
+// passes: no lane runs both reduction paths
 SB_INLINE void flush_batch(BwdWarpSmem& ws, int nb, int lane, int conic_tree, sb_screen_grad* grads) {
     __syncwarp();
-    for (int i = lane; i < nb * kCh; i += 32) {
-        const int c = i / nb, b = i - c * nb, row = c * kBatch + b;
+    int first_tree = 0;
+    if (!conic_tree) {
+        first_tree = 3 * nb;
+        if (lane < 3 * nb) {
+            const int c = lane / nb, b = lane - c * nb;
+            float v[32];
+            load_row(ws, c * kBatch + b, v);
+            emit_row(ws, c, b, row_exp_aligned(v), grads);
+        }
+    }
+    for (int i = first_tree + lane; i < nb * kCh; i += 32) {
+        const int c = i / nb, b = i - c * nb;
         float v[32];
-        const float* base = ws.part + row * 32;
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const float4 x = *reinterpret_cast<const float4*>(base + 4 * ((q + (row & 7)) & 7));
-            v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
-        }
-        const float out = (c < 3 && !conic_tree) ? row_exp_aligned(v) : row_tree(v);
-        sb_screen_grad* gr = grads + ws.slot[b];
-        if (c < 9) {
-            atomicAdd(reinterpret_cast<float*>(gr) + c, out);
-            if (c == 5) atomicAdd(&gr->M, (double)out);       // M = sum of dL/do over the tile
-            if (c == 0) atomicAdd(&gr->C, ws.count[b]);
-        } else {
-            atomicAdd(&gr->S, (double)out);
-        }
+        load_row(ws, c * kBatch + b, v);
+        emit_row(ws, c, b, row_tree(v), grads);
     }
     __syncwarp();
 }
@@ -438,9 +452,9 @@ SB_INLINE void flush_batch(BwdWarpSmem& ws, int nb, int lane, int conic_tree, sb
 __global__ void __launch_bounds__(kThreads, 4)
 raster_bwd_kernel(BwdParams p)
 {
-    __shared__ BwdWarpSmem wsm[kWarpsPerBlock];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    BwdWarpSmem& ws = wsm[warp];
+    BwdWarpSmem& ws = reinterpret_cast<BwdWarpSmem*>(smem_raw)[warp];
     for (int t = next_tile(p.tile_counter, lane); t < p.ntiles; t = next_tile(p.tile_counter, lane)) {
         const int beg = p.offsets[t];
         if (p.offsets[t + 1] == beg) continue;
@@ -476,59 +490,58 @@ raster_bwd_kernel(BwdParams p)
             if (k0 > 0) prefetch_chunk(pf, p.recs, p.prims, beg, max(0, k0 - 32), k0 - max(0, k0 - 32), lane);
             for (int j = cnt - 1; j >= 0; j--) {
                 const int k = k0 + j;
-                const bool act = k < lane_max;
-                if (!__any_sync(0xffffffffu, act)) continue;
+                if (!__any_sync(0xffffffffu, k < lane_max)) continue;
                 const SRec& r = ws.slab[j];
+                float G[4], dx, dy;
+                lane_G(r, px, py0, G, dx, dy);
+                float araw[4], alpha[4];
+                bool ci[4];
+                bool any_c = false;
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    araw[i] = r.o * G[i];
+                    alpha[i] = fminf(araw[i], p.amax);
+                    // contributing: before this pixel's last contributor and usable
+                    ci[i] = (k < last[i]) && (alpha[i] >= p.amin);
+                    any_c |= ci[i];
+                }
+                if (!__any_sync(0xffffffffu, any_c)) continue;
                 float f[4], uG[4], w[4];
-                float dx = 0.f, dy = 0.f;
-                int cnt_l = 0;
-                {
-                    float G[4];
-                    lane_G(r, px, py0, G, dx, dy);
-                    float araw[4], alpha[4];
-                    bool ci[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) f[i] = uG[i] = w[i] = 0.0f;
+                if (any_c) {
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
-                        araw[i] = FMUL(r.o, G[i]);
-                        alpha[i] = fminf(araw[i], p.amax);
-                        // contributing: before this pixel's last contributor and usable
-                        ci[i] = (k < last[i]) && (alpha[i] >= p.amin);
-                        cnt_l += ci[i] ? 1 : 0;
-                        f[i] = uG[i] = w[i] = 0.0f;
-                    }
-                    if (cnt_l > 0) {
-#pragma unroll
-                        for (int i = 0; i < 4; i++) {
-                            const float inv = rcp_approx(1.0f - alpha[i]);
-                            const float Tb = T[i] * inv;
-                            const float dc = dI[i][0] * r.r + dI[i][1] * r.g + dI[i][2] * r.bl;
-                            const float da = Tb * dc - Sd[i] * inv;
-                            const float dpre = (ci[i] && araw[i] < p.amax) ? da : 0.0f;
-                            f[i] = dpre * G[i];
-                            uG[i] = dpre * r.o * G[i];
-                            w[i] = ci[i] ? Tb * alpha[i] : 0.0f;
-                            Sd[i] += w[i] * dc;
-                            T[i] = ci[i] ? Tb : T[i];
-                        }
+                        const float inv = rcp_approx(1.0f - alpha[i]);
+                        const float Tb = T[i] * inv;
+                        const float dc = fmaf(dI[i][2], r.bl, fmaf(dI[i][1], r.g, dI[i][0] * r.r));
+                        const float da = fmaf(Tb, dc, -Sd[i] * inv);
+                        // gradient through a clamped alpha is zero (backward.py:128,169)
+                        f[i] = (ci[i] && araw[i] < p.amax) ? da * G[i] : 0.0f;
+                        uG[i] = f[i] * r.o;
+                        w[i] = ci[i] ? Tb * alpha[i] : 0.0f;
+                        Sd[i] = fmaf(w[i], dc, Sd[i]);
+                        T[i] = ci[i] ? Tb : T[i];
                     }
                 }
-                const bool contrib = cnt_l > 0;
-                if (!__any_sync(0xffffffffu, contrib)) continue;
+                int cnt_l = 0;
+#pragma unroll
+                for (int i = 0; i < 4; i++) cnt_l += ci[i] ? 1 : 0;
                 // scanline_grad_fold (backward.py:175-196) + per-lane partials
                 const float gb = ((uG[0] + uG[1]) + uG[2]) + uG[3];
-                const float gl = (uG[1] + uG[2] * 2.0f) + uG[3] * 3.0f;
-                const float gq = (uG[1] + uG[2] * 4.0f) + uG[3] * 9.0f;
+                const float gl = fmaf(uG[3], 3.0f, fmaf(uG[2], 2.0f, uG[1]));
+                const float gq = fmaf(uG[3], 9.0f, fmaf(uG[2], 4.0f, uG[1]));
                 float* pp = ws.part + nb * 32 + ((lane + 4 * nb) & 31);   // channel c at pp[c * 256]
                 pp[0 * 256] = gb * (-0.5f * dx * dx);
-                pp[1 * 256] = gb * (-dx * dy) + gl * dx;
-                pp[2 * 256] = (gb * (-0.5f * dy * dy) + gl * dy) + gq * -0.5f;
-                pp[3 * 256] = gb * -(r.a * dx + r.b * dy) + gl * r.b;
-                pp[4 * 256] = gb * -(r.b * dx + r.c * dy) + gl * r.c;
+                pp[1 * 256] = fmaf(gb, -dx * dy, gl * dx);
+                pp[2 * 256] = fmaf(gq, -0.5f, fmaf(gb, -0.5f * dy * dy, gl * dy));
+                pp[3 * 256] = fmaf(gl, r.b, -gb * fmaf(r.a, dx, r.b * dy));
+                pp[4 * 256] = fmaf(gl, r.c, -gb * fmaf(r.b, dx, r.c * dy));
                 pp[5 * 256] = ((f[0] + f[1]) + f[2]) + f[3];
-                pp[6 * 256] = ((w[0] * dI[0][0] + w[1] * dI[1][0]) + w[2] * dI[2][0]) + w[3] * dI[3][0];
-                pp[7 * 256] = ((w[0] * dI[0][1] + w[1] * dI[1][1]) + w[2] * dI[2][1]) + w[3] * dI[3][1];
-                pp[8 * 256] = ((w[0] * dI[0][2] + w[1] * dI[1][2]) + w[2] * dI[2][2]) + w[3] * dI[3][2];
-                pp[9 * 256] = ((f[0] * f[0] + f[1] * f[1]) + f[2] * f[2]) + f[3] * f[3];
+                pp[6 * 256] = fmaf(w[3], dI[3][0], fmaf(w[2], dI[2][0], fmaf(w[1], dI[1][0], w[0] * dI[0][0])));
+                pp[7 * 256] = fmaf(w[3], dI[3][1], fmaf(w[2], dI[2][1], fmaf(w[1], dI[1][1], w[0] * dI[0][1])));
+                pp[8 * 256] = fmaf(w[3], dI[3][2], fmaf(w[2], dI[2][2], fmaf(w[1], dI[1][2], w[0] * dI[0][2])));
+                pp[9 * 256] = fmaf(f[3], f[3], fmaf(f[2], f[2], fmaf(f[1], f[1], f[0] * f[0])));
                 const int C = __reduce_add_sync(0xffffffffu, cnt_l);
                 if (lane == 0) {
                     ws.slot[nb] = r.slot;
@@ -589,7 +602,13 @@ void sb_launch_raster_bwd(const RasterRec* recs, const int32_t* offsets, const i
     p.dL_dI = dL_dI; p.T_final = T_final; p.last = last; p.grads = grads;
     const int want = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const int blocks = min(want, sm_count() * 4);
-    if (blocks) raster_bwd_kernel<<<blocks, kThreads, 0, stream>>>(p);
+    const int smem = (int)sizeof(BwdWarpSmem) * kWarpsPerBlock;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    if (blocks) raster_bwd_kernel<<<blocks, kThreads, smem, stream>>>(p);
 }
 
 // ---- standalone lane reductions (reduction.py:21-58), for parity tests ----

@@ -5,10 +5,11 @@ Reference API: pkg/src/tinysplat/forward.py:56-94 (RasterConfig,
 RenderOutput, RenderContext) and 258-308 (forward, render).  The call chain
 per view is four calls through the C-ABI (include/splat_b200.h):
 
-  sb_project_cull_compact  projection.py:130-190 + ccc.py:112-194 + tile-hit counts
-  sb_bin_prepare           stable depth order + scan of hit counts (-> P)
-  sb_bin_finish            tiles.py:75-106: emit pairs in depth order, stable
-                           onesweep sort by tile id, per-tile ranges
+  sb_project_cull_compact  projection.py:130-190 + ccc.py:112-194
+  sb_bin_prepare           tiles.py:75-91 exact hits counted per tile ->
+                           tile offsets (-> P)
+  sb_bin_finish            tiles.py:94-106: scatter (depth, slot) keys into
+                           tile ranges, per-tile sort in shared memory
   sb_raster_fwd            forward.py:161-191 blend + 240-255 assembly
 """
 from __future__ import annotations
@@ -149,21 +150,20 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     coff = torch.empty(max(K, 1), dtype=torch.int32, device=dev)
     cvis = torch.zeros(max(K, 1), dtype=torch.uint8, device=dev)
     counters = torch.zeros(8, dtype=torch.int32, device=dev)   # vis, N_c, ndeg, pad, P
-    order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    pair_offsets = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     lib = _lib.load()
+    tile_offsets = torch.empty(ntiles + 1, dtype=torch.int32, device=dev)
     ws = _lib.workspace("project", lib.sb_project_workspace_bytes(n), dev)
     _lib.call("sb_project_cull_compact", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s), _lib.ptr(recs),
-              _lib.ptr(cmap), _lib.ptr(coff), _lib.ptr(cvis), _lib.ptr(counters), _lib.ptr(ws), ws.numel(), stream)
-    ws_p = _lib.workspace("bin_prepare", lib.sb_bin_prepare_workspace_bytes(n), dev)
-    _lib.call("sb_bin_prepare", _lib.ptr(recs), _lib.ptr(counters), n, _lib.ptr(order), _lib.ptr(pair_offsets),
-              _lib.ptr(counters[4:]), _lib.ptr(ws_p), ws_p.numel(), stream)
+              _lib.ptr(cmap), _lib.ptr(coff), _lib.ptr(cvis), _lib.ptr(counters), _lib.ptr(ws), ws.numel(),
+              stream)
+    state = _lib.workspace("bin_state", lib.sb_bin_state_workspace_bytes(n), dev)
+    _lib.call("sb_bin_prepare", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), _lib.ptr(tile_offsets),
+              _lib.ptr(counters[4:]), _lib.ptr(state), state.numel(), stream)
     vis, nc, ndeg, _, P = (int(v) for v in counters[:5].cpu().tolist())   # one D2H read
-    tile_offsets = torch.empty(ntiles + 1, dtype=torch.int32, device=dev)
     prims = torch.empty(max(P, 1), dtype=torch.int32, device=dev)
     ws_f = _lib.workspace("bin_finish", lib.sb_bin_finish_workspace_bytes(P, ntiles), dev)
-    _lib.call("sb_bin_finish", _lib.ptr(recs), _lib.ptr(counters), n, _lib.ptr(order), _lib.ptr(pair_offsets),
-              C.byref(cam_s), P, _lib.ptr(tile_offsets), _lib.ptr(prims), _lib.ptr(ws_f), ws_f.numel(), stream)
+    _lib.call("sb_bin_finish", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), P, _lib.ptr(tile_offsets),
+              _lib.ptr(state), _lib.ptr(prims), _lib.ptr(ws_f), ws_f.numel(), stream)
     color = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
     T = torch.empty((H, W), dtype=torch.float32, device=dev)
     frags = torch.empty((H, W), dtype=torch.int32, device=dev)
