@@ -20,7 +20,7 @@
 //                | compact slot) through shared-memory cursors (order inside
 //                a tile is arbitrary at this point);
 //            (2) per-tile sort, one CTA per tile, in shared memory: keys are
-//                distributed over up to 1024 buckets by a monotone map of the
+//                distributed over up to 2048 buckets by a monotone map of the
 //                key (float-rounded offset from the tile's minimum), and each
 //                key's final position is its bucket start plus the number of
 //                smaller keys in its bucket.  Lists longer than the shared
@@ -42,9 +42,17 @@ constexpr int kWin = 6144;          // shared-memory tile counters per CTA
 constexpr int kSpanRows = 16;       // rows per primitive in the span format
 constexpr uint32_t kEmptySpan = 0x00ffu;   // a > b
 
+struct PrimSmem {
+    float x, y, r;
+    int tx0, tx1, ty0;
+    unsigned long long key;
+};
+
 struct WinSmem {
     int32_t cnt[kWin];              // (w + 1) x h row-difference / count / cursor window
     uint16_t span[kBinThreads][kSpanRows];
+    PrimSmem prim[kBinThreads];
+    int flat[kBinThreads / 32][32];
     int x0, y0, w, h;
     int red[4][kBinThreads / 32];
 };
@@ -145,6 +153,39 @@ SB_INLINE void window_counts(WinSmem& sm, int tiles_x, F&& f) {
     }
 }
 
+// Warp-flattened iteration over (lane, k < cnt) items: every lane takes
+// items in turn, whoever owns them, so lanes with long and short item lists
+// do not diverge.  f(thread index within the CTA, k).
+template <typename F>
+SB_INLINE void warp_flat(WinSmem& sm, int cnt, F&& f) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int* base = sm.flat[warp];
+    base[lane] = incl - cnt;
+    __syncwarp();
+    for (int i = lane; i < total; i += 32) {
+        int o = 0;   // last lane whose first item is <= i
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1)
+            if (base[o + st] <= i) o += st;
+        f(warp * 32 + o, i - base[o]);
+    }
+    __syncwarp();
+}
+
+SB_INLINE void publish_prim(WinSmem& sm, const Prim& q) {
+    PrimSmem& p = sm.prim[threadIdx.x];
+    p.x = q.x; p.y = q.y; p.r = q.r;
+    p.tx0 = q.tx0; p.tx1 = q.tx1; p.ty0 = q.ty0;
+    p.key = q.key;
+}
+
 // ---- prepare (1): spans + per-tile counts ------------------------------------
 __global__ void __launch_bounds__(kBinThreads)
 tile_count_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ counters, int n_cap, int tiles_x,
@@ -155,14 +196,18 @@ tile_count_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict_
     const int s = blockIdx.x * kBinThreads + threadIdx.x;
     if (blockIdx.x * kBinThreads >= nc) return;
     const Prim q = load_prim(recs, s, nc, tiles_x, tiles_y);
+    publish_prim(sm, q);
+#pragma unroll
+    for (int k = 0; k < kSpanRows; k++) sm.span[threadIdx.x][k] = (uint16_t)kEmptySpan;
+    __syncwarp();
+    // tiles.py:75-91, one exact row interval per tile row (warp-flattened rows)
+    warp_flat(sm, q.spans ? q.ty1 - q.ty0 + 1 : 0, [&](int t, int k) {
+        const PrimSmem& p = sm.prim[t];
+        int a, b;
+        if (sb_row_hits(p.x, p.y, p.r, p.ty0 + k, p.tx0, p.tx1, W, H, a, b))
+            sm.span[t][k] = (uint16_t)((a - p.tx0) | ((b - p.tx0) << 8));
+    });
     if (q.spans) {
-        // tiles.py:75-91, one exact row interval per tile row
-        for (int k = 0; k <= q.ty1 - q.ty0; k++) {
-            int a, b;
-            const int n = sb_row_hits(q.x, q.y, q.r, q.ty0 + k, q.tx0, q.tx1, W, H, a, b);
-            sm.span[threadIdx.x][k] = n ? (uint16_t)((a - q.tx0) | ((b - q.tx0) << 8)) : (uint16_t)kEmptySpan;
-        }
-        for (int k = q.ty1 - q.ty0 + 1; k < kSpanRows; k++) sm.span[threadIdx.x][k] = (uint16_t)kEmptySpan;
         const uint4* sp = reinterpret_cast<const uint4*>(sm.span[threadIdx.x]);
         spans_out[2 * s] = sp[0];
         spans_out[2 * s + 1] = sp[1];
@@ -275,14 +320,24 @@ scatter_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ c
             cell = c ? atomicAdd(&cursor[t], c) : 0;
         });
         __syncthreads();
-        if (q.spans) {
-            const int ww = sm.w + 1;
-            for (int k = 0; k <= q.ty1 - q.ty0; k++) {
-                const uint32_t sp = sm.span[threadIdx.x][k];
-                int32_t* row = sm.cnt + (q.ty0 + k - sm.y0) * ww + (q.tx0 - sm.x0);
-                for (int c = (int)(sp & 0xff); c <= (int)(sp >> 8); c++) keys[atomicAdd(row + c, 1)] = q.key;
+        publish_prim(sm, q);
+        __syncwarp();
+        const int ww = sm.w + 1;
+        warp_flat(sm, q.spans ? q.ty1 - q.ty0 + 1 : 0, [&](int t, int k) {
+            const PrimSmem& p = sm.prim[t];
+            const uint32_t sp = sm.span[t][k];
+            const int a = (int)(sp & 0xff), b = (int)(sp >> 8);
+            int32_t* row = sm.cnt + (p.ty0 + k - sm.y0) * ww + (p.tx0 - sm.x0);
+            // four shared cursor atomics in flight before their stores
+            for (int c = a; c <= b; c += 4) {
+                int pos[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) pos[u] = c + u <= b ? atomicAdd(row + c + u, 1) : -1;
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (pos[u] >= 0) keys[pos[u]] = p.key;
             }
-        }
+        });
     } else if (q.spans) {
         for (int k = 0; k <= q.ty1 - q.ty0; k++) {
             const uint32_t sp = sm.span[threadIdx.x][k];
@@ -294,12 +349,11 @@ scatter_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ c
 
 // ---- finish (2): per-tile sort, one CTA per tile ----------------------------
 constexpr int kSortThreads = 256;
-constexpr int kCap = 4096;       // keys sorted in shared memory at once
-constexpr int kBuckets = 1024;
+constexpr int kCap = kSortThreads * 16;   // keys sorted in one shared-memory pass
+constexpr int kBuckets = 2048;
 
 struct SortSmem {
-    unsigned long long a[kCap];
-    uint16_t b[kCap];            // bucket-distributed positions into a
+    unsigned long long b[kCap];  // keys in bucket order
     uint32_t cnt[kBuckets];
     uint32_t cur[kBuckets];
     unsigned long long red[2][kSortThreads / 32];
@@ -329,17 +383,26 @@ SB_INLINE int bucket_of(unsigned long long k, unsigned long long kmin, float sca
     return min(b, nb - 1);
 }
 
-// sorts sm.a[0, n) ascending (n <= kCap, keys distinct) and hands the key of
-// rank i to out(i, key).  Whole CTA.
-template <typename Out>
-__device__ __forceinline__ void cta_sort(SortSmem& sm, int n, Out&& out)
+// Sorts src[0, n) (global, n <= kCap, keys distinct) and hands the key of
+// rank i to out(i, key).  Whole CTA.  Keys stay in registers (thread t owns
+// items t, t + 256, ...) until they are distributed into bucket order.
+template <int kPerThread, typename Out>
+__device__ __forceinline__ void cta_sort(SortSmem& sm, const unsigned long long* __restrict__ src, int n, Out&& out)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long k[kPerThread];
     unsigned long long lo = ~0ull, hi = 0ull;
-    for (int i = tid; i < n; i += kSortThreads) {
-        const unsigned long long k = sm.a[i];
-        lo = k < lo ? k : lo;
-        hi = k > hi ? k : hi;
+#pragma unroll
+    for (int q = 0; q < kPerThread; q++) {
+        const int i = q * kSortThreads + tid;
+        k[q] = i < n ? src[i] : 0ull;
+    }
+#pragma unroll
+    for (int q = 0; q < kPerThread; q++) {
+        if (q * kSortThreads + tid < n) {
+            lo = k[q] < lo ? k[q] : lo;
+            hi = k[q] > hi ? k[q] : hi;
+        }
     }
     lo = warp_min_u64(lo);
     hi = warp_max_u64(hi);
@@ -356,13 +419,15 @@ __device__ __forceinline__ void cta_sort(SortSmem& sm, int n, Out&& out)
         hi = sm.red[1][w] > hi ? sm.red[1][w] : hi;
     }
     const float scale = (float)nb / __fadd_rn(__ull2float_rn(hi - lo), 1.0f);
-    for (int i = tid; i < n; i += kSortThreads) atomicAdd(&sm.cnt[bucket_of(sm.a[i], lo, scale, nb)], 1u);
-    __syncthreads();
-    // exclusive scan of the bucket counts: 4 consecutive buckets per thread
-    static_assert(kBuckets == 4 * kSortThreads, "scan layout");
-    uint32_t c[4], s = 0;
 #pragma unroll
-    for (int q = 0; q < 4; q++) { c[q] = 4 * tid + q < nb ? sm.cnt[4 * tid + q] : 0u; s += c[q]; }
+    for (int q = 0; q < kPerThread; q++)
+        if (q * kSortThreads + tid < n) atomicAdd(&sm.cnt[bucket_of(k[q], lo, scale, nb)], 1u);
+    __syncthreads();
+    // exclusive scan of the bucket counts: 8 consecutive buckets per thread
+    static_assert(kBuckets == 8 * kSortThreads, "scan layout");
+    uint32_t c[8], s = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) { c[q] = 8 * tid + q < nb ? sm.cnt[8 * tid + q] : 0u; s += c[q]; }
     uint32_t x = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -372,26 +437,28 @@ __device__ __forceinline__ void cta_sort(SortSmem& sm, int n, Out&& out)
     if (lane == 31) sm.wsum[warp] = x;
     __syncthreads();
     uint32_t run = x - s;
-    for (int w = 0; w < warp; w++) run += sm.wsum[w];
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-        if (4 * tid + q < nb) sm.cur[4 * tid + q] = run;
+    for (int w = 0; w < kSortThreads / 32; w++) run += w < warp ? sm.wsum[w] : 0u;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        if (8 * tid + q < nb) sm.cur[8 * tid + q] = run;
         run += c[q];
     }
     __syncthreads();
-    for (int i = tid; i < n; i += kSortThreads) {
-        const uint32_t p = atomicAdd(&sm.cur[bucket_of(sm.a[i], lo, scale, nb)], 1u);
-        sm.b[p] = (uint16_t)i;
-    }
+#pragma unroll
+    for (int q = 0; q < kPerThread; q++)
+        if (q * kSortThreads + tid < n) sm.b[atomicAdd(&sm.cur[bucket_of(k[q], lo, scale, nb)], 1u)] = k[q];
     __syncthreads();
     // rank = bucket start + number of smaller keys in the bucket (cur = end now)
-    for (int i = tid; i < n; i += kSortThreads) {
-        const unsigned long long k = sm.a[sm.b[i]];
-        const int bk = bucket_of(k, lo, scale, nb);
-        const uint32_t end = sm.cur[bk], beg = end - sm.cnt[bk];
-        uint32_t r = 0;
-        for (uint32_t j = beg; j < end; j++) r += sm.a[sm.b[j]] < k ? 1u : 0u;
-        out(beg + r, k);
+#pragma unroll
+    for (int q = 0; q < kPerThread; q++) {
+        if (q * kSortThreads + tid < n) {
+            const int bq = bucket_of(k[q], lo, scale, nb);
+            const uint32_t end = sm.cur[bq], beg = end - sm.cnt[bq];
+            uint32_t r = 0;
+            for (uint32_t j = beg; j < end; j++) r += sm.b[j] < k[q] ? 1u : 0u;
+            out(beg + r, k[q]);
+        }
     }
     __syncthreads();
 }
@@ -406,7 +473,7 @@ SB_INLINE int lower_bound_u64(const unsigned long long* src, int n, unsigned lon
     return lo;
 }
 
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, 4)
 tile_sort_kernel(const int32_t* __restrict__ offsets, unsigned long long* __restrict__ keys,
                  unsigned long long* __restrict__ scratch, int32_t* __restrict__ prims)
 {
@@ -418,10 +485,13 @@ tile_sort_kernel(const int32_t* __restrict__ offsets, unsigned long long* __rest
         if (L == 1 && tid == 0) prims[off] = (int32_t)(uint32_t)keys[off];
         return;
     }
+    const auto to_prims = [&](int pos, unsigned long long k) { prims[off + pos] = (int32_t)(uint32_t)k; };
+    if (L <= 4 * kSortThreads) {
+        cta_sort<4>(sm, keys + off, L, to_prims);
+        return;
+    }
     if (L <= kCap) {
-        for (int i = tid; i < L; i += kSortThreads) sm.a[i] = keys[off + i];
-        __syncthreads();
-        cta_sort(sm, L, [&](int pos, unsigned long long k) { prims[off + pos] = (int32_t)(uint32_t)k; });
+        cta_sort<16>(sm, keys + off, L, to_prims);
         return;
     }
     // long list: sorted chunks of kCap into scratch, then pairwise merges
@@ -429,9 +499,7 @@ tile_sort_kernel(const int32_t* __restrict__ offsets, unsigned long long* __rest
     unsigned long long* dst = keys + off;
     for (int c0 = 0; c0 < L; c0 += kCap) {
         const int n = min(kCap, L - c0);
-        for (int i = tid; i < n; i += kSortThreads) sm.a[i] = keys[off + c0 + i];
-        __syncthreads();
-        cta_sort(sm, n, [&](int pos, unsigned long long k) { src[c0 + pos] = k; });
+        cta_sort<16>(sm, keys + off + c0, n, [&](int pos, unsigned long long k) { src[c0 + pos] = k; });
     }
     for (int width = kCap; width < L; width *= 2) {
         const bool final_pass = 2 * width >= L;
