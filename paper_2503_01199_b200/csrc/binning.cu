@@ -20,7 +20,7 @@
 //                | compact slot) through shared-memory cursors (order inside
 //                a tile is arbitrary at this point);
 //            (2) per-tile sort, one CTA per tile, in shared memory: keys are
-//                distributed over up to 2048 buckets by a monotone map of the
+//                distributed over >= L buckets by a monotone map of the
 //                key (float-rounded offset from the tile's minimum), and each
 //                key's final position is its bucket start plus the number of
 //                smaller keys in its bucket.  Lists longer than the shared
@@ -350,12 +350,12 @@ scatter_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ c
 // ---- finish (2): per-tile sort, one CTA per tile ----------------------------
 constexpr int kSortThreads = 256;
 constexpr int kCap = kSortThreads * 16;   // keys sorted in one shared-memory pass
-constexpr int kBuckets = 2048;
+constexpr int kMaxBuckets = kCap;         // at most one key per bucket on average
 
 struct SortSmem {
-    unsigned long long b[kCap];  // keys in bucket order
-    uint32_t cnt[kBuckets];
-    uint32_t cur[kBuckets];
+    unsigned long long b[kCap];           // keys in bucket order
+    uint32_t cnt[kMaxBuckets / 2];        // packed 16-bit bucket counts (bucket 2w in the low half)
+    uint32_t cur[kMaxBuckets / 2];        // packed 16-bit bucket cursors
     unsigned long long red[2][kSortThreads / 32];
     uint32_t wsum[kSortThreads / 32];
 };
@@ -383,22 +383,27 @@ SB_INLINE int bucket_of(unsigned long long k, unsigned long long kmin, float sca
     return min(b, nb - 1);
 }
 
-// Sorts src[0, n) (global, n <= kCap, keys distinct) and hands the key of
-// rank i to out(i, key).  Whole CTA.  Keys stay in registers (thread t owns
-// items t, t + 256, ...) until they are distributed into bucket order.
-template <int kPerThread, typename Out>
+SB_INLINE uint32_t half_of(uint32_t word, int b) { return (word >> (16 * (b & 1))) & 0xffffu; }
+
+// Sorts src[0, n) (global, n <= 256 * PER, keys distinct) and hands the key
+// of rank i to out(i, key).  Whole CTA.  Keys stay in registers (thread t
+// owns items t, t + 256, ...) until they are distributed, through 256 * PER
+// buckets (<= one key per bucket on average), into bucket order; a key's
+// rank is then its bucket start plus the smaller keys of its bucket.
+template <int PER, typename Out>
 __device__ __forceinline__ void cta_sort(SortSmem& sm, const unsigned long long* __restrict__ src, int n, Out&& out)
 {
+    constexpr int NB = kSortThreads * PER;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    unsigned long long k[kPerThread];
+    unsigned long long k[PER];
     unsigned long long lo = ~0ull, hi = 0ull;
 #pragma unroll
-    for (int q = 0; q < kPerThread; q++) {
+    for (int q = 0; q < PER; q++) {
         const int i = q * kSortThreads + tid;
         k[q] = i < n ? src[i] : 0ull;
     }
 #pragma unroll
-    for (int q = 0; q < kPerThread; q++) {
+    for (int q = 0; q < PER; q++) {
         if (q * kSortThreads + tid < n) {
             lo = k[q] < lo ? k[q] : lo;
             hi = k[q] > hi ? k[q] : hi;
@@ -406,9 +411,8 @@ __device__ __forceinline__ void cta_sort(SortSmem& sm, const unsigned long long*
     }
     lo = warp_min_u64(lo);
     hi = warp_max_u64(hi);
-    // about one key per bucket: nb = smallest power of two >= n, <= kBuckets
-    const int nb = min(kBuckets, 1 << (32 - __clz(max(n - 1, 1))));
-    for (int i = tid; i < nb; i += kSortThreads) sm.cnt[i] = 0;
+#pragma unroll
+    for (int q = 0; q < PER / 2; q++) sm.cnt[q * kSortThreads + tid] = 0;
     if (lane == 0) { sm.red[0][warp] = lo; sm.red[1][warp] = hi; }
     __syncthreads();
     lo = sm.red[0][0];
@@ -418,16 +422,24 @@ __device__ __forceinline__ void cta_sort(SortSmem& sm, const unsigned long long*
         lo = sm.red[0][w] < lo ? sm.red[0][w] : lo;
         hi = sm.red[1][w] > hi ? sm.red[1][w] : hi;
     }
-    const float scale = (float)nb / __fadd_rn(__ull2float_rn(hi - lo), 1.0f);
+    const float scale = (float)NB / __fadd_rn(__ull2float_rn(hi - lo), 1.0f);
 #pragma unroll
-    for (int q = 0; q < kPerThread; q++)
-        if (q * kSortThreads + tid < n) atomicAdd(&sm.cnt[bucket_of(k[q], lo, scale, nb)], 1u);
+    for (int q = 0; q < PER; q++) {
+        if (q * kSortThreads + tid < n) {
+            const int bq = bucket_of(k[q], lo, scale, NB);
+            atomicAdd(&sm.cnt[bq >> 1], 1u << (16 * (bq & 1)));
+        }
+    }
     __syncthreads();
-    // exclusive scan of the bucket counts: 8 consecutive buckets per thread
-    static_assert(kBuckets == 8 * kSortThreads, "scan layout");
-    uint32_t c[8], s = 0;
+    // exclusive scan of the counts: buckets [PER t, PER (t + 1)) per thread
+    uint32_t c[PER], s = 0;
 #pragma unroll
-    for (int q = 0; q < 8; q++) { c[q] = 8 * tid + q < nb ? sm.cnt[8 * tid + q] : 0u; s += c[q]; }
+    for (int q = 0; q < PER / 2; q++) {
+        const uint32_t wd = sm.cnt[tid * (PER / 2) + q];
+        c[2 * q] = wd & 0xffffu;
+        c[2 * q + 1] = wd >> 16;
+        s += c[2 * q] + c[2 * q + 1];
+    }
     uint32_t x = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -440,25 +452,39 @@ __device__ __forceinline__ void cta_sort(SortSmem& sm, const unsigned long long*
 #pragma unroll
     for (int w = 0; w < kSortThreads / 32; w++) run += w < warp ? sm.wsum[w] : 0u;
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-        if (8 * tid + q < nb) sm.cur[8 * tid + q] = run;
-        run += c[q];
+    for (int q = 0; q < PER / 2; q++) {
+        const uint32_t r0 = run, r1 = run + c[2 * q];
+        sm.cur[tid * (PER / 2) + q] = r0 | (r1 << 16);
+        run = r1 + c[2 * q + 1];
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < kPerThread; q++)
-        if (q * kSortThreads + tid < n) sm.b[atomicAdd(&sm.cur[bucket_of(k[q], lo, scale, nb)], 1u)] = k[q];
-    __syncthreads();
-    // rank = bucket start + number of smaller keys in the bucket (cur = end now)
-#pragma unroll
-    for (int q = 0; q < kPerThread; q++) {
+    for (int q = 0; q < PER; q++) {
         if (q * kSortThreads + tid < n) {
-            const int bq = bucket_of(k[q], lo, scale, nb);
-            const uint32_t end = sm.cur[bq], beg = end - sm.cnt[bq];
-            uint32_t r = 0;
-            for (uint32_t j = beg; j < end; j++) r += sm.b[j] < k[q] ? 1u : 0u;
-            out(beg + r, k[q]);
+            const int bq = bucket_of(k[q], lo, scale, NB);
+            const uint32_t old = atomicAdd(&sm.cur[bq >> 1], 1u << (16 * (bq & 1)));
+            sm.b[half_of(old, bq)] = k[q];
         }
+    }
+    __syncthreads();
+    // rank = bucket start + number of smaller keys in the bucket (cur = end
+    // now).  Walk the keys in bucket order: neighbouring threads share
+    // buckets, and buckets of up to 8 keys need no loop.
+    for (int i = tid; i < n; i += kSortThreads) {
+        const unsigned long long key = sm.b[i];
+        const int bq = bucket_of(key, lo, scale, NB);
+        const uint32_t end = half_of(sm.cur[bq >> 1], bq), beg = end - half_of(sm.cnt[bq >> 1], bq);
+        uint32_t r = 0;
+        if (end - beg <= 8) {
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const uint32_t q = min(beg + j, end - 1);
+                r += (beg + j < end && sm.b[q] < key) ? 1u : 0u;
+            }
+        } else {
+            for (uint32_t j = beg; j < end; j++) r += sm.b[j] < key ? 1u : 0u;
+        }
+        out(beg + r, key);
     }
     __syncthreads();
 }
@@ -488,6 +514,10 @@ tile_sort_kernel(const int32_t* __restrict__ offsets, unsigned long long* __rest
     const auto to_prims = [&](int pos, unsigned long long k) { prims[off + pos] = (int32_t)(uint32_t)k; };
     if (L <= 4 * kSortThreads) {
         cta_sort<4>(sm, keys + off, L, to_prims);
+        return;
+    }
+    if (L <= 8 * kSortThreads) {
+        cta_sort<8>(sm, keys + off, L, to_prims);
         return;
     }
     if (L <= kCap) {

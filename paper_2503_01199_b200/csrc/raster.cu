@@ -46,11 +46,11 @@ constexpr int kWarpsPerBlock = 4;
 constexpr int kThreads = kWarpsPerBlock * 32;
 
 // staged record: raw conic (for the backward fold) plus the log2-domain
-// exponent coefficients
+// exponent coefficients and log2(opacity), so alpha_raw = ex2(e + log2 o)
 struct __align__(16) SRec {
     float x, y, A, B;        // A = -log2e/2 a, B = -log2e b
     float Cq, o, r, g;       // Cq = -log2e/2 c
-    float bl, nB, nC2, pad;  // nB = -B, nC2 = -2 Cq
+    float bl, lg2o, inv_o, pad;
     float a, b, c;
     int32_t slot;
 };
@@ -82,9 +82,47 @@ SB_INLINE void commit_chunk(SRec* slab, const Prefetch& pf, int cnt, int lane) {
         float4* d = reinterpret_cast<float4*>(slab + lane);
         d[0] = make_float4(pf.a.x, pf.a.y, A, B);
         d[1] = make_float4(Cq, pf.b.y, pf.b.z, pf.b.w);
-        d[2] = make_float4(pf.bl, -B, -2.0f * Cq, 0.f);
+        d[2] = make_float4(pf.bl, __log2f(pf.b.y), 1.0f / pf.b.y, 0.f);
         d[3] = make_float4(pf.a.z, pf.a.w, pf.b.x, __int_as_float(pf.slot));
     }
+}
+
+// Can the record reach alpha >= alpha_min at any pixel centre of the tile?
+// The minimum of the (positive-definite) quadratic form Q over the centre
+// rectangle [X0, X1] x [Y0, Y1] is 0 if the mean is inside, else the least of
+// the four edge minima (a convex 1-D quadratic per edge, minimiser clamped).
+// alpha = min(o G, alpha_max) >= alpha_min needs -Q/2 >= ln(alpha_min / o);
+// the 1e-3 (log2 units) slack covers the rounding of e and of ex2.  A NaN
+// anywhere keeps the record.
+SB_INLINE bool can_contribute(const Prefetch& pf, float X0, float X1, float Y0, float Y1, float amin) {
+    const float mx = pf.a.x, my = pf.a.y, a = pf.a.z, b = pf.a.w, c = pf.b.x, o = pf.b.y;
+    float q = 0.0f;
+    if (!(mx >= X0 && mx <= X1 && my >= Y0 && my <= Y1)) {
+        float best = INFINITY;
+        const float Xs[2] = {X0, X1}, Ys[2] = {Y0, Y1};
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+            const float dx = mx - Xs[e];
+            const float dy = fminf(fmaxf(-b * dx / c, my - Y1), my - Y0);
+            best = fminf(best, fmaf(a * dx, dx, fmaf(2.0f * b * dx, dy, c * dy * dy)));
+        }
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+            const float dy = my - Ys[e];
+            const float dx = fminf(fmaxf(-b * dy / a, mx - X1), mx - X0);
+            best = fminf(best, fmaf(a * dx, dx, fmaf(2.0f * b * dx, dy, c * dy * dy)));
+        }
+        q = best;
+    }
+    return !(q * 0.72134752f > __log2f(o / amin) + 1e-3f);
+}
+
+// ballot of the chunk's records that can contribute to the tile
+SB_INLINE unsigned chunk_mask(const Prefetch& pf, int cnt, int lane, int x0, int y0, int W, int H, float amin) {
+    const bool keep = lane < cnt &&
+                      can_contribute(pf, (float)x0, (float)min(x0 + SB_TILE_W - 1, W - 1), (float)y0,
+                                     (float)min(y0 + SB_TILE_H - 1, H - 1), amin);
+    return __ballot_sync(0xffffffffu, keep);
 }
 
 SB_INLINE float ex2(float x) {
@@ -93,17 +131,33 @@ SB_INLINE float ex2(float x) {
     return y;
 }
 
-// G at the lane's 4 run pixels: e0 = A dx^2 + B dx dy + Cq dy^2 (log2
-// units), e_i = e0 + l2 i + Cq i^2 with l2 = -(B dx + 2 Cq dy)
-SB_INLINE void lane_G(const SRec& r, float px, float py0, float G[4], float& dx, float& dy) {
+// log2 G at the lane's 4 run pixels: e0 = A dx^2 + B dx dy + Cq dy^2, and
+// with t = B dx + 2 Cq dy, e_i = e0 - t i + Cq i^2
+SB_INLINE void lane_expo(const SRec& r, float px, float py0, float e[4], float& dx, float& dy) {
     dx = r.x - px;
     dy = r.y - py0;
-    const float e0 = fmaf(fmaf(r.A, dx, r.B * dy), dx, (r.Cq * dy) * dy);
-    const float l2 = fmaf(r.nB, dx, r.nC2 * dy);
-    G[0] = ex2(e0);
-    G[1] = ex2(e0 + (l2 + r.Cq));
-    G[2] = ex2(fmaf(4.0f, r.Cq, fmaf(2.0f, l2, e0)));
-    G[3] = ex2(fmaf(9.0f, r.Cq, fmaf(3.0f, l2, e0)));
+    const float cqdy = r.Cq * dy;
+    e[0] = fmaf(fmaf(r.A, dx, r.B * dy), dx, cqdy * dy);
+    const float t = fmaf(cqdy, 2.0f, r.B * dx);
+    e[1] = e[0] + (r.Cq - t);
+    e[2] = fmaf(-2.0f, t, fmaf(4.0f, r.Cq, e[0]));
+    e[3] = fmaf(-3.0f, t, fmaf(9.0f, r.Cq, e[0]));
+}
+
+// G (the half path rounds G itself to binary16)
+SB_INLINE void lane_G(const SRec& r, float px, float py0, float G[4], float& dx, float& dy) {
+    float e[4];
+    lane_expo(r, px, py0, e, dx, dy);
+#pragma unroll
+    for (int i = 0; i < 4; i++) G[i] = ex2(e[i]);
+}
+
+// o * G = ex2(e + log2 o)
+SB_INLINE void lane_alpha_raw(const SRec& r, float px, float py0, float araw[4], float& dx, float& dy) {
+    float e[4];
+    lane_expo(r, px, py0, e, dx, dy);
+#pragma unroll
+    for (int i = 0; i < 4; i++) araw[i] = ex2(e[i] + r.lg2o);
 }
 
 SB_INLINE int next_tile(int* counter, int lane) {
@@ -155,9 +209,12 @@ raster_fwd_kernel(FwdParams p)
             const int cnt = min(32, n - k0);
             __syncwarp();
             commit_chunk(slab, pf, cnt, lane);
+            unsigned todo = chunk_mask(pf, cnt, lane, x0, y0, p.W, p.H, p.amin);
             __syncwarp();
             if (k0 + 32 < n) prefetch_chunk(pf, p.recs, p.prims, beg, k0 + 32, min(32, n - k0 - 32), lane);
-            for (int j = 0; j < cnt; j++) {
+            while (todo) {
+                const int j = __ffs(todo) - 1;
+                todo &= todo - 1;
                 const bool live = fmaxf(fmaxf(T[0], T[1]), fmaxf(T[2], T[3])) >= p.tstop;
                 if (!__any_sync(0xffffffffu, live)) {
                     done = true;
@@ -165,11 +222,11 @@ raster_fwd_kernel(FwdParams p)
                 }
                 if (!live) continue;
                 const SRec& r = slab[j];
-                float G[4], dx, dy;
-                lane_G(r, px, py0, G, dx, dy);
+                float araw[4], dx, dy;
+                lane_alpha_raw(r, px, py0, araw, dx, dy);
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
-                    const float alpha = fminf(r.o * G[i], p.amax);
+                    const float alpha = fminf(araw[i], p.amax);
                     if (T[i] >= p.tstop && alpha >= p.amin) {
                         // T (which decides termination / frag counts) keeps
                         // numpy's rounding; the colour sum may fuse
@@ -232,9 +289,12 @@ raster_fwd_half_kernel(FwdParams p)
             const int cnt = min(32, n - k0);
             __syncwarp();
             commit_chunk(slab, pf, cnt, lane);
+            unsigned todo = chunk_mask(pf, cnt, lane, x0, y0, p.W, p.H, p.amin);
             __syncwarp();
             if (k0 + 32 < n) prefetch_chunk(pf, p.recs, p.prims, beg, k0 + 32, min(32, n - k0 - 32), lane);
-            for (int j = 0; j < cnt; j++) {
+            while (todo) {
+                const int j = __ffs(todo) - 1;
+                todo &= todo - 1;
                 bool live = false;
 #pragma unroll
                 for (int i = 0; i < 4; i++) live |= valid[i] && __hge(T[i], tstop);
@@ -378,16 +438,17 @@ SB_INLINE float row_exp_aligned(const float v[32]) {
     for (int l = 0; l < 32; l++) mx = fmaxf(mx, fabsf(v[l]));
     if (mx == 0.0f) return 0.0f;
     const int emax = f32_exponent(__float_as_uint(mx));
-    int sh = 23 - emax;               // in [-104, 172]
-    float pre = 1.0f;
-    if (sh > 126) {                   // all values below 2^-103: two steps
-        pre = __int_as_float((127 + 64) << 23);
-        sh -= 64;
-    }
-    const float scale = __int_as_float((127 + sh) << 23);
+    const int sh = 23 - emax;         // in [-104, 172]
     int total = 0;
+    if (sh <= 126) {
+        const float scale = __int_as_float((127 + sh) << 23);
 #pragma unroll
-    for (int l = 0; l < 32; l++) total += __float2int_rn((v[l] * pre) * scale);
+        for (int l = 0; l < 32; l++) total += __float2int_rn(v[l] * scale);
+    } else {                          // all values below 2^-103: two steps
+        const float scale = __int_as_float((127 + sh - 64) << 23), pre = __int_as_float((127 + 64) << 23);
+#pragma unroll
+        for (int l = 0; l < 32; l++) total += __float2int_rn((v[l] * pre) * scale);
+    }
     const double out = __longlong_as_double((long long)(emax - 23 + 1023) << 52);
     return __double2float_rn((double)total * out);
 }
@@ -449,7 +510,10 @@ SB_INLINE void flush_batch(BwdWarpSmem& ws, int nb, int lane, int conic_tree, sb
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(kThreads, 4)
+// 3 warps x 6 blocks = 18 warps per SM (shared memory: 6 x 37 KB)
+constexpr int kBwdWarps = 3;
+
+__global__ void __launch_bounds__(kBwdWarps * 32, 6)
 raster_bwd_kernel(BwdParams p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -486,20 +550,22 @@ raster_bwd_kernel(BwdParams p)
             const int k0 = max(0, k1 - 32), cnt = k1 - k0;
             __syncwarp();
             commit_chunk(ws.slab, pf, cnt, lane);
+            unsigned todo = chunk_mask(pf, cnt, lane, x0, y0, p.W, p.H, p.amin);
             __syncwarp();
             if (k0 > 0) prefetch_chunk(pf, p.recs, p.prims, beg, max(0, k0 - 32), k0 - max(0, k0 - 32), lane);
-            for (int j = cnt - 1; j >= 0; j--) {
+            while (todo) {
+                const int j = 31 - __clz(todo);
+                todo &= ~(1u << j);
                 const int k = k0 + j;
                 if (!__any_sync(0xffffffffu, k < lane_max)) continue;
                 const SRec& r = ws.slab[j];
-                float G[4], dx, dy;
-                lane_G(r, px, py0, G, dx, dy);
-                float araw[4], alpha[4];
+                float araw[4], dx, dy;
+                lane_alpha_raw(r, px, py0, araw, dx, dy);
+                float alpha[4];
                 bool ci[4];
                 bool any_c = false;
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
-                    araw[i] = r.o * G[i];
                     alpha[i] = fminf(araw[i], p.amax);
                     // contributing: before this pixel's last contributor and usable
                     ci[i] = (k < last[i]) && (alpha[i] >= p.amin);
@@ -507,26 +573,22 @@ raster_bwd_kernel(BwdParams p)
                 }
                 if (!__any_sync(0xffffffffu, any_c)) continue;
                 float f[4], uG[4], w[4];
-#pragma unroll
-                for (int i = 0; i < 4; i++) f[i] = uG[i] = w[i] = 0.0f;
-                if (any_c) {
-#pragma unroll
-                    for (int i = 0; i < 4; i++) {
-                        const float inv = rcp_approx(1.0f - alpha[i]);
-                        const float Tb = T[i] * inv;
-                        const float dc = fmaf(dI[i][2], r.bl, fmaf(dI[i][1], r.g, dI[i][0] * r.r));
-                        const float da = fmaf(Tb, dc, -Sd[i] * inv);
-                        // gradient through a clamped alpha is zero (backward.py:128,169)
-                        f[i] = (ci[i] && araw[i] < p.amax) ? da * G[i] : 0.0f;
-                        uG[i] = f[i] * r.o;
-                        w[i] = ci[i] ? Tb * alpha[i] : 0.0f;
-                        Sd[i] = fmaf(w[i], dc, Sd[i]);
-                        T[i] = ci[i] ? Tb : T[i];
-                    }
-                }
                 int cnt_l = 0;
 #pragma unroll
-                for (int i = 0; i < 4; i++) cnt_l += ci[i] ? 1 : 0;
+                for (int i = 0; i < 4; i++) {
+                    const float inv = rcp_approx(1.0f - alpha[i]);
+                    const float Tb = T[i] * inv;
+                    const float dc = fmaf(dI[i][2], r.bl, fmaf(dI[i][1], r.g, dI[i][0] * r.r));
+                    const float da = fmaf(Tb, dc, -Sd[i] * inv);
+                    // u G = dL/dalpha o G; gradient through a clamped alpha is
+                    // zero (backward.py:128,169); f = dL/do = u G / o
+                    uG[i] = (ci[i] && araw[i] < p.amax) ? da * araw[i] : 0.0f;
+                    f[i] = uG[i] * r.inv_o;
+                    w[i] = ci[i] ? Tb * alpha[i] : 0.0f;
+                    Sd[i] = fmaf(w[i], dc, Sd[i]);
+                    T[i] = ci[i] ? Tb : T[i];
+                    cnt_l += ci[i] ? 1 : 0;
+                }
                 // scanline_grad_fold (backward.py:175-196) + per-lane partials
                 const float gb = ((uG[0] + uG[1]) + uG[2]) + uG[3];
                 const float gl = fmaf(uG[3], 3.0f, fmaf(uG[2], 2.0f, uG[1]));
@@ -600,15 +662,15 @@ void sb_launch_raster_bwd(const RasterRec* recs, const int32_t* offsets, const i
     p.conic_tree = cfg.conic_reduce == 1;
     p.tile_counter = tile_counter;
     p.dL_dI = dL_dI; p.T_final = T_final; p.last = last; p.grads = grads;
-    const int want = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    const int blocks = min(want, sm_count() * 4);
-    const int smem = (int)sizeof(BwdWarpSmem) * kWarpsPerBlock;
+    const int want = (ntiles + kBwdWarps - 1) / kBwdWarps;
+    const int blocks = min(want, sm_count() * 6);
+    const int smem = (int)sizeof(BwdWarpSmem) * kBwdWarps;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    if (blocks) raster_bwd_kernel<<<blocks, kThreads, smem, stream>>>(p);
+    if (blocks) raster_bwd_kernel<<<blocks, kBwdWarps * 32, smem, stream>>>(p);
 }
 
 // ---- standalone lane reductions (reduction.py:21-58), for parity tests ----
