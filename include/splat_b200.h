@@ -121,10 +121,10 @@ int sb_raster_bwd(const void* recs, const int32_t* tile_offsets, const int32_t* 
 /* backward.py:272-278 (_chain_projection 384-516 + scatter_grads
  * ccc.py:197-216 + stats np.add.at): grads (N, 16) float32 for every row
  * (zero for culled clusters); S, M (float64) and C (int32) accumulated in
- * place when non-NULL. */
+ * place when non-NULL.  recs are the forward's compact records (validity). */
 int sb_chain_projection_bwd(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
-                            const int32_t* cluster_offset, const sb_screen_grad* sgrad, float* grads, double* S,
-                            double* M, int32_t* C, sb_stream_t stream);
+                            const int32_t* cluster_offset, const void* recs, const sb_screen_grad* sgrad,
+                            float* grads, double* S, double* M, int32_t* C, sb_stream_t stream);
 
 /* ---- optimiser / densification ------------------------------------------- */
 /* optim.py:69-98: Adam (0.9, 0.999, 1e-15) on rows of true-masked clusters;

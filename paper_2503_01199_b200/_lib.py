@@ -39,7 +39,7 @@ SIGNATURES = {
     "sb_raster_workspace_bytes": ([], SZ),
     "sb_raster_fwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_raster_bwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, VP, SZ, VP], C.c_int),
-    "sb_chain_projection_bwd": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP], C.c_int),
+    "sb_chain_projection_bwd": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP], C.c_int),
     "sb_adam_sparse": ([VP, VP, VP, VP, VP, VP, I64, VP, VP], C.c_int),
     "sb_variance_score": ([VP, VP, VP, I64, VP, VP], C.c_int),
     "sb_lane_reduce": ([VP, I64, C.c_int, VP, VP, VP], C.c_int),

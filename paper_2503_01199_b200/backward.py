@@ -135,7 +135,7 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
               _lib.ptr(sgrad), ctx.n_compact, _lib.ptr(ws_r), ws_r.numel(), stream)
     grads = torch.empty((n, 16), dtype=torch.float32, device=dev)
     _lib.call("sb_chain_projection_bwd", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s),
-              _lib.ptr(ctx.cluster_offset), _lib.ptr(sgrad), _lib.ptr(grads), _lib.ptr(stats.S),
+              _lib.ptr(ctx.cluster_offset), _lib.ptr(ctx.recs), _lib.ptr(sgrad), _lib.ptr(grads), _lib.ptr(stats.S),
               _lib.ptr(stats.M), _lib.ptr(stats.C), stream)
     return BackwardResult(grads=SceneGrads(grads), stats=stats, cluster_mask=ctx.cluster_vis.bool())
 

@@ -22,7 +22,8 @@ void sb_launch_raster_fwd(const RasterRec*, const int32_t*, const int32_t*, int,
 void sb_launch_raster_bwd(const RasterRec*, const int32_t*, const int32_t*, int, int, int, int, const sb_raster_cfg&,
                           int*, const float*, const float*, const int32_t*, sb_screen_grad*, cudaStream_t);
 void sb_launch_lane_reduce(const float*, int, int, float*, double*, cudaStream_t);
-void sb_launch_chain(const float*, int, const CamDev&, const int32_t*, const sb_screen_grad*, float*, double*,
+void sb_launch_chain(const float*, int, const CamDev&, const int32_t*, const RasterRec*, const sb_screen_grad*, float*,
+                     double*,
                      double*, int32_t*, cudaStream_t);
 void sb_launch_adam(float*, const float*, float*, float*, int32_t*, const uint8_t*, int, const double[5],
                     cudaStream_t);
@@ -213,12 +214,13 @@ int sb_raster_bwd(const void* recs, const int32_t* tile_offsets, const int32_t* 
 }
 
 int sb_chain_projection_bwd(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
-                            const int32_t* cluster_offset, const sb_screen_grad* sgrad, float* grads, double* S_,
-                            double* M_, int32_t* C_, sb_stream_t stream) {
+                            const int32_t* cluster_offset, const void* recs, const sb_screen_grad* sgrad,
+                            float* grads, double* S_, double* M_, int32_t* C_, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
     const CamDev d = make_cam(cam, cfg);
-    sb_launch_chain(params, (int)n, d, cluster_offset, sgrad, grads, S_, M_, C_, S(stream));
+    sb_launch_chain(params, (int)n, d, cluster_offset, static_cast<const RasterRec*>(recs), sgrad, grads, S_, M_, C_,
+                    S(stream));
     return check_launch("sb_chain_projection_bwd");
 }
 

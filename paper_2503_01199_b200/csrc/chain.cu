@@ -23,10 +23,10 @@ SB_INLINE void rotmat_grad_to_quat(const double d[3][3], const double q[4], doub
                     y * d[1][2]) + x * d[2][0]) + y * d[2][1]);
 }
 
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256)
 chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t* __restrict__ cluster_offset,
-             const sb_screen_grad* __restrict__ sg, float4* __restrict__ grads, double* __restrict__ stat_S,
-             double* __restrict__ stat_M, int32_t* __restrict__ stat_C)
+             const RasterRec* __restrict__ recs, const sb_screen_grad* __restrict__ sg, float4* __restrict__ grads,
+             double* __restrict__ stat_S, double* __restrict__ stat_M, int32_t* __restrict__ stat_C)
 {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
@@ -43,8 +43,11 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
             const float4 v = __ldg(row + k);
             p[4 * k] = v.x; p[4 * k + 1] = v.y; p[4 * k + 2] = v.z; p[4 * k + 3] = v.w;
         }
+        // intermediates of the projection; activations to float32 accuracy,
+        // validity exactly as the forward decided it (record flags)
         ProjOut o;
-        sb_project(p, cam, o);
+        sb_project<false>(p, cam, o);
+        o.valid = (__float_as_uint(__ldg(reinterpret_cast<const float*>(recs + slot) + 11)) & 1u) != 0;
         const sb_screen_grad s = sg[slot];
         // activation chains (backward.py:403-404): sigmoid' in float32, product in float64
         const float gcol[3] = {s.r, s.g, s.bl};
@@ -194,11 +197,13 @@ __global__ void variance_kernel(const double* __restrict__ S, const double* __re
 }  // namespace
 
 void sb_launch_chain(const float* params, int n, const CamDev& cam, const int32_t* cluster_offset,
-                     const sb_screen_grad* sg, float* grads, double* S, double* M, int32_t* C, cudaStream_t stream)
+                     const RasterRec* recs, const sb_screen_grad* sg, float* grads, double* S, double* M, int32_t* C,
+                     cudaStream_t stream)
 {
     if (n <= 0) return;
     chain_kernel<<<(n + 255) / 256, 256, 0, stream>>>(reinterpret_cast<const float4*>(params), n, cam,
-                                                      cluster_offset, sg, reinterpret_cast<float4*>(grads), S, M, C);
+                                                      cluster_offset, recs, sg, reinterpret_cast<float4*>(grads), S,
+                                                      M, C);
 }
 
 void sb_launch_adam(float* params, const float* grads, float* m, float* v, int32_t* step, const uint8_t* mask,

@@ -91,22 +91,36 @@ struct ProjOut {
     bool valid, in_image, degenerate;
 };
 
+// kExact: activations exactly as the reference rounds them (float64 exp /
+// sigmoid / normalisation, then float32), which the bit-exact forward needs.
+// The backward chain only needs them to float32 accuracy (gradient
+// tolerance), so it uses the float32 forms.
+template <bool kExact = true>
 SB_INLINE void sb_project(const float* __restrict__ p, const CamDev& cam, ProjOut& o, double* s64 = nullptr) {
     // activations in float64, then rounded (projection.py:134-138)
     float pos[3] = {p[0], p[1], p[2]};
-    for (int k = 0; k < 3; k++) {
-        const double e = exp((double)p[SB_COL_LS + k]);
-        if (s64) s64[k] = e;
-        o.s[k] = (float)e;
+    if (kExact) {
+        for (int k = 0; k < 3; k++) {
+            const double e = exp((double)p[SB_COL_LS + k]);
+            if (s64) s64[k] = e;
+            o.s[k] = (float)e;
+        }
+        double q0 = p[SB_COL_ROT], q1 = p[SB_COL_ROT + 1], q2 = p[SB_COL_ROT + 2], q3 = p[SB_COL_ROT + 3];
+        double qn = __dsqrt_rn(DADD(DADD(DADD(DMUL(q0, q0), DMUL(q1, q1)), DMUL(q2, q2)), DMUL(q3, q3)));
+        o.q[0] = (float)DDIV(q0, qn);
+        o.q[1] = (float)DDIV(q1, qn);
+        o.q[2] = (float)DDIV(q2, qn);
+        o.q[3] = (float)DDIV(q3, qn);
+        for (int k = 0; k < 3; k++) o.col[k] = (float)sb_sigmoid((double)p[SB_COL_COL + k]);
+        o.op = (float)sb_sigmoid((double)p[SB_COL_OPA]);
+    } else {
+        for (int k = 0; k < 3; k++) o.s[k] = expf(p[SB_COL_LS + k]);
+        const float q0 = p[SB_COL_ROT], q1 = p[SB_COL_ROT + 1], q2 = p[SB_COL_ROT + 2], q3 = p[SB_COL_ROT + 3];
+        const float rn = rsqrtf(fmaf(q3, q3, fmaf(q2, q2, fmaf(q1, q1, q0 * q0))));
+        o.q[0] = q0 * rn; o.q[1] = q1 * rn; o.q[2] = q2 * rn; o.q[3] = q3 * rn;
+        for (int k = 0; k < 3; k++) o.col[k] = 1.0f / (1.0f + expf(-p[SB_COL_COL + k]));
+        o.op = 1.0f / (1.0f + expf(-p[SB_COL_OPA]));
     }
-    double q0 = p[SB_COL_ROT], q1 = p[SB_COL_ROT + 1], q2 = p[SB_COL_ROT + 2], q3 = p[SB_COL_ROT + 3];
-    double qn = __dsqrt_rn(DADD(DADD(DADD(DMUL(q0, q0), DMUL(q1, q1)), DMUL(q2, q2)), DMUL(q3, q3)));
-    o.q[0] = (float)DDIV(q0, qn);
-    o.q[1] = (float)DDIV(q1, qn);
-    o.q[2] = (float)DDIV(q2, qn);
-    o.q[3] = (float)DDIV(q3, qn);
-    for (int k = 0; k < 3; k++) o.col[k] = (float)sb_sigmoid((double)p[SB_COL_COL + k]);
-    o.op = (float)sb_sigmoid((double)p[SB_COL_OPA]);
 
     // t = pos @ R.T + trans: k-order FMA chain (numpy/OpenBLAS sgemm), then add
     for (int j = 0; j < 3; j++)
