@@ -416,13 +416,18 @@ SB_INLINE float rcp_approx(float x) {
 // per-lane partials (10 channels) to a warp-private shared-memory batch; a
 // full batch is reduced row-wise (one (fragment, channel) row of 32 lane
 // values per lane at a time) and flushed with one atomic per row.
+//   conic rows   [3 channels][8 slots][32 lanes], lane l at ((l + 4 (row & 7)) & 31)
+//   tree rows    [7 channels][4 slot pairs][32 lanes] float2 (slot b, slot b + 4),
+//                lane l's pair at ((l + 2 (row & 7)) & 31): one lane reduces both
+//                fragments of a pair with f32x2 adds (the same tree for each)
 constexpr int kBatch = 8;
-constexpr int kCh = 10;            // a b c | u v o r g bl | S
-constexpr int kRows = kBatch * kCh;
+constexpr int kConicCh = 3;        // a b c (exponent-aligned)
+constexpr int kTreeCh = 7;         // u v o r g bl S (pairwise tree)
 
 struct BwdWarpSmem {
     SRec slab[32];
-    float part[kRows * 32];        // row r = channel * kBatch + slot; lane l at ((l + 4 * (r & 7)) & 31)
+    float conic[kConicCh * kBatch * 32];
+    float2 tree[kTreeCh * (kBatch / 2) * 32];
     int slot[kBatch];
     int count[kBatch];
 };
@@ -462,13 +467,10 @@ SB_INLINE float row_tree(float v[32]) {
     return v[0];
 }
 
-// rows of a batch: row = channel * kBatch + slot, so the 3 conic channels
-// come first and all 10 stores of one fragment share the swizzle
-// (row & 7) == slot.
-static_assert(kBatch == 8, "row swizzle assumes 8 slots");
+static_assert(kBatch == 8, "row swizzles assume 8 slots");
 
-SB_INLINE void load_row(const BwdWarpSmem& ws, int row, float v[32]) {
-    const float* base = ws.part + row * 32;
+SB_INLINE void load_conic_row(const BwdWarpSmem& ws, int row, float v[32]) {
+    const float* base = ws.conic + row * 32;
 #pragma unroll
     for (int q = 0; q < 8; q++) {
         const float4 x = *reinterpret_cast<const float4*>(base + 4 * ((q + (row & 7)) & 7));
@@ -476,7 +478,27 @@ SB_INLINE void load_row(const BwdWarpSmem& ws, int row, float v[32]) {
     }
 }
 
-SB_INLINE void emit_row(const BwdWarpSmem& ws, int c, int b, float out, sb_screen_grad* grads) {
+SB_INLINE void load_tree_row(const BwdWarpSmem& ws, int row, float2 v[32]) {
+    const float2* base = ws.tree + row * 32;
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+        const float4 x = *reinterpret_cast<const float4*>(base + 2 * ((q + (row & 7)) & 15));
+        v[2 * q] = make_float2(x.x, x.y);
+        v[2 * q + 1] = make_float2(x.z, x.w);
+    }
+}
+
+// reduction.py:21-32 tree on two rows at once
+SB_INLINE float2 row_tree2(float2 v[32]) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1)
+#pragma unroll
+        for (int l = 0; l < s; l++) v[l] = __fadd2_rn(v[l], v[l + s]);
+    return v[0];
+}
+
+// channel c of the screen-gradient record: 0-2 conic, 3-8 u v o r g bl, 9 S
+SB_INLINE void emit(const BwdWarpSmem& ws, int c, int b, float out, sb_screen_grad* grads) {
     sb_screen_grad* gr = grads + ws.slot[b];
     if (c < 9) {
         atomicAdd(reinterpret_cast<float*>(gr) + c, out);
@@ -487,25 +509,22 @@ SB_INLINE void emit_row(const BwdWarpSmem& ws, int c, int b, float out, sb_scree
     }
 }
 
-// conic rows (exponent-aligned) and tree rows in separate, lane-uniform
-// passes: no lane runs both reduction paths
 SB_INLINE void flush_batch(BwdWarpSmem& ws, int nb, int lane, int conic_tree, sb_screen_grad* grads) {
     __syncwarp();
-    int first_tree = 0;
-    if (!conic_tree) {
-        first_tree = 3 * nb;
-        if (lane < 3 * nb) {
-            const int c = lane / nb, b = lane - c * nb;
-            float v[32];
-            load_row(ws, c * kBatch + b, v);
-            emit_row(ws, c, b, row_exp_aligned(v), grads);
-        }
-    }
-    for (int i = first_tree + lane; i < nb * kCh; i += 32) {
-        const int c = i / nb, b = i - c * nb;
+    if (lane < kConicCh * nb) {
+        const int c = lane / nb, b = lane - c * nb;
         float v[32];
-        load_row(ws, c * kBatch + b, v);
-        emit_row(ws, c, b, row_tree(v), grads);
+        load_conic_row(ws, c * kBatch + b, v);
+        emit(ws, c, b, conic_tree ? row_tree(v) : row_exp_aligned(v), grads);
+    }
+    const int npair = min(nb, kBatch / 2);
+    if (lane < kTreeCh * npair) {
+        const int c = lane / npair, pb = lane - c * npair;
+        float2 v[32];
+        load_tree_row(ws, c * (kBatch / 2) + pb, v);
+        const float2 out = row_tree2(v);
+        emit(ws, kConicCh + c, pb, out.x, grads);
+        if (pb + kBatch / 2 < nb) emit(ws, kConicCh + c, pb + kBatch / 2, out.y, grads);
     }
     __syncwarp();
 }
@@ -527,20 +546,30 @@ raster_bwd_kernel(BwdParams p)
         const float px = (float)pxi, py0 = (float)py0i;
         // per pixel: T (recovered back to front), dI, and Sd = dI . suffix where
         // suffix = sum_{j>k} w_j c_j + T_final bg (backward.py:155-159), so
-        // dL/dalpha = T (dI . c) - Sd / (1 - alpha)
-        float T[4], Sd[4], dI[4][3];
+        // dL/dalpha = T (dI . c) - Sd / (1 - alpha).  Pixel pairs (0,1) and
+        // (2,3) are packed in float2 for the f32x2 FMA/FMUL path.
+        float2 T2[2], Sd2[2], dI2[2][3];
         int last[4];
         int lane_max = 0;
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
-            const bool v = pxi < p.W && py0i + i < p.H;
-            const size_t pix = (size_t)(py0i + i) * p.W + pxi;
-            T[i] = v ? p.T_final[pix] : 1.0f;
-            last[i] = v ? p.last[pix] : 0;
+        for (int h = 0; h < 2; h++) {
+            float Tv[2], Sv[2], dv[2][3];
 #pragma unroll
-            for (int ch = 0; ch < 3; ch++) dI[i][ch] = v ? p.dL_dI[3 * pix + ch] : 0.0f;
-            Sd[i] = T[i] * (dI[i][0] * p.bg[0] + dI[i][1] * p.bg[1] + dI[i][2] * p.bg[2]);
-            lane_max = max(lane_max, last[i]);
+            for (int e = 0; e < 2; e++) {
+                const int i = 2 * h + e;
+                const bool v = pxi < p.W && py0i + i < p.H;
+                const size_t pix = (size_t)(py0i + i) * p.W + pxi;
+                Tv[e] = v ? p.T_final[pix] : 1.0f;
+                last[i] = v ? p.last[pix] : 0;
+#pragma unroll
+                for (int ch = 0; ch < 3; ch++) dv[e][ch] = v ? p.dL_dI[3 * pix + ch] : 0.0f;
+                Sv[e] = Tv[e] * (dv[e][0] * p.bg[0] + dv[e][1] * p.bg[1] + dv[e][2] * p.bg[2]);
+                lane_max = max(lane_max, last[i]);
+            }
+            T2[h] = make_float2(Tv[0], Tv[1]);
+            Sd2[h] = make_float2(Sv[0], Sv[1]);
+#pragma unroll
+            for (int ch = 0; ch < 3; ch++) dI2[h][ch] = make_float2(dv[0][ch], dv[1][ch]);
         }
         const int kmax = __reduce_max_sync(0xffffffffu, lane_max);
         Prefetch pf;
@@ -563,48 +592,64 @@ raster_bwd_kernel(BwdParams p)
                 lane_alpha_raw(r, px, py0, araw, dx, dy);
                 float alpha[4];
                 bool ci[4];
-                bool any_c = false;
+                unsigned cmask = 0;
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
                     alpha[i] = fminf(araw[i], p.amax);
                     // contributing: before this pixel's last contributor and usable
                     ci[i] = (k < last[i]) && (alpha[i] >= p.amin);
-                    any_c |= ci[i];
+                    cmask |= ci[i] ? 1u << i : 0u;
                 }
-                if (!__any_sync(0xffffffffu, any_c)) continue;
-                float f[4], uG[4], w[4];
-                int cnt_l = 0;
+                if (!__any_sync(0xffffffffu, cmask != 0)) continue;
+                const float2 cr = make_float2(r.r, r.r), cg = make_float2(r.g, r.g), cb = make_float2(r.bl, r.bl);
+                float2 uG2[2], w2[2];
 #pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const float inv = rcp_approx(1.0f - alpha[i]);
-                    const float Tb = T[i] * inv;
-                    const float dc = fmaf(dI[i][2], r.bl, fmaf(dI[i][1], r.g, dI[i][0] * r.r));
-                    const float da = fmaf(Tb, dc, -Sd[i] * inv);
+                for (int h = 0; h < 2; h++) {
+                    const int i0 = 2 * h, i1 = 2 * h + 1;
+                    const float2 a2 = make_float2(alpha[i0], alpha[i1]);
+                    const float2 om = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-a2.x, -a2.y));
+                    const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+                    const float2 Tb = __fmul2_rn(T2[h], inv);
+                    const float2 dc = __ffma2_rn(dI2[h][2], cb, __ffma2_rn(dI2[h][1], cg, __fmul2_rn(dI2[h][0], cr)));
+                    const float2 si = __fmul2_rn(Sd2[h], inv);
+                    const float2 da = __ffma2_rn(Tb, dc, make_float2(-si.x, -si.y));
+                    const float2 u = __fmul2_rn(da, make_float2(araw[i0], araw[i1]));
+                    const float2 tw = __fmul2_rn(Tb, a2);
                     // u G = dL/dalpha o G; gradient through a clamped alpha is
-                    // zero (backward.py:128,169); f = dL/do = u G / o
-                    uG[i] = (ci[i] && araw[i] < p.amax) ? da * araw[i] : 0.0f;
-                    f[i] = uG[i] * r.inv_o;
-                    w[i] = ci[i] ? Tb * alpha[i] : 0.0f;
-                    Sd[i] = fmaf(w[i], dc, Sd[i]);
-                    T[i] = ci[i] ? Tb : T[i];
-                    cnt_l += ci[i] ? 1 : 0;
+                    // zero (backward.py:128,169)
+                    uG2[h] = make_float2((ci[i0] && araw[i0] < p.amax) ? u.x : 0.0f,
+                                         (ci[i1] && araw[i1] < p.amax) ? u.y : 0.0f);
+                    w2[h] = make_float2(ci[i0] ? tw.x : 0.0f, ci[i1] ? tw.y : 0.0f);
+                    Sd2[h] = __ffma2_rn(w2[h], dc, Sd2[h]);
+                    T2[h] = make_float2(ci[i0] ? Tb.x : T2[h].x, ci[i1] ? Tb.y : T2[h].y);
                 }
-                // scanline_grad_fold (backward.py:175-196) + per-lane partials
-                const float gb = ((uG[0] + uG[1]) + uG[2]) + uG[3];
+                // scanline_grad_fold (backward.py:175-196) + per-lane partials;
+                // f = dL/do = u G / o, so sum f = gb / o and sum f^2 = sum (uG)^2 / o^2
+                const float uG[4] = {uG2[0].x, uG2[0].y, uG2[1].x, uG2[1].y};
+                const float2 gs = __fadd2_rn(uG2[0], uG2[1]);
+                const float gb = gs.x + gs.y;
                 const float gl = fmaf(uG[3], 3.0f, fmaf(uG[2], 2.0f, uG[1]));
                 const float gq = fmaf(uG[3], 9.0f, fmaf(uG[2], 4.0f, uG[1]));
-                float* pp = ws.part + nb * 32 + ((lane + 4 * nb) & 31);   // channel c at pp[c * 256]
-                pp[0 * 256] = gb * (-0.5f * dx * dx);
-                pp[1 * 256] = fmaf(gb, -dx * dy, gl * dx);
-                pp[2 * 256] = fmaf(gq, -0.5f, fmaf(gb, -0.5f * dy * dy, gl * dy));
-                pp[3 * 256] = fmaf(gl, r.b, -gb * fmaf(r.a, dx, r.b * dy));
-                pp[4 * 256] = fmaf(gl, r.c, -gb * fmaf(r.b, dx, r.c * dy));
-                pp[5 * 256] = ((f[0] + f[1]) + f[2]) + f[3];
-                pp[6 * 256] = fmaf(w[3], dI[3][0], fmaf(w[2], dI[2][0], fmaf(w[1], dI[1][0], w[0] * dI[0][0])));
-                pp[7 * 256] = fmaf(w[3], dI[3][1], fmaf(w[2], dI[2][1], fmaf(w[1], dI[1][1], w[0] * dI[0][1])));
-                pp[8 * 256] = fmaf(w[3], dI[3][2], fmaf(w[2], dI[2][2], fmaf(w[1], dI[1][2], w[0] * dI[0][2])));
-                pp[9 * 256] = fmaf(f[3], f[3], fmaf(f[2], f[2], fmaf(f[1], f[1], f[0] * f[0])));
-                const int C = __reduce_add_sync(0xffffffffu, cnt_l);
+                const float2 q2 = __ffma2_rn(uG2[1], uG2[1], __fmul2_rn(uG2[0], uG2[0]));
+                // da = gb (-dx^2/2); db = dx t1; dc = dy (gl - gb dy / 2) - gq / 2;
+                // du = b t1 - a t2; dv = c t1 - b t2 with t1 = gl - gb dy, t2 = gb dx
+                const float t1 = fmaf(-gb, dy, gl), t2 = gb * dx;
+                float* pc = ws.conic + nb * 32 + ((lane + 4 * nb) & 31);           // conic c at pc[c * 256]
+                pc[0 * 256] = -0.5f * (t2 * dx);
+                pc[1 * 256] = dx * t1;
+                pc[2 * 256] = fmaf(dy, fmaf(-0.5f * gb, dy, gl), -0.5f * gq);
+                const int pr = nb & 3;
+                float* pt = reinterpret_cast<float*>(ws.tree + pr * 32 + ((lane + 2 * pr) & 31)) + (nb >> 2);
+                pt[0 * 256] = fmaf(r.b, t1, -r.a * t2);                           // tree c at pt[c * 256]
+                pt[1 * 256] = fmaf(r.c, t1, -r.b * t2);
+                pt[2 * 256] = gb * r.inv_o;
+#pragma unroll
+                for (int ch = 0; ch < 3; ch++) {
+                    const float2 t = __ffma2_rn(w2[1], dI2[1][ch], __fmul2_rn(w2[0], dI2[0][ch]));
+                    pt[(3 + ch) * 256] = t.x + t.y;
+                }
+                pt[6 * 256] = (q2.x + q2.y) * (r.inv_o * r.inv_o);
+                const int C = __reduce_add_sync(0xffffffffu, __popc(cmask));
                 if (lane == 0) {
                     ws.slot[nb] = r.slot;
                     ws.count[nb] = C;
