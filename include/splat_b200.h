@@ -86,10 +86,11 @@ int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam
 /* tiles.py:50-107 binning, part 1: enumerate the exact disc/rect hits
  * (tiles.py:75-91), count them per tile and scan the counts ->
  * tile_offsets[ntiles + 1]; *n_pairs (device int) receives P.  The per-row
- * hit intervals are kept in `state` (sb_bin_state_workspace_bytes(n_cap)
- * bytes, caller-owned) for part 2.  n_cap bounds N_c (read from counters[1]
+ * hit intervals and the list of long tiles are kept in `state`
+ * (sb_bin_state_workspace_bytes(n_cap, ntiles) bytes, caller-owned) for
+ * part 2.  n_cap bounds N_c (read from counters[1]
  * on the device). */
-size_t sb_bin_state_workspace_bytes(int64_t n_cap);
+size_t sb_bin_state_workspace_bytes(int64_t n_cap, int32_t ntiles);
 int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam,
                    int32_t* tile_offsets, int32_t* n_pairs, void* state, size_t state_bytes, sb_stream_t stream);
 

@@ -32,7 +32,7 @@ SIGNATURES = {
     "sb_permute_rows": ([VP, I64, C.c_int, VP, VP, VP, VP], C.c_int),
     "sb_project_workspace_bytes": ([I64], SZ),
     "sb_project_cull_compact": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
-    "sb_bin_state_workspace_bytes": ([I64], SZ),
+    "sb_bin_state_workspace_bytes": ([I64, I32], SZ),
     "sb_bin_prepare": ([VP, VP, I64, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_bin_finish_workspace_bytes": ([I64, I32], SZ),
     "sb_bin_finish": ([VP, VP, I64, VP, I64, VP, VP, VP, VP, SZ, VP], C.c_int),

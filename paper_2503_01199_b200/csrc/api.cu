@@ -9,7 +9,7 @@
 void sb_launch_project_cull_compact(const float*, int, const CamDev&, int, RasterRec*, int32_t*, int32_t*, uint8_t*,
                                     int32_t*, unsigned long long*, unsigned int*, cudaStream_t);
 int sb_project_blocks(int n);
-size_t sb_bin_state_bytes(int n_cap);
+size_t sb_bin_state_bytes(int n_cap, int ntiles);
 void sb_launch_bin_prepare(const RasterRec*, const int32_t*, int, const CamDev&, int32_t*, int32_t*, void*,
                            cudaStream_t);
 size_t sb_bin_finish_ws(long long n_pairs, int ntiles);
@@ -150,15 +150,18 @@ int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam
     return check_launch("sb_project_cull_compact");
 }
 
-size_t sb_bin_state_workspace_bytes(int64_t n_cap) { return sb_bin_state_bytes((int)n_cap) + 256; }
+size_t sb_bin_state_workspace_bytes(int64_t n_cap, int32_t ntiles) {
+    return sb_bin_state_bytes((int)n_cap, ntiles) + 256;
+}
 
 int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam,
                    int32_t* tile_offsets, int32_t* n_pairs, void* state, size_t state_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (n_cap < 0 || n_cap > INT32_MAX / 2) return fail(SB_EINVAL, "n_cap out of range");
     if (!tile_offsets || !n_pairs) return fail(SB_EINVAL, "NULL buffer");
-    if (state_bytes < sb_bin_state_workspace_bytes(n_cap)) return fail(SB_EWORKSPACE, "bin state too small");
     const CamDev d = make_cam(cam, nullptr);
+    if (state_bytes < sb_bin_state_workspace_bytes(n_cap, d.tiles_x * d.tiles_y))
+        return fail(SB_EWORKSPACE, "bin state too small");
     sb_launch_bin_prepare(static_cast<const RasterRec*>(recs), counters, (int)n_cap, d, tile_offsets, n_pairs, state,
                           S(stream));
     return check_launch("sb_bin_prepare");

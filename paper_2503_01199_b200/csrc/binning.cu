@@ -235,16 +235,18 @@ tile_count_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict_
 }
 
 // ---- prepare (2): counts -> exclusive offsets, in place ------------------------
+constexpr int kShortList = 128 * 16;   // lists up to this length: 128-thread sort kernel
+
 constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 16;   // per thread and round
 
 __global__ void __launch_bounds__(kScanThreads)
-tile_scan_kernel(int32_t* __restrict__ offsets, int ntiles, int32_t* __restrict__ n_pairs)
+tile_scan_kernel(int32_t* __restrict__ offsets, int ntiles, int32_t* __restrict__ n_pairs, int32_t* __restrict__ longs)
 {
     __shared__ uint32_t s_warp[kScanThreads / 32];
     __shared__ uint32_t s_carry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_carry = 0;
+    if (threadIdx.x == 0) { s_carry = 0; longs[0] = 0; }
     __syncthreads();
     for (int base = 0; base < ntiles; base += kScanThreads * kScanItems) {
         // each thread: kScanItems consecutive counts (all loads in flight)
@@ -277,6 +279,8 @@ tile_scan_kernel(int32_t* __restrict__ offsets, int ntiles, int32_t* __restrict_
 #pragma unroll
         for (int j = 0; j < kScanItems; j++) {
             if (beg + j < ntiles) offsets[beg + j] = (int32_t)run;
+            // tiles for the long-list sort (binning finish)
+            if (v[j] > (uint32_t)kShortList) longs[1 + atomicAdd(&longs[0], 1)] = beg + j;
             run += v[j];
         }
         __syncthreads();
@@ -348,16 +352,17 @@ scatter_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ c
 }
 
 // ---- finish (2): per-tile sort, one CTA per tile ----------------------------
-constexpr int kSortThreads = 256;
-constexpr int kCap = kSortThreads * 16;   // keys sorted in one shared-memory pass
-constexpr int kMaxBuckets = kCap;         // at most one key per bucket on average
-
+// Two launches over all tiles: 128-thread CTAs sort lists of up to 2048 keys
+// (8 or 16 per thread), 256-thread CTAs the longer ones (16 per thread, then
+// chunk merges beyond 4096).
+template <int THREADS>
 struct SortSmem {
-    unsigned long long b[kCap];           // keys in bucket order
-    uint32_t cnt[kMaxBuckets / 2];        // packed 16-bit bucket counts (bucket 2w in the low half)
-    uint32_t cur[kMaxBuckets / 2];        // packed 16-bit bucket cursors
-    unsigned long long red[2][kSortThreads / 32];
-    uint32_t wsum[kSortThreads / 32];
+    static constexpr int kCap = THREADS * 16;       // keys sorted in one shared-memory pass
+    unsigned long long b[kCap];                     // keys in bucket order
+    uint32_t cnt[kCap / 2];                         // packed 16-bit bucket counts (bucket 2w low)
+    uint32_t cur[kCap / 2];                         // packed 16-bit bucket cursors
+    unsigned long long red[2][THREADS / 32];
+    uint32_t wsum[THREADS / 32];
 };
 
 SB_INLINE unsigned long long warp_min_u64(unsigned long long v) {
@@ -385,26 +390,29 @@ SB_INLINE int bucket_of(unsigned long long k, unsigned long long kmin, float sca
 
 SB_INLINE uint32_t half_of(uint32_t word, int b) { return (word >> (16 * (b & 1))) & 0xffffu; }
 
-// Sorts src[0, n) (global, n <= 256 * PER, keys distinct) and hands the key
-// of rank i to out(i, key).  Whole CTA.  Keys stay in registers (thread t
-// owns items t, t + 256, ...) until they are distributed, through 256 * PER
-// buckets (<= one key per bucket on average), into bucket order; a key's
-// rank is then its bucket start plus the smaller keys of its bucket.
-template <int PER, typename Out>
-__device__ __forceinline__ void cta_sort(SortSmem& sm, const unsigned long long* __restrict__ src, int n, Out&& out)
+// Sorts src[0, n) (global, n <= THREADS * PER, keys distinct) and hands the
+// key of rank i to out(i, key).  Whole CTA.  Keys stay in registers (thread t
+// owns items t, t + THREADS, ...) until they are distributed, through
+// THREADS * PER buckets (<= one key per bucket on average), into bucket
+// order; a key's rank is then its bucket start plus the smaller keys of its
+// bucket.
+template <int THREADS, int PER, typename Out>
+__device__ __forceinline__ void cta_sort(SortSmem<THREADS>& sm, const unsigned long long* __restrict__ src, int n,
+                                         Out&& out)
 {
-    constexpr int NB = kSortThreads * PER;
+    constexpr int NB = THREADS * PER;
+    constexpr int NW = THREADS / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned long long k[PER];
     unsigned long long lo = ~0ull, hi = 0ull;
 #pragma unroll
     for (int q = 0; q < PER; q++) {
-        const int i = q * kSortThreads + tid;
+        const int i = q * THREADS + tid;
         k[q] = i < n ? src[i] : 0ull;
     }
 #pragma unroll
     for (int q = 0; q < PER; q++) {
-        if (q * kSortThreads + tid < n) {
+        if (q * THREADS + tid < n) {
             lo = k[q] < lo ? k[q] : lo;
             hi = k[q] > hi ? k[q] : hi;
         }
@@ -412,20 +420,20 @@ __device__ __forceinline__ void cta_sort(SortSmem& sm, const unsigned long long*
     lo = warp_min_u64(lo);
     hi = warp_max_u64(hi);
 #pragma unroll
-    for (int q = 0; q < PER / 2; q++) sm.cnt[q * kSortThreads + tid] = 0;
+    for (int q = 0; q < PER / 2; q++) sm.cnt[q * THREADS + tid] = 0;
     if (lane == 0) { sm.red[0][warp] = lo; sm.red[1][warp] = hi; }
     __syncthreads();
     lo = sm.red[0][0];
     hi = sm.red[1][0];
 #pragma unroll
-    for (int w = 1; w < kSortThreads / 32; w++) {
+    for (int w = 1; w < NW; w++) {
         lo = sm.red[0][w] < lo ? sm.red[0][w] : lo;
         hi = sm.red[1][w] > hi ? sm.red[1][w] : hi;
     }
     const float scale = (float)NB / __fadd_rn(__ull2float_rn(hi - lo), 1.0f);
 #pragma unroll
     for (int q = 0; q < PER; q++) {
-        if (q * kSortThreads + tid < n) {
+        if (q * THREADS + tid < n) {
             const int bq = bucket_of(k[q], lo, scale, NB);
             atomicAdd(&sm.cnt[bq >> 1], 1u << (16 * (bq & 1)));
         }
@@ -449,8 +457,7 @@ __device__ __forceinline__ void cta_sort(SortSmem& sm, const unsigned long long*
     if (lane == 31) sm.wsum[warp] = x;
     __syncthreads();
     uint32_t run = x - s;
-#pragma unroll
-    for (int w = 0; w < kSortThreads / 32; w++) run += w < warp ? sm.wsum[w] : 0u;
+    for (int w = 0; w < warp; w++) run += sm.wsum[w];
 #pragma unroll
     for (int q = 0; q < PER / 2; q++) {
         const uint32_t r0 = run, r1 = run + c[2 * q];
@@ -460,7 +467,7 @@ __device__ __forceinline__ void cta_sort(SortSmem& sm, const unsigned long long*
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < PER; q++) {
-        if (q * kSortThreads + tid < n) {
+        if (q * THREADS + tid < n) {
             const int bq = bucket_of(k[q], lo, scale, NB);
             const uint32_t old = atomicAdd(&sm.cur[bq >> 1], 1u << (16 * (bq & 1)));
             sm.b[half_of(old, bq)] = k[q];
@@ -468,22 +475,13 @@ __device__ __forceinline__ void cta_sort(SortSmem& sm, const unsigned long long*
     }
     __syncthreads();
     // rank = bucket start + number of smaller keys in the bucket (cur = end
-    // now).  Walk the keys in bucket order: neighbouring threads share
-    // buckets, and buckets of up to 8 keys need no loop.
-    for (int i = tid; i < n; i += kSortThreads) {
+    // now); walk the keys in bucket order so neighbouring threads share buckets
+    for (int i = tid; i < n; i += THREADS) {
         const unsigned long long key = sm.b[i];
         const int bq = bucket_of(key, lo, scale, NB);
         const uint32_t end = half_of(sm.cur[bq >> 1], bq), beg = end - half_of(sm.cnt[bq >> 1], bq);
         uint32_t r = 0;
-        if (end - beg <= 8) {
-#pragma unroll
-            for (int j = 0; j < 8; j++) {
-                const uint32_t q = min(beg + j, end - 1);
-                r += (beg + j < end && sm.b[q] < key) ? 1u : 0u;
-            }
-        } else {
-            for (uint32_t j = beg; j < end; j++) r += sm.b[j] < key ? 1u : 0u;
-        }
+        for (uint32_t j = beg; j < end; j++) r += sm.b[j] < key ? 1u : 0u;
         out(beg + r, key);
     }
     __syncthreads();
@@ -499,12 +497,12 @@ SB_INLINE int lower_bound_u64(const unsigned long long* src, int n, unsigned lon
     return lo;
 }
 
-__global__ void __launch_bounds__(kSortThreads, 4)
-tile_sort_kernel(const int32_t* __restrict__ offsets, unsigned long long* __restrict__ keys,
-                 unsigned long long* __restrict__ scratch, int32_t* __restrict__ prims)
+__global__ void __launch_bounds__(128, 6)
+tile_sort_short_kernel(const int32_t* __restrict__ offsets, const unsigned long long* __restrict__ keys,
+                       int32_t* __restrict__ prims)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
+    SortSmem<128>& sm = *reinterpret_cast<SortSmem<128>*>(smem_raw);
     const int t = blockIdx.x, tid = threadIdx.x;
     const int off = offsets[t], L = offsets[t + 1] - off;
     if (L <= 1) {
@@ -512,28 +510,38 @@ tile_sort_kernel(const int32_t* __restrict__ offsets, unsigned long long* __rest
         return;
     }
     const auto to_prims = [&](int pos, unsigned long long k) { prims[off + pos] = (int32_t)(uint32_t)k; };
-    if (L <= 4 * kSortThreads) {
-        cta_sort<4>(sm, keys + off, L, to_prims);
-        return;
-    }
-    if (L <= 8 * kSortThreads) {
-        cta_sort<8>(sm, keys + off, L, to_prims);
-        return;
-    }
+    if (L <= 8 * 128) cta_sort<128, 8>(sm, keys + off, L, to_prims);
+    else if (L <= kShortList) cta_sort<128, 16>(sm, keys + off, L, to_prims);
+}
+
+__global__ void __launch_bounds__(256)
+tile_sort_long_kernel(const int32_t* __restrict__ offsets, const int32_t* __restrict__ longs,
+                      unsigned long long* __restrict__ keys,
+                      unsigned long long* __restrict__ scratch, int32_t* __restrict__ prims)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SortSmem<256>& sm = *reinterpret_cast<SortSmem<256>*>(smem_raw);
+    constexpr int kCap = SortSmem<256>::kCap;
+    const int tid = threadIdx.x;
+    // persistent: a few CTAs take the (rare) long tiles listed by the scan
+    const int nlong = longs[0];
+    for (int li = blockIdx.x; li < nlong; li += gridDim.x) {
+    const int t = longs[1 + li];
+    const int off = offsets[t], L = offsets[t + 1] - off;
     if (L <= kCap) {
-        cta_sort<16>(sm, keys + off, L, to_prims);
-        return;
+        cta_sort<256, 16>(sm, keys + off, L, [&](int pos, unsigned long long k) { prims[off + pos] = (int32_t)(uint32_t)k; });
+        continue;
     }
-    // long list: sorted chunks of kCap into scratch, then pairwise merges
+    // very long list: sorted chunks of kCap into scratch, then pairwise merges
     unsigned long long* src = scratch + off;
     unsigned long long* dst = keys + off;
     for (int c0 = 0; c0 < L; c0 += kCap) {
         const int n = min(kCap, L - c0);
-        cta_sort<16>(sm, keys + off + c0, n, [&](int pos, unsigned long long k) { src[c0 + pos] = k; });
+        cta_sort<256, 16>(sm, keys + off + c0, n, [&](int pos, unsigned long long k) { src[c0 + pos] = k; });
     }
     for (int width = kCap; width < L; width *= 2) {
         const bool final_pass = 2 * width >= L;
-        for (int i = tid; i < L; i += kSortThreads) {
+        for (int i = tid; i < L; i += 256) {
             const int run = i / width, rs = run * width, ps = (run ^ 1) * width;
             const int pl = max(0, min(width, L - ps));
             const unsigned long long k = src[i];
@@ -544,6 +552,7 @@ tile_sort_kernel(const int32_t* __restrict__ offsets, unsigned long long* __rest
         __syncthreads();
         unsigned long long* tmp = src; src = dst; dst = tmp;
     }
+    }
 }
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -551,7 +560,13 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 }  // namespace
 
 // ---- prepare -------------------------------------------------------------------
-size_t sb_bin_state_bytes(int n_cap) { return align256((size_t)(n_cap > 0 ? n_cap : 1) * 32); }
+// state: spans (32 B per compact slot) | long-tile list (1 + ntiles ints)
+size_t sb_bin_state_bytes(int n_cap, int ntiles) {
+    return align256((size_t)(n_cap > 0 ? n_cap : 1) * 32) + align256((size_t)(ntiles + 1) * 4);
+}
+static int32_t* long_list(void* state, int n_cap) {
+    return reinterpret_cast<int32_t*>(static_cast<char*>(state) + align256((size_t)(n_cap > 0 ? n_cap : 1) * 32));
+}
 
 void sb_launch_bin_prepare(const RasterRec* recs, const int32_t* counters, int n_cap, const CamDev& cam,
                            int32_t* tile_offsets, int32_t* n_pairs, void* state, cudaStream_t stream)
@@ -561,7 +576,7 @@ void sb_launch_bin_prepare(const RasterRec* recs, const int32_t* counters, int n
     if (n_cap > 0)
         tile_count_kernel<<<(n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream>>>(
             recs, counters, n_cap, cam.tiles_x, cam.tiles_y, cam.W, cam.H, static_cast<uint4*>(state), tile_offsets);
-    tile_scan_kernel<<<1, kScanThreads, 0, stream>>>(tile_offsets, ntiles, n_pairs);
+    tile_scan_kernel<<<1, kScanThreads, 0, stream>>>(tile_offsets, ntiles, n_pairs, long_list(state, n_cap));
 }
 
 // ---- finish --------------------------------------------------------------------
@@ -586,8 +601,13 @@ void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_
         keys);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem));
+        cudaFuncSetAttribute(tile_sort_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(SortSmem<128>));
+        cudaFuncSetAttribute(tile_sort_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(SortSmem<256>));
         attr = true;
     }
-    tile_sort_kernel<<<ntiles, kSortThreads, sizeof(SortSmem), stream>>>(tile_offsets, keys, scratch, tile_prims);
+    tile_sort_short_kernel<<<ntiles, 128, sizeof(SortSmem<128>), stream>>>(tile_offsets, keys, tile_prims);
+    tile_sort_long_kernel<<<2 * 148, 256, sizeof(SortSmem<256>), stream>>>(
+        tile_offsets, long_list(const_cast<void*>(state), n_cap), keys, scratch, tile_prims);
 }

@@ -156,7 +156,7 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     _lib.call("sb_project_cull_compact", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s), _lib.ptr(recs),
               _lib.ptr(cmap), _lib.ptr(coff), _lib.ptr(cvis), _lib.ptr(counters), _lib.ptr(ws), ws.numel(),
               stream)
-    state = _lib.workspace("bin_state", lib.sb_bin_state_workspace_bytes(n), dev)
+    state = _lib.workspace("bin_state", lib.sb_bin_state_workspace_bytes(n, ntiles), dev)
     _lib.call("sb_bin_prepare", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), _lib.ptr(tile_offsets),
               _lib.ptr(counters[4:]), _lib.ptr(state), state.numel(), stream)
     vis, nc, ndeg, _, P = (int(v) for v in counters[:5].cpu().tolist())   # one D2H read
