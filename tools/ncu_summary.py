@@ -32,6 +32,17 @@ for rep in sys.argv[1:]:
     for k in WANT:
         if k in vals:
             print(f"   {k:32s} {vals[k]}")
+    raw = list(csv.reader(run([rep, "--page", "raw", "--csv"]).splitlines()))
+    if len(raw) >= 3:
+        rv = dict(zip(raw[0], raw[2]))
+        try:
+            rd = float(rv["dram__bytes_read.sum"].replace(",", ""))
+            wr = float(rv["dram__bytes_write.sum"].replace(",", ""))
+            unit = raw[1][raw[0].index("dram__bytes_read.sum")]
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            print(f"   {'DRAM bytes (read + write)':32s} {(rd + wr) * scale / 1e6:.1f} MB")
+        except (KeyError, ValueError):
+            pass
     src = list(csv.reader(run([rep, "--page", "source", "--csv", "--print-source", "sass"]).splitlines()))
     hdr = src[1]
     data = src[2:]
