@@ -574,7 +574,7 @@ raster_bwd_kernel(BwdParams p)
         const int kmax = __reduce_max_sync(0xffffffffu, lane_max);
         Prefetch pf;
         if (kmax > 0) prefetch_chunk(pf, p.recs, p.prims, beg, max(0, kmax - 32), kmax - max(0, kmax - 32), lane);
-        int nb = 0;
+        int nb = 0, pc_off = lane, pt_off = 2 * lane;
         for (int k1 = kmax; k1 > 0; k1 -= 32) {
             const int k0 = max(0, k1 - 32), cnt = k1 - k0;
             __syncwarp();
@@ -606,22 +606,23 @@ raster_bwd_kernel(BwdParams p)
 #pragma unroll
                 for (int h = 0; h < 2; h++) {
                     const int i0 = 2 * h, i1 = 2 * h + 1;
-                    const float2 a2 = make_float2(alpha[i0], alpha[i1]);
+                    // a non-contributing pixel gets alpha 0: 1 / (1 - 0) = 1 exactly,
+                    // so Tb = T, w = 0 and the state passes through unchanged
+                    const float2 a2 = make_float2(ci[i0] ? alpha[i0] : 0.0f, ci[i1] ? alpha[i1] : 0.0f);
                     const float2 om = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-a2.x, -a2.y));
                     const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
                     const float2 Tb = __fmul2_rn(T2[h], inv);
                     const float2 dc = __ffma2_rn(dI2[h][2], cb, __ffma2_rn(dI2[h][1], cg, __fmul2_rn(dI2[h][0], cr)));
                     const float2 si = __fmul2_rn(Sd2[h], inv);
                     const float2 da = __ffma2_rn(Tb, dc, make_float2(-si.x, -si.y));
-                    const float2 u = __fmul2_rn(da, make_float2(araw[i0], araw[i1]));
-                    const float2 tw = __fmul2_rn(Tb, a2);
                     // u G = dL/dalpha o G; gradient through a clamped alpha is
                     // zero (backward.py:128,169)
-                    uG2[h] = make_float2((ci[i0] && araw[i0] < p.amax) ? u.x : 0.0f,
-                                         (ci[i1] && araw[i1] < p.amax) ? u.y : 0.0f);
-                    w2[h] = make_float2(ci[i0] ? tw.x : 0.0f, ci[i1] ? tw.y : 0.0f);
+                    const float2 ag = make_float2((ci[i0] && araw[i0] < p.amax) ? araw[i0] : 0.0f,
+                                                  (ci[i1] && araw[i1] < p.amax) ? araw[i1] : 0.0f);
+                    uG2[h] = __fmul2_rn(da, ag);
+                    w2[h] = __fmul2_rn(Tb, a2);
                     Sd2[h] = __ffma2_rn(w2[h], dc, Sd2[h]);
-                    T2[h] = make_float2(ci[i0] ? Tb.x : T2[h].x, ci[i1] ? Tb.y : T2[h].y);
+                    T2[h] = Tb;
                 }
                 // scanline_grad_fold (backward.py:175-196) + per-lane partials;
                 // f = dL/do = u G / o, so sum f = gb / o and sum f^2 = sum (uG)^2 / o^2
@@ -634,12 +635,11 @@ raster_bwd_kernel(BwdParams p)
                 // da = gb (-dx^2/2); db = dx t1; dc = dy (gl - gb dy / 2) - gq / 2;
                 // du = b t1 - a t2; dv = c t1 - b t2 with t1 = gl - gb dy, t2 = gb dx
                 const float t1 = fmaf(-gb, dy, gl), t2 = gb * dx;
-                float* pc = ws.conic + nb * 32 + ((lane + 4 * nb) & 31);           // conic c at pc[c * 256]
+                float* pc = ws.conic + pc_off;                                      // conic c at pc[c * 256]
                 pc[0 * 256] = -0.5f * (t2 * dx);
                 pc[1 * 256] = dx * t1;
                 pc[2 * 256] = fmaf(dy, fmaf(-0.5f * gb, dy, gl), -0.5f * gq);
-                const int pr = nb & 3;
-                float* pt = reinterpret_cast<float*>(ws.tree + pr * 32 + ((lane + 2 * pr) & 31)) + (nb >> 2);
+                float* pt = reinterpret_cast<float*>(ws.tree) + pt_off;
                 pt[0 * 256] = fmaf(r.b, t1, -r.a * t2);                           // tree c at pt[c * 256]
                 pt[1 * 256] = fmaf(r.c, t1, -r.b * t2);
                 pt[2 * 256] = gb * r.inv_o;
@@ -654,9 +654,16 @@ raster_bwd_kernel(BwdParams p)
                     ws.slot[nb] = r.slot;
                     ws.count[nb] = C;
                 }
-                if (++nb == kBatch) {
+                // next slot: conic row nb * 32, lane rotated by 4 nb; tree pair row
+                // (nb & 3) * 32 (lane rotated by 2 (nb & 3)), component nb >> 2
+                ++nb;
+                pc_off = nb * 32 + ((lane + 4 * nb) & 31);
+                pt_off = 2 * ((nb & 3) * 32 + ((lane + 2 * (nb & 3)) & 31)) + (nb >> 2);
+                if (nb == kBatch) {
                     flush_batch(ws, nb, lane, p.conic_tree, p.grads);
                     nb = 0;
+                    pc_off = lane;
+                    pt_off = 2 * lane;
                 }
             }
         }
