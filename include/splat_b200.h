@@ -85,23 +85,23 @@ int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam
 
 /* tiles.py:50-107 binning, part 1: enumerate the exact disc/rect hits
  * (tiles.py:75-91), count them per tile and scan the counts ->
- * tile_offsets[ntiles + 1]; *n_pairs (device int) receives P.  The per-row
- * hit intervals and the list of long tiles are kept in `state`
+ * tile_offsets[ntiles + 1]; totals[0] (device int) receives P, totals[1]
+ * the number E of (primitive, 4x4-tile super-tile) entries.  The per-row hit
+ * spans and the super-tile offsets are kept in `state`
  * (sb_bin_state_workspace_bytes(n_cap, ntiles) bytes, caller-owned) for
- * part 2.  n_cap bounds N_c (read from counters[1]
- * on the device). */
+ * part 2.  n_cap bounds N_c (read from counters[1] on the device). */
 size_t sb_bin_state_workspace_bytes(int64_t n_cap, int32_t ntiles);
 int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam,
-                   int32_t* tile_offsets, int32_t* n_pairs, void* state, size_t state_bytes, sb_stream_t stream);
+                   int32_t* tile_offsets, int32_t* totals, void* state, size_t state_bytes, sb_stream_t stream);
 
-/* tiles.py:50-107 binning, part 2 (P from part 1, `state` as part 1 left
- * it): scatter every hit into its tile's range, then sort each tile by
- * (depth, compact slot): tile_prims[P] (compact slots, per tile in
- * (depth, index) order == np.lexsort((prim, depth, tile_id)) of tiles.py:98). */
-size_t sb_bin_finish_workspace_bytes(int64_t n_pairs, int32_t ntiles);
+/* tiles.py:50-107 binning, part 2 (P and E from part 1, `state` as part 1
+ * left it): depth-sort each super-tile's entries once and emit the per-tile
+ * lists: tile_prims[P] (compact slots, per tile in (depth, index) order ==
+ * np.lexsort((prim, depth, tile_id)) of tiles.py:98). */
+size_t sb_bin_finish_workspace_bytes(int64_t n_entries, int32_t ntiles);
 int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam, int64_t n_pairs,
-                  const int32_t* tile_offsets, const void* state, int32_t* tile_prims, void* ws, size_t ws_bytes,
-                  sb_stream_t stream);
+                  int64_t n_entries, const int32_t* tile_offsets, const void* state, int32_t* tile_prims, void* ws,
+                  size_t ws_bytes, sb_stream_t stream);
 
 /* forward.py:161-191 + 240-255: color (H,W,3), transmittance (H,W),
  * frag_count (H,W) and last[(H,W)] = 1 + list position of each pixel's last

@@ -35,7 +35,7 @@ SIGNATURES = {
     "sb_bin_state_workspace_bytes": ([I64, I32], SZ),
     "sb_bin_prepare": ([VP, VP, I64, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_bin_finish_workspace_bytes": ([I64, I32], SZ),
-    "sb_bin_finish": ([VP, VP, I64, VP, I64, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_bin_finish": ([VP, VP, I64, VP, I64, I64, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_raster_workspace_bytes": ([], SZ),
     "sb_raster_fwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_raster_bwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, VP, SZ, VP], C.c_int),
@@ -108,7 +108,7 @@ def ptr(t: torch.Tensor | None):
 # the radix sort issues 3 per 8-bit pass and is counted by the caller.
 KERNELS_PER_CALL = {
     "sb_morton_keys": 3, "sb_permute_rows": 1, "sb_project_cull_compact": 1, "sb_bin_prepare": 2,
-    "sb_bin_finish": 2, "sb_raster_fwd": 1, "sb_raster_bwd": 1, "sb_radix_sort_pairs_u64": 10,
+    "sb_bin_finish": 3, "sb_raster_fwd": 1, "sb_raster_bwd": 1, "sb_radix_sort_pairs_u64": 10,
     "sb_chain_projection_bwd": 1, "sb_adam_sparse": 1, "sb_variance_score": 1, "sb_lane_reduce": 1,
     "sb_loss_fwd_bwd": 2,
 }

@@ -12,7 +12,7 @@ int sb_project_blocks(int n);
 size_t sb_bin_state_bytes(int n_cap, int ntiles);
 void sb_launch_bin_prepare(const RasterRec*, const int32_t*, int, const CamDev&, int32_t*, int32_t*, void*,
                            cudaStream_t);
-size_t sb_bin_finish_ws(long long n_pairs, int ntiles);
+size_t sb_bin_finish_ws(long long n_entries, int ntiles);
 void sb_launch_bin_finish(const RasterRec*, const int32_t*, int, const CamDev&, int, const int32_t*, const void*,
                           int32_t*, void*, cudaStream_t);
 size_t sb_sort_u64_ws(int n, int bits);
@@ -167,21 +167,23 @@ int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, con
     return check_launch("sb_bin_prepare");
 }
 
-size_t sb_bin_finish_workspace_bytes(int64_t n_pairs, int32_t ntiles) {
-    return sb_bin_finish_ws((long long)n_pairs, ntiles) + 256;
+size_t sb_bin_finish_workspace_bytes(int64_t n_entries, int32_t ntiles) {
+    return sb_bin_finish_ws((long long)n_entries, ntiles) + 256;
 }
 
 int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam, int64_t n_pairs,
-                  const int32_t* tile_offsets, const void* state, int32_t* tile_prims, void* ws, size_t ws_bytes,
-                  sb_stream_t stream) {
+                  int64_t n_entries, const int32_t* tile_offsets, const void* state, int32_t* tile_prims, void* ws,
+                  size_t ws_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (n_pairs < 0 || n_pairs > INT32_MAX / 2) return fail(SB_EINVAL, "n_pairs out of range");
+    if (n_entries < 0 || n_entries > INT32_MAX / 2) return fail(SB_EINVAL, "n_entries out of range");
     if (n_cap < 0 || n_cap > INT32_MAX / 2) return fail(SB_EINVAL, "n_cap out of range");
     const CamDev d = make_cam(cam, nullptr);
-    if (ws_bytes < sb_bin_finish_workspace_bytes(n_pairs, d.tiles_x * d.tiles_y))
+    if (ws_bytes < sb_bin_finish_workspace_bytes(n_entries, d.tiles_x * d.tiles_y))
         return fail(SB_EWORKSPACE, "bin finish workspace too small");
-    sb_launch_bin_finish(static_cast<const RasterRec*>(recs), counters, (int)n_cap, d, (int)n_pairs, tile_offsets,
-                         state, tile_prims, ws, S(stream));
+    if (n_pairs > 0)
+        sb_launch_bin_finish(static_cast<const RasterRec*>(recs), counters, (int)n_cap, d, (int)n_entries,
+                             tile_offsets, state, tile_prims, ws, S(stream));
     return check_launch("sb_bin_finish");
 }
 

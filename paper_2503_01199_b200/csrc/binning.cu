@@ -1,34 +1,40 @@
 // K6/K7: tile binning with the per-tile depth order (tiles.py:50-107).
 //
 // The reference builds (tile, depth, index) triples for every exact
-// disc/rect hit and lexsorts them (tiles.py:94-106).  No global sort here:
+// disc/rect hit and lexsorts them (tiles.py:94-106).  Here the depth order is
+// established once per super-tile (4 x 4 tiles) instead of once per tile:
 //
 //   prepare  (1) count: each CTA takes 256 consecutive compact slots (Morton
 //                order, so their footprints cluster on screen).  Each thread
 //                enumerates its primitive's exact hits once, row by row
 //                (tiles.py:75-91; float32-filtered float64 disc test), and
 //                stores the per-row hit intervals ("spans", 16 rows x 2 bytes
-//                relative to the bounding tile rectangle).  The CTA counts
-//                the hits per tile in a shared-memory window over its tile
-//                bounding box with two atomics per span (row difference
-//                array, then a row prefix sum) and adds each touched tile's
-//                count to the global counts once;
-//            (2) one CTA: exclusive scan of the counts -> tile_offsets and P;
-//   finish   (1) scatter: the same CTAs rebuild their window counts from the
-//                stored spans, reserve each touched tile's sub-range with ONE
-//                global atomic, and place their 64-bit keys (depth bits << 32
-//                | compact slot) through shared-memory cursors (order inside
-//                a tile is arbitrary at this point);
-//            (2) per-tile sort, one CTA per tile, in shared memory: keys are
-//                distributed over >= L buckets by a monotone map of the
-//                key (float-rounded offset from the tile's minimum), and each
-//                key's final position is its bucket start plus the number of
-//                smaller keys in its bucket.  Lists longer than the shared
-//                capacity sort capacity-sized chunks and merge them in global
-//                scratch (merge position by binary search).
-// Primitives whose bounding rectangle exceeds the span format (more than 16
-// tile rows or 255 tile columns), and CTAs whose window exceeds the shared
-// counters, take a direct path (re-enumeration, one global atomic per hit).
+//                relative to the bounding tile rectangle) and the rectangle's
+//                origin.  Per-tile hit counts go through a shared-memory
+//                window over the CTA's tile bounding box (two atomics per
+//                span, then a row prefix sum); per-super-tile entry counts
+//                (super-tiles overlapping the rectangle) through a second,
+//                smaller window; one global add per touched cell;
+//            (2) one CTA: exclusive scans -> tile_offsets and P, super-tile
+//                offsets and E, and the list of super-tiles too long to sort
+//                in one shared-memory pass;
+//   finish   (1) scatter: the same CTAs reserve each touched super-tile's
+//                sub-range with one global atomic and place their 64-bit
+//                keys (depth bits << 32 | compact slot) through
+//                shared-memory cursors (E ~ 0.2 P at config B);
+//            (2) per super-tile, one CTA: sort its keys in shared memory
+//                (keys distributed over >= E_s buckets by a monotone float map
+//                of (key - min); rank = bucket start + smaller keys of the
+//                bucket), then emit: each thread takes a contiguous run of the
+//                sorted entries, forms each entry's 16-bit mask of hit tiles
+//                from the stored spans, and a CTA-wide prefix count per tile
+//                gives every (entry, tile) its position in that tile's list
+//                -- stable by construction, so no per-tile sort.  Super-tiles
+//                longer than the shared capacity sort capacity-sized chunks
+//                and merge them in global scratch first.
+// Primitives whose rectangle exceeds the span format (more than 16 tile rows
+// or 255 tile columns) take direct paths (re-enumeration, direct disc tests),
+// and so do CTAs whose windows exceed the shared counters.
 //
 // Depth > near > 0, so the float32 bit pattern orders depths; ties fall
 // back to the compact slot.  The result is exactly np.lexsort((prim, depth,
@@ -39,8 +45,11 @@ namespace {
 
 constexpr int kBinThreads = 256;
 constexpr int kWin = 6144;          // shared-memory tile counters per CTA
+constexpr int kStWin = 1024;        // shared-memory super-tile counters per CTA
 constexpr int kSpanRows = 16;       // rows per primitive in the span format
 constexpr uint32_t kEmptySpan = 0x00ffu;   // a > b
+constexpr int kST = 4;              // super-tile = kST x kST tiles
+constexpr uint32_t kNoSpans = 0x80000000u; // origin flag: rectangle exceeds the span format
 
 struct PrimSmem {
     float x, y, r;
@@ -53,7 +62,9 @@ struct WinSmem {
     uint16_t span[kBinThreads][kSpanRows];
     PrimSmem prim[kBinThreads];
     int flat[kBinThreads / 32][32];
+    int32_t scnt[kStWin];           // super-tile count / cursor window
     int x0, y0, w, h;
+    int sx0, sy0, sw, sh;
     int red[4][kBinThreads / 32];
 };
 
@@ -186,10 +197,62 @@ SB_INLINE void publish_prim(WinSmem& sm, const Prim& q) {
     p.key = q.key;
 }
 
-// ---- prepare (1): spans + per-tile counts ------------------------------------
+
+// super-tile rectangle of a primitive's tile rectangle
+SB_INLINE void st_rect(const Prim& q, int& sx0, int& sx1, int& sy0, int& sy1) {
+    sx0 = q.tx0 / kST; sx1 = q.tx1 / kST; sy0 = q.ty0 / kST; sy1 = q.ty1 / kST;
+}
+
+// CTA super-tile window = bounding box of its primitives' super-tile
+// rectangles; returns true when it fits (and is zeroed).  Whole CTA.
+SB_INLINE bool setup_st_window(WinSmem& sm, const Prim& q) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int v[4] = {0x7fffffff, 1, 0x7fffffff, 1};
+    if (q.hit) {
+        int sx0, sx1, sy0, sy1;
+        st_rect(q, sx0, sx1, sy0, sy1);
+        v[0] = sx0; v[1] = -sx1; v[2] = sy0; v[3] = -sy1;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        v[k] = __reduce_min_sync(0xffffffffu, v[k]);
+        if (lane == 0) sm.red[k][warp] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int m[4];
+        for (int k = 0; k < 4; k++) {
+            m[k] = sm.red[k][0];
+            for (int w = 1; w < kBinThreads / 32; w++) m[k] = min(m[k], sm.red[k][w]);
+        }
+        sm.sx0 = m[0]; sm.sw = -m[1] - m[0] + 1;
+        sm.sy0 = m[2]; sm.sh = -m[3] - m[2] + 1;
+        if (sm.sw <= 0 || sm.sh <= 0) sm.sw = sm.sh = 0;
+    }
+    __syncthreads();
+    const int area = sm.sw * sm.sh;
+    const bool fits = area <= kStWin;
+    if (fits)
+        for (int i = threadIdx.x; i < area; i += kBinThreads) sm.scnt[i] = 0;
+    __syncthreads();
+    return fits;
+}
+
+// f(super-tile x, y) for every super-tile overlapping the primitive's rectangle
+template <typename F>
+SB_INLINE void for_each_st(const Prim& q, F&& f) {
+    if (!q.hit) return;
+    int sx0, sx1, sy0, sy1;
+    st_rect(q, sx0, sx1, sy0, sy1);
+    for (int sy = sy0; sy <= sy1; sy++)
+        for (int sx = sx0; sx <= sx1; sx++) f(sx, sy);
+}
+
+// ---- prepare (1): spans, per-tile counts, per-super-tile entry counts -------
 __global__ void __launch_bounds__(kBinThreads)
 tile_count_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ counters, int n_cap, int tiles_x,
-                  int tiles_y, int W, int H, uint4* __restrict__ spans_out, int32_t* __restrict__ counts)
+                  int tiles_y, int st_x, int W, int H, uint4* __restrict__ spans_out, uint32_t* __restrict__ origin,
+                  int32_t* __restrict__ counts, int32_t* __restrict__ st_counts)
 {
     __shared__ WinSmem sm;
     const int nc = min(counters[1], n_cap);
@@ -207,6 +270,8 @@ tile_count_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict_
         if (sb_row_hits(p.x, p.y, p.r, p.ty0 + k, p.tx0, p.tx1, W, H, a, b))
             sm.span[t][k] = (uint16_t)((a - p.tx0) | ((b - p.tx0) << 8));
     });
+    if (s < nc)
+        origin[s] = q.hit ? ((uint32_t)q.tx0 | ((uint32_t)q.ty0 << 16) | (q.spans ? 0u : kNoSpans)) : 0xffffffffu;
     if (q.spans) {
         const uint4* sp = reinterpret_cast<const uint4*>(sm.span[threadIdx.x]);
         spans_out[2 * s] = sp[0];
@@ -232,29 +297,50 @@ tile_count_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict_
                 atomicAdd(&counts[(q.ty0 + k) * tiles_x + tx], 1);
         }
     }
+    // super-tile entries (every super-tile the rectangle overlaps)
+    const bool sfits = setup_st_window(sm, q);
+    if (sfits) {
+        for_each_st(q, [&](int sx, int sy) { atomicAdd(&sm.scnt[(sy - sm.sy0) * sm.sw + (sx - sm.sx0)], 1); });
+        __syncthreads();
+        for (int i = threadIdx.x; i < sm.sw * sm.sh; i += kBinThreads) {
+            const int c = sm.scnt[i];
+            if (c) {
+                const int wy = i / sm.sw;
+                atomicAdd(&st_counts[(sm.sy0 + wy) * st_x + sm.sx0 + (i - wy * sm.sw)], c);
+            }
+        }
+    } else {
+        for_each_st(q, [&](int sx, int sy) { atomicAdd(&st_counts[sy * st_x + sx], 1); });
+    }
 }
 
 // ---- prepare (2): counts -> exclusive offsets, in place ------------------------
-constexpr int kShortList = 128 * 16;   // lists up to this length: 128-thread sort kernel
-
 constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 16;   // per thread and round
+constexpr int kStThreads = 384;
+constexpr int kStCap = kStThreads * 16;   // super-tile entries sorted in one shared-memory pass
 
-__global__ void __launch_bounds__(kScanThreads)
-tile_scan_kernel(int32_t* __restrict__ offsets, int ntiles, int32_t* __restrict__ n_pairs, int32_t* __restrict__ longs)
+// exclusive scan of a[0, n) in place, total to a[n]; with `longs`, the
+// indices whose count exceeds `long_min` are appended to longs[1..]
+// (longs[0] = how many).  Whole (1024-thread) CTA.
+__device__ void cta_scan_inplace(int32_t* __restrict__ a, int n, int32_t* __restrict__ total,
+                                 int32_t* __restrict__ longs, uint32_t long_min)
 {
     __shared__ uint32_t s_warp[kScanThreads / 32];
     __shared__ uint32_t s_carry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) { s_carry = 0; longs[0] = 0; }
+    if (threadIdx.x == 0) {
+        s_carry = 0;
+        if (longs) longs[0] = 0;
+    }
     __syncthreads();
-    for (int base = 0; base < ntiles; base += kScanThreads * kScanItems) {
+    for (int base = 0; base < n; base += kScanThreads * kScanItems) {
         // each thread: kScanItems consecutive counts (all loads in flight)
         const int beg = base + threadIdx.x * kScanItems;
         uint32_t v[kScanItems], sum = 0;
 #pragma unroll
         for (int j = 0; j < kScanItems; j++) {
-            v[j] = beg + j < ntiles ? (uint32_t)offsets[beg + j] : 0u;
+            v[j] = beg + j < n ? (uint32_t)a[beg + j] : 0u;
             sum += v[j];
         }
         uint32_t x = sum;
@@ -278,9 +364,8 @@ tile_scan_kernel(int32_t* __restrict__ offsets, int ntiles, int32_t* __restrict_
         uint32_t run = s_carry + (warp ? s_warp[warp - 1] : 0u) + x - sum;
 #pragma unroll
         for (int j = 0; j < kScanItems; j++) {
-            if (beg + j < ntiles) offsets[beg + j] = (int32_t)run;
-            // tiles for the long-list sort (binning finish)
-            if (v[j] > (uint32_t)kShortList) longs[1 + atomicAdd(&longs[0], 1)] = beg + j;
+            if (beg + j < n) a[beg + j] = (int32_t)run;
+            if (longs && v[j] > long_min) longs[1 + atomicAdd(&longs[0], 1)] = beg + j;
             run += v[j];
         }
         __syncthreads();
@@ -288,73 +373,52 @@ tile_scan_kernel(int32_t* __restrict__ offsets, int ntiles, int32_t* __restrict_
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        offsets[ntiles] = (int32_t)s_carry;
-        *n_pairs = (int32_t)s_carry;
+        a[n] = (int32_t)s_carry;
+        *total = (int32_t)s_carry;
     }
+    __syncthreads();
 }
 
-// ---- finish (1): scatter keys into tile ranges ------------------------------
+__global__ void __launch_bounds__(kScanThreads)
+tile_scan_kernel(int32_t* __restrict__ offsets, int ntiles, int32_t* __restrict__ st_offsets, int nst,
+                 int32_t* __restrict__ totals, int32_t* __restrict__ st_longs)
+{
+    cta_scan_inplace(offsets, ntiles, totals, nullptr, 0);
+    cta_scan_inplace(st_offsets, nst, totals + 1, st_longs, (uint32_t)kStCap);
+}
+
+// ---- finish (1): scatter keys into super-tile ranges ---------------------------
 __global__ void __launch_bounds__(kBinThreads)
-scatter_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ counters, int n_cap, int tiles_x,
-               int tiles_y, int W, int H, const uint4* __restrict__ spans_in, int32_t* __restrict__ cursor,
-               unsigned long long* __restrict__ keys)
+st_scatter_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ counters, int n_cap, int tiles_x,
+                  int tiles_y, int st_x, int32_t* __restrict__ cursor, unsigned long long* __restrict__ keys)
 {
     __shared__ WinSmem sm;
     const int nc = min(counters[1], n_cap);
     const int s = blockIdx.x * kBinThreads + threadIdx.x;
     if (blockIdx.x * kBinThreads >= nc) return;
     const Prim q = load_prim(recs, s, nc, tiles_x, tiles_y);
-    if (q.spans) {
-        uint4* sp = reinterpret_cast<uint4*>(sm.span[threadIdx.x]);
-        sp[0] = spans_in[2 * s];
-        sp[1] = spans_in[2 * s + 1];
-    } else if (q.hit) {
-        for (int ty = q.ty0; ty <= q.ty1; ty++) {
-            int a, b;
-            if (!sb_row_hits(q.x, q.y, q.r, ty, q.tx0, q.tx1, W, H, a, b)) continue;
-            for (int tx = a; tx <= b; tx++) keys[atomicAdd(&cursor[ty * tiles_x + tx], 1)] = q.key;
-        }
-    }
-    const bool fits = setup_window(sm, q);
-    if (fits) {
-        if (q.spans) window_add_spans(sm, q);
+    const bool sfits = setup_st_window(sm, q);
+    if (sfits) {
+        for_each_st(q, [&](int sx, int sy) { atomicAdd(&sm.scnt[(sy - sm.sy0) * sm.sw + (sx - sm.sx0)], 1); });
         __syncthreads();
-        // reserve each touched tile's sub-range: the cell becomes its cursor
-        window_counts(sm, tiles_x, [&](int c, int t, int32_t& cell) {
-            cell = c ? atomicAdd(&cursor[t], c) : 0;
-        });
-        __syncthreads();
-        publish_prim(sm, q);
-        __syncwarp();
-        const int ww = sm.w + 1;
-        warp_flat(sm, q.spans ? q.ty1 - q.ty0 + 1 : 0, [&](int t, int k) {
-            const PrimSmem& p = sm.prim[t];
-            const uint32_t sp = sm.span[t][k];
-            const int a = (int)(sp & 0xff), b = (int)(sp >> 8);
-            int32_t* row = sm.cnt + (p.ty0 + k - sm.y0) * ww + (p.tx0 - sm.x0);
-            // four shared cursor atomics in flight before their stores
-            for (int c = a; c <= b; c += 4) {
-                int pos[4];
-#pragma unroll
-                for (int u = 0; u < 4; u++) pos[u] = c + u <= b ? atomicAdd(row + c + u, 1) : -1;
-#pragma unroll
-                for (int u = 0; u < 4; u++)
-                    if (pos[u] >= 0) keys[pos[u]] = p.key;
+        // reserve each touched super-tile's sub-range: the cell becomes its cursor
+        for (int i = threadIdx.x; i < sm.sw * sm.sh; i += kBinThreads) {
+            const int c = sm.scnt[i];
+            if (c) {
+                const int wy = i / sm.sw;
+                sm.scnt[i] = atomicAdd(&cursor[(sm.sy0 + wy) * st_x + sm.sx0 + (i - wy * sm.sw)], c);
             }
-        });
-    } else if (q.spans) {
-        for (int k = 0; k <= q.ty1 - q.ty0; k++) {
-            const uint32_t sp = sm.span[threadIdx.x][k];
-            for (int tx = q.tx0 + (int)(sp & 0xff); tx <= q.tx0 + (int)(sp >> 8); tx++)
-                keys[atomicAdd(&cursor[(q.ty0 + k) * tiles_x + tx], 1)] = q.key;
         }
+        __syncthreads();
+        for_each_st(q, [&](int sx, int sy) {
+            keys[atomicAdd(&sm.scnt[(sy - sm.sy0) * sm.sw + (sx - sm.sx0)], 1)] = q.key;
+        });
+    } else {
+        for_each_st(q, [&](int sx, int sy) { keys[atomicAdd(&cursor[sy * st_x + sx], 1)] = q.key; });
     }
 }
 
-// ---- finish (2): per-tile sort, one CTA per tile ----------------------------
-// Two launches over all tiles: 128-thread CTAs sort lists of up to 2048 keys
-// (8 or 16 per thread), 256-thread CTAs the longer ones (16 per thread, then
-// chunk merges beyond 4096).
+// ---- finish (2): per super-tile sort + per-tile emission -----------------------
 template <int THREADS>
 struct SortSmem {
     static constexpr int kCap = THREADS * 16;       // keys sorted in one shared-memory pass
@@ -482,7 +546,7 @@ __device__ __forceinline__ void cta_sort(SortSmem<THREADS>& sm, const unsigned l
         const uint32_t end = half_of(sm.cur[bq >> 1], bq), beg = end - half_of(sm.cnt[bq >> 1], bq);
         uint32_t r = 0;
         for (uint32_t j = beg; j < end; j++) r += sm.b[j] < key ? 1u : 0u;
-        out(beg + r, key);
+        out(i, beg + r, key);
     }
     __syncthreads();
 }
@@ -497,117 +561,244 @@ SB_INLINE int lower_bound_u64(const unsigned long long* src, int n, unsigned lon
     return lo;
 }
 
-__global__ void __launch_bounds__(128, 6)
-tile_sort_short_kernel(const int32_t* __restrict__ offsets, const unsigned long long* __restrict__ keys,
-                       int32_t* __restrict__ prims)
+
+// Shared memory of one super-tile CTA.  After the sort's rank phase the
+// bucket counters are free and hold the sorted compact slots; the ranks
+// (u16, per bucket-order position) live where the emission later keeps
+// each entry's tile mask.
+struct StSmem {
+    SortSmem<kStThreads> sort;
+    uint16_t mask[kStCap];                 // ranks, then per sorted entry: hit tiles of the super-tile
+    int32_t toff[kST * kST];
+    __device__ uint32_t* slots() { return sort.cnt; }   // kStCap u32 over cnt + cur
+};
+static_assert(sizeof(SortSmem<kStThreads>::cnt) + sizeof(SortSmem<kStThreads>::cur) >= kStCap * 4,
+              "sorted slots alias the bucket counters");
+
+
+// 16-bit mask (bit 4 i + c) of the tiles (4 sx + c, 4 sy + i) the entry hits
+SB_INLINE uint32_t entry_mask(const RasterRec* __restrict__ recs, uint32_t org, uint4 s0, uint4 s1, uint32_t slot,
+                              int sx, int sy, int tiles_x, int tiles_y, int W, int H)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortSmem<128>& sm = *reinterpret_cast<SortSmem<128>*>(smem_raw);
-    const int t = blockIdx.x, tid = threadIdx.x;
-    const int off = offsets[t], L = offsets[t + 1] - off;
-    if (L <= 1) {
-        if (L == 1 && tid == 0) prims[off] = (int32_t)(uint32_t)keys[off];
-        return;
+    const int tx0 = (int)(org & 0x7fffu), ty0 = (int)((org >> 16) & 0x7fffu);
+    const int cx0 = kST * sx, cy0 = kST * sy;
+    uint32_t m = 0;
+    if (!(org & kNoSpans)) {
+        const uint32_t w[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+        for (int i = 0; i < kST; i++) {
+            const int k = cy0 + i - ty0;
+            if (k < 0 || k >= kSpanRows) continue;
+            const uint32_t sp = (w[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+            const int a = tx0 + (int)(sp & 0xff), b = tx0 + (int)(sp >> 8);
+            const int lo = max(a, cx0), hi = min(b, cx0 + kST - 1);
+            if (lo <= hi) m |= ((2u << (hi - cx0)) - (1u << (lo - cx0))) << (kST * i);
+        }
+    } else {
+        // rectangle beyond the span format: exact disc tests (tiles.py:75-91)
+        const float4* r4 = reinterpret_cast<const float4*>(recs + slot);
+        const float4 a4 = __ldg(r4), c4 = __ldg(r4 + 2);
+        int rx0, rx1, ry0, ry1;
+        sb_tile_range(a4.x, a4.y, c4.z, tiles_x, tiles_y, rx0, rx1, ry0, ry1);
+        for (int i = 0; i < kST; i++) {
+            const int ty = cy0 + i;
+            if (ty < ry0 || ty > ry1) continue;
+            for (int c = 0; c < kST; c++) {
+                const int tx = cx0 + c;
+                if (tx >= rx0 && tx <= rx1 && sb_disc_hits_fast(a4.x, a4.y, c4.z, tx, ty, W, H)) m |= 1u << (kST * i + c);
+            }
+        }
     }
-    const auto to_prims = [&](int pos, unsigned long long k) { prims[off + pos] = (int32_t)(uint32_t)k; };
-    if (L <= 8 * 128) cta_sort<128, 8>(sm, keys + off, L, to_prims);
-    else if (L <= kShortList) cta_sort<128, 16>(sm, keys + off, L, to_prims);
+    return m;
 }
 
-__global__ void __launch_bounds__(256)
-tile_sort_long_kernel(const int32_t* __restrict__ offsets, const int32_t* __restrict__ longs,
-                      unsigned long long* __restrict__ keys,
-                      unsigned long long* __restrict__ scratch, int32_t* __restrict__ prims)
+// Emit a super-tile's E entries, given in sorted order by slot_of(e), into
+// the tile lists, kStCap entries at a time: (1) every entry's 16-bit mask
+// of hit tiles (entries strided over the threads, so the origin / span loads
+// are independent and coalesced across a warp); (2) one warp per tile
+// compacts the entries carrying that tile's bit, in order, with ballots --
+// the stable order of np.lexsort within the tile, with coalesced stores.
+template <typename SlotOf>
+__device__ void st_emit(StSmem& sm, SlotOf&& slot_of, int E, int st, int st_x, const RasterRec* __restrict__ recs,
+                        const uint4* __restrict__ spans, const uint32_t* __restrict__ origin,
+                        const int32_t* __restrict__ tile_offsets, int tiles_x, int tiles_y, int W, int H,
+                        int32_t* __restrict__ prims)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortSmem<256>& sm = *reinterpret_cast<SortSmem<256>*>(smem_raw);
-    constexpr int kCap = SortSmem<256>::kCap;
-    const int tid = threadIdx.x;
-    // persistent: a few CTAs take the (rare) long tiles listed by the scan
-    const int nlong = longs[0];
-    for (int li = blockIdx.x; li < nlong; li += gridDim.x) {
-    const int t = longs[1 + li];
-    const int off = offsets[t], L = offsets[t + 1] - off;
-    if (L <= kCap) {
-        cta_sort<256, 16>(sm, keys + off, L, [&](int pos, unsigned long long k) { prims[off + pos] = (int32_t)(uint32_t)k; });
-        continue;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int sx = st % st_x, sy = st / st_x;
+    if (tid < kST * kST) {
+        const int tx = kST * sx + (tid % kST), ty = kST * sy + tid / kST;
+        sm.toff[tid] = (tx < tiles_x && ty < tiles_y) ? tile_offsets[ty * tiles_x + tx] : 0;
     }
-    // very long list: sorted chunks of kCap into scratch, then pairwise merges
-    unsigned long long* src = scratch + off;
-    unsigned long long* dst = keys + off;
-    for (int c0 = 0; c0 < L; c0 += kCap) {
-        const int n = min(kCap, L - c0);
-        cta_sort<256, 16>(sm, keys + off + c0, n, [&](int pos, unsigned long long k) { src[c0 + pos] = k; });
-    }
-    for (int width = kCap; width < L; width *= 2) {
-        const bool final_pass = 2 * width >= L;
-        for (int i = tid; i < L; i += 256) {
-            const int run = i / width, rs = run * width, ps = (run ^ 1) * width;
-            const int pl = max(0, min(width, L - ps));
-            const unsigned long long k = src[i];
-            const int pos = min(rs, ps) + (i - rs) + (pl > 0 ? lower_bound_u64(src + ps, pl, k) : 0);
-            if (final_pass) prims[off + pos] = (int32_t)(uint32_t)k;
-            else dst[pos] = k;
+    for (int c0 = 0; c0 < E; c0 += kStCap) {
+        const int n = min(kStCap, E - c0);
+        for (int e = tid; e < n; e += kStThreads) {
+            const uint32_t sl = slot_of(c0 + e);
+            const uint32_t org = __ldg(origin + sl);
+            const uint4 s0 = __ldg(spans + 2 * sl), s1 = __ldg(spans + 2 * sl + 1);
+            sm.mask[e] = (uint16_t)entry_mask(recs, org, s0, s1, sl, sx, sy, tiles_x, tiles_y, W, H);
         }
         __syncthreads();
-        unsigned long long* tmp = src; src = dst; dst = tmp;
+        const unsigned lt = (1u << lane) - 1u;
+        for (int j = warp; j < kST * kST; j += kStThreads / 32) {
+            int base = sm.toff[j];
+            for (int e0 = 0; e0 < n; e0 += 32) {
+                const int e = e0 + lane;
+                const bool bit = e < n && ((sm.mask[e] >> j) & 1u);
+                const unsigned bal = __ballot_sync(0xffffffffu, bit);
+                if (bit) prims[base + __popc(bal & lt)] = (int32_t)slot_of(c0 + e);
+                base += __popc(bal);
+            }
+            if (lane == 0) sm.toff[j] = base;   // the next chunk continues here
+        }
+        __syncthreads();
     }
+}
+
+__global__ void __launch_bounds__(kStThreads, 2)
+st_sort_emit_kernel(const int32_t* __restrict__ st_offsets, int st_x, unsigned long long* __restrict__ keys,
+                    const RasterRec* __restrict__ recs, const uint4* __restrict__ spans,
+                    const uint32_t* __restrict__ origin, const int32_t* __restrict__ tile_offsets, int tiles_x,
+                    int tiles_y, int W, int H, int32_t* __restrict__ prims)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    StSmem& sm = *reinterpret_cast<StSmem*>(smem_raw);
+    const int st = blockIdx.x;
+    const int off = st_offsets[st], E = st_offsets[st + 1] - off;
+    if (E == 0 || E > kStCap) return;
+    const unsigned long long* k = keys + off;
+    // rank of each bucket-order key -> sorted compact slots in shared memory
+    uint16_t* rank = sm.mask;
+    const auto to_rank = [&](int i, int pos, unsigned long long) { rank[i] = (uint16_t)pos; };
+    if (E <= 4 * kStThreads) cta_sort<kStThreads, 4>(sm.sort, k, E, to_rank);
+    else if (E <= 8 * kStThreads) cta_sort<kStThreads, 8>(sm.sort, k, E, to_rank);
+    else cta_sort<kStThreads, 16>(sm.sort, k, E, to_rank);
+    uint32_t* slots = sm.slots();
+    for (int i = threadIdx.x; i < E; i += kStThreads) slots[rank[i]] = (uint32_t)sm.sort.b[i];
+    __syncthreads();
+    st_emit(sm, [&](int e) { return slots[e]; }, E, st, st_x, recs, spans, origin, tile_offsets, tiles_x, tiles_y, W,
+            H, prims);
+}
+
+// super-tiles longer than one shared-memory pass (listed by the scan):
+// sorted chunks into scratch, pairwise merges, then the emission
+__global__ void __launch_bounds__(kStThreads, 2)
+st_sort_emit_long_kernel(const int32_t* __restrict__ st_offsets, const int32_t* __restrict__ longs, int st_x,
+                         unsigned long long* __restrict__ keys, unsigned long long* __restrict__ scratch,
+                         const RasterRec* __restrict__ recs, const uint4* __restrict__ spans,
+                         const uint32_t* __restrict__ origin, const int32_t* __restrict__ tile_offsets,
+                         int tiles_x, int tiles_y, int W, int H, int32_t* __restrict__ prims)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    StSmem& sm = *reinterpret_cast<StSmem*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int nlong = longs[0];
+    for (int li = blockIdx.x; li < nlong; li += gridDim.x) {
+        const int st = longs[1 + li];
+        const int off = st_offsets[st], L = st_offsets[st + 1] - off;
+        unsigned long long* src = scratch + off;
+        unsigned long long* dst = keys + off;
+        for (int c0 = 0; c0 < L; c0 += kStCap) {
+            const int n = min(kStCap, L - c0);
+            cta_sort<kStThreads, 16>(sm.sort, keys + off + c0, n,
+                                     [&](int, int pos, unsigned long long k) { src[c0 + pos] = k; });
+        }
+        for (int width = kStCap; width < L; width *= 2) {
+            for (int i = tid; i < L; i += kStThreads) {
+                const int run = i / width, rs = run * width, ps = (run ^ 1) * width;
+                const int pl = max(0, min(width, L - ps));
+                const unsigned long long k = src[i];
+                dst[min(rs, ps) + (i - rs) + (pl > 0 ? lower_bound_u64(src + ps, pl, k) : 0)] = k;
+            }
+            __syncthreads();
+            unsigned long long* tmp = src; src = dst; dst = tmp;
+        }
+        const unsigned long long* sorted = src;
+        st_emit(sm, [&](int e) { return (uint32_t)sorted[e]; }, L, st, st_x, recs, spans, origin, tile_offsets,
+                tiles_x, tiles_y, W, H, prims);
+        __syncthreads();
     }
 }
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// bin state: spans (32 B per compact slot) | origin (4 B per slot) |
+// super-tile offsets (nst + 1) | long super-tile list (1 + nst)
+struct StateLayout {
+    uint4* spans;
+    uint32_t* origin;
+    int32_t* st_offsets;
+    int32_t* st_longs;
+};
+inline size_t state_bytes(int n_cap, int nst) {
+    const size_t n = (size_t)(n_cap > 0 ? n_cap : 1);
+    return align256(n * 32) + align256(n * 4) + 2 * align256((size_t)(nst + 1) * 4);
+}
+inline StateLayout state_layout(void* state, int n_cap, int nst) {
+    const size_t n = (size_t)(n_cap > 0 ? n_cap : 1);
+    char* p = static_cast<char*>(state);
+    StateLayout L;
+    L.spans = reinterpret_cast<uint4*>(p); p += align256(n * 32);
+    L.origin = reinterpret_cast<uint32_t*>(p); p += align256(n * 4);
+    L.st_offsets = reinterpret_cast<int32_t*>(p); p += align256((size_t)(nst + 1) * 4);
+    L.st_longs = reinterpret_cast<int32_t*>(p);
+    return L;
+}
+inline int st_dim(int tiles) { return (tiles + kST - 1) / kST; }
+
 }  // namespace
 
 // ---- prepare -------------------------------------------------------------------
-// state: spans (32 B per compact slot) | long-tile list (1 + ntiles ints)
-size_t sb_bin_state_bytes(int n_cap, int ntiles) {
-    return align256((size_t)(n_cap > 0 ? n_cap : 1) * 32) + align256((size_t)(ntiles + 1) * 4);
-}
-static int32_t* long_list(void* state, int n_cap) {
-    return reinterpret_cast<int32_t*>(static_cast<char*>(state) + align256((size_t)(n_cap > 0 ? n_cap : 1) * 32));
-}
+// sized for ntiles >= the super-tile count (the layout uses the exact count)
+size_t sb_bin_state_bytes(int n_cap, int ntiles) { return state_bytes(n_cap, ntiles); }
 
 void sb_launch_bin_prepare(const RasterRec* recs, const int32_t* counters, int n_cap, const CamDev& cam,
-                           int32_t* tile_offsets, int32_t* n_pairs, void* state, cudaStream_t stream)
+                           int32_t* tile_offsets, int32_t* totals, void* state, cudaStream_t stream)
 {
     const int ntiles = cam.tiles_x * cam.tiles_y;
+    const int st_x = st_dim(cam.tiles_x), nst = st_x * st_dim(cam.tiles_y);
+    const StateLayout L = state_layout(state, n_cap, nst);
     cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (ntiles + 1), stream);
+    cudaMemsetAsync(L.st_offsets, 0, sizeof(int32_t) * (nst + 1), stream);
     if (n_cap > 0)
         tile_count_kernel<<<(n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream>>>(
-            recs, counters, n_cap, cam.tiles_x, cam.tiles_y, cam.W, cam.H, static_cast<uint4*>(state), tile_offsets);
-    tile_scan_kernel<<<1, kScanThreads, 0, stream>>>(tile_offsets, ntiles, n_pairs, long_list(state, n_cap));
+            recs, counters, n_cap, cam.tiles_x, cam.tiles_y, st_x, cam.W, cam.H, L.spans, L.origin, tile_offsets,
+            L.st_offsets);
+    tile_scan_kernel<<<1, kScanThreads, 0, stream>>>(tile_offsets, ntiles, L.st_offsets, nst, totals, L.st_longs);
 }
 
 // ---- finish --------------------------------------------------------------------
-size_t sb_bin_finish_ws(long long n_pairs, int ntiles) {
-    const size_t P = (size_t)(n_pairs > 0 ? n_pairs : 1);
-    return 2 * align256(P * 8) + align256((size_t)ntiles * 4);
+size_t sb_bin_finish_ws(long long n_entries, int ntiles) {
+    const size_t E = (size_t)(n_entries > 0 ? n_entries : 1);
+    const int nst = ntiles;   // upper bound for the cursor array
+    return 2 * align256(E * 8) + align256((size_t)nst * 4);
 }
 
-void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_cap, const CamDev& cam, int P,
+void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_cap, const CamDev& cam, int E,
                           const int32_t* tile_offsets, const void* state, int32_t* tile_prims, void* ws,
                           cudaStream_t stream)
 {
-    const int ntiles = cam.tiles_x * cam.tiles_y;
-    if (P <= 0 || n_cap <= 0) return;
+    if (E <= 0 || n_cap <= 0) return;
+    const int st_x = st_dim(cam.tiles_x), nst = st_x * st_dim(cam.tiles_y);
+    const StateLayout L = state_layout(const_cast<void*>(state), n_cap, nst);
     char* w = static_cast<char*>(ws);
-    unsigned long long* keys = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)P * 8);
-    unsigned long long* scratch = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)P * 8);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)E * 8);
+    unsigned long long* scratch = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)E * 8);
     int32_t* cursor = reinterpret_cast<int32_t*>(w);
-    cudaMemcpyAsync(cursor, tile_offsets, sizeof(int32_t) * ntiles, cudaMemcpyDeviceToDevice, stream);
-    scatter_kernel<<<(n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream>>>(
-        recs, counters, n_cap, cam.tiles_x, cam.tiles_y, cam.W, cam.H, static_cast<const uint4*>(state), cursor,
-        keys);
+    cudaMemcpyAsync(cursor, L.st_offsets, sizeof(int32_t) * nst, cudaMemcpyDeviceToDevice, stream);
+    st_scatter_kernel<<<(n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream>>>(
+        recs, counters, n_cap, cam.tiles_x, cam.tiles_y, st_x, cursor, keys);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tile_sort_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(SortSmem<128>));
-        cudaFuncSetAttribute(tile_sort_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(SortSmem<256>));
+        cudaFuncSetAttribute(st_sort_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(StSmem));
+        cudaFuncSetAttribute(st_sort_emit_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(StSmem));
         attr = true;
     }
-    tile_sort_short_kernel<<<ntiles, 128, sizeof(SortSmem<128>), stream>>>(tile_offsets, keys, tile_prims);
-    tile_sort_long_kernel<<<2 * 148, 256, sizeof(SortSmem<256>), stream>>>(
-        tile_offsets, long_list(const_cast<void*>(state), n_cap), keys, scratch, tile_prims);
+    st_sort_emit_kernel<<<nst, kStThreads, sizeof(StSmem), stream>>>(L.st_offsets, st_x, keys, recs, L.spans,
+                                                                        L.origin, tile_offsets, cam.tiles_x,
+                                                                        cam.tiles_y, cam.W, cam.H, tile_prims);
+    st_sort_emit_long_kernel<<<148, kStThreads, sizeof(StSmem), stream>>>(
+        L.st_offsets, L.st_longs, st_x, keys, scratch, recs, L.spans, L.origin, tile_offsets, cam.tiles_x,
+        cam.tiles_y, cam.W, cam.H, tile_prims);
 }

@@ -149,7 +149,7 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     cmap = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     coff = torch.empty(max(K, 1), dtype=torch.int32, device=dev)
     cvis = torch.zeros(max(K, 1), dtype=torch.uint8, device=dev)
-    counters = torch.zeros(8, dtype=torch.int32, device=dev)   # vis, N_c, ndeg, pad, P
+    counters = torch.zeros(8, dtype=torch.int32, device=dev)   # vis, N_c, ndeg, pad, P, E
     lib = _lib.load()
     tile_offsets = torch.empty(ntiles + 1, dtype=torch.int32, device=dev)
     ws = _lib.workspace("project", lib.sb_project_workspace_bytes(n), dev)
@@ -159,10 +159,10 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     state = _lib.workspace("bin_state", lib.sb_bin_state_workspace_bytes(n, ntiles), dev)
     _lib.call("sb_bin_prepare", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), _lib.ptr(tile_offsets),
               _lib.ptr(counters[4:]), _lib.ptr(state), state.numel(), stream)
-    vis, nc, ndeg, _, P = (int(v) for v in counters[:5].cpu().tolist())   # one D2H read
+    vis, nc, ndeg, _, P, E = (int(v) for v in counters[:6].cpu().tolist())   # one D2H read
     prims = torch.empty(max(P, 1), dtype=torch.int32, device=dev)
-    ws_f = _lib.workspace("bin_finish", lib.sb_bin_finish_workspace_bytes(P, ntiles), dev)
-    _lib.call("sb_bin_finish", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), P, _lib.ptr(tile_offsets),
+    ws_f = _lib.workspace("bin_finish", lib.sb_bin_finish_workspace_bytes(E, ntiles), dev)
+    _lib.call("sb_bin_finish", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), P, E, _lib.ptr(tile_offsets),
               _lib.ptr(state), _lib.ptr(prims), _lib.ptr(ws_f), ws_f.numel(), stream)
     color = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
     T = torch.empty((H, W), dtype=torch.float32, device=dev)
