@@ -43,7 +43,8 @@ typedef struct sb_raster_cfg {
     float low_pass;        /* 0.3 px^2 */
     int32_t use_culling;   /* 1: cluster cull + compact; 0: identity map     */
     int32_t conic_reduce;  /* 0: exp_aligned, 1: tree                        */
-    int32_t half_state;    /* 1: fp16 blending state (forward.py:194-230)    */
+    int32_t half_state;    /* 1: fp16 blending state (forward.py:194-230);
+                              2: bf16 blending state (a variant)          */
 } sb_raster_cfg;
 
 /* Per-compact-primitive screen-gradient record written by the raster

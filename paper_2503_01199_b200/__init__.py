@@ -11,6 +11,7 @@ its C-ABI (include/splat_b200.h).  There is no CPU fallback.
 from .backward import BackwardResult, DensifyStats, SceneGrads, backward
 from .camera import CameraView, build_frustum, look_at
 from .ccc import morton_sort
+from .checkpoint import adam_state_from, checkpoint, load_checkpoint, load_ply, save_checkpoint, save_ply
 from .densify import DensifyConfig, densify_step, opacity_decay, prune, variance_score
 from .errors import ShapeMismatchError, StaleSceneError, TrainingDiverged, ValidationError
 from .forward import RasterConfig, RenderContext, RenderOutput, forward, render
@@ -23,6 +24,7 @@ from .train import TrainConfig, TrainResult, train
 __all__ = [
     "BackwardResult", "DensifyStats", "SceneGrads", "backward",
     "CameraView", "build_frustum", "look_at", "morton_sort",
+    "adam_state_from", "checkpoint", "load_checkpoint", "load_ply", "save_checkpoint", "save_ply",
     "DensifyConfig", "densify_step", "opacity_decay", "prune", "variance_score",
     "ShapeMismatchError", "StaleSceneError", "TrainingDiverged", "ValidationError",
     "RasterConfig", "RenderContext", "RenderOutput", "forward", "render",

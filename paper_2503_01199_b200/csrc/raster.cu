@@ -38,6 +38,7 @@
 // the 48-byte records of the next 32 list entries are fetched into registers
 // while the current 32 are consumed from a warp-private shared-memory slab.
 #include <cuda_fp16.h>
+#include <cuda_bf16.h>
 #include "common.cuh"
 
 namespace {
@@ -257,21 +258,35 @@ raster_fwd_kernel(FwdParams p)
 
 // forward.py:194-230 (half_path_blend): the exponent and G in float32 (the
 // shared lane_G), then G, opacity, colour, alpha, T and every accumulation
-// in IEEE binary16 (__half ops round once per op, like numpy's float16).
+// in a 16-bit float: IEEE binary16 (__half ops round once per op, like
+// numpy's float16) or, as a variant the reference does not have (SURVEY
+// 8(f) rank 4), bfloat16.
+template <typename T> struct Half16;
+template <> struct Half16<__half> {
+    static SB_INLINE __half from(float f) { return __float2half_rn(f); }
+    static SB_INLINE float to(__half h) { return __half2float(h); }
+};
+template <> struct Half16<__nv_bfloat16> {
+    static SB_INLINE __nv_bfloat16 from(float f) { return __float2bfloat16_rn(f); }
+    static SB_INLINE float to(__nv_bfloat16 h) { return __bfloat162float(h); }
+};
+
+template <typename H>
 __global__ void __launch_bounds__(kThreads)
 raster_fwd_half_kernel(FwdParams p)
 {
+    using O = Half16<H>;
     __shared__ SRec slabs[kWarpsPerBlock][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     SRec* slab = slabs[warp];
-    const __half amin = __float2half_rn(p.amin), amax = __float2half_rn(p.amax), tstop = __float2half_rn(p.tstop);
-    const __half one = __float2half_rn(1.0f), zero = __float2half_rn(0.0f);
+    const H amin = O::from(p.amin), amax = O::from(p.amax), tstop = O::from(p.tstop);
+    const H one = O::from(1.0f), zero = O::from(0.0f);
     for (int t = next_tile(p.tile_counter, lane); t < p.ntiles; t = next_tile(p.tile_counter, lane)) {
         const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
         const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
         const float px = (float)pxi, py0 = (float)py0i;
         bool valid[4];
-        __half T[4], rgb[4][3];
+        H T[4], rgb[4][3];
         int frags[4], last[4];
 #pragma unroll
         for (int i = 0; i < 4; i++) {
@@ -306,14 +321,14 @@ raster_fwd_half_kernel(FwdParams p)
                 const SRec& r = slab[j];
                 float G[4], dx, dy;
                 lane_G(r, px, py0, G, dx, dy);
-                const __half o = __float2half_rn(r.o);
-                const __half c[3] = {__float2half_rn(r.r), __float2half_rn(r.g), __float2half_rn(r.bl)};
+                const H o = O::from(r.o);
+                const H c[3] = {O::from(r.r), O::from(r.g), O::from(r.bl)};
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
-                    __half alpha = __hmul(o, __float2half_rn(G[i]));
+                    H alpha = __hmul(o, O::from(G[i]));
                     if (__hgt(alpha, amax)) alpha = amax;
                     if (valid[i] && __hge(T[i], tstop) && __hge(alpha, amin)) {
-                        const __half w = __hmul(T[i], alpha);
+                        const H w = __hmul(T[i], alpha);
                         rgb[i][0] = __hadd(rgb[i][0], __hmul(w, c[0]));
                         rgb[i][1] = __hadd(rgb[i][1], __hmul(w, c[1]));
                         rgb[i][2] = __hadd(rgb[i][2], __hmul(w, c[2]));
@@ -330,9 +345,8 @@ raster_fwd_half_kernel(FwdParams p)
             const size_t pix = (size_t)(py0i + i) * p.W + pxi;
 #pragma unroll
             for (int ch = 0; ch < 3; ch++)
-                p.out_color[3 * pix + ch] =
-                    __half2float(__hadd(rgb[i][ch], __hmul(T[i], __float2half_rn(p.bg[ch]))));
-            p.out_T[pix] = __half2float(T[i]);
+                p.out_color[3 * pix + ch] = O::to(__hadd(rgb[i][ch], __hmul(T[i], O::from(p.bg[ch]))));
+            p.out_T[pix] = O::to(T[i]);
             p.out_frags[pix] = frags[i];
             p.out_last[pix] = last[i];
         }
@@ -698,7 +712,8 @@ void sb_launch_raster_fwd(const RasterRec* recs, const int32_t* offsets, const i
     const int want = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const int blocks = min(want, sm_count() * 8);
     if (!blocks) return;
-    if (cfg.half_state) raster_fwd_half_kernel<<<blocks, kThreads, 0, stream>>>(p);
+    if (cfg.half_state == 2) raster_fwd_half_kernel<__nv_bfloat16><<<blocks, kThreads, 0, stream>>>(p);
+    else if (cfg.half_state) raster_fwd_half_kernel<__half><<<blocks, kThreads, 0, stream>>>(p);
     else raster_fwd_kernel<<<blocks, kThreads, 0, stream>>>(p);
 }
 

@@ -43,7 +43,7 @@ class RasterConfig:
     use_culling: bool = True
     conic_reduce: str = "exp_aligned"   # backward: "exp_aligned" | "tree"
 
-    def struct(self, half: bool = False) -> _lib.SbRasterCfg:
+    def struct(self, half=False) -> _lib.SbRasterCfg:
         if self.dtype != "float32":
             raise ValueError("the B200 path rasterizes in float32 (dtype='float32'); "
                              "float64 exists only in the CPU oracle")
@@ -57,7 +57,7 @@ class RasterConfig:
         s.low_pass = self.low_pass
         s.use_culling = int(bool(self.use_culling))
         s.conic_reduce = 0 if self.conic_reduce == "exp_aligned" else 1
-        s.half_state = int(bool(half))
+        s.half_state = _half_mode(half)
         return s
 
 
@@ -99,7 +99,7 @@ class RenderContext:
     transmittance: torch.Tensor   # (H, W)
     last: torch.Tensor            # (H, W) int32
     n_degenerate: int = 0
-    half: bool = False            # produced by the fp16 blending-state path
+    half: bool | str = False      # produced by a 16-bit blending-state path
     _tiles: list | None = field(default=None, repr=False)
 
     @property
@@ -133,7 +133,19 @@ class RenderContext:
         }
 
 
-def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, half: bool):
+def _half_mode(half) -> int:
+    """half=False: float32 state; True / "fp16": the reference's binary16
+    path (forward.py:194-230); "bf16": a bfloat16 variant."""
+    if half is False or half is None:
+        return 0
+    if half is True or half == "fp16":
+        return 1
+    if half == "bf16":
+        return 2
+    raise ValueError(f"half must be False, True, 'fp16' or 'bf16', not {half!r}")
+
+
+def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, half):
     _lib.require_cuda(scene.data)
     dev = scene.device
     n = scene.n
@@ -181,12 +193,12 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     return out, ctx
 
 
-def forward(scene: SceneSoA, camera, config: RasterConfig | None = None, counter=None, half: bool = False):
+def forward(scene: SceneSoA, camera, config: RasterConfig | None = None, counter=None, half=False):
     """Render `scene` from `camera`; returns (RenderOutput, RenderContext).
 
-    forward.py:258-304.  half=True renders with fp16 blending state
-    (forward.py:194-230); the backward then replays in float32 as the
-    reference does.  `counter` (the reference's CPU op tally) is not
+    forward.py:258-304.  half=True (or "fp16") renders with fp16 blending
+    state (forward.py:194-230), half="bf16" with bfloat16 state; the backward
+    then replays in float32 as the reference does.  `counter` (the reference's CPU op tally) is not
     applicable on the device and must be None; use ncu counters instead."""
     if counter is not None:
         raise ValueError("OpCounter instrumentation is CPU-only; profile the device path with ncu")

@@ -372,6 +372,28 @@ def test_half_path_vs_reference(fname, prefix):
     assert G.floored_rel(g_h, g_f) <= 1e-3
 
 
+@pytest.mark.parametrize("fname,prefix", G.CASES)
+def test_bf16_state_variant(fname, prefix):
+    """bfloat16 blending state (unpinned by the
+    reference, which only has the fp16 path): PSNR against the fp32 image
+    and a float32 backward replay identical to the fp32 forward's."""
+    sb = _sb()
+    d = G.load(fname)
+    scene, cam, cfg = _scene(d, prefix), G.camera(d, prefix), _cfg(d, prefix)
+    out, ctx = sb.forward(scene, cam, cfg, half="bf16")
+    col = out.color.cpu().numpy().astype(np.float64)
+    mse = ((col - d[f"{prefix}fwd_color"]) ** 2).mean()
+    db = 99.0 if mse == 0 else 10 * np.log10(1 / mse)
+    print(f"bf16 state PSNR vs fp32: {db:.1f} dB")
+    assert db >= 42.0   # measured 46.4-51.4 dB on the fixtures
+    res_b = sb.backward(scene, ctx, torch.from_numpy(d[f"{prefix}dL_dI"]), sb.DensifyStats.zeros(scene.n))
+    _, ctx32 = sb.forward(scene, cam, cfg)
+    res_f = sb.backward(scene, ctx32, torch.from_numpy(d[f"{prefix}dL_dI"]), sb.DensifyStats.zeros(scene.n))
+    assert G.floored_rel(res_b.grads.packed.double().cpu().numpy(), res_f.grads.packed.double().cpu().numpy()) <= 1e-3
+    with pytest.raises(ValueError):
+        sb.forward(scene, cam, cfg, half="fp8")
+
+
 def test_densify_hooks_vs_reference():
     """densify.py:57-187: variance score -> top-k selection (score desc, index
     asc) -> clone / split -> prune -> stats reset -> Morton re-sort."""
