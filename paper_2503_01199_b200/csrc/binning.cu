@@ -297,10 +297,24 @@ tile_count_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict_
                 atomicAdd(&counts[(q.ty0 + k) * tiles_x + tx], 1);
         }
     }
-    // super-tile entries (every super-tile the rectangle overlaps)
-    const bool sfits = setup_st_window(sm, q);
+    // super-tile entries (every super-tile the rectangle overlaps), in a
+    // window derived from the tile window (floor division is monotone);
+    // primitives outside it (beyond the span format) add globally
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sm.sx0 = sm.x0 / kST; sm.sy0 = sm.y0 / kST;
+        sm.sw = sm.w > 0 ? (sm.x0 + sm.w - 1) / kST - sm.sx0 + 1 : 0;
+        sm.sh = sm.h > 0 ? (sm.y0 + sm.h - 1) / kST - sm.sy0 + 1 : 0;
+    }
+    __syncthreads();
+    const bool sfits = fits && sm.sw * sm.sh <= kStWin;
     if (sfits) {
-        for_each_st(q, [&](int sx, int sy) { atomicAdd(&sm.scnt[(sy - sm.sy0) * sm.sw + (sx - sm.sx0)], 1); });
+        for (int i = threadIdx.x; i < sm.sw * sm.sh; i += kBinThreads) sm.scnt[i] = 0;
+        __syncthreads();
+        for_each_st(q, [&](int sx, int sy) {
+            if (q.spans) atomicAdd(&sm.scnt[(sy - sm.sy0) * sm.sw + (sx - sm.sx0)], 1);
+            else atomicAdd(&st_counts[sy * st_x + sx], 1);
+        });
         __syncthreads();
         for (int i = threadIdx.x; i < sm.sw * sm.sh; i += kBinThreads) {
             const int c = sm.scnt[i];
