@@ -94,10 +94,14 @@ size_t sb_bin_state_workspace_bytes(int64_t n_cap, int32_t ntiles);
 int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam,
                    int32_t* tile_offsets, int32_t* totals, void* state, size_t state_bytes, sb_stream_t stream);
 
-/* tiles.py:50-107 binning, part 2 (P and E from part 1, `state` as part 1
- * left it): depth-sort each super-tile's entries once and emit the per-tile
- * lists: tile_prims[P] (compact slots, per tile in (depth, index) order ==
- * np.lexsort((prim, depth, tile_id)) of tiles.py:98). */
+/* tiles.py:50-107 binning, part 2 (`state` as part 1 left it):
+ * depth-sort each super-tile's entries once and emit the per-tile lists:
+ * tile_prims (compact slots, per tile in (depth, index) order ==
+ * np.lexsort((prim, depth, tile_id)) of tiles.py:98).  n_pairs / n_entries
+ * are CAPACITIES: tile_prims holds n_pairs slots and ws was sized with
+ * n_entries.  The call can be made before the host has read P and E: if the
+ * device totals exceed the capacities nothing is written, and the caller,
+ * once it has read counters[4:6], re-launches with larger buffers. */
 size_t sb_bin_finish_workspace_bytes(int64_t n_entries, int32_t ntiles);
 int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam, int64_t n_pairs,
                   int64_t n_entries, const int32_t* tile_offsets, const void* state, int32_t* tile_prims, void* ws,

@@ -137,11 +137,4 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
     _lib.call("sb_chain_projection_bwd", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s),
               _lib.ptr(ctx.cluster_offset), _lib.ptr(ctx.recs), _lib.ptr(sgrad), _lib.ptr(grads), _lib.ptr(stats.S),
               _lib.ptr(stats.M), _lib.ptr(stats.C), stream)
-    return BackwardResult(grads=SceneGrads(grads), stats=stats, cluster_mask=ctx.cluster_vis.bool())
-
-
-def screen_grads(ctx: RenderContext) -> torch.Tensor:
-    """The last backward's compact screen-space records as (N_c, 16) float32
-    view: a b c u v o r g b | C(int) | S(f64) | M(f64) (debug / parity)."""
-    buf = _lib._arena[("sgrad", str(ctx.recs.device))]
-    return buf[: ctx.n_compact * SGRAD_BYTES].view(torch.float32).reshape(ctx.n_compact, 16)
+    return BackwardResult(grads=SceneGrads(grads), stats=stats, cluster_mask=ctx.cluster_vis.view(torch.bool))

@@ -13,8 +13,8 @@ size_t sb_bin_state_bytes(int n_cap, int ntiles);
 void sb_launch_bin_prepare(const RasterRec*, const int32_t*, int, const CamDev&, int32_t*, int32_t*, void*,
                            cudaStream_t);
 size_t sb_bin_finish_ws(long long n_entries, int ntiles);
-void sb_launch_bin_finish(const RasterRec*, const int32_t*, int, const CamDev&, int, const int32_t*, const void*,
-                          int32_t*, void*, cudaStream_t);
+void sb_launch_bin_finish(const RasterRec*, const int32_t*, int, const CamDev&, int, int, const int32_t*,
+                          const void*, int32_t*, void*, cudaStream_t);
 size_t sb_sort_u64_ws(int n, int bits);
 int sb_launch_sort_u64(unsigned long long*, uint32_t*, unsigned long long*, uint32_t*, int, int, void*, cudaStream_t);
 void sb_launch_raster_fwd(const RasterRec*, const int32_t*, const int32_t*, int, int, int, int, const sb_raster_cfg&,
@@ -183,7 +183,7 @@ int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, cons
         return fail(SB_EWORKSPACE, "bin finish workspace too small");
     if (n_pairs > 0)
         sb_launch_bin_finish(static_cast<const RasterRec*>(recs), counters, (int)n_cap, d, (int)n_entries,
-                             tile_offsets, state, tile_prims, ws, S(stream));
+                             (int)n_pairs, tile_offsets, state, tile_prims, ws, S(stream));
     return check_launch("sb_bin_finish");
 }
 

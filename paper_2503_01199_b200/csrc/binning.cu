@@ -404,9 +404,11 @@ tile_scan_kernel(int32_t* __restrict__ offsets, int ntiles, int32_t* __restrict_
 // ---- finish (1): scatter keys into super-tile ranges ---------------------------
 __global__ void __launch_bounds__(kBinThreads)
 st_scatter_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ counters, int n_cap, int tiles_x,
-                  int tiles_y, int st_x, int32_t* __restrict__ cursor, unsigned long long* __restrict__ keys)
+                  int tiles_y, int st_x, int32_t* __restrict__ cursor, unsigned long long* __restrict__ keys,
+                  int e_cap, int p_cap)
 {
     __shared__ WinSmem sm;
+    if (counters[5] > e_cap || counters[4] > p_cap) return;   // buffers too small: the caller re-launches
     const int nc = min(counters[1], n_cap);
     const int s = blockIdx.x * kBinThreads + threadIdx.x;
     if (blockIdx.x * kBinThreads >= nc) return;
@@ -673,8 +675,10 @@ __global__ void __launch_bounds__(kStThreads, 2)
 st_sort_emit_kernel(const int32_t* __restrict__ st_offsets, int st_x, unsigned long long* __restrict__ keys,
                     const RasterRec* __restrict__ recs, const uint4* __restrict__ spans,
                     const uint32_t* __restrict__ origin, const int32_t* __restrict__ tile_offsets, int tiles_x,
-                    int tiles_y, int W, int H, int32_t* __restrict__ prims)
+                    int tiles_y, int W, int H, int32_t* __restrict__ prims, const int32_t* __restrict__ counters,
+                    int e_cap, int p_cap)
 {
+    if (counters[5] > e_cap || counters[4] > p_cap) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StSmem& sm = *reinterpret_cast<StSmem*>(smem_raw);
     const int st = blockIdx.x;
@@ -701,8 +705,10 @@ st_sort_emit_long_kernel(const int32_t* __restrict__ st_offsets, const int32_t* 
                          unsigned long long* __restrict__ keys, unsigned long long* __restrict__ scratch,
                          const RasterRec* __restrict__ recs, const uint4* __restrict__ spans,
                          const uint32_t* __restrict__ origin, const int32_t* __restrict__ tile_offsets,
-                         int tiles_x, int tiles_y, int W, int H, int32_t* __restrict__ prims)
+                         int tiles_x, int tiles_y, int W, int H, int32_t* __restrict__ prims,
+                         const int32_t* __restrict__ counters, int e_cap, int p_cap)
 {
+    if (counters[5] > e_cap || counters[4] > p_cap) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StSmem& sm = *reinterpret_cast<StSmem*>(smem_raw);
     const int tid = threadIdx.x;
@@ -788,20 +794,24 @@ size_t sb_bin_finish_ws(long long n_entries, int ntiles) {
     return 2 * align256(E * 8) + align256((size_t)nst * 4);
 }
 
-void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_cap, const CamDev& cam, int E,
-                          const int32_t* tile_offsets, const void* state, int32_t* tile_prims, void* ws,
+// e_cap / p_cap: what the keys workspace and tile_prims hold.  When the
+// device totals (counters[5] = E, counters[4] = P) exceed them the kernels
+// write nothing; the caller compares the totals with the capacities once it
+// has read them and re-launches with larger buffers.
+void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_cap, const CamDev& cam, int e_cap,
+                          int p_cap, const int32_t* tile_offsets, const void* state, int32_t* tile_prims, void* ws,
                           cudaStream_t stream)
 {
-    if (E <= 0 || n_cap <= 0) return;
+    if (e_cap <= 0 || p_cap <= 0 || n_cap <= 0) return;
     const int st_x = st_dim(cam.tiles_x), nst = st_x * st_dim(cam.tiles_y);
     const StateLayout L = state_layout(const_cast<void*>(state), n_cap, nst);
     char* w = static_cast<char*>(ws);
-    unsigned long long* keys = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)E * 8);
-    unsigned long long* scratch = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)E * 8);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)e_cap * 8);
+    unsigned long long* scratch = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)e_cap * 8);
     int32_t* cursor = reinterpret_cast<int32_t*>(w);
     cudaMemcpyAsync(cursor, L.st_offsets, sizeof(int32_t) * nst, cudaMemcpyDeviceToDevice, stream);
     st_scatter_kernel<<<(n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream>>>(
-        recs, counters, n_cap, cam.tiles_x, cam.tiles_y, st_x, cursor, keys);
+        recs, counters, n_cap, cam.tiles_x, cam.tiles_y, st_x, cursor, keys, e_cap, p_cap);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(st_sort_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(StSmem));
@@ -811,8 +821,9 @@ void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_
     }
     st_sort_emit_kernel<<<nst, kStThreads, sizeof(StSmem), stream>>>(L.st_offsets, st_x, keys, recs, L.spans,
                                                                         L.origin, tile_offsets, cam.tiles_x,
-                                                                        cam.tiles_y, cam.W, cam.H, tile_prims);
+                                                                        cam.tiles_y, cam.W, cam.H, tile_prims,
+                                                                        counters, e_cap, p_cap);
     st_sort_emit_long_kernel<<<148, kStThreads, sizeof(StSmem), stream>>>(
         L.st_offsets, L.st_longs, st_x, keys, scratch, recs, L.spans, L.origin, tile_offsets, cam.tiles_x,
-        cam.tiles_y, cam.W, cam.H, tile_prims);
+        cam.tiles_y, cam.W, cam.H, tile_prims, counters, e_cap, p_cap);
 }

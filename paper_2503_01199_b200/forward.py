@@ -133,6 +133,20 @@ class RenderContext:
         }
 
 
+# (device, W, H) -> (pair, super-tile entry) capacities of the binning buffers
+_bin_capacity: dict = {}
+_pinned: dict = {}
+
+
+def _pinned_counters(dev) -> torch.Tensor:
+    """Pinned host mirror of the counters (one per device; the forward waits
+    on its copy before returning, so it is never in flight twice)."""
+    key = str(dev)
+    if key not in _pinned:
+        _pinned[key] = torch.empty(8, dtype=torch.int32, pin_memory=True)
+    return _pinned[key]
+
+
 def _half_mode(half) -> int:
     """half=False: float32 state; True / "fp16": the reference's binary16
     path (forward.py:194-230); "bf16": a bfloat16 variant."""
@@ -160,7 +174,7 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     recs = torch.empty((max(n, 1), REC_FLOATS), dtype=torch.float32, device=dev)
     cmap = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     coff = torch.empty(max(K, 1), dtype=torch.int32, device=dev)
-    cvis = torch.zeros(max(K, 1), dtype=torch.uint8, device=dev)
+    cvis = torch.empty(max(K, 1), dtype=torch.uint8, device=dev)   # written for every cluster
     counters = torch.zeros(8, dtype=torch.int32, device=dev)   # vis, N_c, ndeg, pad, P, E
     lib = _lib.load()
     tile_offsets = torch.empty(ntiles + 1, dtype=torch.int32, device=dev)
@@ -171,11 +185,33 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     state = _lib.workspace("bin_state", lib.sb_bin_state_workspace_bytes(n, ntiles), dev)
     _lib.call("sb_bin_prepare", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), _lib.ptr(tile_offsets),
               _lib.ptr(counters[4:]), _lib.ptr(state), state.numel(), stream)
-    vis, nc, ndeg, _, P, E = (int(v) for v in counters[:6].cpu().tolist())   # one D2H read
-    prims = torch.empty(max(P, 1), dtype=torch.int32, device=dev)
-    ws_f = _lib.workspace("bin_finish", lib.sb_bin_finish_workspace_bytes(E, ntiles), dev)
-    _lib.call("sb_bin_finish", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), P, E, _lib.ptr(tile_offsets),
-              _lib.ptr(state), _lib.ptr(prims), _lib.ptr(ws_f), ws_f.numel(), stream)
+    # Binning part 2 is launched before the host knows P and E, with the
+    # capacities of earlier views of this resolution; the one device-to-host
+    # read below then overlaps it, and it is re-launched only if they were
+    # exceeded (its kernels write nothing in that case).
+    key = (str(dev), W, H)
+    p_cap, e_cap = _bin_capacity.get(key, (0, 0))
+
+    def finish(p_cap, e_cap):
+        prims = torch.empty(max(p_cap, 1), dtype=torch.int32, device=dev)
+        ws_f = _lib.workspace("bin_finish", lib.sb_bin_finish_workspace_bytes(e_cap, ntiles), dev)
+        _lib.call("sb_bin_finish", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), p_cap, e_cap,
+                  _lib.ptr(tile_offsets), _lib.ptr(state), _lib.ptr(prims), _lib.ptr(ws_f), ws_f.numel(), stream)
+        return prims
+
+    host = _pinned_counters(dev)
+    host.copy_(counters, non_blocking=True)           # queued before part 2
+    ready = torch.cuda.Event()
+    ready.record()
+    prims = finish(p_cap, e_cap) if p_cap else None
+    ready.synchronize()                                # the one device-to-host read
+    vis, nc, ndeg, _, P, E = (int(v) for v in host[:6].tolist())
+    if P > p_cap or E > e_cap:
+        p_cap, e_cap = P + P // 4 + 1024, E + E // 4 + 1024
+        _bin_capacity[key] = (p_cap, e_cap)
+        prims = finish(p_cap, e_cap)
+    if prims is None:
+        prims = torch.empty(1, dtype=torch.int32, device=dev)
     color = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
     T = torch.empty((H, W), dtype=torch.float32, device=dev)
     frags = torch.empty((H, W), dtype=torch.int32, device=dev)

@@ -84,7 +84,8 @@ def adam_step(scene: SceneSoA, grads, state: AdamState, cluster_mask, lrs: dict,
     if not isinstance(grads, SceneGrads):
         grads = SceneGrads.from_dict(grads.as_dict() if hasattr(grads, "as_dict") else grads, n, scene.device)
     packed = grads.packed.contiguous()
-    mask = torch.as_tensor(cluster_mask, device=scene.device).to(torch.uint8).contiguous()
+    mask = torch.as_tensor(cluster_mask, device=scene.device)
+    mask = (mask.view(torch.uint8) if mask.dtype == torch.bool else mask.to(torch.uint8)).contiguous()
     lr = (C.c_double * 5)(*[float(lrs[k]) for k in RAW_CHANNELS])
     _lib.call("sb_adam_sparse", _lib.ptr(scene.data), _lib.ptr(packed), _lib.ptr(state.m_rows),
               _lib.ptr(state.v_rows), _lib.ptr(state.step), _lib.ptr(mask), n, lr,
