@@ -283,7 +283,8 @@ def main():
     from paper_2503_01199_b200 import _lib
     scene, state, views, targets_host = build_workload(device)
     trainer = Trainer(scene, state, views, ws, rank)
-    targets_dev = [t.to(device).float().div_(255.0) for t in targets_host]
+    # targets stay uint8 (the dataset format); the fused loss reads them directly
+    targets_dev = [t.to(device) for t in targets_host]
 
     it = {"i": 0}
 
@@ -303,22 +304,38 @@ def main():
     ms_step = ms / args.steps
     value = ws * args.steps / (ms / 1e3)
 
-    # e2e: public API with host buffers (H2D target per step, D2H loss per step)
+    # e2e: public API with host buffers -- every step copies its uint8 target
+    # from pinned host memory (prefetched on a copy stream while the previous
+    # step computes) and reads its loss back (asynchronously, into pinned
+    # memory); the timed region ends after the last read has landed
     W, H = RES
     h2d = H * W * 3
-    losses = []
+    copy_stream = torch.cuda.Stream(device)
+    loss_host = torch.empty(max(args.steps, 2), dtype=torch.float64, pin_memory=True)
+
+    def fetch(i):
+        with torch.cuda.stream(copy_stream):
+            t = targets_host[trainer.view_index(i)].to(device, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy_stream)
+        return t, ev
 
     def run_e2e(k):
-        for _ in range(k):
+        nxt = fetch(it["i"])
+        for j in range(k):
             i = it["i"]
-            host = targets_host[trainer.view_index(i)]
-            tgt = host.to(device, non_blocking=True).float().div_(255.0)
+            tgt, ev = nxt
+            torch.cuda.current_stream(device).wait_event(ev)
+            tgt.record_stream(torch.cuda.current_stream(device))
+            if j + 1 < k:
+                nxt = fetch(i + 1)
             loss, _ = trainer.step(i, tgt)
-            losses.append(float(loss.item()))
+            loss_host[j].copy_(loss, non_blocking=True)
             it["i"] += 1
 
     run_e2e(2)
     e2e_ms, _ = timed(lambda: run_e2e(args.steps), args.steps, ws)
+    losses = loss_host[:args.steps].tolist()
     e2e_val = ws * args.steps / (e2e_ms / 1e3)
 
     # per-kernel durations (CUDA events on the launching stream, separate pass)
@@ -376,7 +393,7 @@ def main():
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "algorithmic_bytes": ab, "peak_kind": peak_kind},
-            "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
+            "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": loss_host.element_size()},
             "gpu_launches": launches,
             "clocks": clk,
             "cpu_baseline": cpu,
