@@ -631,8 +631,8 @@ raster_bwd_kernel(BwdParams p)
                     const float2 da = __ffma2_rn(Tb, dc, make_float2(-si.x, -si.y));
                     // u G = dL/dalpha o G; gradient through a clamped alpha is
                     // zero (backward.py:128,169)
-                    const float2 ag = make_float2((ci[i0] && araw[i0] < p.amax) ? araw[i0] : 0.0f,
-                                                  (ci[i1] && araw[i1] < p.amax) ? araw[i1] : 0.0f);
+                    // (alpha_eff < alpha_max <=> contributing and unclamped; then alpha = o G)
+                    const float2 ag = make_float2(a2.x < p.amax ? a2.x : 0.0f, a2.y < p.amax ? a2.y : 0.0f);
                     uG2[h] = __fmul2_rn(da, ag);
                     w2[h] = __fmul2_rn(Tb, a2);
                     Sd2[h] = __ffma2_rn(w2[h], dc, Sd2[h]);
