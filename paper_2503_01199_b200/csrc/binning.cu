@@ -585,6 +585,7 @@ SB_INLINE int lower_bound_u64(const unsigned long long* src, int n, unsigned lon
 struct StSmem {
     SortSmem<kStThreads> sort;
     uint16_t mask[kStCap];                 // ranks, then per sorted entry: hit tiles of the super-tile
+    int32_t tot[kStThreads / 32][kST * kST];
     int32_t toff[kST * kST];
     __device__ uint32_t* slots() { return sort.cnt; }   // kStCap u32 over cnt + cur
 };
@@ -631,9 +632,10 @@ SB_INLINE uint32_t entry_mask(const RasterRec* __restrict__ recs, uint32_t org, 
 // Emit a super-tile's E entries, given in sorted order by slot_of(e), into
 // the tile lists, kStCap entries at a time: (1) every entry's 16-bit mask
 // of hit tiles (entries strided over the threads, so the origin / span loads
-// are independent and coalesced across a warp); (2) one warp per tile
-// compacts the entries carrying that tile's bit, in order, with ballots --
-// the stable order of np.lexsort within the tile, with coalesced stores.
+// are independent and coalesced across a warp); (2) each warp compacts a
+// contiguous range of the entries for all 16 tiles with ballots, after a
+// per-tile prefix over the warps' counts -- the stable order of np.lexsort
+// within each tile, with coalesced stores.
 template <typename SlotOf>
 __device__ void st_emit(StSmem& sm, SlotOf&& slot_of, int E, int st, int st_x, const RasterRec* __restrict__ recs,
                         const uint4* __restrict__ spans, const uint32_t* __restrict__ origin,
@@ -655,17 +657,49 @@ __device__ void st_emit(StSmem& sm, SlotOf&& slot_of, int E, int st, int st_x, c
             sm.mask[e] = (uint16_t)entry_mask(recs, org, s0, s1, sl, sx, sy, tiles_x, tiles_y, W, H);
         }
         __syncthreads();
+        // compaction, balanced over the warps: warp w takes entries
+        // [w R, (w + 1) R) for all 16 tiles; (a) per-tile counts with ballots,
+        // (b) exclusive prefix over the warps, (c) ordered writes
+        constexpr int NW = kStThreads / 32;
         const unsigned lt = (1u << lane) - 1u;
-        for (int j = warp; j < kST * kST; j += kStThreads / 32) {
-            int base = sm.toff[j];
-            for (int e0 = 0; e0 < n; e0 += 32) {
-                const int e = e0 + lane;
-                const bool bit = e < n && ((sm.mask[e] >> j) & 1u);
-                const unsigned bal = __ballot_sync(0xffffffffu, bit);
-                if (bit) prims[base + __popc(bal & lt)] = (int32_t)slot_of(c0 + e);
-                base += __popc(bal);
+        const int R = ((n + NW - 1) / NW + 31) & ~31;
+        const int e_beg = min(n, warp * R), e_end = min(n, e_beg + R);
+        int cnt = 0;   // lane j: this warp's count for tile j
+        for (int e0 = e_beg; e0 < e_end; e0 += 32) {
+            const int e = e0 + lane;
+            const uint32_t m = e < e_end ? sm.mask[e] : 0u;
+#pragma unroll
+            for (int j = 0; j < kST * kST; j++) {
+                const int c = __popc(__ballot_sync(0xffffffffu, (m >> j) & 1u));
+                if (lane == j) cnt += c;
             }
-            if (lane == 0) sm.toff[j] = base;   // the next chunk continues here
+        }
+        if (lane < kST * kST) sm.tot[warp][lane] = cnt;
+        __syncthreads();
+        if (tid < kST * kST) {
+            int run = sm.toff[tid];
+            for (int w = 0; w < NW; w++) {
+                const int t = sm.tot[w][tid];
+                sm.tot[w][tid] = run;
+                run += t;
+            }
+            sm.toff[tid] = run;   // the next chunk continues here
+        }
+        __syncthreads();
+        int base = lane < kST * kST ? sm.tot[warp][lane] : 0;   // lane j: tile j's cursor
+        for (int e0 = e_beg; e0 < e_end; e0 += 32) {
+            const int e = e0 + lane;
+            const uint32_t m = e < e_end ? sm.mask[e] : 0u;
+            const int32_t slot = e < e_end ? (int32_t)slot_of(c0 + e) : 0;
+#pragma unroll
+            for (int j = 0; j < kST * kST; j++) {
+                const unsigned bal = __ballot_sync(0xffffffffu, (m >> j) & 1u);
+                if (bal) {
+                    const int b = __shfl_sync(0xffffffffu, base, j);
+                    if ((m >> j) & 1u) prims[b + __popc(bal & lt)] = slot;
+                    if (lane == j) base += __popc(bal);
+                }
+            }
         }
         __syncthreads();
     }
