@@ -51,6 +51,7 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
         const sb_screen_grad s = sg[slot];
         // activation chains (backward.py:403-404): sigmoid' in float32, product in float64
         const float gcol[3] = {s.r, s.g, s.bl};
+#pragma unroll
         for (int ch = 0; ch < 3; ch++) {
             const float y = o.col[ch];
             const float sp = FMUL(y, FSUB(1.0f, y));
@@ -73,21 +74,35 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
             const double gsa = -q00, gsb = -2.0 * q01, gsc = -q11;
             const double Gs[2][2] = {{gsa, 0.5 * gsb}, {0.5 * gsb, gsc}};
             double M[2][3], cw[3][3];
+#pragma unroll
             for (int i = 0; i < 2; i++)
+#pragma unroll
                 for (int j = 0; j < 3; j++) M[i][j] = o.M[i][j];
+#pragma unroll
             for (int i = 0; i < 3; i++)
+#pragma unroll
                 for (int j = 0; j < 3; j++) cw[i][j] = o.cov[i][j];
             double B[3][2], dcw[3][3], GM[2][3], dM[2][3], dJ[2][3];
+#pragma unroll
             for (int i = 0; i < 3; i++)
+#pragma unroll
                 for (int j = 0; j < 2; j++) B[i][j] = fma(M[1][i], Gs[1][j], M[0][i] * Gs[0][j]);
+#pragma unroll
             for (int i = 0; i < 3; i++)
+#pragma unroll
                 for (int j = 0; j < 3; j++) dcw[i][j] = fma(B[i][1], M[1][j], B[i][0] * M[0][j]);
+#pragma unroll
             for (int i = 0; i < 2; i++)
+#pragma unroll
                 for (int j = 0; j < 3; j++) GM[i][j] = fma(Gs[i][1], M[1][j], Gs[i][0] * M[0][j]);
+#pragma unroll
             for (int i = 0; i < 2; i++)
+#pragma unroll
                 for (int j = 0; j < 3; j++)
                     dM[i][j] = 2.0 * fma(GM[i][2], cw[2][j], fma(GM[i][1], cw[1][j], GM[i][0] * cw[0][j]));
+#pragma unroll
             for (int i = 0; i < 2; i++)
+#pragma unroll
                 for (int j = 0; j < 3; j++)
                     dJ[i][j] = fma(dM[i][2], cam.Rd[3 * j + 2], fma(dM[i][1], cam.Rd[3 * j + 1], dM[i][0] * cam.Rd[3 * j]));
             const double tx = o.t[0], ty = o.t[1], tz = o.t[2];
@@ -101,22 +116,30 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
             dt[0] += gu * fx / tz;
             dt[1] += gv * fy / tz;
             dt[2] += gu * (-fx * tx / tz2) + gv * (-fy * ty / tz2);
+#pragma unroll
             for (int j = 0; j < 3; j++)
                 out[SB_COL_POS + j] =
                     (float)fma(dt[2], cam.Rd[6 + j], fma(dt[1], cam.Rd[3 + j], dt[0] * cam.Rd[j]));
             double sc3[3], q[4], Rq[3][3];
+#pragma unroll
             for (int j = 0; j < 3; j++) sc3[j] = o.s[j];
+#pragma unroll
             for (int j = 0; j < 4; j++) q[j] = o.q[j];
             sb_quat_to_rotmat(q[0], q[1], q[2], q[3], Rq);
             double T1[3][3], dRq[3][3];
+#pragma unroll
             for (int i = 0; i < 3; i++)
+#pragma unroll
                 for (int j = 0; j < 3; j++)
                     T1[i][j] = fma(Rq[2][i], dcw[2][j], fma(Rq[1][i], dcw[1][j], Rq[0][i] * dcw[0][j]));
+#pragma unroll
             for (int j = 0; j < 3; j++) {
                 const double dDjj = fma(T1[j][2], Rq[2][j], fma(T1[j][1], Rq[1][j], T1[j][0] * Rq[0][j]));
                 out[SB_COL_LS + j] = (float)(dDjj * 2.0 * (sc3[j] * sc3[j]));
             }
+#pragma unroll
             for (int i = 0; i < 3; i++)
+#pragma unroll
                 for (int j = 0; j < 3; j++)
                     dRq[i][j] = 2.0 * fma(dcw[i][2], Rq[2][j], fma(dcw[i][1], Rq[1][j], dcw[i][0] * Rq[0][j])) *
                                 (sc3[j] * sc3[j]);
@@ -125,6 +148,7 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
             const double r0 = p[SB_COL_ROT], r1 = p[SB_COL_ROT + 1], r2 = p[SB_COL_ROT + 2], r3 = p[SB_COL_ROT + 3];
             const double nrm = sqrt(((r0 * r0 + r1 * r1) + r2 * r2) + r3 * r3);
             const double proj = ((dq[0] * q[0] + dq[1] * q[1]) + dq[2] * q[2]) + dq[3] * q[3];
+#pragma unroll
             for (int j = 0; j < 4; j++) out[SB_COL_ROT + j] = (float)((dq[j] - proj * q[j]) / nrm);
         }
         if (stat_S) {

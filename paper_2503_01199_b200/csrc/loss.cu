@@ -10,9 +10,9 @@
 // separably on the tile + 5 halo, the three gradient fields (g_mu, 2 dA2,
 // dB2) are formed there, filtered back (adjoint) onto the tile and combined
 // with the L1 sign term.  The field buffer reuses the staged input's shared
-// memory (x and y are re-read from L2 for the final combination), so two
-// CTAs fit per SM.  Every separable pass is a register sliding window: a
-// thread owns a short run of outputs along the filter axis, loads the run +
+// memory, so two CTAs fit per SM; maps sharing a filter sit interleaved in
+// float2 planes so each tap is one f32x2 FMA per pair.  Every separable
+// pass is a register sliding window: a thread owns a short run of outputs along the filter axis, loads the run +
 // 10 inputs once from shared memory and forms all outputs from registers.
 // Loss partial sums go to two float64 accumulators.
 #include "common.cuh"
@@ -22,18 +22,23 @@ namespace {
 constexpr int TW = 64, TH = 32, R = 5, NT = 2 * R + 1;
 constexpr int IW = TW + 4 * R, IH = TH + 4 * R;   // input region (halo 10): 84 x 52
 constexpr int FW = TW + 2 * R, FH = TH + 2 * R;   // field region (halo 5):  74 x 42
+constexpr int VW = IW + 4;                        // vertical-moment row pitch (padded: the last
+                                                  // horizontal run reads past IW into outputs it drops)
 constexpr int kThreads = 512;
 
 struct Win { float w[NT]; };
 
+// Maps that share a filter are interleaved in float2 planes so one f32x2
+// FMA (FFMA2) advances two of them per tap: (x, y), (xx, yy), xy for the
+// moments; (g_mu, g_xy), g_xx for the gradient fields.
 struct Smem {
     union {
-        float sxy[2][IH][IW];     // staged x, y (this channel)
-        float fl[3][FH][FW];      // g_mu, g_xy (= 2 dA2), g_xx (= dB2)
+        float2 sxy[IH][IW];                       // staged (x, y) of this channel
+        struct { float2 f01[FH][FW]; float f2[FH][FW]; } fl;   // (g_mu, g_xy = 2 dA2), g_xx = dB2
     } a;
     union {
-        float vm[5][FH][IW];      // vertical moments
-        float av[3][TH][FW];      // adjoint vertical pass
+        struct { float2 m01[FH][VW]; float2 m23[FH][VW]; float m4[FH][VW]; } vm;   // vertical moments
+        struct { float2 a01[TH][FW]; float a2[TH][FW]; } av;                       // adjoint vertical pass
     } b;
     double red[2][kThreads / 32];
 };
@@ -41,6 +46,8 @@ struct Smem {
 SB_INLINE float load_y(const float* __restrict__ y_img, const uint8_t* __restrict__ y_u8, size_t idx) {
     return y_u8 ? (float)y_u8[idx] * (1.0f / 255.0f) : y_img[idx];
 }
+
+SB_INLINE float2 f2(float v) { return make_float2(v, v); }
 
 __global__ void __launch_bounds__(kThreads, 2)
 loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, const uint8_t* __restrict__ y_u8,
@@ -70,30 +77,26 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
             fy[o] = load_y(y_img, y_u8, idx);
         }
     }
-    // (1) stage this channel of x, y with a 10-pixel halo, zero outside the
+    // (1) stage this channel of (x, y) with a 10-pixel halo, zero outside the
     //     image (all of a thread's loads issued before its stores)
     {
         constexpr int NS = (IH * IW + kThreads - 1) / kThreads;
-        float xv[NS], yv[NS];
+        float2 v[NS];
 #pragma unroll
         for (int j = 0; j < NS; j++) {
             const int i = tid + j * kThreads;
             const int r = i / IW, c = i - r * IW;
             const int gy = oy - 2 * R + r, gx = ox - 2 * R + c;
-            xv[j] = yv[j] = 0.f;
+            v[j] = make_float2(0.f, 0.f);
             if (i < IH * IW && gy >= 0 && gy < H && gx >= 0 && gx < W) {
                 const size_t idx = ((size_t)gy * W + gx) * 3 + ch;
-                xv[j] = x_img[idx];
-                yv[j] = load_y(y_img, y_u8, idx);
+                v[j] = make_float2(x_img[idx], load_y(y_img, y_u8, idx));
             }
         }
 #pragma unroll
         for (int j = 0; j < NS; j++) {
             const int i = tid + j * kThreads;
-            if (i < IH * IW) {
-                (&sm.a.sxy[0][0][0])[i] = xv[j];
-                (&sm.a.sxy[1][0][0])[i] = yv[j];
-            }
+            if (i < IH * IW) (&sm.a.sxy[0][0])[i] = v[j];
         }
     }
     __syncthreads();
@@ -104,28 +107,27 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
         constexpr int RUN = 7, NRUN = FH / RUN;          // 6 runs x 84 columns = 504 threads
         if (tid < NRUN * IW) {
             const int c = tid % IW, r0 = (tid / IW) * RUN;
-            float xs[RUN + NT - 1], ys[RUN + NT - 1], xx[RUN + NT - 1], yy[RUN + NT - 1], xy[RUN + NT - 1];
+            float2 p[RUN + NT - 1], q[RUN + NT - 1];
+            float xy[RUN + NT - 1];
 #pragma unroll
             for (int k = 0; k < RUN + NT - 1; k++) {
-                xs[k] = sm.a.sxy[0][r0 + k][c];
-                ys[k] = sm.a.sxy[1][r0 + k][c];
-                xx[k] = xs[k] * xs[k];
-                yy[k] = ys[k] * ys[k];
-                xy[k] = xs[k] * ys[k];
+                p[k] = sm.a.sxy[r0 + k][c];
+                q[k] = __fmul2_rn(p[k], p[k]);
+                xy[k] = p[k].x * p[k].y;
             }
 #pragma unroll
             for (int o = 0; o < RUN; o++) {
-                float a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+                float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+                float a4 = 0.f;
 #pragma unroll
                 for (int k = 0; k < NT; k++) {
-                    a0 += w[k] * xs[o + k];
-                    a1 += w[k] * ys[o + k];
-                    a2 += w[k] * xx[o + k];
-                    a3 += w[k] * yy[o + k];
-                    a4 += w[k] * xy[o + k];
+                    a01 = __ffma2_rn(f2(w[k]), p[o + k], a01);
+                    a23 = __ffma2_rn(f2(w[k]), q[o + k], a23);
+                    a4 = fmaf(w[k], xy[o + k], a4);
                 }
-                sm.b.vm[0][r0 + o][c] = a0; sm.b.vm[1][r0 + o][c] = a1; sm.b.vm[2][r0 + o][c] = a2;
-                sm.b.vm[3][r0 + o][c] = a3; sm.b.vm[4][r0 + o][c] = a4;
+                sm.b.vm.m01[r0 + o][c] = a01;
+                sm.b.vm.m23[r0 + o][c] = a23;
+                sm.b.vm.m4[r0 + o][c] = a4;
             }
         }
     }
@@ -135,32 +137,55 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
     //     fields (written over the staged input)
     {
         constexpr int RUN = 7, NRUN = (FW + RUN - 1) / RUN;   // 11 runs x 42 rows = 462 threads
+        static_assert(NRUN * RUN + NT - 1 <= VW, "padded pitch covers the last run");
         if (tid < NRUN * FH) {
             const int r = tid / NRUN, c0 = (tid % NRUN) * RUN;
-            float m[5][RUN];
+            float2 m01[RUN], m23[RUN];
+            float m4[RUN];
+            {
+                float2 in[RUN + NT - 1];
 #pragma unroll
-            for (int q = 0; q < 5; q++) {
-                float in[RUN + NT - 1];
-#pragma unroll
-                for (int k = 0; k < RUN + NT - 1; k++) in[k] = (c0 + k < IW) ? sm.b.vm[q][r][c0 + k] : 0.f;
+                for (int k = 0; k < RUN + NT - 1; k++) in[k] = sm.b.vm.m01[r][c0 + k];
 #pragma unroll
                 for (int o = 0; o < RUN; o++) {
-                    float a = 0;
+                    float2 a = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int k = 0; k < NT; k++) a += w[k] * in[o + k];
-                    m[q][o] = a;
+                    for (int k = 0; k < NT; k++) a = __ffma2_rn(f2(w[k]), in[o + k], a);
+                    m01[o] = a;
+                }
+#pragma unroll
+                for (int k = 0; k < RUN + NT - 1; k++) in[k] = sm.b.vm.m23[r][c0 + k];
+#pragma unroll
+                for (int o = 0; o < RUN; o++) {
+                    float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int k = 0; k < NT; k++) a = __ffma2_rn(f2(w[k]), in[o + k], a);
+                    m23[o] = a;
+                }
+            }
+            {
+                float in[RUN + NT - 1];
+#pragma unroll
+                for (int k = 0; k < RUN + NT - 1; k++) in[k] = sm.b.vm.m4[r][c0 + k];
+#pragma unroll
+                for (int o = 0; o < RUN; o++) {
+                    float a = 0.f;
+#pragma unroll
+                    for (int k = 0; k < NT; k++) a = fmaf(w[k], in[o + k], a);
+                    m4[o] = a;
                 }
             }
             const int gy = oy - R + r;
+            const bool row_in = gy >= R && gy < H - R, row_own = r >= R && r < R + TH;
 #pragma unroll
             for (int o = 0; o < RUN; o++) {
                 const int c = c0 + o;
                 if (c >= FW) continue;
                 const int gx = ox - R + c;
                 float g_mu = 0.f, g_xy = 0.f, g_xx = 0.f;
-                if (gy >= R && gy < H - R && gx >= R && gx < W - R) {
-                    const float mx = m[0][o], my = m[1][o];
-                    const float vx = m[2][o] - mx * mx, vy = m[3][o] - my * my, cv = m[4][o] - mx * my;
+                if (row_in && gx >= R && gx < W - R) {
+                    const float mx = m01[o].x, my = m01[o].y;
+                    const float vx = m23[o].x - mx * mx, vy = m23[o].y - my * my, cv = m4[o] - mx * my;
                     const float A1 = 2.f * mx * my + C1, A2 = 2.f * cv + C2;
                     const float B1 = mx * mx + my * my + C1, B2 = vx + vy + C2;
                     const float iB1 = __frcp_rn(B1), iB2 = __frcp_rn(B2), iBB = iB1 * iB2;
@@ -169,9 +194,10 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
                     g_mu = 2.f * my * dA1 - 2.f * my * dA2 + 2.f * mx * dB1 - 2.f * mx * dB2;
                     g_xy = 2.f * dA2;
                     g_xx = dB2;
-                    if (r >= R && r < R + TH && c >= R && c < R + TW) s_sum += (double)S;
+                    if (row_own && c >= R && c < R + TW) s_sum += (double)S;
                 }
-                sm.a.fl[0][r][c] = g_mu; sm.a.fl[1][r][c] = g_xy; sm.a.fl[2][r][c] = g_xx;
+                sm.a.fl.f01[r][c] = make_float2(g_mu, g_xy);
+                sm.a.fl.f2[r][c] = g_xx;
             }
         }
     }
@@ -182,24 +208,35 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
         constexpr int RUN = 8, NRUN = TH / RUN;           // 4 runs x 74 columns = 296 threads
         if (tid < NRUN * FW) {
             const int c = tid % FW, r0 = (tid / FW) * RUN;
+            {
+                float2 in[RUN + NT - 1];
 #pragma unroll
-            for (int q = 0; q < 3; q++) {
-                float in[RUN + NT - 1];
-#pragma unroll
-                for (int k = 0; k < RUN + NT - 1; k++) in[k] = sm.a.fl[q][r0 + k][c];
+                for (int k = 0; k < RUN + NT - 1; k++) in[k] = sm.a.fl.f01[r0 + k][c];
 #pragma unroll
                 for (int o = 0; o < RUN; o++) {
-                    float a = 0;
+                    float2 a = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int k = 0; k < NT; k++) a += w[k] * in[o + k];
-                    sm.b.av[q][r0 + o][c] = a;
+                    for (int k = 0; k < NT; k++) a = __ffma2_rn(f2(w[k]), in[o + k], a);
+                    sm.b.av.a01[r0 + o][c] = a;
+                }
+            }
+            {
+                float in[RUN + NT - 1];
+#pragma unroll
+                for (int k = 0; k < RUN + NT - 1; k++) in[k] = sm.a.fl.f2[r0 + k][c];
+#pragma unroll
+                for (int o = 0; o < RUN; o++) {
+                    float a = 0.f;
+#pragma unroll
+                    for (int k = 0; k < NT; k++) a = fmaf(w[k], in[o + k], a);
+                    sm.b.av.a2[r0 + o][c] = a;
                 }
             }
         }
     }
     __syncthreads();
 
-    // (5) adjoint horizontal pass + combination with the L1 term (x, y from L2)
+    // (5) adjoint horizontal pass + combination with the L1 term
     {
         const int ni_w = W - 2 * R, ni_h = H - 2 * R;
         const float n_int = (float)ni_w * (float)ni_h;
@@ -208,18 +245,30 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
         constexpr int RUN = ORUN;
         const int r = orow, c0 = oc0;
         const int gy = oy + r;
-        float t[3][RUN];
+        float2 t01[RUN];
+        float t2[RUN];
+        {
+            float2 in[RUN + NT - 1];
 #pragma unroll
-        for (int q = 0; q < 3; q++) {
-            float in[RUN + NT - 1];
-#pragma unroll
-            for (int k = 0; k < RUN + NT - 1; k++) in[k] = sm.b.av[q][r][c0 + k];
+            for (int k = 0; k < RUN + NT - 1; k++) in[k] = sm.b.av.a01[r][c0 + k];
 #pragma unroll
             for (int o = 0; o < RUN; o++) {
-                float a = 0;
+                float2 a = make_float2(0.f, 0.f);
 #pragma unroll
-                for (int k = 0; k < NT; k++) a += w[k] * in[o + k];
-                t[q][o] = a;
+                for (int k = 0; k < NT; k++) a = __ffma2_rn(f2(w[k]), in[o + k], a);
+                t01[o] = a;
+            }
+        }
+        {
+            float in[RUN + NT - 1];
+#pragma unroll
+            for (int k = 0; k < RUN + NT - 1; k++) in[k] = sm.b.av.a2[r][c0 + k];
+#pragma unroll
+            for (int o = 0; o < RUN; o++) {
+                float a = 0.f;
+#pragma unroll
+                for (int k = 0; k < NT; k++) a = fmaf(w[k], in[o + k], a);
+                t2[o] = a;
             }
         }
 #pragma unroll
@@ -228,7 +277,7 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
             if (gy >= H || gx >= W) continue;
             const size_t idx = ((size_t)gy * W + gx) * 3 + ch;
             const float xv = fx[o], yv = fy[o];
-            const float g_ssim = t[0][o] + t[1][o] * yv + t[2][o] * (2.f * xv);
+            const float g_ssim = t01[o].x + t01[o].y * yv + t2[o] * (2.f * xv);
             const float diff = xv - yv;
             const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
             grad[idx] = sgn * l1_scale - ssim_scale * g_ssim;

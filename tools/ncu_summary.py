@@ -36,11 +36,12 @@ for rep in sys.argv[1:]:
     if len(raw) >= 3:
         rv = dict(zip(raw[0], raw[2]))
         try:
-            rd = float(rv["dram__bytes_read.sum"].replace(",", ""))
-            wr = float(rv["dram__bytes_write.sum"].replace(",", ""))
-            unit = raw[1][raw[0].index("dram__bytes_read.sum")]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-            print(f"   {'DRAM bytes (read + write)':32s} {(rd + wr) * scale / 1e6:.1f} MB")
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tot = 0.0
+            for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                unit = raw[1][raw[0].index(m)]
+                tot += float(rv[m].replace(",", "")) * scale.get(unit, 1)
+            print(f"   {'DRAM bytes (read + write)':32s} {tot / 1e6:.1f} MB")
         except (KeyError, ValueError):
             pass
     src = list(csv.reader(run([rep, "--page", "source", "--csv", "--print-source", "sass"]).splitlines()))
