@@ -30,25 +30,40 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
 {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
-    const int off = cluster_offset[g / SB_CLUSTER_SIZE];
+    // every load that depends only on g is issued together with the cluster
+    // lookup (one memory round trip), the screen record after it (a second)
+    const int off = __ldg(cluster_offset + g / SB_CLUSTER_SIZE);
+    float p[16];
+    const float4* row = params + (size_t)g * 4;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const float4 v = __ldg(row + k);
+        p[4 * k] = v.x; p[4 * k + 1] = v.y; p[4 * k + 2] = v.z; p[4 * k + 3] = v.w;
+    }
+    double S0 = 0.0, M0 = 0.0;
+    int32_t C0 = 0;
+    if (stat_S) { S0 = stat_S[g]; M0 = stat_M[g]; C0 = stat_C[g]; }
     float out[16];
 #pragma unroll
     for (int k = 0; k < 16; k++) out[k] = 0.0f;
     if (off >= 0) {
         const int slot = off + g % SB_CLUSTER_SIZE;
-        float p[16];
-        const float4* row = params + (size_t)g * 4;
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const float4 v = __ldg(row + k);
-            p[4 * k] = v.x; p[4 * k + 1] = v.y; p[4 * k + 2] = v.z; p[4 * k + 3] = v.w;
+        const uint32_t rflags = __float_as_uint(__ldg(reinterpret_cast<const float*>(recs + slot) + 11));
+        sb_screen_grad s;   // 64-byte record: a b c u | v o r g | bl C S | M pad
+        {
+            const float4* src = reinterpret_cast<const float4*>(sg + slot);
+            const float4 q0 = __ldg(src), q1 = __ldg(src + 1), q2 = __ldg(src + 2), q3 = __ldg(src + 3);
+            s.a = q0.x; s.b = q0.y; s.c = q0.z; s.u = q0.w;
+            s.v = q1.x; s.o = q1.y; s.r = q1.z; s.g = q1.w;
+            s.bl = q2.x; s.C = __float_as_int(q2.y);
+            s.S = __hiloint2double(__float_as_int(q2.w), __float_as_int(q2.z));
+            s.M = __hiloint2double(__float_as_int(q3.y), __float_as_int(q3.x));
         }
         // intermediates of the projection; activations to float32 accuracy,
         // validity exactly as the forward decided it (record flags)
         ProjOut o;
         sb_project<false>(p, cam, o);
-        o.valid = (__float_as_uint(__ldg(reinterpret_cast<const float*>(recs + slot) + 11)) & 1u) != 0;
-        const sb_screen_grad s = sg[slot];
+        o.valid = (rflags & 1u) != 0;
         // activation chains (backward.py:403-404): sigmoid' in float32, product in float64
         const float gcol[3] = {s.r, s.g, s.bl};
 #pragma unroll
@@ -152,9 +167,9 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
             for (int j = 0; j < 4; j++) out[SB_COL_ROT + j] = (float)((dq[j] - proj * q[j]) / nrm);
         }
         if (stat_S) {
-            stat_S[g] += s.S;
-            stat_M[g] += s.M;
-            stat_C[g] += s.C;
+            stat_S[g] = S0 + s.S;
+            stat_M[g] = M0 + s.M;
+            stat_C[g] = C0 + s.C;
         }
     }
     float4* dst = grads + (size_t)g * 4;
