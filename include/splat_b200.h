@@ -72,16 +72,21 @@ int sb_permute_rows(const uint32_t* perm, int64_t n, int count, const void* cons
 
 /* ---- forward: project + cull + compact + bin (forward.py:258-290) -------- */
 /* projection.py:130-190 + ccc.py:112-194 + tiles.py:70-91 (hit counting).
- * Outputs: recs[N] (first N_c used; flags = valid | in_image << 1 |
- * tile_hits << 2), compact_map[N] (int32, first N_c used), cluster_offset[K]
- * (compact start of each visible cluster, -1 if culled), cluster_vis[K],
- * counters[4] (must be ZEROED): visible clusters, N_c, n_degenerate.
+ * Outputs: recs[N] (first N_c used; flags = valid | in_image << 1),
+ * compact_map[N] (int32, first N_c used), cluster_offset[K] (compact start
+ * of each visible cluster, -1 if culled), cluster_vis[K], counters[0..3]
+ * (written): visible clusters, N_c, n_degenerate, 0.  ws holds the
+ * look-back state: zero it once before first use; every call leaves it
+ * zeroed.  sgrad_zero (nullable,
+ * N rows): its rows [0, N_c) -- the slots sb_raster_bwd accumulates into --
+ * are zeroed alongside the records, so that call can take n_cap = 0.
  * Replaces project_scene + build_clusters + cull_clusters +
  * cluster_visibility + compact_arrays (projection.py:130, ccc.py:112/134/149/171). */
 size_t sb_project_workspace_bytes(int64_t n);
 int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
                             void* recs, int32_t* compact_map, int32_t* cluster_offset, uint8_t* cluster_vis,
-                            int32_t* counters, void* ws, size_t ws_bytes, sb_stream_t stream);
+                            int32_t* counters, sb_screen_grad* sgrad_zero, void* ws, size_t ws_bytes,
+                            sb_stream_t stream);
 
 /* tiles.py:50-107 binning, part 1: enumerate the exact disc/rect hits
  * (tiles.py:75-91), count them per tile and scan the counts ->
@@ -89,10 +94,17 @@ int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam
  * the number E of (primitive, 4x4-tile super-tile) entries.  The per-row hit
  * spans and the super-tile offsets are kept in `state`
  * (sb_bin_state_workspace_bytes(n_cap, ntiles) bytes, caller-owned) for
- * part 2.  n_cap bounds N_c (read from counters[1] on the device). */
+ * part 2.  n_cap bounds N_c (read from counters[1] on the device).  The
+ * state's per-tile count arrays are re-zeroed by the call itself: zero the
+ * state once before its first use, and again if it is reused for a
+ * different tile grid (resolution).  counters_mirror (nullable; device
+ * address of mapped pinned host memory, see sb_host_mapped_pointer)
+ * receives (visible clusters, N_c, n_degenerate, 0, P, E) from the device,
+ * readable on the host once the stream has passed this call. */
 size_t sb_bin_state_workspace_bytes(int64_t n_cap, int32_t ntiles);
 int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam,
-                   int32_t* tile_offsets, int32_t* totals, void* state, size_t state_bytes, sb_stream_t stream);
+                   int32_t* tile_offsets, int32_t* totals, int32_t* counters_mirror, void* state,
+                   size_t state_bytes, sb_stream_t stream);
 
 /* tiles.py:50-107 binning, part 2 (`state` as part 1 left it):
  * depth-sort each super-tile's entries once and emit the per-tile lists:
@@ -110,7 +122,10 @@ int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, cons
 /* forward.py:161-191 + 240-255: color (H,W,3), transmittance (H,W),
  * frag_count (H,W) and last[(H,W)] = 1 + list position of each pixel's last
  * contributing fragment (consumed by the backward).  cfg->half_state = 1
- * selects the fp16 blending-state path (forward.py:194-230, half=True). */
+ * selects the fp16 blending-state path (forward.py:194-230, half=True).
+ * ws (sb_raster_workspace_bytes, shared with sb_raster_bwd) holds the
+ * dynamic tile queue: zero it once before its first use; every call leaves
+ * it zeroed again. */
 size_t sb_raster_workspace_bytes(void);
 int sb_raster_fwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
                   const sb_raster_cfg* cfg, float* color, float* transmittance, int32_t* frag_count, int32_t* last,
@@ -118,7 +133,8 @@ int sb_raster_fwd(const void* recs, const int32_t* tile_offsets, const int32_t* 
 
 /* ---- backward (backward.py:205-279) --------------------------------------- */
 /* backward.py:112-267: screen-space gradients + S/M/C per compact primitive.
- * sgrad[n_cap] is zeroed by the call. */
+ * Rows [0, n_cap) of sgrad are zeroed first; n_cap = 0 accumulates into
+ * sgrad as given (rows zeroed by sb_project_cull_compact's sgrad_zero). */
 int sb_raster_bwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
                   const sb_raster_cfg* cfg, const float* dL_dI, const float* transmittance, const int32_t* last,
                   sb_screen_grad* sgrad, int64_t n_cap, void* ws, size_t ws_bytes, sb_stream_t stream);
@@ -144,7 +160,8 @@ int sb_variance_score(const double* S, const double* M, const int32_t* C, int64_
 /* metrics.py:118-132 loss_and_grad, fused: (1 - lam) L1 + lam (1 - SSIM)
  * over (H, W, 3) float32 images and dL/d rendered.  target is float32, or
  * uint8 (value / 255) when target_u8 != NULL.  loss[0] (float64, device) is
- * written on the stream; accum: 2 float64 scratch. */
+ * written on the stream; accum: 2 float64 scratch, zeroed once before its
+ * first use and left zeroed by every call. */
 int sb_loss_fwd_bwd(const float* rendered, const float* target, const uint8_t* target_u8, int32_t width,
                     int32_t height, float lam, float* grad, double* accum, double* loss, sb_stream_t stream);
 
@@ -153,6 +170,10 @@ int sb_loss_fwd_bwd(const float* rendered, const float* target, const uint8_t* t
  * (result cast to float32), 2 = lane_group_reduce in float64 (out_d),
  * 3 / 4 = the raster backward's register row reductions (tree /
  * exponent-aligned) on the same 32 values. */
+/* Device address of pinned host memory (cudaHostGetDevicePointer); error
+ * if the buffer is not mapped. */
+int sb_host_mapped_pointer(void* host, void** device);
+
 int sb_lane_reduce(const float* values, int64_t groups, int mode, float* out_f, double* out_d, sb_stream_t stream);
 
 #ifdef __cplusplus

@@ -31,9 +31,10 @@ SIGNATURES = {
     "sb_radix_sort_pairs_u64": ([VP, VP, VP, VP, I64, C.c_int, VP, VP, SZ, VP], C.c_int),
     "sb_permute_rows": ([VP, I64, C.c_int, VP, VP, VP, VP], C.c_int),
     "sb_project_workspace_bytes": ([I64], SZ),
-    "sb_project_cull_compact": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_project_cull_compact": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_bin_state_workspace_bytes": ([I64, I32], SZ),
-    "sb_bin_prepare": ([VP, VP, I64, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_bin_prepare": ([VP, VP, I64, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_host_mapped_pointer": ([VP, C.POINTER(C.c_void_p)], C.c_int),
     "sb_bin_finish_workspace_bytes": ([I64, I32], SZ),
     "sb_bin_finish": ([VP, VP, I64, VP, I64, I64, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_raster_workspace_bytes": ([], SZ),
@@ -161,7 +162,9 @@ def workspace(purpose: str, nbytes: int, device) -> torch.Tensor:
     key = (purpose, str(device))
     buf = _arena.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(int(nbytes * 1.25), 256), dtype=torch.uint8, device=device)
+        # zero-filled once: the raster tile queues expect a zeroed workspace
+        # on first use and leave it zeroed (include/splat_b200.h)
+        buf = torch.zeros(max(int(nbytes * 1.25), 256), dtype=torch.uint8, device=device)
         _arena[key] = buf
     return buf
 

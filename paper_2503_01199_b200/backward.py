@@ -19,11 +19,10 @@ import torch
 
 from . import _lib
 from .errors import ShapeMismatchError, StaleSceneError
-from .forward import RenderContext
+from .forward import SGRAD_BYTES, RenderContext, _sgrad_clean
 from .scene import CHANNEL_COLS, RAW_CHANNELS, SceneSoA
 
 GRAD_CHANNELS = RAW_CHANNELS
-SGRAD_BYTES = 64
 
 
 class SceneGrads:
@@ -129,10 +128,14 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
                   C.byref(cam_s), C.byref(cfg_s), _lib.ptr(scratch), _lib.ptr(T_final), _lib.ptr(frags),
                   _lib.ptr(last), _lib.ptr(ws_f), ws_f.numel(), stream)
     sgrad = _lib.workspace("sgrad", nc * SGRAD_BYTES, dev)
+    # rows already zeroed by this context's forward (project kernel), unless
+    # another forward or backward has used the workspace since
+    prezeroed = ctx.token != 0 and _sgrad_clean.get(str(dev)) == ctx.token
+    _sgrad_clean.pop(str(dev), None)
     ws_r = _lib.workspace("raster_bwd", _lib.load().sb_raster_workspace_bytes(), dev)
     _lib.call("sb_raster_bwd", _lib.ptr(ctx.recs), _lib.ptr(ctx.tile_offsets), _lib.ptr(ctx.tile_prims),
               C.byref(cam_s), C.byref(cfg_s), _lib.ptr(dI), _lib.ptr(T_final), _lib.ptr(last),
-              _lib.ptr(sgrad), ctx.n_compact, _lib.ptr(ws_r), ws_r.numel(), stream)
+              _lib.ptr(sgrad), 0 if prezeroed else ctx.n_compact, _lib.ptr(ws_r), ws_r.numel(), stream)
     grads = torch.empty((n, 16), dtype=torch.float32, device=dev)
     _lib.call("sb_chain_projection_bwd", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s),
               _lib.ptr(ctx.cluster_offset), _lib.ptr(ctx.recs), _lib.ptr(sgrad), _lib.ptr(grads), _lib.ptr(stats.S),

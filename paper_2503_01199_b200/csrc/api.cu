@@ -7,11 +7,11 @@
 
 // launchers (one per kernel family)
 void sb_launch_project_cull_compact(const float*, int, const CamDev&, int, RasterRec*, int32_t*, int32_t*, uint8_t*,
-                                    int32_t*, unsigned long long*, unsigned int*, cudaStream_t);
+                                    int32_t*, void*, unsigned long long*, unsigned int*, cudaStream_t);
 int sb_project_blocks(int n);
 size_t sb_bin_state_bytes(int n_cap, int ntiles);
-void sb_launch_bin_prepare(const RasterRec*, const int32_t*, int, const CamDev&, int32_t*, int32_t*, void*,
-                           cudaStream_t);
+void sb_launch_bin_prepare(const RasterRec*, const int32_t*, int, const CamDev&, int32_t*, int32_t*, int32_t*,
+                           void*, cudaStream_t);
 size_t sb_bin_finish_ws(long long n_entries, int ntiles);
 void sb_launch_bin_finish(const RasterRec*, const int32_t*, int, const CamDev&, int, int, const int32_t*,
                           const void*, int32_t*, void*, cudaStream_t);
@@ -134,7 +134,8 @@ size_t sb_project_workspace_bytes(int64_t n) {
 
 int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
                             void* recs, int32_t* compact_map, int32_t* cluster_offset, uint8_t* cluster_vis,
-                            int32_t* counters, void* ws, size_t ws_bytes, sb_stream_t stream) {
+                            int32_t* counters, sb_screen_grad* sgrad_zero, void* ws, size_t ws_bytes,
+                            sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
     if (n < 0 || n > INT32_MAX - 256) return fail(SB_EINVAL, "n out of range");
@@ -143,10 +144,9 @@ int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam
     const int blocks = sb_project_blocks((int)n);
     unsigned long long* status = static_cast<unsigned long long*>(ws);
     unsigned int* ticket = reinterpret_cast<unsigned int*>(status + blocks);
-    cudaMemsetAsync(ws, 0, sizeof(unsigned long long) * blocks + 16, S(stream));
     const CamDev d = make_cam(cam, cfg);
     sb_launch_project_cull_compact(params, (int)n, d, cfg->use_culling, static_cast<RasterRec*>(recs), compact_map,
-                                   cluster_offset, cluster_vis, counters, status, ticket, S(stream));
+                                   cluster_offset, cluster_vis, counters, sgrad_zero, status, ticket, S(stream));
     return check_launch("sb_project_cull_compact");
 }
 
@@ -155,15 +155,16 @@ size_t sb_bin_state_workspace_bytes(int64_t n_cap, int32_t ntiles) {
 }
 
 int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, const sb_camera* cam,
-                   int32_t* tile_offsets, int32_t* n_pairs, void* state, size_t state_bytes, sb_stream_t stream) {
+                   int32_t* tile_offsets, int32_t* n_pairs, int32_t* counters_mirror, void* state,
+                   size_t state_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (n_cap < 0 || n_cap > INT32_MAX / 2) return fail(SB_EINVAL, "n_cap out of range");
     if (!tile_offsets || !n_pairs) return fail(SB_EINVAL, "NULL buffer");
     const CamDev d = make_cam(cam, nullptr);
     if (state_bytes < sb_bin_state_workspace_bytes(n_cap, d.tiles_x * d.tiles_y))
         return fail(SB_EWORKSPACE, "bin state too small");
-    sb_launch_bin_prepare(static_cast<const RasterRec*>(recs), counters, (int)n_cap, d, tile_offsets, n_pairs, state,
-                          S(stream));
+    sb_launch_bin_prepare(static_cast<const RasterRec*>(recs), counters, (int)n_cap, d, tile_offsets, n_pairs,
+                          counters_mirror, state, S(stream));
     return check_launch("sb_bin_prepare");
 }
 
@@ -196,7 +197,6 @@ int sb_raster_fwd(const void* recs, const int32_t* tile_offsets, const int32_t* 
     if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
     if (ws_bytes < sb_raster_workspace_bytes()) return fail(SB_EWORKSPACE, "raster workspace too small");
     const CamDev d = make_cam(cam, cfg);
-    cudaMemsetAsync(ws, 0, sizeof(int), S(stream));
     sb_launch_raster_fwd(static_cast<const RasterRec*>(recs), tile_offsets, tile_prims, d.W, d.H, d.tiles_x,
                          d.tiles_x * d.tiles_y, *cfg, static_cast<int*>(ws), color, transmittance, frag_count, last,
                          S(stream));
@@ -211,7 +211,6 @@ int sb_raster_bwd(const void* recs, const int32_t* tile_offsets, const int32_t* 
     if (ws_bytes < sb_raster_workspace_bytes()) return fail(SB_EWORKSPACE, "raster workspace too small");
     const CamDev d = make_cam(cam, cfg);
     if (n_cap > 0) cudaMemsetAsync(sgrad, 0, sizeof(sb_screen_grad) * (size_t)n_cap, S(stream));
-    cudaMemsetAsync(ws, 0, sizeof(int), S(stream));
     sb_launch_raster_bwd(static_cast<const RasterRec*>(recs), tile_offsets, tile_prims, d.W, d.H, d.tiles_x,
                          d.tiles_x * d.tiles_y, *cfg, static_cast<int*>(ws), dL_dI, transmittance, last, sgrad,
                          S(stream));
@@ -251,6 +250,17 @@ int sb_loss_fwd_bwd(const float* rendered, const float* target, const uint8_t* t
     if (!target && !target_u8) return fail(SB_EINVAL, "target is NULL");
     sb_launch_loss(rendered, target, target_u8, width, height, lam, grad, accum, loss, S(stream));
     return check_launch("sb_loss_fwd_bwd");
+}
+
+int sb_host_mapped_pointer(void* host, void** device) {
+    if (!host || !device) return fail(SB_EINVAL, "NULL pointer");
+    if (cudaHostGetDevicePointer(device, host, 0) != cudaSuccess) {
+        cudaGetLastError();
+        *device = nullptr;
+        return fail(SB_EINVAL, "host buffer is not mapped pinned memory");
+    }
+    g_err.clear();
+    return SB_OK;
 }
 
 int sb_lane_reduce(const float* values, int64_t groups, int mode, float* out_f, double* out_d, sb_stream_t stream) {

@@ -254,6 +254,7 @@ tile_count_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict_
                   int tiles_y, int st_x, int W, int H, uint4* __restrict__ spans_out, uint32_t* __restrict__ origin,
                   int32_t* __restrict__ counts, int32_t* __restrict__ st_counts)
 {
+    sb_pdl_begin();
     __shared__ WinSmem sm;
     const int nc = min(counters[1], n_cap);
     const int s = blockIdx.x * kBinThreads + threadIdx.x;
@@ -334,11 +335,13 @@ constexpr int kScanItems = 16;   // per thread and round
 constexpr int kStThreads = 384;
 constexpr int kStCap = kStThreads * 16;   // super-tile entries sorted in one shared-memory pass
 
-// exclusive scan of a[0, n) in place, total to a[n]; with `longs`, the
+// exclusive scan of cnt[0, n) into out[0, n], total to out[n] and *total;
+// cnt is re-zeroed as it is read (ready for the next call); with `copy` the
+// offsets are also written there (the scatter cursors); with `longs`, the
 // indices whose count exceeds `long_min` are appended to longs[1..]
 // (longs[0] = how many).  Whole (1024-thread) CTA.
-__device__ void cta_scan_inplace(int32_t* __restrict__ a, int n, int32_t* __restrict__ total,
-                                 int32_t* __restrict__ longs, uint32_t long_min)
+__device__ void cta_scan(int32_t* __restrict__ cnt, int32_t* __restrict__ out, int n, int32_t* __restrict__ total,
+                         int32_t* __restrict__ copy, int32_t* __restrict__ longs, uint32_t long_min)
 {
     __shared__ uint32_t s_warp[kScanThreads / 32];
     __shared__ uint32_t s_carry;
@@ -354,9 +357,12 @@ __device__ void cta_scan_inplace(int32_t* __restrict__ a, int n, int32_t* __rest
         uint32_t v[kScanItems], sum = 0;
 #pragma unroll
         for (int j = 0; j < kScanItems; j++) {
-            v[j] = beg + j < n ? (uint32_t)a[beg + j] : 0u;
+            v[j] = beg + j < n ? (uint32_t)cnt[beg + j] : 0u;
             sum += v[j];
         }
+#pragma unroll
+        for (int j = 0; j < kScanItems; j++)
+            if (beg + j < n) cnt[beg + j] = 0;
         uint32_t x = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -378,7 +384,10 @@ __device__ void cta_scan_inplace(int32_t* __restrict__ a, int n, int32_t* __rest
         uint32_t run = s_carry + (warp ? s_warp[warp - 1] : 0u) + x - sum;
 #pragma unroll
         for (int j = 0; j < kScanItems; j++) {
-            if (beg + j < n) a[beg + j] = (int32_t)run;
+            if (beg + j < n) {
+                out[beg + j] = (int32_t)run;
+                if (copy) copy[beg + j] = (int32_t)run;
+            }
             if (longs && v[j] > long_min) longs[1 + atomicAdd(&longs[0], 1)] = beg + j;
             run += v[j];
         }
@@ -387,18 +396,24 @@ __device__ void cta_scan_inplace(int32_t* __restrict__ a, int n, int32_t* __rest
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        a[n] = (int32_t)s_carry;
+        out[n] = (int32_t)s_carry;
         *total = (int32_t)s_carry;
     }
     __syncthreads();
 }
 
 __global__ void __launch_bounds__(kScanThreads)
-tile_scan_kernel(int32_t* __restrict__ offsets, int ntiles, int32_t* __restrict__ st_offsets, int nst,
-                 int32_t* __restrict__ totals, int32_t* __restrict__ st_longs)
+tile_scan_kernel(int32_t* __restrict__ tile_cnt, int32_t* __restrict__ offsets, int ntiles,
+                 int32_t* __restrict__ st_cnt, int32_t* __restrict__ st_offsets, int nst,
+                 int32_t* __restrict__ totals, int32_t* __restrict__ st_longs, int32_t* __restrict__ cursor,
+                 const int32_t* __restrict__ counters, int32_t* __restrict__ mirror)
 {
-    cta_scan_inplace(offsets, ntiles, totals, nullptr, 0);
-    cta_scan_inplace(st_offsets, nst, totals + 1, st_longs, (uint32_t)kStCap);
+    sb_pdl_begin();
+    cta_scan(tile_cnt, offsets, ntiles, totals, nullptr, nullptr, 0);
+    cta_scan(st_cnt, st_offsets, nst, totals + 1, cursor, st_longs, (uint32_t)kStCap);
+    // host-mapped copy of (vis, N_c, ndeg, 0, P, E): the host's one read
+    // needs no device-to-host copy in the stream
+    if (mirror && threadIdx.x < 6) mirror[threadIdx.x] = threadIdx.x < 4 ? counters[threadIdx.x] : totals[threadIdx.x - 4];
 }
 
 // ---- finish (1): scatter keys into super-tile ranges ---------------------------
@@ -407,6 +422,7 @@ st_scatter_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict_
                   int tiles_y, int st_x, int32_t* __restrict__ cursor, unsigned long long* __restrict__ keys,
                   int e_cap, int p_cap)
 {
+    sb_pdl_begin();
     __shared__ WinSmem sm;
     if (counters[5] > e_cap || counters[4] > p_cap) return;   // buffers too small: the caller re-launches
     const int nc = min(counters[1], n_cap);
@@ -650,11 +666,30 @@ __device__ void st_emit(StSmem& sm, SlotOf&& slot_of, int E, int st, int st_x, c
     }
     for (int c0 = 0; c0 < E; c0 += kStCap) {
         const int n = min(kStCap, E - c0);
-        for (int e = tid; e < n; e += kStThreads) {
-            const uint32_t sl = slot_of(c0 + e);
-            const uint32_t org = __ldg(origin + sl);
-            const uint4 s0 = __ldg(spans + 2 * sl), s1 = __ldg(spans + 2 * sl + 1);
-            sm.mask[e] = (uint16_t)entry_mask(recs, org, s0, s1, sl, sx, sy, tiles_x, tiles_y, W, H);
+        constexpr int U = 2;   // entries per thread in flight
+        for (int e0 = tid; e0 < n; e0 += U * kStThreads) {
+            uint32_t sl[U], org[U];
+            uint4 s0[U], s1[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int e = e0 + u * kStThreads;
+                sl[u] = e < n ? slot_of(c0 + e) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (e0 + u * kStThreads < n) {
+                    org[u] = __ldg(origin + sl[u]);
+                    s0[u] = __ldg(spans + 2 * sl[u]);
+                    s1[u] = __ldg(spans + 2 * sl[u] + 1);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int e = e0 + u * kStThreads;
+                if (e < n)
+                    sm.mask[e] = (uint16_t)entry_mask(recs, org[u], s0[u], s1[u], sl[u], sx, sy, tiles_x, tiles_y,
+                                                      W, H);
+            }
         }
         __syncthreads();
         // compaction, balanced over the warps: warp w takes entries
@@ -712,6 +747,7 @@ st_sort_emit_kernel(const int32_t* __restrict__ st_offsets, int st_x, unsigned l
                     int tiles_y, int W, int H, int32_t* __restrict__ prims, const int32_t* __restrict__ counters,
                     int e_cap, int p_cap)
 {
+    sb_pdl_begin();
     if (counters[5] > e_cap || counters[4] > p_cap) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StSmem& sm = *reinterpret_cast<StSmem*>(smem_raw);
@@ -742,6 +778,7 @@ st_sort_emit_long_kernel(const int32_t* __restrict__ st_offsets, const int32_t* 
                          int tiles_x, int tiles_y, int W, int H, int32_t* __restrict__ prims,
                          const int32_t* __restrict__ counters, int e_cap, int p_cap)
 {
+    sb_pdl_begin();
     if (counters[5] > e_cap || counters[4] > p_cap) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StSmem& sm = *reinterpret_cast<StSmem*>(smem_raw);
@@ -776,22 +813,31 @@ st_sort_emit_long_kernel(const int32_t* __restrict__ st_offsets, const int32_t* 
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// bin state: spans (32 B per compact slot) | origin (4 B per slot) |
-// super-tile offsets (nst + 1) | long super-tile list (1 + nst)
+// bin state: tile counts (ntiles + 1) | super-tile counts (nst + 1) |
+// scatter cursors (nst) | spans (32 B per compact slot) | origin (4 B per
+// slot) | super-tile offsets (nst + 1) | long super-tile list (1 + nst).
+// The count arrays come first (offsets independent of n_cap): zeroed once
+// before first use, accumulated by the count kernel, re-zeroed by the scan.
 struct StateLayout {
+    int32_t* tile_cnt;
+    int32_t* st_cnt;
+    int32_t* cursor;
     uint4* spans;
     uint32_t* origin;
     int32_t* st_offsets;
     int32_t* st_longs;
 };
-inline size_t state_bytes(int n_cap, int nst) {
-    const size_t n = (size_t)(n_cap > 0 ? n_cap : 1);
-    return align256(n * 32) + align256(n * 4) + 2 * align256((size_t)(nst + 1) * 4);
+inline size_t state_bytes(int n_cap, int ntiles) {
+    const size_t n = (size_t)(n_cap > 0 ? n_cap : 1), t = (size_t)ntiles + 1;
+    return 5 * align256(t * 4) + align256(n * 32) + align256(n * 4);
 }
-inline StateLayout state_layout(void* state, int n_cap, int nst) {
+inline StateLayout state_layout(void* state, int n_cap, int ntiles, int nst) {
     const size_t n = (size_t)(n_cap > 0 ? n_cap : 1);
     char* p = static_cast<char*>(state);
     StateLayout L;
+    L.tile_cnt = reinterpret_cast<int32_t*>(p); p += align256((size_t)(ntiles + 1) * 4);
+    L.st_cnt = reinterpret_cast<int32_t*>(p); p += align256((size_t)(nst + 1) * 4);
+    L.cursor = reinterpret_cast<int32_t*>(p); p += align256((size_t)(nst + 1) * 4);
     L.spans = reinterpret_cast<uint4*>(p); p += align256(n * 32);
     L.origin = reinterpret_cast<uint32_t*>(p); p += align256(n * 4);
     L.st_offsets = reinterpret_cast<int32_t*>(p); p += align256((size_t)(nst + 1) * 4);
@@ -807,25 +853,23 @@ inline int st_dim(int tiles) { return (tiles + kST - 1) / kST; }
 size_t sb_bin_state_bytes(int n_cap, int ntiles) { return state_bytes(n_cap, ntiles); }
 
 void sb_launch_bin_prepare(const RasterRec* recs, const int32_t* counters, int n_cap, const CamDev& cam,
-                           int32_t* tile_offsets, int32_t* totals, void* state, cudaStream_t stream)
+                           int32_t* tile_offsets, int32_t* totals, int32_t* mirror, void* state, cudaStream_t stream)
 {
     const int ntiles = cam.tiles_x * cam.tiles_y;
     const int st_x = st_dim(cam.tiles_x), nst = st_x * st_dim(cam.tiles_y);
-    const StateLayout L = state_layout(state, n_cap, nst);
-    cudaMemsetAsync(tile_offsets, 0, sizeof(int32_t) * (ntiles + 1), stream);
-    cudaMemsetAsync(L.st_offsets, 0, sizeof(int32_t) * (nst + 1), stream);
+    const StateLayout L = state_layout(state, n_cap, ntiles, nst);
     if (n_cap > 0)
-        tile_count_kernel<<<(n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream>>>(
-            recs, counters, n_cap, cam.tiles_x, cam.tiles_y, st_x, cam.W, cam.H, L.spans, L.origin, tile_offsets,
-            L.st_offsets);
-    tile_scan_kernel<<<1, kScanThreads, 0, stream>>>(tile_offsets, ntiles, L.st_offsets, nst, totals, L.st_longs);
+        sb_launch(tile_count_kernel, (n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream, recs, counters, n_cap, cam.tiles_x, cam.tiles_y, st_x, cam.W, cam.H, L.spans, L.origin, L.tile_cnt,
+            L.st_cnt);
+    sb_launch(tile_scan_kernel, 1, kScanThreads, 0, stream, L.tile_cnt, tile_offsets, ntiles, L.st_cnt, L.st_offsets, nst,
+                                                     totals, L.st_longs, L.cursor, counters, mirror);
 }
 
 // ---- finish --------------------------------------------------------------------
 size_t sb_bin_finish_ws(long long n_entries, int ntiles) {
     const size_t E = (size_t)(n_entries > 0 ? n_entries : 1);
-    const int nst = ntiles;   // upper bound for the cursor array
-    return 2 * align256(E * 8) + align256((size_t)nst * 4);
+    (void)ntiles;
+    return 2 * align256(E * 8);
 }
 
 // e_cap / p_cap: what the keys workspace and tile_prims hold.  When the
@@ -838,14 +882,12 @@ void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_
 {
     if (e_cap <= 0 || p_cap <= 0 || n_cap <= 0) return;
     const int st_x = st_dim(cam.tiles_x), nst = st_x * st_dim(cam.tiles_y);
-    const StateLayout L = state_layout(const_cast<void*>(state), n_cap, nst);
+    const StateLayout L = state_layout(const_cast<void*>(state), n_cap, cam.tiles_x * cam.tiles_y, nst);
     char* w = static_cast<char*>(ws);
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)e_cap * 8);
-    unsigned long long* scratch = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)e_cap * 8);
-    int32_t* cursor = reinterpret_cast<int32_t*>(w);
-    cudaMemcpyAsync(cursor, L.st_offsets, sizeof(int32_t) * nst, cudaMemcpyDeviceToDevice, stream);
-    st_scatter_kernel<<<(n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream>>>(
-        recs, counters, n_cap, cam.tiles_x, cam.tiles_y, st_x, cursor, keys, e_cap, p_cap);
+    unsigned long long* scratch = reinterpret_cast<unsigned long long*>(w);
+    int32_t* cursor = L.cursor;   // the scan's copy of the super-tile offsets
+    sb_launch(st_scatter_kernel, (n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream, recs, counters, n_cap, cam.tiles_x, cam.tiles_y, st_x, cursor, keys, e_cap, p_cap);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(st_sort_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(StSmem));
@@ -853,11 +895,10 @@ void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_
                              (int)sizeof(StSmem));
         attr = true;
     }
-    st_sort_emit_kernel<<<nst, kStThreads, sizeof(StSmem), stream>>>(L.st_offsets, st_x, keys, recs, L.spans,
+    sb_launch(st_sort_emit_kernel, nst, kStThreads, sizeof(StSmem), stream, L.st_offsets, st_x, keys, recs, L.spans,
                                                                         L.origin, tile_offsets, cam.tiles_x,
                                                                         cam.tiles_y, cam.W, cam.H, tile_prims,
                                                                         counters, e_cap, p_cap);
-    st_sort_emit_long_kernel<<<148, kStThreads, sizeof(StSmem), stream>>>(
-        L.st_offsets, L.st_longs, st_x, keys, scratch, recs, L.spans, L.origin, tile_offsets, cam.tiles_x,
+    sb_launch(st_sort_emit_long_kernel, 148, kStThreads, sizeof(StSmem), stream, L.st_offsets, L.st_longs, st_x, keys, scratch, recs, L.spans, L.origin, tile_offsets, cam.tiles_x,
         cam.tiles_y, cam.W, cam.H, tile_prims, counters, e_cap, p_cap);
 }

@@ -28,6 +28,7 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
              const RasterRec* __restrict__ recs, const sb_screen_grad* __restrict__ sg, float4* __restrict__ grads,
              double* __restrict__ stat_S, double* __restrict__ stat_M, int32_t* __restrict__ stat_C)
 {
+    sb_pdl_begin();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     // every load that depends only on g is issued together with the cluster
@@ -188,6 +189,7 @@ adam_kernel(float4* __restrict__ params, const float4* __restrict__ grads, float
             float4* __restrict__ v, int32_t* __restrict__ step, const uint8_t* __restrict__ cluster_mask, int n,
             double lr0, double lr1, double lr2, double lr3, double lr4)
 {
+    sb_pdl_begin();
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     const int g = tid >> 2, kq = tid & 3;
     if (g >= n || !cluster_mask[g / SB_CLUSTER_SIZE]) return;
@@ -226,6 +228,7 @@ adam_kernel(float4* __restrict__ params, const float4* __restrict__ grads, float
 __global__ void variance_kernel(const double* __restrict__ S, const double* __restrict__ M,
                                 const int32_t* __restrict__ C, int n, double* __restrict__ out)
 {
+    sb_pdl_begin();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     const double c = (double)C[g];
@@ -240,7 +243,7 @@ void sb_launch_chain(const float* params, int n, const CamDev& cam, const int32_
                      cudaStream_t stream)
 {
     if (n <= 0) return;
-    chain_kernel<<<(n + 255) / 256, 256, 0, stream>>>(reinterpret_cast<const float4*>(params), n, cam,
+    sb_launch(chain_kernel, (n + 255) / 256, 256, 0, stream, reinterpret_cast<const float4*>(params), n, cam,
                                                       cluster_offset, recs, sg, reinterpret_cast<float4*>(grads), S,
                                                       M, C);
 }
@@ -249,13 +252,12 @@ void sb_launch_adam(float* params, const float* grads, float* m, float* v, int32
                     int n, const double lr5[5], cudaStream_t stream)
 {
     if (n <= 0) return;
-    adam_kernel<<<(4 * n + 255) / 256, 256, 0, stream>>>(
-        reinterpret_cast<float4*>(params), reinterpret_cast<const float4*>(grads), reinterpret_cast<float4*>(m),
+    sb_launch(adam_kernel, (4 * n + 255) / 256, 256, 0, stream, reinterpret_cast<float4*>(params), reinterpret_cast<const float4*>(grads), reinterpret_cast<float4*>(m),
         reinterpret_cast<float4*>(v), step, mask, n, lr5[0], lr5[1], lr5[2], lr5[3], lr5[4]);
 }
 
 void sb_launch_variance(const double* S, const double* M, const int32_t* C, int n, double* out, cudaStream_t stream)
 {
     if (n <= 0) return;
-    variance_kernel<<<(n + 255) / 256, 256, 0, stream>>>(S, M, C, n, out);
+    sb_launch(variance_kernel, (n + 255) / 256, 256, 0, stream, S, M, C, n, out);
 }

@@ -10,6 +10,41 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include "../../include/splat_types.h"
+#include <utility>
+
+// Programmatic dependent launch.  Every kernel is launched with programmatic
+// stream serialization (sb_launch) and opens with sb_pdl_begin(), which
+// waits until the preceding kernel in the stream has completed and its
+// writes are visible (nothing below may assume otherwise).  No kernel
+// triggers its dependents early: the next grid launches at completion, but
+// pre-staged, which removes most of the launch gap.  (Triggering at kernel
+// start was measured slower: dependents' CTAs sat resident through the
+// previous kernel's tail.)  -DSB_NO_PDL gives plain launches for A/B runs.
+__device__ __forceinline__ void sb_pdl_begin() {
+#ifndef SB_NO_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+inline void sb_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                      Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+#ifndef SB_NO_PDL
+    cfg.numAttrs = 1;
+#else
+    cfg.numAttrs = 0;
+#endif
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 #define SB_INLINE __device__ __forceinline__
 

@@ -12,8 +12,9 @@
 // with the L1 sign term.  The field buffer reuses the staged input's shared
 // memory, so two CTAs fit per SM; maps sharing a filter sit interleaved in
 // float2 planes so each tap is one f32x2 FMA per pair.  Every separable
-// pass is a register sliding window: a thread owns a short run of outputs along the filter axis, loads the run +
-// 10 inputs once from shared memory and forms all outputs from registers.
+// pass is a register sliding window: a thread owns a short run of outputs
+// along the filter axis, loads the run + 10 inputs once from shared memory
+// and forms all outputs from registers.
 // Loss partial sums go to two float64 accumulators.
 #include "common.cuh"
 
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, const uint8_t* __restrict__ y_u8,
             int W, int H, float lam, Win win, float* __restrict__ grad, double* __restrict__ accum)
 {
+    sb_pdl_begin();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     const int ox = blockIdx.x * TW, oy = blockIdx.y * TH, ch = blockIdx.z;
@@ -300,13 +302,15 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
     }
 }
 
-__global__ void loss_finalize_kernel(const double* __restrict__ accum, int W, int H, float lam, double* loss)
+__global__ void loss_finalize_kernel(double* __restrict__ accum, int W, int H, float lam, double* loss)
 {
+    sb_pdl_begin();
     const double n = (double)W * H * 3.0;
     const double ni = (double)(W - 2 * R) * (double)(H - 2 * R);
     double l = (1.0 - lam) * accum[0] / n;
     if (lam != 0.f) l += lam * (1.0 - (ni > 0 ? accum[1] / (3.0 * ni) : 0.0));
     loss[0] = l;
+    accum[0] = accum[1] = 0.0;   // left zeroed for the next call (no memset per call)
 }
 
 }  // namespace
@@ -327,8 +331,7 @@ void sb_launch_loss(const float* x, const float* y, const uint8_t* y_u8, int W, 
         cudaFuncSetAttribute(loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
         attr = true;
     }
-    cudaMemsetAsync(accum, 0, 2 * sizeof(double), stream);
     dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, 3);
-    loss_kernel<<<grid, kThreads, sizeof(Smem), stream>>>(x, y, y_u8, W, H, lam, win, grad, accum);
-    loss_finalize_kernel<<<1, 1, 0, stream>>>(accum, W, H, lam, loss);
+    sb_launch(loss_kernel, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum);
+    sb_launch(loss_finalize_kernel, 1, 1, 0, stream, accum, W, H, lam, loss);
 }

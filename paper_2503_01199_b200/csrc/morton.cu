@@ -16,6 +16,7 @@ constexpr int kBoundsBlocks = 4 * 148;
 __global__ void __launch_bounds__(256)
 bounds_partial_kernel(const float4* __restrict__ params, int n, float* __restrict__ partial)
 {
+    sb_pdl_begin();
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     bool nan = false;
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) {
@@ -52,6 +53,7 @@ bounds_partial_kernel(const float4* __restrict__ params, int n, float* __restric
 
 __global__ void bounds_final_kernel(const float* __restrict__ partial, int nb, int n, double* __restrict__ lohi)
 {
+    sb_pdl_begin();
     const int k = threadIdx.x;
     if (k >= 6) return;
     if (n == 0) { lohi[k] = 0.0; return; }
@@ -80,6 +82,7 @@ __global__ void __launch_bounds__(256)
 morton_keys_kernel(const float4* __restrict__ params, int n, const double* __restrict__ lohi,
                    unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals, int* __restrict__ bad)
 {
+    sb_pdl_begin();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     const float4 p = __ldg(params + (size_t)g * 4);
@@ -112,6 +115,7 @@ struct PermArrays {
 __global__ void __launch_bounds__(256)
 permute_kernel(const uint32_t* __restrict__ perm, int n, PermArrays a)
 {
+    sb_pdl_begin();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     const size_t from = perm[g];
@@ -134,15 +138,15 @@ permute_kernel(const uint32_t* __restrict__ perm, int n, PermArrays a)
 }  // namespace
 
 void sb_launch_bounds(const float* params, int n, float* partial, double* lohi, cudaStream_t stream) {
-    bounds_partial_kernel<<<kBoundsBlocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(params), n, partial);
-    bounds_final_kernel<<<1, 32, 0, stream>>>(partial, kBoundsBlocks, n, lohi);
+    sb_launch(bounds_partial_kernel, kBoundsBlocks, 256, 0, stream, reinterpret_cast<const float4*>(params), n, partial);
+    sb_launch(bounds_final_kernel, 1, 32, 0, stream, partial, kBoundsBlocks, n, lohi);
 }
 int sb_bounds_partial_floats() { return kBoundsBlocks * 6; }
 
 void sb_launch_morton_keys(const float* params, int n, const double* lohi, unsigned long long* keys, uint32_t* vals,
                            int* bad, cudaStream_t stream) {
     if (n <= 0) return;
-    morton_keys_kernel<<<(n + 255) / 256, 256, 0, stream>>>(reinterpret_cast<const float4*>(params), n, lohi, keys,
+    sb_launch(morton_keys_kernel, (n + 255) / 256, 256, 0, stream, reinterpret_cast<const float4*>(params), n, lohi, keys,
                                                             vals, bad);
 }
 
@@ -156,7 +160,7 @@ void sb_launch_permute(const uint32_t* perm, int n, int count, const void* const
         a.dst[k] = static_cast<char*>(dst[k]);
         a.row_bytes[k] = row_bytes[k];
     }
-    permute_kernel<<<(n + 255) / 256, 256, 0, stream>>>(perm, n, a);
+    sb_launch(permute_kernel, (n + 255) / 256, 256, 0, stream, perm, n, a);
 }
 
 // ---- Morton sort (u64 keys): stable onesweep LSD radix sort -----------------

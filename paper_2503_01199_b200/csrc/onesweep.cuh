@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(kThreads)
 hist_kernel(const K* __restrict__ keys, const int* __restrict__ n_dev, int n_cap, int passes,
             uint32_t* __restrict__ hist)
 {
+    sb_pdl_begin();
     // two copies per pass (even / odd warps) to halve cross-warp contention;
     // same-bin lanes of one warp are serialised by the hardware
     __shared__ uint32_t h[2][8][256];
@@ -87,6 +88,7 @@ hist_kernel(const K* __restrict__ keys, const int* __restrict__ n_dev, int n_cap
 // in place: hist[p][*] -> exclusive prefix over digits
 __global__ void __launch_bounds__(256) scan_hist_kernel(uint32_t* hist, int passes)
 {
+    sb_pdl_begin();
     __shared__ uint32_t s[256];
     for (int p = 0; p < passes; p++) {
         const uint32_t v = hist[p * 256 + threadIdx.x];
@@ -109,6 +111,7 @@ pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
             uint32_t* __restrict__ vout, const int* __restrict__ n_dev, int n_cap, int shift,
             const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status, unsigned* __restrict__ ticket)
 {
+    sb_pdl_begin();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem<K>& sm = *reinterpret_cast<Smem<K>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -249,8 +252,8 @@ int sort(K* keys, uint32_t* vals, K* k_alt, uint32_t* v_alt, const int* n_dev, i
     unsigned* ticket = reinterpret_cast<unsigned*>(status + (size_t)tiles * 256);
     cudaMemsetAsync(hist, 0, 256 * sizeof(uint32_t) * passes, stream);
     const int hb = min((n_cap + kThreads * kHistItems - 1) / (kThreads * kHistItems), 8 * 148);
-    hist_kernel<K><<<hb, kThreads, 0, stream>>>(keys, n_dev, n_cap, passes, hist);
-    scan_hist_kernel<<<1, 256, 0, stream>>>(hist, passes);
+    sb_launch(hist_kernel<K>, hb, kThreads, 0, stream, keys, n_dev, n_cap, passes, hist);
+    sb_launch(scan_hist_kernel, 1, 256, 0, stream, hist, passes);
     int flip = 0;
     for (int p = 0; p < passes; p++) {
         cudaMemsetAsync(status, 0, (size_t)tiles * 256 * sizeof(uint32_t) + sizeof(unsigned), stream);
@@ -259,8 +262,7 @@ int sort(K* keys, uint32_t* vals, K* k_alt, uint32_t* v_alt, const int* n_dev, i
         K* ko = flip ? keys : k_alt;
         uint32_t* vo = flip ? vals : v_alt;
         const bool last = p == passes - 1;
-        pass_kernel<K><<<tiles, kThreads, sizeof(Smem<K>), stream>>>(
-            ki, (p == 0 && iota) ? nullptr : vi, (last && !keep_keys) ? nullptr : ko, vo, n_dev, n_cap,
+        sb_launch(pass_kernel<K>, tiles, kThreads, sizeof(Smem<K>), stream, ki, (p == 0 && iota) ? nullptr : vi, (last && !keep_keys) ? nullptr : ko, vo, n_dev, n_cap,
             8 * p, hist + 256 * p, status, ticket);
         flip ^= 1;
     }

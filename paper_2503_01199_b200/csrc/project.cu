@@ -36,9 +36,10 @@ __global__ void __launch_bounds__(kThreads, 3)
 project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clusters, CamDev cam,
                             int use_culling, RasterRec* __restrict__ rec_out, int32_t* __restrict__ compact_map,
                             int32_t* __restrict__ cluster_offset, uint8_t* __restrict__ cluster_vis,
-                            int32_t* __restrict__ counters,
+                            int32_t* __restrict__ counters, float4* __restrict__ sgrad_zero,
                             unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket)
 {
+    sb_pdl_begin();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpStage* stage = reinterpret_cast<WarpStage*>(smem_raw);
     __shared__ int s_bid;
@@ -113,7 +114,7 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
             vis = true;
         }
         int nd = __reduce_add_sync(0xffffffffu, ndeg);
-        if (lane == 0 && nd) atomicAdd(&counters[2], nd);
+        if (lane == 0 && nd) atomicAdd(ticket + 2, (unsigned)nd);
     }
     if (lane == 0) s_warp_vis[warp] = vis ? 1u : 0u;
     __syncthreads();
@@ -124,34 +125,63 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
         if (lane == 0) s_prefix = pre;
     }
     __syncthreads();
-    if (cl >= n_clusters) return;
-    uint32_t before = s_prefix;
-    for (int w = 0; w < warp; w++) before += s_warp_vis[w];
-    if (lane == 0) {
-        cluster_vis[cl] = vis ? 1 : 0;
-        cluster_offset[cl] = vis ? (int32_t)(before * SB_CLUSTER_SIZE) : -1;
+    if (cl < n_clusters) {
+        uint32_t before = s_prefix;
+        for (int w = 0; w < warp; w++) before += s_warp_vis[w];
+        if (lane == 0) {
+            cluster_vis[cl] = vis ? 1 : 0;
+            cluster_offset[cl] = vis ? (int32_t)(before * SB_CLUSTER_SIZE) : -1;
+        }
+        if (vis) {
+            const int members = min(SB_CLUSTER_SIZE, n - cl * SB_CLUSTER_SIZE);
+            __syncwarp();
+            // coalesced copy of the staged records: 128 x 48 B = 384 float4
+            const size_t base = (size_t)before * SB_CLUSTER_SIZE;
+            const float4* src = reinterpret_cast<const float4*>(st);
+            float4* dst = reinterpret_cast<float4*>(rec_out + base);
+            const int nvec = members * 3;
+            for (int v = lane; v < nvec; v += 32) dst[v] = src[v];
+            for (int s = lane; s < members; s += 32) compact_map[base + s] = cl * SB_CLUSTER_SIZE + s;
+            // the backward's screen-gradient rows of these slots start at
+            // zero (64 B each), written here while the kernel is compute-bound
+            if (sgrad_zero) {
+                float4* z = sgrad_zero + base * 4;
+                for (int v = lane; v < members * 4; v += 32) z[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
     }
-    if (!vis) return;
-    const int members = min(SB_CLUSTER_SIZE, n - cl * SB_CLUSTER_SIZE);
-    if (lane == 0) {
-        atomicAdd(&counters[0], 1);
-        atomicAdd(&counters[1], members);
+    // The last CTA to finish publishes the counters -- visible clusters (the
+    // last block's inclusive look-back total), N_c, n_degenerate -- and
+    // re-zeroes the look-back workspace for the next call (no memset).
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s_last = atomicAdd(ticket + 1, 1u) == gridDim.x - 1;
     }
-    __syncwarp();
-    // coalesced copy of the staged records: 128 x 48 B = 384 float4
-    const size_t base = (size_t)before * SB_CLUSTER_SIZE;
-    const float4* src = reinterpret_cast<const float4*>(st);
-    float4* dst = reinterpret_cast<float4*>(rec_out + base);
-    const int nvec = members * 3;
-    for (int v = lane; v < nvec; v += 32) dst[v] = src[v];
-    for (int s = lane; s < members; s += 32) compact_map[base + s] = cl * SB_CLUSTER_SIZE + s;
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        if (threadIdx.x == 0) {
+            const uint32_t vis_total = (uint32_t)atomicAdd(&status[gridDim.x - 1], 0ull);
+            const int last_members = n - (n_clusters - 1) * SB_CLUSTER_SIZE;
+            const bool last_vis = *reinterpret_cast<volatile uint8_t*>(cluster_vis + n_clusters - 1) != 0;
+            counters[0] = (int32_t)vis_total;
+            counters[1] = (int32_t)(vis_total * SB_CLUSTER_SIZE) - (last_vis ? SB_CLUSTER_SIZE - last_members : 0);
+            counters[2] = (int32_t)atomicExch(ticket + 2, 0u);
+            counters[3] = 0;
+            atomicExch(ticket, 0u);
+            atomicExch(ticket + 1, 0u);
+        }
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) status[i] = 0ull;
+    }
 }
 
 }  // namespace
 
 void sb_launch_project_cull_compact(const float* params, int n, const CamDev& cam, int use_culling,
                                     RasterRec* rec_out, int32_t* compact_map, int32_t* cluster_offset,
-                                    uint8_t* cluster_vis, int32_t* counters,
+                                    uint8_t* cluster_vis, int32_t* counters, void* sgrad_zero,
                                     unsigned long long* status, unsigned int* ticket, cudaStream_t stream)
 {
     const int k = (n + SB_CLUSTER_SIZE - 1) / SB_CLUSTER_SIZE;
@@ -163,9 +193,8 @@ void sb_launch_project_cull_compact(const float* params, int n, const CamDev& ca
         cudaFuncSetAttribute(project_cull_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    project_cull_compact_kernel<<<blocks, kThreads, smem, stream>>>(
-        reinterpret_cast<const float4*>(params), n, k, cam, use_culling, rec_out, compact_map, cluster_offset,
-        cluster_vis, counters, status, ticket);
+    sb_launch(project_cull_compact_kernel, blocks, kThreads, smem, stream, reinterpret_cast<const float4*>(params), n, k, cam, use_culling, rec_out, compact_map, cluster_offset,
+        cluster_vis, counters, static_cast<float4*>(sgrad_zero), status, ticket);
 }
 
 int sb_project_blocks(int n) {

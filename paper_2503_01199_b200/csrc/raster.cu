@@ -161,9 +161,22 @@ SB_INLINE void lane_alpha_raw(const SRec& r, float px, float py0, float araw[4],
     for (int i = 0; i < 4; i++) araw[i] = ex2(e[i] + r.lg2o);
 }
 
-SB_INLINE int next_tile(int* counter, int lane) {
+// Dynamic tile queue: counter[0] hands out tiles, counter[1] counts the
+// warps that drew past the end.  The last such warp resets both, so the
+// workspace is left zeroed for the next launch (no memset per call): every
+// warp draws exactly one past-the-end ticket, after which it draws no more.
+SB_INLINE int next_tile(int* counter, int lane, int ntiles) {
     int t = 0;
-    if (lane == 0) t = atomicAdd(counter, 1);
+    if (lane == 0) {
+        t = atomicAdd(counter, 1);
+        if (t >= ntiles) {
+            const int nwarps = (int)(gridDim.x * (blockDim.x >> 5));
+            if (atomicAdd(counter + 1, 1) == nwarps - 1) {
+                atomicExch(counter, 0);
+                atomicExch(counter + 1, 0);
+            }
+        }
+    }
     return __shfl_sync(0xffffffffu, t, 0);
 }
 
@@ -184,10 +197,11 @@ struct FwdParams {
 __global__ void __launch_bounds__(kThreads)
 raster_fwd_kernel(FwdParams p)
 {
+    sb_pdl_begin();
     __shared__ SRec slabs[kWarpsPerBlock][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     SRec* slab = slabs[warp];
-    for (int t = next_tile(p.tile_counter, lane); t < p.ntiles; t = next_tile(p.tile_counter, lane)) {
+    for (int t = next_tile(p.tile_counter, lane, p.ntiles); t < p.ntiles; t = next_tile(p.tile_counter, lane, p.ntiles)) {
         const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
         const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
         const float px = (float)pxi, py0 = (float)py0i;
@@ -275,13 +289,14 @@ template <typename H>
 __global__ void __launch_bounds__(kThreads)
 raster_fwd_half_kernel(FwdParams p)
 {
+    sb_pdl_begin();
     using O = Half16<H>;
     __shared__ SRec slabs[kWarpsPerBlock][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     SRec* slab = slabs[warp];
     const H amin = O::from(p.amin), amax = O::from(p.amax), tstop = O::from(p.tstop);
     const H one = O::from(1.0f), zero = O::from(0.0f);
-    for (int t = next_tile(p.tile_counter, lane); t < p.ntiles; t = next_tile(p.tile_counter, lane)) {
+    for (int t = next_tile(p.tile_counter, lane, p.ntiles); t < p.ntiles; t = next_tile(p.tile_counter, lane, p.ntiles)) {
         const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
         const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
         const float px = (float)pxi, py0 = (float)py0i;
@@ -549,10 +564,11 @@ constexpr int kBwdWarps = 3;
 __global__ void __launch_bounds__(kBwdWarps * 32, 6)
 raster_bwd_kernel(BwdParams p)
 {
+    sb_pdl_begin();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     BwdWarpSmem& ws = reinterpret_cast<BwdWarpSmem*>(smem_raw)[warp];
-    for (int t = next_tile(p.tile_counter, lane); t < p.ntiles; t = next_tile(p.tile_counter, lane)) {
+    for (int t = next_tile(p.tile_counter, lane, p.ntiles); t < p.ntiles; t = next_tile(p.tile_counter, lane, p.ntiles)) {
         const int beg = p.offsets[t];
         if (p.offsets[t + 1] == beg) continue;
         const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
@@ -712,9 +728,9 @@ void sb_launch_raster_fwd(const RasterRec* recs, const int32_t* offsets, const i
     const int want = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const int blocks = min(want, sm_count() * 8);
     if (!blocks) return;
-    if (cfg.half_state == 2) raster_fwd_half_kernel<__nv_bfloat16><<<blocks, kThreads, 0, stream>>>(p);
-    else if (cfg.half_state) raster_fwd_half_kernel<__half><<<blocks, kThreads, 0, stream>>>(p);
-    else raster_fwd_kernel<<<blocks, kThreads, 0, stream>>>(p);
+    if (cfg.half_state == 2) sb_launch(raster_fwd_half_kernel<__nv_bfloat16>, blocks, kThreads, 0, stream, p);
+    else if (cfg.half_state) sb_launch(raster_fwd_half_kernel<__half>, blocks, kThreads, 0, stream, p);
+    else sb_launch(raster_fwd_kernel, blocks, kThreads, 0, stream, p);
 }
 
 void sb_launch_raster_bwd(const RasterRec* recs, const int32_t* offsets, const int32_t* prims, int W, int H,
@@ -737,7 +753,7 @@ void sb_launch_raster_bwd(const RasterRec* recs, const int32_t* offsets, const i
         cudaFuncSetAttribute(raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    if (blocks) raster_bwd_kernel<<<blocks, kBwdWarps * 32, smem, stream>>>(p);
+    if (blocks) sb_launch(raster_bwd_kernel, blocks, kBwdWarps * 32, smem, stream, p);
 }
 
 // ---- standalone lane reductions (reduction.py:21-58), for parity tests ----
@@ -745,6 +761,7 @@ namespace {
 __global__ void lane_reduce_kernel(const float* __restrict__ v, int groups, int mode, float* __restrict__ out_f,
                                    double* __restrict__ out_d)
 {
+    sb_pdl_begin();
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (gw >= groups) return;
@@ -773,5 +790,5 @@ void sb_launch_lane_reduce(const float* v, int groups, int mode, float* out_f, d
     if (groups <= 0) return;
     const int threads = 256;
     const int blocks = (groups * 32 + threads - 1) / threads;
-    lane_reduce_kernel<<<blocks, threads, 0, stream>>>(v, groups, mode, out_f, out_d);
+    sb_launch(lane_reduce_kernel, blocks, threads, 0, stream, v, groups, mode, out_f, out_d);
 }

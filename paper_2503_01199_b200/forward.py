@@ -15,6 +15,7 @@ per view is four calls through the C-ABI (include/splat_b200.h):
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -100,6 +101,7 @@ class RenderContext:
     last: torch.Tensor            # (H, W) int32
     n_degenerate: int = 0
     half: bool | str = False      # produced by a 16-bit blending-state path
+    token: int = 0                # owner token of the pre-zeroed sgrad workspace (0: none)
     _tiles: list | None = field(default=None, repr=False)
 
     @property
@@ -136,14 +138,25 @@ class RenderContext:
 # (device, W, H) -> (pair, super-tile entry) capacities of the binning buffers
 _bin_capacity: dict = {}
 _pinned: dict = {}
+# The backward's screen-gradient workspace ("sgrad", 64 B per compact slot)
+# is zeroed by the forward's project kernel; _sgrad_clean[device] names the
+# one context whose backward may use it without zeroing again.
+SGRAD_BYTES = 64
+_sgrad_clean: dict = {}
+_ctx_tokens = itertools.count(1)
 
 
-def _pinned_counters(dev) -> torch.Tensor:
-    """Pinned host mirror of the counters (one per device; the forward waits
-    on its copy before returning, so it is never in flight twice)."""
+def _pinned_counters(dev):
+    """Pinned host mirror of the counters and its device address (one per
+    device; the forward reads it before returning, so it is never in flight
+    twice).  The bin scan kernel writes it directly when the buffer is
+    mapped (address not None); otherwise it is filled by a copy."""
     key = str(dev)
     if key not in _pinned:
-        _pinned[key] = torch.empty(8, dtype=torch.int32, pin_memory=True)
+        host = torch.zeros(8, dtype=torch.int32, pin_memory=True)
+        addr = C.c_void_p()
+        rc = _lib.load().sb_host_mapped_pointer(C.c_void_p(host.data_ptr()), C.byref(addr))
+        _pinned[key] = (host, addr if rc == 0 and addr.value else None)
     return _pinned[key]
 
 
@@ -159,7 +172,7 @@ def _half_mode(half) -> int:
     raise ValueError(f"half must be False, True, 'fp16' or 'bf16', not {half!r}")
 
 
-def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, half):
+def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, half, zero_sgrad=True):
     _lib.require_cuda(scene.data)
     dev = scene.device
     n = scene.n
@@ -175,16 +188,20 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     cmap = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     coff = torch.empty(max(K, 1), dtype=torch.int32, device=dev)
     cvis = torch.empty(max(K, 1), dtype=torch.uint8, device=dev)   # written for every cluster
-    counters = torch.zeros(8, dtype=torch.int32, device=dev)   # vis, N_c, ndeg, pad, P, E
+    counters = torch.empty(8, dtype=torch.int32, device=dev)   # vis, N_c, ndeg, 0 (project); P, E (bin)
     lib = _lib.load()
     tile_offsets = torch.empty(ntiles + 1, dtype=torch.int32, device=dev)
     ws = _lib.workspace("project", lib.sb_project_workspace_bytes(n), dev)
+    sgrad = _lib.workspace("sgrad", max(n, 1) * SGRAD_BYTES, dev) if zero_sgrad else None
+    _sgrad_clean.pop(str(dev), None)
     _lib.call("sb_project_cull_compact", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s), _lib.ptr(recs),
-              _lib.ptr(cmap), _lib.ptr(coff), _lib.ptr(cvis), _lib.ptr(counters), _lib.ptr(ws), ws.numel(),
-              stream)
-    state = _lib.workspace("bin_state", lib.sb_bin_state_workspace_bytes(n, ntiles), dev)
+              _lib.ptr(cmap), _lib.ptr(coff), _lib.ptr(cvis), _lib.ptr(counters),
+              _lib.ptr(sgrad) if sgrad is not None else None, _lib.ptr(ws), ws.numel(), stream)
+    # one zero-initialised state per tile grid (its count arrays stay zeroed)
+    state = _lib.workspace(f"bin_state_{tx_n}x{ty_n}", lib.sb_bin_state_workspace_bytes(n, ntiles), dev)
+    host, mirror = _pinned_counters(dev)
     _lib.call("sb_bin_prepare", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), _lib.ptr(tile_offsets),
-              _lib.ptr(counters[4:]), _lib.ptr(state), state.numel(), stream)
+              _lib.ptr(counters[4:]), mirror, _lib.ptr(state), state.numel(), stream)
     # Binning part 2 is launched before the host knows P and E, with the
     # capacities of earlier views of this resolution; the one device-to-host
     # read below then overlaps it, and it is re-launched only if they were
@@ -199,8 +216,8 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
                   _lib.ptr(tile_offsets), _lib.ptr(state), _lib.ptr(prims), _lib.ptr(ws_f), ws_f.numel(), stream)
         return prims
 
-    host = _pinned_counters(dev)
-    host.copy_(counters, non_blocking=True)           # queued before part 2
+    if mirror is None:
+        host.copy_(counters, non_blocking=True)       # queued before part 2
     ready = torch.cuda.Event()
     ready.record()
     prims = finish(p_cap, e_cap) if p_cap else None
@@ -226,6 +243,9 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
                         compact_map_full=cmap, cluster_offset=coff[:K], cluster_vis=cvis[:K],
                         tile_offsets=tile_offsets, tile_prims=prims[:P], transmittance=T, last=last,
                         n_degenerate=ndeg, half=half)
+    if sgrad is not None:
+        ctx.token = next(_ctx_tokens)
+        _sgrad_clean[str(dev)] = ctx.token
     return out, ctx
 
 
@@ -244,4 +264,6 @@ def forward(scene: SceneSoA, camera, config: RasterConfig | None = None, counter
 
 
 def render(scene: SceneSoA, camera, config: RasterConfig | None = None) -> RenderOutput:
-    return forward(scene, camera, config)[0]
+    """forward.py:307-308 (no backward follows: the sgrad rows are left alone)."""
+    return _launch_forward(scene, CameraView.from_any(camera), config or RasterConfig(), False,
+                           zero_sgrad=False)[0]

@@ -116,10 +116,11 @@ def loss_and_grad(rendered: torch.Tensor, target, lam: float, return_tensor: boo
     else:
         y = y.float().contiguous()
     grad = torch.empty_like(x)
-    acc = torch.empty(3, dtype=torch.float64, device=x.device)
+    acc = _lib.workspace("loss_accum", 16, x.device)       # zeroed once, left zeroed by the call
+    out = torch.empty(1, dtype=torch.float64, device=x.device)
     _lib.call("sb_loss_fwd_bwd", _lib.ptr(x), _lib.ptr(y), _lib.ptr(y8), W, H, float(lam), _lib.ptr(grad),
-              _lib.ptr(acc), _lib.ptr(acc[2:]), C.c_void_p(_lib.stream_ptr(x.device)))
-    loss = acc[2]
+              _lib.ptr(acc), _lib.ptr(out), C.c_void_p(_lib.stream_ptr(x.device)))
+    loss = out[0]
     return (loss if return_tensor else float(loss)), grad
 
 

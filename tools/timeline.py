@@ -39,13 +39,19 @@ ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUD
 ev.sort(key=lambda e: e.time_range.start)
 # last step only: from the last projection kernel on
 starts = [i for i, e in enumerate(ev) if "project_cull" in e.name]
+period = ev[starts[-1]].time_range.start - ev[starts[-2]].time_range.start
 ev = ev[starts[-2]:starts[-1]]
 prev_end = None
 idle = 0.0
+# with programmatic dependent launch a kernel's CTAs may start before its
+# predecessor ends (negative gap); "own" is the time it adds after that end
+print("    gap       own      span")
 for e in ev:
     s, d = e.time_range.start, e.time_range.elapsed_us()
     gap = 0.0 if prev_end is None else s - prev_end
     idle += max(gap, 0.0)
-    print(f"gap {gap:7.1f}  {d:8.1f} us  {e.name[:90]}")
-    prev_end = s + d
+    own = d if prev_end is None else s + d - max(s, prev_end)
+    print(f"gap {gap:7.1f}  {own:8.1f}  {d:8.1f} us  {e.name[:90]}")
+    prev_end = max(s + d, prev_end or 0.0)
 print(f"total idle between operations: {idle:.1f} us")
+print(f"step period (projection to projection): {period:.1f} us")
