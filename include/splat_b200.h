@@ -90,7 +90,10 @@ int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam
 
 /* tiles.py:50-107 binning, part 1: enumerate the exact disc/rect hits
  * (tiles.py:75-91), count them per tile and scan the counts ->
- * tile_offsets[ntiles + 1]; totals[0] (device int) receives P, totals[1]
+ * tile_offsets[0 .. ntiles] (the reference's offsets), followed by
+ * tile_offsets[ntiles + 1 .. 2 ntiles]: the raster schedule, tile ids
+ * longest list first (the buffer holds 2 ntiles + 1 int32; sb_raster_fwd /
+ * sb_raster_bwd take the whole of it).  totals[0] (device int) receives P, totals[1]
  * the number E of (primitive, 4x4-tile super-tile) entries.  The per-row hit
  * spans and the super-tile offsets are kept in `state`
  * (sb_bin_state_workspace_bytes(n_cap, ntiles) bytes, caller-owned) for
@@ -119,7 +122,9 @@ int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, cons
                   int64_t n_entries, const int32_t* tile_offsets, const void* state, int32_t* tile_prims, void* ws,
                   size_t ws_bytes, sb_stream_t stream);
 
-/* forward.py:161-191 + 240-255: color (H,W,3), transmittance (H,W),
+/* tile_offsets: the 2 ntiles + 1 entries written by sb_bin_prepare (offsets,
+ * then the heavy-first schedule the tile queue follows).
+ * forward.py:161-191 + 240-255: color (H,W,3), transmittance (H,W),
  * frag_count (H,W) and last[(H,W)] = 1 + list position of each pixel's last
  * contributing fragment (consumed by the backward).  cfg->half_state = 1
  * selects the fp16 blending-state path (forward.py:194-230, half=True).

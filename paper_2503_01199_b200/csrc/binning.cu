@@ -343,6 +343,10 @@ constexpr int kStCap = kStThreads * 16;   // super-tile entries sorted in one sh
 __device__ void cta_scan(int32_t* __restrict__ cnt, int32_t* __restrict__ out, int n, int32_t* __restrict__ total,
                          int32_t* __restrict__ copy, int32_t* __restrict__ longs, uint32_t long_min)
 {
+    // Rounds of kScanThreads * kScanItems counts; warp w owns a contiguous
+    // block of 32 * kScanItems of them, read row by row (lane l of row j is
+    // item 32 j + l), so every load and store is coalesced -- this kernel
+    // runs on one SM, whose load/store queue is its bound.
     __shared__ uint32_t s_warp[kScanThreads / 32];
     __shared__ uint32_t s_carry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -352,24 +356,35 @@ __device__ void cta_scan(int32_t* __restrict__ cnt, int32_t* __restrict__ out, i
     }
     __syncthreads();
     for (int base = 0; base < n; base += kScanThreads * kScanItems) {
-        // each thread: kScanItems consecutive counts (all loads in flight)
-        const int beg = base + threadIdx.x * kScanItems;
-        uint32_t v[kScanItems], sum = 0;
+        const int wbase = base + warp * 32 * kScanItems + lane;
+        uint32_t v[kScanItems];
 #pragma unroll
         for (int j = 0; j < kScanItems; j++) {
-            v[j] = beg + j < n ? (uint32_t)cnt[beg + j] : 0u;
-            sum += v[j];
+            const int i = wbase + 32 * j;
+            v[j] = i < n ? (uint32_t)cnt[i] : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < kScanItems; j++)
-            if (beg + j < n) cnt[beg + j] = 0;
-        uint32_t x = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+        for (int j = 0; j < kScanItems; j++) {
+            const int i = wbase + 32 * j;
+            if (i < n) cnt[i] = 0;
         }
-        if (lane == 31) s_warp[warp] = x;
+        // exclusive prefix within the warp's block, row by row
+        uint32_t carry = 0;
+#pragma unroll
+        for (int j = 0; j < kScanItems; j++) {
+            uint32_t x = v[j];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            const uint32_t row_total = __shfl_sync(0xffffffffu, x, 31);
+            const uint32_t cj = v[j];
+            v[j] = carry + x - cj;     // exclusive, within the block
+            carry += row_total;
+            if (longs && cj > long_min) longs[1 + atomicAdd(&longs[0], 1)] = wbase + 32 * j;
+        }
+        if (lane == 0) s_warp[warp] = carry;
         __syncthreads();
         if (warp == 0) {
             uint32_t w = s_warp[lane];
@@ -381,15 +396,14 @@ __device__ void cta_scan(int32_t* __restrict__ cnt, int32_t* __restrict__ out, i
             s_warp[lane] = w;   // inclusive over warps
         }
         __syncthreads();
-        uint32_t run = s_carry + (warp ? s_warp[warp - 1] : 0u) + x - sum;
+        const uint32_t off = s_carry + (warp ? s_warp[warp - 1] : 0u);
 #pragma unroll
         for (int j = 0; j < kScanItems; j++) {
-            if (beg + j < n) {
-                out[beg + j] = (int32_t)run;
-                if (copy) copy[beg + j] = (int32_t)run;
+            const int i = wbase + 32 * j;
+            if (i < n) {
+                out[i] = (int32_t)(off + v[j]);
+                if (copy) copy[i] = (int32_t)(off + v[j]);
             }
-            if (longs && v[j] > long_min) longs[1 + atomicAdd(&longs[0], 1)] = beg + j;
-            run += v[j];
         }
         __syncthreads();
         if (threadIdx.x == 0) s_carry += s_warp[31];
@@ -402,6 +416,71 @@ __device__ void cta_scan(int32_t* __restrict__ cnt, int32_t* __restrict__ out, i
     __syncthreads();
 }
 
+// Heavy-first raster schedule: the tiles ordered by list length, longest
+// first (bucketed by the length's leading three bits), so the dynamic tile
+// queues of the forward and backward end on the cheapest tiles instead of
+// leaving SMs idle behind a late long tile.  Order within a bucket is
+// arbitrary (scheduling only; the outputs do not depend on it).
+SB_INLINE int sched_bucket(int c) {
+    if (c <= 0) return 0;
+    const int l = 31 - __clz(c);
+    const int frac = l >= 2 ? (c >> (l - 2)) & 3 : (c << (2 - l)) & 3;
+    return min(63, 1 + 4 * l + frac);
+}
+
+__device__ void tile_schedule(const int32_t* __restrict__ offs, int ntiles, int32_t* __restrict__ sched)
+{
+    constexpr int R = kScanItems;   // tiles per thread and round (coalesced, all loads in flight)
+    __shared__ uint32_t s_cnt[64];
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 64) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    // (a) bucket histogram, one shared atomic per (warp, distinct bucket)
+    for (int t0 = 0; t0 < ntiles; t0 += kScanThreads * R) {
+        int b[R];
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int t = t0 + r * kScanThreads + threadIdx.x;
+            b[r] = t < ntiles ? sched_bucket(offs[t + 1] - offs[t]) : -1;
+        }
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const unsigned peers = __match_any_sync(0xffffffffu, b[r]);
+            if (b[r] >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[b[r]], (uint32_t)__popc(peers));
+        }
+    }
+    __syncthreads();
+    // (b) bucket starts, heaviest bucket first
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int b = 63; b >= 0; b--) {
+            const uint32_t c = s_cnt[b];
+            s_cnt[b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    // (c) scatter the tile ids
+    for (int t0 = 0; t0 < ntiles; t0 += kScanThreads * R) {
+        int b[R];
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int t = t0 + r * kScanThreads + threadIdx.x;
+            b[r] = t < ntiles ? sched_bucket(offs[t + 1] - offs[t]) : -1;
+        }
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int t = t0 + r * kScanThreads + threadIdx.x;
+            const unsigned peers = __match_any_sync(0xffffffffu, b[r]);
+            const int leader = __ffs(peers) - 1;
+            uint32_t pos = 0;
+            if (b[r] >= 0 && lane == leader) pos = atomicAdd(&s_cnt[b[r]], (uint32_t)__popc(peers));
+            pos = __shfl_sync(0xffffffffu, pos, leader);
+            if (b[r] >= 0) sched[pos + __popc(peers & ((1u << lane) - 1u))] = t;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kScanThreads)
 tile_scan_kernel(int32_t* __restrict__ tile_cnt, int32_t* __restrict__ offsets, int ntiles,
                  int32_t* __restrict__ st_cnt, int32_t* __restrict__ st_offsets, int nst,
@@ -411,6 +490,7 @@ tile_scan_kernel(int32_t* __restrict__ tile_cnt, int32_t* __restrict__ offsets, 
     sb_pdl_begin();
     cta_scan(tile_cnt, offsets, ntiles, totals, nullptr, nullptr, 0);
     cta_scan(st_cnt, st_offsets, nst, totals + 1, cursor, st_longs, (uint32_t)kStCap);
+    tile_schedule(offsets, ntiles, offsets + ntiles + 1);
     // host-mapped copy of (vis, N_c, ndeg, 0, P, E): the host's one read
     // needs no device-to-host copy in the stream
     if (mirror && threadIdx.x < 6) mirror[threadIdx.x] = threadIdx.x < 4 ? counters[threadIdx.x] : totals[threadIdx.x - 4];

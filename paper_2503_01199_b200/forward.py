@@ -102,6 +102,7 @@ class RenderContext:
     n_degenerate: int = 0
     half: bool | str = False      # produced by a 16-bit blending-state path
     token: int = 0                # owner token of the pre-zeroed sgrad workspace (0: none)
+    tile_buffer: torch.Tensor | None = field(default=None, repr=False)   # offsets + raster schedule (2T + 1)
     _tiles: list | None = field(default=None, repr=False)
 
     @property
@@ -190,7 +191,9 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     cvis = torch.empty(max(K, 1), dtype=torch.uint8, device=dev)   # written for every cluster
     counters = torch.empty(8, dtype=torch.int32, device=dev)   # vis, N_c, ndeg, 0 (project); P, E (bin)
     lib = _lib.load()
-    tile_offsets = torch.empty(ntiles + 1, dtype=torch.int32, device=dev)
+    # offsets (T + 1) followed by the heavy-first raster schedule (T)
+    tile_buf = torch.empty(2 * ntiles + 1, dtype=torch.int32, device=dev)
+    tile_offsets = tile_buf[: ntiles + 1]
     ws = _lib.workspace("project", lib.sb_project_workspace_bytes(n), dev)
     sgrad = _lib.workspace("sgrad", max(n, 1) * SGRAD_BYTES, dev) if zero_sgrad else None
     _sgrad_clean.pop(str(dev), None)
@@ -200,7 +203,7 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     # one zero-initialised state per tile grid (its count arrays stay zeroed)
     state = _lib.workspace(f"bin_state_{tx_n}x{ty_n}", lib.sb_bin_state_workspace_bytes(n, ntiles), dev)
     host, mirror = _pinned_counters(dev)
-    _lib.call("sb_bin_prepare", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), _lib.ptr(tile_offsets),
+    _lib.call("sb_bin_prepare", _lib.ptr(recs), _lib.ptr(counters), n, C.byref(cam_s), _lib.ptr(tile_buf),
               _lib.ptr(counters[4:]), mirror, _lib.ptr(state), state.numel(), stream)
     # Binning part 2 is launched before the host knows P and E, with the
     # capacities of earlier views of this resolution; the one device-to-host
@@ -234,7 +237,7 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     frags = torch.empty((H, W), dtype=torch.int32, device=dev)
     last = torch.empty((H, W), dtype=torch.int32, device=dev)
     ws_r = _lib.workspace("raster_fwd", _lib.load().sb_raster_workspace_bytes(), dev)
-    _lib.call("sb_raster_fwd", _lib.ptr(recs), _lib.ptr(tile_offsets), _lib.ptr(prims), C.byref(cam_s),
+    _lib.call("sb_raster_fwd", _lib.ptr(recs), _lib.ptr(tile_buf), _lib.ptr(prims), C.byref(cam_s),
               C.byref(cfg_s), _lib.ptr(color), _lib.ptr(T), _lib.ptr(frags), _lib.ptr(last), _lib.ptr(ws_r),
               ws_r.numel(), stream)
     out = RenderOutput(color=color, transmittance=T, frag_count=frags)
@@ -242,6 +245,7 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
                         n_compact=nc, n_pairs=P, visible_clusters=vis, culled_clusters=K - vis, recs=recs,
                         compact_map_full=cmap, cluster_offset=coff[:K], cluster_vis=cvis[:K],
                         tile_offsets=tile_offsets, tile_prims=prims[:P], transmittance=T, last=last,
+                        tile_buffer=tile_buf,
                         n_degenerate=ndeg, half=half)
     if sgrad is not None:
         ctx.token = next(_ctx_tokens)
