@@ -8,7 +8,7 @@
 // launchers (one per kernel family)
 void sb_launch_project_cull_compact(const float*, int, const CamDev&, int, RasterRec*, int32_t*, int32_t*, uint8_t*,
                                     int32_t*, void*, unsigned long long*, unsigned int*, cudaStream_t);
-int sb_project_blocks(int n);
+int sb_project_status_words(int n);
 size_t sb_bin_state_bytes(int n_cap, int ntiles);
 void sb_launch_bin_prepare(const RasterRec*, const int32_t*, int, const CamDev&, int32_t*, int32_t*, int32_t*,
                            void*, cudaStream_t);
@@ -129,7 +129,7 @@ int sb_permute_rows(const uint32_t* perm, int64_t n, int count, const void* cons
 }
 
 size_t sb_project_workspace_bytes(int64_t n) {
-    return align256(sizeof(unsigned long long) * (sb_project_blocks((int)n) + 1) + 16);
+    return align256(sizeof(unsigned long long) * (sb_project_status_words((int)n) + 1) + 16);
 }
 
 int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
@@ -141,7 +141,7 @@ int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam
     if (n < 0 || n > INT32_MAX - 256) return fail(SB_EINVAL, "n out of range");
     if (ws_bytes < sb_project_workspace_bytes(n)) return fail(SB_EWORKSPACE, "project workspace too small");
     if (n == 0) { g_err.clear(); return SB_OK; }
-    const int blocks = sb_project_blocks((int)n);
+    const int blocks = sb_project_status_words((int)n);
     unsigned long long* status = static_cast<unsigned long long*>(ws);
     unsigned int* ticket = reinterpret_cast<unsigned int*>(status + blocks);
     const CamDev d = make_cam(cam, cfg);

@@ -10,13 +10,14 @@
 //
 // One pass over the 64-byte parameter rows (four 128-bit loads per lane per
 // Gaussian, 2 KB contiguous per warp), records staged in shared memory, the
-// compact offset of each cluster from a decoupled look-back over blocks, then
-// coalesced 128-bit stores of the 48-byte compact records.
+// compact offset of each cluster from a warp-level decoupled look-back over
+// clusters (persistent warps, clusters in ticket order), then coalesced
+// 128-bit stores of the 48-byte compact records.
 #include "common.cuh"
 
 namespace {
 
-constexpr int kWarps = 8;                      // clusters per block
+constexpr int kWarps = 8;                      // warps (concurrent clusters) per block
 constexpr int kThreads = kWarps * 32;
 
 struct WarpStage {
@@ -42,21 +43,21 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
     sb_pdl_begin();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpStage* stage = reinterpret_cast<WarpStage*>(smem_raw);
-    __shared__ int s_bid;
-    __shared__ uint32_t s_prefix;
-    __shared__ uint32_t s_warp_vis[kWarps];
-
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) s_bid = (int)atomicAdd(ticket, 1u);
-    __syncthreads();
-    const int bid = s_bid;
-    const int cl = bid * kWarps + warp;
     RasterRec* st = stage[warp].rec;
-
-    bool any_in = false;
-    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    int ndeg = 0;
-    if (cl < n_clusters) {
+    // Persistent warps draw clusters in ticket order (ticket[0]); each warp
+    // projects its cluster, culls it and finds its compact offset with a
+    // warp-level decoupled look-back over the clusters before it, so no
+    // warp waits for the rest of its CTA and the SMs stay busy to the end.
+    for (;;) {
+        int cl = 0;
+        if (lane == 0) cl = (int)atomicAdd(ticket, 1u);
+        cl = __shfl_sync(0xffffffffu, cl, 0);
+        if (cl >= n_clusters) break;
+        bool any_in = false;
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        int ndeg = 0;
+        __syncwarp();   // the previous cluster's records have been copied out
 #pragma unroll 1
         for (int j = 0; j < 4; j++) {
             const int slot = j * 32 + lane;
@@ -90,10 +91,8 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
             }
             st[slot] = r;
         }
-    }
-    // cluster visibility (p-vertex test, einsum order (c0 n0 + c2 n2) + c1 n1)
-    bool vis = false;
-    if (cl < n_clusters) {
+        // cluster visibility (p-vertex test, einsum order (c0 n0 + c2 n2) + c1 n1)
+        bool vis = true;
         const bool any_ii = __any_sync(0xffffffffu, any_in);
         if (use_culling) {
             for (int k = 0; k < 3; k++) {
@@ -110,24 +109,10 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
                 inside = inside && (dist >= 0.0);
             }
             vis = inside || any_ii;
-        } else {
-            vis = true;
         }
-        int nd = __reduce_add_sync(0xffffffffu, ndeg);
+        const int nd = __reduce_add_sync(0xffffffffu, ndeg);
         if (lane == 0 && nd) atomicAdd(ticket + 2, (unsigned)nd);
-    }
-    if (lane == 0) s_warp_vis[warp] = vis ? 1u : 0u;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t agg = 0;
-        for (int w = 0; w < kWarps; w++) agg += s_warp_vis[w];
-        const uint32_t pre = sb_lookback_warp(status, bid, agg);
-        if (lane == 0) s_prefix = pre;
-    }
-    __syncthreads();
-    if (cl < n_clusters) {
-        uint32_t before = s_prefix;
-        for (int w = 0; w < warp; w++) before += s_warp_vis[w];
+        const uint32_t before = sb_lookback_warp(status, cl, vis ? 1u : 0u);
         if (lane == 0) {
             cluster_vis[cl] = vis ? 1 : 0;
             cluster_offset[cl] = vis ? (int32_t)(before * SB_CLUSTER_SIZE) : -1;
@@ -151,19 +136,17 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
         }
     }
     // The last CTA to finish publishes the counters -- visible clusters (the
-    // last block's inclusive look-back total), N_c, n_degenerate -- and
+    // last cluster's inclusive look-back total), N_c, n_degenerate -- and
     // re-zeroes the look-back workspace for the next call (no memset).
     __shared__ int s_last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) {
-        s_last = atomicAdd(ticket + 1, 1u) == gridDim.x - 1;
-    }
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket + 1, 1u) == gridDim.x - 1;
     __syncthreads();
     if (s_last) {
         __threadfence();
         if (threadIdx.x == 0) {
-            const uint32_t vis_total = (uint32_t)atomicAdd(&status[gridDim.x - 1], 0ull);
+            const uint32_t vis_total = (uint32_t)atomicAdd(&status[n_clusters - 1], 0ull);
             const int last_members = n - (n_clusters - 1) * SB_CLUSTER_SIZE;
             const bool last_vis = *reinterpret_cast<volatile uint8_t*>(cluster_vis + n_clusters - 1) != 0;
             counters[0] = (int32_t)vis_total;
@@ -173,7 +156,7 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
             atomicExch(ticket, 0u);
             atomicExch(ticket + 1, 0u);
         }
-        for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) status[i] = 0ull;
+        for (int i = threadIdx.x; i < n_clusters; i += blockDim.x) status[i] = 0ull;
     }
 }
 
@@ -185,19 +168,22 @@ void sb_launch_project_cull_compact(const float* params, int n, const CamDev& ca
                                     unsigned long long* status, unsigned int* ticket, cudaStream_t stream)
 {
     const int k = (n + SB_CLUSTER_SIZE - 1) / SB_CLUSTER_SIZE;
-    const int blocks = (k + kWarps - 1) / kWarps;
-    if (blocks == 0) return;
+    if (k == 0) return;
     const size_t smem = sizeof(WarpStage) * kWarps;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static int resident = 0;   // persistent grid: CTAs resident at once
+    if (!resident) {
         cudaFuncSetAttribute(project_cull_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, project_cull_compact_kernel, kThreads, smem);
+        resident = max(1, sms) * max(1, per_sm);
     }
-    sb_launch(project_cull_compact_kernel, blocks, kThreads, smem, stream, reinterpret_cast<const float4*>(params), n, k, cam, use_culling, rec_out, compact_map, cluster_offset,
-        cluster_vis, counters, static_cast<float4*>(sgrad_zero), status, ticket);
+    const int blocks = min(resident, (k + kWarps - 1) / kWarps);
+    sb_launch(project_cull_compact_kernel, blocks, kThreads, smem, stream, reinterpret_cast<const float4*>(params),
+              n, k, cam, use_culling, rec_out, compact_map, cluster_offset, cluster_vis, counters,
+              static_cast<float4*>(sgrad_zero), status, ticket);
 }
 
-int sb_project_blocks(int n) {
-    const int k = (n + SB_CLUSTER_SIZE - 1) / SB_CLUSTER_SIZE;
-    return (k + kWarps - 1) / kWarps;
-}
+// look-back status words (one per cluster) before the ticket words
+int sb_project_status_words(int n) { return (n + SB_CLUSTER_SIZE - 1) / SB_CLUSTER_SIZE; }
