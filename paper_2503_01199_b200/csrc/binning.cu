@@ -368,10 +368,13 @@ __device__ void cta_scan(int32_t* __restrict__ cnt, int32_t* __restrict__ out, i
             const int i = wbase + 32 * j;
             if (i < n) cnt[i] = 0;
         }
-        // exclusive prefix within the warp's block, row by row
+        // exclusive prefix within the warp's block, row by row (rows past
+        // n hold zeros; warp-uniform skip)
         uint32_t carry = 0;
+        const int wrows = min(kScanItems, max(0, (n - (base + warp * 32 * kScanItems) + 31) / 32));
 #pragma unroll
         for (int j = 0; j < kScanItems; j++) {
+            if (j >= wrows) { v[j] = carry; continue; }
             uint32_t x = v[j];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -428,56 +431,89 @@ SB_INLINE int sched_bucket(int c) {
     return min(63, 1 + 4 * l + frac);
 }
 
-__device__ void tile_schedule(const int32_t* __restrict__ offs, int ntiles, int32_t* __restrict__ sched)
-{
-    constexpr int R = kScanItems;   // tiles per thread and round (coalesced, all loads in flight)
-    __shared__ uint32_t s_cnt[64];
+// Both schedules (tiles -> raster queues, super-tiles -> sort/emit CTAs) in
+// one pass: bucket histograms, a warp-parallel prefix (heaviest bucket
+// first), then the scatter, with the buckets kept in registers when one
+// round covers the array (the common case) so each count is loaded once.
+struct SchedArr {
+    const int32_t* offs;
+    int n;
+    int32_t* out;
+};
+
+SB_INLINE void sched_load(const SchedArr& a, int t0, int (&b)[kScanItems]) {
+    const int rows = min(kScanItems, (a.n - t0 + kScanThreads - 1) / kScanThreads);
+#pragma unroll
+    for (int r = 0; r < kScanItems; r++) {
+        const int t = t0 + r * kScanThreads + (int)threadIdx.x;
+        b[r] = r < rows && t < a.n ? sched_bucket(a.offs[t + 1] - a.offs[t]) : -1;
+    }
+}
+
+SB_INLINE void sched_hist(const int (&b)[kScanItems], int rows, uint32_t* cnt) {
     const int lane = threadIdx.x & 31;
-    if (threadIdx.x < 64) s_cnt[threadIdx.x] = 0;
+#pragma unroll
+    for (int r = 0; r < kScanItems; r++) {
+        if (r >= rows) break;
+        const unsigned peers = __match_any_sync(0xffffffffu, b[r]);
+        if (b[r] >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[b[r]], (uint32_t)__popc(peers));
+    }
+}
+
+SB_INLINE void sched_scatter(const int (&b)[kScanItems], int rows, int t0, uint32_t* cnt, int32_t* out) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int r = 0; r < kScanItems; r++) {
+        if (r >= rows) break;
+        const int t = t0 + r * kScanThreads + (int)threadIdx.x;
+        const unsigned peers = __match_any_sync(0xffffffffu, b[r]);
+        const int leader = __ffs(peers) - 1;
+        uint32_t pos = 0;
+        if (b[r] >= 0 && lane == leader) pos = atomicAdd(&cnt[b[r]], (uint32_t)__popc(peers));
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        if (b[r] >= 0) out[pos + __popc(peers & ((1u << lane) - 1u))] = t;
+    }
+}
+
+__device__ void schedules(const SchedArr (&arr)[2])
+{
+    constexpr int kRound = kScanThreads * kScanItems;
+    __shared__ uint32_t s_cnt[2][64];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < 128) s_cnt[threadIdx.x >> 6][threadIdx.x & 63] = 0;
     __syncthreads();
-    // (a) bucket histogram, one shared atomic per (warp, distinct bucket)
-    for (int t0 = 0; t0 < ntiles; t0 += kScanThreads * R) {
-        int b[R];
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-            const int t = t0 + r * kScanThreads + threadIdx.x;
-            b[r] = t < ntiles ? sched_bucket(offs[t + 1] - offs[t]) : -1;
-        }
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-            const unsigned peers = __match_any_sync(0xffffffffu, b[r]);
-            if (b[r] >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[b[r]], (uint32_t)__popc(peers));
-        }
+    int b0[kScanItems], b1[kScanItems];
+    const bool single = arr[0].n <= kRound && arr[1].n <= kRound;
+    for (int t0 = 0; t0 < max(arr[0].n, arr[1].n); t0 += kRound) {
+        sched_load(arr[0], t0, b0);
+        sched_load(arr[1], t0, b1);
+        sched_hist(b0, min(kScanItems, (arr[0].n - t0 + kScanThreads - 1) / kScanThreads), s_cnt[0]);
+        sched_hist(b1, min(kScanItems, (arr[1].n - t0 + kScanThreads - 1) / kScanThreads), s_cnt[1]);
     }
     __syncthreads();
-    // (b) bucket starts, heaviest bucket first
-    if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (int b = 63; b >= 0; b--) {
-            const uint32_t c = s_cnt[b];
-            s_cnt[b] = run;
-            run += c;
+    if (warp < 2) {   // exclusive prefix over 64 buckets, descending: lane owns buckets 63 - 2l, 62 - 2l
+        uint32_t* c = s_cnt[warp];
+        const uint32_t hi = c[63 - 2 * lane], lo = c[62 - 2 * lane];
+        uint32_t x = hi + lo;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
+        const uint32_t ex = x - hi - lo;
+        c[63 - 2 * lane] = ex;
+        c[62 - 2 * lane] = ex + hi;
     }
     __syncthreads();
-    // (c) scatter the tile ids
-    for (int t0 = 0; t0 < ntiles; t0 += kScanThreads * R) {
-        int b[R];
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-            const int t = t0 + r * kScanThreads + threadIdx.x;
-            b[r] = t < ntiles ? sched_bucket(offs[t + 1] - offs[t]) : -1;
+    for (int t0 = 0; t0 < max(arr[0].n, arr[1].n); t0 += kRound) {
+        if (!single) {
+            sched_load(arr[0], t0, b0);
+            sched_load(arr[1], t0, b1);
         }
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-            const int t = t0 + r * kScanThreads + threadIdx.x;
-            const unsigned peers = __match_any_sync(0xffffffffu, b[r]);
-            const int leader = __ffs(peers) - 1;
-            uint32_t pos = 0;
-            if (b[r] >= 0 && lane == leader) pos = atomicAdd(&s_cnt[b[r]], (uint32_t)__popc(peers));
-            pos = __shfl_sync(0xffffffffu, pos, leader);
-            if (b[r] >= 0) sched[pos + __popc(peers & ((1u << lane) - 1u))] = t;
-        }
+        sched_scatter(b0, min(kScanItems, (arr[0].n - t0 + kScanThreads - 1) / kScanThreads), t0, s_cnt[0],
+                      arr[0].out);
+        sched_scatter(b1, min(kScanItems, (arr[1].n - t0 + kScanThreads - 1) / kScanThreads), t0, s_cnt[1],
+                      arr[1].out);
     }
 }
 
@@ -485,15 +521,26 @@ __global__ void __launch_bounds__(kScanThreads)
 tile_scan_kernel(int32_t* __restrict__ tile_cnt, int32_t* __restrict__ offsets, int ntiles,
                  int32_t* __restrict__ st_cnt, int32_t* __restrict__ st_offsets, int nst,
                  int32_t* __restrict__ totals, int32_t* __restrict__ st_longs, int32_t* __restrict__ cursor,
-                 const int32_t* __restrict__ counters, int32_t* __restrict__ mirror)
+                 const int32_t* __restrict__ counters, int32_t* __restrict__ mirror, int32_t* __restrict__ st_sched)
 {
     sb_pdl_begin();
-    cta_scan(tile_cnt, offsets, ntiles, totals, nullptr, nullptr, 0);
-    cta_scan(st_cnt, st_offsets, nst, totals + 1, cursor, st_longs, (uint32_t)kStCap);
-    tile_schedule(offsets, ntiles, offsets + ntiles + 1);
+    // CTA 0: tiles (offsets, raster schedule); CTA 1: super-tiles (offsets,
+    // scatter cursors, long list, sort/emit schedule) -- independent halves
+    if (blockIdx.x == 0) {
+        cta_scan(tile_cnt, offsets, ntiles, totals, nullptr, nullptr, 0);
+        const SchedArr arr[2] = {{offsets, ntiles, offsets + ntiles + 1}, {nullptr, 0, nullptr}};
+        schedules(arr);
+    } else {
+        cta_scan(st_cnt, st_offsets, nst, totals + 1, cursor, st_longs, (uint32_t)kStCap);
+        const SchedArr arr[2] = {{st_offsets, nst, st_sched}, {nullptr, 0, nullptr}};
+        schedules(arr);
+    }
     // host-mapped copy of (vis, N_c, ndeg, 0, P, E): the host's one read
     // needs no device-to-host copy in the stream
-    if (mirror && threadIdx.x < 6) mirror[threadIdx.x] = threadIdx.x < 4 ? counters[threadIdx.x] : totals[threadIdx.x - 4];
+    if (mirror) {
+        if (blockIdx.x == 0 && threadIdx.x < 5) mirror[threadIdx.x] = threadIdx.x < 4 ? counters[threadIdx.x] : totals[0];
+        if (blockIdx.x == 1 && threadIdx.x == 0) mirror[5] = totals[1];
+    }
 }
 
 // ---- finish (1): scatter keys into super-tile ranges ---------------------------
@@ -825,13 +872,13 @@ st_sort_emit_kernel(const int32_t* __restrict__ st_offsets, int st_x, unsigned l
                     const RasterRec* __restrict__ recs, const uint4* __restrict__ spans,
                     const uint32_t* __restrict__ origin, const int32_t* __restrict__ tile_offsets, int tiles_x,
                     int tiles_y, int W, int H, int32_t* __restrict__ prims, const int32_t* __restrict__ counters,
-                    int e_cap, int p_cap)
+                    int e_cap, int p_cap, const int32_t* __restrict__ st_sched)
 {
     sb_pdl_begin();
     if (counters[5] > e_cap || counters[4] > p_cap) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StSmem& sm = *reinterpret_cast<StSmem*>(smem_raw);
-    const int st = blockIdx.x;
+    const int st = st_sched[blockIdx.x];   // largest super-tile first
     const int off = st_offsets[st], E = st_offsets[st + 1] - off;
     if (E == 0 || E > kStCap) return;
     const unsigned long long* k = keys + off;
@@ -895,7 +942,8 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // bin state: tile counts (ntiles + 1) | super-tile counts (nst + 1) |
 // scatter cursors (nst) | spans (32 B per compact slot) | origin (4 B per
-// slot) | super-tile offsets (nst + 1) | long super-tile list (1 + nst).
+// slot) | super-tile offsets (nst + 1) | long super-tile list (1 + nst) |
+// super-tile schedule (nst, largest first).
 // The count arrays come first (offsets independent of n_cap): zeroed once
 // before first use, accumulated by the count kernel, re-zeroed by the scan.
 struct StateLayout {
@@ -906,10 +954,11 @@ struct StateLayout {
     uint32_t* origin;
     int32_t* st_offsets;
     int32_t* st_longs;
+    int32_t* st_sched;
 };
 inline size_t state_bytes(int n_cap, int ntiles) {
     const size_t n = (size_t)(n_cap > 0 ? n_cap : 1), t = (size_t)ntiles + 1;
-    return 5 * align256(t * 4) + align256(n * 32) + align256(n * 4);
+    return 6 * align256(t * 4) + align256(n * 32) + align256(n * 4);
 }
 inline StateLayout state_layout(void* state, int n_cap, int ntiles, int nst) {
     const size_t n = (size_t)(n_cap > 0 ? n_cap : 1);
@@ -921,7 +970,8 @@ inline StateLayout state_layout(void* state, int n_cap, int ntiles, int nst) {
     L.spans = reinterpret_cast<uint4*>(p); p += align256(n * 32);
     L.origin = reinterpret_cast<uint32_t*>(p); p += align256(n * 4);
     L.st_offsets = reinterpret_cast<int32_t*>(p); p += align256((size_t)(nst + 1) * 4);
-    L.st_longs = reinterpret_cast<int32_t*>(p);
+    L.st_longs = reinterpret_cast<int32_t*>(p); p += align256((size_t)(nst + 1) * 4);
+    L.st_sched = reinterpret_cast<int32_t*>(p);
     return L;
 }
 inline int st_dim(int tiles) { return (tiles + kST - 1) / kST; }
@@ -941,8 +991,8 @@ void sb_launch_bin_prepare(const RasterRec* recs, const int32_t* counters, int n
     if (n_cap > 0)
         sb_launch(tile_count_kernel, (n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream, recs, counters, n_cap, cam.tiles_x, cam.tiles_y, st_x, cam.W, cam.H, L.spans, L.origin, L.tile_cnt,
             L.st_cnt);
-    sb_launch(tile_scan_kernel, 1, kScanThreads, 0, stream, L.tile_cnt, tile_offsets, ntiles, L.st_cnt, L.st_offsets, nst,
-                                                     totals, L.st_longs, L.cursor, counters, mirror);
+    sb_launch(tile_scan_kernel, 2, kScanThreads, 0, stream, L.tile_cnt, tile_offsets, ntiles, L.st_cnt, L.st_offsets, nst,
+                                                     totals, L.st_longs, L.cursor, counters, mirror, L.st_sched);
 }
 
 // ---- finish --------------------------------------------------------------------
@@ -978,7 +1028,7 @@ void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_
     sb_launch(st_sort_emit_kernel, nst, kStThreads, sizeof(StSmem), stream, L.st_offsets, st_x, keys, recs, L.spans,
                                                                         L.origin, tile_offsets, cam.tiles_x,
                                                                         cam.tiles_y, cam.W, cam.H, tile_prims,
-                                                                        counters, e_cap, p_cap);
+                                                                        counters, e_cap, p_cap, L.st_sched);
     sb_launch(st_sort_emit_long_kernel, 148, kStThreads, sizeof(StSmem), stream, L.st_offsets, L.st_longs, st_x, keys, scratch, recs, L.spans, L.origin, tile_offsets, cam.tiles_x,
         cam.tiles_y, cam.W, cam.H, tile_prims, counters, e_cap, p_cap);
 }
