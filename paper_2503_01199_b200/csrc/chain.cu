@@ -181,9 +181,9 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
 // optim.py:69-98: rows of true-masked clusters, per-row step counters.
 // Four threads per row, one 16-byte column chunk each (full occupancy, four
 // independent 128-bit loads per thread).  Per row the bias corrections are
-// formed in float64 (beta^t = exp2(t log2 beta)) and folded into two scalars
-// per channel; the moment and parameter updates run in float32 on the
-// float32 state.
+// formed as -expm1(t ln beta) in float32 (~2e-7 relative) and folded into
+// two scalars per channel; the moment and parameter updates run in float32
+// on the float32 state.
 __global__ void __launch_bounds__(256)
 adam_kernel(float4* __restrict__ params, const float4* __restrict__ grads, float4* __restrict__ m,
             float4* __restrict__ v, int32_t* __restrict__ step, const uint8_t* __restrict__ cluster_mask, int n,
@@ -198,14 +198,16 @@ adam_kernel(float4* __restrict__ params, const float4* __restrict__ grads, float
     const float4 Gr = __ldg(grads + i);
     const int s = step[g] + 1;
     if (kq == 0) step[g] = s;
-    const double t = (double)s;
-    const double bc1 = 1.0 - exp2(t * -0.15200309344504997);    // log2(0.9)
-    const double bc2 = 1.0 - exp2(t * -0.0014434168696687937);  // log2(0.999)
+    // bias corrections 1 - beta^t = -expm1(t ln beta): float32 expm1 keeps
+    // them to ~2e-7 relative for every t (no cancellation at small t)
+    const float t = (float)s;
+    const float bc1 = -expm1f(t * -0.105360515657826301f);    // ln(0.9)
+    const float bc2 = -expm1f(t * -0.00100050033358353f);     // ln(0.999)
     // p -= lr * (m / bc1) / (sqrt(v / bc2) + eps) = a * m / (sqrt(v) * b + eps)
-    const float b = (float)(1.0 / sqrt(bc2));
-    const double inv1 = 1.0 / bc1;
-    const float a0 = (float)(lr0 * inv1), a1 = (float)(lr1 * inv1), a2 = (float)(lr2 * inv1);
-    const float a3 = (float)(lr3 * inv1), a4 = (float)(lr4 * inv1);
+    const float b = rsqrtf(bc2);
+    const float inv1 = 1.0f / bc1;
+    const float a0 = (float)lr0 * inv1, a1 = (float)lr1 * inv1, a2 = (float)lr2 * inv1;
+    const float a3 = (float)lr3 * inv1, a4 = (float)lr4 * inv1;
     float* pp = &P.x; const float* gg = &Gr.x; float* mm = &M.x; float* vv = &V.x;
 #pragma unroll
     for (int e = 0; e < 4; e++) {
