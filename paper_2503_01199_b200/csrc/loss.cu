@@ -64,44 +64,50 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
 #pragma unroll
     for (int k = 0; k < NT; k++) w[k] = win.w[k];
 
-    // the final phase's own x, y (4 outputs per thread), fetched now so the
-    // loads overlap the filtering
-    constexpr int ORUN = 4, ONRUN = TW / ORUN;          // 16 runs x 32 rows = 512 threads
+    constexpr int ORUN = 4, ONRUN = TW / ORUN;          // final phase: 16 runs x 32 rows = 512 threads
     const int orow = tid / ONRUN, oc0 = (tid % ONRUN) * ORUN;
-    float fx[ORUN], fy[ORUN];
-#pragma unroll
-    for (int o = 0; o < ORUN; o++) {
-        const int gy = oy + orow, gx = ox + oc0 + o;
-        fx[o] = fy[o] = 0.f;
-        if (gy < H && gx < W) {
-            const size_t idx = ((size_t)gy * W + gx) * 3 + ch;
-            fx[o] = x_img[idx];
-            fy[o] = load_y(y_img, y_u8, idx);
-        }
-    }
     // (1) stage this channel of (x, y) with a 10-pixel halo, zero outside the
-    //     image (all of a thread's loads issued before its stores)
+    //     image: warp w takes rows w, w + 16, ...; lane c of a row chunk
+    //     takes column c (all of a thread's loads issued before its stores)
     {
-        constexpr int NS = (IH * IW + kThreads - 1) / kThreads;
-        float2 v[NS];
+        constexpr int NCH = (IW + 31) / 32;               // 3 column chunks
+        constexpr int NROW = (IH + kThreads / 32 - 1) / (kThreads / 32);   // 4 rows per warp
+        const int warp = tid >> 5, lane = tid & 31;
+        float2 v[NROW][NCH];
 #pragma unroll
-        for (int j = 0; j < NS; j++) {
-            const int i = tid + j * kThreads;
-            const int r = i / IW, c = i - r * IW;
-            const int gy = oy - 2 * R + r, gx = ox - 2 * R + c;
-            v[j] = make_float2(0.f, 0.f);
-            if (i < IH * IW && gy >= 0 && gy < H && gx >= 0 && gx < W) {
-                const size_t idx = ((size_t)gy * W + gx) * 3 + ch;
-                v[j] = make_float2(x_img[idx], load_y(y_img, y_u8, idx));
+        for (int q = 0; q < NROW; q++) {
+            const int r = warp + q * (kThreads / 32);
+            const int gy = oy - 2 * R + r;
+            const bool row_ok = r < IH && gy >= 0 && gy < H;
+            const size_t rbase = (size_t)(row_ok ? gy : 0) * W;
+#pragma unroll
+            for (int k = 0; k < NCH; k++) {
+                const int gx = ox - 2 * R + 32 * k + lane;
+                v[q][k] = make_float2(0.f, 0.f);
+                if (row_ok && 32 * k + lane < IW && gx >= 0 && gx < W) {
+                    const size_t idx = (rbase + gx) * 3 + ch;
+                    v[q][k] = make_float2(x_img[idx], load_y(y_img, y_u8, idx));
+                }
             }
         }
 #pragma unroll
-        for (int j = 0; j < NS; j++) {
-            const int i = tid + j * kThreads;
-            if (i < IH * IW) (&sm.a.sxy[0][0])[i] = v[j];
+        for (int q = 0; q < NROW; q++) {
+            const int r = warp + q * (kThreads / 32);
+#pragma unroll
+            for (int k = 0; k < NCH; k++)
+                if (r < IH && 32 * k + lane < IW) sm.a.sxy[r][32 * k + lane] = v[q][k];
         }
     }
     __syncthreads();
+    // the final phase's own (x, y), read before the field buffer reuses the
+    // staged tile
+    float fx[ORUN], fy[ORUN];
+#pragma unroll
+    for (int o = 0; o < ORUN; o++) {
+        const float2 xy = sm.a.sxy[2 * R + orow][2 * R + oc0 + o];
+        fx[o] = xy.x;
+        fy[o] = xy.y;
+    }
     double s_sum = 0.0, l1_sum = 0.0;
 
     // (2) vertical moments on rows [oy-5, oy+TH+5): column c, runs of 7 rows
