@@ -108,7 +108,8 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
         fx[o] = xy.x;
         fy[o] = xy.y;
     }
-    double s_sum = 0.0, l1_sum = 0.0;
+    // per-thread partials in float32 (at most 7 / 4 terms), reduced in float64
+    float s_part = 0.0f, l1_part = 0.0f;
 
     // (2) vertical moments on rows [oy-5, oy+TH+5): column c, runs of 7 rows
     {
@@ -202,7 +203,7 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
                     g_mu = 2.f * my * dA1 - 2.f * my * dA2 + 2.f * mx * dB1 - 2.f * mx * dB2;
                     g_xy = 2.f * dA2;
                     g_xx = dB2;
-                    if (row_own && c >= R && c < R + TW) s_sum += (double)S;
+                    if (row_own && c >= R && c < R + TW) s_part += S;
                 }
                 sm.a.fl.f01[r][c] = make_float2(g_mu, g_xy);
                 sm.a.fl.f2[r][c] = g_xx;
@@ -289,11 +290,12 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
             const float diff = xv - yv;
             const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
             grad[idx] = sgn * l1_scale - ssim_scale * g_ssim;
-            l1_sum += (double)fabsf(diff);
+            l1_part += fabsf(diff);
         }
     }
     // block reduction of the two loss partials
     const int lane = tid & 31, warp = tid >> 5;
+    double s_sum = (double)s_part, l1_sum = (double)l1_part;
     for (int o = 16; o >= 1; o >>= 1) {
         s_sum += __shfl_xor_sync(0xffffffffu, s_sum, o);
         l1_sum += __shfl_xor_sync(0xffffffffu, l1_sum, o);
