@@ -447,18 +447,22 @@ SB_INLINE float rcp_approx(float x) {
 // per-lane partials (10 channels) to a warp-private shared-memory batch; a
 // full batch is reduced row-wise (one (fragment, channel) row of 32 lane
 // values per lane at a time) and flushed with one atomic per row.
-//   conic rows   [3 channels][8 slots][32 lanes], lane l at ((l + 4 (row & 7)) & 31)
-//   tree rows    [7 channels][4 slot pairs][32 lanes] float2 (slot b, slot b + 4),
-//                lane l's pair at ((l + 2 (row & 7)) & 31): one lane reduces both
-//                fragments of a pair with f32x2 adds (the same tree for each)
+//   float rows  [4][8 slots][32 lanes]: conic a b c (exponent-aligned sum)
+//               and S (tree); lane l of slot b at ((l + 4 b) & 31)
+//   pair rows   [3][8 slots][32 lanes] float2: (u v), (o r), (g bl) of one
+//               fragment; lane l of slot b at ((l + 2 b) & 31).  One 64-bit
+//               store per pair (bank-conflict free), and one lane reduces
+//               both channels of a pair with f32x2 adds, each channel in
+//               its own reference tree order.
 constexpr int kBatch = 8;
 constexpr int kConicCh = 3;        // a b c (exponent-aligned)
-constexpr int kTreeCh = 7;         // u v o r g bl S (pairwise tree)
+constexpr int kRowCh = 4;          // a b c S
+constexpr int kPairCh = 3;         // (u v) (o r) (g bl)
 
 struct BwdWarpSmem {
     SRec slab[32];
-    float conic[kConicCh * kBatch * 32];
-    float2 tree[kTreeCh * (kBatch / 2) * 32];
+    float rows[kRowCh * kBatch * 32];
+    float2 pairs[kPairCh * kBatch * 32];
     int slot[kBatch];
     int count[kBatch];
 };
@@ -500,8 +504,8 @@ SB_INLINE float row_tree(float v[32]) {
 
 static_assert(kBatch == 8, "row swizzles assume 8 slots");
 
-SB_INLINE void load_conic_row(const BwdWarpSmem& ws, int row, float v[32]) {
-    const float* base = ws.conic + row * 32;
+SB_INLINE void load_row(const BwdWarpSmem& ws, int row, float v[32]) {
+    const float* base = ws.rows + row * 32;
 #pragma unroll
     for (int q = 0; q < 8; q++) {
         const float4 x = *reinterpret_cast<const float4*>(base + 4 * ((q + (row & 7)) & 7));
@@ -509,8 +513,8 @@ SB_INLINE void load_conic_row(const BwdWarpSmem& ws, int row, float v[32]) {
     }
 }
 
-SB_INLINE void load_tree_row(const BwdWarpSmem& ws, int row, float2 v[32]) {
-    const float2* base = ws.tree + row * 32;
+SB_INLINE void load_pair_row(const BwdWarpSmem& ws, int row, float2 v[32]) {
+    const float2* base = ws.pairs + row * 32;
 #pragma unroll
     for (int q = 0; q < 16; q++) {
         const float4 x = *reinterpret_cast<const float4*>(base + 2 * ((q + (row & 7)) & 15));
@@ -542,20 +546,20 @@ SB_INLINE void emit(const BwdWarpSmem& ws, int c, int b, float out, sb_screen_gr
 
 SB_INLINE void flush_batch(BwdWarpSmem& ws, int nb, int lane, int conic_tree, sb_screen_grad* grads) {
     __syncwarp();
-    if (lane < kConicCh * nb) {
+    if (lane < kRowCh * nb) {
         const int c = lane / nb, b = lane - c * nb;
         float v[32];
-        load_conic_row(ws, c * kBatch + b, v);
-        emit(ws, c, b, conic_tree ? row_tree(v) : row_exp_aligned(v), grads);
+        load_row(ws, c * kBatch + b, v);
+        if (c == kConicCh) emit(ws, 9, b, row_tree(v), grads);                    // S
+        else emit(ws, c, b, conic_tree ? row_tree(v) : row_exp_aligned(v), grads);
     }
-    const int npair = min(nb, kBatch / 2);
-    if (lane < kTreeCh * npair) {
-        const int c = lane / npair, pb = lane - c * npair;
+    if (lane < kPairCh * nb) {
+        const int cp = lane / nb, b = lane - cp * nb;
         float2 v[32];
-        load_tree_row(ws, c * (kBatch / 2) + pb, v);
+        load_pair_row(ws, cp * kBatch + b, v);
         const float2 out = row_tree2(v);
-        emit(ws, kConicCh + c, pb, out.x, grads);
-        if (pb + kBatch / 2 < nb) emit(ws, kConicCh + c, pb + kBatch / 2, out.y, grads);
+        emit(ws, kConicCh + 2 * cp, b, out.x, grads);
+        emit(ws, kConicCh + 2 * cp + 1, b, out.y, grads);
     }
     __syncwarp();
 }
@@ -607,7 +611,7 @@ raster_bwd_kernel(BwdParams p)
         const int kmax = __reduce_max_sync(0xffffffffu, lane_max);
         Prefetch pf;
         if (kmax > 0) prefetch_chunk(pf, p.recs, p.prims, beg, max(0, kmax - 32), kmax - max(0, kmax - 32), lane);
-        int nb = 0, pc_off = lane, pt_off = 2 * lane;
+        int nb = 0, pc_off = lane, pp_off = lane;
         for (int k1 = kmax; k1 > 0; k1 -= 32) {
             const int k0 = max(0, k1 - 32), cnt = k1 - k0;
             __syncwarp();
@@ -668,35 +672,35 @@ raster_bwd_kernel(BwdParams p)
                 // da = gb (-dx^2/2); db = dx t1; dc = dy (gl - gb dy / 2) - gq / 2;
                 // du = b t1 - a t2; dv = c t1 - b t2 with t1 = gl - gb dy, t2 = gb dx
                 const float t1 = fmaf(-gb, dy, gl), t2 = gb * dx;
-                float* pc = ws.conic + pc_off;                                      // conic c at pc[c * 256]
+                float* pc = ws.rows + pc_off;                                       // row c at pc[c * 256]
                 pc[0 * 256] = -0.5f * (t2 * dx);
                 pc[1 * 256] = dx * t1;
                 pc[2 * 256] = fmaf(dy, fmaf(-0.5f * gb, dy, gl), -0.5f * gq);
-                float* pt = reinterpret_cast<float*>(ws.tree) + pt_off;
-                pt[0 * 256] = fmaf(r.b, t1, -r.a * t2);                           // tree c at pt[c * 256]
-                pt[1 * 256] = fmaf(r.c, t1, -r.b * t2);
-                pt[2 * 256] = gb * r.inv_o;
+                pc[3 * 256] = (q2.x + q2.y) * (r.inv_o * r.inv_o);                   // S
+                float rgb[3];
 #pragma unroll
                 for (int ch = 0; ch < 3; ch++) {
                     const float2 t = __ffma2_rn(w2[1], dI2[1][ch], __fmul2_rn(w2[0], dI2[0][ch]));
-                    pt[(3 + ch) * 256] = t.x + t.y;
+                    rgb[ch] = t.x + t.y;
                 }
-                pt[6 * 256] = (q2.x + q2.y) * (r.inv_o * r.inv_o);
+                float2* pp = ws.pairs + pp_off;                                      // pair row c at pp[c * 256]
+                pp[0 * 256] = make_float2(fmaf(r.b, t1, -r.a * t2), fmaf(r.c, t1, -r.b * t2));   // u v
+                pp[1 * 256] = make_float2(gb * r.inv_o, rgb[0]);                               // o r
+                pp[2 * 256] = make_float2(rgb[1], rgb[2]);                                     // g bl
                 const int C = __reduce_add_sync(0xffffffffu, __popc(cmask));
                 if (lane == 0) {
                     ws.slot[nb] = r.slot;
                     ws.count[nb] = C;
                 }
-                // next slot: conic row nb * 32, lane rotated by 4 nb; tree pair row
-                // (nb & 3) * 32 (lane rotated by 2 (nb & 3)), component nb >> 2
+                // next slot nb: float rows rotated by 4 nb, pair rows by 2 nb
                 ++nb;
                 pc_off = nb * 32 + ((lane + 4 * nb) & 31);
-                pt_off = 2 * ((nb & 3) * 32 + ((lane + 2 * (nb & 3)) & 31)) + (nb >> 2);
+                pp_off = nb * 32 + ((lane + 2 * nb) & 31);
                 if (nb == kBatch) {
                     flush_batch(ws, nb, lane, p.conic_tree, p.grads);
                     nb = 0;
                     pc_off = lane;
-                    pt_off = 2 * lane;
+                    pp_off = lane;
                 }
             }
         }
