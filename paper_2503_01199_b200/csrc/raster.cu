@@ -77,14 +77,38 @@ SB_INLINE void prefetch_chunk(Prefetch& pf, const RasterRec* __restrict__ recs, 
 constexpr float kHalfLog2e = -0.72134752044448170f;   // -log2(e) / 2
 constexpr float kLog2e = -1.44269504088896341f;       // -log2(e)
 
+// The 16-byte chunks of record l sit XOR-swizzled by (l >> 1) & 3, so the
+// 32 lanes' 128-bit stores in commit_chunk (64-byte record stride) hit every
+// bank group of a quarter warp once instead of four times.
+// (The backward, bound by shared memory, uses it; the issue-bound forwards
+// keep the plain layout, whose 3 extra wavefronts per chunk cost less than
+// the swizzle arithmetic per fragment.)
+template <bool kSwz>
+SB_INLINE int slab_swizzle(int l) { return kSwz ? (l >> 1) & 3 : 0; }
+
+template <bool kSwz>
+SB_INLINE SRec slab_get(const SRec* slab, int j) {
+    const float4* b = reinterpret_cast<const float4*>(slab + j);
+    const int sw = slab_swizzle<kSwz>(j);
+    const float4 c0 = b[0 ^ sw], c1 = b[1 ^ sw], c2 = b[2 ^ sw], c3 = b[3 ^ sw];
+    SRec r;
+    r.x = c0.x; r.y = c0.y; r.A = c0.z; r.B = c0.w;
+    r.Cq = c1.x; r.o = c1.y; r.r = c1.z; r.g = c1.w;
+    r.bl = c2.x; r.lg2o = c2.y; r.inv_o = c2.z; r.pad = c2.w;
+    r.a = c3.x; r.b = c3.y; r.c = c3.z; r.slot = __float_as_int(c3.w);
+    return r;
+}
+
+template <bool kSwz>
 SB_INLINE void commit_chunk(SRec* slab, const Prefetch& pf, int cnt, int lane) {
     if (lane < cnt) {
         const float A = kHalfLog2e * pf.a.z, B = kLog2e * pf.a.w, Cq = kHalfLog2e * pf.b.x;
         float4* d = reinterpret_cast<float4*>(slab + lane);
-        d[0] = make_float4(pf.a.x, pf.a.y, A, B);
-        d[1] = make_float4(Cq, pf.b.y, pf.b.z, pf.b.w);
-        d[2] = make_float4(pf.bl, __log2f(pf.b.y), 1.0f / pf.b.y, 0.f);
-        d[3] = make_float4(pf.a.z, pf.a.w, pf.b.x, __int_as_float(pf.slot));
+        const int sw = slab_swizzle<kSwz>(lane);
+        d[0 ^ sw] = make_float4(pf.a.x, pf.a.y, A, B);
+        d[1 ^ sw] = make_float4(Cq, pf.b.y, pf.b.z, pf.b.w);
+        d[2 ^ sw] = make_float4(pf.bl, __log2f(pf.b.y), 1.0f / pf.b.y, 0.f);
+        d[3 ^ sw] = make_float4(pf.a.z, pf.a.w, pf.b.x, __int_as_float(pf.slot));
     }
 }
 
@@ -224,7 +248,7 @@ raster_fwd_kernel(FwdParams p)
         for (int k0 = 0; k0 < n && !done; k0 += 32) {
             const int cnt = min(32, n - k0);
             __syncwarp();
-            commit_chunk(slab, pf, cnt, lane);
+            commit_chunk<false>(slab, pf, cnt, lane);
             unsigned todo = chunk_mask(pf, cnt, lane, x0, y0, p.W, p.H, p.amin);
             __syncwarp();
             if (k0 + 32 < n) prefetch_chunk(pf, p.recs, p.prims, beg, k0 + 32, min(32, n - k0 - 32), lane);
@@ -237,7 +261,7 @@ raster_fwd_kernel(FwdParams p)
                     break;
                 }
                 if (!live) continue;
-                const SRec& r = slab[j];
+                const SRec r = slab_get<false>(slab, j);
                 float araw[4], dx, dy;
                 lane_alpha_raw(r, px, py0, araw, dx, dy);
 #pragma unroll
@@ -320,7 +344,7 @@ raster_fwd_half_kernel(FwdParams p)
         for (int k0 = 0; k0 < n && !done; k0 += 32) {
             const int cnt = min(32, n - k0);
             __syncwarp();
-            commit_chunk(slab, pf, cnt, lane);
+            commit_chunk<false>(slab, pf, cnt, lane);
             unsigned todo = chunk_mask(pf, cnt, lane, x0, y0, p.W, p.H, p.amin);
             __syncwarp();
             if (k0 + 32 < n) prefetch_chunk(pf, p.recs, p.prims, beg, k0 + 32, min(32, n - k0 - 32), lane);
@@ -335,7 +359,7 @@ raster_fwd_half_kernel(FwdParams p)
                     break;
                 }
                 if (!live) continue;
-                const SRec& r = slab[j];
+                const SRec r = slab_get<false>(slab, j);
                 float G[4], dx, dy;
                 lane_G(r, px, py0, G, dx, dy);
                 const H o = O::from(r.o);
@@ -615,7 +639,7 @@ raster_bwd_kernel(BwdParams p)
         for (int k1 = kmax; k1 > 0; k1 -= 32) {
             const int k0 = max(0, k1 - 32), cnt = k1 - k0;
             __syncwarp();
-            commit_chunk(ws.slab, pf, cnt, lane);
+            commit_chunk<true>(ws.slab, pf, cnt, lane);
             unsigned todo = chunk_mask(pf, cnt, lane, x0, y0, p.W, p.H, p.amin);
             __syncwarp();
             if (k0 > 0) prefetch_chunk(pf, p.recs, p.prims, beg, max(0, k0 - 32), k0 - max(0, k0 - 32), lane);
@@ -624,7 +648,7 @@ raster_bwd_kernel(BwdParams p)
                 todo &= ~(1u << j);
                 const int k = k0 + j;
                 if (!__any_sync(0xffffffffu, k < lane_max)) continue;
-                const SRec& r = ws.slab[j];
+                const SRec r = slab_get<true>(ws.slab, j);
                 float araw[4], dx, dy;
                 lane_alpha_raw(r, px, py0, araw, dx, dy);
                 float alpha[4];
