@@ -538,7 +538,8 @@ tile_scan_kernel(int32_t* __restrict__ tile_cnt, int32_t* __restrict__ offsets, 
     // host-mapped copy of (vis, N_c, ndeg, 0, P, E): the host's one read
     // needs no device-to-host copy in the stream
     if (mirror) {
-        if (blockIdx.x == 0 && threadIdx.x < 5) mirror[threadIdx.x] = threadIdx.x < 4 ? counters[threadIdx.x] : totals[0];
+        if (blockIdx.x == 0 && threadIdx.x < 5)
+            mirror[threadIdx.x] = threadIdx.x < 4 ? counters[threadIdx.x] : totals[0];
         if (blockIdx.x == 1 && threadIdx.x == 0) mirror[5] = totals[1];
     }
 }
@@ -765,7 +766,8 @@ SB_INLINE uint32_t entry_mask(const RasterRec* __restrict__ recs, uint32_t org, 
             if (ty < ry0 || ty > ry1) continue;
             for (int c = 0; c < kST; c++) {
                 const int tx = cx0 + c;
-                if (tx >= rx0 && tx <= rx1 && sb_disc_hits_fast(a4.x, a4.y, c4.z, tx, ty, W, H)) m |= 1u << (kST * i + c);
+                if (tx >= rx0 && tx <= rx1 && sb_disc_hits_fast(a4.x, a4.y, c4.z, tx, ty, W, H))
+                    m |= 1u << (kST * i + c);
             }
         }
     }
@@ -989,10 +991,10 @@ void sb_launch_bin_prepare(const RasterRec* recs, const int32_t* counters, int n
     const int st_x = st_dim(cam.tiles_x), nst = st_x * st_dim(cam.tiles_y);
     const StateLayout L = state_layout(state, n_cap, ntiles, nst);
     if (n_cap > 0)
-        sb_launch(tile_count_kernel, (n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream, recs, counters, n_cap, cam.tiles_x, cam.tiles_y, st_x, cam.W, cam.H, L.spans, L.origin, L.tile_cnt,
-            L.st_cnt);
-    sb_launch(tile_scan_kernel, 2, kScanThreads, 0, stream, L.tile_cnt, tile_offsets, ntiles, L.st_cnt, L.st_offsets, nst,
-                                                     totals, L.st_longs, L.cursor, counters, mirror, L.st_sched);
+        sb_launch(tile_count_kernel, (n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream, recs, counters,
+                  n_cap, cam.tiles_x, cam.tiles_y, st_x, cam.W, cam.H, L.spans, L.origin, L.tile_cnt, L.st_cnt);
+    sb_launch(tile_scan_kernel, 2, kScanThreads, 0, stream, L.tile_cnt, tile_offsets, ntiles, L.st_cnt, L.st_offsets,
+              nst, totals, L.st_longs, L.cursor, counters, mirror, L.st_sched);
 }
 
 // ---- finish --------------------------------------------------------------------
@@ -1017,7 +1019,8 @@ void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(w); w += align256((size_t)e_cap * 8);
     unsigned long long* scratch = reinterpret_cast<unsigned long long*>(w);
     int32_t* cursor = L.cursor;   // the scan's copy of the super-tile offsets
-    sb_launch(st_scatter_kernel, (n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream, recs, counters, n_cap, cam.tiles_x, cam.tiles_y, st_x, cursor, keys, e_cap, p_cap);
+    sb_launch(st_scatter_kernel, (n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream, recs, counters, n_cap,
+              cam.tiles_x, cam.tiles_y, st_x, cursor, keys, e_cap, p_cap);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(st_sort_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(StSmem));
@@ -1026,9 +1029,9 @@ void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_
         attr = true;
     }
     sb_launch(st_sort_emit_kernel, nst, kStThreads, sizeof(StSmem), stream, L.st_offsets, st_x, keys, recs, L.spans,
-                                                                        L.origin, tile_offsets, cam.tiles_x,
-                                                                        cam.tiles_y, cam.W, cam.H, tile_prims,
-                                                                        counters, e_cap, p_cap, L.st_sched);
-    sb_launch(st_sort_emit_long_kernel, 148, kStThreads, sizeof(StSmem), stream, L.st_offsets, L.st_longs, st_x, keys, scratch, recs, L.spans, L.origin, tile_offsets, cam.tiles_x,
-        cam.tiles_y, cam.W, cam.H, tile_prims, counters, e_cap, p_cap);
+              L.origin, tile_offsets, cam.tiles_x, cam.tiles_y, cam.W, cam.H, tile_prims, counters, e_cap, p_cap,
+              L.st_sched);
+    sb_launch(st_sort_emit_long_kernel, 148, kStThreads, sizeof(StSmem), stream, L.st_offsets, L.st_longs, st_x, keys,
+              scratch, recs, L.spans, L.origin, tile_offsets, cam.tiles_x, cam.tiles_y, cam.W, cam.H, tile_prims,
+              counters, e_cap, p_cap);
 }

@@ -120,7 +120,8 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
             for (int i = 0; i < 2; i++)
 #pragma unroll
                 for (int j = 0; j < 3; j++)
-                    dJ[i][j] = fma(dM[i][2], cam.Rd[3 * j + 2], fma(dM[i][1], cam.Rd[3 * j + 1], dM[i][0] * cam.Rd[3 * j]));
+                    dJ[i][j] = fma(dM[i][2], cam.Rd[3 * j + 2],
+                                   fma(dM[i][1], cam.Rd[3 * j + 1], dM[i][0] * cam.Rd[3 * j]));
             const double tx = o.t[0], ty = o.t[1], tz = o.t[2];
             const double fx = cam.fxd, fy = cam.fyd;
             const double tz2 = tz * tz, tz3 = tz * tz * tz;
@@ -246,16 +247,16 @@ void sb_launch_chain(const float* params, int n, const CamDev& cam, const int32_
 {
     if (n <= 0) return;
     sb_launch(chain_kernel, (n + 255) / 256, 256, 0, stream, reinterpret_cast<const float4*>(params), n, cam,
-                                                      cluster_offset, recs, sg, reinterpret_cast<float4*>(grads), S,
-                                                      M, C);
+              cluster_offset, recs, sg, reinterpret_cast<float4*>(grads), S, M, C);
 }
 
 void sb_launch_adam(float* params, const float* grads, float* m, float* v, int32_t* step, const uint8_t* mask,
                     int n, const double lr5[5], cudaStream_t stream)
 {
     if (n <= 0) return;
-    sb_launch(adam_kernel, (4 * n + 255) / 256, 256, 0, stream, reinterpret_cast<float4*>(params), reinterpret_cast<const float4*>(grads), reinterpret_cast<float4*>(m),
-        reinterpret_cast<float4*>(v), step, mask, n, lr5[0], lr5[1], lr5[2], lr5[3], lr5[4]);
+    sb_launch(adam_kernel, (4 * n + 255) / 256, 256, 0, stream, reinterpret_cast<float4*>(params),
+              reinterpret_cast<const float4*>(grads), reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), step,
+              mask, n, lr5[0], lr5[1], lr5[2], lr5[3], lr5[4]);
 }
 
 void sb_launch_variance(const double* S, const double* M, const int32_t* C, int n, double* out, cudaStream_t stream)

@@ -138,7 +138,8 @@ permute_kernel(const uint32_t* __restrict__ perm, int n, PermArrays a)
 }  // namespace
 
 void sb_launch_bounds(const float* params, int n, float* partial, double* lohi, cudaStream_t stream) {
-    sb_launch(bounds_partial_kernel, kBoundsBlocks, 256, 0, stream, reinterpret_cast<const float4*>(params), n, partial);
+    sb_launch(bounds_partial_kernel, kBoundsBlocks, 256, 0, stream, reinterpret_cast<const float4*>(params), n,
+              partial);
     sb_launch(bounds_final_kernel, 1, 32, 0, stream, partial, kBoundsBlocks, n, lohi);
 }
 int sb_bounds_partial_floats() { return kBoundsBlocks * 6; }
@@ -146,8 +147,8 @@ int sb_bounds_partial_floats() { return kBoundsBlocks * 6; }
 void sb_launch_morton_keys(const float* params, int n, const double* lohi, unsigned long long* keys, uint32_t* vals,
                            int* bad, cudaStream_t stream) {
     if (n <= 0) return;
-    sb_launch(morton_keys_kernel, (n + 255) / 256, 256, 0, stream, reinterpret_cast<const float4*>(params), n, lohi, keys,
-                                                            vals, bad);
+    sb_launch(morton_keys_kernel, (n + 255) / 256, 256, 0, stream, reinterpret_cast<const float4*>(params), n, lohi,
+              keys, vals, bad);
 }
 
 void sb_launch_permute(const uint32_t* perm, int n, int count, const void* const* src, void* const* dst,

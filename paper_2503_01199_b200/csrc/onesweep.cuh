@@ -262,8 +262,8 @@ int sort(K* keys, uint32_t* vals, K* k_alt, uint32_t* v_alt, const int* n_dev, i
         K* ko = flip ? keys : k_alt;
         uint32_t* vo = flip ? vals : v_alt;
         const bool last = p == passes - 1;
-        sb_launch(pass_kernel<K>, tiles, kThreads, sizeof(Smem<K>), stream, ki, (p == 0 && iota) ? nullptr : vi, (last && !keep_keys) ? nullptr : ko, vo, n_dev, n_cap,
-            8 * p, hist + 256 * p, status, ticket);
+        sb_launch(pass_kernel<K>, tiles, kThreads, sizeof(Smem<K>), stream, ki, (p == 0 && iota) ? nullptr : vi,
+                  (last && !keep_keys) ? nullptr : ko, vo, n_dev, n_cap, 8 * p, hist + 256 * p, status, ticket);
         flip ^= 1;
     }
     return flip;

@@ -180,8 +180,8 @@ void sb_launch_project_cull_compact(const float* params, int n, const CamDev& ca
         resident = max(1, sms) * max(1, per_sm);
     }
     const int blocks = min(resident, (k + kWarps - 1) / kWarps);
-    sb_launch(project_cull_compact_kernel, blocks, kThreads, smem, stream, reinterpret_cast<const float4*>(params),
-              n, k, cam, use_culling, rec_out, compact_map, cluster_offset, cluster_vis, counters,
+    sb_launch(project_cull_compact_kernel, blocks, kThreads, smem, stream, reinterpret_cast<const float4*>(params), n,
+              k, cam, use_culling, rec_out, compact_map, cluster_offset, cluster_vis, counters,
               static_cast<float4*>(sgrad_zero), status, ticket);
 }
 

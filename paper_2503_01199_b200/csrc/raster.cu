@@ -225,7 +225,8 @@ raster_fwd_kernel(FwdParams p)
     __shared__ SRec slabs[kWarpsPerBlock][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     SRec* slab = slabs[warp];
-    for (int q = next_tile(p.tile_counter, lane, p.ntiles); q < p.ntiles; q = next_tile(p.tile_counter, lane, p.ntiles)) {
+    for (int q = next_tile(p.tile_counter, lane, p.ntiles); q < p.ntiles;
+         q = next_tile(p.tile_counter, lane, p.ntiles)) {
         const int t = p.offsets[p.ntiles + 1 + q];   // heavy-first schedule (binning scan)
         const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
         const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
@@ -321,7 +322,8 @@ raster_fwd_half_kernel(FwdParams p)
     SRec* slab = slabs[warp];
     const H amin = O::from(p.amin), amax = O::from(p.amax), tstop = O::from(p.tstop);
     const H one = O::from(1.0f), zero = O::from(0.0f);
-    for (int q = next_tile(p.tile_counter, lane, p.ntiles); q < p.ntiles; q = next_tile(p.tile_counter, lane, p.ntiles)) {
+    for (int q = next_tile(p.tile_counter, lane, p.ntiles); q < p.ntiles;
+         q = next_tile(p.tile_counter, lane, p.ntiles)) {
         const int t = p.offsets[p.ntiles + 1 + q];   // heavy-first schedule (binning scan)
         const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
         const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
@@ -598,7 +600,8 @@ raster_bwd_kernel(BwdParams p)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     BwdWarpSmem& ws = reinterpret_cast<BwdWarpSmem*>(smem_raw)[warp];
-    for (int q = next_tile(p.tile_counter, lane, p.ntiles); q < p.ntiles; q = next_tile(p.tile_counter, lane, p.ntiles)) {
+    for (int q = next_tile(p.tile_counter, lane, p.ntiles); q < p.ntiles;
+         q = next_tile(p.tile_counter, lane, p.ntiles)) {
         const int t = p.offsets[p.ntiles + 1 + q];   // heavy-first schedule (binning scan)
         const int beg = p.offsets[t];
         if (p.offsets[t + 1] == beg) continue;
