@@ -112,6 +112,12 @@ SB_INLINE void commit_chunk(SRec* slab, const Prefetch& pf, int cnt, int lane) {
     }
 }
 
+SB_INLINE float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Can the record reach alpha >= alpha_min at any pixel centre of the tile?
 // The minimum of the (positive-definite) quadratic form Q over the centre
 // rectangle [X0, X1] x [Y0, Y1] is 0 if the mean is inside, else the least of
@@ -119,34 +125,38 @@ SB_INLINE void commit_chunk(SRec* slab, const Prefetch& pf, int cnt, int lane) {
 // alpha = min(o G, alpha_max) >= alpha_min needs -Q/2 >= ln(alpha_min / o);
 // the 1e-3 (log2 units) slack covers the rounding of e and of ex2.  A NaN
 // anywhere keeps the record.
-SB_INLINE bool can_contribute(const Prefetch& pf, float X0, float X1, float Y0, float Y1, float amin) {
+// The edge minimisers use MUFU reciprocals: Q is stationary at its minimum
+// along an edge, so their ulp-level error moves Q only at second order, far
+// inside the slack.  log2 o is the one commit_chunk stages.
+SB_INLINE bool can_contribute(const Prefetch& pf, float X0, float X1, float Y0, float Y1, float lg2_amin) {
     const float mx = pf.a.x, my = pf.a.y, a = pf.a.z, b = pf.a.w, c = pf.b.x, o = pf.b.y;
     float q = 0.0f;
     if (!(mx >= X0 && mx <= X1 && my >= Y0 && my <= Y1)) {
         float best = INFINITY;
         const float Xs[2] = {X0, X1}, Ys[2] = {Y0, Y1};
+        const float nbc = -b * rcp_approx(c), nba = -b * rcp_approx(a);
 #pragma unroll
         for (int e = 0; e < 2; e++) {
             const float dx = mx - Xs[e];
-            const float dy = fminf(fmaxf(-b * dx / c, my - Y1), my - Y0);
+            const float dy = fminf(fmaxf(nbc * dx, my - Y1), my - Y0);
             best = fminf(best, fmaf(a * dx, dx, fmaf(2.0f * b * dx, dy, c * dy * dy)));
         }
 #pragma unroll
         for (int e = 0; e < 2; e++) {
             const float dy = my - Ys[e];
-            const float dx = fminf(fmaxf(-b * dy / a, mx - X1), mx - X0);
+            const float dx = fminf(fmaxf(nba * dy, mx - X1), mx - X0);
             best = fminf(best, fmaf(a * dx, dx, fmaf(2.0f * b * dx, dy, c * dy * dy)));
         }
         q = best;
     }
-    return !(q * 0.72134752f > __log2f(o / amin) + 1e-3f);
+    return !(q * 0.72134752f > (__log2f(o) - lg2_amin) + 1e-3f);
 }
 
 // ballot of the chunk's records that can contribute to the tile
 SB_INLINE unsigned chunk_mask(const Prefetch& pf, int cnt, int lane, int x0, int y0, int W, int H, float amin) {
     const bool keep = lane < cnt &&
                       can_contribute(pf, (float)x0, (float)min(x0 + SB_TILE_W - 1, W - 1), (float)y0,
-                                     (float)min(y0 + SB_TILE_H - 1, H - 1), amin);
+                                     (float)min(y0 + SB_TILE_H - 1, H - 1), __log2f(amin));
     return __ballot_sync(0xffffffffu, keep);
 }
 
@@ -463,11 +473,6 @@ SB_INLINE float warp_exp_aligned(float v) {
     return __double2float_rn((double)total * scale);
 }
 
-SB_INLINE float rcp_approx(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
 
 // Batched transpose for the backward: contributing fragments append their
 // per-lane partials (10 channels) to a warp-private shared-memory batch; a
