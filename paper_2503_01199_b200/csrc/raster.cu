@@ -77,6 +77,12 @@ SB_INLINE void prefetch_chunk(Prefetch& pf, const RasterRec* __restrict__ recs, 
 constexpr float kHalfLog2e = -0.72134752044448170f;   // -log2(e) / 2
 constexpr float kLog2e = -1.44269504088896341f;       // -log2(e)
 
+SB_INLINE float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // The 16-byte chunks of record l sit XOR-swizzled by (l >> 1) & 3, so the
 // 32 lanes' 128-bit stores in commit_chunk (64-byte record stride) hit every
 // bank group of a quarter warp once instead of four times.
@@ -107,16 +113,11 @@ SB_INLINE void commit_chunk(SRec* slab, const Prefetch& pf, int cnt, int lane) {
         const int sw = slab_swizzle<kSwz>(lane);
         d[0 ^ sw] = make_float4(pf.a.x, pf.a.y, A, B);
         d[1 ^ sw] = make_float4(Cq, pf.b.y, pf.b.z, pf.b.w);
-        d[2 ^ sw] = make_float4(pf.bl, __log2f(pf.b.y), 1.0f / pf.b.y, 0.f);
+        d[2 ^ sw] = make_float4(pf.bl, __log2f(pf.b.y), rcp_approx(pf.b.y), 0.f);
         d[3 ^ sw] = make_float4(pf.a.z, pf.a.w, pf.b.x, __int_as_float(pf.slot));
     }
 }
 
-SB_INLINE float rcp_approx(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
 
 // Can the record reach alpha >= alpha_min at any pixel centre of the tile?
 // The minimum of the (positive-definite) quadratic form Q over the centre
