@@ -205,7 +205,8 @@ SB_INLINE void st_rect(const Prim& q, int& sx0, int& sx1, int& sy0, int& sy1) {
 
 // CTA super-tile window = bounding box of its primitives' super-tile
 // rectangles; returns true when it fits (and is zeroed).  Whole CTA.
-SB_INLINE bool setup_st_window(WinSmem& sm, const Prim& q) {
+template <typename SM>
+SB_INLINE bool setup_st_window(SM& sm, const Prim& q) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int v[4] = {0x7fffffff, 1, 0x7fffffff, 1};
     if (q.hit) {
@@ -545,13 +546,21 @@ tile_scan_kernel(int32_t* __restrict__ tile_cnt, int32_t* __restrict__ offsets, 
 }
 
 // ---- finish (1): scatter keys into super-tile ranges ---------------------------
+// the scatter needs only the super-tile window (not the count kernel's tile
+// window and spans): a small shared footprint keeps the SM full
+struct StWinSmem {
+    int32_t scnt[kStWin];
+    int sx0, sy0, sw, sh;
+    int red[4][kBinThreads / 32];
+};
+
 __global__ void __launch_bounds__(kBinThreads)
 st_scatter_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict__ counters, int n_cap, int tiles_x,
                   int tiles_y, int st_x, int32_t* __restrict__ cursor, unsigned long long* __restrict__ keys,
                   int e_cap, int p_cap)
 {
     sb_pdl_begin();
-    __shared__ WinSmem sm;
+    __shared__ StWinSmem sm;
     if (counters[5] > e_cap || counters[4] > p_cap) return;   // buffers too small: the caller re-launches
     const int nc = min(counters[1], n_cap);
     const int s = blockIdx.x * kBinThreads + threadIdx.x;
