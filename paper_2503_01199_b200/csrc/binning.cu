@@ -44,7 +44,7 @@
 namespace {
 
 constexpr int kBinThreads = 256;
-constexpr int kWin = 6144;          // shared-memory tile counters per CTA
+constexpr int kWin = 5120;          // shared-memory tile counters per CTA (5 CTAs / SM)
 constexpr int kStWin = 1024;        // shared-memory super-tile counters per CTA
 constexpr int kSpanRows = 16;       // rows per primitive in the span format
 constexpr uint32_t kEmptySpan = 0x00ffu;   // a > b
