@@ -731,6 +731,10 @@ SB_INLINE int lower_bound_u64(const unsigned long long* src, int n, unsigned lon
 }
 
 
+constexpr int kLongBins = 2048;          // key-range histogram of a long super-tile
+constexpr int kGroup = kStCap / 2;       // group quantum: every group holds < kStCap keys
+constexpr int kMaxGroups = 128;
+
 // Shared memory of one super-tile CTA.  After the sort's rank phase the
 // bucket counters are free and hold the sorted compact slots; the ranks
 // (u16, per bucket-order position) live where the emission later keeps
@@ -740,7 +744,10 @@ struct StSmem {
     uint16_t mask[kStCap];                 // ranks, then per sorted entry: hit tiles of the super-tile
     int32_t tot[kStThreads / 32][kST * kST];
     int32_t toff[kST * kST];
+    int32_t gstart[kMaxGroups + 1];         // long path: key-range group starts
+    int32_t fallback;
     __device__ uint32_t* slots() { return sort.cnt; }   // kStCap u32 over cnt + cur
+    __device__ uint32_t* hist() { return reinterpret_cast<uint32_t*>(sort.b); }   // long path, before the sorts
 };
 static_assert(sizeof(SortSmem<kStThreads>::cnt) + sizeof(SortSmem<kStThreads>::cur) >= kStCap * 4,
               "sorted slots alias the bucket counters");
@@ -906,8 +913,15 @@ st_sort_emit_kernel(const int32_t* __restrict__ st_offsets, int st_x, unsigned l
             H, prims);
 }
 
-// super-tiles longer than one shared-memory pass (listed by the scan):
-// sorted chunks into scratch, pairwise merges, then the emission
+// super-tiles longer than one shared-memory pass (listed by the scan): a
+// one-pass sample sort.  Keys are binned by value into kLongBins linear
+// ranges (the monotone map cta_sort uses); bin b belongs to group
+// excl[b] / kGroup, so consecutive groups cover consecutive key ranges and
+// each holds at most kGroup + (largest bin) <= kStCap keys; the keys are
+// scattered into their bins' ranges of the scratch copy and every group is
+// sorted in shared memory straight back into place.  A bin above kGroup keys
+// (or more than kMaxGroups groups) falls back to sorted chunks and pairwise
+// merges.  Then the emission, as for short super-tiles.
 __global__ void __launch_bounds__(kStThreads, 2)
 st_sort_emit_long_kernel(const int32_t* __restrict__ st_offsets, const int32_t* __restrict__ longs, int st_x,
                          unsigned long long* __restrict__ keys, unsigned long long* __restrict__ scratch,
@@ -920,29 +934,111 @@ st_sort_emit_long_kernel(const int32_t* __restrict__ st_offsets, const int32_t* 
     if (counters[5] > e_cap || counters[4] > p_cap) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StSmem& sm = *reinterpret_cast<StSmem*>(smem_raw);
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kStThreads / 32;
     const int nlong = longs[0];
     for (int li = blockIdx.x; li < nlong; li += gridDim.x) {
         const int st = longs[1 + li];
         const int off = st_offsets[st], L = st_offsets[st + 1] - off;
-        unsigned long long* src = scratch + off;
-        unsigned long long* dst = keys + off;
-        for (int c0 = 0; c0 < L; c0 += kStCap) {
-            const int n = min(kStCap, L - c0);
-            cta_sort<kStThreads, 16>(sm.sort, keys + off + c0, n,
-                                     [&](int, int pos, unsigned long long k) { src[c0 + pos] = k; });
+        unsigned long long* kk = keys + off;
+        unsigned long long* sc = scratch + off;
+        // (1) key range
+        unsigned long long lo = ~0ull, hi = 0ull;
+        for (int i = tid; i < L; i += kStThreads) {
+            const unsigned long long k = kk[i];
+            lo = k < lo ? k : lo;
+            hi = k > hi ? k : hi;
         }
-        for (int width = kStCap; width < L; width *= 2) {
+        lo = warp_min_u64(lo);
+        hi = warp_max_u64(hi);
+        uint32_t* hist = sm.hist();
+        for (int b = tid; b < kLongBins; b += kStThreads) hist[b] = 0;
+        for (int g = tid; g <= kMaxGroups; g += kStThreads) sm.gstart[g] = L;
+        if (lane == 0) { sm.sort.red[0][warp] = lo; sm.sort.red[1][warp] = hi; }
+        __syncthreads();
+        lo = sm.sort.red[0][0];
+        hi = sm.sort.red[1][0];
+#pragma unroll
+        for (int w = 1; w < NW; w++) {
+            lo = sm.sort.red[0][w] < lo ? sm.sort.red[0][w] : lo;
+            hi = sm.sort.red[1][w] > hi ? sm.sort.red[1][w] : hi;
+        }
+        const float scale = (float)kLongBins / __fadd_rn(__ull2float_rn(hi - lo), 1.0f);
+        // (2) histogram
+        for (int i = tid; i < L; i += kStThreads) atomicAdd(&hist[bucket_of(kk[i], lo, scale, kLongBins)], 1u);
+        __syncthreads();
+        // (3) exclusive scan (warp 0, 64 bins per lane); a group starts at
+        // its first bin's offset (atomicMin), empty groups at the next start
+        if (warp == 0) {
+            constexpr int PB = kLongBins / 32;
+            uint32_t s = 0, mx = 0;
+            for (int q = 0; q < PB; q++) {
+                const uint32_t c = hist[lane * PB + q];
+                s += c;
+                mx = max(mx, c);
+            }
+            uint32_t x = s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            const bool bad = __any_sync(0xffffffffu, mx > (uint32_t)kGroup) || L > kMaxGroups * kGroup;
+            if (lane == 0) sm.fallback = bad ? 1 : 0;
+            uint32_t run = x - s;
+            for (int q = 0; q < PB; q++) {
+                const int b = lane * PB + q;
+                const uint32_t c = hist[b];
+                if (c && !bad) atomicMin(&sm.gstart[run / kGroup], (int)run);
+                hist[b] = run;
+                run += c;
+            }
+            __syncwarp();
+            if (lane == 0 && !bad)
+                for (int g = kMaxGroups - 1; g >= 0; g--) sm.gstart[g] = min(sm.gstart[g], sm.gstart[g + 1]);
+        }
+        __syncthreads();
+        const unsigned long long* sorted = kk;
+        if (!sm.fallback) {
+            // (4) scatter into the bins' ranges of the scratch copy
             for (int i = tid; i < L; i += kStThreads) {
-                const int run = i / width, rs = run * width, ps = (run ^ 1) * width;
-                const int pl = max(0, min(width, L - ps));
-                const unsigned long long k = src[i];
-                dst[min(rs, ps) + (i - rs) + (pl > 0 ? lower_bound_u64(src + ps, pl, k) : 0)] = k;
+                const unsigned long long k = kk[i];
+                sc[atomicAdd(&hist[bucket_of(k, lo, scale, kLongBins)], 1u)] = k;
             }
             __syncthreads();
-            unsigned long long* tmp = src; src = dst; dst = tmp;
+            // (5) each group sorted in shared memory, back into place
+            const int ng = (L + kGroup - 1) / kGroup;
+            for (int g = 0; g < ng; g++) {
+                const int g0 = sm.gstart[g], n = sm.gstart[g + 1] - g0;
+                if (n <= 0) continue;
+                unsigned long long* dst = kk + g0;
+                const auto put = [&](int, int pos, unsigned long long k) { dst[pos] = k; };
+                if (n <= 4 * kStThreads) cta_sort<kStThreads, 4>(sm.sort, sc + g0, n, put);
+                else if (n <= 8 * kStThreads) cta_sort<kStThreads, 8>(sm.sort, sc + g0, n, put);
+                else cta_sort<kStThreads, 16>(sm.sort, sc + g0, n, put);
+            }
+        } else {
+            // sorted chunks into scratch, then pairwise merges
+            unsigned long long* src = sc;
+            unsigned long long* dst = kk;
+            for (int c0 = 0; c0 < L; c0 += kStCap) {
+                const int n = min(kStCap, L - c0);
+                cta_sort<kStThreads, 16>(sm.sort, kk + c0, n,
+                                         [&](int, int pos, unsigned long long k) { src[c0 + pos] = k; });
+            }
+            for (int width = kStCap; width < L; width *= 2) {
+                for (int i = tid; i < L; i += kStThreads) {
+                    const int run = i / width, rs = run * width, ps = (run ^ 1) * width;
+                    const int pl = max(0, min(width, L - ps));
+                    const unsigned long long k = src[i];
+                    dst[min(rs, ps) + (i - rs) + (pl > 0 ? lower_bound_u64(src + ps, pl, k) : 0)] = k;
+                }
+                __syncthreads();
+                unsigned long long* tmp = src; src = dst; dst = tmp;
+            }
+            sorted = src;
         }
-        const unsigned long long* sorted = src;
+        __syncthreads();
         st_emit(sm, [&](int e) { return (uint32_t)sorted[e]; }, L, st, st_x, recs, spans, origin, tile_offsets,
                 tiles_x, tiles_y, W, H, prims);
         __syncthreads();
@@ -1040,7 +1136,7 @@ void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_
     sb_launch(st_sort_emit_kernel, nst, kStThreads, sizeof(StSmem), stream, L.st_offsets, st_x, keys, recs, L.spans,
               L.origin, tile_offsets, cam.tiles_x, cam.tiles_y, cam.W, cam.H, tile_prims, counters, e_cap, p_cap,
               L.st_sched);
-    sb_launch(st_sort_emit_long_kernel, 148, kStThreads, sizeof(StSmem), stream, L.st_offsets, L.st_longs, st_x, keys,
+    sb_launch(st_sort_emit_long_kernel, 2 * 148, kStThreads, sizeof(StSmem), stream, L.st_offsets, L.st_longs, st_x, keys,
               scratch, recs, L.spans, L.origin, tile_offsets, cam.tiles_x, cam.tiles_y, cam.W, cam.H, tile_prims,
               counters, e_cap, p_cap);
 }
