@@ -30,8 +30,12 @@
 //                from the stored spans, and a CTA-wide prefix count per tile
 //                gives every (entry, tile) its position in that tile's list
 //                -- stable by construction, so no per-tile sort.  Super-tiles
-//                longer than the shared capacity sort capacity-sized chunks
-//                and merge them in global scratch first.
+//                longer than the shared capacity (scheduled first, largest
+//                first, in the same launch) are sample-sorted: a key-range
+//                histogram splits them into groups of < capacity keys that
+//                are scattered through global scratch and sorted in shared
+//                memory one by one (chunk sorts + pairwise merges remain as
+//                the fallback for degenerate key distributions).
 // Primitives whose rectangle exceeds the span format (more than 16 tile rows
 // or 255 tile columns) take direct paths (re-enumeration, direct disc tests),
 // and so do CTAs whose windows exceed the shared counters.
@@ -885,12 +889,151 @@ __device__ void st_emit(StSmem& sm, SlotOf&& slot_of, int E, int st, int st_x, c
     }
 }
 
+// super-tiles longer than one shared-memory pass (listed by the scan): a
+// one-pass sample sort.  Keys are binned by value into kLongBins linear
+// ranges (the monotone map cta_sort uses); bin b belongs to group
+// excl[b] / kGroup, so consecutive groups cover consecutive key ranges and
+// each holds at most kGroup + (largest bin) <= kStCap keys; the keys are
+// scattered into their bins' ranges of the scratch copy and every group is
+// sorted in shared memory straight back into place.  A bin above kGroup keys
+// (or more than kMaxGroups groups) falls back to sorted chunks and pairwise
+// merges.  Then the emission, as for short super-tiles.
+__device__ void st_long(StSmem& sm, int st, int st_x, const int32_t* __restrict__ st_offsets,
+                        unsigned long long* __restrict__ keys, unsigned long long* __restrict__ scratch,
+                        const RasterRec* __restrict__ recs, const uint4* __restrict__ spans,
+                        const uint32_t* __restrict__ origin, const int32_t* __restrict__ tile_offsets, int tiles_x,
+                        int tiles_y, int W, int H, int32_t* __restrict__ prims)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kStThreads / 32;
+    const int off = st_offsets[st], L = st_offsets[st + 1] - off;
+    unsigned long long* kk = keys + off;
+    unsigned long long* sc = scratch + off;
+    // (1) key range (every pass keeps kU independent loads in flight)
+    constexpr int kU = 4;
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int i0 = tid; i0 < L; i0 += kU * kStThreads) {
+        unsigned long long k[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) k[u] = i0 + u * kStThreads < L ? kk[i0 + u * kStThreads] : kk[i0];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            lo = k[u] < lo ? k[u] : lo;
+            hi = k[u] > hi ? k[u] : hi;
+        }
+    }
+    lo = warp_min_u64(lo);
+    hi = warp_max_u64(hi);
+    uint32_t* hist = sm.hist();
+    for (int b = tid; b < kLongBins; b += kStThreads) hist[b] = 0;
+    for (int g = tid; g <= kMaxGroups; g += kStThreads) sm.gstart[g] = L;
+    if (lane == 0) { sm.sort.red[0][warp] = lo; sm.sort.red[1][warp] = hi; }
+    __syncthreads();
+    lo = sm.sort.red[0][0];
+    hi = sm.sort.red[1][0];
+#pragma unroll
+    for (int w = 1; w < NW; w++) {
+        lo = sm.sort.red[0][w] < lo ? sm.sort.red[0][w] : lo;
+        hi = sm.sort.red[1][w] > hi ? sm.sort.red[1][w] : hi;
+    }
+    const float scale = (float)kLongBins / __fadd_rn(__ull2float_rn(hi - lo), 1.0f);
+    // (2) histogram
+    for (int i0 = tid; i0 < L; i0 += kU * kStThreads) {
+        unsigned long long k[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) k[u] = i0 + u * kStThreads < L ? kk[i0 + u * kStThreads] : 0ull;
+#pragma unroll
+        for (int u = 0; u < kU; u++)
+            if (i0 + u * kStThreads < L) atomicAdd(&hist[bucket_of(k[u], lo, scale, kLongBins)], 1u);
+    }
+    __syncthreads();
+    // (3) exclusive scan (warp 0, 64 bins per lane); a group starts at
+    // its first bin's offset (atomicMin), empty groups at the next start
+    if (warp == 0) {
+        constexpr int PB = kLongBins / 32;
+        uint32_t s = 0, mx = 0;
+        for (int q = 0; q < PB; q++) {
+            const uint32_t c = hist[lane * PB + q];
+            s += c;
+            mx = max(mx, c);
+        }
+        uint32_t x = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const bool bad = __any_sync(0xffffffffu, mx > (uint32_t)kGroup) || L > kMaxGroups * kGroup;
+        if (lane == 0) sm.fallback = bad ? 1 : 0;
+        uint32_t run = x - s;
+        for (int q = 0; q < PB; q++) {
+            const int b = lane * PB + q;
+            const uint32_t c = hist[b];
+            if (c && !bad) atomicMin(&sm.gstart[run / kGroup], (int)run);
+            hist[b] = run;
+            run += c;
+        }
+        __syncwarp();
+        if (lane == 0 && !bad)
+            for (int g = kMaxGroups - 1; g >= 0; g--) sm.gstart[g] = min(sm.gstart[g], sm.gstart[g + 1]);
+    }
+    __syncthreads();
+    const unsigned long long* sorted = kk;
+    if (!sm.fallback) {
+        // (4) scatter into the bins' ranges of the scratch copy
+        for (int i0 = tid; i0 < L; i0 += kU * kStThreads) {
+            unsigned long long k[kU];
+#pragma unroll
+            for (int u = 0; u < kU; u++) k[u] = i0 + u * kStThreads < L ? kk[i0 + u * kStThreads] : 0ull;
+#pragma unroll
+            for (int u = 0; u < kU; u++)
+                if (i0 + u * kStThreads < L) sc[atomicAdd(&hist[bucket_of(k[u], lo, scale, kLongBins)], 1u)] = k[u];
+        }
+        __syncthreads();
+        // (5) each group sorted in shared memory, back into place
+        const int ng = (L + kGroup - 1) / kGroup;
+        for (int g = 0; g < ng; g++) {
+            const int g0 = sm.gstart[g], n = sm.gstart[g + 1] - g0;
+            if (n <= 0) continue;
+            unsigned long long* dst = kk + g0;
+            const auto put = [&](int, int pos, unsigned long long k) { dst[pos] = k; };
+            if (n <= 4 * kStThreads) cta_sort<kStThreads, 4>(sm.sort, sc + g0, n, put);
+            else if (n <= 8 * kStThreads) cta_sort<kStThreads, 8>(sm.sort, sc + g0, n, put);
+            else cta_sort<kStThreads, 16>(sm.sort, sc + g0, n, put);
+        }
+    } else {
+        // sorted chunks into scratch, then pairwise merges
+        unsigned long long* src = sc;
+        unsigned long long* dst = kk;
+        for (int c0 = 0; c0 < L; c0 += kStCap) {
+            const int n = min(kStCap, L - c0);
+            cta_sort<kStThreads, 16>(sm.sort, kk + c0, n,
+                                     [&](int, int pos, unsigned long long k) { src[c0 + pos] = k; });
+        }
+        for (int width = kStCap; width < L; width *= 2) {
+            for (int i = tid; i < L; i += kStThreads) {
+                const int run = i / width, rs = run * width, ps = (run ^ 1) * width;
+                const int pl = max(0, min(width, L - ps));
+                const unsigned long long k = src[i];
+                dst[min(rs, ps) + (i - rs) + (pl > 0 ? lower_bound_u64(src + ps, pl, k) : 0)] = k;
+            }
+            __syncthreads();
+            unsigned long long* tmp = src; src = dst; dst = tmp;
+        }
+        sorted = src;
+    }
+    __syncthreads();
+    __syncthreads();
+    st_emit(sm, [&](int e) { return (uint32_t)sorted[e]; }, L, st, st_x, recs, spans, origin, tile_offsets, tiles_x,
+            tiles_y, W, H, prims);
+}
+
 __global__ void __launch_bounds__(kStThreads, 2)
 st_sort_emit_kernel(const int32_t* __restrict__ st_offsets, int st_x, unsigned long long* __restrict__ keys,
                     const RasterRec* __restrict__ recs, const uint4* __restrict__ spans,
                     const uint32_t* __restrict__ origin, const int32_t* __restrict__ tile_offsets, int tiles_x,
                     int tiles_y, int W, int H, int32_t* __restrict__ prims, const int32_t* __restrict__ counters,
-                    int e_cap, int p_cap, const int32_t* __restrict__ st_sched)
+                    int e_cap, int p_cap, const int32_t* __restrict__ st_sched, unsigned long long* __restrict__ scratch)
 {
     sb_pdl_begin();
     if (counters[5] > e_cap || counters[4] > p_cap) return;
@@ -898,7 +1041,12 @@ st_sort_emit_kernel(const int32_t* __restrict__ st_offsets, int st_x, unsigned l
     StSmem& sm = *reinterpret_cast<StSmem*>(smem_raw);
     const int st = st_sched[blockIdx.x];   // largest super-tile first
     const int off = st_offsets[st], E = st_offsets[st + 1] - off;
-    if (E == 0 || E > kStCap) return;
+    if (E == 0) return;
+    if (E > kStCap) {
+        st_long(sm, st, st_x, st_offsets, keys, scratch, recs, spans, origin, tile_offsets, tiles_x, tiles_y, W, H,
+                prims);
+        return;
+    }
     const unsigned long long* k = keys + off;
     // rank of each bucket-order key -> sorted compact slots in shared memory
     uint16_t* rank = sm.mask;
@@ -911,138 +1059,6 @@ st_sort_emit_kernel(const int32_t* __restrict__ st_offsets, int st_x, unsigned l
     __syncthreads();
     st_emit(sm, [&](int e) { return slots[e]; }, E, st, st_x, recs, spans, origin, tile_offsets, tiles_x, tiles_y, W,
             H, prims);
-}
-
-// super-tiles longer than one shared-memory pass (listed by the scan): a
-// one-pass sample sort.  Keys are binned by value into kLongBins linear
-// ranges (the monotone map cta_sort uses); bin b belongs to group
-// excl[b] / kGroup, so consecutive groups cover consecutive key ranges and
-// each holds at most kGroup + (largest bin) <= kStCap keys; the keys are
-// scattered into their bins' ranges of the scratch copy and every group is
-// sorted in shared memory straight back into place.  A bin above kGroup keys
-// (or more than kMaxGroups groups) falls back to sorted chunks and pairwise
-// merges.  Then the emission, as for short super-tiles.
-__global__ void __launch_bounds__(kStThreads, 2)
-st_sort_emit_long_kernel(const int32_t* __restrict__ st_offsets, const int32_t* __restrict__ longs, int st_x,
-                         unsigned long long* __restrict__ keys, unsigned long long* __restrict__ scratch,
-                         const RasterRec* __restrict__ recs, const uint4* __restrict__ spans,
-                         const uint32_t* __restrict__ origin, const int32_t* __restrict__ tile_offsets,
-                         int tiles_x, int tiles_y, int W, int H, int32_t* __restrict__ prims,
-                         const int32_t* __restrict__ counters, int e_cap, int p_cap)
-{
-    sb_pdl_begin();
-    if (counters[5] > e_cap || counters[4] > p_cap) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    StSmem& sm = *reinterpret_cast<StSmem*>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int NW = kStThreads / 32;
-    const int nlong = longs[0];
-    for (int li = blockIdx.x; li < nlong; li += gridDim.x) {
-        const int st = longs[1 + li];
-        const int off = st_offsets[st], L = st_offsets[st + 1] - off;
-        unsigned long long* kk = keys + off;
-        unsigned long long* sc = scratch + off;
-        // (1) key range
-        unsigned long long lo = ~0ull, hi = 0ull;
-        for (int i = tid; i < L; i += kStThreads) {
-            const unsigned long long k = kk[i];
-            lo = k < lo ? k : lo;
-            hi = k > hi ? k : hi;
-        }
-        lo = warp_min_u64(lo);
-        hi = warp_max_u64(hi);
-        uint32_t* hist = sm.hist();
-        for (int b = tid; b < kLongBins; b += kStThreads) hist[b] = 0;
-        for (int g = tid; g <= kMaxGroups; g += kStThreads) sm.gstart[g] = L;
-        if (lane == 0) { sm.sort.red[0][warp] = lo; sm.sort.red[1][warp] = hi; }
-        __syncthreads();
-        lo = sm.sort.red[0][0];
-        hi = sm.sort.red[1][0];
-#pragma unroll
-        for (int w = 1; w < NW; w++) {
-            lo = sm.sort.red[0][w] < lo ? sm.sort.red[0][w] : lo;
-            hi = sm.sort.red[1][w] > hi ? sm.sort.red[1][w] : hi;
-        }
-        const float scale = (float)kLongBins / __fadd_rn(__ull2float_rn(hi - lo), 1.0f);
-        // (2) histogram
-        for (int i = tid; i < L; i += kStThreads) atomicAdd(&hist[bucket_of(kk[i], lo, scale, kLongBins)], 1u);
-        __syncthreads();
-        // (3) exclusive scan (warp 0, 64 bins per lane); a group starts at
-        // its first bin's offset (atomicMin), empty groups at the next start
-        if (warp == 0) {
-            constexpr int PB = kLongBins / 32;
-            uint32_t s = 0, mx = 0;
-            for (int q = 0; q < PB; q++) {
-                const uint32_t c = hist[lane * PB + q];
-                s += c;
-                mx = max(mx, c);
-            }
-            uint32_t x = s;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            const bool bad = __any_sync(0xffffffffu, mx > (uint32_t)kGroup) || L > kMaxGroups * kGroup;
-            if (lane == 0) sm.fallback = bad ? 1 : 0;
-            uint32_t run = x - s;
-            for (int q = 0; q < PB; q++) {
-                const int b = lane * PB + q;
-                const uint32_t c = hist[b];
-                if (c && !bad) atomicMin(&sm.gstart[run / kGroup], (int)run);
-                hist[b] = run;
-                run += c;
-            }
-            __syncwarp();
-            if (lane == 0 && !bad)
-                for (int g = kMaxGroups - 1; g >= 0; g--) sm.gstart[g] = min(sm.gstart[g], sm.gstart[g + 1]);
-        }
-        __syncthreads();
-        const unsigned long long* sorted = kk;
-        if (!sm.fallback) {
-            // (4) scatter into the bins' ranges of the scratch copy
-            for (int i = tid; i < L; i += kStThreads) {
-                const unsigned long long k = kk[i];
-                sc[atomicAdd(&hist[bucket_of(k, lo, scale, kLongBins)], 1u)] = k;
-            }
-            __syncthreads();
-            // (5) each group sorted in shared memory, back into place
-            const int ng = (L + kGroup - 1) / kGroup;
-            for (int g = 0; g < ng; g++) {
-                const int g0 = sm.gstart[g], n = sm.gstart[g + 1] - g0;
-                if (n <= 0) continue;
-                unsigned long long* dst = kk + g0;
-                const auto put = [&](int, int pos, unsigned long long k) { dst[pos] = k; };
-                if (n <= 4 * kStThreads) cta_sort<kStThreads, 4>(sm.sort, sc + g0, n, put);
-                else if (n <= 8 * kStThreads) cta_sort<kStThreads, 8>(sm.sort, sc + g0, n, put);
-                else cta_sort<kStThreads, 16>(sm.sort, sc + g0, n, put);
-            }
-        } else {
-            // sorted chunks into scratch, then pairwise merges
-            unsigned long long* src = sc;
-            unsigned long long* dst = kk;
-            for (int c0 = 0; c0 < L; c0 += kStCap) {
-                const int n = min(kStCap, L - c0);
-                cta_sort<kStThreads, 16>(sm.sort, kk + c0, n,
-                                         [&](int, int pos, unsigned long long k) { src[c0 + pos] = k; });
-            }
-            for (int width = kStCap; width < L; width *= 2) {
-                for (int i = tid; i < L; i += kStThreads) {
-                    const int run = i / width, rs = run * width, ps = (run ^ 1) * width;
-                    const int pl = max(0, min(width, L - ps));
-                    const unsigned long long k = src[i];
-                    dst[min(rs, ps) + (i - rs) + (pl > 0 ? lower_bound_u64(src + ps, pl, k) : 0)] = k;
-                }
-                __syncthreads();
-                unsigned long long* tmp = src; src = dst; dst = tmp;
-            }
-            sorted = src;
-        }
-        __syncthreads();
-        st_emit(sm, [&](int e) { return (uint32_t)sorted[e]; }, L, st, st_x, recs, spans, origin, tile_offsets,
-                tiles_x, tiles_y, W, H, prims);
-        __syncthreads();
-    }
 }
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -1129,14 +1145,9 @@ void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(st_sort_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(StSmem));
-        cudaFuncSetAttribute(st_sort_emit_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(StSmem));
         attr = true;
     }
     sb_launch(st_sort_emit_kernel, nst, kStThreads, sizeof(StSmem), stream, L.st_offsets, st_x, keys, recs, L.spans,
               L.origin, tile_offsets, cam.tiles_x, cam.tiles_y, cam.W, cam.H, tile_prims, counters, e_cap, p_cap,
-              L.st_sched);
-    sb_launch(st_sort_emit_long_kernel, 2 * 148, kStThreads, sizeof(StSmem), stream, L.st_offsets, L.st_longs, st_x, keys,
-              scratch, recs, L.spans, L.origin, tile_offsets, cam.tiles_x, cam.tiles_y, cam.W, cam.H, tile_prims,
-              counters, e_cap, p_cap);
+              L.st_sched, scratch);
 }
