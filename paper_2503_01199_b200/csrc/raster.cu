@@ -480,7 +480,7 @@ SB_INLINE float warp_exp_aligned(float v) {
 // full batch is reduced row-wise (one (fragment, channel) row of 32 lane
 // values per lane at a time) and flushed with one atomic per row.
 //   float rows  [4][8 slots][32 lanes]: conic a b c (exponent-aligned sum)
-//               and S (tree); lane l of slot b at ((l + 4 b) & 31)
+//               and S (also exponent-aligned); lane l of slot b at ((l + 4 b) & 31)
 //   pair rows   [3][8 slots][32 lanes] float2: (u v), (o r), (g bl) of one
 //               fragment; lane l of slot b at ((l + 2 b) & 31).  One 64-bit
 //               store per pair (bank-conflict free), and one lane reduces
@@ -582,8 +582,10 @@ SB_INLINE void flush_batch(BwdWarpSmem& ws, int nb, int lane, int conic_tree, sb
         const int c = lane / nb, b = lane - c * nb;
         float v[32];
         load_row(ws, c * kBatch + b, v);
-        if (c == kConicCh) emit(ws, 9, b, row_tree(v), grads);                    // S
-        else emit(ws, c, b, conic_tree ? row_tree(v) : row_exp_aligned(v), grads);
+        // S takes the conic rows' reduction (an exact sum rounded once, so no
+        // less accurate than a tree): one code path for the whole warp
+        const float out = conic_tree ? row_tree(v) : row_exp_aligned(v);
+        emit(ws, c == kConicCh ? 9 : c, b, out, grads);
     }
     if (lane < kPairCh * nb) {
         const int cp = lane / nb, b = lane - cp * nb;
