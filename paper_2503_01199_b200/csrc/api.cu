@@ -248,6 +248,7 @@ int sb_loss_fwd_bwd(const float* rendered, const float* target, const uint8_t* t
                     int32_t height, float lam, float* grad, double* accum, double* loss, sb_stream_t stream) {
     if (width <= 0 || height <= 0) return fail(SB_EINVAL, "resolution must be positive");
     if (!target && !target_u8) return fail(SB_EINVAL, "target is NULL");
+    if ((int64_t)width * height * 3 > INT32_MAX) return fail(SB_EINVAL, "image too large (H W 3 >= 2^31)");
     sb_launch_loss(rendered, target, target_u8, width, height, lam, grad, accum, loss, S(stream));
     return check_launch("sb_loss_fwd_bwd");
 }

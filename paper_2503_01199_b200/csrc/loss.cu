@@ -44,12 +44,23 @@ struct Smem {
     double red[2][kThreads / 32];
 };
 
-SB_INLINE float load_y(const float* __restrict__ y_img, const uint8_t* __restrict__ y_u8, size_t idx) {
-    return y_u8 ? (float)y_u8[idx] * (1.0f / 255.0f) : y_img[idx];
+template <bool kU8>
+SB_INLINE float load_y(const float* __restrict__ y_img, const uint8_t* __restrict__ y_u8, int idx) {
+    if (kU8) return (float)y_u8[idx] * (1.0f / 255.0f);
+    return y_img[idx];
+}
+
+SB_INLINE float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
 SB_INLINE float2 f2(float v) { return make_float2(v, v); }
 
+// kU8: the target is uint8 (value / 255) instead of float.  Element
+// indices are 32-bit (H W 3 < 2^31 is checked by the launcher).
+template <bool kU8>
 __global__ void __launch_bounds__(kThreads, 2)
 loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, const uint8_t* __restrict__ y_u8,
             int W, int H, float lam, Win win, float* __restrict__ grad, double* __restrict__ accum)
@@ -79,14 +90,14 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
             const int r = warp + q * (kThreads / 32);
             const int gy = oy - 2 * R + r;
             const bool row_ok = r < IH && gy >= 0 && gy < H;
-            const size_t rbase = (size_t)(row_ok ? gy : 0) * W;
+            const int rbase = (row_ok ? gy : 0) * W;
 #pragma unroll
             for (int k = 0; k < NCH; k++) {
                 const int gx = ox - 2 * R + 32 * k + lane;
                 v[q][k] = make_float2(0.f, 0.f);
                 if (row_ok && 32 * k + lane < IW && gx >= 0 && gx < W) {
-                    const size_t idx = (rbase + gx) * 3 + ch;
-                    v[q][k] = make_float2(x_img[idx], load_y(y_img, y_u8, idx));
+                    const int idx = (rbase + gx) * 3 + ch;
+                    v[q][k] = make_float2(x_img[idx], load_y<kU8>(y_img, y_u8, idx));
                 }
             }
         }
@@ -197,7 +208,8 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
                     const float vx = m23[o].x - mx * mx, vy = m23[o].y - my * my, cv = m4[o] - mx * my;
                     const float A1 = 2.f * mx * my + C1, A2 = 2.f * cv + C2;
                     const float B1 = mx * mx + my * my + C1, B2 = vx + vy + C2;
-                    const float iB1 = __frcp_rn(B1), iB2 = __frcp_rn(B2), iBB = iB1 * iB2;
+                    // B1 >= C1, B2 >= C2 (> 0, normal): MUFU reciprocals, <= 1 ulp
+                    const float iB1 = rcp_approx(B1), iB2 = rcp_approx(B2), iBB = iB1 * iB2;
                     const float S = (A1 * A2) * iBB;
                     const float dA1 = A2 * iBB, dA2 = A1 * iBB, dB1 = -S * iB1, dB2 = -S * iB2;
                     g_mu = 2.f * my * dA1 - 2.f * my * dA2 + 2.f * mx * dB1 - 2.f * mx * dB2;
@@ -284,7 +296,7 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
         for (int o = 0; o < RUN; o++) {
             const int gx = ox + c0 + o;
             if (gy >= H || gx >= W) continue;
-            const size_t idx = ((size_t)gy * W + gx) * 3 + ch;
+            const int idx = (gy * W + gx) * 3 + ch;
             const float xv = fx[o], yv = fy[o];
             const float g_ssim = t01[o].x + t01[o].y * yv + t2[o] * (2.f * xv);
             const float diff = xv - yv;
@@ -336,10 +348,12 @@ void sb_launch_loss(const float* x, const float* y, const uint8_t* y_u8, int W, 
     for (int k = 0; k < NT; k++) win.w[k] = (float)(ws[k] / s);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+        cudaFuncSetAttribute(loss_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+        cudaFuncSetAttribute(loss_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
         attr = true;
     }
     dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, 3);
-    sb_launch(loss_kernel, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum);
+    if (y_u8) sb_launch(loss_kernel<true>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum);
+    else sb_launch(loss_kernel<false>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum);
     sb_launch(loss_finalize_kernel, 1, 1, 0, stream, accum, W, H, lam, loss);
 }
