@@ -279,6 +279,33 @@ def test_long_tile_lists_vs_oracle(n, res):
     assert np.abs(out.color.cpu().numpy() - col).max() <= 1e-3
 
 
+def test_long_super_tile_degenerate_depths_vs_oracle():
+    """8000 identical Gaussians (one depth) plus one far behind them, all on
+    the same super-tiles: the long super-tiles' key-range histogram puts the
+    cluster into one bin above the group quantum, so the sort takes its
+    chunk-sort + merge fallback.  Tile lists bit-exact with the oracle."""
+    sb = _sb()
+    from paper_2503_01199_b200.synthetic import SyntheticSceneSpec, camera_ring
+    res = (128, 128)
+    cam = camera_ring(SyntheticSceneSpec(n_gaussians=8001, n_views=1, view_resolution=res, seed=1))[0]
+    n = 8001
+    c = np.asarray(cam.center, np.float64)
+    far = -2.0 * c / np.linalg.norm(c)          # behind the origin on the same view ray
+    arr = {"position": np.zeros((n, 3)), "log_scale": np.full((n, 3), np.log(0.05)),
+           "rotation": np.tile([1.0, 0.0, 0.0, 0.0], (n, 1)), "color": np.full((n, 3), 0.25),
+           "opacity_logit": np.full(n, -4.0)}
+    arr["position"][n // 2] = far
+    arr["color"][n // 2] = [1.0, -1.0, 0.5]
+    arr = {k: v.astype(np.float32) for k, v in arr.items()}
+    scene = sb.SceneSoA(*[arr[k] for k in G.CH], device="cuda")
+    out, ctx = sb.forward(scene, cam)
+    col, T, frags, octx = O.forward({k: np.asarray(arr[k], np.float64) for k in G.CH}, cam, O.RasterConfig())
+    assert np.diff(octx.tile_offsets).max() > 6144
+    assert np.array_equal(ctx.tile_offsets.cpu().numpy().astype(np.int64), octx.tile_offsets)
+    assert np.array_equal(ctx.tile_prims.cpu().numpy().astype(np.int64), octx.prims)
+    assert np.abs(out.color.cpu().numpy() - col).max() <= 1e-3
+
+
 @pytest.mark.parametrize("name", ["B", "C", "E"])
 def test_big_configs_bit_exact_hashes(name):
     """Configs B/C/E at full size: Morton order, projection, cull masks,
