@@ -8,7 +8,8 @@ seed 7, footprints shrunk by (N/512)^(1/3) per SURVEY 8(d)), Morton-sorted,
 1920x1080 views on the reference's camera ring.  One step = one full training
 iteration per GPU: project + cluster cull + compact + bin + per-tile sort +
 raster forward + L1/D-SSIM loss + raster backward + projection chain +
-(NCCL all-reduce of grads and statistics when N > 1) + cluster-sparse Adam.
+(one NCCL all-reduce of the gradient rows and cluster masks when N > 1;
+densification statistics stay rank-local until read) + cluster-sparse Adam.
 Each rank rasterises its own view against replicated Gaussians (weak scaling).
 
 `value`  whole-job views/s with inputs resident in HBM, device-timed with CUDA
@@ -148,7 +149,6 @@ class Trainer:
         self.ws, self.rank = ws, rank
         self.vp = ViewParallel()
         self.lrs = sb.LearningRates().at(0.0, position_scale=3.2)
-        self.stats_step = sb.DensifyStats.zeros(scene.n, scene.device)
 
     def view_index(self, it):
         return self.vp.views_for_step(it, len(self.views))[0]
@@ -158,20 +158,14 @@ class Trainer:
         cam = self.views[self.view_index(it)]
         out, ctx = sb.forward(self.scene, cam)
         loss, dI = sb.loss_and_grad(out.color, target, 0.2, return_tensor=True)
-        if self.ws > 1:
-            stats = self.stats_step
-            stats.reset()
-        else:
-            stats = sb.DensifyStats.from_scene(self.scene)
-        res = sb.backward(self.scene, ctx, dI, stats)
+        # statistics accumulate rank-locally in the scene (summed over ranks
+        # only when read: ViewParallel.reduce_stats before a densify step)
+        res = sb.backward(self.scene, ctx, dI, sb.DensifyStats.from_scene(self.scene))
         mask = res.cluster_mask
         if self.ws > 1:
-            # sum grads / stats over the views of this step, OR masks
-            mask = self.vp.reduce(res.grads.packed, stats.S, stats.M, stats.C, mask)
-            run = sb.DensifyStats.from_scene(self.scene)
-            run.S += stats.S
-            run.M += stats.M
-            run.C += stats.C
+            # sum the views' grads over ranks, OR the masks --
+            # one all-reduce of the gradient rows (mask in a padding column)
+            mask = self.vp.reduce_grads(res.grads.packed, mask)
         sb.adam_step(self.scene, res.grads, self.state, mask, self.lrs)
         return loss, ctx
 

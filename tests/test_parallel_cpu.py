@@ -28,8 +28,18 @@ def _worker(rank, world, port, out):
         C = torch.full((n,), rank + 2, dtype=torch.int32)
         mask = torch.tensor([rank == 0, rank == 1, False])
         m = vp.reduce(g, S, M, C, mask)
+        # one-collective step: mask in the padding column, stats reduced lazily
+        g2 = torch.zeros((n, 16))
+        g2[:, :14] = float(rank + 1)
+        m2 = vp.reduce_grads(g2, mask)
+        S2 = torch.arange(n, dtype=torch.float64) * (rank + 1)
+        M2 = -S2.clone()
+        C2 = torch.full((n,), rank + 2, dtype=torch.int32)
+        vp.reduce_stats(S2, M2, C2)
         out[rank] = dict(g=float(g[0, 0]), g_all=bool((g == 3.0).all()), S=float(S[10]), M=float(M[10]),
-                         C=int(C[5]), mask=m.tolist(), views=[vp.views_for_step(s, 8) for s in range(4)])
+                         C=int(C[5]), mask=m.tolist(), views=[vp.views_for_step(s, 8) for s in range(4)],
+                         g2_ok=bool((g2[:, :14] == 3.0).all()) and bool((g2[:, 14:] == 0).all()), mask2=m2.tolist(),
+                         S2=float(S2[10]), M2=float(M2[10]), C2=int(C2[5]), C2_dtype=str(C2.dtype))
     finally:
         dist.destroy_process_group()
 
@@ -45,6 +55,8 @@ def test_view_parallel_reduce_gloo():
         assert o["S"] == 30.0 and o["M"] == -30.0
         assert o["C"] == 5
         assert o["mask"] == [True, True, False]
+        assert o["g2_ok"] and o["mask2"] == [True, True, False]
+        assert o["S2"] == 30.0 and o["M2"] == -30.0 and o["C2"] == 5 and o["C2_dtype"] == "torch.int32"
     # every view of an 8-view ring is rendered exactly once per 4 steps
     seen = sorted(v for r in range(world) for step in out[r]["views"] for v in step)
     assert seen == sorted(list(range(8)))
