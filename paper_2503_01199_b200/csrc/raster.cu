@@ -572,7 +572,7 @@ SB_INLINE void emit(const BwdWarpSmem& ws, int c, int b, float out, sb_screen_gr
         if (c == 5) atomicAdd(&gr->M, (double)out);       // M = sum of dL/do over the tile
         if (c == 0) atomicAdd(&gr->C, ws.count[b]);
     } else {
-        atomicAdd(&gr->S, (double)out);
+        atomicAdd(&gr->S, (double)out * 0x1p-64);   // rows carry S * 2^64
     }
 }
 
@@ -711,7 +711,10 @@ raster_bwd_kernel(BwdParams p)
                 pc[0 * 256] = -0.5f * (t2 * dx);
                 pc[1 * 256] = dx * t1;
                 pc[2 * 256] = fmaf(dy, fmaf(-0.5f * gb, dy, gl), -0.5f * gq);
-                pc[3 * 256] = (q2.x + q2.y) * (r.inv_o * r.inv_o);                   // S
+                // S, scaled by 2^64 (exact) so the squares' rows stay off the
+                // exponent-aligned sum's two-step path for values below 2^-103
+                const float io = r.inv_o * 4294967296.0f;
+                pc[3 * 256] = (q2.x + q2.y) * (io * io);                             // S * 2^64
                 float rgb[3];
 #pragma unroll
                 for (int ch = 0; ch < 3; ch++) {
