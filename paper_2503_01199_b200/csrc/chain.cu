@@ -81,8 +81,10 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
         if (o.valid) {
             const double ga = s.a, gb = s.b, gc = s.c, gu = s.u, gv = s.v;
             const double sa = o.sa, sb = o.sb, sc = o.sc;
-            const double det = sa * sc - sb * sb;
-            const double a = sc / det, b = -sb / det, c = sa / det;
+            // one reciprocal per denominator (<= 1.5 ulp from the divisions;
+            // the chain is held to the gradient tolerance, not bit-exactness)
+            const double rdet = 1.0 / (sa * sc - sb * sb);
+            const double a = sc * rdet, b = -sb * rdet, c = sa * rdet;
             const double p00 = ga, p01 = 0.5 * gb, p11 = gc;
             const double cp00 = a * p00 + b * p01, cp01 = a * p01 + b * p11;
             const double cp10 = b * p00 + c * p01, cp11 = b * p01 + c * p11;
@@ -124,15 +126,15 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
                                    fma(dM[i][1], cam.Rd[3 * j + 1], dM[i][0] * cam.Rd[3 * j]));
             const double tx = o.t[0], ty = o.t[1], tz = o.t[2];
             const double fx = cam.fxd, fy = cam.fyd;
-            const double tz2 = tz * tz, tz3 = tz * tz * tz;
+            const double rtz = 1.0 / tz, rtz2 = rtz * rtz, rtz3 = rtz2 * rtz;
             double dt[3];
-            dt[0] = dJ[0][2] * (-fx / tz2);
-            dt[1] = dJ[1][2] * (-fy / tz2);
-            dt[2] = ((dJ[0][0] * (-fx / tz2) + dJ[1][1] * (-fy / tz2)) + dJ[0][2] * (2.0 * fx * tx / tz3)) +
-                    dJ[1][2] * (2.0 * fy * ty / tz3);
-            dt[0] += gu * fx / tz;
-            dt[1] += gv * fy / tz;
-            dt[2] += gu * (-fx * tx / tz2) + gv * (-fy * ty / tz2);
+            dt[0] = dJ[0][2] * (-fx * rtz2);
+            dt[1] = dJ[1][2] * (-fy * rtz2);
+            dt[2] = ((dJ[0][0] * (-fx * rtz2) + dJ[1][1] * (-fy * rtz2)) + dJ[0][2] * (2.0 * fx * tx * rtz3)) +
+                    dJ[1][2] * (2.0 * fy * ty * rtz3);
+            dt[0] += gu * fx * rtz;
+            dt[1] += gv * fy * rtz;
+            dt[2] += gu * (-fx * tx * rtz2) + gv * (-fy * ty * rtz2);
 #pragma unroll
             for (int j = 0; j < 3; j++)
                 out[SB_COL_POS + j] =
@@ -163,10 +165,10 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
             double dq[4];
             rotmat_grad_to_quat(dRq, q, dq);
             const double r0 = p[SB_COL_ROT], r1 = p[SB_COL_ROT + 1], r2 = p[SB_COL_ROT + 2], r3 = p[SB_COL_ROT + 3];
-            const double nrm = sqrt(((r0 * r0 + r1 * r1) + r2 * r2) + r3 * r3);
+            const double rnrm = rsqrt(((r0 * r0 + r1 * r1) + r2 * r2) + r3 * r3);
             const double proj = ((dq[0] * q[0] + dq[1] * q[1]) + dq[2] * q[2]) + dq[3] * q[3];
 #pragma unroll
-            for (int j = 0; j < 4; j++) out[SB_COL_ROT + j] = (float)((dq[j] - proj * q[j]) / nrm);
+            for (int j = 0; j < 4; j++) out[SB_COL_ROT + j] = (float)((dq[j] - proj * q[j]) * rnrm);
         }
         if (stat_S) {
             stat_S[g] = S0 + s.S;
