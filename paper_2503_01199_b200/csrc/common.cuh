@@ -97,10 +97,12 @@ struct __align__(16) RasterRec {
 };
 
 SB_INLINE double sb_sigmoid(double x) {
-    // scene.py:31-38
-    if (x >= 0) return DDIV(1.0, DADD(1.0, exp(-x)));
-    double ex = exp(x);
-    return DDIV(ex, DADD(1.0, ex));
+    // scene.py:31-38: 1 / (1 + exp(-x)) for x >= 0, exp(x) / (1 + exp(x))
+    // otherwise -- both branches are exp(-|x|) (negation is exact) and one
+    // division, so this branch-free form is bit-identical and a warp with
+    // mixed signs runs one exp and one division instead of two of each
+    const double ex = exp(-fabs(x));
+    return DDIV(x >= 0 ? 1.0 : ex, DADD(1.0, ex));
 }
 
 SB_INLINE void sb_quat_to_rotmat(double w, double x, double y, double z, double R[3][3]) {
