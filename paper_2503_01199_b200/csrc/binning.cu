@@ -765,12 +765,16 @@ SB_INLINE uint32_t entry_mask(const RasterRec* __restrict__ recs, uint32_t org, 
     const int cx0 = kST * sx, cy0 = kST * sy;
     uint32_t m = 0;
     if (!(org & kNoSpans)) {
-        const uint32_t w[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
         for (int i = 0; i < kST; i++) {
             const int k = cy0 + i - ty0;
             if (k < 0 || k >= kSpanRows) continue;
-            const uint32_t sp = (w[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+            // word k / 2 of the 8 span words by selects (a dynamically
+            // indexed register array would live in local memory)
+            const int wi = k >> 1;
+            const uint4 h = (wi & 4) ? s1 : s0;
+            const uint32_t w = (wi & 2) ? ((wi & 1) ? h.w : h.z) : ((wi & 1) ? h.y : h.x);
+            const uint32_t sp = (w >> (16 * (k & 1))) & 0xffffu;
             const int a = tx0 + (int)(sp & 0xff), b = tx0 + (int)(sp >> 8);
             const int lo = max(a, cx0), hi = min(b, cx0 + kST - 1);
             if (lo <= hi) m |= ((2u << (hi - cx0)) - (1u << (lo - cx0))) << (kST * i);
