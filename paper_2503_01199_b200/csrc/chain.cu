@@ -222,7 +222,9 @@ adam_kernel(float4* __restrict__ params, const float4* __restrict__ grads, float
         const float gr = gg[e];
         const float mn = 0.9f * mm[e] + 0.1f * gr;
         const float vn = 0.999f * vv[e] + 0.001f * gr * gr;
-        pp[e] -= a * mn / (sqrtf(vn) * b + 1e-15f);
+        // two-instruction division (<= 2 ulp): the update is ~lr, so its
+        // error stays ~1e-7 lr (the IEEE sequence cost issue slots here)
+        pp[e] -= a * __fdividef(mn, fmaf(sqrtf(vn), b, 1e-15f));
         mm[e] = mn;
         vv[e] = vn;
     }
