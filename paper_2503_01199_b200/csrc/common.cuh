@@ -234,10 +234,14 @@ SB_INLINE int sb_clip_floor(float v, int hi) {
 // Candidate tile rectangle of a footprint disc (tiles.py:70-73), float32
 SB_INLINE void sb_tile_range(float cx, float cy, float r, int txn, int tyn, int& tx0, int& tx1, int& ty0,
                              int& ty1) {
-    tx0 = sb_clip_floor(FDIV(FSUB(cx, r), (float)SB_TILE_W), txn - 1);
-    tx1 = sb_clip_floor(FDIV(FADD(cx, r), (float)SB_TILE_W), txn - 1);
-    ty0 = sb_clip_floor(FDIV(FSUB(cy, r), (float)SB_TILE_H), tyn - 1);
-    ty1 = sb_clip_floor(FDIV(FADD(cy, r), (float)SB_TILE_H), tyn - 1);
+    // the tile sizes are powers of two: v / 16 and v * 2^-4 are the same real
+    // number, so the correctly rounded product equals the quotient bit for bit
+    static_assert((SB_TILE_W & (SB_TILE_W - 1)) == 0 && (SB_TILE_H & (SB_TILE_H - 1)) == 0, "power-of-two tiles");
+    constexpr float iw = 1.0f / SB_TILE_W, ih = 1.0f / SB_TILE_H;
+    tx0 = sb_clip_floor(FMUL(FSUB(cx, r), iw), txn - 1);
+    tx1 = sb_clip_floor(FMUL(FADD(cx, r), iw), txn - 1);
+    ty0 = sb_clip_floor(FMUL(FSUB(cy, r), ih), tyn - 1);
+    ty1 = sb_clip_floor(FMUL(FADD(cy, r), ih), tyn - 1);
 }
 
 // Exact disc/rect test (tiles.py:43-47): dx, dy in float64 (int64 - float32
