@@ -93,3 +93,8 @@ class ViewParallel:
         dist.all_reduce(C, group=self.group)
         w1.wait()
         w2.wait()
+
+    def all_sum(self, t: torch.Tensor):
+        """In place sum over ranks (small host-side metrics)."""
+        if self.world > 1:
+            dist.all_reduce(t, group=self.group)
