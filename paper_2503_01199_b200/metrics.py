@@ -95,10 +95,14 @@ def psnr(a, b) -> float:
     return math.inf if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
 
 
-def loss_and_grad(rendered: torch.Tensor, target, lam: float, return_tensor: bool = False):
+def loss_and_grad(rendered: torch.Tensor, target, lam: float, return_tensor: bool = False, loss_out=None):
     """(loss, dL/d rendered) for (H, W, 3) images (metrics.py:118-132), fused
     kernel.  `target` may be float (any dtype) or uint8 (value / 255).  With
-    return_tensor=True the loss stays a 0-d float64 device tensor (no sync)."""
+    return_tensor=True the loss stays a 0-d float64 device tensor (no sync).
+    `loss_out`: a 1-element float64 tensor in pinned host memory that the
+    kernel writes directly (mapped, zero-copy; no device-to-host copy in the
+    stream) -- valid once the stream has reached this point; returned as the
+    loss tensor with return_tensor=True."""
     import ctypes as C
     from . import _lib
     from .errors import ShapeMismatchError
@@ -117,9 +121,21 @@ def loss_and_grad(rendered: torch.Tensor, target, lam: float, return_tensor: boo
         y = y.float().contiguous()
     grad = torch.empty_like(x)
     acc = _lib.workspace("loss_accum", 16, x.device)       # zeroed once, left zeroed by the call
-    out = torch.empty(1, dtype=torch.float64, device=x.device)
+    out_ptr = None
+    if loss_out is not None:
+        if loss_out.device.type != "cpu" or not loss_out.is_pinned() or loss_out.dtype != torch.float64:
+            raise ValueError("loss_out must be a pinned host float64 tensor")
+        addr = C.c_void_p()
+        if _lib.load().sb_host_mapped_pointer(C.c_void_p(loss_out.data_ptr()), C.byref(addr)) == 0 and addr.value:
+            out, out_ptr = loss_out, addr
+    if out_ptr is None:
+        out = torch.empty(1, dtype=torch.float64, device=x.device)
+        out_ptr = _lib.ptr(out)
     _lib.call("sb_loss_fwd_bwd", _lib.ptr(x), _lib.ptr(y), _lib.ptr(y8), W, H, float(lam), _lib.ptr(grad),
-              _lib.ptr(acc), _lib.ptr(out), C.c_void_p(_lib.stream_ptr(x.device)))
+              _lib.ptr(acc), out_ptr, C.c_void_p(_lib.stream_ptr(x.device)))
+    if loss_out is not None and out is not loss_out:
+        loss_out.copy_(out, non_blocking=True)   # not mappable: an async copy instead
+        out = loss_out
     loss = out[0]
     return (loss if return_tensor else float(loss)), grad
 

@@ -372,6 +372,12 @@ def test_fused_loss_vs_reference(fname, prefix):
     l8r, g8r = O.loss_and_grad(col, t8.astype(np.float64) / 255.0, 0.2)
     assert abs(l8 - l8r) <= 1e-5 * abs(l8r)
     assert np.abs(g8.cpu().numpy() - g8r).max() <= 1e-4 * np.abs(g8r).max()
+    # loss written straight into mapped pinned host memory (no D2H copy)
+    host = torch.full((3,), -1.0, dtype=torch.float64, pin_memory=True)
+    lt, g9 = sb.loss_and_grad(x, torch.from_numpy(t8).cuda(), 0.2, return_tensor=True, loss_out=host[1:2])
+    torch.cuda.synchronize()
+    assert float(host[1]) == l8 and float(lt) == l8 and host[0] == -1.0 and host[2] == -1.0
+    assert torch.equal(g9, g8)
 
 
 @pytest.mark.parametrize("fname,prefix", G.CASES)
