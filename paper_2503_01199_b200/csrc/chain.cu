@@ -23,7 +23,7 @@ SB_INLINE void rotmat_grad_to_quat(const double d[3][3], const double q[4], doub
                     y * d[1][2]) + x * d[2][0]) + y * d[2][1]);
 }
 
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, 2)
 chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t* __restrict__ cluster_offset,
              const RasterRec* __restrict__ recs, const sb_screen_grad* __restrict__ sg, float4* __restrict__ grads,
              double* __restrict__ stat_S, double* __restrict__ stat_M, int32_t* __restrict__ stat_C)
