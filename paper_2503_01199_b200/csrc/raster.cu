@@ -272,7 +272,8 @@ raster_fwd_kernel(FwdParams p)
                     done = true;
                     break;
                 }
-                if (!live) continue;
+                // (no per-lane skip: a terminated lane's pixels fail the
+                // T >= t_stop test below, and SIMT runs the body anyway)
                 const SRec r = slab_get<false>(slab, j);
                 float araw[4], dx, dy;
                 lane_alpha_raw(r, px, py0, araw, dx, dy);
@@ -371,7 +372,8 @@ raster_fwd_half_kernel(FwdParams p)
                     done = true;
                     break;
                 }
-                if (!live) continue;
+                // (no per-lane skip: a terminated lane's pixels fail the
+                // T >= t_stop test below, and SIMT runs the body anyway)
                 const SRec r = slab_get<false>(slab, j);
                 float G[4], dx, dy;
                 lane_G(r, px, py0, G, dx, dy);
