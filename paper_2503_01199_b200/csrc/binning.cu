@@ -15,9 +15,8 @@
 //                span, then a row prefix sum); per-super-tile entry counts
 //                (super-tiles overlapping the rectangle) through a second,
 //                smaller window; one global add per touched cell;
-//            (2) one CTA: exclusive scans -> tile_offsets and P, super-tile
-//                offsets and E, and the list of super-tiles too long to sort
-//                in one shared-memory pass;
+//            (2) two CTAs: exclusive scans -> tile_offsets and P, super-tile
+//                offsets and E, and the heavy-first schedules;
 //   finish   (1) scatter: the same CTAs reserve each touched super-tile's
 //                sub-range with one global atomic and place their 64-bit
 //                keys (depth bits << 32 | compact slot) through
@@ -342,11 +341,10 @@ constexpr int kStCap = kStThreads * 16;   // super-tile entries sorted in one sh
 
 // exclusive scan of cnt[0, n) into out[0, n], total to out[n] and *total;
 // cnt is re-zeroed as it is read (ready for the next call); with `copy` the
-// offsets are also written there (the scatter cursors); with `longs`, the
-// indices whose count exceeds `long_min` are appended to longs[1..]
-// (longs[0] = how many).  Whole (1024-thread) CTA.
+// offsets are also written there (the scatter cursors).  Whole (1024-thread)
+// CTA.
 __device__ void cta_scan(int32_t* __restrict__ cnt, int32_t* __restrict__ out, int n, int32_t* __restrict__ total,
-                         int32_t* __restrict__ copy, int32_t* __restrict__ longs, uint32_t long_min)
+                         int32_t* __restrict__ copy)
 {
     // Rounds of kScanThreads * kScanItems counts; warp w owns a contiguous
     // block of 32 * kScanItems of them, read row by row (lane l of row j is
@@ -355,10 +353,7 @@ __device__ void cta_scan(int32_t* __restrict__ cnt, int32_t* __restrict__ out, i
     __shared__ uint32_t s_warp[kScanThreads / 32];
     __shared__ uint32_t s_carry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
-        s_carry = 0;
-        if (longs) longs[0] = 0;
-    }
+    if (threadIdx.x == 0) s_carry = 0;
     __syncthreads();
     for (int base = 0; base < n; base += kScanThreads * kScanItems) {
         const int wbase = base + warp * 32 * kScanItems + lane;
@@ -387,10 +382,8 @@ __device__ void cta_scan(int32_t* __restrict__ cnt, int32_t* __restrict__ out, i
                 if (lane >= o) x += y;
             }
             const uint32_t row_total = __shfl_sync(0xffffffffu, x, 31);
-            const uint32_t cj = v[j];
-            v[j] = carry + x - cj;     // exclusive, within the block
+            v[j] = carry + x - v[j];   // exclusive, within the block
             carry += row_total;
-            if (longs && cj > long_min) longs[1 + atomicAdd(&longs[0], 1)] = wbase + 32 * j;
         }
         if (lane == 0) s_warp[warp] = carry;
         __syncthreads();
@@ -525,18 +518,18 @@ __device__ void schedules(const SchedArr (&arr)[2])
 __global__ void __launch_bounds__(kScanThreads)
 tile_scan_kernel(int32_t* __restrict__ tile_cnt, int32_t* __restrict__ offsets, int ntiles,
                  int32_t* __restrict__ st_cnt, int32_t* __restrict__ st_offsets, int nst,
-                 int32_t* __restrict__ totals, int32_t* __restrict__ st_longs, int32_t* __restrict__ cursor,
+                 int32_t* __restrict__ totals, int32_t* __restrict__ cursor,
                  const int32_t* __restrict__ counters, int32_t* __restrict__ mirror, int32_t* __restrict__ st_sched)
 {
     sb_pdl_begin();
     // CTA 0: tiles (offsets, raster schedule); CTA 1: super-tiles (offsets,
-    // scatter cursors, long list, sort/emit schedule) -- independent halves
+    // scatter cursors, sort/emit schedule) -- independent halves
     if (blockIdx.x == 0) {
-        cta_scan(tile_cnt, offsets, ntiles, totals, nullptr, nullptr, 0);
+        cta_scan(tile_cnt, offsets, ntiles, totals, nullptr);
         const SchedArr arr[2] = {{offsets, ntiles, offsets + ntiles + 1}, {nullptr, 0, nullptr}};
         schedules(arr);
     } else {
-        cta_scan(st_cnt, st_offsets, nst, totals + 1, cursor, st_longs, (uint32_t)kStCap);
+        cta_scan(st_cnt, st_offsets, nst, totals + 1, cursor);
         const SchedArr arr[2] = {{st_offsets, nst, st_sched}, {nullptr, 0, nullptr}};
         schedules(arr);
     }
@@ -1069,8 +1062,8 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // bin state: tile counts (ntiles + 1) | super-tile counts (nst + 1) |
 // scatter cursors (nst) | spans (32 B per compact slot) | origin (4 B per
-// slot) | super-tile offsets (nst + 1) | long super-tile list (1 + nst) |
-// super-tile schedule (nst, largest first).
+// slot) | super-tile offsets (nst + 1) | super-tile schedule (nst, largest
+// first).
 // The count arrays come first (offsets independent of n_cap): zeroed once
 // before first use, accumulated by the count kernel, re-zeroed by the scan.
 struct StateLayout {
@@ -1080,12 +1073,11 @@ struct StateLayout {
     uint4* spans;
     uint32_t* origin;
     int32_t* st_offsets;
-    int32_t* st_longs;
     int32_t* st_sched;
 };
 inline size_t state_bytes(int n_cap, int ntiles) {
     const size_t n = (size_t)(n_cap > 0 ? n_cap : 1), t = (size_t)ntiles + 1;
-    return 6 * align256(t * 4) + align256(n * 32) + align256(n * 4);
+    return 5 * align256(t * 4) + align256(n * 32) + align256(n * 4);
 }
 inline StateLayout state_layout(void* state, int n_cap, int ntiles, int nst) {
     const size_t n = (size_t)(n_cap > 0 ? n_cap : 1);
@@ -1097,7 +1089,6 @@ inline StateLayout state_layout(void* state, int n_cap, int ntiles, int nst) {
     L.spans = reinterpret_cast<uint4*>(p); p += align256(n * 32);
     L.origin = reinterpret_cast<uint32_t*>(p); p += align256(n * 4);
     L.st_offsets = reinterpret_cast<int32_t*>(p); p += align256((size_t)(nst + 1) * 4);
-    L.st_longs = reinterpret_cast<int32_t*>(p); p += align256((size_t)(nst + 1) * 4);
     L.st_sched = reinterpret_cast<int32_t*>(p);
     return L;
 }
@@ -1119,7 +1110,7 @@ void sb_launch_bin_prepare(const RasterRec* recs, const int32_t* counters, int n
         sb_launch(tile_count_kernel, (n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream, recs, counters,
                   n_cap, cam.tiles_x, cam.tiles_y, st_x, cam.W, cam.H, L.spans, L.origin, L.tile_cnt, L.st_cnt);
     sb_launch(tile_scan_kernel, 2, kScanThreads, 0, stream, L.tile_cnt, tile_offsets, ntiles, L.st_cnt, L.st_offsets,
-              nst, totals, L.st_longs, L.cursor, counters, mirror, L.st_sched);
+              nst, totals, L.cursor, counters, mirror, L.st_sched);
 }
 
 // ---- finish --------------------------------------------------------------------
