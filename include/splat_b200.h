@@ -56,6 +56,12 @@ size_t sb_morton_keys_workspace_bytes(int64_t n);
 int sb_morton_keys(const float* params, int64_t n, uint64_t* keys, uint32_t* vals, double* lohi,
                    int32_t* bad_index, void* ws, size_t ws_bytes, sb_stream_t stream);
 
+/* ccc.py:59-66 morton_encode(positions, bounds_min, bounds_max): keys of
+ * caller positions (n, 3) float64 for explicit bounds lohi[6] = (min xyz,
+ * max xyz) float64 (device).  *bad_index as for sb_morton_keys. */
+int sb_morton_encode(const double* positions, int64_t n, const double* lohi, uint64_t* keys, int32_t* bad_index,
+                     sb_stream_t stream);
+
 /* ccc.py:88 np.argsort(kind="stable"): stable onesweep LSD radix sort of
  * (key, value) pairs over key bits [0, bits) (8-bit digits; one kernel per
  * digit with decoupled look-back).  *result_in_alt (host int) is set to 1

@@ -27,6 +27,7 @@ SIGNATURES = {
     "sb_screen_grad_bytes": ([], C.c_int),
     "sb_morton_keys_workspace_bytes": ([I64], SZ),
     "sb_morton_keys": ([VP, I64, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_morton_encode": ([VP, I64, VP, VP, VP, VP], C.c_int),
     "sb_sort_workspace_bytes": ([I64], SZ),
     "sb_radix_sort_pairs_u64": ([VP, VP, VP, VP, I64, C.c_int, VP, VP, SZ, VP], C.c_int),
     "sb_permute_rows": ([VP, I64, C.c_int, VP, VP, VP, VP], C.c_int),
@@ -108,7 +109,7 @@ def ptr(t: torch.Tensor | None):
 # kernel launches issued by each entry point (for bench.py's gpu_launches);
 # the radix sort issues 3 per 8-bit pass and is counted by the caller.
 KERNELS_PER_CALL = {
-    "sb_morton_keys": 3, "sb_permute_rows": 1, "sb_project_cull_compact": 1, "sb_bin_prepare": 2,
+    "sb_morton_keys": 3, "sb_morton_encode": 1, "sb_permute_rows": 1, "sb_project_cull_compact": 1, "sb_bin_prepare": 2,
     "sb_bin_finish": 2, "sb_raster_fwd": 1, "sb_raster_bwd": 1, "sb_radix_sort_pairs_u64": 10,
     "sb_chain_projection_bwd": 1, "sb_adam_sparse": 1, "sb_variance_score": 1, "sb_lane_reduce": 1,
     "sb_loss_fwd_bwd": 2,

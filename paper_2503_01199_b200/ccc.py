@@ -4,7 +4,9 @@ Reference: pkg/src/tinysplat/ccc.py.  Culling and compaction themselves run
 fused inside the forward (sb_project_cull_compact); this module exposes the
 Morton re-sort (ccc.py:59-90) and the small index helpers.
 
-  morton_encode  -> sb_morton_keys (bounds + float64 quantise + bit interleave)
+  morton_encode  -> sb_morton_encode (caller positions and bounds, float64
+                    quantise + bit interleave); morton_encode_scene ->
+                    sb_morton_keys (the scene's own bounds on the device)
   morton_sort    -> sb_morton_keys + sb_radix_sort_pairs_u64 (63-bit keys,
                     8 stable LSD passes) + sb_permute_rows over the parameter
                     rows and every registered extra
@@ -38,6 +40,28 @@ def _keys(rows: torch.Tensor, n: int):
     _lib.call("sb_morton_keys", _lib.ptr(rows), n, _lib.ptr(keys), _lib.ptr(vals), _lib.ptr(lohi), _lib.ptr(bad),
               _lib.ptr(ws), ws.numel(), stream)
     return keys, vals, lohi, bad
+
+
+def morton_encode(positions, bounds_min, bounds_max, device=None) -> torch.Tensor:
+    """ccc.py:59-66 on the device (sb_morton_encode): 63-bit Z-order keys of
+    (N, 3) positions, quantised in float64 within the given bounds.  Keys are
+    uint64 values carried in an int64 tensor (view as uint64 on the host).
+    Raises ValidationError on a non-finite position, as quantize does."""
+    if device is None:
+        device = positions.device if torch.is_tensor(positions) and positions.is_cuda else torch.device("cuda")
+    pos = torch.as_tensor(positions, dtype=torch.float64, device=device).reshape(-1, 3).contiguous()
+    _lib.require_cuda(pos)
+    n = pos.shape[0]
+    lohi = torch.cat([torch.as_tensor(bounds_min, dtype=torch.float64).reshape(3),
+                      torch.as_tensor(bounds_max, dtype=torch.float64).reshape(3)]).to(device)
+    keys = torch.empty(max(n, 1), dtype=torch.int64, device=device)
+    bad = torch.empty(1, dtype=torch.int32, device=device)
+    _lib.call("sb_morton_encode", _lib.ptr(pos), n, _lib.ptr(lohi), _lib.ptr(keys), _lib.ptr(bad),
+              C.c_void_p(_lib.stream_ptr(device)))
+    b = int(bad.item())
+    if b < n:
+        raise ValidationError("position", b, "non-finite position")
+    return keys[:n]
 
 
 def morton_encode_scene(scene: SceneSoA):

@@ -33,6 +33,7 @@ void sb_launch_variance(const double*, const double*, const int32_t*, int, doubl
 void sb_launch_bounds(const float*, int, float*, double*, cudaStream_t);
 int sb_bounds_partial_floats();
 void sb_launch_morton_keys(const float*, int, const double*, unsigned long long*, uint32_t*, int*, cudaStream_t);
+void sb_launch_morton_encode(const double*, int, const double*, unsigned long long*, int*, cudaStream_t);
 void sb_launch_permute(const uint32_t*, int, int, const void* const*, void* const*, const int*, cudaStream_t);
 
 static thread_local std::string g_err;
@@ -101,6 +102,15 @@ int sb_morton_keys(const float* params, int64_t n, uint64_t* keys, uint32_t* val
     sb_launch_morton_keys(params, (int)n, lohi, reinterpret_cast<unsigned long long*>(keys), vals, bad_index,
                           S(stream));
     return check_launch("sb_morton_keys");
+}
+
+int sb_morton_encode(const double* positions, int64_t n, const double* lohi, uint64_t* keys, int32_t* bad_index,
+                     sb_stream_t stream) {
+    if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
+    cudaMemsetAsync(bad_index, 0x7F, sizeof(int32_t), S(stream));   // 0x7F7F7F7F: no bad index
+    sb_launch_morton_encode(positions, (int)n, lohi, reinterpret_cast<unsigned long long*>(keys), bad_index,
+                            S(stream));
+    return check_launch("sb_morton_encode");
 }
 
 size_t sb_sort_workspace_bytes(int64_t n) { return sb_sort_u64_ws((int)n, 64) + 256; }

@@ -78,18 +78,13 @@ SB_INLINE unsigned long long spread_bits(unsigned long long x) {
     return x;
 }
 
-__global__ void __launch_bounds__(256)
-morton_keys_kernel(const float4* __restrict__ params, int n, const double* __restrict__ lohi,
-                   unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals, int* __restrict__ bad)
-{
-    sb_pdl_begin();
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n) return;
-    const float4 p = __ldg(params + (size_t)g * 4);
-    const double v[3] = {p.x, p.y, p.z};
+// ccc.py:48-66: float64 quantise (extent floored at MIN_EXTENT, clip,
+// floor(u * (2^21 - 1))) and 3-way bit interleave; finite = false (key 0)
+// for a non-finite coordinate
+SB_INLINE unsigned long long morton_key(const double v[3], const double* __restrict__ lohi, bool& finite) {
     const double qmax = (double)((1u << SB_MORTON_BITS) - 1);
     unsigned long long q[3];
-    bool finite = true;
+    finite = true;
     for (int k = 0; k < 3; k++) {
         const double lo = lohi[k];
         double ext = DSUB(lohi[3 + k], lo);
@@ -99,9 +94,39 @@ morton_keys_kernel(const float4* __restrict__ params, int n, const double* __res
         u = u < 0.0 ? 0.0 : (u > 1.0 ? 1.0 : u);
         q[k] = finite ? (unsigned long long)floor(DMUL(u, qmax)) : 0ull;
     }
+    return spread_bits(q[0]) | (spread_bits(q[1]) << 1) | (spread_bits(q[2]) << 2);
+}
+
+__global__ void __launch_bounds__(256)
+morton_keys_kernel(const float4* __restrict__ params, int n, const double* __restrict__ lohi,
+                   unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals, int* __restrict__ bad)
+{
+    sb_pdl_begin();
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const float4 p = __ldg(params + (size_t)g * 4);
+    const double v[3] = {p.x, p.y, p.z};
+    bool finite;
+    const unsigned long long key = morton_key(v, lohi, finite);
     if (!finite) atomicMin(bad, g);
-    keys[g] = spread_bits(q[0]) | (spread_bits(q[1]) << 1) | (spread_bits(q[2]) << 2);
+    keys[g] = key;
     vals[g] = (uint32_t)g;
+}
+
+// ccc.py:59-66 morton_encode(positions, bounds_min, bounds_max) for caller
+// positions (n, 3) float64 and explicit bounds
+__global__ void __launch_bounds__(256)
+morton_encode_kernel(const double* __restrict__ pos, int n, const double* __restrict__ lohi,
+                     unsigned long long* __restrict__ keys, int* __restrict__ bad)
+{
+    sb_pdl_begin();
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const double v[3] = {pos[3 * (size_t)g], pos[3 * (size_t)g + 1], pos[3 * (size_t)g + 2]};
+    bool finite;
+    const unsigned long long key = morton_key(v, lohi, finite);
+    if (!finite) atomicMin(bad, g);
+    keys[g] = key;
 }
 
 // ---- K4 multi-array row permute (gather) -------------------------------------
@@ -149,6 +174,12 @@ void sb_launch_morton_keys(const float* params, int n, const double* lohi, unsig
     if (n <= 0) return;
     sb_launch(morton_keys_kernel, (n + 255) / 256, 256, 0, stream, reinterpret_cast<const float4*>(params), n, lohi,
               keys, vals, bad);
+}
+
+void sb_launch_morton_encode(const double* pos, int n, const double* lohi, unsigned long long* keys, int* bad,
+                             cudaStream_t stream) {
+    if (n <= 0) return;
+    sb_launch(morton_encode_kernel, (n + 255) / 256, 256, 0, stream, pos, n, lohi, keys, bad);
 }
 
 void sb_launch_permute(const uint32_t* perm, int n, int count, const void* const* src, void* const* dst,

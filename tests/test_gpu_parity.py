@@ -140,6 +140,19 @@ def test_morton_keys_and_sort_bit_exact():
     got, _, _ = morton_encode_scene(scene)
     assert np.array_equal(got.cpu().numpy().view(np.uint64), keys)
     assert np.array_equal(sb.morton_sort(scene.copy()).cpu().numpy(), perm)
+    # ccc.morton_encode on the float64 positions themselves: the reference's
+    # own keys (fixture), bounds as morton_sort takes them (scene.py:256-260)
+    from paper_2503_01199_b200.ccc import morton_encode
+    k64 = morton_encode(pos, pos.min(axis=0), pos.max(axis=0))
+    assert np.array_equal(k64.cpu().numpy().view(np.uint64), d["mort_keys"])
+    # explicit bounds narrower than the data: clipped to the grid edges
+    lo, hi = np.full(3, -0.25), np.full(3, 0.25)
+    kk = morton_encode(torch.from_numpy(pos).cuda(), lo, hi).cpu().numpy().view(np.uint64)
+    assert np.array_equal(kk, O.morton_encode(pos, lo, hi))
+    with pytest.raises(sb.ValidationError):
+        bad = pos.copy()
+        bad[3, 1] = np.nan
+        morton_encode(bad, lo, hi)
 
 
 def test_radix_sort_random_keys_stable():
