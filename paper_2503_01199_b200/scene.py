@@ -35,7 +35,10 @@ def pack_rows(position, log_scale, rotation, color, opacity_logit, device=None) 
              "opacity_logit": opacity_logit}
     ts = {}
     for k, v in chans.items():
-        t = torch.as_tensor(np.asarray(v) if not torch.is_tensor(v) else v)
+        if not torch.is_tensor(v):
+            a = np.asarray(v)
+            v = a if a.flags.writeable else a.copy()   # read-only inputs (e.g. npz views)
+        t = torch.as_tensor(v)
         ts[k] = t.to(torch.float32).reshape(-1, CHANNEL_WIDTHS[k])
     n = ts["position"].shape[0]
     for k, t in ts.items():
