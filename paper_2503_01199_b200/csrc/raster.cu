@@ -659,8 +659,7 @@ raster_bwd_kernel(BwdParams p)
             while (todo) {
                 const int j = 31 - __clz(todo);
                 todo &= ~(1u << j);
-                const int k = k0 + j;
-                if (!__any_sync(0xffffffffu, k < lane_max)) continue;
+                const int k = k0 + j;   // k < kmax: some lane's pixel is still before its last
                 const SRec r = slab_get<true>(ws.slab, j);
                 float araw[4], dx, dy;
                 lane_alpha_raw(r, px, py0, araw, dx, dy);
