@@ -188,12 +188,18 @@ SB_INLINE void lane_G(const SRec& r, float px, float py0, float G[4], float& dx,
     for (int i = 0; i < 4; i++) G[i] = ex2(e[i]);
 }
 
-// o * G = ex2(e + log2 o)
+// o * G = ex2(e + log2 o), with log2 o folded into the run's base term
+// (one add instead of four; forward and backward share this rounding)
 SB_INLINE void lane_alpha_raw(const SRec& r, float px, float py0, float araw[4], float& dx, float& dy) {
-    float e[4];
-    lane_expo(r, px, py0, e, dx, dy);
-#pragma unroll
-    for (int i = 0; i < 4; i++) araw[i] = ex2(e[i] + r.lg2o);
+    dx = r.x - px;
+    dy = r.y - py0;
+    const float cqdy = r.Cq * dy;
+    const float e0 = fmaf(fmaf(r.A, dx, r.B * dy), dx, fmaf(cqdy, dy, r.lg2o));
+    const float t = fmaf(cqdy, 2.0f, r.B * dx);
+    araw[0] = ex2(e0);
+    araw[1] = ex2(e0 + (r.Cq - t));
+    araw[2] = ex2(fmaf(-2.0f, t, fmaf(4.0f, r.Cq, e0)));
+    araw[3] = ex2(fmaf(-3.0f, t, fmaf(9.0f, r.Cq, e0)));
 }
 
 // Dynamic tile queue: counter[0] hands out tiles, counter[1] counts the
