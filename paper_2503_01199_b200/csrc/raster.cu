@@ -51,7 +51,7 @@ constexpr int kThreads = kWarpsPerBlock * 32;
 struct __align__(16) SRec {
     float x, y, A, B;        // A = -log2e/2 a, B = -log2e b
     float Cq, o, r, g;       // Cq = -log2e/2 c
-    float bl, lg2o, inv_o, pad;
+    float bl, lg2o, inv_o, s2io;   // s2io = 2^64 / o^2 (the backward's S scale)
     float a, b, c;
     int32_t slot;
 };
@@ -100,7 +100,7 @@ SB_INLINE SRec slab_get(const SRec* slab, int j) {
     SRec r;
     r.x = c0.x; r.y = c0.y; r.A = c0.z; r.B = c0.w;
     r.Cq = c1.x; r.o = c1.y; r.r = c1.z; r.g = c1.w;
-    r.bl = c2.x; r.lg2o = c2.y; r.inv_o = c2.z; r.pad = c2.w;
+    r.bl = c2.x; r.lg2o = c2.y; r.inv_o = c2.z; r.s2io = c2.w;
     r.a = c3.x; r.b = c3.y; r.c = c3.z; r.slot = __float_as_int(c3.w);
     return r;
 }
@@ -113,7 +113,9 @@ SB_INLINE void commit_chunk(SRec* slab, const Prefetch& pf, int cnt, int lane) {
         const int sw = slab_swizzle<kSwz>(lane);
         d[0 ^ sw] = make_float4(pf.a.x, pf.a.y, A, B);
         d[1 ^ sw] = make_float4(Cq, pf.b.y, pf.b.z, pf.b.w);
-        d[2 ^ sw] = make_float4(pf.bl, __log2f(pf.b.y), rcp_approx(pf.b.y), 0.f);
+        const float io = rcp_approx(pf.b.y), io32 = io * 4294967296.0f;
+        // (finite even for opacities far below any alpha_min: 0 * s2io = 0)
+        d[2 ^ sw] = make_float4(pf.bl, __log2f(pf.b.y), io, fminf(io32 * io32, 3.0e38f));
         d[3 ^ sw] = make_float4(pf.a.z, pf.a.w, pf.b.x, __int_as_float(pf.slot));
     }
 }
@@ -720,8 +722,7 @@ raster_bwd_kernel(BwdParams p)
                 pc[2 * 256] = fmaf(dy, fmaf(-0.5f * gb, dy, gl), -0.5f * gq);
                 // S, scaled by 2^64 (exact) so the squares' rows stay off the
                 // exponent-aligned sum's two-step path for values below 2^-103
-                const float io = r.inv_o * 4294967296.0f;
-                pc[3 * 256] = (q2.x + q2.y) * (io * io);                             // S * 2^64
+                pc[3 * 256] = (q2.x + q2.y) * r.s2io;                                // S * 2^64
                 float rgb[3];
 #pragma unroll
                 for (int ch = 0; ch < 3; ch++) {
