@@ -171,6 +171,8 @@ int sb_bin_prepare(const void* recs, const int32_t* counters, int64_t n_cap, con
     if (n_cap < 0 || n_cap > INT32_MAX / 2) return fail(SB_EINVAL, "n_cap out of range");
     if (!tile_offsets || !n_pairs) return fail(SB_EINVAL, "NULL buffer");
     const CamDev d = make_cam(cam, nullptr);
+    if ((int64_t)d.tiles_x * d.tiles_y > (int64_t)256 * 4096)
+        return fail(SB_EINVAL, "resolution too large (more than 2^20 tiles)");
     if (state_bytes < sb_bin_state_workspace_bytes(n_cap, d.tiles_x * d.tiles_y))
         return fail(SB_EWORKSPACE, "bin state too small");
     sb_launch_bin_prepare(static_cast<const RasterRec*>(recs), counters, (int)n_cap, d, tile_offsets, n_pairs,

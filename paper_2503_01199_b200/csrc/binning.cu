@@ -15,8 +15,9 @@
 //                span, then a row prefix sum); per-super-tile entry counts
 //                (super-tiles overlapping the rectangle) through a second,
 //                smaller window; one global add per touched cell;
-//            (2) two CTAs: exclusive scans -> tile_offsets and P, super-tile
-//                offsets and E, and the heavy-first schedules;
+//            (2) scan_local + scan_finish, one CTA per chunk of counts:
+//                exclusive scans -> tile_offsets and P, super-tile offsets
+//                and E, and the heavy-first schedules;
 //   finish   (1) scatter: the same CTAs reserve each touched super-tile's
 //                sub-range with one global atomic and place their 64-bit
 //                keys (depth bits << 32 | compact slot) through
@@ -334,88 +335,8 @@ tile_count_kernel(const RasterRec* __restrict__ recs, const int32_t* __restrict_
 }
 
 // ---- prepare (2): counts -> exclusive offsets, in place ------------------------
-constexpr int kScanThreads = 1024;
-constexpr int kScanItems = 16;   // per thread and round
 constexpr int kStThreads = 384;
 constexpr int kStCap = kStThreads * 16;   // super-tile entries sorted in one shared-memory pass
-
-// exclusive scan of cnt[0, n) into out[0, n], total to out[n] and *total;
-// cnt is re-zeroed as it is read (ready for the next call); with `copy` the
-// offsets are also written there (the scatter cursors).  Whole (1024-thread)
-// CTA.
-__device__ void cta_scan(int32_t* __restrict__ cnt, int32_t* __restrict__ out, int n, int32_t* __restrict__ total,
-                         int32_t* __restrict__ copy)
-{
-    // Rounds of kScanThreads * kScanItems counts; warp w owns a contiguous
-    // block of 32 * kScanItems of them, read row by row (lane l of row j is
-    // item 32 j + l), so every load and store is coalesced -- this kernel
-    // runs on one SM, whose load/store queue is its bound.
-    __shared__ uint32_t s_warp[kScanThreads / 32];
-    __shared__ uint32_t s_carry;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (int base = 0; base < n; base += kScanThreads * kScanItems) {
-        const int wbase = base + warp * 32 * kScanItems + lane;
-        uint32_t v[kScanItems];
-#pragma unroll
-        for (int j = 0; j < kScanItems; j++) {
-            const int i = wbase + 32 * j;
-            v[j] = i < n ? (uint32_t)cnt[i] : 0u;
-        }
-#pragma unroll
-        for (int j = 0; j < kScanItems; j++) {
-            const int i = wbase + 32 * j;
-            if (i < n) cnt[i] = 0;
-        }
-        // exclusive prefix within the warp's block, row by row (rows past
-        // n hold zeros; warp-uniform skip)
-        uint32_t carry = 0;
-        const int wrows = min(kScanItems, max(0, (n - (base + warp * 32 * kScanItems) + 31) / 32));
-#pragma unroll
-        for (int j = 0; j < kScanItems; j++) {
-            if (j >= wrows) { v[j] = carry; continue; }
-            uint32_t x = v[j];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            const uint32_t row_total = __shfl_sync(0xffffffffu, x, 31);
-            v[j] = carry + x - v[j];   // exclusive, within the block
-            carry += row_total;
-        }
-        if (lane == 0) s_warp[warp] = carry;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = s_warp[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += y;
-            }
-            s_warp[lane] = w;   // inclusive over warps
-        }
-        __syncthreads();
-        const uint32_t off = s_carry + (warp ? s_warp[warp - 1] : 0u);
-#pragma unroll
-        for (int j = 0; j < kScanItems; j++) {
-            const int i = wbase + 32 * j;
-            if (i < n) {
-                out[i] = (int32_t)(off + v[j]);
-                if (copy) copy[i] = (int32_t)(off + v[j]);
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry += s_warp[31];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        out[n] = (int32_t)s_carry;
-        *total = (int32_t)s_carry;
-    }
-    __syncthreads();
-}
 
 // Heavy-first raster schedule: the tiles ordered by list length, longest
 // first (bucketed by the length's leading three bits), so the dynamic tile
@@ -429,116 +350,222 @@ SB_INLINE int sched_bucket(int c) {
     return min(63, 1 + 4 * l + frac);
 }
 
-// Both schedules (tiles -> raster queues, super-tiles -> sort/emit CTAs) in
-// one pass: bucket histograms, a warp-parallel prefix (heaviest bucket
-// first), then the scatter, with the buckets kept in registers when one
-// round covers the array (the common case) so each count is loaded once.
-struct SchedArr {
-    const int32_t* offs;
-    int n;
-    int32_t* out;
+// Scan + schedules over many SMs, in two launches (no grid-wide barrier).
+// Each array (tiles; super-tiles) is cut into chunks of kScanBlock * ipt
+// counts, one CTA per chunk of either array:
+//   scan_local   load the chunk's counts (re-zeroing them for the next
+//                call), block-exclusive scan -> out[] (local offsets), chunk
+//                total -> aux.chunk[c], each count's schedule bucket -> a
+//                byte per element, and the chunk's bucket histogram added
+//                into the array's global histogram;
+//   scan_finish  out[] += the sum of the earlier chunks' totals (a few
+//                hundred values at most, summed by one warp), the scatter
+//                cursor copy for super-tiles, the array total, then the
+//                heavy-first schedule: bucket offsets from the global
+//                histogram (descending), a position per element from a
+//                per-bucket global cursor (order within a bucket is
+//                arbitrary -- scheduling only).  The last CTA to finish
+//                re-zeroes the histograms, cursors and its ticket.
+constexpr int kScanBlock = 512;
+constexpr int kMaxIpt = 8;
+constexpr int kMaxChunks = 512;
+constexpr int kBuckets = 64;
+
+struct ScanAux {                 // zeroed once; left zeroed by scan_finish
+    uint32_t hist[2][kBuckets];
+    uint32_t cur[2][kBuckets];
+    uint32_t done;
+    uint32_t pad[3];
+    uint32_t chunk[kMaxChunks];  // per-chunk totals (overwritten every call)
 };
 
-SB_INLINE void sched_load(const SchedArr& a, int t0, int (&b)[kScanItems]) {
-    const int rows = min(kScanItems, (a.n - t0 + kScanThreads - 1) / kScanThreads);
-#pragma unroll
-    for (int r = 0; r < kScanItems; r++) {
-        const int t = t0 + r * kScanThreads + (int)threadIdx.x;
-        b[r] = r < rows && t < a.n ? sched_bucket(a.offs[t + 1] - a.offs[t]) : -1;
-    }
+struct ScanArgs {
+    int32_t* cnt[2];             // counts, re-zeroed as read
+    int32_t* out[2];             // exclusive offsets (n + 1)
+    int32_t* sched[2];           // heavy-first schedules (n)
+    int32_t* copy;               // super-tile scatter cursors
+    int n[2];
+    int g0, g1, ipt;             // chunks of each array, items per thread
+    uint8_t* bucket;             // bucket id per element (tiles, then super-tiles)
+    ScanAux* aux;
+    int32_t* totals;             // (P, E)
+    const int32_t* counters;
+    int32_t* mirror;
+};
+
+// this CTA's array and chunk, with the array's pointers picked by selects
+// (indexing the parameter struct by a runtime value would copy it to local
+// memory)
+struct ScanView {
+    int arr, c, c0, n;
+    int32_t* cnt;
+    int32_t* out;
+    int32_t* sched;
+    const uint8_t* bk;
+};
+SB_INLINE ScanView scan_view(const ScanArgs& a) {
+    ScanView v;
+    v.c = blockIdx.x;
+    v.arr = v.c < a.g0 ? 0 : 1;
+    const bool s = v.arr != 0;
+    v.c0 = s ? v.c - a.g0 : v.c;
+    v.n = s ? a.n[1] : a.n[0];
+    v.cnt = s ? a.cnt[1] : a.cnt[0];
+    v.out = s ? a.out[1] : a.out[0];
+    v.sched = s ? a.sched[1] : a.sched[0];
+    v.bk = a.bucket + (s ? a.n[0] : 0);
+    return v;
 }
 
-SB_INLINE void sched_hist(const int (&b)[kScanItems], int rows, uint32_t* cnt) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int r = 0; r < kScanItems; r++) {
-        if (r >= rows) break;
-        const unsigned peers = __match_any_sync(0xffffffffu, b[r]);
-        if (b[r] >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[b[r]], (uint32_t)__popc(peers));
-    }
-}
-
-SB_INLINE void sched_scatter(const int (&b)[kScanItems], int rows, int t0, uint32_t* cnt, int32_t* out) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int r = 0; r < kScanItems; r++) {
-        if (r >= rows) break;
-        const int t = t0 + r * kScanThreads + (int)threadIdx.x;
-        const unsigned peers = __match_any_sync(0xffffffffu, b[r]);
-        const int leader = __ffs(peers) - 1;
-        uint32_t pos = 0;
-        if (b[r] >= 0 && lane == leader) pos = atomicAdd(&cnt[b[r]], (uint32_t)__popc(peers));
-        pos = __shfl_sync(0xffffffffu, pos, leader);
-        if (b[r] >= 0) out[pos + __popc(peers & ((1u << lane) - 1u))] = t;
-    }
-}
-
-__device__ void schedules(const SchedArr (&arr)[2])
+__global__ void __launch_bounds__(kScanBlock)
+scan_local_kernel(ScanArgs a)
 {
-    constexpr int kRound = kScanThreads * kScanItems;
-    __shared__ uint32_t s_cnt[2][64];
+    sb_pdl_begin();
+    __shared__ uint32_t s_warp[kScanBlock / 32];
+    __shared__ uint32_t s_hist[kBuckets];
+    const ScanView sv = scan_view(a);
+    const int arr = sv.arr, c = sv.c, n = sv.n, ipt = a.ipt;
+    const int base = sv.c0 * kScanBlock * ipt + threadIdx.x * ipt;   // thread's consecutive items
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x < 128) s_cnt[threadIdx.x >> 6][threadIdx.x & 63] = 0;
+    if (threadIdx.x < kBuckets) s_hist[threadIdx.x] = 0;
+    uint32_t v[kMaxIpt];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxIpt; k++) {
+        const int i = base + k;
+        v[k] = (k < ipt && i < n) ? (uint32_t)sv.cnt[i] : 0u;
+        sum += v[k];
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxIpt; k++) {
+        const int i = base + k;
+        if (k < ipt && i < n) sv.cnt[i] = 0;
+    }
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
     __syncthreads();
-    int b0[kScanItems], b1[kScanItems];
-    const bool single = arr[0].n <= kRound && arr[1].n <= kRound;
-    for (int t0 = 0; t0 < max(arr[0].n, arr[1].n); t0 += kRound) {
-        sched_load(arr[0], t0, b0);
-        sched_load(arr[1], t0, b1);
-        sched_hist(b0, min(kScanItems, (arr[0].n - t0 + kScanThreads - 1) / kScanThreads), s_cnt[0]);
-        sched_hist(b1, min(kScanItems, (arr[1].n - t0 + kScanThreads - 1) / kScanThreads), s_cnt[1]);
+    if (warp == 0) {
+        uint32_t w = lane < kScanBlock / 32 ? s_warp[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < kScanBlock / 32) s_warp[lane] = w;   // inclusive over warps
     }
     __syncthreads();
-    if (warp < 2) {   // exclusive prefix over 64 buckets, descending: lane owns buckets 63 - 2l, 62 - 2l
-        uint32_t* c = s_cnt[warp];
-        const uint32_t hi = c[63 - 2 * lane], lo = c[62 - 2 * lane];
+    uint32_t run = x - sum + (warp ? s_warp[warp - 1] : 0u);
+    uint8_t* bk = const_cast<uint8_t*>(sv.bk);
+#pragma unroll
+    for (int k = 0; k < kMaxIpt; k++) {
+        const int i = base + k;
+        if (k < ipt && i < n) {
+            sv.out[i] = (int32_t)run;
+            run += v[k];
+            const int b = sched_bucket((int)v[k]);
+            bk[i] = (uint8_t)b;
+            atomicAdd(&s_hist[b], 1u);
+        }
+    }
+    if (threadIdx.x == kScanBlock - 1) a.aux->chunk[c] = run;   // the chunk's total
+    __syncthreads();
+    if (threadIdx.x < kBuckets && s_hist[threadIdx.x])
+        atomicAdd(&a.aux->hist[0][0] + arr * kBuckets + threadIdx.x, s_hist[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(kScanBlock)
+scan_finish_kernel(ScanArgs a)
+{
+    sb_pdl_begin();
+    __shared__ uint32_t s_base[kBuckets];
+    __shared__ uint32_t s_off, s_tot[2];
+    __shared__ bool s_last;
+    const ScanView sv = scan_view(a);
+    const int arr = sv.arr, c = sv.c, c0 = sv.c0, n = sv.n, ipt = a.ipt;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t* hist = &a.aux->hist[0][0] + arr * kBuckets;
+    uint32_t* cur = &a.aux->cur[0][0] + arr * kBuckets;
+    // warp 0: this chunk's base and both array totals; warp 1: the
+    // descending bucket prefix of this array's histogram
+    if (warp == 0) {
+        const int first = arr ? a.g0 : 0, last = arr ? a.g0 + a.g1 : a.g0;
+        uint32_t pre = 0, tot = 0;
+        for (int j = first + lane; j < last; j += 32) {
+            const uint32_t t = a.aux->chunk[j];
+            tot += t;
+            if (j < c) pre += t;
+        }
+        pre = __reduce_add_sync(0xffffffffu, pre);
+        tot = __reduce_add_sync(0xffffffffu, tot);
+        if (lane == 0) { s_off = pre; s_tot[arr & 1] = tot; }
+        if (c == 0) {   // the other array's total too (mirror, totals)
+            uint32_t t1 = 0;
+            for (int j = a.g0 + lane; j < a.g0 + a.g1; j += 32) t1 += a.aux->chunk[j];
+            t1 = __reduce_add_sync(0xffffffffu, t1);
+            if (lane == 0) s_tot[1] = t1;
+        }
+    } else if (warp == 1) {
+        const uint32_t hi = hist[63 - 2 * lane], lo = hist[62 - 2 * lane];
         uint32_t x = hi + lo;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
-        const uint32_t ex = x - hi - lo;
-        c[63 - 2 * lane] = ex;
-        c[62 - 2 * lane] = ex + hi;
+        s_base[63 - 2 * lane] = x - hi - lo;
+        s_base[62 - 2 * lane] = x - lo;
     }
     __syncthreads();
-    for (int t0 = 0; t0 < max(arr[0].n, arr[1].n); t0 += kRound) {
-        if (!single) {
-            sched_load(arr[0], t0, b0);
-            sched_load(arr[1], t0, b1);
+    const int base = c0 * kScanBlock * ipt + threadIdx.x * ipt;
+    const uint32_t off = s_off;
+    for (int k = 0; k < ipt; k++) {
+        const int i = base + k;
+        const bool ok = i < n;
+        int b = -1;
+        if (ok) {
+            const int32_t o = sv.out[i] + (int32_t)off;
+            sv.out[i] = o;
+            if (arr && a.copy) a.copy[i] = o;
+            b = sv.bk[i];
         }
-        sched_scatter(b0, min(kScanItems, (arr[0].n - t0 + kScanThreads - 1) / kScanThreads), t0, s_cnt[0],
-                      arr[0].out);
-        sched_scatter(b1, min(kScanItems, (arr[1].n - t0 + kScanThreads - 1) / kScanThreads), t0, s_cnt[1],
-                      arr[1].out);
+        // one global cursor bump per (warp, bucket) group
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        const int leader = __ffs(peers) - 1;
+        uint32_t pos = 0;
+        if (ok && lane == leader) pos = atomicAdd(&cur[b], (uint32_t)__popc(peers));
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        if (ok) sv.sched[s_base[b] + pos + __popc(peers & ((1u << lane) - 1u))] = i;
     }
-}
-
-__global__ void __launch_bounds__(kScanThreads)
-tile_scan_kernel(int32_t* __restrict__ tile_cnt, int32_t* __restrict__ offsets, int ntiles,
-                 int32_t* __restrict__ st_cnt, int32_t* __restrict__ st_offsets, int nst,
-                 int32_t* __restrict__ totals, int32_t* __restrict__ cursor,
-                 const int32_t* __restrict__ counters, int32_t* __restrict__ mirror, int32_t* __restrict__ st_sched)
-{
-    sb_pdl_begin();
-    // CTA 0: tiles (offsets, raster schedule); CTA 1: super-tiles (offsets,
-    // scatter cursors, sort/emit schedule) -- independent halves
-    if (blockIdx.x == 0) {
-        cta_scan(tile_cnt, offsets, ntiles, totals, nullptr);
-        const SchedArr arr[2] = {{offsets, ntiles, offsets + ntiles + 1}, {nullptr, 0, nullptr}};
-        schedules(arr);
-    } else {
-        cta_scan(st_cnt, st_offsets, nst, totals + 1, cursor);
-        const SchedArr arr[2] = {{st_offsets, nst, st_sched}, {nullptr, 0, nullptr}};
-        schedules(arr);
+    if (threadIdx.x == 0) {
+        const int last_chunk = arr ? a.g1 - 1 : a.g0 - 1;
+        if (c0 == last_chunk) sv.out[n] = (int32_t)s_tot[arr & 1];
+        if (c == 0) {
+            a.totals[0] = (int32_t)s_tot[0];
+            a.totals[1] = (int32_t)s_tot[1];
+            // host-mapped copy of (vis, N_c, ndeg, 0, P, E): the host's one
+            // read needs no device-to-host copy in the stream
+            if (a.mirror) {
+                for (int j = 0; j < 4; j++) a.mirror[j] = a.counters[j];
+                a.mirror[4] = (int32_t)s_tot[0];
+                a.mirror[5] = (int32_t)s_tot[1];
+            }
+        }
+        __threadfence();
+        s_last = atomicAdd(&a.aux->done, 1u) == (uint32_t)(a.g0 + a.g1 - 1);
     }
-    // host-mapped copy of (vis, N_c, ndeg, 0, P, E): the host's one read
-    // needs no device-to-host copy in the stream
-    if (mirror) {
-        if (blockIdx.x == 0 && threadIdx.x < 5)
-            mirror[threadIdx.x] = threadIdx.x < 4 ? counters[threadIdx.x] : totals[0];
-        if (blockIdx.x == 1 && threadIdx.x == 0) mirror[5] = totals[1];
+    __syncthreads();
+    if (s_last) {   // every CTA has read the histograms: leave them zeroed
+        __threadfence();
+        if (threadIdx.x < 2 * kBuckets) {
+            (&a.aux->hist[0][0])[threadIdx.x] = 0;
+            (&a.aux->cur[0][0])[threadIdx.x] = 0;
+        }
+        if (threadIdx.x == 0) a.aux->done = 0;
     }
 }
 
@@ -1061,15 +1088,19 @@ st_sort_emit_kernel(const int32_t* __restrict__ st_offsets, int st_x, unsigned l
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // bin state: tile counts (ntiles + 1) | super-tile counts (nst + 1) |
-// scatter cursors (nst) | spans (32 B per compact slot) | origin (4 B per
-// slot) | super-tile offsets (nst + 1) | super-tile schedule (nst, largest
-// first).
-// The count arrays come first (offsets independent of n_cap): zeroed once
-// before first use, accumulated by the count kernel, re-zeroed by the scan.
+// scatter cursors (nst) | scan histograms / cursors / chunk totals |
+// schedule bucket per tile and super-tile | spans (32 B per compact slot) |
+// origin (4 B per slot) | super-tile offsets (nst + 1) | super-tile schedule
+// (nst, largest first).
+// The count arrays and the scan's self-resetting words come first (offsets
+// independent of n_cap): zeroed once before first use, left zeroed by the
+// scan.
 struct StateLayout {
     int32_t* tile_cnt;
     int32_t* st_cnt;
     int32_t* cursor;
+    ScanAux* aux;
+    uint8_t* bucket;
     uint4* spans;
     uint32_t* origin;
     int32_t* st_offsets;
@@ -1077,7 +1108,7 @@ struct StateLayout {
 };
 inline size_t state_bytes(int n_cap, int ntiles) {
     const size_t n = (size_t)(n_cap > 0 ? n_cap : 1), t = (size_t)ntiles + 1;
-    return 5 * align256(t * 4) + align256(n * 32) + align256(n * 4);
+    return 6 * align256(t * 4) + align256(sizeof(ScanAux)) + align256(n * 32) + align256(n * 4);
 }
 inline StateLayout state_layout(void* state, int n_cap, int ntiles, int nst) {
     const size_t n = (size_t)(n_cap > 0 ? n_cap : 1);
@@ -1086,6 +1117,8 @@ inline StateLayout state_layout(void* state, int n_cap, int ntiles, int nst) {
     L.tile_cnt = reinterpret_cast<int32_t*>(p); p += align256((size_t)(ntiles + 1) * 4);
     L.st_cnt = reinterpret_cast<int32_t*>(p); p += align256((size_t)(nst + 1) * 4);
     L.cursor = reinterpret_cast<int32_t*>(p); p += align256((size_t)(nst + 1) * 4);
+    L.aux = reinterpret_cast<ScanAux*>(p); p += align256(sizeof(ScanAux));
+    L.bucket = reinterpret_cast<uint8_t*>(p); p += align256((size_t)(ntiles + 1) * 4);   // ntiles + nst bytes
     L.spans = reinterpret_cast<uint4*>(p); p += align256(n * 32);
     L.origin = reinterpret_cast<uint32_t*>(p); p += align256(n * 4);
     L.st_offsets = reinterpret_cast<int32_t*>(p); p += align256((size_t)(nst + 1) * 4);
@@ -1109,8 +1142,18 @@ void sb_launch_bin_prepare(const RasterRec* recs, const int32_t* counters, int n
     if (n_cap > 0)
         sb_launch(tile_count_kernel, (n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream, recs, counters,
                   n_cap, cam.tiles_x, cam.tiles_y, st_x, cam.W, cam.H, L.spans, L.origin, L.tile_cnt, L.st_cnt);
-    sb_launch(tile_scan_kernel, 2, kScanThreads, 0, stream, L.tile_cnt, tile_offsets, ntiles, L.st_cnt, L.st_offsets,
-              nst, totals, L.cursor, counters, mirror, L.st_sched);
+    ScanArgs a;
+    a.cnt[0] = L.tile_cnt; a.out[0] = tile_offsets; a.sched[0] = tile_offsets + ntiles + 1; a.n[0] = ntiles;
+    a.cnt[1] = L.st_cnt; a.out[1] = L.st_offsets; a.sched[1] = L.st_sched; a.n[1] = nst;
+    a.copy = L.cursor;
+    // chunks of kScanBlock * ipt counts, ipt chosen to keep the chunk count bounded
+    a.ipt = max(2, min(kMaxIpt, (ntiles + 255 * kScanBlock) / (256 * kScanBlock)));
+    const int chunk = kScanBlock * a.ipt;
+    a.g0 = max(1, (ntiles + chunk - 1) / chunk);
+    a.g1 = max(1, (nst + chunk - 1) / chunk);
+    a.bucket = L.bucket; a.aux = L.aux; a.totals = totals; a.counters = counters; a.mirror = mirror;
+    sb_launch(scan_local_kernel, a.g0 + a.g1, kScanBlock, 0, stream, a);
+    sb_launch(scan_finish_kernel, a.g0 + a.g1, kScanBlock, 0, stream, a);
 }
 
 // ---- finish --------------------------------------------------------------------
