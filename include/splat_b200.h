@@ -171,8 +171,9 @@ int sb_variance_score(const double* S, const double* M, const int32_t* C, int64_
 /* metrics.py:118-132 loss_and_grad, fused: (1 - lam) L1 + lam (1 - SSIM)
  * over (H, W, 3) float32 images and dL/d rendered.  target is float32, or
  * uint8 (value / 255) when target_u8 != NULL.  loss[0] (float64, device) is
- * written on the stream; accum: 2 float64 scratch, zeroed once before its
- * first use and left zeroed by every call. */
+ * written on the stream (by the kernel's last CTA; it may be mapped host
+ * memory); accum: 4 float64 (32 bytes) of scratch -- two sums and a ticket --
+ * zeroed once before its first use and left zeroed by every call. */
 int sb_loss_fwd_bwd(const float* rendered, const float* target, const uint8_t* target_u8, int32_t width,
                     int32_t height, float lam, float* grad, double* accum, double* loss, sb_stream_t stream);
 

@@ -112,7 +112,7 @@ KERNELS_PER_CALL = {
     "sb_morton_keys": 3, "sb_morton_encode": 1, "sb_permute_rows": 1, "sb_project_cull_compact": 1, "sb_bin_prepare": 3,
     "sb_bin_finish": 2, "sb_raster_fwd": 1, "sb_raster_bwd": 1, "sb_radix_sort_pairs_u64": 10,
     "sb_chain_projection_bwd": 1, "sb_adam_sparse": 1, "sb_variance_score": 1, "sb_lane_reduce": 1,
-    "sb_loss_fwd_bwd": 2,
+    "sb_loss_fwd_bwd": 1,
 }
 launch_count = {"n": 0}
 # optional per-call CUDA-event timing: {name: [(start_event, end_event), ...]}

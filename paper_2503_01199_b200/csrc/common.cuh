@@ -132,11 +132,6 @@ struct ProjOut {
 // sigmoid / normalisation, then float32), which the bit-exact forward needs.
 // The backward chain only needs them to float32 accuracy (gradient
 // tolerance), so it uses the float32 forms.
-// float32 division: IEEE round-to-nearest where the result must be
-// bit-exact, the two-instruction approximate form (<= 2 ulp) otherwise
-template <bool kExact>
-SB_INLINE float sb_pdiv(float a, float b) { return kExact ? __fdiv_rn(a, b) : __fdividef(a, b); }
-
 template <bool kExact = true>
 SB_INLINE void sb_project(const float* __restrict__ p, const CamDev& cam, ProjOut& o, double* s64 = nullptr) {
     // activations in float64, then rounded (projection.py:134-138)
@@ -156,7 +151,7 @@ SB_INLINE void sb_project(const float* __restrict__ p, const CamDev& cam, ProjOu
         for (int k = 0; k < 3; k++) o.col[k] = (float)sb_sigmoid((double)p[SB_COL_COL + k]);
         o.op = (float)sb_sigmoid((double)p[SB_COL_OPA]);
     } else {
-        for (int k = 0; k < 3; k++) o.s[k] = __expf(p[SB_COL_LS + k]);
+        for (int k = 0; k < 3; k++) o.s[k] = expf(p[SB_COL_LS + k]);   // the scale feeds every covariance term
         const float q0 = p[SB_COL_ROT], q1 = p[SB_COL_ROT + 1], q2 = p[SB_COL_ROT + 2], q3 = p[SB_COL_ROT + 3];
         const float rn = rsqrtf(fmaf(q3, q3, fmaf(q2, q2, fmaf(q1, q1, q0 * q0))));
         o.q[0] = q0 * rn; o.q[1] = q1 * rn; o.q[2] = q2 * rn; o.q[3] = q3 * rn;
@@ -191,8 +186,10 @@ SB_INLINE void sb_project(const float* __restrict__ p, const CamDev& cam, ProjOu
     }
     const float tzz = FMUL(tzs, tzs);
     float J[2][3];
-    J[0][0] = sb_pdiv<kExact>(cam.fx, tzs); J[0][1] = 0.0f; J[0][2] = sb_pdiv<kExact>(FMUL(-cam.fx, o.t[0]), tzz);
-    J[1][0] = 0.0f; J[1][1] = sb_pdiv<kExact>(cam.fy, tzs); J[1][2] = sb_pdiv<kExact>(FMUL(-cam.fy, o.t[1]), tzz);
+    // (IEEE divisions in both forms: the backward chain's near-plane rows
+    // are ill-conditioned in J)
+    J[0][0] = FDIV(cam.fx, tzs); J[0][1] = 0.0f; J[0][2] = FDIV(FMUL(-cam.fx, o.t[0]), tzz);
+    J[1][0] = 0.0f; J[1][1] = FDIV(cam.fy, tzs); J[1][2] = FDIV(FMUL(-cam.fy, o.t[1]), tzz);
     float A[2][3], S[2][2];
     for (int i = 0; i < 2; i++)
         for (int j = 0; j < 3; j++)

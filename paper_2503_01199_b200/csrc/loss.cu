@@ -15,7 +15,8 @@
 // pass is a register sliding window: a thread owns a short run of outputs
 // along the filter axis, loads the run + 10 inputs once from shared memory
 // and forms all outputs from registers.
-// Loss partial sums go to two float64 accumulators.
+// Loss partial sums go to two float64 accumulators; the last CTA to finish
+// (a ticket next to them) forms the loss and re-zeroes them.
 #include "common.cuh"
 
 namespace {
@@ -63,7 +64,8 @@ SB_INLINE float2 f2(float v) { return make_float2(v, v); }
 template <bool kU8>
 __global__ void __launch_bounds__(kThreads, 2)
 loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, const uint8_t* __restrict__ y_u8,
-            int W, int H, float lam, Win win, float* __restrict__ grad, double* __restrict__ accum)
+            int W, int H, float lam, Win win, float* __restrict__ grad, double* __restrict__ accum,
+            double* __restrict__ loss_out)
 {
     sb_pdl_begin();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -319,18 +321,23 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
         for (int q = 0; q < kThreads / 32; q++) { a += sm.red[0][q]; b += sm.red[1][q]; }
         atomicAdd(&accum[0], a);
         atomicAdd(&accum[1], b);
+        // the last CTA to finish forms the loss and leaves the accumulators
+        // and its ticket (accum[2]) zeroed for the next call
+        __threadfence();
+        unsigned long long* ticket = reinterpret_cast<unsigned long long*>(accum + 2);
+        const unsigned long long ncta = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+        if (atomicAdd(ticket, 1ull) == ncta - 1) {
+            __threadfence();
+            const double l1 = atomicAdd(&accum[0], 0.0), ss = atomicAdd(&accum[1], 0.0);
+            const double n = (double)W * H * 3.0;
+            const double ni = (double)(W - 2 * R) * (double)(H - 2 * R);
+            double l = (1.0 - lam) * l1 / n;
+            if (lam != 0.f) l += lam * (1.0 - (ni > 0 ? ss / (3.0 * ni) : 0.0));
+            *loss_out = l;
+            accum[0] = accum[1] = 0.0;
+            *ticket = 0ull;
+        }
     }
-}
-
-__global__ void loss_finalize_kernel(double* __restrict__ accum, int W, int H, float lam, double* loss)
-{
-    sb_pdl_begin();
-    const double n = (double)W * H * 3.0;
-    const double ni = (double)(W - 2 * R) * (double)(H - 2 * R);
-    double l = (1.0 - lam) * accum[0] / n;
-    if (lam != 0.f) l += lam * (1.0 - (ni > 0 ? accum[1] / (3.0 * ni) : 0.0));
-    loss[0] = l;
-    accum[0] = accum[1] = 0.0;   // left zeroed for the next call (no memset per call)
 }
 
 }  // namespace
@@ -353,7 +360,9 @@ void sb_launch_loss(const float* x, const float* y, const uint8_t* y_u8, int W, 
         attr = true;
     }
     dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, 3);
-    if (y_u8) sb_launch(loss_kernel<true>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum);
-    else sb_launch(loss_kernel<false>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum);
-    sb_launch(loss_finalize_kernel, 1, 1, 0, stream, accum, W, H, lam, loss);
+    if (y_u8)
+        sb_launch(loss_kernel<true>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum, loss);
+    else
+        sb_launch(loss_kernel<false>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum,
+                  loss);
 }
