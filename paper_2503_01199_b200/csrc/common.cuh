@@ -276,12 +276,33 @@ SB_INLINE bool sb_disc_hits_fast(float cx, float cy, float r, int tx, int ty, in
 // float64 differences of an integer and a float32 are exact and rounding is
 // monotone), so the hit set in a row is one contiguous interval [*a, *b];
 // find it by scanning in from both ends.  Returns b - a + 1 (0 if empty).
+// The row's dy, dy^2, r^2 and the dx-independent part of the margin are
+// formed once; each tile then costs its dx, q and the dx term of the margin.
+// (The margin's terms are summed in another order than sb_disc_hits_fast's;
+// all of them carry a 2^-19 relative inflation, far above that rounding, so
+// the float32 verdict is still only taken outside the true error bound.)
 SB_INLINE int sb_row_hits(float cx, float cy, float r, int ty, int tx0, int tx1, int W, int H, int& a, int& b) {
+    const int ry0 = ty * SB_TILE_H, ry1 = min(ry0 + SB_TILE_H - 1, H - 1);
+    const float dy = fmaxf(fmaxf((float)ry0 - cy, cy - (float)ry1), 0.0f);
+    const float rr = FMUL(r, r), dy2 = dy * dy;
+    constexpr float kInfl = 1.0000019f;                            // 1 + 2^-19
+    const float E = (fabsf(cx) + fabsf(cy) + (float)(W + H)) * (1.1920929e-7f * kInfl);
+    const float mrow = fmaf(2.0f * (dy + E), E, rr * (2.384185791e-7f * kInfl)) + 1e-30f;
+    const float e2 = 2.0f * E;
+    const auto hit = [&](int tx) {
+        const int rx0 = tx * SB_TILE_W, rx1 = min(rx0 + SB_TILE_W - 1, W - 1);
+        const float dx = fmaxf(fmaxf((float)rx0 - cx, cx - (float)rx1), 0.0f);
+        const float q = fmaf(dx, dx, dy2);
+        const float m = fmaf(e2, dx, fmaf(q, 2.384185791e-7f * kInfl, mrow));
+        if (q < rr - m) return true;
+        if (q > rr + m) return false;
+        return sb_disc_hits(cx, cy, r, tx, ty, W, H);
+    };
     a = tx0;
-    while (a <= tx1 && !sb_disc_hits_fast(cx, cy, r, a, ty, W, H)) a++;
+    while (a <= tx1 && !hit(a)) a++;
     if (a > tx1) return 0;
     b = tx1;
-    while (b > a && !sb_disc_hits_fast(cx, cy, r, b, ty, W, H)) b--;
+    while (b > a && !hit(b)) b--;
     return b - a + 1;
 }
 
