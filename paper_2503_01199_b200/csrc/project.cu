@@ -156,6 +156,8 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
             atomicExch(ticket, 0u);
             atomicExch(ticket + 1, 0u);
         }
+        // thread 0 has read the last cluster's status before anyone clears it
+        __syncthreads();
         for (int i = threadIdx.x; i < n_clusters; i += blockDim.x) status[i] = 0ull;
     }
 }
