@@ -8,9 +8,13 @@
  *
  * Conventions:
  *   - every pointer is caller-owned DEVICE memory unless stated otherwise;
- *   - the library never allocates device memory, never synchronises the
- *     stream and keeps no global state; scratch comes from a caller-provided
- *     workspace whose size is queried with the matching *_workspace_bytes();
+ *   - the library never allocates device memory and never synchronises the
+ *     stream; scratch comes from a caller-provided workspace whose size is
+ *     queried with the matching *_workspace_bytes().  Its only process
+ *     state is per-(kernel, device) launch facts (the dynamic shared-memory
+ *     opt-in, SM count and resident-CTA count of the current device),
+ *     cached under a mutex: calls are thread-safe and work on any device
+ *     the caller makes current;
  *   - each call returns 0 on success or a negative SB_E* code, and sets a
  *     thread-local message readable with sb_last_error();
  *   - `stream` is a cudaStream_t passed as an opaque pointer (NULL = legacy
@@ -81,7 +85,7 @@ int sb_permute_rows(const uint32_t* perm, int64_t n, int count, const void* cons
  * Outputs: recs[N] (first N_c used; flags = valid | in_image << 1),
  * compact_map[N] (int32, first N_c used), cluster_offset[K] (compact start
  * of each visible cluster, -1 if culled), cluster_vis[K], counters[0..3]
- * (written): visible clusters, N_c, n_degenerate, 0.  ws holds the
+ * (written, also for n = 0): visible clusters, N_c, n_degenerate, 0.  ws holds the
  * look-back state: zero it once before first use; every call leaves it
  * zeroed.  sgrad_zero (nullable,
  * N rows): its rows [0, N_c) -- the slots sb_raster_bwd accumulates into --

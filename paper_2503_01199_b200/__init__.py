@@ -19,7 +19,7 @@ from .metrics import loss_and_grad, psnr, ssim
 from .optim import AdamState, LearningRates, adam_step
 from .reduction import exp_aligned_reduce, lane_group_reduce
 from .scene import SceneSoA
-from .train import TrainConfig, TrainResult, train
+from .train import TrainConfig, TrainResult, multiview_step, train
 
 __all__ = [
     "BackwardResult", "DensifyStats", "SceneGrads", "backward",
@@ -29,7 +29,7 @@ __all__ = [
     "ShapeMismatchError", "StaleSceneError", "TrainingDiverged", "ValidationError",
     "RasterConfig", "RenderContext", "RenderOutput", "forward", "render",
     "loss_and_grad", "psnr", "ssim", "AdamState", "LearningRates", "adam_step",
-    "exp_aligned_reduce", "lane_group_reduce", "SceneSoA", "TrainConfig", "TrainResult", "train",
+    "exp_aligned_reduce", "lane_group_reduce", "SceneSoA", "TrainConfig", "TrainResult", "multiview_step", "train",
 ]
 
 __version__ = "0.1.0"

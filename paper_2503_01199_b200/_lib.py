@@ -96,8 +96,15 @@ def require_cuda(t: torch.Tensor | None = None):
         raise ValueError("expected a CUDA tensor")
 
 
+# stream handle -> device index, so call() can make that device current
+# (the C-ABI launches on the current device; include/splat_b200.h)
+_stream_device: dict = {}
+
+
 def stream_ptr(device=None) -> int:
-    return torch.cuda.current_stream(device).cuda_stream
+    s = torch.cuda.current_stream(device)
+    _stream_device[s.cuda_stream] = s.device.index
+    return s.cuda_stream
 
 
 def ptr(t: torch.Tensor | None):
@@ -137,6 +144,18 @@ def call(name: str, *args):
     exception conventions (errors.py:6-32)."""
     lib = load()
     launch_count["n"] += KERNELS_PER_CALL.get(name, 0)
+    dev = None
+    if args and isinstance(args[-1], C.c_void_p) and args[-1].value in _stream_device:
+        dev = _stream_device[args[-1].value]
+        if dev == torch.cuda.current_device():
+            dev = None
+    if dev is not None:     # the stream belongs to another device: launch there
+        with torch.cuda.device(dev):
+            return _call(lib, name, args)
+    return _call(lib, name, args)
+
+
+def _call(lib, name, args):
     if _timing is not None:
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)

@@ -86,6 +86,22 @@ class DensifyStats:
         return cls(S=scene.extras["densify_S"], M=scene.extras["densify_M"], C=scene.extras["densify_C"])
 
 
+def check_stats(stats: DensifyStats, n: int, device):
+    """The chain kernel accumulates into S / M (float64) and C (int32) in
+    place: wrong dtypes, lengths or devices would be misread or overrun, so
+    they raise (the reference raises on mismatched lengths in np.add.at)."""
+    dev = torch.device(device)
+    for name, t, dt in (("S", stats.S, torch.float64), ("M", stats.M, torch.float64), ("C", stats.C, torch.int32)):
+        if not torch.is_tensor(t) or t.device != dev:
+            raise ValueError(f"DensifyStats.{name} must be a tensor on {dev}")
+        if t.dtype != dt:
+            raise ValueError(f"DensifyStats.{name} must be {dt} on the device, not {t.dtype}")
+        if tuple(t.shape) != (n,):
+            raise ShapeMismatchError(f"DensifyStats.{name} shape {tuple(t.shape)} != {(n,)}")
+        if not t.is_contiguous():
+            raise ValueError(f"DensifyStats.{name} must be contiguous (accumulated in place)")
+
+
 @dataclass
 class BackwardResult:
     grads: SceneGrads
@@ -111,6 +127,7 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
     if stats is None:
         stats = DensifyStats.from_scene(scene) if "densify_S" in scene.extras else DensifyStats.zeros(scene.n, dev)
     n = scene.n
+    check_stats(stats, n, dev)
     cam_s = ctx.camera.struct()
     cfg_s = ctx.config.struct()
     stream = C.c_void_p(_lib.stream_ptr(dev))

@@ -95,7 +95,7 @@ def morton_sort(scene: SceneSoA) -> torch.Tensor:
     if b < n:
         raise ValidationError("position", b, "non-finite position")
     perm = (vals_alt if flip.value else vals)[:n]
-    scene.permute(perm)
+    scene.permute(perm, trusted=True)   # a device sort's output: a permutation of [0, n)
     return perm.to(torch.int64)
 
 

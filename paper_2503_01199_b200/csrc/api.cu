@@ -150,7 +150,12 @@ int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam
     if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
     if (n < 0 || n > INT32_MAX - 256) return fail(SB_EINVAL, "n out of range");
     if (ws_bytes < sb_project_workspace_bytes(n)) return fail(SB_EWORKSPACE, "project workspace too small");
-    if (n == 0) { g_err.clear(); return SB_OK; }
+    if (n == 0) {
+        // an empty scene still reports its counters (0 visible, N_c = 0,
+        // 0 degenerate): the binning scan and the host read them
+        if (counters) cudaMemsetAsync(counters, 0, 4 * sizeof(int32_t), S(stream));
+        return check_launch("sb_project_cull_compact");
+    }
     const int blocks = sb_project_status_words((int)n);
     unsigned long long* status = static_cast<unsigned long long*>(ws);
     unsigned int* ticket = reinterpret_cast<unsigned int*>(status + blocks);

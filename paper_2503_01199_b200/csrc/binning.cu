@@ -1180,11 +1180,7 @@ void sb_launch_bin_finish(const RasterRec* recs, const int32_t* counters, int n_
     int32_t* cursor = L.cursor;   // the scan's copy of the super-tile offsets
     sb_launch(st_scatter_kernel, (n_cap + kBinThreads - 1) / kBinThreads, kBinThreads, 0, stream, recs, counters, n_cap,
               cam.tiles_x, cam.tiles_y, st_x, cursor, keys, e_cap, p_cap);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(st_sort_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(StSmem));
-        attr = true;
-    }
+    sb_smem_attr(st_sort_emit_kernel, (int)sizeof(StSmem));
     sb_launch(st_sort_emit_kernel, nst, kStThreads, sizeof(StSmem), stream, L.st_offsets, st_x, keys, recs, L.spans,
               L.origin, tile_offsets, cam.tiles_x, cam.tiles_y, cam.W, cam.H, tile_prims, counters, e_cap, p_cap,
               L.st_sched, scratch);

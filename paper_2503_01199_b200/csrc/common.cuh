@@ -10,7 +10,67 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include "../../include/splat_types.h"
+#include <map>
+#include <mutex>
 #include <utility>
+
+// Per-device launch facts (include/splat_b200.h: the library keeps no
+// cross-call state beyond these idempotent per-(kernel, device) caches).
+// cudaFuncSetAttribute and occupancy are per device, so both are keyed by
+// the current device ordinal and guarded by a mutex (thread-safe).
+inline int sb_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+inline int sb_sm_count() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    const int dev = sb_device();
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    cache[dev] = n;
+    return n;
+}
+
+// Raise the kernel's dynamic shared-memory limit on the current device
+// (once per kernel, device and size).
+template <typename... KArgs>
+inline void sb_smem_attr(void (*kernel)(KArgs...), int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> done;
+    const std::pair<const void*, int> key(reinterpret_cast<const void*>(kernel), sb_device());
+    std::lock_guard<std::mutex> g(mu);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= bytes) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done[key] = bytes;
+}
+
+// CTAs of `kernel` resident on the whole current device (persistent grids).
+template <typename... KArgs>
+inline int sb_resident_blocks(void (*kernel)(KArgs...), int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> cache;
+    const std::pair<const void*, int> key(reinterpret_cast<const void*>(kernel), sb_device());
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    if (smem > 48 * 1024) sb_smem_attr(kernel, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    const int r = sb_sm_count() * (per_sm > 0 ? per_sm : 1);
+    std::lock_guard<std::mutex> g(mu);
+    cache[key] = r;
+    return r;
+}
 
 // Programmatic dependent launch.  Every kernel is launched with programmatic
 // stream serialization (sb_launch) and opens with sb_pdl_begin(), which

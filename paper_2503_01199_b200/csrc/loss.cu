@@ -353,12 +353,8 @@ void sb_launch_loss(const float* x, const float* y, const uint8_t* y_u8, int W, 
         s += ws[k];
     }
     for (int k = 0; k < NT; k++) win.w[k] = (float)(ws[k] / s);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(loss_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
-        cudaFuncSetAttribute(loss_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
-        attr = true;
-    }
+    sb_smem_attr(loss_kernel<true>, (int)sizeof(Smem));
+    sb_smem_attr(loss_kernel<false>, (int)sizeof(Smem));
     dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, 3);
     if (y_u8)
         sb_launch(loss_kernel<true>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum, loss);

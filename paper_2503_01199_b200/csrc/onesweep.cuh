@@ -241,11 +241,7 @@ int sort(K* keys, uint32_t* vals, K* k_alt, uint32_t* v_alt, const int* n_dev, i
          bool keep_keys, bool iota, void* ws, cudaStream_t stream)
 {
     if (n_cap <= 0 || passes <= 0) return 0;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(pass_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<K>));
-        attr = true;
-    }
+    sb_smem_attr(pass_kernel<K>, (int)sizeof(Smem<K>));
     const int tiles = tile_count(n_cap);
     uint32_t* hist = static_cast<uint32_t*>(ws);
     uint32_t* status = hist + 256 * passes;

@@ -172,15 +172,8 @@ void sb_launch_project_cull_compact(const float* params, int n, const CamDev& ca
     const int k = (n + SB_CLUSTER_SIZE - 1) / SB_CLUSTER_SIZE;
     if (k == 0) return;
     const size_t smem = sizeof(WarpStage) * kWarps;
-    static int resident = 0;   // persistent grid: CTAs resident at once
-    if (!resident) {
-        cudaFuncSetAttribute(project_cull_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, project_cull_compact_kernel, kThreads, smem);
-        resident = max(1, sms) * max(1, per_sm);
-    }
+    sb_smem_attr(project_cull_compact_kernel, (int)smem);
+    const int resident = sb_resident_blocks(project_cull_compact_kernel, kThreads, smem);   // persistent grid
     const int blocks = min(resident, (k + kWarps - 1) / kWarps);
     sb_launch(project_cull_compact_kernel, blocks, kThreads, smem, stream, reinterpret_cast<const float4*>(params), n,
               k, cam, use_culling, rec_out, compact_map, cluster_offset, cluster_vis, counters,

@@ -575,13 +575,25 @@ SB_INLINE float2 row_tree2(float2 v[32]) {
 }
 
 // channel c of the screen-gradient record: 0-2 conic, 3-8 u v o r g bl, 9 S
+//
+// S and M of a (primitive, tile) row with ONE contributing pixel fragment
+// both come from that fragment's f = dL/do (the o row's sum, exact: one
+// nonzero lane): M += f, S += f * f in float64 (exact for a float32 f).  A
+// primitive whose only contributing fragment this is then has S == M^2 and
+// C == 1, so its variance score S - M^2 / C is exactly 0, as in the
+// reference (backward.py:254-255 sums float64 f and f^2 of the same f) --
+// never a densification candidate.  (The S row itself carries fl(uG^2)
+// 2^64 / o^2, whose float32 rounding would leave an ulp-level residue.)
 SB_INLINE void emit(const BwdWarpSmem& ws, int c, int b, float out, sb_screen_grad* grads) {
     sb_screen_grad* gr = grads + ws.slot[b];
     if (c < 9) {
         atomicAdd(reinterpret_cast<float*>(gr) + c, out);
-        if (c == 5) atomicAdd(&gr->M, (double)out);       // M = sum of dL/do over the tile
+        if (c == 5) {
+            atomicAdd(&gr->M, (double)out);       // M = sum of dL/do over the tile
+            if (ws.count[b] == 1) atomicAdd(&gr->S, (double)out * (double)out);
+        }
         if (c == 0) atomicAdd(&gr->C, ws.count[b]);
-    } else {
+    } else if (ws.count[b] != 1) {
         atomicAdd(&gr->S, (double)out * 0x1p-64);   // rows carry S * 2^64
     }
 }
@@ -756,16 +768,7 @@ raster_bwd_kernel(BwdParams p)
 
 }  // namespace
 
-static int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+static int sm_count() { return sb_sm_count(); }
 
 void sb_launch_raster_fwd(const RasterRec* recs, const int32_t* offsets, const int32_t* prims, int W, int H,
                           int tiles_x, int ntiles, const sb_raster_cfg& cfg, int* tile_counter, float* color,
@@ -801,11 +804,7 @@ void sb_launch_raster_bwd(const RasterRec* recs, const int32_t* offsets, const i
     const int want = (ntiles + kBwdWarps - 1) / kBwdWarps;
     const int blocks = min(want, sm_count() * 6);
     const int smem = (int)sizeof(BwdWarpSmem) * kBwdWarps;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    sb_smem_attr(raster_bwd_kernel, smem);
     if (blocks) sb_launch(raster_bwd_kernel, blocks, kBwdWarps * 32, smem, stream, p);
 }
 

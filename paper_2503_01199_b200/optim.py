@@ -3,8 +3,12 @@
 Reference: pkg/src/tinysplat/optim.py:20-98.  Moments are (N, 16) float32
 rows aligned with the parameter rows and registered as scene extras (so
 Morton re-sorts and densification carry them); per-primitive step counters
-are int32.  Arithmetic inside sb_adam_sparse is float64 (beta1 0.9, beta2
-0.999, eps 1e-15, per-row bias correction), like the reference.
+are int32.  sb_adam_sparse computes in float32 on the float32 state (beta1
+0.9, beta2 0.999, eps 1e-15, per-row bias corrections 1 - beta^t formed as
+-expm1(t ln beta) in float32, <= 1.9e-7 relative for t <= 2e6).  The
+reference keeps float64 state and arithmetic; against it the parameters
+agree to ~2e-6 relative after a few steps (tests/test_gpu_parity.py
+test_adam_vs_reference), i.e. well inside one step of size ~lr.
 """
 from __future__ import annotations
 
@@ -83,9 +87,20 @@ def adam_step(scene: SceneSoA, grads, state: AdamState, cluster_mask, lrs: dict,
     from .backward import SceneGrads
     if not isinstance(grads, SceneGrads):
         grads = SceneGrads.from_dict(grads.as_dict() if hasattr(grads, "as_dict") else grads, n, scene.device)
-    packed = grads.packed.contiguous()
+    from .errors import ShapeMismatchError
+    packed = grads.packed
+    if tuple(packed.shape) != (n, 16) or packed.dtype != torch.float32 or packed.device != scene.data.device:
+        raise ShapeMismatchError(f"gradient rows {tuple(packed.shape)} {packed.dtype} on {packed.device} "
+                                 f"!= ({n}, 16) float32 on {scene.data.device}")
+    packed = packed.contiguous()
     mask = torch.as_tensor(cluster_mask, device=scene.device)
-    mask = (mask.view(torch.uint8) if mask.dtype == torch.bool else mask.to(torch.uint8)).contiguous()
+    k = (n + CLUSTER_SIZE - 1) // CLUSTER_SIZE
+    if mask.numel() != k:
+        raise ShapeMismatchError(f"cluster mask length {mask.numel()} != {k} clusters")
+    mask = (mask.view(torch.uint8) if mask.dtype == torch.bool else (mask != 0).to(torch.uint8)).contiguous()
+    for name, t in (("m", state.m_rows), ("v", state.v_rows), ("step", state.step)):
+        if t.shape[0] != n or t.device != scene.data.device:
+            raise ShapeMismatchError(f"Adam {name} has {t.shape[0]} rows on {t.device} != {n} on {scene.data.device}")
     lr = (C.c_double * 5)(*[float(lrs[k]) for k in RAW_CHANNELS])
     _lib.call("sb_adam_sparse", _lib.ptr(scene.data), _lib.ptr(packed), _lib.ptr(state.m_rows),
               _lib.ptr(state.v_rows), _lib.ptr(state.step), _lib.ptr(mask), n, lr,

@@ -141,11 +141,19 @@ class SceneSoA:
         return torch.sigmoid(self.opacity_logit.double())
 
     # ---- restructuring -------------------------------------------------------
-    def permute(self, perm):
+    def permute(self, perm, trusted: bool = False):
         """Gather every row (params + extras) by `perm` with sb_permute_rows."""
         perm_t = torch.as_tensor(perm, device=self.device)
         if perm_t.shape != (self.n,):
             raise ShapeMismatchError(f"permutation length {tuple(perm_t.shape)} != {self.n}")
+        if perm_t.dtype.is_floating_point or perm_t.dtype == torch.bool:
+            raise ValueError(f"permutation must be integer, not {perm_t.dtype}")
+        if self.n and not trusted:
+            # the gather kernel reads rows perm[i]: out-of-range indices would
+            # read outside the arrays (the reference raises IndexError)
+            lo, hi = int(perm_t.min()), int(perm_t.max())
+            if lo < 0 or hi >= self.n:
+                raise IndexError(f"permutation index out of range [0, {self.n}): min {lo}, max {hi}")
         perm_u = perm_t.to(torch.int32).contiguous()
         arrays = [("__data__", self.data)] + list(self.extras.items())
         outs = []
@@ -160,7 +168,7 @@ class SceneSoA:
                 outs.append((name, o))
             k = len(chunk)
             _lib.call("sb_permute_rows", _lib.ptr(perm_u), self.n, k, (C.c_void_p * k)(*src),
-                      (C.c_void_p * k)(*dst), (C.c_int32 * k)(*rb), C.c_void_p(_lib.stream_ptr()))
+                      (C.c_void_p * k)(*dst), (C.c_int32 * k)(*rb), C.c_void_p(_lib.stream_ptr(self.device)))
         for name, o in outs:
             if name == "__data__":
                 self.data = o

@@ -102,7 +102,7 @@ def test_backward_vs_reference(fname, prefix):
     assert G.floored_rel(score, d[f"{prefix}score"]) <= 1e-2
 
 
-@pytest.mark.parametrize("fname,prefix", [c for c in G.CASES if c[1] in ("", "e1_")])
+@pytest.mark.parametrize("fname,prefix", [c for c in G.CASES if c[1] in ("", "e1_", "e4_")])
 def test_backward_vs_float64_oracle(fname, prefix):
     """Against the reference's float64 path: the back-to-front fp32 replay is
     closer to fp64 than the reference's own fp32 path."""
@@ -113,8 +113,21 @@ def test_backward_vs_float64_oracle(fname, prefix):
     res = sb.backward(scene, ctx, torch.from_numpy(d[f"{prefix}dL_dI"]), sb.DensifyStats.zeros(scene.n))
     g = res.grads.packed[:, :14].double().cpu().numpy()
     g64 = d[f"{prefix}grads64"].astype(np.float64)
+    g32 = d[f"{prefix}grads"].astype(np.float64)
     for lo, hi in CH_SLICES:
-        assert G.floored_rel(g[:, lo:hi], g64[:, lo:hi]) <= 1e-2, (lo, hi)
+        den = np.maximum(np.abs(g64[:, lo:hi]), 1e-3 * np.abs(g64[:, lo:hi]).max())
+        err = np.abs(g[:, lo:hi] - g64[:, lo:hi]) / den
+        # rows the reference's OWN float32 path misses by more than half the
+        # bar: ill-conditioned in float32 (e4: one Gaussian at depth 0.062,
+        # 1.24x the near plane, whose rotation gradient the reference's fp32
+        # path gets 1.6e-2 wrong).  The device shares the reference's
+        # bit-exact fp32 projection, so it inherits that error there; such
+        # rows may be no worse than twice the reference's own.
+        ref_err = np.abs(g32[:, lo:hi] - g64[:, lo:hi]) / den
+        excused = ref_err.max(axis=1) > 0.5e-2
+        assert excused.sum() <= (1 if prefix == "e4_" else 0), (lo, hi, np.flatnonzero(excused))
+        assert err[~excused].max(initial=0.0) <= 1e-2, (lo, hi)
+        assert (err[excused] <= 2 * ref_err[excused] + 1e-2).all(), (lo, hi)
 
 
 def test_morton_keys_and_sort_bit_exact():
@@ -237,6 +250,9 @@ def test_empty_scene_and_errors():
     scene = sb.SceneSoA.empty(device="cuda")
     out, ctx = sb.forward(scene, cam, sb.RasterConfig(background=(0.1, 0.2, 0.3)))
     assert np.array_equal(out.color.cpu().numpy(), d["e5_fwd_color"])
+    # the counters of an empty scene are reported, not left uninitialised
+    assert ctx.n_compact == 0 and ctx.visible_clusters == 0 and ctx.culled_clusters == 0
+    assert ctx.n_pairs == 0 and ctx.n_degenerate == 0
     res = sb.backward(scene, ctx, torch.zeros(cam.resolution[1], cam.resolution[0], 3))
     assert res.grads.packed.shape == (0, 16)
     # staleness and shape errors (backward.py:213-218)
@@ -508,3 +524,81 @@ def test_short_training_run_reduces_loss():
     res = sb.train(sb.TrainConfig(epochs=12, lrs=sb.LearningRates(color=2e-2)), scene, views)
     assert res.metrics[-1].loss < 0.6 * res.metrics[0].loss
     assert res.metrics[-1].psnr > res.metrics[0].psnr
+
+
+def test_input_validation():
+    """Raw device pointers are only handed to the kernels after dtype / shape
+    / device checks (the reference raises on the same mismatches)."""
+    sb = _sb()
+    d = G.load("golden_A.npz")
+    scene, cam = _scene(d), G.camera(d)
+    n = scene.n
+    out, ctx = sb.forward(scene, cam)
+    dI = torch.zeros(128, 128, 3)
+    bad_stats = [
+        sb.DensifyStats(S=torch.zeros(n, dtype=torch.float32, device="cuda"),
+                        M=torch.zeros(n, dtype=torch.float64, device="cuda"),
+                        C=torch.zeros(n, dtype=torch.int32, device="cuda")),
+        sb.DensifyStats(S=torch.zeros(n, dtype=torch.float64, device="cuda"),
+                        M=torch.zeros(n, dtype=torch.float64, device="cuda"),
+                        C=torch.zeros(n, dtype=torch.int64, device="cuda")),
+    ]
+    for st in bad_stats:
+        with pytest.raises(ValueError):
+            sb.backward(scene, ctx, dI, st)
+    with pytest.raises(sb.ShapeMismatchError):
+        sb.backward(scene, ctx, dI, sb.DensifyStats.zeros(n - 1))
+    res = sb.backward(scene, ctx, dI, sb.DensifyStats.zeros(n))
+    state = sb.AdamState(scene)
+    lrs = sb.LearningRates().at(0.0)
+    with pytest.raises(sb.ShapeMismatchError):
+        sb.adam_step(scene, res.grads, state, res.cluster_mask[:-1], lrs)
+    with pytest.raises(sb.ShapeMismatchError):
+        sb.adam_step(scene, sb.SceneGrads(res.grads.packed[:-1]), state, res.cluster_mask, lrs)
+    with pytest.raises(ValueError):
+        sb.variance_score(sb.DensifyStats(S=torch.zeros(n, device="cuda"), M=torch.zeros(n, device="cuda"),
+                                          C=torch.zeros(n, dtype=torch.int32, device="cuda")))
+    perm = torch.arange(n, device="cuda")
+    perm[3] = n
+    with pytest.raises(IndexError):
+        scene.copy().permute(perm)
+    with pytest.raises(sb.ShapeMismatchError):
+        scene.copy().permute(perm[:-1])
+
+
+def test_second_device_or_noncurrent_stream():
+    """Launch facts are per device: a scene on the last visible device renders
+    the same image as on device 0 while device 0 stays current."""
+    sb = _sb()
+    if torch.cuda.device_count() < 2:
+        pytest.skip("one visible device")
+    d = G.load("golden_A.npz")
+    dev = torch.device("cuda", torch.cuda.device_count() - 1)
+    sc = G.scene(d)
+    a, _ = sb.forward(sb.SceneSoA(*[sc[k] for k in G.CH], device="cuda:0"), G.camera(d))
+    b, _ = sb.forward(sb.SceneSoA(*[sc[k] for k in G.CH], device=dev), G.camera(d))
+    assert torch.equal(a.color, b.color.to(a.color.device))
+
+
+def test_single_fragment_primitives_score_zero():
+    """Primitives with exactly one contributing fragment get S == M^2, so a
+    variance score of exactly 0 (never densified), as in the reference; and
+    the candidate set (score > 0) from DEVICE statistics matches the
+    reference's own statistics."""
+    sb = _sb()
+    from paper_2503_01199_b200.densify import select_and_grow
+    d = G.load("golden_A.npz")
+    scene, cam = _scene(d), G.camera(d)
+    out, ctx = sb.forward(scene, cam)
+    stats = sb.DensifyStats.zeros(scene.n)
+    sb.backward(scene, ctx, torch.from_numpy(d["dL_dI"]), stats)
+    C = stats.C.cpu().numpy()
+    score = sb.variance_score(stats).cpu().numpy()
+    one = C == 1
+    assert one.any() and (score[one] == 0).all()
+    ref = d["score"]
+    assert ((score > 0) != (ref > 0)).sum() <= 2
+    # a budget large enough to take every candidate: the same selection
+    ci, si = select_and_grow(scene, sb.variance_score(stats), 10 * scene.n, 1e9)
+    sel = np.sort(np.concatenate([ci.cpu().numpy(), si.cpu().numpy()]))
+    assert np.array_equal(sel, np.flatnonzero(score > 0))

@@ -1,0 +1,396 @@
+"""Parity at the BASELINE configurations themselves (not only the fixtures).
+
+  config B   1M Gaussians, 1920x1080 (the bench config): image, gradients,
+             S / M / C and the variance score against the CPU oracle on the
+             same Morton-sorted scene and the same dL/dI; the projection,
+             validity and in-image hashes the reference produced for B, C, E
+             (tests/golden/golden_big.json, tools/make_golden.py --big)
+  config D   8 views of config B per optimiser step: SUM_v backward grads,
+             summed statistics, OR-ed masks and ONE Adam step against the
+             oracle's per-view backward summed + its adam_step (
+             reference train.py:95-104, optim.py:69-98); and the same step
+             with the views split over two ranks (gloo on the one GPU)
+  criterion 9   the reference's standard-scene fit (test_acceptance.py:47-80,
+             353-364): 512-Gaussian ground truth, 8 views at 128x128, seed
+             112, perturbed 64-Gaussian init, FAST_LRS, 60 epochs, budget 512
+             must reach the calibrated final PSNR >= 31.2 dB
+  criterion 11  the half-precision path within 60 dB of float32 on the
+             standard scene (test_acceptance.py:382-394)
+
+Bars as in test_gpu_parity.py: bit-exact integer stages, image <= 1e-3 max
+abs, gradients / S / M / score <= 1e-2 floored relative; C (and frag counts)
+exact except alpha / T threshold flips, whose number is bounded
+here and printed.
+"""
+import hashlib
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from tests import goldens as G
+
+pytestmark = pytest.mark.gpu
+
+CH_SLICES = ((0, 3), (3, 6), (6, 10), (10, 13), (13, 14))
+# threshold flips per million blended fragments allowed in
+# frag_count / C (the reference's own exp is ~2.5 ulp; ours ex2 a few ulp)
+FLIPS_PER_M_FRAGMENTS = 2.0
+
+
+def _sb():
+    import paper_2503_01199_b200 as sb
+    return sb
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _host_arrays(scene):
+    h = scene.data.cpu().numpy().astype(np.float64)
+    return {"position": h[:, 0:3], "log_scale": h[:, 3:6], "rotation": h[:, 6:10], "color": h[:, 10:13],
+            "opacity_logit": h[:, 13]}
+
+
+def _config_scene(n, res, n_views, seed=7):
+    sb = _sb()
+    from paper_2503_01199_b200.synthetic import SyntheticSceneSpec, camera_ring, scaled_scene_arrays
+    arr = scaled_scene_arrays(n, seed, res)
+    scene = sb.SceneSoA(*[arr[k] for k in G.CH], device="cuda")
+    sb.morton_sort(scene)
+    cams = camera_ring(SyntheticSceneSpec(n_gaussians=n, n_views=n_views, view_resolution=res, seed=seed))
+    return scene, cams
+
+
+def _check_grads(g, ref, what):
+    worst = []
+    for lo, hi in CH_SLICES:
+        r = G.floored_rel(g[:, lo:hi], ref[:, lo:hi])
+        worst.append(r)
+        assert r <= 1e-2, (what, lo, hi, r)
+    return worst
+
+
+@pytest.fixture(scope="module")
+def config_b():
+    """Device and oracle forward + backward of config B, view 0."""
+    sb = _sb()
+    scene, cams = _config_scene(1_000_000, (1920, 1080), 1)
+    cam = cams[0]
+    arr = _host_arrays(scene)
+    out, ctx = sb.forward(scene, cam)
+    col, T, frags, octx = O.forward(arr, cam, O.RasterConfig())
+    rng = np.random.default_rng(2024)
+    target = rng.uniform(0, 1, col.shape)
+    # the same dL/dI for both backwards: the oracle's loss on the oracle image
+    _, dI = O.loss_and_grad(col, target, 0.2)
+    dI = dI.astype(np.float32)
+    stats = sb.DensifyStats.zeros(scene.n)
+    res = sb.backward(scene, ctx, torch.from_numpy(dI), stats)
+    ob = O.backward(arr, octx, dI)
+    return dict(scene=scene, cam=cam, out=out, ctx=ctx, res=res, stats=stats, col=col, T=T, frags=frags,
+                octx=octx, ob=ob)
+
+
+def test_config_B_forward_full_image(config_b):
+    c = config_b
+    out, ctx, octx = c["out"], c["ctx"], c["octx"]
+    assert np.array_equal(ctx.compact_map.cpu().numpy(), octx.compact_map)
+    assert np.array_equal(ctx.tile_offsets.cpu().numpy().astype(np.int64), octx.tile_offsets)
+    assert np.array_equal(ctx.tile_prims.cpu().numpy().astype(np.int64), octx.prims)
+    err = float(np.abs(out.color.cpu().numpy() - c["col"]).max())
+    terr = float(np.abs(out.transmittance.cpu().numpy() - c["T"]).max())
+    fr = out.frag_count.cpu().numpy()
+    flips = int((fr != c["frags"]).sum())
+    total = int(c["frags"].sum())
+    print(f"config B: image max abs {err:.2e}, T {terr:.2e}, frag-count flips {flips} of {total} fragments")
+    assert err <= 1e-3 and terr <= 1e-3
+    assert flips <= FLIPS_PER_M_FRAGMENTS * total / 1e6
+
+
+def test_config_B_gradients_and_stats(config_b):
+    sb = _sb()
+    c = config_b
+    ob, res, stats = c["ob"], c["res"], c["stats"]
+    g = res.grads.packed[:, :14].double().cpu().numpy()
+    worst = _check_grads(g, ob["grads"], "config B grads")
+    S, M, Cn = stats.S.cpu().numpy(), stats.M.cpu().numpy(), stats.C.cpu().numpy()
+    rs, rm = G.floored_rel(S, ob["S"]), G.floored_rel(M, ob["M"])
+    flips = int((Cn != ob["C"]).sum())
+    total = int(ob["C"].sum())
+    score = sb.variance_score(stats).cpu().numpy()
+    oscore = O.variance_score(ob["S"], ob["M"], ob["C"])
+    rsc = G.floored_rel(score, oscore)
+    print(f"config B: grads worst per channel {[f'{w:.1e}' for w in worst]}, S {rs:.1e}, M {rm:.1e}, "
+          f"score {rsc:.1e}, C flips {flips} of {total}")
+    assert rs <= 1e-2 and rm <= 1e-2 and rsc <= 1e-2
+    assert flips <= FLIPS_PER_M_FRAGMENTS * total / 1e6
+    assert np.array_equal(res.cluster_mask.cpu().numpy(), ob["cluster_mask"])
+    # single-fragment primitives score exactly 0, as in the reference
+    one = (Cn == 1) & (ob["C"] == 1)
+    assert one.any() and (score[one] == 0).all() and (oscore[one] == 0).all()
+    # the densify candidate set (score > 0) matches the reference's
+    pos, opos = score > 0, oscore > 0
+    print(f"config B: positive scores {int(pos.sum())} vs oracle {int(opos.sum())}, "
+          f"differing {int((pos != opos).sum())}")
+    assert (pos != opos).sum() <= flips + 2
+
+
+@pytest.mark.parametrize("name", ["B", "C", "E"])
+def test_big_configs_projection_hashes(name):
+    """The reference's full-length projected arrays (invalid rows zeroed),
+    validity and in-image masks at configs B / C / E, hash-identical: with
+    culling off the compact records are every Gaussian in Morton order."""
+    sb = _sb()
+    gb = G.load("golden_big.json")[name]
+    n, res = gb["n"], tuple(gb["res"])
+    scene, cams = _config_scene(n, res, 1)
+    out, ctx = sb.forward(scene, cams[0], sb.RasterConfig(use_culling=False))
+    assert ctx.n_compact == n
+    assert np.array_equal(ctx.compact_map.cpu().numpy(), np.arange(n))
+    p = {k: v.cpu().numpy() for k, v in ctx.projected.items()}
+    valid = p["valid"]
+    assert _sha(valid.astype(np.uint8)) == gb["proj_valid_sha"]
+    assert _sha(p["in_image"].astype(np.uint8)) == gb["proj_in_image_sha"]
+    for k in ("xy", "depth", "conic", "radius"):
+        a = np.ascontiguousarray(p[k], dtype=np.float32).copy()
+        a[~valid] = 0
+        assert _sha(a) == gb[f"proj_{k}_sha_valid"], k
+    if name == "B":
+        # exactly-invisible culling: the culled render is the same image
+        out_c, ctx_c = sb.forward(scene, cams[0])
+        assert torch.equal(out.color, out_c.color) and torch.equal(out.frag_count, out_c.frag_count)
+
+
+def _floor_den(g):
+    """Per-entry denominator of the floored rule, per channel group."""
+    den = np.empty_like(g)
+    for lo, hi in CH_SLICES:
+        den[:, lo:hi] = np.maximum(np.abs(g[:, lo:hi]), 1e-3 * np.abs(g[:, lo:hi]).max())
+    return den
+
+
+def _oracle_multiview(arr, cams, dIs):
+    """Oracle SUM_v backward + the per-entry tolerance of the sum: the sum of
+    the per-view floored denominators (each view is held to 1e-2 of its own;
+    a sum that cancels cannot be held to 1e-2 of the cancelled value)."""
+    g = np.zeros((len(arr["position"]), 14))
+    den = np.zeros_like(g)
+    S = np.zeros(len(g)); M = np.zeros(len(g)); Cn = np.zeros(len(g), np.int64)
+    Sden = np.zeros(len(g)); Mden = np.zeros(len(g))
+    mask = None
+    for cam, dI in zip(cams, dIs):
+        col, T, frags, octx = O.forward(arr, cam, O.RasterConfig())
+        ob = O.backward(arr, octx, dI)
+        g += ob["grads"]
+        den += _floor_den(ob["grads"])
+        S += ob["S"]; M += ob["M"]; Cn += ob["C"]
+        Sden += np.maximum(np.abs(ob["S"]), 1e-3 * np.abs(ob["S"]).max())
+        Mden += np.maximum(np.abs(ob["M"]), 1e-3 * np.abs(ob["M"]).max())
+        mask = ob["cluster_mask"] if mask is None else (mask | ob["cluster_mask"])
+    return g, den, S, M, Cn, mask, Sden, Mden
+
+
+def _check_sum(got, ref, den, what):
+    """|sum_dev - sum_ref| <= 1e-2 * (sum of the per-view floored
+    denominators); also prints the plain floored rule on the sum."""
+    worst = []
+    for lo, hi in CH_SLICES:
+        r = float((np.abs(got[:, lo:hi] - ref[:, lo:hi]) / den[:, lo:hi]).max())
+        worst.append((r, G.floored_rel(got[:, lo:hi], ref[:, lo:hi])))
+        assert r <= 1e-2, (what, lo, hi, r)
+    print(f"{what}: per channel (vs summed per-view bar, plain floored rule on the sum) "
+          f"{[(f'{a:.1e}', f'{b:.1e}') for a, b in worst]}")
+
+
+@pytest.fixture(scope="module")
+def config_d():
+    """8 views of config B: one device multi-view step vs the oracle sum."""
+    sb = _sb()
+    scene, cams = _config_scene(1_000_000, (1920, 1080), 8)
+    arr = _host_arrays(scene)
+    p0 = scene.data[:, :14].double().cpu().numpy()
+    rng = np.random.default_rng(99)
+    W, H = cams[0].resolution
+    targets = [torch.from_numpy(rng.uniform(0, 1, (H, W, 3)).astype(np.float32)).cuda() for _ in cams]
+    # dL/dI of each view from the device image, fed to both backwards
+    dIs = []
+    for cam, t in zip(cams, targets):
+        out, _ = sb.forward(scene, cam)
+        _, dI = sb.loss_and_grad(out.color, t, 0.2, return_tensor=True)
+        dIs.append(dI.cpu().numpy())
+    state = sb.AdamState(scene)
+    stats = sb.DensifyStats.zeros(scene.n)
+    lrs = sb.LearningRates().at(0.0, position_scale=3.2)
+    # device step with the fixed dL/dI (multiview_step forms dI itself; the
+    # sum-then-one-Adam semantics are the same)
+    acc = torch.zeros((scene.n, 16), dtype=torch.float32, device="cuda")
+    mask = torch.zeros((scene.n + 127) // 128, dtype=torch.bool, device="cuda")
+    for cam, dI in zip(cams, dIs):
+        out, ctx = sb.forward(scene, cam)
+        r = sb.backward(scene, ctx, torch.from_numpy(dI), stats)
+        acc += r.grads.packed
+        mask |= r.cluster_mask
+    g_dev = acc[:, :14].double().cpu().numpy()
+    sb.adam_step(scene, sb.SceneGrads(acc), state, mask, lrs)
+    og, oden, oS, oM, oC, omask, oSden, oMden = _oracle_multiview(arr, cams, dIs)
+    # the oracle's one Adam step on the float64 parameters
+    params = np.ascontiguousarray(p0)
+    m = np.zeros_like(params); v = np.zeros_like(params)
+    step = np.zeros(len(params), np.int64)
+    lr14 = np.array([lrs[c] for c in G.CH])
+    O.adam_step(params, np.ascontiguousarray(og), m, v, step, omask, lr14)
+    return dict(scene=scene, cams=cams, dIs=dIs, targets=targets, g_dev=g_dev, mask=mask.cpu().numpy(),
+                stats=stats, p0=p0, og=og, oden=oden, oS=oS, oM=oM, oC=oC, omask=omask, oSden=oSden,
+                oMden=oMden, oparams=params, lrs=lrs)
+
+
+def test_config_D_multiview_sum_and_adam(config_d):
+    c = config_d
+    _check_sum(c["g_dev"], c["og"], c["oden"], "config D summed grads")
+    assert np.array_equal(c["mask"], c["omask"])
+    st = c["stats"]
+    rs = float((np.abs(st.S.cpu().numpy() - c["oS"]) / c["oSden"]).max())
+    rm = float((np.abs(st.M.cpu().numpy() - c["oM"]) / c["oMden"]).max())
+    flips = int((st.C.cpu().numpy() != c["oC"]).sum())
+    print(f"config D: S {rs:.1e}, M {rm:.1e}, C flips {flips} of {int(c['oC'].sum())}")
+    assert rs <= 1e-2 and rm <= 1e-2
+    assert flips <= FLIPS_PER_M_FRAGMENTS * c["oC"].sum() / 1e6
+    # one Adam step from zero moments moves each updated entry by lr * sign(g)
+    # (H12: |delta| <= 2 lr_channel); sign flips only where the summed
+    # gradient is at rounding level
+    got = c["scene"].data[:, :14].double().cpu().numpy()
+    lr14 = np.repeat([c["lrs"][k] for k in G.CH], [3, 3, 4, 3, 1])
+    d = np.abs(got - c["oparams"])
+    assert (d <= 2 * lr14 * (1 + 1e-5) + 1e-6 * np.abs(c["oparams"])).all()
+    flipped = d > 0.5 * lr14
+    if flipped.any():
+        assert (np.abs(c["og"])[flipped] <= 1e-2 * c["oden"][flipped]).all()
+    print(f"config D: post-Adam parameters, {int(flipped.sum())} sign-level flips of {flipped.size}")
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _d_worker(rank, world, port, dI_path, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        sb = _sb()
+        from paper_2503_01199_b200.parallel import ViewParallel
+        vp = ViewParallel()
+        scene, cams = _config_scene(1_000_000, (1920, 1080), 8)
+        dIs = np.load(dI_path)
+        state = sb.AdamState(scene)
+        stats = sb.DensifyStats.zeros(scene.n)
+        lrs = sb.LearningRates().at(0.0, position_scale=3.2)
+        acc = torch.zeros((scene.n, 16), dtype=torch.float32, device="cuda")
+        mask = torch.zeros((scene.n + 127) // 128, dtype=torch.bool, device="cuda")
+        for v in range(rank, 8, world):     # this rank's views
+            _, ctx = sb.forward(scene, cams[v])
+            r = sb.backward(scene, ctx, torch.from_numpy(dIs[v]), stats)
+            acc += r.grads.packed
+            mask |= r.cluster_mask
+        mask = vp.reduce_grads(acc, mask)
+        g = acc[:, :14].cpu().numpy().copy()
+        sb.adam_step(scene, sb.SceneGrads(acc), state, mask, lrs)
+        vp.reduce_stats(stats.S, stats.M, stats.C)
+        out[rank] = dict(g=g, params=scene.data[:, :14].cpu().numpy(), mask=mask.cpu().numpy(),
+                         S=stats.S.cpu().numpy(), C=stats.C.cpu().numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_config_D_two_ranks_vs_oracle(config_d, tmp_path):
+    """The same step with views 0,2,4,6 on rank 0 and 1,3,5,7 on rank 1 and
+    one all-reduce: ranks identical, sums within tolerance of the oracle."""
+    import torch.multiprocessing as mp
+    c = config_d
+    path = str(tmp_path / "dI.npy")
+    np.save(path, np.stack(c["dIs"]))
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_d_worker, args=(2, _free_port(), path, out), nprocs=2, join=True, start_method="spawn")
+    a, b = out[0], out[1]
+    assert np.array_equal(a["params"], b["params"]) and np.array_equal(a["g"], b["g"])
+    assert np.array_equal(a["mask"], c["omask"])
+    _check_sum(a["g"].astype(np.float64), c["og"], c["oden"], "config D two-rank grads")
+    assert (np.abs(a["S"] - c["oS"]) <= 1e-2 * c["oSden"]).all()
+    assert (a["C"] != c["oC"]).sum() <= FLIPS_PER_M_FRAGMENTS * c["oC"].sum() / 1e6
+    lr14 = np.repeat([c["lrs"][k] for k in G.CH], [3, 3, 4, 3, 1])
+    d = np.abs(a["params"].astype(np.float64) - c["oparams"])
+    assert (d <= 2 * lr14 * (1 + 1e-5) + 1e-6 * np.abs(c["oparams"])).all()
+
+
+# ---- the reference's standard scene (test_acceptance.py:47-80) -------------
+FAST_LRS = dict(position=3.2e-3, position_final=3.2e-5, log_scale=0.1, rotation=0.02, color=0.05,
+                opacity_logit=0.1)
+FIT_THRESHOLD = 31.700 - 0.5     # test_acceptance.py:28-29 (REF64_PSNR - 0.5)
+HALF_PSNR_FLOOR = 60.0           # test_acceptance.py:31
+
+
+def _standard_scene():
+    """512 ground-truth Gaussians, 8 views at 128x128, seed 112; targets are
+    float64 renders (the oracle's float64 path, pinned to the reference's
+    fwd64 fixtures)."""
+    from paper_2503_01199_b200.synthetic import SyntheticSceneSpec, camera_ring, random_scene_arrays
+    spec = SyntheticSceneSpec(n_gaussians=512, n_views=8, view_resolution=(128, 128), seed=112)
+    gt = random_scene_arrays(spec)
+    cams = camera_ring(spec)
+    views = [(c, O.forward(gt, c, O.RasterConfig(dtype="float64"))[0]) for c in cams]
+    return gt, views
+
+
+def _perturbed_init(gt, n=64, seed=77):
+    """test_acceptance.py:61-71, draw for draw."""
+    rng = np.random.default_rng(seed)
+    idx = rng.choice(len(gt["position"]), size=n, replace=False)
+    return {
+        "position": gt["position"][idx] + rng.normal(0, 0.08, (n, 3)),
+        "log_scale": gt["log_scale"][idx] + rng.normal(0, 0.25, (n, 3)),
+        "rotation": gt["rotation"][idx] + rng.normal(0, 0.1, (n, 4)),
+        "color": gt["color"][idx] + rng.normal(0, 0.4, (n, 3)),
+        "opacity_logit": gt["opacity_logit"][idx] + rng.normal(0, 0.3, n),
+    }
+
+
+def test_criterion_09_standard_fit():
+    """Reference acceptance criterion 9 through the device path: the
+    standard fit reaches the calibrated threshold (reference float32 result
+    31.754 dB, float64 31.700 dB; threshold 31.2 dB)."""
+    sb = _sb()
+    gt, views = _standard_scene()
+    init = _perturbed_init(gt)
+    scene = sb.SceneSoA(*[init[k] for k in G.CH], device="cuda")
+    cfg = sb.TrainConfig(epochs=60, lrs=sb.LearningRates(**FAST_LRS), seed=5,
+                         raster=sb.RasterConfig(dtype="float32"), densify=sb.DensifyConfig(budget=512))
+    res = sb.train(cfg, scene, views)
+    got = res.metrics[-1].psnr
+    print(f"criterion 9: final PSNR {got:.3f} dB (threshold {FIT_THRESHOLD:.2f}, reference fp32 31.754), "
+          f"{scene.n} primitives, {len(res.densify_log)} densify events")
+    assert got >= FIT_THRESHOLD
+
+
+def test_criterion_11_half_precision_standard_scene():
+    """Reference acceptance criterion 11: fp16 blending state within
+    HALF_PSNR_FLOOR dB of float32 on the standard scene's first three views
+    (the reference measured 65.7-66.5 dB)."""
+    sb = _sb()
+    gt, views = _standard_scene()
+    scene = sb.SceneSoA(*[gt[k] for k in G.CH], device="cuda")
+    worst = np.inf
+    for cam, _ in views[:3]:
+        full, _ = sb.forward(scene, cam)
+        half, _ = sb.forward(scene, cam, half=True)
+        worst = min(worst, sb.psnr(full.color.double(), half.color.double()))
+    print(f"criterion 11: worst view PSNR fp16 vs fp32 {worst:.1f} dB")
+    assert worst >= 40.0 and worst >= HALF_PSNR_FLOOR
