@@ -50,6 +50,9 @@ enum {
 const char* sb_last_error(void);
 int sb_version(void);
 int sb_record_bytes(void);        /* sizeof compact raster record (48)          */
+int sb_raster_row_bytes(void);    /* sizeof raster row (64): x y A B | Cq o r g |
+                                     bl log2(o) 1/o 2^64/o^2 | a b c slot, with
+                                     A B Cq the conic scaled to log2 units      */
 int sb_screen_grad_bytes(void);   /* sizeof(sb_screen_grad) (64)                */
 
 /* ---- Morton sort (ccc.py:79-90) ------------------------------------------ */
@@ -90,13 +93,16 @@ int sb_permute_rows(const uint32_t* perm, int64_t n, int count, const void* cons
  * zeroed.  sgrad_zero (nullable,
  * N rows): its rows [0, N_c) -- the slots sb_raster_bwd accumulates into --
  * are zeroed alongside the records, so that call can take n_cap = 0.
+ * raster_rows (nullable, N rows of sb_raster_row_bytes()): the raster row
+ * of every compact slot, which sb_raster_fwd / sb_raster_bwd stage with TMA
+ * bulk copies.
  * Replaces project_scene + build_clusters + cull_clusters +
  * cluster_visibility + compact_arrays (projection.py:130, ccc.py:112/134/149/171). */
 size_t sb_project_workspace_bytes(int64_t n);
 int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
                             void* recs, int32_t* compact_map, int32_t* cluster_offset, uint8_t* cluster_vis,
-                            int32_t* counters, sb_screen_grad* sgrad_zero, void* ws, size_t ws_bytes,
-                            sb_stream_t stream);
+                            int32_t* counters, sb_screen_grad* sgrad_zero, void* raster_rows, void* ws,
+                            size_t ws_bytes, sb_stream_t stream);
 
 /* tiles.py:50-107 binning, part 1: enumerate the exact disc/rect hits
  * (tiles.py:75-91), count them per tile and scan the counts ->
@@ -140,19 +146,21 @@ int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, cons
  * selects the fp16 blending-state path (forward.py:194-230, half=True).
  * ws (sb_raster_workspace_bytes, shared with sb_raster_bwd) holds the
  * dynamic tile queue: zero it once before its first use; every call leaves
- * it zeroed again. */
+ * it zeroed again.  raster_rows (nullable): sb_project_cull_compact's rows of
+ * the same records; when given, the fp32 kernels may stage them with TMA. */
 size_t sb_raster_workspace_bytes(void);
-int sb_raster_fwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
-                  const sb_raster_cfg* cfg, float* color, float* transmittance, int32_t* frag_count, int32_t* last,
-                  void* ws, size_t ws_bytes, sb_stream_t stream);
+int sb_raster_fwd(const void* recs, const void* raster_rows, const int32_t* tile_offsets, const int32_t* tile_prims,
+                  const sb_camera* cam, const sb_raster_cfg* cfg, float* color, float* transmittance,
+                  int32_t* frag_count, int32_t* last, void* ws, size_t ws_bytes, sb_stream_t stream);
 
 /* ---- backward (backward.py:205-279) --------------------------------------- */
 /* backward.py:112-267: screen-space gradients + S/M/C per compact primitive.
  * Rows [0, n_cap) of sgrad are zeroed first; n_cap = 0 accumulates into
  * sgrad as given (rows zeroed by sb_project_cull_compact's sgrad_zero). */
-int sb_raster_bwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
-                  const sb_raster_cfg* cfg, const float* dL_dI, const float* transmittance, const int32_t* last,
-                  sb_screen_grad* sgrad, int64_t n_cap, void* ws, size_t ws_bytes, sb_stream_t stream);
+int sb_raster_bwd(const void* recs, const void* raster_rows, const int32_t* tile_offsets, const int32_t* tile_prims,
+                  const sb_camera* cam, const sb_raster_cfg* cfg, const float* dL_dI, const float* transmittance,
+                  const int32_t* last, sb_screen_grad* sgrad, int64_t n_cap, void* ws, size_t ws_bytes,
+                  sb_stream_t stream);
 
 /* backward.py:272-278 (_chain_projection 384-516 + scatter_grads
  * ccc.py:197-216 + stats np.add.at): grads (N, 16) float32 for every row

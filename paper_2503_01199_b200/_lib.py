@@ -24,6 +24,7 @@ SIGNATURES = {
     "sb_last_error": ([], C.c_char_p),
     "sb_version": ([], C.c_int),
     "sb_record_bytes": ([], C.c_int),
+    "sb_raster_row_bytes": ([], C.c_int),
     "sb_screen_grad_bytes": ([], C.c_int),
     "sb_morton_keys_workspace_bytes": ([I64], SZ),
     "sb_morton_keys": ([VP, I64, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
@@ -32,15 +33,15 @@ SIGNATURES = {
     "sb_radix_sort_pairs_u64": ([VP, VP, VP, VP, I64, C.c_int, VP, VP, SZ, VP], C.c_int),
     "sb_permute_rows": ([VP, I64, C.c_int, VP, VP, VP, VP], C.c_int),
     "sb_project_workspace_bytes": ([I64], SZ),
-    "sb_project_cull_compact": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_project_cull_compact": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_bin_state_workspace_bytes": ([I64, I32], SZ),
     "sb_bin_prepare": ([VP, VP, I64, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_host_mapped_pointer": ([VP, C.POINTER(C.c_void_p)], C.c_int),
     "sb_bin_finish_workspace_bytes": ([I64, I32], SZ),
     "sb_bin_finish": ([VP, VP, I64, VP, I64, I64, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_raster_workspace_bytes": ([], SZ),
-    "sb_raster_fwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
-    "sb_raster_bwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, VP, SZ, VP], C.c_int),
+    "sb_raster_fwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_raster_bwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, VP, SZ, VP], C.c_int),
     "sb_chain_projection_bwd": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP], C.c_int),
     "sb_adam_sparse": ([VP, VP, VP, VP, VP, VP, I64, VP, VP], C.c_int),
     "sb_variance_score": ([VP, VP, VP, I64, VP, VP], C.c_int),

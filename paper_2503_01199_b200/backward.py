@@ -141,7 +141,8 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
         scratch = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
         frags = torch.empty_like(ctx.last)
         ws_f = _lib.workspace("raster_fwd", _lib.load().sb_raster_workspace_bytes(), dev)
-        _lib.call("sb_raster_fwd", _lib.ptr(ctx.recs), _lib.ptr(ctx.tile_buffer), _lib.ptr(ctx.tile_prims),
+        _lib.call("sb_raster_fwd", _lib.ptr(ctx.recs), _lib.ptr(ctx.rows), _lib.ptr(ctx.tile_buffer),
+                  _lib.ptr(ctx.tile_prims),
                   C.byref(cam_s), C.byref(cfg_s), _lib.ptr(scratch), _lib.ptr(T_final), _lib.ptr(frags),
                   _lib.ptr(last), _lib.ptr(ws_f), ws_f.numel(), stream)
     sgrad = _lib.workspace("sgrad", nc * SGRAD_BYTES, dev)
@@ -150,7 +151,8 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
     prezeroed = ctx.token != 0 and _sgrad_clean.get(str(dev)) == ctx.token
     _sgrad_clean.pop(str(dev), None)
     ws_r = _lib.workspace("raster_bwd", _lib.load().sb_raster_workspace_bytes(), dev)
-    _lib.call("sb_raster_bwd", _lib.ptr(ctx.recs), _lib.ptr(ctx.tile_buffer), _lib.ptr(ctx.tile_prims),
+    _lib.call("sb_raster_bwd", _lib.ptr(ctx.recs), _lib.ptr(ctx.rows), _lib.ptr(ctx.tile_buffer),
+              _lib.ptr(ctx.tile_prims),
               C.byref(cam_s), C.byref(cfg_s), _lib.ptr(dI), _lib.ptr(T_final), _lib.ptr(last),
               _lib.ptr(sgrad), 0 if prezeroed else ctx.n_compact, _lib.ptr(ws_r), ws_r.numel(), stream)
     grads = torch.empty((n, 16), dtype=torch.float32, device=dev)

@@ -7,7 +7,7 @@
 
 // launchers (one per kernel family)
 void sb_launch_project_cull_compact(const float*, int, const CamDev&, int, RasterRec*, int32_t*, int32_t*, uint8_t*,
-                                    int32_t*, void*, unsigned long long*, unsigned int*, cudaStream_t);
+                                    int32_t*, void*, void*, unsigned long long*, unsigned int*, cudaStream_t);
 int sb_project_status_words(int n);
 size_t sb_bin_state_bytes(int n_cap, int ntiles);
 void sb_launch_bin_prepare(const RasterRec*, const int32_t*, int, const CamDev&, int32_t*, int32_t*, int32_t*,
@@ -17,9 +17,11 @@ void sb_launch_bin_finish(const RasterRec*, const int32_t*, int, const CamDev&, 
                           const void*, int32_t*, void*, cudaStream_t);
 size_t sb_sort_u64_ws(int n, int bits);
 int sb_launch_sort_u64(unsigned long long*, uint32_t*, unsigned long long*, uint32_t*, int, int, void*, cudaStream_t);
-void sb_launch_raster_fwd(const RasterRec*, const int32_t*, const int32_t*, int, int, int, int, const sb_raster_cfg&,
+void sb_launch_raster_fwd(const RasterRec*, const RasterRow*, const int32_t*, const int32_t*, int, int, int, int,
+                          const sb_raster_cfg&,
                           int*, float*, float*, int32_t*, int32_t*, cudaStream_t);
-void sb_launch_raster_bwd(const RasterRec*, const int32_t*, const int32_t*, int, int, int, int, const sb_raster_cfg&,
+void sb_launch_raster_bwd(const RasterRec*, const RasterRow*, const int32_t*, const int32_t*, int, int, int, int,
+                          const sb_raster_cfg&,
                           int*, const float*, const float*, const int32_t*, sb_screen_grad*, cudaStream_t);
 void sb_launch_lane_reduce(const float*, int, int, float*, double*, cudaStream_t);
 void sb_launch_chain(const float*, int, const CamDev&, const int32_t*, const RasterRec*, const sb_screen_grad*, float*,
@@ -86,6 +88,7 @@ extern "C" {
 const char* sb_last_error(void) { return g_err.c_str(); }
 int sb_version(void) { return 1; }
 int sb_record_bytes(void) { return (int)sizeof(RasterRec); }
+int sb_raster_row_bytes(void) { return (int)sizeof(RasterRow); }
 int sb_screen_grad_bytes(void) { return (int)sizeof(sb_screen_grad); }
 
 size_t sb_morton_keys_workspace_bytes(int64_t n) {
@@ -144,8 +147,8 @@ size_t sb_project_workspace_bytes(int64_t n) {
 
 int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
                             void* recs, int32_t* compact_map, int32_t* cluster_offset, uint8_t* cluster_vis,
-                            int32_t* counters, sb_screen_grad* sgrad_zero, void* ws, size_t ws_bytes,
-                            sb_stream_t stream) {
+                            int32_t* counters, sb_screen_grad* sgrad_zero, void* raster_rows, void* ws,
+                            size_t ws_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
     if (n < 0 || n > INT32_MAX - 256) return fail(SB_EINVAL, "n out of range");
@@ -161,7 +164,8 @@ int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam
     unsigned int* ticket = reinterpret_cast<unsigned int*>(status + blocks);
     const CamDev d = make_cam(cam, cfg);
     sb_launch_project_cull_compact(params, (int)n, d, cfg->use_culling, static_cast<RasterRec*>(recs), compact_map,
-                                   cluster_offset, cluster_vis, counters, sgrad_zero, status, ticket, S(stream));
+                                   cluster_offset, cluster_vis, counters, sgrad_zero, raster_rows, status, ticket,
+                                   S(stream));
     return check_launch("sb_project_cull_compact");
 }
 
@@ -207,20 +211,23 @@ int sb_bin_finish(const void* recs, const int32_t* counters, int64_t n_cap, cons
 
 size_t sb_raster_workspace_bytes(void) { return 256; }
 
-int sb_raster_fwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
+int sb_raster_fwd(const void* recs, const void* raster_rows, const int32_t* tile_offsets, const int32_t* tile_prims,
+                  const sb_camera* cam,
                   const sb_raster_cfg* cfg, float* color, float* transmittance, int32_t* frag_count, int32_t* last,
                   void* ws, size_t ws_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
     if (ws_bytes < sb_raster_workspace_bytes()) return fail(SB_EWORKSPACE, "raster workspace too small");
     const CamDev d = make_cam(cam, cfg);
-    sb_launch_raster_fwd(static_cast<const RasterRec*>(recs), tile_offsets, tile_prims, d.W, d.H, d.tiles_x,
+    sb_launch_raster_fwd(static_cast<const RasterRec*>(recs), static_cast<const RasterRow*>(raster_rows), tile_offsets,
+                         tile_prims, d.W, d.H, d.tiles_x,
                          d.tiles_x * d.tiles_y, *cfg, static_cast<int*>(ws), color, transmittance, frag_count, last,
                          S(stream));
     return check_launch("sb_raster_fwd");
 }
 
-int sb_raster_bwd(const void* recs, const int32_t* tile_offsets, const int32_t* tile_prims, const sb_camera* cam,
+int sb_raster_bwd(const void* recs, const void* raster_rows, const int32_t* tile_offsets, const int32_t* tile_prims,
+                  const sb_camera* cam,
                   const sb_raster_cfg* cfg, const float* dL_dI, const float* transmittance, const int32_t* last,
                   sb_screen_grad* sgrad, int64_t n_cap, void* ws, size_t ws_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
@@ -228,7 +235,8 @@ int sb_raster_bwd(const void* recs, const int32_t* tile_offsets, const int32_t* 
     if (ws_bytes < sb_raster_workspace_bytes()) return fail(SB_EWORKSPACE, "raster workspace too small");
     const CamDev d = make_cam(cam, cfg);
     if (n_cap > 0) cudaMemsetAsync(sgrad, 0, sizeof(sb_screen_grad) * (size_t)n_cap, S(stream));
-    sb_launch_raster_bwd(static_cast<const RasterRec*>(recs), tile_offsets, tile_prims, d.W, d.H, d.tiles_x,
+    sb_launch_raster_bwd(static_cast<const RasterRec*>(recs), static_cast<const RasterRow*>(raster_rows), tile_offsets,
+                         tile_prims, d.W, d.H, d.tiles_x,
                          d.tiles_x * d.tiles_y, *cfg, static_cast<int*>(ws), dL_dI, transmittance, last, sgrad,
                          S(stream));
     return check_launch("sb_raster_bwd");

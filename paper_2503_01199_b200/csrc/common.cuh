@@ -156,6 +156,110 @@ struct __align__(16) RasterRec {
     uint32_t flags;          // bit0 valid, bit1 in_image
 };
 
+// Raster row (64 B): the record as the rasterizer consumes it, written by
+// the projection kernel next to the 48-byte record (one row per compact
+// slot), so the raster kernels stage rows with plain bulk copies (TMA) and
+// no per-chunk transform.  The footprint exponent is in log2 units:
+// A = -log2(e)/2 a, B = -log2(e) b, Cq = -log2(e)/2 c, so
+// o G = ex2(A dx^2 + B dx dy + Cq dy^2 + log2 o).
+struct __align__(16) RasterRow {
+    float x, y, A, B;        // screen mean, log2-domain conic a, b
+    float Cq, o, r, g;       // log2-domain conic c, opacity, colour r, g
+    float bl, lg2o, inv_o, s2io;   // colour b, log2 o, 1/o, 2^64 / o^2 (the backward's S scale)
+    float a, b, c;           // raw conic (the backward's fold)
+    int32_t slot;            // compact slot (the backward's scatter target)
+};
+static_assert(sizeof(RasterRow) == 64, "raster rows are 64 bytes");
+
+constexpr float kSbHalfLog2e = -0.72134752044448170f;   // -log2(e) / 2
+constexpr float kSbLog2e = -1.44269504088896341f;       // -log2(e)
+
+SB_INLINE float sb_rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// The raster row of one record (the exact arithmetic the rasterizer's
+// staging used to do per chunk; forward and backward share it).
+SB_INLINE RasterRow sb_raster_row(float x, float y, float a, float b, float c, float o, float r, float g, float bl,
+                                  int32_t slot) {
+    RasterRow w;
+    w.x = x; w.y = y;
+    w.A = kSbHalfLog2e * a; w.B = kSbLog2e * b; w.Cq = kSbHalfLog2e * c;
+    w.o = o; w.r = r; w.g = g; w.bl = bl;
+    w.lg2o = __log2f(o);
+    const float io = sb_rcp_approx(o), io32 = io * 4294967296.0f;
+    w.inv_o = io;
+    // (finite even for opacities far below any alpha_min: 0 * s2io = 0)
+    w.s2io = fminf(io32 * io32, 3.0e38f);
+    w.a = a; w.b = b; w.c = c;
+    w.slot = slot;
+    return w;
+}
+
+// ---- TMA bulk copies and mbarriers (sm_90+ PTX, SASS UBLKCP / SYNCS) -----
+SB_INLINE uint32_t sb_smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+SB_INLINE void sb_mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sb_smem_addr(bar)), "r"(count) : "memory");
+}
+// make the initialised barriers visible to the async (TMA) proxy
+SB_INLINE void sb_mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+SB_INLINE void sb_mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(sb_smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+SB_INLINE bool sb_mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n" : "=r"(ok) : "r"(sb_smem_addr(bar)), "r"(parity) : "memory");
+    return ok != 0;
+}
+// wait for the phase with the given parity; a transfer that never lands
+// (a malformed copy) traps after ~1 s instead of hanging the device
+SB_INLINE void sb_mbar_wait(uint64_t* bar, uint32_t parity) {
+    if (sb_mbar_try_wait(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!sb_mbar_try_wait(bar, parity))
+        if (clock64() - t0 > (1ll << 31)) __trap();
+}
+// warp-wide wait with a warp-uniform exit (every lane observes the phase;
+// the loop condition is a vote, so the code after it stays converged)
+SB_INLINE void sb_mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+    if (__all_sync(0xffffffffu, sb_mbar_try_wait(bar, parity))) return;
+    const long long t0 = clock64();
+    while (!__all_sync(0xffffffffu, sb_mbar_try_wait(bar, parity)))
+        if (clock64() - t0 > (1ll << 31)) __trap();
+}
+// 2-D tensor gather (sm_100a TMA tile::gather4, SASS UTMALDG...GATHER4): four
+// rows (row0..row3) of `tmap`'s box width, starting at column col, into dst
+SB_INLINE void sb_gather4(void* dst, const void* tmap, int col, int r0, int r1, int r2, int r3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+        :: "r"(sb_smem_addr(dst)), "l"(tmap), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+           "r"(sb_smem_addr(bar)) : "memory");
+}
+// generic-proxy accesses of shared memory before async-proxy writes to it
+SB_INLINE void sb_fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, 16-B aligned),
+// completing `bytes` of transaction count on `bar`
+SB_INLINE void sb_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        :: "r"(sb_smem_addr(dst)), "l"(src), "r"(bytes), "r"(sb_smem_addr(bar)) : "memory");
+}
+
 SB_INLINE double sb_sigmoid(double x) {
     // scene.py:31-38: 1 / (1 + exp(-x)) for x >= 0, exp(x) / (1 + exp(x))
     // otherwise -- both branches are exp(-|x|) (negation is exact) and one

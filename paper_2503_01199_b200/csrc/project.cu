@@ -38,6 +38,7 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
                             int use_culling, RasterRec* __restrict__ rec_out, int32_t* __restrict__ compact_map,
                             int32_t* __restrict__ cluster_offset, uint8_t* __restrict__ cluster_vis,
                             int32_t* __restrict__ counters, float4* __restrict__ sgrad_zero,
+                            RasterRow* __restrict__ rows_out,
                             unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket)
 {
     sb_pdl_begin();
@@ -127,6 +128,17 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
             const int nvec = members * 3;
             for (int v = lane; v < nvec; v += 32) dst[v] = src[v];
             for (int s = lane; s < members; s += 32) compact_map[base + s] = cl * SB_CLUSTER_SIZE + s;
+            // the rasterizer's 64-byte rows (log2-domain coefficients, 1/o, ...)
+            if (rows_out) {
+                for (int s = lane; s < members; s += 32) {
+                    const RasterRec& q = st[s];
+                    const RasterRow w = sb_raster_row(q.x, q.y, q.a, q.b, q.c, q.o, q.r, q.g, q.bl,
+                                                      (int32_t)(base + s));
+                    const float4* wv = reinterpret_cast<const float4*>(&w);
+                    float4* d = reinterpret_cast<float4*>(rows_out + base + s);
+                    d[0] = wv[0]; d[1] = wv[1]; d[2] = wv[2]; d[3] = wv[3];
+                }
+            }
             // the backward's screen-gradient rows of these slots start at
             // zero (64 B each), written here while the kernel is compute-bound
             if (sgrad_zero) {
@@ -166,7 +178,7 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
 
 void sb_launch_project_cull_compact(const float* params, int n, const CamDev& cam, int use_culling,
                                     RasterRec* rec_out, int32_t* compact_map, int32_t* cluster_offset,
-                                    uint8_t* cluster_vis, int32_t* counters, void* sgrad_zero,
+                                    uint8_t* cluster_vis, int32_t* counters, void* sgrad_zero, void* rows_out,
                                     unsigned long long* status, unsigned int* ticket, cudaStream_t stream)
 {
     const int k = (n + SB_CLUSTER_SIZE - 1) / SB_CLUSTER_SIZE;
@@ -177,7 +189,7 @@ void sb_launch_project_cull_compact(const float* params, int n, const CamDev& ca
     const int blocks = min(resident, (k + kWarps - 1) / kWarps);
     sb_launch(project_cull_compact_kernel, blocks, kThreads, smem, stream, reinterpret_cast<const float4*>(params), n,
               k, cam, use_culling, rec_out, compact_map, cluster_offset, cluster_vis, counters,
-              static_cast<float4*>(sgrad_zero), status, ticket);
+              static_cast<float4*>(sgrad_zero), static_cast<RasterRow*>(rows_out), status, ticket);
 }
 
 // look-back status words (one per cluster) before the ticket words

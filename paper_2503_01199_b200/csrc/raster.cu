@@ -37,6 +37,10 @@
 // Scheduling: warps pull tiles from an atomic counter (persistent grid), and
 // the 48-byte records of the next 32 list entries are fetched into registers
 // while the current 32 are consumed from a warp-private shared-memory slab.
+#include <cstdlib>
+#include <cstring>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
 #include "common.cuh"
@@ -44,6 +48,7 @@
 namespace {
 
 constexpr int kWarpsPerBlock = 4;
+constexpr int kDefaultStaging = 0;   // register prefetch (see staging_mode)
 constexpr int kThreads = kWarpsPerBlock * 32;
 
 // staged record: raw conic (for the backward fold) plus the log2-domain
@@ -546,7 +551,8 @@ SB_INLINE float row_tree(float v[32]) {
 
 static_assert(kBatch == 8, "row swizzles assume 8 slots");
 
-SB_INLINE void load_row(const BwdWarpSmem& ws, int row, float v[32]) {
+template <class WS>
+SB_INLINE void load_row(const WS& ws, int row, float v[32]) {
     const float* base = ws.rows + row * 32;
 #pragma unroll
     for (int q = 0; q < 8; q++) {
@@ -555,7 +561,8 @@ SB_INLINE void load_row(const BwdWarpSmem& ws, int row, float v[32]) {
     }
 }
 
-SB_INLINE void load_pair_row(const BwdWarpSmem& ws, int row, float2 v[32]) {
+template <class WS>
+SB_INLINE void load_pair_row(const WS& ws, int row, float2 v[32]) {
     const float2* base = ws.pairs + row * 32;
 #pragma unroll
     for (int q = 0; q < 16; q++) {
@@ -584,7 +591,8 @@ SB_INLINE float2 row_tree2(float2 v[32]) {
 // reference (backward.py:254-255 sums float64 f and f^2 of the same f) --
 // never a densification candidate.  (The S row itself carries fl(uG^2)
 // 2^64 / o^2, whose float32 rounding would leave an ulp-level residue.)
-SB_INLINE void emit(const BwdWarpSmem& ws, int c, int b, float out, sb_screen_grad* grads) {
+template <class WS>
+SB_INLINE void emit(const WS& ws, int c, int b, float out, sb_screen_grad* grads) {
     sb_screen_grad* gr = grads + ws.slot[b];
     if (c < 9) {
         atomicAdd(reinterpret_cast<float*>(gr) + c, out);
@@ -598,7 +606,8 @@ SB_INLINE void emit(const BwdWarpSmem& ws, int c, int b, float out, sb_screen_gr
     }
 }
 
-SB_INLINE void flush_batch(BwdWarpSmem& ws, int nb, int lane, int conic_tree, sb_screen_grad* grads) {
+template <class WS>
+SB_INLINE void flush_batch(WS& ws, int nb, int lane, int conic_tree, sb_screen_grad* grads) {
     __syncwarp();
     if (lane < kRowCh * nb) {
         const int c = lane / nb, b = lane - c * nb;
@@ -766,13 +775,420 @@ raster_bwd_kernel(BwdParams p)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// TMA staging variant (north_star item 4): each warp stages its chunks of
+// 64-byte raster rows (written by the projection kernel) into a double-
+// buffered warp slab with bulk copies (cp.async.bulk, SASS UBLKCP), one per
+// lane, completing on a per-buffer mbarrier (SASS SYNCS): chunk c + 1 is in
+// flight while chunk c is blended, and no record is held in registers.  The
+// only per-lane prefetch is the 4-byte list entry of the chunk after next.
+// The contribution mask and the blend are the register variant's, on the same
+// values (RasterRow carries exactly what commit_chunk computed).
+
+template <int kC>
+SB_INLINE void issue_rows(RasterRow* dst, const RasterRow* __restrict__ rows, int slot, int cnt, uint64_t* bar,
+                          int lane) {
+    sb_fence_proxy_async();                // earlier generic reads of dst before the async writes
+    if (lane == 0) sb_mbar_arrive_expect_tx(bar, (uint32_t)cnt * (uint32_t)sizeof(RasterRow));
+    __syncwarp();
+    if (lane < cnt) sb_bulk_g2s(dst + lane, rows + slot, (uint32_t)sizeof(RasterRow), bar);
+}
+
+// the same chunk with tile::gather4: four rows per TMA instruction (row
+// coordinates broadcast from the lanes that hold them); lane 0 issues.
+// Rows of the last group past cnt repeat slot 0 (never read).
+SB_INLINE void issue_rows_g4(RasterRow* dst, const CUtensorMap* tmap, int slot, int cnt, uint64_t* bar, int lane) {
+    sb_fence_proxy_async();
+    const int s0 = __shfl_sync(0xffffffffu, slot, 0);
+    const int s = lane < cnt ? slot : s0;
+    const int groups = (cnt + 3) >> 2;
+    if (lane == 0) sb_mbar_arrive_expect_tx(bar, (uint32_t)groups * 4u * (uint32_t)sizeof(RasterRow));
+    __syncwarp();
+    for (int g = 0; g < groups; g++) {
+        const int r0 = __shfl_sync(0xffffffffu, s, 4 * g), r1 = __shfl_sync(0xffffffffu, s, 4 * g + 1);
+        const int r2 = __shfl_sync(0xffffffffu, s, 4 * g + 2), r3 = __shfl_sync(0xffffffffu, s, 4 * g + 3);
+        if (lane == 0) sb_gather4(dst + 4 * g, tmap, 0, r0, r1, r2, r3, bar);
+    }
+    __syncwarp();
+}
+
+template <bool kG4>
+SB_INLINE void stage_rows(RasterRow* dst, const RasterRow* __restrict__ rows, const CUtensorMap* tmap, int slot,
+                          int cnt, uint64_t* bar, int lane) {
+    if (kG4) issue_rows_g4(dst, tmap, slot, cnt, bar, lane);
+    else issue_rows<32>(dst, rows, slot, cnt, bar, lane);
+}
+
+SB_INLINE float4 row_part(const RasterRow* slab, int j, int part) {
+    return reinterpret_cast<const float4*>(slab + j)[part];
+}
+
+SB_INLINE SRec row_get(const RasterRow* slab, int j) {
+    const float4 c0 = row_part(slab, j, 0), c1 = row_part(slab, j, 1), c2 = row_part(slab, j, 2),
+                 c3 = row_part(slab, j, 3);
+    SRec r;
+    r.x = c0.x; r.y = c0.y; r.A = c0.z; r.B = c0.w;
+    r.Cq = c1.x; r.o = c1.y; r.r = c1.z; r.g = c1.w;
+    r.bl = c2.x; r.lg2o = c2.y; r.inv_o = c2.z; r.s2io = c2.w;
+    r.a = c3.x; r.b = c3.y; r.c = c3.z; r.slot = __float_as_int(c3.w);
+    return r;
+}
+
+// ballot of the staged chunk's rows that can contribute to the tile
+template <int kC>
+SB_INLINE unsigned row_mask(const RasterRow* slab, int cnt, int lane, int x0, int y0, int W, int H, float amin) {
+    bool keep = false;
+    if (lane < cnt && lane < kC) {
+        const float4 c0 = row_part(slab, lane, 0), c1 = row_part(slab, lane, 1), c3 = row_part(slab, lane, 3);
+        Prefetch pf;
+        pf.a = make_float4(c0.x, c0.y, c3.x, c3.y);
+        pf.b = make_float4(c3.z, c1.y, 0.0f, 0.0f);
+        keep = can_contribute(pf, (float)x0, (float)min(x0 + SB_TILE_W - 1, W - 1), (float)y0,
+                              (float)min(y0 + SB_TILE_H - 1, H - 1), __log2f(amin));
+    }
+    return __ballot_sync(0xffffffffu, keep);
+}
+
+struct TmaFwdParams {
+    CUtensorMap tmap;          // rows as a 2-D fp32 tensor [rows][16] (gather4 variant)
+    FwdParams f;
+    const RasterRow* rows;
+};
+
+struct FwdLane {
+    float T[4], rgb[4][3];
+    int frags[4], last[4];
+};
+
+// One chunk of the TMA forward with a compile-time buffer index B (so the
+// slab address and the chunk mask stay in the uniform datapath, as in the
+// register variant): stage chunk c + 1 into buffer B ^ 1, wait for chunk c
+// in buffer B, blend.  Returns true when the whole warp has terminated.
+template <int B, bool kG4>
+SB_INLINE bool fwd_tma_chunk(const TmaFwdParams& tp, RasterRow (*slab2)[32], uint64_t* bar, uint32_t& phase, int c,
+                             int nch, int n, int beg, int& s_next, int x0, int y0, float px, float py0, FwdLane& L,
+                             int lane)
+{
+    const FwdParams& p = tp.f;
+    const int k0 = c * 32, cnt = min(32, n - k0);
+    if (c + 1 < nch) {
+        stage_rows<kG4>(slab2[B ^ 1], tp.rows, &tp.tmap, s_next, min(32, n - k0 - 32), &bar[B ^ 1], lane);
+        s_next = k0 + 64 + lane < n ? __ldg(p.prims + beg + k0 + 64 + lane) : 0;
+    }
+    sb_mbar_wait_warp(&bar[B], (phase >> B) & 1u);
+    phase ^= 1u << B;
+    const RasterRow* slab = slab2[B];
+    unsigned todo = row_mask<32>(slab, cnt, lane, x0, y0, p.W, p.H, p.amin);
+    bool done = false;
+    while (todo) {
+        const int j = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const bool live = fmaxf(fmaxf(L.T[0], L.T[1]), fmaxf(L.T[2], L.T[3])) >= p.tstop;
+        if (!__any_sync(0xffffffffu, live)) {
+            done = true;
+            break;
+        }
+        const SRec r = row_get(slab, j);
+        float araw[4], dx, dy;
+        lane_alpha_raw(r, px, py0, araw, dx, dy);
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const float alpha = fminf(araw[i], p.amax);
+            if (L.T[i] >= p.tstop && alpha >= p.amin) {
+                const float w = L.T[i] * alpha;
+                L.rgb[i][0] = fmaf(w, r.r, L.rgb[i][0]);
+                L.rgb[i][1] = fmaf(w, r.g, L.rgb[i][1]);
+                L.rgb[i][2] = fmaf(w, r.bl, L.rgb[i][2]);
+                L.T[i] = FMUL(L.T[i], FSUB(1.0f, alpha));
+                L.frags[i]++;
+                L.last[i] = k0 + j + 1;
+            }
+        }
+    }
+    __syncwarp();
+    return done;
+}
+
+template <bool kG4>
+__global__ void __launch_bounds__(kThreads)
+raster_fwd_tma_kernel(const __grid_constant__ TmaFwdParams tp)
+{
+    const FwdParams& p = tp.f;
+    __shared__ __align__(128) RasterRow slabs[kWarpsPerBlock][2][32];
+    __shared__ __align__(8) uint64_t bars[kWarpsPerBlock][2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* bar = bars[warp];
+    if (lane == 0) {
+        sb_mbar_init(&bar[0], 1);
+        sb_mbar_init(&bar[1], 1);
+        sb_mbar_init_fence();
+    }
+    __syncwarp();
+    sb_pdl_begin();
+    uint32_t phase = 0;   // bit b: parity of buffer b's next completion
+    for (int q = next_tile(p.tile_counter, lane, p.ntiles); q < p.ntiles;
+         q = next_tile(p.tile_counter, lane, p.ntiles)) {
+        const int t = p.offsets[p.ntiles + 1 + q];   // heavy-first schedule (binning scan)
+        const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
+        const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
+        const float px = (float)pxi, py0 = (float)py0i;
+        FwdLane L;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            L.T[i] = (pxi < p.W && py0i + i < p.H) ? 1.0f : 0.0f;
+            L.rgb[i][0] = L.rgb[i][1] = L.rgb[i][2] = 0.0f;
+            L.frags[i] = 0;
+            L.last[i] = 0;
+        }
+        const int beg = p.offsets[t], n = p.offsets[t + 1] - beg;
+        const int nch = (n + 31) >> 5;
+        if (n > 0) {
+            const int slot = lane < n ? __ldg(p.prims + beg + lane) : 0;
+            stage_rows<kG4>(slabs[warp][0], tp.rows, &tp.tmap, slot, min(32, n), &bar[0], lane);
+        }
+        int s_next = 32 + lane < n ? __ldg(p.prims + beg + 32 + lane) : 0;
+        int c = 0;
+        while (c < nch) {
+            if (fwd_tma_chunk<0, kG4>(tp, slabs[warp], bar, phase, c++, nch, n, beg, s_next, x0, y0, px, py0, L,
+                                      lane) || c >= nch)
+                break;
+            if (fwd_tma_chunk<1, kG4>(tp, slabs[warp], bar, phase, c++, nch, n, beg, s_next, x0, y0, px, py0, L,
+                                      lane))
+                break;
+        }
+        if (c < nch) {          // early-terminated tile: drain the chunk in flight
+            sb_mbar_wait(&bar[c & 1], (phase >> (c & 1)) & 1u);
+            phase ^= 1u << (c & 1);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            if (!(pxi < p.W && py0i + i < p.H)) continue;
+            const size_t pix = (size_t)(py0i + i) * p.W + pxi;
+            p.out_color[3 * pix + 0] = FADD(L.rgb[i][0], FMUL(L.T[i], p.bg[0]));
+            p.out_color[3 * pix + 1] = FADD(L.rgb[i][1], FMUL(L.T[i], p.bg[1]));
+            p.out_color[3 * pix + 2] = FADD(L.rgb[i][2], FMUL(L.T[i], p.bg[2]));
+            p.out_T[pix] = L.T[i];
+            p.out_frags[pix] = L.frags[i];
+            p.out_last[pix] = L.last[i];
+        }
+    }
+}
+
+// Backward with TMA-staged rows: kC-row chunks, double-buffered (kC = 16
+// keeps the register variant's shared memory per warp, so 18 warps / SM).
+template <int kC>
+struct __align__(128) BwdTmaWarpSmem {   // (tensor TMA destinations are 128-byte aligned)
+    RasterRow slab[2][kC];
+    float rows[kRowCh * kBatch * 32];
+    float2 pairs[kPairCh * kBatch * 32];
+    int slot[kBatch];
+    int count[kBatch];
+    uint64_t bar[2];
+};
+
+struct TmaBwdParams {
+    CUtensorMap tmap;
+    BwdParams b;
+    const RasterRow* rows;
+};
+
+template <int kC, int kMinBlocks, bool kG4>
+__global__ void __launch_bounds__(kBwdWarps * 32, kMinBlocks)
+raster_bwd_tma_kernel(const __grid_constant__ TmaBwdParams tp)
+{
+    const BwdParams& p = tp.b;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    BwdTmaWarpSmem<kC>& ws = reinterpret_cast<BwdTmaWarpSmem<kC>*>(smem_raw)[warp];
+    if (lane == 0) {
+        sb_mbar_init(&ws.bar[0], 1);
+        sb_mbar_init(&ws.bar[1], 1);
+        sb_mbar_init_fence();
+    }
+    __syncwarp();
+    sb_pdl_begin();
+    uint32_t phase = 0;
+    for (int q = next_tile(p.tile_counter, lane, p.ntiles); q < p.ntiles;
+         q = next_tile(p.tile_counter, lane, p.ntiles)) {
+        const int t = p.offsets[p.ntiles + 1 + q];
+        const int beg = p.offsets[t];
+        if (p.offsets[t + 1] == beg) continue;
+        const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
+        const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
+        const float px = (float)pxi, py0 = (float)py0i;
+        float2 T2[2], Sd2[2], dI2[2][3];
+        int last[4];
+        int lane_max = 0;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            float Tv[2], Sv[2], dv[2][3];
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const int i = 2 * h + e;
+                const bool v = pxi < p.W && py0i + i < p.H;
+                const size_t pix = (size_t)(py0i + i) * p.W + pxi;
+                Tv[e] = v ? p.T_final[pix] : 1.0f;
+                last[i] = v ? p.last[pix] : 0;
+#pragma unroll
+                for (int ch = 0; ch < 3; ch++) dv[e][ch] = v ? p.dL_dI[3 * pix + ch] : 0.0f;
+                Sv[e] = Tv[e] * (dv[e][0] * p.bg[0] + dv[e][1] * p.bg[1] + dv[e][2] * p.bg[2]);
+                lane_max = max(lane_max, last[i]);
+            }
+            T2[h] = make_float2(Tv[0], Tv[1]);
+            Sd2[h] = make_float2(Sv[0], Sv[1]);
+#pragma unroll
+            for (int ch = 0; ch < 3; ch++) dI2[h][ch] = make_float2(dv[0][ch], dv[1][ch]);
+        }
+        const int kmax = __reduce_max_sync(0xffffffffu, lane_max);
+        // chunks back to front: chunk i holds entries [max(0, kmax - kC (i+1)), kmax - kC i)
+        const int nch = (kmax + kC - 1) / kC;
+        if (nch > 0) {
+            const int k0 = max(0, kmax - kC), cnt = kmax - k0;
+            const int slot = lane < cnt ? __ldg(p.prims + beg + k0 + lane) : 0;
+            stage_rows<kG4>(ws.slab[0], tp.rows, &tp.tmap, slot, cnt, &ws.bar[0], lane);
+        }
+        int s_next = 0;
+        if (nch > 1) {
+            const int k1 = kmax - kC, k0 = max(0, k1 - kC);
+            s_next = lane < k1 - k0 ? __ldg(p.prims + beg + k0 + lane) : 0;
+        }
+        int nb = 0, pc_off = lane, pp_off = lane;
+        for (int c = 0; c < nch; c++) {
+            const int b = c & 1;
+            const int k1 = kmax - kC * c, k0 = max(0, k1 - kC), cnt = k1 - k0;
+            if (c + 1 < nch) {
+                const int n1 = k0 - max(0, k0 - kC);
+                stage_rows<kG4>(ws.slab[b ^ 1], tp.rows, &tp.tmap, s_next, n1, &ws.bar[b ^ 1], lane);
+                if (c + 2 < nch) {
+                    const int k1b = k0 - kC, k0b = max(0, k1b - kC);
+                    s_next = lane < k1b - k0b ? __ldg(p.prims + beg + k0b + lane) : 0;
+                }
+            }
+            sb_mbar_wait_warp(&ws.bar[b], (phase >> b) & 1u);
+            phase ^= 1u << b;
+            const RasterRow* slab = ws.slab[b];
+            unsigned todo = row_mask<kC>(slab, cnt, lane, x0, y0, p.W, p.H, p.amin);
+            while (todo) {
+                const int j = 31 - __clz(todo);
+                todo &= ~(1u << j);
+                const int k = k0 + j;
+                const SRec r = row_get(slab, j);
+                float araw[4], dx, dy;
+                lane_alpha_raw(r, px, py0, araw, dx, dy);
+                float alpha[4];
+                bool ci[4];
+                unsigned cmask = 0;
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    alpha[i] = fminf(araw[i], p.amax);
+                    ci[i] = (k < last[i]) && (alpha[i] >= p.amin);
+                    cmask |= ci[i] ? 1u << i : 0u;
+                }
+                if (!__any_sync(0xffffffffu, cmask != 0)) continue;
+                const float2 cr = make_float2(r.r, r.r), cg = make_float2(r.g, r.g), cb = make_float2(r.bl, r.bl);
+                float2 uG2[2], w2[2];
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int i0 = 2 * h, i1 = 2 * h + 1;
+                    const float2 a2 = make_float2(ci[i0] ? alpha[i0] : 0.0f, ci[i1] ? alpha[i1] : 0.0f);
+                    const float2 om = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-a2.x, -a2.y));
+                    const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+                    const float2 Tb = __fmul2_rn(T2[h], inv);
+                    const float2 dc = __ffma2_rn(dI2[h][2], cb, __ffma2_rn(dI2[h][1], cg, __fmul2_rn(dI2[h][0], cr)));
+                    const float2 si = __fmul2_rn(Sd2[h], inv);
+                    const float2 da = __ffma2_rn(Tb, dc, make_float2(-si.x, -si.y));
+                    const float2 ag = make_float2(a2.x < p.amax ? a2.x : 0.0f, a2.y < p.amax ? a2.y : 0.0f);
+                    uG2[h] = __fmul2_rn(da, ag);
+                    w2[h] = __fmul2_rn(Tb, a2);
+                    Sd2[h] = __ffma2_rn(w2[h], dc, Sd2[h]);
+                    T2[h] = Tb;
+                }
+                const float uG[4] = {uG2[0].x, uG2[0].y, uG2[1].x, uG2[1].y};
+                const float2 gs = __fadd2_rn(uG2[0], uG2[1]);
+                const float gb = gs.x + gs.y;
+                const float gl = fmaf(uG[3], 3.0f, fmaf(uG[2], 2.0f, uG[1]));
+                const float gq = fmaf(uG[3], 9.0f, fmaf(uG[2], 4.0f, uG[1]));
+                const float2 q2 = __ffma2_rn(uG2[1], uG2[1], __fmul2_rn(uG2[0], uG2[0]));
+                const float t1 = fmaf(-gb, dy, gl), t2 = gb * dx;
+                float* pc = ws.rows + pc_off;
+                pc[0 * 256] = -0.5f * (t2 * dx);
+                pc[1 * 256] = dx * t1;
+                pc[2 * 256] = fmaf(dy, fmaf(-0.5f * gb, dy, gl), -0.5f * gq);
+                pc[3 * 256] = (q2.x + q2.y) * r.s2io;
+                float rgb[3];
+#pragma unroll
+                for (int ch = 0; ch < 3; ch++) {
+                    const float2 tt = __ffma2_rn(w2[1], dI2[1][ch], __fmul2_rn(w2[0], dI2[0][ch]));
+                    rgb[ch] = tt.x + tt.y;
+                }
+                float2* pp = ws.pairs + pp_off;
+                pp[0 * 256] = make_float2(fmaf(r.b, t1, -r.a * t2), fmaf(r.c, t1, -r.b * t2));
+                pp[1 * 256] = make_float2(gb * r.inv_o, rgb[0]);
+                pp[2 * 256] = make_float2(rgb[1], rgb[2]);
+                const int C = __reduce_add_sync(0xffffffffu, __popc(cmask));
+                if (lane == 0) {
+                    ws.slot[nb] = r.slot;
+                    ws.count[nb] = C;
+                }
+                ++nb;
+                pc_off = nb * 32 + ((lane + 4 * nb) & 31);
+                pp_off = nb * 32 + ((lane + 2 * nb) & 31);
+                if (nb == kBatch) {
+                    flush_batch(ws, nb, lane, p.conic_tree, p.grads);
+                    nb = 0;
+                    pc_off = lane;
+                    pp_off = lane;
+                }
+            }
+            __syncwarp();
+        }
+        if (nb) flush_batch(ws, nb, lane, p.conic_tree, p.grads);
+    }
+}
+
 }  // namespace
 
 static int sm_count() { return sb_sm_count(); }
 
-void sb_launch_raster_fwd(const RasterRec* recs, const int32_t* offsets, const int32_t* prims, int W, int H,
-                          int tiles_x, int ntiles, const sb_raster_cfg& cfg, int* tile_counter, float* color,
-                          float* T, int32_t* frags, int32_t* last, cudaStream_t stream)
+// Record staging of the fp32 raster kernels: "reg" (records gathered into
+// registers one chunk ahead, committed to the warp slab) or "tma" (64-byte
+// raster rows bulk-copied into a double-buffered slab under mbarriers; the
+// backward with 16-row chunks, "tma32" for 32-row chunks at 15 warps / SM).
+// SB_RASTER_STAGING selects one for A/B runs; the default is the measured
+// faster one (profiles/).
+static int staging_mode() {
+    const char* e = getenv("SB_RASTER_STAGING");
+    if (!e || !*e) return kDefaultStaging;
+    if (!strcmp(e, "reg")) return 0;
+    if (!strcmp(e, "tma32")) return 2;
+    if (!strcmp(e, "g4")) return 3;
+    return 1;
+}
+
+// rows as a 2-D float32 tensor (16 columns, one 64-byte row per compact
+// slot) for tile::gather4: box = one full row; 4 coordinates per load
+static bool encode_rows_tmap(CUtensorMap* m, const RasterRow* rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return false;
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {16, (cuuint64_t)1 << 28};   // rows: any compact slot count below 2^28
+    const cuuint64_t strides[1] = {sizeof(RasterRow)};
+    const cuuint32_t box[2] = {16, 1};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<RasterRow*>(rows), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void sb_launch_raster_fwd(const RasterRec* recs, const RasterRow* rows, const int32_t* offsets, const int32_t* prims,
+                          int W, int H, int tiles_x, int ntiles, const sb_raster_cfg& cfg, int* tile_counter,
+                          float* color, float* T, int32_t* frags, int32_t* last, cudaStream_t stream)
 {
     FwdParams p;
     p.recs = recs; p.offsets = offsets; p.prims = prims;
@@ -786,12 +1202,21 @@ void sb_launch_raster_fwd(const RasterRec* recs, const int32_t* offsets, const i
     if (!blocks) return;
     if (cfg.half_state == 2) sb_launch(raster_fwd_half_kernel<__nv_bfloat16>, blocks, kThreads, 0, stream, p);
     else if (cfg.half_state) sb_launch(raster_fwd_half_kernel<__half>, blocks, kThreads, 0, stream, p);
-    else sb_launch(raster_fwd_kernel, blocks, kThreads, 0, stream, p);
+    else if (rows && staging_mode() != 0) {
+        TmaFwdParams tp;
+        tp.f = p;
+        tp.rows = rows;
+        if (staging_mode() == 3 && encode_rows_tmap(&tp.tmap, rows))
+            sb_launch(raster_fwd_tma_kernel<true>, blocks, kThreads, 0, stream, tp);
+        else
+            sb_launch(raster_fwd_tma_kernel<false>, blocks, kThreads, 0, stream, tp);
+    } else sb_launch(raster_fwd_kernel, blocks, kThreads, 0, stream, p);
 }
 
-void sb_launch_raster_bwd(const RasterRec* recs, const int32_t* offsets, const int32_t* prims, int W, int H,
-                          int tiles_x, int ntiles, const sb_raster_cfg& cfg, int* tile_counter, const float* dL_dI,
-                          const float* T_final, const int32_t* last, sb_screen_grad* grads, cudaStream_t stream)
+void sb_launch_raster_bwd(const RasterRec* recs, const RasterRow* rows, const int32_t* offsets, const int32_t* prims,
+                          int W, int H, int tiles_x, int ntiles, const sb_raster_cfg& cfg, int* tile_counter,
+                          const float* dL_dI, const float* T_final, const int32_t* last, sb_screen_grad* grads,
+                          cudaStream_t stream)
 {
     BwdParams p;
     p.recs = recs; p.offsets = offsets; p.prims = prims;
@@ -802,10 +1227,35 @@ void sb_launch_raster_bwd(const RasterRec* recs, const int32_t* offsets, const i
     p.tile_counter = tile_counter;
     p.dL_dI = dL_dI; p.T_final = T_final; p.last = last; p.grads = grads;
     const int want = (ntiles + kBwdWarps - 1) / kBwdWarps;
-    const int blocks = min(want, sm_count() * 6);
-    const int smem = (int)sizeof(BwdWarpSmem) * kBwdWarps;
-    sb_smem_attr(raster_bwd_kernel, smem);
-    if (blocks) sb_launch(raster_bwd_kernel, blocks, kBwdWarps * 32, smem, stream, p);
+    if (!want) return;
+    const int mode = rows ? staging_mode() : 0;
+    if (mode == 1) {
+        TmaBwdParams tp;
+        tp.b = p;
+        tp.rows = rows;
+        const int smem = (int)sizeof(BwdTmaWarpSmem<16>) * kBwdWarps;
+        sb_smem_attr(raster_bwd_tma_kernel<16, 6, false>, smem);
+        sb_launch(raster_bwd_tma_kernel<16, 6, false>, min(want, sm_count() * 6), kBwdWarps * 32, smem, stream, tp);
+    } else if (mode == 3) {
+        TmaBwdParams tp;
+        tp.b = p;
+        tp.rows = rows;
+        const int smem = (int)sizeof(BwdTmaWarpSmem<16>) * kBwdWarps;
+        if (!encode_rows_tmap(&tp.tmap, rows)) return;
+        sb_smem_attr(raster_bwd_tma_kernel<16, 6, true>, smem);
+        sb_launch(raster_bwd_tma_kernel<16, 6, true>, min(want, sm_count() * 6), kBwdWarps * 32, smem, stream, tp);
+    } else if (mode == 2) {
+        TmaBwdParams tp;
+        tp.b = p;
+        tp.rows = rows;
+        const int smem = (int)sizeof(BwdTmaWarpSmem<32>) * kBwdWarps;
+        sb_smem_attr(raster_bwd_tma_kernel<32, 5, false>, smem);
+        sb_launch(raster_bwd_tma_kernel<32, 5, false>, min(want, sm_count() * 5), kBwdWarps * 32, smem, stream, tp);
+    } else {
+        const int smem = (int)sizeof(BwdWarpSmem) * kBwdWarps;
+        sb_smem_attr(raster_bwd_kernel, smem);
+        sb_launch(raster_bwd_kernel, min(want, sm_count() * 6), kBwdWarps * 32, smem, stream, p);
+    }
 }
 
 // ---- standalone lane reductions (reduction.py:21-58), for parity tests ----

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import itertools
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -28,6 +29,8 @@ from .scene import SceneSoA
 TILE_W, TILE_H, LANES, PIXELS_PER_LANE = 16, 8, 32, 4
 CLUSTER_SIZE = 128
 REC_FLOATS = 12  # 48-byte compact record
+ROW_FLOATS = 16  # 64-byte raster row
+TMA_STAGING = ("tma", "tma32", "g4")
 
 
 @dataclass
@@ -92,6 +95,7 @@ class RenderContext:
     visible_clusters: int
     culled_clusters: int
     recs: torch.Tensor            # (N, 12) float32 compact records (first n_compact rows)
+    rows: torch.Tensor | None     # (N, 16) float32 raster rows (TMA staging only; sb_raster_row_bytes)
     compact_map_full: torch.Tensor  # (N,) int32
     cluster_offset: torch.Tensor  # (K,) int32
     cluster_vis: torch.Tensor     # (K,) uint8
@@ -186,6 +190,11 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     stream = C.c_void_p(_lib.stream_ptr(dev))
 
     recs = torch.empty((max(n, 1), REC_FLOATS), dtype=torch.float32, device=dev)
+    # 64-byte raster rows, consumed only by the TMA-staged raster variants
+    # (SB_RASTER_STAGING=tma|tma32|g4; the default register staging reads
+    # the 48-byte records): not written otherwise
+    rows = (torch.empty((max(n, 1), ROW_FLOATS), dtype=torch.float32, device=dev)
+            if os.environ.get("SB_RASTER_STAGING", "reg") in TMA_STAGING else None)
     cmap = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     coff = torch.empty(max(K, 1), dtype=torch.int32, device=dev)
     cvis = torch.empty(max(K, 1), dtype=torch.uint8, device=dev)   # written for every cluster
@@ -199,7 +208,7 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     _sgrad_clean.pop(str(dev), None)
     _lib.call("sb_project_cull_compact", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s), _lib.ptr(recs),
               _lib.ptr(cmap), _lib.ptr(coff), _lib.ptr(cvis), _lib.ptr(counters),
-              _lib.ptr(sgrad) if sgrad is not None else None, _lib.ptr(ws), ws.numel(), stream)
+              _lib.ptr(sgrad) if sgrad is not None else None, _lib.ptr(rows), _lib.ptr(ws), ws.numel(), stream)
     # one zero-initialised state per tile grid (its count arrays stay zeroed)
     state = _lib.workspace(f"bin_state_{tx_n}x{ty_n}", lib.sb_bin_state_workspace_bytes(n, ntiles), dev)
     host, mirror = _pinned_counters(dev)
@@ -237,12 +246,12 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     frags = torch.empty((H, W), dtype=torch.int32, device=dev)
     last = torch.empty((H, W), dtype=torch.int32, device=dev)
     ws_r = _lib.workspace("raster_fwd", _lib.load().sb_raster_workspace_bytes(), dev)
-    _lib.call("sb_raster_fwd", _lib.ptr(recs), _lib.ptr(tile_buf), _lib.ptr(prims), C.byref(cam_s),
+    _lib.call("sb_raster_fwd", _lib.ptr(recs), _lib.ptr(rows), _lib.ptr(tile_buf), _lib.ptr(prims), C.byref(cam_s),
               C.byref(cfg_s), _lib.ptr(color), _lib.ptr(T), _lib.ptr(frags), _lib.ptr(last), _lib.ptr(ws_r),
               ws_r.numel(), stream)
     out = RenderOutput(color=color, transmittance=T, frag_count=frags)
     ctx = RenderContext(generation=scene.generation, camera=camera, config=config, n_total=n, n_clusters=K,
-                        n_compact=nc, n_pairs=P, visible_clusters=vis, culled_clusters=K - vis, recs=recs,
+                        n_compact=nc, n_pairs=P, visible_clusters=vis, culled_clusters=K - vis, recs=recs, rows=rows,
                         compact_map_full=cmap, cluster_offset=coff[:K], cluster_vis=cvis[:K],
                         tile_offsets=tile_offsets, tile_prims=prims[:P], transmittance=T, last=last,
                         tile_buffer=tile_buf,
