@@ -155,12 +155,20 @@ int sb_raster_fwd(const void* recs, const void* raster_rows, const int32_t* tile
 
 /* ---- backward (backward.py:205-279) --------------------------------------- */
 /* backward.py:112-267: screen-space gradients + S/M/C per compact primitive.
- * Rows [0, n_cap) of sgrad are zeroed first; n_cap = 0 accumulates into
- * sgrad as given (rows zeroed by sb_project_cull_compact's sgrad_zero). */
+ * cfg->deterministic = 0: one float atomic per (primitive, tile, channel)
+ * into sgrad; rows [0, n_cap) of sgrad are zeroed first, n_cap = 0
+ * accumulates into sgrad as given (rows zeroed by sb_project_cull_compact's
+ * sgrad_zero).  cfg->deterministic = 1: no atomics -- one row per tile-list
+ * entry, grouped by primitive with a stable radix sort and summed in tile
+ * order (the reference's np.add.at order, backward.py:261-270); every row
+ * [0, n_compact) of sgrad is written; n_pairs = P and n_compact = N_c of the
+ * forward size the workspace.  ws: sb_raster_bwd_workspace_bytes(...); its
+ * first sb_raster_workspace_bytes() are the tile queue (zero once). */
+size_t sb_raster_bwd_workspace_bytes(int32_t deterministic, int64_t n_pairs, int64_t n_compact);
 int sb_raster_bwd(const void* recs, const void* raster_rows, const int32_t* tile_offsets, const int32_t* tile_prims,
                   const sb_camera* cam, const sb_raster_cfg* cfg, const float* dL_dI, const float* transmittance,
-                  const int32_t* last, sb_screen_grad* sgrad, int64_t n_cap, void* ws, size_t ws_bytes,
-                  sb_stream_t stream);
+                  const int32_t* last, sb_screen_grad* sgrad, int64_t n_cap, int64_t n_pairs, int64_t n_compact,
+                  void* ws, size_t ws_bytes, sb_stream_t stream);
 
 /* backward.py:272-278 (_chain_projection 384-516 + scatter_grads
  * ccc.py:197-216 + stats np.add.at): grads (N, 16) float32 for every row
@@ -184,8 +192,11 @@ int sb_variance_score(const double* S, const double* M, const int32_t* C, int64_
  * over (H, W, 3) float32 images and dL/d rendered.  target is float32, or
  * uint8 (value / 255) when target_u8 != NULL.  loss[0] (float64, device) is
  * written on the stream (by the kernel's last CTA; it may be mapped host
- * memory); accum: 4 float64 (32 bytes) of scratch -- two sums and a ticket --
- * zeroed once before its first use and left zeroed by every call. */
+ * memory).  accum: sb_loss_workspace_bytes(width, height) of scratch -- a
+ * ticket and one pair of partial sums per CTA, summed in a fixed order by
+ * the last CTA (bit-reproducible) -- zeroed once before its first use; every
+ * call leaves the ticket zeroed. */
+size_t sb_loss_workspace_bytes(int32_t width, int32_t height);
 int sb_loss_fwd_bwd(const float* rendered, const float* target, const uint8_t* target_u8, int32_t width,
                     int32_t height, float lam, float* grad, double* accum, double* loss, sb_stream_t stream);
 

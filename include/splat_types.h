@@ -45,6 +45,10 @@ typedef struct sb_raster_cfg {
     int32_t conic_reduce;  /* 0: exp_aligned, 1: tree                        */
     int32_t half_state;    /* 1: fp16 blending state (forward.py:194-230);
                               2: bf16 blending state (a variant)          */
+    int32_t deterministic; /* backward: 1 = no float atomics; per-(primitive,
+                              tile) rows reduced per primitive in tile order
+                              (bit-reproducible); 0 = one
+                              atomic per (primitive, tile, channel)      */
 } sb_raster_cfg;
 
 /* Per-compact-primitive screen-gradient record written by the raster

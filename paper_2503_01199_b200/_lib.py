@@ -41,11 +41,13 @@ SIGNATURES = {
     "sb_bin_finish": ([VP, VP, I64, VP, I64, I64, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_raster_workspace_bytes": ([], SZ),
     "sb_raster_fwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
-    "sb_raster_bwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, VP, SZ, VP], C.c_int),
+    "sb_raster_bwd_workspace_bytes": ([I32, I64, I64], SZ),
+    "sb_raster_bwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, I64, I64, VP, SZ, VP], C.c_int),
     "sb_chain_projection_bwd": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP], C.c_int),
     "sb_adam_sparse": ([VP, VP, VP, VP, VP, VP, I64, VP, VP], C.c_int),
     "sb_variance_score": ([VP, VP, VP, I64, VP, VP], C.c_int),
     "sb_lane_reduce": ([VP, I64, C.c_int, VP, VP, VP], C.c_int),
+    "sb_loss_workspace_bytes": ([I32, I32], SZ),
     "sb_loss_fwd_bwd": ([VP, VP, VP, I32, I32, C.c_float, VP, VP, VP, VP], C.c_int),
 }
 
@@ -60,7 +62,8 @@ class SbCamera(C.Structure):
 class SbRasterCfg(C.Structure):
     _fields_ = [("alpha_min", C.c_float), ("alpha_max", C.c_float), ("t_stop", C.c_float),
                 ("background", C.c_float * 3), ("low_pass", C.c_float),
-                ("use_culling", C.c_int32), ("conic_reduce", C.c_int32), ("half_state", C.c_int32)]
+                ("use_culling", C.c_int32), ("conic_reduce", C.c_int32), ("half_state", C.c_int32),
+                ("deterministic", C.c_int32)]
 
 
 _lib = None

@@ -150,11 +150,14 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
     # another forward or backward has used the workspace since
     prezeroed = ctx.token != 0 and _sgrad_clean.get(str(dev)) == ctx.token
     _sgrad_clean.pop(str(dev), None)
-    ws_r = _lib.workspace("raster_bwd", _lib.load().sb_raster_workspace_bytes(), dev)
+    det = int(bool(ctx.config.deterministic))
+    ws_r = _lib.workspace("raster_bwd",
+                          _lib.load().sb_raster_bwd_workspace_bytes(det, ctx.n_pairs, ctx.n_compact), dev)
     _lib.call("sb_raster_bwd", _lib.ptr(ctx.recs), _lib.ptr(ctx.rows), _lib.ptr(ctx.tile_buffer),
               _lib.ptr(ctx.tile_prims),
               C.byref(cam_s), C.byref(cfg_s), _lib.ptr(dI), _lib.ptr(T_final), _lib.ptr(last),
-              _lib.ptr(sgrad), 0 if prezeroed else ctx.n_compact, _lib.ptr(ws_r), ws_r.numel(), stream)
+              _lib.ptr(sgrad), 0 if prezeroed else ctx.n_compact, ctx.n_pairs, ctx.n_compact, _lib.ptr(ws_r),
+              ws_r.numel(), stream)
     grads = torch.empty((n, 16), dtype=torch.float32, device=dev)
     _lib.call("sb_chain_projection_bwd", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s),
               _lib.ptr(ctx.cluster_offset), _lib.ptr(ctx.recs), _lib.ptr(sgrad), _lib.ptr(grads), _lib.ptr(stats.S),

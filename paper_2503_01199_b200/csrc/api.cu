@@ -22,7 +22,9 @@ void sb_launch_raster_fwd(const RasterRec*, const RasterRow*, const int32_t*, co
                           int*, float*, float*, int32_t*, int32_t*, cudaStream_t);
 void sb_launch_raster_bwd(const RasterRec*, const RasterRow*, const int32_t*, const int32_t*, int, int, int, int,
                           const sb_raster_cfg&,
-                          int*, const float*, const float*, const int32_t*, sb_screen_grad*, cudaStream_t);
+                          int*, const float*, const float*, const int32_t*, sb_screen_grad*, long long, long long, void*,
+                          cudaStream_t);
+size_t sb_det_workspace_bytes(long long n_pairs, long long n_compact);
 void sb_launch_lane_reduce(const float*, int, int, float*, double*, cudaStream_t);
 void sb_launch_chain(const float*, int, const CamDev&, const int32_t*, const RasterRec*, const sb_screen_grad*, float*,
                      double*,
@@ -31,6 +33,7 @@ void sb_launch_adam(float*, const float*, float*, float*, int32_t*, const uint8_
                     cudaStream_t);
 void sb_launch_loss(const float*, const float*, const uint8_t*, int, int, float, float*, double*, double*,
                     cudaStream_t);
+size_t sb_loss_accum_bytes(int W, int H);
 void sb_launch_variance(const double*, const double*, const int32_t*, int, double*, cudaStream_t);
 void sb_launch_bounds(const float*, int, float*, double*, cudaStream_t);
 int sb_bounds_partial_floats();
@@ -226,19 +229,30 @@ int sb_raster_fwd(const void* recs, const void* raster_rows, const int32_t* tile
     return check_launch("sb_raster_fwd");
 }
 
+size_t sb_raster_bwd_workspace_bytes(int32_t deterministic, int64_t n_pairs, int64_t n_compact) {
+    return sb_raster_workspace_bytes() + (deterministic ? sb_det_workspace_bytes(n_pairs, n_compact) : 0);
+}
+
 int sb_raster_bwd(const void* recs, const void* raster_rows, const int32_t* tile_offsets, const int32_t* tile_prims,
                   const sb_camera* cam,
                   const sb_raster_cfg* cfg, const float* dL_dI, const float* transmittance, const int32_t* last,
-                  sb_screen_grad* sgrad, int64_t n_cap, void* ws, size_t ws_bytes, sb_stream_t stream) {
+                  sb_screen_grad* sgrad, int64_t n_cap, int64_t n_pairs, int64_t n_compact, void* ws,
+                  size_t ws_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
-    if (ws_bytes < sb_raster_workspace_bytes()) return fail(SB_EWORKSPACE, "raster workspace too small");
+    const int det = cfg->deterministic != 0;
+    if (n_pairs < 0 || n_pairs > INT32_MAX / 2 || n_compact < 0 || n_compact > INT32_MAX / 2)
+        return fail(SB_EINVAL, "n_pairs / n_compact out of range");
+    if (ws_bytes < sb_raster_bwd_workspace_bytes(det, n_pairs, n_compact))
+        return fail(SB_EWORKSPACE, "raster backward workspace too small");
     const CamDev d = make_cam(cam, cfg);
-    if (n_cap > 0) cudaMemsetAsync(sgrad, 0, sizeof(sb_screen_grad) * (size_t)n_cap, S(stream));
+    // (the deterministic reduction writes every compact row itself)
+    if (n_cap > 0 && !det) cudaMemsetAsync(sgrad, 0, sizeof(sb_screen_grad) * (size_t)n_cap, S(stream));
+    void* det_ws = det ? static_cast<char*>(ws) + sb_raster_workspace_bytes() : nullptr;
     sb_launch_raster_bwd(static_cast<const RasterRec*>(recs), static_cast<const RasterRow*>(raster_rows), tile_offsets,
                          tile_prims, d.W, d.H, d.tiles_x,
                          d.tiles_x * d.tiles_y, *cfg, static_cast<int*>(ws), dL_dI, transmittance, last, sgrad,
-                         S(stream));
+                         n_pairs, n_compact, det_ws, S(stream));
     return check_launch("sb_raster_bwd");
 }
 
@@ -267,6 +281,11 @@ int sb_variance_score(const double* S_, const double* M_, const int32_t* C_, int
     if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
     sb_launch_variance(S_, M_, C_, (int)n, out, S(stream));
     return check_launch("sb_variance_score");
+}
+
+size_t sb_loss_workspace_bytes(int32_t width, int32_t height) {
+    if (width <= 0 || height <= 0) return 0;
+    return sb_loss_accum_bytes(width, height);
 }
 
 int sb_loss_fwd_bwd(const float* rendered, const float* target, const uint8_t* target_u8, int32_t width,

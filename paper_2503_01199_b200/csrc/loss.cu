@@ -15,8 +15,8 @@
 // pass is a register sliding window: a thread owns a short run of outputs
 // along the filter axis, loads the run + 10 inputs once from shared memory
 // and forms all outputs from registers.
-// Loss partial sums go to two float64 accumulators; the last CTA to finish
-// (a ticket next to them) forms the loss and re-zeroes them.
+// Loss partial sums: one float64 pair per CTA; the last CTA to finish (a
+// ticket) sums them in a fixed order (bit-reproducible) and forms the loss.
 #include "common.cuh"
 
 namespace {
@@ -316,26 +316,48 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
     }
     if (lane == 0) { sm.red[0][warp] = l1_sum; sm.red[1][warp] = s_sum; }
     __syncthreads();
+    // Each CTA stores its two partials in its own slot; the last CTA to
+    // finish (a ticket, accum[0]) sums all slots in a fixed order -- thread t
+    // takes slots t, t + 512, ... in sequence, then a fixed tree -- so the
+    // loss is bit-reproducible (no float atomics), forms it and re-zeroes the
+    // ticket for the next call.
+    const unsigned ncta = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    double* part = accum + 2;                 // [ncta][2]
+    __shared__ int s_last;
     if (tid == 0) {
         double a = 0, b = 0;
         for (int q = 0; q < kThreads / 32; q++) { a += sm.red[0][q]; b += sm.red[1][q]; }
-        atomicAdd(&accum[0], a);
-        atomicAdd(&accum[1], b);
-        // the last CTA to finish forms the loss and leaves the accumulators
-        // and its ticket (accum[2]) zeroed for the next call
+        part[2 * cta] = a;
+        part[2 * cta + 1] = b;
         __threadfence();
-        unsigned long long* ticket = reinterpret_cast<unsigned long long*>(accum + 2);
-        const unsigned long long ncta = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
-        if (atomicAdd(ticket, 1ull) == ncta - 1) {
-            __threadfence();
-            const double l1 = atomicAdd(&accum[0], 0.0), ss = atomicAdd(&accum[1], 0.0);
+        unsigned long long* ticket = reinterpret_cast<unsigned long long*>(accum);
+        s_last = atomicAdd(ticket, 1ull) == (unsigned long long)ncta - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        double a = 0, b = 0;
+        for (unsigned q = tid; q < ncta; q += kThreads) {
+            a += __ldcg(part + 2 * q);
+            b += __ldcg(part + 2 * q + 1);
+        }
+        for (int o = 16; o >= 1; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        __syncthreads();
+        if (lane == 0) { sm.red[0][warp] = a; sm.red[1][warp] = b; }
+        __syncthreads();
+        if (tid == 0) {
+            double l1 = 0, ss = 0;
+            for (int q = 0; q < kThreads / 32; q++) { l1 += sm.red[0][q]; ss += sm.red[1][q]; }
             const double n = (double)W * H * 3.0;
             const double ni = (double)(W - 2 * R) * (double)(H - 2 * R);
             double l = (1.0 - lam) * l1 / n;
             if (lam != 0.f) l += lam * (1.0 - (ni > 0 ? ss / (3.0 * ni) : 0.0));
             *loss_out = l;
-            accum[0] = accum[1] = 0.0;
-            *ticket = 0ull;
+            *reinterpret_cast<unsigned long long*>(accum) = 0ull;
         }
     }
 }
@@ -361,4 +383,9 @@ void sb_launch_loss(const float* x, const float* y, const uint8_t* y_u8, int W, 
     else
         sb_launch(loss_kernel<false>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum,
                   loss);
+}
+
+size_t sb_loss_accum_bytes(int W, int H) {
+    const size_t ncta = (size_t)((W + TW - 1) / TW) * (size_t)((H + TH - 1) / TH) * 3;
+    return 16 + 16 * ncta;
 }

@@ -435,6 +435,7 @@ struct BwdParams {
     const float* T_final;   // (H, W)
     const int32_t* last;    // (H, W)
     sb_screen_grad* grads;  // (N_c,) compact, zeroed
+    sb_screen_grad* pair_rows;  // deterministic mode: (P,) one row per tile-list entry, zeroed
 };
 
 SB_INLINE float warp_tree_f(float v) {
@@ -512,6 +513,7 @@ struct BwdWarpSmem {
     float2 pairs[kPairCh * kBatch * 32];
     int slot[kBatch];
     int count[kBatch];
+    int pos[kBatch];        // tile-list position of the entry (deterministic mode)
 };
 
 // reduction.py:35-58 over one row of 32 lane values held in registers:
@@ -591,6 +593,24 @@ SB_INLINE float2 row_tree2(float2 v[32]) {
 // reference (backward.py:254-255 sums float64 f and f^2 of the same f) --
 // never a densification candidate.  (The S row itself carries fl(uG^2)
 // 2^64 / o^2, whose float32 rounding would leave an ulp-level residue.)
+// Deterministic mode: the (primitive, tile) row goes to its own slot of the
+// per-entry buffer (tile-list position) with plain stores; a later ordered
+// per-primitive reduction (det_reduce_kernel) sums the rows in tile order.
+template <class WS>
+SB_INLINE void emit_row(const WS& ws, int c, int b, float out, sb_screen_grad* pair_rows) {
+    sb_screen_grad* gr = pair_rows + ws.pos[b];
+    if (c < 9) {
+        reinterpret_cast<float*>(gr)[c] = out;
+        if (c == 5) {
+            gr->M = (double)out;
+            if (ws.count[b] == 1) gr->S = (double)out * (double)out;
+        }
+        if (c == 0) gr->C = ws.count[b];
+    } else if (ws.count[b] != 1) {
+        gr->S = (double)out * 0x1p-64;
+    }
+}
+
 template <class WS>
 SB_INLINE void emit(const WS& ws, int c, int b, float out, sb_screen_grad* grads) {
     sb_screen_grad* gr = grads + ws.slot[b];
@@ -606,8 +626,9 @@ SB_INLINE void emit(const WS& ws, int c, int b, float out, sb_screen_grad* grads
     }
 }
 
-template <class WS>
-SB_INLINE void flush_batch(WS& ws, int nb, int lane, int conic_tree, sb_screen_grad* grads) {
+template <bool kDet, class WS>
+SB_INLINE void flush_batch(WS& ws, int nb, int lane, int conic_tree, sb_screen_grad* grads,
+                           sb_screen_grad* pair_rows) {
     __syncwarp();
     if (lane < kRowCh * nb) {
         const int c = lane / nb, b = lane - c * nb;
@@ -616,15 +637,21 @@ SB_INLINE void flush_batch(WS& ws, int nb, int lane, int conic_tree, sb_screen_g
         // S takes the conic rows' reduction (an exact sum rounded once, so no
         // less accurate than a tree): one code path for the whole warp
         const float out = conic_tree ? row_tree(v) : row_exp_aligned(v);
-        emit(ws, c == kConicCh ? 9 : c, b, out, grads);
+        if (kDet) emit_row(ws, c == kConicCh ? 9 : c, b, out, pair_rows);
+        else emit(ws, c == kConicCh ? 9 : c, b, out, grads);
     }
     if (lane < kPairCh * nb) {
         const int cp = lane / nb, b = lane - cp * nb;
         float2 v[32];
         load_pair_row(ws, cp * kBatch + b, v);
         const float2 out = row_tree2(v);
-        emit(ws, kConicCh + 2 * cp, b, out.x, grads);
-        emit(ws, kConicCh + 2 * cp + 1, b, out.y, grads);
+        if (kDet) {
+            emit_row(ws, kConicCh + 2 * cp, b, out.x, pair_rows);
+            emit_row(ws, kConicCh + 2 * cp + 1, b, out.y, pair_rows);
+        } else {
+            emit(ws, kConicCh + 2 * cp, b, out.x, grads);
+            emit(ws, kConicCh + 2 * cp + 1, b, out.y, grads);
+        }
     }
     __syncwarp();
 }
@@ -632,6 +659,7 @@ SB_INLINE void flush_batch(WS& ws, int nb, int lane, int conic_tree, sb_screen_g
 // 3 warps x 6 blocks = 18 warps per SM (shared memory: 6 x 37 KB)
 constexpr int kBwdWarps = 3;
 
+template <bool kDet>
 __global__ void __launch_bounds__(kBwdWarps * 32, 6)
 raster_bwd_kernel(BwdParams p)
 {
@@ -758,20 +786,21 @@ raster_bwd_kernel(BwdParams p)
                 if (lane == 0) {
                     ws.slot[nb] = r.slot;
                     ws.count[nb] = C;
+                    if (kDet) ws.pos[nb] = beg + k;
                 }
                 // next slot nb: float rows rotated by 4 nb, pair rows by 2 nb
                 ++nb;
                 pc_off = nb * 32 + ((lane + 4 * nb) & 31);
                 pp_off = nb * 32 + ((lane + 2 * nb) & 31);
                 if (nb == kBatch) {
-                    flush_batch(ws, nb, lane, p.conic_tree, p.grads);
+                    flush_batch<kDet>(ws, nb, lane, p.conic_tree, p.grads, p.pair_rows);
                     nb = 0;
                     pc_off = lane;
                     pp_off = lane;
                 }
             }
         }
-        if (nb) flush_batch(ws, nb, lane, p.conic_tree, p.grads);
+        if (nb) flush_batch<kDet>(ws, nb, lane, p.conic_tree, p.grads, p.pair_rows);
     }
 }
 
@@ -984,6 +1013,7 @@ struct __align__(128) BwdTmaWarpSmem {   // (tensor TMA destinations are 128-byt
     float2 pairs[kPairCh * kBatch * 32];
     int slot[kBatch];
     int count[kBatch];
+    int pos[kBatch];
     uint64_t bar[2];
 };
 
@@ -1135,7 +1165,7 @@ raster_bwd_tma_kernel(const __grid_constant__ TmaBwdParams tp)
                 pc_off = nb * 32 + ((lane + 4 * nb) & 31);
                 pp_off = nb * 32 + ((lane + 2 * nb) & 31);
                 if (nb == kBatch) {
-                    flush_batch(ws, nb, lane, p.conic_tree, p.grads);
+                    flush_batch<false>(ws, nb, lane, p.conic_tree, p.grads, nullptr);
                     nb = 0;
                     pc_off = lane;
                     pp_off = lane;
@@ -1143,7 +1173,7 @@ raster_bwd_tma_kernel(const __grid_constant__ TmaBwdParams tp)
             }
             __syncwarp();
         }
-        if (nb) flush_batch(ws, nb, lane, p.conic_tree, p.grads);
+        if (nb) flush_batch<false>(ws, nb, lane, p.conic_tree, p.grads, nullptr);
     }
 }
 
@@ -1213,10 +1243,114 @@ void sb_launch_raster_fwd(const RasterRec* recs, const RasterRow* rows, const in
     } else sb_launch(raster_fwd_kernel, blocks, kThreads, 0, stream, p);
 }
 
+// ---- deterministic backward: ordered per-primitive reduction -------------
+// (backward.py:261-270: np.add.at scatters each tile's per-primitive values
+// in tile order.)  The raster backward wrote one sb_screen_grad row per
+// tile-list entry; the entries are grouped by compact slot with a stable
+// radix sort of the slots (values = entry positions, so each group stays in
+// tile order), and each primitive's rows are summed in that order -- float32
+// channels in float32 like the reference's g_screen, S / M in float64, C in
+// integers.  No atomics: bit-reproducible for identical inputs.
+size_t sb_sort_u32_ws(int n_cap, int bits);
+int sb_launch_sort_u32_iota(uint32_t*, uint32_t*, uint32_t*, uint32_t*, const int*, int, int, void*, cudaStream_t);
+
+namespace {
+__global__ void det_segments_kernel(const uint32_t* __restrict__ keys, const int32_t* __restrict__ n_dev,
+                                    int32_t* __restrict__ start, int32_t* __restrict__ end)
+{
+    sb_pdl_begin();
+    const int P = *n_dev;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        if (i == 0 || keys[i - 1] != k) start[k] = i;
+        if (i == P - 1 || keys[i + 1] != k) end[k] = i + 1;
+    }
+}
+
+__global__ void det_reduce_kernel(const sb_screen_grad* __restrict__ rows, const uint32_t* __restrict__ order,
+                                  const int32_t* __restrict__ start, const int32_t* __restrict__ end, int nc,
+                                  sb_screen_grad* __restrict__ out)
+{
+    sb_pdl_begin();
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nc) return;
+    float acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    double S = 0.0, M = 0.0;
+    int C = 0;
+    const int e = end[s];
+    for (int i = start[s]; i < e; i++) {
+        const sb_screen_grad& r = rows[order[i]];
+        const float* f = reinterpret_cast<const float*>(&r);
+#pragma unroll
+        for (int c = 0; c < 9; c++) acc[c] = FADD(acc[c], f[c]);
+        S = DADD(S, r.S);
+        M = DADD(M, r.M);
+        C += r.C;
+    }
+    sb_screen_grad o;
+    o.a = acc[0]; o.b = acc[1]; o.c = acc[2]; o.u = acc[3]; o.v = acc[4]; o.o = acc[5];
+    o.r = acc[6]; o.g = acc[7]; o.bl = acc[8];
+    o.C = C; o.S = S; o.M = M; o.pad_ = 0.0;
+    out[s] = o;
+}
+}  // namespace
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static int bits_for(long long n) {
+    int b = 1;
+    while (b < 32 && (1ll << b) < n) b++;
+    return b;
+}
+
+size_t sb_det_workspace_bytes(long long n_pairs, long long n_compact) {
+    const size_t P = (size_t)(n_pairs > 0 ? n_pairs : 1), nc = (size_t)(n_compact > 0 ? n_compact : 1);
+    return align256(P * sizeof(sb_screen_grad)) + 4 * align256(P * 4) + 2 * align256(nc * 4) +
+           align256(sb_sort_u32_ws((int)P, bits_for((long long)nc)));
+}
+
+// deterministic backward: rows per tile-list entry, grouped by slot (stable
+// sort), reduced in tile order into p.grads (every compact slot written)
+static void raster_bwd_det(BwdParams p, int want, const int32_t* n_pairs_dev, const int32_t* prims, long long n_pairs,
+                           long long n_compact, void* ws, cudaStream_t stream)
+{
+    const size_t P = (size_t)(n_pairs > 0 ? n_pairs : 1), nc = (size_t)(n_compact > 0 ? n_compact : 1);
+    char* w = static_cast<char*>(ws);
+    sb_screen_grad* pair_rows = reinterpret_cast<sb_screen_grad*>(w); w += align256(P * sizeof(sb_screen_grad));
+    uint32_t* keys = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
+    uint32_t* keys_alt = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
+    uint32_t* vals = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
+    uint32_t* vals_alt = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
+    int32_t* start = reinterpret_cast<int32_t*>(w); w += align256(nc * 4);
+    int32_t* end = reinterpret_cast<int32_t*>(w); w += align256(nc * 4);
+    void* sort_ws = w;
+    if (n_pairs > 0) cudaMemsetAsync(pair_rows, 0, (size_t)n_pairs * sizeof(sb_screen_grad), stream);
+    cudaMemsetAsync(start, 0, nc * 4, stream);
+    cudaMemsetAsync(end, 0, nc * 4, stream);
+    p.pair_rows = pair_rows;
+    const int smem = (int)sizeof(BwdWarpSmem) * kBwdWarps;
+    sb_smem_attr(raster_bwd_kernel<true>, smem);
+    sb_launch(raster_bwd_kernel<true>, min(want, sm_count() * 6), kBwdWarps * 32, smem, stream, p);
+    if (n_compact <= 0) return;
+    if (n_pairs > 0) {
+        cudaMemcpyAsync(keys, prims, (size_t)n_pairs * 4, cudaMemcpyDeviceToDevice, stream);
+        const int flip = sb_launch_sort_u32_iota(keys, vals, keys_alt, vals_alt, n_pairs_dev, (int)n_pairs,
+                                                 bits_for(n_compact), sort_ws, stream);
+        if (flip) {
+            keys = keys_alt;
+            vals = vals_alt;
+        }
+        sb_launch(det_segments_kernel, min((int)((n_pairs + 255) / 256), sm_count() * 8), 256, 0, stream, keys,
+                  n_pairs_dev, start, end);
+    }
+    sb_launch(det_reduce_kernel, (int)((n_compact + 255) / 256), 256, 0, stream, pair_rows, vals, start, end,
+              (int)n_compact, p.grads);
+}
+
 void sb_launch_raster_bwd(const RasterRec* recs, const RasterRow* rows, const int32_t* offsets, const int32_t* prims,
                           int W, int H, int tiles_x, int ntiles, const sb_raster_cfg& cfg, int* tile_counter,
                           const float* dL_dI, const float* T_final, const int32_t* last, sb_screen_grad* grads,
-                          cudaStream_t stream)
+                          long long n_pairs, long long n_compact, void* det_ws, cudaStream_t stream)
 {
     BwdParams p;
     p.recs = recs; p.offsets = offsets; p.prims = prims;
@@ -1225,9 +1359,13 @@ void sb_launch_raster_bwd(const RasterRec* recs, const RasterRow* rows, const in
     for (int c = 0; c < 3; c++) p.bg[c] = cfg.background[c];
     p.conic_tree = cfg.conic_reduce == 1;
     p.tile_counter = tile_counter;
-    p.dL_dI = dL_dI; p.T_final = T_final; p.last = last; p.grads = grads;
+    p.dL_dI = dL_dI; p.T_final = T_final; p.last = last; p.grads = grads; p.pair_rows = nullptr;
     const int want = (ntiles + kBwdWarps - 1) / kBwdWarps;
     if (!want) return;
+    if (det_ws) {
+        raster_bwd_det(p, want, offsets + ntiles, prims, n_pairs, n_compact, det_ws, stream);
+        return;
+    }
     const int mode = rows ? staging_mode() : 0;
     if (mode == 1) {
         TmaBwdParams tp;
@@ -1253,8 +1391,8 @@ void sb_launch_raster_bwd(const RasterRec* recs, const RasterRow* rows, const in
         sb_launch(raster_bwd_tma_kernel<32, 5, false>, min(want, sm_count() * 5), kBwdWarps * 32, smem, stream, tp);
     } else {
         const int smem = (int)sizeof(BwdWarpSmem) * kBwdWarps;
-        sb_smem_attr(raster_bwd_kernel, smem);
-        sb_launch(raster_bwd_kernel, min(want, sm_count() * 6), kBwdWarps * 32, smem, stream, p);
+        sb_smem_attr(raster_bwd_kernel<false>, smem);
+        sb_launch(raster_bwd_kernel<false>, min(want, sm_count() * 6), kBwdWarps * 32, smem, stream, p);
     }
 }
 

@@ -46,6 +46,11 @@ class RasterConfig:
     low_pass: float = 0.3
     use_culling: bool = True
     conic_reduce: str = "exp_aligned"   # backward: "exp_aligned" | "tree"
+    # backward without float atomics: per-(primitive, tile) rows reduced per
+    # primitive in tile order, bit-reproducible (the
+    # reference's "deterministic" mode).  train() turns it on
+    # with TrainConfig(deterministic=True), the reference's default.
+    deterministic: bool = False
 
     def struct(self, half=False) -> _lib.SbRasterCfg:
         if self.dtype != "float32":
@@ -62,6 +67,7 @@ class RasterConfig:
         s.use_culling = int(bool(self.use_culling))
         s.conic_reduce = 0 if self.conic_reduce == "exp_aligned" else 1
         s.half_state = _half_mode(half)
+        s.deterministic = int(bool(self.deterministic))
         return s
 
 

@@ -120,7 +120,8 @@ def loss_and_grad(rendered: torch.Tensor, target, lam: float, return_tensor: boo
     else:
         y = y.float().contiguous()
     grad = torch.empty_like(x)
-    acc = _lib.workspace("loss_accum", 32, x.device)       # zeroed once, left zeroed by the call
+    # ticket + per-CTA partials: zeroed once, the ticket left zeroed by the call
+    acc = _lib.workspace("loss_accum", _lib.load().sb_loss_workspace_bytes(W, H), x.device)
     out_ptr = None
     if loss_out is not None:
         if loss_out.device.type != "cpu" or not loss_out.is_pinned() or loss_out.dtype != torch.float64:

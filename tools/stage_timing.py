@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--res", default="1920x1080")
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--deterministic", action="store_true", help="RasterConfig(deterministic=True)")
     a = ap.parse_args()
     W, H = (int(v) for v in a.res.split("x"))
     arr = scaled_scene_arrays(a.n, 7, (W, H))
@@ -42,11 +43,12 @@ def main():
     cam = camera_ring(SyntheticSceneSpec(n_gaussians=a.n, n_views=1, view_resolution=(W, H), seed=7))[0]
     target = torch.rand(H, W, 3, device="cuda", generator=torch.Generator("cuda").manual_seed(0))
     lrs = sb.LearningRates().at(0.0, 3.2)
+    rcfg = sb.RasterConfig(deterministic=a.deterministic)
     rows = []
     for it in range(a.iters + 3):
         es = [ev() for _ in range(5)]
         es[0].record()
-        out, ctx = sb.forward(scene, cam)
+        out, ctx = sb.forward(scene, cam, rcfg)
         es[1].record()
         loss, dI = sb.loss_and_grad(out.color, target, 0.2, return_tensor=True)
         es[2].record()
@@ -58,7 +60,7 @@ def main():
         if it >= 3:
             rows.append([es[i].elapsed_time(es[i + 1]) for i in range(4)])
     r = np.median(np.array(rows), axis=0)
-    print(json.dumps({"n": a.n, "res": [W, H], "P": ctx.n_pairs, "n_compact": ctx.n_compact,
+    print(json.dumps({"deterministic": a.deterministic, "n": a.n, "res": [W, H], "P": ctx.n_pairs, "n_compact": ctx.n_compact,
                       "morton_sort_ms": t_sort, "forward_ms": r[0], "loss_ms": r[1], "backward_ms": r[2],
                       "adam_ms": r[3], "iter_ms": float(r.sum())}))
 
