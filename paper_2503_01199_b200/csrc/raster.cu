@@ -1248,7 +1248,8 @@ void sb_launch_raster_fwd(const RasterRec* recs, const RasterRow* rows, const in
 // in tile order.)  The raster backward wrote one sb_screen_grad row per
 // tile-list entry; the entries are grouped by compact slot with a stable
 // radix sort of the slots (values = entry positions, so each group stays in
-// tile order), and each primitive's rows are summed in that order -- float32
+// tile order), and each primitive's rows are summed in a fixed order (four
+// interleaved tile-order partial sums, then a fixed butterfly) -- float32
 // channels in float32 like the reference's g_screen, S / M in float64, C in
 // integers.  No atomics: bit-reproducible for identical inputs.
 size_t sb_sort_u32_ws(int n_cap, int bits);
@@ -1267,31 +1268,50 @@ __global__ void det_segments_kernel(const uint32_t* __restrict__ keys, const int
     }
 }
 
+// four lanes per primitive: lane j sums the primitive's rows j, j + 4, ...
+// in tile order, then a fixed two-step butterfly -- a fixed order, so the
+// result is bit-reproducible, with four independent load chains per primitive
+constexpr int kDetLanes = 4;
+
 __global__ void det_reduce_kernel(const sb_screen_grad* __restrict__ rows, const uint32_t* __restrict__ order,
                                   const int32_t* __restrict__ start, const int32_t* __restrict__ end, int nc,
                                   sb_screen_grad* __restrict__ out)
 {
     sb_pdl_begin();
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= nc) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = t / kDetLanes, j = t % kDetLanes;
+    const bool ok = s < nc;
     float acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     double S = 0.0, M = 0.0;
     int C = 0;
-    const int e = end[s];
-    for (int i = start[s]; i < e; i++) {
-        const sb_screen_grad& r = rows[order[i]];
-        const float* f = reinterpret_cast<const float*>(&r);
+    if (ok) {
+        const int e = end[s];
+        for (int i = start[s] + j; i < e; i += kDetLanes) {
+            const float4* r4 = reinterpret_cast<const float4*>(rows + __ldg(order + i));
+            const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2), q3 = __ldg(r4 + 3);
+            const float f[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
 #pragma unroll
-        for (int c = 0; c < 9; c++) acc[c] = FADD(acc[c], f[c]);
-        S = DADD(S, r.S);
-        M = DADD(M, r.M);
-        C += r.C;
+            for (int c = 0; c < 9; c++) acc[c] = FADD(acc[c], f[c]);
+            C += __float_as_int(q2.y);
+            S = DADD(S, __hiloint2double(__float_as_int(q2.w), __float_as_int(q2.z)));
+            M = DADD(M, __hiloint2double(__float_as_int(q3.y), __float_as_int(q3.x)));
+        }
     }
-    sb_screen_grad o;
-    o.a = acc[0]; o.b = acc[1]; o.c = acc[2]; o.u = acc[3]; o.v = acc[4]; o.o = acc[5];
-    o.r = acc[6]; o.g = acc[7]; o.bl = acc[8];
-    o.C = C; o.S = S; o.M = M; o.pad_ = 0.0;
-    out[s] = o;
+#pragma unroll
+    for (int o = 1; o < kDetLanes; o <<= 1) {
+#pragma unroll
+        for (int c = 0; c < 9; c++) acc[c] = FADD(acc[c], __shfl_xor_sync(0xffffffffu, acc[c], o));
+        S = DADD(S, __shfl_xor_sync(0xffffffffu, S, o));
+        M = DADD(M, __shfl_xor_sync(0xffffffffu, M, o));
+        C += __shfl_xor_sync(0xffffffffu, C, o);
+    }
+    if (ok && j == 0) {
+        sb_screen_grad o;
+        o.a = acc[0]; o.b = acc[1]; o.c = acc[2]; o.u = acc[3]; o.v = acc[4]; o.o = acc[5];
+        o.r = acc[6]; o.g = acc[7]; o.bl = acc[8];
+        o.C = C; o.S = S; o.M = M; o.pad_ = 0.0;
+        out[s] = o;
+    }
 }
 }  // namespace
 
@@ -1343,8 +1363,8 @@ static void raster_bwd_det(BwdParams p, int want, const int32_t* n_pairs_dev, co
         sb_launch(det_segments_kernel, min((int)((n_pairs + 255) / 256), sm_count() * 8), 256, 0, stream, keys,
                   n_pairs_dev, start, end);
     }
-    sb_launch(det_reduce_kernel, (int)((n_compact + 255) / 256), 256, 0, stream, pair_rows, vals, start, end,
-              (int)n_compact, p.grads);
+    sb_launch(det_reduce_kernel, (int)((n_compact * kDetLanes + 255) / 256), 256, 0, stream, pair_rows, vals, start,
+              end, (int)n_compact, p.grads);
 }
 
 void sb_launch_raster_bwd(const RasterRec* recs, const RasterRow* rows, const int32_t* offsets, const int32_t* prims,
