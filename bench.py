@@ -111,6 +111,9 @@ def setup_dist():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # NCCL's own report of the communicator (ranks, NVLink / NVLS paths)
+        # on stderr, for the driver's multi-GPU records
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         ndev = max(torch.cuda.device_count(), 1)
         if ws <= ndev:
             torch.cuda.set_device(local)
@@ -141,13 +144,13 @@ def build_workload(device):
 class Trainer:
     """One training iteration through the public API (train.py:95-104)."""
 
-    def __init__(self, scene, state, views, ws, rank):
+    def __init__(self, scene, state, views, ws, rank, zero1=False):
         import paper_2503_01199_b200 as sb
         from paper_2503_01199_b200.parallel import ViewParallel
         self.sb = sb
         self.scene, self.state, self.views = scene, state, views
         self.ws, self.rank = ws, rank
-        self.vp = ViewParallel()
+        self.vp = ViewParallel(zero1=zero1)
         self.lrs = sb.LearningRates().at(0.0, position_scale=3.2)
 
     def view_index(self, it):
@@ -160,6 +163,12 @@ class Trainer:
         loss, dI = sb.loss_and_grad(out.color, target, 0.2, return_tensor=True, loss_out=loss_out)
         # statistics accumulate rank-locally in the scene (summed over ranks
         # only when read: ViewParallel.reduce_stats before a densify step)
+        if self.vp.zero1:
+            # ZeRO-1: reduce-scatter the gradient rows, sharded Adam, all-gather
+            gbuf = self.vp.grad_buffer(self.scene.n, self.scene.device)
+            res = sb.backward(self.scene, ctx, dI, sb.DensifyStats.from_scene(self.scene), grads_out=gbuf)
+            self.vp.zero1_step(self.scene, gbuf, res.cluster_mask, self.state, self.lrs)
+            return loss, ctx
         res = sb.backward(self.scene, ctx, dI, sb.DensifyStats.from_scene(self.scene))
         mask = res.cluster_mask
         if self.ws > 1:
@@ -265,6 +274,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--zero1", action="store_true", help="N > 1: reduce-scatter + sharded Adam + all-gather")
     args = ap.parse_args()
     ws, rank, local = setup_dist()
     if args.impl == "reference":
@@ -279,7 +289,7 @@ def main():
     import paper_2503_01199_b200 as sb
     from paper_2503_01199_b200 import _lib
     scene, state, views, targets_host = build_workload(device)
-    trainer = Trainer(scene, state, views, ws, rank)
+    trainer = Trainer(scene, state, views, ws, rank, zero1=args.zero1)
     # targets stay uint8 (the dataset format); the fused loss reads them directly
     targets_dev = [t.to(device) for t in targets_host]
 
@@ -389,6 +399,18 @@ def main():
             cpu = {"value": None, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {e}"}
 
+    # rank consistency: every rank must hold bit-identical parameters after
+    # the timed steps (one identical Adam step per step on every rank)
+    consistency = None
+    if ws > 1:
+        h = scene.data.contiguous().view(torch.int32).to(torch.int64)
+        w = torch.arange(1, h.numel() + 1, device=h.device, dtype=torch.int64).view_as(h) % 1000003
+        ck = torch.stack([(h * w).sum() % (1 << 61), h.sum()])
+        allck = [torch.zeros_like(ck) for _ in range(ws)]
+        dist.all_gather(allck, ck)
+        vals = [tuple(int(v) for v in c.tolist()) for c in allck]
+        consistency = {"param_checksums": [v[0] for v in vals], "ranks_identical": len(set(vals)) == 1}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
@@ -411,6 +433,10 @@ def main():
             "clocks": clk,
             "cpu_baseline": cpu,
         }
+        if consistency is not None:
+            line["rank_consistency"] = consistency
+            line["config"]["optimizer_step"] = "zero1 (reduce-scatter, sharded Adam, all-gather)" if args.zero1 \
+                else "all-reduce of the gradient rows, replicated Adam"
         print(json.dumps(line))
     if ws > 1:
         dist.barrier()

@@ -110,9 +110,11 @@ class BackwardResult:
 
 
 def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | None = None,
-             trace=None) -> BackwardResult:
+             trace=None, grads_out: torch.Tensor | None = None) -> BackwardResult:
     """backward.py:205-279.  dL_dI is (H, W, 3) (any float dtype / device;
-    cast to float32 on the scene's device)."""
+    cast to float32 on the scene's device).  grads_out: optional preallocated
+    float32 rows (>= N, 16), e.g. padded for a reduce-scatter; the gradient
+    rows are its first N rows."""
     if trace is not None:
         raise ValueError("per-fragment traces are a CPU-oracle debug feature")
     if ctx.generation != scene.generation:
@@ -158,7 +160,14 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
               C.byref(cam_s), C.byref(cfg_s), _lib.ptr(dI), _lib.ptr(T_final), _lib.ptr(last),
               _lib.ptr(sgrad), 0 if prezeroed else ctx.n_compact, ctx.n_pairs, ctx.n_compact, _lib.ptr(ws_r),
               ws_r.numel(), stream)
-    grads = torch.empty((n, 16), dtype=torch.float32, device=dev)
+    if grads_out is None:
+        grads = torch.empty((n, 16), dtype=torch.float32, device=dev)
+    else:
+        if (grads_out.dtype != torch.float32 or grads_out.dim() != 2 or grads_out.shape[1] != 16
+                or grads_out.shape[0] < n or not grads_out.is_contiguous() or grads_out.device != scene.data.device):
+            raise ShapeMismatchError(f"grads_out {tuple(grads_out.shape)} {grads_out.dtype} must be contiguous "
+                                     f"float32 (>= {n}, 16) on {scene.data.device}")
+        grads = grads_out[:n]
     _lib.call("sb_chain_projection_bwd", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s),
               _lib.ptr(ctx.cluster_offset), _lib.ptr(ctx.recs), _lib.ptr(sgrad), _lib.ptr(grads), _lib.ptr(stats.S),
               _lib.ptr(stats.M), _lib.ptr(stats.C), stream)

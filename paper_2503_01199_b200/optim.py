@@ -77,24 +77,34 @@ class AdamState:
 
 
 def adam_step(scene: SceneSoA, grads, state: AdamState, cluster_mask, lrs: dict,
-              cluster_size: int = CLUSTER_SIZE):
-    """One sparse Adam update confined to true-masked clusters (optim.py:69-98)."""
+              cluster_size: int = CLUSTER_SIZE, rows: tuple | None = None):
+    """One sparse Adam update confined to true-masked clusters (optim.py:69-98).
+
+    rows=(r0, r1) (r0 a multiple of 128) updates only scene rows [r0, r1):
+    `grads` and `cluster_mask` then hold just those rows / their clusters (a
+    ZeRO-1 shard, parallel.ViewParallel(zero1=True))."""
     n = scene.n
     if n == 0:
         return
     if cluster_size != CLUSTER_SIZE:
         raise ValueError("the device optimiser uses 128-primitive clusters")
+    r0, r1 = (0, n) if rows is None else (int(rows[0]), int(rows[1]))
+    if r0 % CLUSTER_SIZE or not (0 <= r0 <= r1 <= n):
+        raise ValueError(f"row range {rows} must be cluster-aligned within [0, {n}]")
+    m = r1 - r0
+    if m == 0:
+        return
     from .backward import SceneGrads
     if not isinstance(grads, SceneGrads):
-        grads = SceneGrads.from_dict(grads.as_dict() if hasattr(grads, "as_dict") else grads, n, scene.device)
+        grads = SceneGrads.from_dict(grads.as_dict() if hasattr(grads, "as_dict") else grads, m, scene.device)
     from .errors import ShapeMismatchError
     packed = grads.packed
-    if tuple(packed.shape) != (n, 16) or packed.dtype != torch.float32 or packed.device != scene.data.device:
+    if tuple(packed.shape) != (m, 16) or packed.dtype != torch.float32 or packed.device != scene.data.device:
         raise ShapeMismatchError(f"gradient rows {tuple(packed.shape)} {packed.dtype} on {packed.device} "
-                                 f"!= ({n}, 16) float32 on {scene.data.device}")
+                                 f"!= ({m}, 16) float32 on {scene.data.device}")
     packed = packed.contiguous()
     mask = torch.as_tensor(cluster_mask, device=scene.device)
-    k = (n + CLUSTER_SIZE - 1) // CLUSTER_SIZE
+    k = (m + CLUSTER_SIZE - 1) // CLUSTER_SIZE
     if mask.numel() != k:
         raise ShapeMismatchError(f"cluster mask length {mask.numel()} != {k} clusters")
     mask = (mask.view(torch.uint8) if mask.dtype == torch.bool else (mask != 0).to(torch.uint8)).contiguous()
@@ -102,6 +112,6 @@ def adam_step(scene: SceneSoA, grads, state: AdamState, cluster_mask, lrs: dict,
         if t.shape[0] != n or t.device != scene.data.device:
             raise ShapeMismatchError(f"Adam {name} has {t.shape[0]} rows on {t.device} != {n} on {scene.data.device}")
     lr = (C.c_double * 5)(*[float(lrs[k]) for k in RAW_CHANNELS])
-    _lib.call("sb_adam_sparse", _lib.ptr(scene.data), _lib.ptr(packed), _lib.ptr(state.m_rows),
-              _lib.ptr(state.v_rows), _lib.ptr(state.step), _lib.ptr(mask), n, lr,
+    _lib.call("sb_adam_sparse", _lib.ptr(scene.data[r0:r1]), _lib.ptr(packed), _lib.ptr(state.m_rows[r0:r1]),
+              _lib.ptr(state.v_rows[r0:r1]), _lib.ptr(state.step[r0:r1]), _lib.ptr(mask), m, lr,
               C.c_void_p(_lib.stream_ptr(scene.device)))

@@ -36,10 +36,86 @@ MASK_COL = 14     # padding column of the gradient rows that carries the cluster
 
 
 class ViewParallel:
-    def __init__(self, group=None):
+    """zero1=True: the optimiser step is sharded (ZeRO stage 1) -- the
+    gradient rows are REDUCE-SCATTERED in cluster-aligned row shards (mask in
+    the padding column), each rank runs the sparse Adam on its shard only
+    (the 400 B/row Adam traffic splits by the world size), and the updated
+    parameter rows are ALL-GATHERED.  Same bytes on the wire as one
+    all-reduce (which is a reduce-scatter + all-gather); the moments of other
+    ranks' shards are stale until sync_optimizer_state(), which every
+    restructuring (densify, Morton re-sort, checkpoint) must be preceded by."""
+
+    def __init__(self, group=None, zero1: bool = False):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.zero1 = bool(zero1) and self.world > 1
+        self._bufs = {}
+
+    # ---- ZeRO-1 ---------------------------------------------------------------
+    def shard_rows(self, n: int) -> int:
+        """Rows per rank: equal, cluster-aligned shards covering n rows."""
+        k = (n + CLUSTER_SIZE - 1) // CLUSTER_SIZE
+        return ((k + self.world - 1) // self.world) * CLUSTER_SIZE
+
+    def padded_rows(self, n: int) -> int:
+        return self.shard_rows(n) * self.world
+
+    def grad_buffer(self, n: int, device) -> torch.Tensor:
+        """Padded (world x shard, 16) gradient rows for backward(grads_out=);
+        rows >= n stay zero."""
+        key = ("grads", n, str(device))
+        if key not in self._bufs:
+            self._bufs = {k: v for k, v in self._bufs.items() if k[1] == n}
+            self._bufs[key] = torch.zeros((self.padded_rows(n), 16), dtype=torch.float32, device=device)
+        return self._bufs[key]
+
+    def zero1_step(self, scene, grads_padded: torch.Tensor, cluster_mask: torch.Tensor, state, lrs: dict):
+        """Reduce-scatter the (padded) gradient rows, sharded sparse Adam,
+        all-gather the parameter rows.  grads_padded: grad_buffer(n) whose
+        first n rows hold this rank's gradient sum; cluster_mask: (K,)."""
+        from .backward import SceneGrads
+        from .optim import adam_step
+        n = scene.n
+        per = self.shard_rows(n)
+        if grads_padded.shape[0] != per * self.world:
+            raise ValueError("grads_padded must come from grad_buffer(scene.n)")
+        heads = grads_padded[:n:CLUSTER_SIZE, MASK_COL]
+        heads.copy_(cluster_mask.to(grads_padded.dtype))
+        shard = torch.empty((per, 16), dtype=grads_padded.dtype, device=grads_padded.device)
+        dist.reduce_scatter_tensor(shard, grads_padded, group=self.group)
+        r0 = self.rank * per
+        r1 = min(r0 + per, n)
+        m = max(r1 - r0, 0)
+        mask = shard[::CLUSTER_SIZE, MASK_COL] > 0
+        shard[::CLUSTER_SIZE, MASK_COL] = 0.0
+        if m:
+            adam_step(scene, SceneGrads(shard[:m].contiguous()), state,
+                      mask[:(m + CLUSTER_SIZE - 1) // CLUSTER_SIZE], lrs, rows=(r0, r1))
+        send = torch.zeros((per, 16), dtype=scene.data.dtype, device=scene.data.device)
+        if m:
+            send[:m] = scene.data[r0:r1]
+        full = torch.empty((per * self.world, 16), dtype=scene.data.dtype, device=scene.data.device)
+        dist.all_gather_into_tensor(full, send, group=self.group)
+        scene.data.copy_(full[:n])
+
+    def sync_optimizer_state(self, state):
+        """All-gather every rank's Adam moment / step shards (ZeRO-1), so all
+        ranks hold the full optimiser state before a restructuring."""
+        if not self.zero1:
+            return
+        scene = state.scene
+        n = scene.n
+        per = self.shard_rows(n)
+        r0, r1 = self.rank * per, min(self.rank * per + per, n)
+        for t in (state.m_rows, state.v_rows, state.step.view(-1, 1)):
+            width = t.shape[1]
+            send = torch.zeros((per, width), dtype=t.dtype, device=t.device)
+            if r1 > r0:
+                send[:r1 - r0] = t[r0:r1]
+            full = torch.empty((per * self.world, width), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(full, send, group=self.group)
+            t.copy_(full[:n])
 
     def views_for_step(self, step: int, n_views: int, views_per_rank: int = 1) -> list:
         """Indices of the views this rank renders at `step` (round robin)."""

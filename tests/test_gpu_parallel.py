@@ -23,7 +23,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, zero1=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -41,12 +41,13 @@ def _worker(rank, world, port, out):
         scene = sb.SceneSoA(*[init[k] for k in G.CH], device="cuda")
         cfg = sb.TrainConfig(epochs=8, lrs=sb.LearningRates(color=2e-2),
                              densify=sb.DensifyConfig(start_epoch=2, densify_interval_epochs=3, budget=660))
-        vp = ViewParallel()
+        vp = ViewParallel(zero1=zero1)
         res = sb.train(cfg, scene, views, parallel=vp)
         st = sb.DensifyStats.from_scene(scene)     # rank-local since the last densify
         S = st.S.clone()
         vp.reduce_stats(S, st.M.clone(), st.C.clone())
         out[rank] = dict(data=scene.data.cpu().numpy(), S=S.cpu().numpy(), S_local=st.S.cpu().numpy(),
+                         m=scene.extras["adam_m"].cpu().numpy(), step=scene.extras["adam_step"].cpu().numpy(),
                          losses=[m.loss for m in res.metrics], n=scene.n, log=len(res.densify_log))
     finally:
         dist.destroy_process_group()
@@ -64,3 +65,22 @@ def test_view_parallel_train_two_ranks():
     assert not np.array_equal(a["S_local"], b["S_local"])   # reduced only when read
     assert a["losses"] == b["losses"]
     assert a["losses"][-1] < 0.7 * a["losses"][0]
+
+
+def test_view_parallel_train_two_ranks_zero1():
+    """ViewParallel(zero1=True): reduce-scatter + sharded Adam + all-gather
+    gives the same parameters and (after the final sync) the same optimiser
+    state as the all-reduce step."""
+    world = 2
+    res = {}
+    for z in (False, True):
+        mgr = mp.Manager()
+        out = mgr.dict()
+        mp.start_processes(_worker, args=(world, _free_port(), out, z), nprocs=world, join=True,
+                           start_method="spawn")
+        res[z] = (out[0], out[1])
+    for r in range(2):
+        assert np.array_equal(res[True][r]["data"], res[False][r]["data"])
+        assert np.array_equal(res[True][r]["m"], res[False][r]["m"])
+        assert np.array_equal(res[True][r]["step"], res[False][r]["step"])
+    assert res[True][0]["losses"] == res[False][0]["losses"]

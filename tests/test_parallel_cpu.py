@@ -69,3 +69,58 @@ def test_single_process_is_identity():
     m = vp.reduce(g, torch.zeros(4, dtype=torch.float64), torch.zeros(4, dtype=torch.float64),
                   torch.zeros(4, dtype=torch.int32), torch.tensor([1], dtype=torch.uint8))
     assert m.tolist() == [True] and float(g.sum()) == 64.0
+
+
+def _zero1_worker(rank, world, port, out):
+    """ZeRO-1 step on CPU tensors with a torch stand-in for the device Adam:
+    reduce-scatter of cluster-aligned shards (mask in the padding column),
+    each rank updates only its rows, all-gather of the parameters, then a
+    sync of the per-shard optimiser state."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import types
+        import paper_2503_01199_b200.optim as optim
+        from paper_2503_01199_b200.parallel import ViewParallel
+
+        def fake_adam(scene, grads, state, mask, lrs, rows=None):
+            r0, r1 = rows
+            m = torch.repeat_interleave(mask, 128)[: r1 - r0]
+            g = grads.packed if hasattr(grads, "packed") else grads
+            upd = torch.where(m[:, None], -0.5 * torch.sign(g), torch.zeros_like(g))
+            scene.data[r0:r1] += upd
+            state.m_rows[r0:r1] += torch.where(m[:, None], g, torch.zeros_like(g))
+            state.step[r0:r1] += m.to(torch.int32)
+        optim.adam_step = fake_adam
+        vp = ViewParallel(zero1=True)
+        n = 700                                      # 6 clusters, shards of 3 clusters = 384 rows
+        assert vp.shard_rows(n) == 384 and vp.padded_rows(n) == 768
+        scene = types.SimpleNamespace(n=n, data=torch.zeros((n, 16)))
+        state = types.SimpleNamespace(scene=scene, m_rows=torch.zeros((n, 16)), v_rows=torch.zeros((n, 16)),
+                                      step=torch.zeros(n, dtype=torch.int32))
+        gb = vp.grad_buffer(n, "cpu")
+        gb[:n, :14] = float(rank + 1)
+        mask = torch.zeros(6, dtype=torch.bool)
+        mask[rank] = True                              # rank 0 sees cluster 0, rank 1 cluster 1
+        mask[4] = True
+        vp.zero1_step(scene, gb, mask, state, {})
+        vp.sync_optimizer_state(state)
+        out[rank] = dict(data=scene.data.clone(), m=state.m_rows.clone(), step=state.step.clone())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_zero1_shards_gloo():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_zero1_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    a, b = out[0], out[1]
+    assert torch.equal(a["data"], b["data"]) and torch.equal(a["m"], b["m"]) and torch.equal(a["step"], b["step"])
+    rows_upd = torch.zeros(700, dtype=torch.bool)
+    for c in (0, 1, 4):                               # OR of the masks
+        rows_upd[c * 128:(c + 1) * 128] = True
+    assert torch.equal(a["step"], rows_upd.to(torch.int32))
+    assert (a["data"][rows_upd, :14] == -0.5).all() and (a["data"][~rows_upd] == 0).all()
+    assert (a["m"][rows_upd, :14] == 3.0).all()      # summed gradients (1 + 2)
+    assert (a["data"][:, 14:] == 0).all()
