@@ -95,14 +95,29 @@ int sb_permute_rows(const uint32_t* perm, int64_t n, int count, const void* cons
  * are zeroed alongside the records, so that call can take n_cap = 0.
  * raster_rows (nullable, N rows of sb_raster_row_bytes()): the raster row
  * of every compact slot, which sb_raster_fwd / sb_raster_bwd stage with TMA
- * bulk copies.
+ * bulk copies.  aabb (nullable, K x 6 float64: min xyz, max xyz) and
+ * cull_mask (nullable, K bytes): each cluster's AABB (build_clusters,
+ * ccc.py:112-131) and pure frustum test (cull_clusters, ccc.py:134-146). 
  * Replaces project_scene + build_clusters + cull_clusters +
  * cluster_visibility + compact_arrays (projection.py:130, ccc.py:112/134/149/171). */
 size_t sb_project_workspace_bytes(int64_t n);
 int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
                             void* recs, int32_t* compact_map, int32_t* cluster_offset, uint8_t* cluster_vis,
-                            int32_t* counters, sb_screen_grad* sgrad_zero, void* raster_rows, void* ws,
-                            size_t ws_bytes, sb_stream_t stream);
+                            int32_t* counters, sb_screen_grad* sgrad_zero, void* raster_rows, double* aabb,
+                            uint8_t* cull_mask, void* ws, size_t ws_bytes, sb_stream_t stream);
+
+/* ccc.py:112-131 (build_clusters), standalone: aabb[K x 6] (float64 min xyz,
+ * max xyz) of p -+ 3 max(exp(log_scale)) over K = ceil(n / cluster_size)
+ * blocks of consecutive parameter rows. */
+int sb_build_clusters(const float* params, int64_t n, int32_t cluster_size, double* aabb, sb_stream_t stream);
+
+/* ccc.py:134-146 (cull_clusters) and 149-164 (cluster_visibility) on given
+ * AABBs: cull_mask[k] = the p-vertex frustum test (planes: 24 HOST doubles,
+ * the Frustum's (6, 4) rows); vis_mask[k] = cull_mask[k] | any(in_image of
+ * cluster k's members) when in_image (device, n bytes) is given, else the
+ * cull mask.  Either output may be NULL. */
+int sb_cull_clusters(const double* aabb, int64_t n_clusters, int32_t cluster_size, int64_t n, const double* planes,
+                     const uint8_t* in_image, uint8_t* cull_mask, uint8_t* vis_mask, sb_stream_t stream);
 
 /* tiles.py:50-107 binning, part 1: enumerate the exact disc/rect hits
  * (tiles.py:75-91), count them per tile and scan the counts ->

@@ -33,7 +33,9 @@ SIGNATURES = {
     "sb_radix_sort_pairs_u64": ([VP, VP, VP, VP, I64, C.c_int, VP, VP, SZ, VP], C.c_int),
     "sb_permute_rows": ([VP, I64, C.c_int, VP, VP, VP, VP], C.c_int),
     "sb_project_workspace_bytes": ([I64], SZ),
-    "sb_project_cull_compact": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_project_cull_compact": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_build_clusters": ([VP, I64, I32, VP, VP], C.c_int),
+    "sb_cull_clusters": ([VP, I64, I32, I64, VP, VP, VP, VP, VP], C.c_int),
     "sb_bin_state_workspace_bytes": ([I64, I32], SZ),
     "sb_bin_prepare": ([VP, VP, I64, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_host_mapped_pointer": ([VP, C.POINTER(C.c_void_p)], C.c_int),
@@ -122,7 +124,7 @@ def ptr(t: torch.Tensor | None):
 KERNELS_PER_CALL = {
     "sb_morton_keys": 3, "sb_morton_encode": 1, "sb_permute_rows": 1, "sb_project_cull_compact": 1, "sb_bin_prepare": 3,
     "sb_bin_finish": 2, "sb_raster_fwd": 1, "sb_raster_bwd": 1, "sb_radix_sort_pairs_u64": 10,
-    "sb_chain_projection_bwd": 1, "sb_adam_sparse": 1, "sb_variance_score": 1, "sb_lane_reduce": 1,
+    "sb_chain_projection_bwd": 1, "sb_adam_sparse": 1, "sb_build_clusters": 1, "sb_cull_clusters": 1, "sb_variance_score": 1, "sb_lane_reduce": 1,
     "sb_loss_fwd_bwd": 1,
 }
 launch_count = {"n": 0}

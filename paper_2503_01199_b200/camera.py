@@ -61,7 +61,7 @@ class CameraView:
         return (W + 15) // 16, (H + 7) // 8
 
     def frustum_planes(self) -> np.ndarray:
-        return build_frustum(self)
+        return frustum_planes(self)
 
     def struct(self) -> SbCamera:
         s = SbCamera()
@@ -69,14 +69,34 @@ class CameraView:
         s.fx, s.fy = float(self.focal[0]), float(self.focal[1])
         s.cx, s.cy = float(self.principal_point[0]), float(self.principal_point[1])
         s.near_plane, s.far_plane = self.near, self.far
-        s.planes[:] = [float(v) for v in build_frustum(self).reshape(24)]
+        s.planes[:] = [float(v) for v in frustum_planes(self).reshape(24)]
         s.width, s.height = self.resolution
         return s
 
 
-def build_frustum(camera) -> np.ndarray:
-    """(6, 4) inward unit planes n.x + d >= 0: near, far, left (u >= 0),
-    right (u <= W-1), top (v >= 0), bottom (v <= H-1)."""
+@dataclass
+class Frustum:
+    """projection.py:24-35: six inward-facing unit planes (n, d), a point x
+    is inside iff n.x + d >= 0 for all six."""
+    planes: np.ndarray  # (6, 4) float64
+
+    def signed_distances(self, points) -> np.ndarray:
+        points = np.atleast_2d(np.asarray(points, dtype=np.float64))
+        return points @ self.planes[:, :3].T + self.planes[:, 3]
+
+    def contains(self, points) -> np.ndarray:
+        return np.all(self.signed_distances(points) >= 0.0, axis=-1)
+
+
+def build_frustum(camera) -> Frustum:
+    """projection.py:38-65: (6, 4) inward unit planes n.x + d >= 0: near,
+    far, left (u >= 0), right (u <= W-1), top (v >= 0), bottom (v <= H-1)."""
+    return Frustum(frustum_planes(camera))
+
+
+def frustum_planes(camera) -> np.ndarray:
+    """The planes of build_frustum as a (6, 4) float64 array (same float64
+    expressions and order as the reference)."""
     R = np.asarray(camera.world_to_camera, dtype=np.float64)[:3, :3]
     t = np.asarray(camera.world_to_camera, dtype=np.float64)[:3, 3]
     centre = -R.T @ t

@@ -1,8 +1,14 @@
 """Cluster-Cull-Compact host API: Morton keys / sort on the device.
 
-Reference: pkg/src/tinysplat/ccc.py.  Culling and compaction themselves run
-fused inside the forward (sb_project_cull_compact); this module exposes the
-Morton re-sort (ccc.py:59-90) and the small index helpers.
+Reference: pkg/src/tinysplat/ccc.py.  Culling and compaction run fused
+inside the forward (sb_project_cull_compact); this module exposes the Morton
+re-sort (ccc.py:59-90) and the reference's cluster-index API as separate
+device calls:
+
+  build_clusters      -> sb_build_clusters (float64 AABB per 128-row block)
+  cull_clusters       -> sb_cull_clusters (p-vertex frustum test)
+  cluster_visibility  -> sb_cull_clusters with the in_image widening
+  compact_arrays      -> device gather of the visible clusters' rows
 
   morton_encode  -> sb_morton_encode (caller positions and bounds, float64
                     quantise + bit interleave); morton_encode_scene ->
@@ -17,8 +23,12 @@ import ctypes as C
 
 import torch
 
+from dataclasses import dataclass
+
+import numpy as np
+
 from . import _lib
-from .errors import ValidationError
+from .errors import ShapeMismatchError, ValidationError
 from .scene import SceneSoA
 
 CLUSTER_SIZE = 128
@@ -126,3 +136,100 @@ def scatter_grads(compact_grads: torch.Tensor, compact_map: torch.Tensor, n: int
     if idx.numel():
         mask[idx // cluster_size] = True
     return out, mask
+
+
+# ---- cluster index (ccc.py:97-194) ------------------------------------------
+@dataclass
+class ClusterIndex:
+    """ccc.py:97-109: per-cluster float64 AABBs (device tensors)."""
+    cluster_size: int
+    aabb_min: torch.Tensor   # (K, 3) float64
+    aabb_max: torch.Tensor   # (K, 3) float64
+    n: int
+
+    @property
+    def n_clusters(self) -> int:
+        return int(self.aabb_min.shape[0])
+
+    def member_slice(self, k: int) -> slice:
+        return slice(k * self.cluster_size, min((k + 1) * self.cluster_size, self.n))
+
+
+def build_clusters(scene: SceneSoA, cluster_size: int = CLUSTER_SIZE) -> ClusterIndex:
+    """ccc.py:112-131: AABBs of p -+ 3 max(exp(log_scale)) over consecutive
+    blocks of the (Morton-sorted) scene, on the device (sb_build_clusters)."""
+    _lib.require_cuda(scene.data)
+    n = scene.n
+    k = cluster_count(n, cluster_size)
+    aabb = torch.empty((max(k, 1), 6), dtype=torch.float64, device=scene.device)
+    if n:
+        _lib.call("sb_build_clusters", _lib.ptr(scene.data), n, int(cluster_size), _lib.ptr(aabb),
+                  C.c_void_p(_lib.stream_ptr(scene.device)))
+    return ClusterIndex(cluster_size=int(cluster_size), aabb_min=aabb[:k, :3], aabb_max=aabb[:k, 3:], n=n)
+
+
+def _planes(frustum) -> C.Array:
+    planes = np.asarray(getattr(frustum, "planes", frustum), dtype=np.float64).reshape(-1)
+    if planes.size != 24:
+        raise ShapeMismatchError(f"frustum planes must be (6, 4), got {planes.size} values")
+    return (C.c_double * 24)(*[float(v) for v in planes])
+
+
+def _cull(index: ClusterIndex, frustum, in_image=None):
+    k = index.n_clusters
+    dev = index.aabb_min.device
+    aabb = torch.cat([index.aabb_min, index.aabb_max], dim=1).to(torch.float64).contiguous()
+    out = torch.zeros(max(k, 1), dtype=torch.uint8, device=dev)
+    ii = None
+    if in_image is not None:
+        ii = torch.as_tensor(in_image, device=dev)
+        if ii.numel() != index.n:
+            raise ShapeMismatchError(f"in_image length {ii.numel()} != {index.n}")
+        ii = ii.to(torch.uint8).contiguous()
+    if k:
+        _lib.call("sb_cull_clusters", _lib.ptr(aabb), k, index.cluster_size, index.n, _planes(frustum), _lib.ptr(ii),
+                  None if ii is not None else _lib.ptr(out), _lib.ptr(out) if ii is not None else None,
+                  C.c_void_p(_lib.stream_ptr(dev)))
+    return out[:k].bool()
+
+
+def cull_clusters(index: ClusterIndex, frustum) -> torch.Tensor:
+    """ccc.py:134-146: (K,) bool -- a cluster survives unless its AABB lies
+    entirely behind some frustum plane (p-vertex test, the reference's einsum
+    order)."""
+    return _cull(index, frustum)
+
+
+def cluster_visibility(index: ClusterIndex, frustum, in_image) -> torch.Tensor:
+    """ccc.py:149-164: cull_clusters widened by any member with in_image
+    (culling is then exactly invisible in the render)."""
+    return _cull(index, frustum, in_image)
+
+
+def compact_arrays(struct_or_dict, cluster_mask, cluster_size: int, n: int):
+    """ccc.py:171-194: the visible clusters' rows of every length-n array
+    (dict values or ndarray / tensor attributes), gathered on the device;
+    returns (compacted, compact_map int64)."""
+    mask = torch.as_tensor(cluster_mask)
+    dev = mask.device if mask.is_cuda else torch.device("cuda")
+    mask = mask.to(dev).bool()
+    k = mask.numel()
+    starts = torch.arange(k, device=dev, dtype=torch.int64) * cluster_size
+    ends = torch.clamp(starts + cluster_size, max=n)
+    keep = mask & (ends > starts)
+    rows = torch.arange(k * cluster_size, device=dev, dtype=torch.int64)
+    member = rows < n
+    cmap = rows[keep.repeat_interleave(cluster_size) & member]
+
+    def gather(v):
+        t = torch.as_tensor(v, device=dev) if not torch.is_tensor(v) else v.to(dev)
+        return t.index_select(0, cmap).contiguous()
+
+    if isinstance(struct_or_dict, dict):
+        return {kk: gather(v) for kk, v in struct_or_dict.items()}, cmap
+    import copy as _copy
+    out = _copy.copy(struct_or_dict)
+    for name, value in vars(struct_or_dict).items():
+        if (isinstance(value, (np.ndarray, torch.Tensor)) and value.ndim >= 1 and len(value) == n):
+            setattr(out, name, gather(value))
+    return out, cmap

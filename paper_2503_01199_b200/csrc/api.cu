@@ -7,7 +7,11 @@
 
 // launchers (one per kernel family)
 void sb_launch_project_cull_compact(const float*, int, const CamDev&, int, RasterRec*, int32_t*, int32_t*, uint8_t*,
-                                    int32_t*, void*, void*, unsigned long long*, unsigned int*, cudaStream_t);
+                                    int32_t*, void*, void*, double*, uint8_t*, unsigned long long*, unsigned int*,
+                                    cudaStream_t);
+void sb_launch_cluster_aabb(const float*, int, int, double*, cudaStream_t);
+void sb_launch_cluster_cull(const double*, int, int, int, const double*, const uint8_t*, uint8_t*, uint8_t*,
+                            cudaStream_t);
 int sb_project_status_words(int n);
 size_t sb_bin_state_bytes(int n_cap, int ntiles);
 void sb_launch_bin_prepare(const RasterRec*, const int32_t*, int, const CamDev&, int32_t*, int32_t*, int32_t*,
@@ -150,8 +154,8 @@ size_t sb_project_workspace_bytes(int64_t n) {
 
 int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
                             void* recs, int32_t* compact_map, int32_t* cluster_offset, uint8_t* cluster_vis,
-                            int32_t* counters, sb_screen_grad* sgrad_zero, void* raster_rows, void* ws,
-                            size_t ws_bytes, sb_stream_t stream) {
+                            int32_t* counters, sb_screen_grad* sgrad_zero, void* raster_rows, double* aabb,
+                            uint8_t* cull_mask, void* ws, size_t ws_bytes, sb_stream_t stream) {
     if (int r = check_cam(cam)) return r;
     if (!cfg) return fail(SB_EINVAL, "raster config is NULL");
     if (n < 0 || n > INT32_MAX - 256) return fail(SB_EINVAL, "n out of range");
@@ -167,9 +171,28 @@ int sb_project_cull_compact(const float* params, int64_t n, const sb_camera* cam
     unsigned int* ticket = reinterpret_cast<unsigned int*>(status + blocks);
     const CamDev d = make_cam(cam, cfg);
     sb_launch_project_cull_compact(params, (int)n, d, cfg->use_culling, static_cast<RasterRec*>(recs), compact_map,
-                                   cluster_offset, cluster_vis, counters, sgrad_zero, raster_rows, status, ticket,
-                                   S(stream));
+                                   cluster_offset, cluster_vis, counters, sgrad_zero, raster_rows, aabb, cull_mask,
+                                   status, ticket, S(stream));
     return check_launch("sb_project_cull_compact");
+}
+
+int sb_build_clusters(const float* params, int64_t n, int32_t cluster_size, double* aabb, sb_stream_t stream) {
+    if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
+    if (cluster_size <= 0 || cluster_size > (1 << 20)) return fail(SB_EINVAL, "cluster_size out of range");
+    if (n > 0 && !aabb) return fail(SB_EINVAL, "aabb is NULL");
+    sb_launch_cluster_aabb(params, (int)n, cluster_size, aabb, S(stream));
+    return check_launch("sb_build_clusters");
+}
+
+int sb_cull_clusters(const double* aabb, int64_t n_clusters, int32_t cluster_size, int64_t n, const double* planes,
+                     const uint8_t* in_image, uint8_t* cull_mask, uint8_t* vis_mask, sb_stream_t stream) {
+    if (n_clusters < 0 || n_clusters > INT32_MAX || n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "size out of range");
+    if (cluster_size <= 0) return fail(SB_EINVAL, "cluster_size out of range");
+    if (!planes) return fail(SB_EINVAL, "planes is NULL (24 host doubles)");
+    if (in_image && (int64_t)cluster_size * n_clusters < n) return fail(SB_EINVAL, "clusters do not cover n rows");
+    sb_launch_cluster_cull(aabb, (int)n_clusters, cluster_size, (int)n, planes, in_image, cull_mask, vis_mask,
+                           S(stream));
+    return check_launch("sb_cull_clusters");
 }
 
 size_t sb_bin_state_workspace_bytes(int64_t n_cap, int32_t ntiles) {

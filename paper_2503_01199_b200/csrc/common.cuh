@@ -527,4 +527,32 @@ SB_INLINE uint32_t sb_lookback_warp(unsigned long long* status, int bid, uint32_
     return excl;
 }
 
+// ccc.py:134-146 (cull_clusters): a cluster survives unless the corner of
+// its AABB farthest along some plane normal lies behind that plane; the
+// distance in the reference's einsum order (c0 n0 + c2 n2) + c1 n1, then + d.
+SB_INLINE bool sb_aabb_in_frustum(const double lo[3], const double hi[3], const double* planes) {
+    bool inside = true;
+    for (int pl = 0; pl < 6; pl++) {
+        const double* P = planes + 4 * pl;
+        const double c0 = P[0] >= 0.0 ? hi[0] : lo[0];
+        const double c1 = P[1] >= 0.0 ? hi[1] : lo[1];
+        const double c2 = P[2] >= 0.0 ? hi[2] : lo[2];
+        const double dist = DADD(DADD(DADD(DMUL(c0, P[0]), DMUL(c2, P[2])), DMUL(c1, P[1])), P[3]);
+        inside = inside && (dist >= 0.0);
+    }
+    return inside;
+}
+
+// ccc.py:125-130: one member's contribution to its cluster's AABB,
+// p -+ 3 * max(exp(log_scale)) in float64 (scene.scales() is float64)
+SB_INLINE void sb_member_reach(const float* p, double lo[3], double hi[3]) {
+    const double m = fmax(fmax(exp((double)p[SB_COL_LS]), exp((double)p[SB_COL_LS + 1])),
+                          exp((double)p[SB_COL_LS + 2]));
+    const double reach = DMUL(3.0, m);
+    for (int k = 0; k < 3; k++) {
+        lo[k] = fmin(lo[k], DSUB((double)p[k], reach));
+        hi[k] = fmax(hi[k], DADD((double)p[k], reach));
+    }
+}
+
 SB_INLINE unsigned lane_id() { return threadIdx.x & 31; }

@@ -38,7 +38,8 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
                             int use_culling, RasterRec* __restrict__ rec_out, int32_t* __restrict__ compact_map,
                             int32_t* __restrict__ cluster_offset, uint8_t* __restrict__ cluster_vis,
                             int32_t* __restrict__ counters, float4* __restrict__ sgrad_zero,
-                            RasterRow* __restrict__ rows_out,
+                            RasterRow* __restrict__ rows_out, double* __restrict__ aabb_out,
+                            uint8_t* __restrict__ cull_out,
                             unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket)
 {
     sb_pdl_begin();
@@ -95,21 +96,23 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
         // cluster visibility (p-vertex test, einsum order (c0 n0 + c2 n2) + c1 n1)
         bool vis = true;
         const bool any_ii = __any_sync(0xffffffffu, any_in);
-        if (use_culling) {
+        if (use_culling || aabb_out || cull_out) {
             for (int k = 0; k < 3; k++) {
                 lo[k] = warp_min_d(lo[k]);
                 hi[k] = warp_max_d(hi[k]);
             }
-            bool inside = true;
-            for (int pl = 0; pl < 6; pl++) {
-                const double* P = cam.planes + 4 * pl;
-                double c0 = P[0] >= 0.0 ? hi[0] : lo[0];
-                double c1 = P[1] >= 0.0 ? hi[1] : lo[1];
-                double c2 = P[2] >= 0.0 ? hi[2] : lo[2];
-                double dist = DADD(DADD(DADD(DMUL(c0, P[0]), DMUL(c2, P[2])), DMUL(c1, P[1])), P[3]);
-                inside = inside && (dist >= 0.0);
+            const bool inside = sb_aabb_in_frustum(lo, hi, cam.planes);
+            if (use_culling) vis = inside || any_ii;
+            // optional outputs: the cluster's AABB (build_clusters, ccc.py:112-131)
+            // and the pure frustum test (cull_clusters, ccc.py:134-146)
+            if (lane == 0) {
+                if (aabb_out)
+                    for (int k = 0; k < 3; k++) {
+                        aabb_out[6 * cl + k] = lo[k];
+                        aabb_out[6 * cl + 3 + k] = hi[k];
+                    }
+                if (cull_out) cull_out[cl] = inside ? 1 : 0;
             }
-            vis = inside || any_ii;
         }
         const int nd = __reduce_add_sync(0xffffffffu, ndeg);
         if (lane == 0 && nd) atomicAdd(ticket + 2, (unsigned)nd);
@@ -179,7 +182,8 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
 void sb_launch_project_cull_compact(const float* params, int n, const CamDev& cam, int use_culling,
                                     RasterRec* rec_out, int32_t* compact_map, int32_t* cluster_offset,
                                     uint8_t* cluster_vis, int32_t* counters, void* sgrad_zero, void* rows_out,
-                                    unsigned long long* status, unsigned int* ticket, cudaStream_t stream)
+                                    double* aabb_out, uint8_t* cull_out, unsigned long long* status,
+                                    unsigned int* ticket, cudaStream_t stream)
 {
     const int k = (n + SB_CLUSTER_SIZE - 1) / SB_CLUSTER_SIZE;
     if (k == 0) return;
@@ -189,8 +193,91 @@ void sb_launch_project_cull_compact(const float* params, int n, const CamDev& ca
     const int blocks = min(resident, (k + kWarps - 1) / kWarps);
     sb_launch(project_cull_compact_kernel, blocks, kThreads, smem, stream, reinterpret_cast<const float4*>(params), n,
               k, cam, use_culling, rec_out, compact_map, cluster_offset, cluster_vis, counters,
-              static_cast<float4*>(sgrad_zero), static_cast<RasterRow*>(rows_out), status, ticket);
+              static_cast<float4*>(sgrad_zero), static_cast<RasterRow*>(rows_out), aabb_out, cull_out, status,
+              ticket);
 }
 
 // look-back status words (one per cluster) before the ticket words
 int sb_project_status_words(int n) { return (n + SB_CLUSTER_SIZE - 1) / SB_CLUSTER_SIZE; }
+
+// ---- standalone cluster index (the reference's build_clusters /
+// cull_clusters / cluster_visibility as separate calls; the forward fuses
+// them into the kernel above) ----------------------------------------------
+namespace {
+struct Planes {
+    double p[24];
+};
+
+// ccc.py:112-131: one warp per cluster of `cs` consecutive rows
+__global__ void cluster_aabb_kernel(const float4* __restrict__ params, int n, int k, int cs,
+                                    double* __restrict__ aabb)
+{
+    sb_pdl_begin();
+    const int lane = threadIdx.x & 31;
+    for (int cl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; cl < k;
+         cl += (gridDim.x * blockDim.x) >> 5) {
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        const int g0 = cl * cs, g1 = min(g0 + cs, n);
+        for (int g = g0 + lane; g < g1; g += 32) {
+            float p[16];
+            const float4* row = params + (size_t)g * 4;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const float4 v = __ldg(row + q);
+                p[4 * q] = v.x; p[4 * q + 1] = v.y; p[4 * q + 2] = v.z; p[4 * q + 3] = v.w;
+            }
+            sb_member_reach(p, lo, hi);
+        }
+        for (int q = 0; q < 3; q++) {
+            lo[q] = warp_min_d(lo[q]);
+            hi[q] = warp_max_d(hi[q]);
+        }
+        if (lane == 0)
+            for (int q = 0; q < 3; q++) {
+                aabb[6 * cl + q] = lo[q];
+                aabb[6 * cl + 3 + q] = hi[q];
+            }
+    }
+}
+
+// ccc.py:134-164: pure frustum test of given AABBs, widened by any member's
+// in_image flag (cluster_visibility) when in_image is given
+__global__ void cluster_cull_kernel(const double* __restrict__ aabb, int k, int cs, int n, Planes pl,
+                                    const uint8_t* __restrict__ in_image, uint8_t* __restrict__ cull,
+                                    uint8_t* __restrict__ vis)
+{
+    sb_pdl_begin();
+    const int cl = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cl >= k) return;
+    double lo[3], hi[3];
+    for (int q = 0; q < 3; q++) {
+        lo[q] = aabb[6 * cl + q];
+        hi[q] = aabb[6 * cl + 3 + q];
+    }
+    const bool inside = sb_aabb_in_frustum(lo, hi, pl.p);
+    if (cull) cull[cl] = inside ? 1 : 0;
+    if (vis) {
+        bool v = inside;
+        if (in_image)
+            for (int g = cl * cs, g1 = min(cl * cs + cs, n); g < g1 && !v; g++) v = in_image[g] != 0;
+        vis[cl] = v ? 1 : 0;
+    }
+}
+}  // namespace
+
+void sb_launch_cluster_aabb(const float* params, int n, int cs, double* aabb, cudaStream_t stream)
+{
+    const int k = (n + cs - 1) / cs;
+    if (k <= 0) return;
+    const int blocks = min((k + 7) / 8, sb_sm_count() * 8);
+    sb_launch(cluster_aabb_kernel, blocks, 256, 0, stream, reinterpret_cast<const float4*>(params), n, k, cs, aabb);
+}
+
+void sb_launch_cluster_cull(const double* aabb, int k, int cs, int n, const double* planes, const uint8_t* in_image,
+                            uint8_t* cull, uint8_t* vis, cudaStream_t stream)
+{
+    if (k <= 0) return;
+    Planes pl;
+    for (int i = 0; i < 24; i++) pl.p[i] = planes[i];
+    sb_launch(cluster_cull_kernel, (k + 255) / 256, 256, 0, stream, aabb, k, cs, n, pl, in_image, cull, vis);
+}

@@ -113,6 +113,8 @@ class RenderContext:
     half: bool | str = False      # produced by a 16-bit blending-state path
     token: int = 0                # owner token of the pre-zeroed sgrad workspace (0: none)
     tile_buffer: torch.Tensor | None = field(default=None, repr=False)   # offsets + raster schedule (2T + 1)
+    cluster_cull: torch.Tensor | None = field(default=None, repr=False)  # (K,) uint8 pure frustum test
+    cluster_aabb: torch.Tensor | None = field(default=None, repr=False)  # (K, 6) float64 min xyz, max xyz
     _tiles: list | None = field(default=None, repr=False)
 
     @property
@@ -204,6 +206,8 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     cmap = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     coff = torch.empty(max(K, 1), dtype=torch.int32, device=dev)
     cvis = torch.empty(max(K, 1), dtype=torch.uint8, device=dev)   # written for every cluster
+    ccull = torch.empty(max(K, 1), dtype=torch.uint8, device=dev)  # pure frustum test (cull_clusters)
+    caabb = torch.empty((max(K, 1), 6), dtype=torch.float64, device=dev)   # build_clusters AABBs
     counters = torch.empty(8, dtype=torch.int32, device=dev)   # vis, N_c, ndeg, 0 (project); P, E (bin)
     lib = _lib.load()
     # offsets (T + 1) followed by the heavy-first raster schedule (T)
@@ -214,7 +218,8 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     _sgrad_clean.pop(str(dev), None)
     _lib.call("sb_project_cull_compact", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s), _lib.ptr(recs),
               _lib.ptr(cmap), _lib.ptr(coff), _lib.ptr(cvis), _lib.ptr(counters),
-              _lib.ptr(sgrad) if sgrad is not None else None, _lib.ptr(rows), _lib.ptr(ws), ws.numel(), stream)
+              _lib.ptr(sgrad) if sgrad is not None else None, _lib.ptr(rows), _lib.ptr(caabb), _lib.ptr(ccull),
+              _lib.ptr(ws), ws.numel(), stream)
     # one zero-initialised state per tile grid (its count arrays stay zeroed)
     state = _lib.workspace(f"bin_state_{tx_n}x{ty_n}", lib.sb_bin_state_workspace_bytes(n, ntiles), dev)
     host, mirror = _pinned_counters(dev)
@@ -260,7 +265,7 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
                         n_compact=nc, n_pairs=P, visible_clusters=vis, culled_clusters=K - vis, recs=recs, rows=rows,
                         compact_map_full=cmap, cluster_offset=coff[:K], cluster_vis=cvis[:K],
                         tile_offsets=tile_offsets, tile_prims=prims[:P], transmittance=T, last=last,
-                        tile_buffer=tile_buf,
+                        tile_buffer=tile_buf, cluster_cull=ccull[:K], cluster_aabb=caabb[:K],
                         n_degenerate=ndeg, half=half)
     if sgrad is not None:
         ctx.token = next(_ctx_tokens)
@@ -286,3 +291,98 @@ def render(scene: SceneSoA, camera, config: RasterConfig | None = None) -> Rende
     """forward.py:307-308 (no backward follows: the sgrad rows are left alone)."""
     return _launch_forward(scene, CameraView.from_any(camera), config or RasterConfig(), False,
                            zero_sgrad=False)[0]
+
+
+# ---- single-tile blending (forward.py:161-230) -------------------------------
+def _lane_pixels(origin, resolution):
+    """forward.py:117-127: lane l -> pixel x0 + l % 16, rows y0 + 4 (l // 16) + i."""
+    x0, y0 = origin
+    W, H = resolution
+    lane = np.arange(LANES)
+    px = x0 + lane % TILE_W
+    py = y0 + 4 * (lane // TILE_W)[:, None] + np.arange(PIXELS_PER_LANE)[None, :]
+    valid = (px[:, None] < W) & (py < H)
+    return px, py, valid
+
+
+def _records_from_projected(projected) -> torch.Tensor:
+    """Pack projected arrays (ProjectedScene or a ctx.projected dict) into
+    the device's 48-byte compact records."""
+    get = (lambda k: projected[k]) if isinstance(projected, dict) else (lambda k: getattr(projected, k))
+    xy = torch.as_tensor(get("xy"))
+    dev = xy.device if xy.is_cuda else torch.device("cuda")
+    f = lambda k: torch.as_tensor(get(k), device=dev).to(torch.float32)  # noqa: E731
+    xy, conic, color = f("xy").reshape(-1, 2), f("conic").reshape(-1, 3), f("color").reshape(-1, 3)
+    n = xy.shape[0]
+    flags = (torch.as_tensor(get("valid"), device=dev).to(torch.int32)
+             | (torch.as_tensor(get("in_image"), device=dev).to(torch.int32) << 1))
+    recs = torch.empty((max(n, 1), REC_FLOATS), dtype=torch.float32, device=dev)
+    recs[:n, 0:2] = xy
+    recs[:n, 2:5] = conic
+    recs[:n, 5] = f("opacity").reshape(-1)
+    recs[:n, 6:9] = color
+    recs[:n, 9] = f("depth").reshape(-1)
+    recs[:n, 10] = f("radius").reshape(-1)
+    recs[:n, 11] = flags.view(torch.float32)
+    return recs
+
+
+def _blend_one_tile(tile, projected, config, resolution, half):
+    config = config or RasterConfig()
+    W, H = int(resolution[0]), int(resolution[1])
+    tx_n, ty_n = (W + TILE_W - 1) // TILE_W, (H + TILE_H - 1) // TILE_H
+    ntiles = tx_n * ty_n
+    t = int(tile.tile_y) * tx_n + int(tile.tile_x)
+    recs = _records_from_projected(projected)
+    dev = recs.device
+    prims = torch.as_tensor(np.asarray(tile.primitives), device=dev).to(torch.int32).reshape(-1)
+    P = prims.numel()
+    offs = torch.zeros(2 * ntiles + 1, dtype=torch.int32, device=dev)
+    offs[t + 1:ntiles + 1] = P
+    sched = torch.arange(ntiles, dtype=torch.int32, device=dev)
+    sched[0], sched[t] = t, 0                  # the one non-empty tile first
+    offs[ntiles + 1:] = sched
+    color = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+    T = torch.empty((H, W), dtype=torch.float32, device=dev)
+    frags = torch.empty((H, W), dtype=torch.int32, device=dev)
+    last = torch.empty((H, W), dtype=torch.int32, device=dev)
+    cam = CameraView(np.eye(4), (1.0, 1.0), (0.0, 0.0), (W, H), 0.05, 20.0)
+    cam_s, cfg_s = cam.struct(), config.struct(half)
+    ws = _lib.workspace("raster_fwd", _lib.load().sb_raster_workspace_bytes(), dev)
+    _lib.call("sb_raster_fwd", _lib.ptr(recs), None, _lib.ptr(offs), _lib.ptr(prims if P else offs), C.byref(cam_s),
+              C.byref(cfg_s), _lib.ptr(color), _lib.ptr(T), _lib.ptr(frags), _lib.ptr(last), _lib.ptr(ws),
+              ws.numel(), C.c_void_p(_lib.stream_ptr(dev)))
+    px, py, valid = _lane_pixels(tile.origin, (W, H))
+    bg = torch.tensor(config.background, dtype=torch.float32, device=dev)
+    rgb = bg.expand(LANES, PIXELS_PER_LANE, 3).clone()
+    Tl = torch.ones((LANES, PIXELS_PER_LANE), dtype=torch.float32, device=dev)
+    fl = torch.zeros((LANES, PIXELS_PER_LANE), dtype=torch.int32, device=dev)
+    li, ii = np.nonzero(valid)
+    if li.size:
+        ys = torch.as_tensor(py[li, ii], device=dev)
+        xs = torch.as_tensor(px[li], device=dev)
+        lt, it = torch.as_tensor(li, device=dev), torch.as_tensor(ii, device=dev)
+        rgb[lt, it] = color[ys, xs]
+        Tl[lt, it] = T[ys, xs]
+        fl[lt, it] = frags[ys, xs]
+    return rgb, Tl, fl, torch.as_tensor(valid, device=dev)
+
+
+def blend_tile(tile: TileWorkload, projected, config: RasterConfig | None = None, resolution=None, counter=None):
+    """forward.py:161-191: composite ONE tile with the device's warp kernel;
+    returns (rgb (32, 4, 3), T (32, 4), frags (32, 4), valid (32, 4)) in lane
+    layout (lane l -> column l % 16, rows 4 (l // 16) + i).  `projected` holds
+    the arrays `tile.primitives` indexes (ProjectedScene or ctx.projected)."""
+    if counter is not None:
+        raise ValueError("OpCounter instrumentation is CPU-only; profile the device path with ncu")
+    if resolution is None:
+        raise ValueError("resolution is required")
+    return _blend_one_tile(tile, projected, config, resolution, False)
+
+
+def half_path_blend(tile: TileWorkload, projected, config: RasterConfig | None = None, resolution=None):
+    """forward.py:194-230: the same with binary16 blending state (rgb / T
+    returned in float32, as the reference upcasts them)."""
+    if resolution is None:
+        raise ValueError("resolution is required")
+    return _blend_one_tile(tile, projected, config, resolution, True)

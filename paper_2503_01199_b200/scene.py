@@ -29,6 +29,35 @@ CHANNEL_COLS = {"position": (0, 3), "log_scale": (3, 6), "rotation": (6, 10), "c
 ROW = 16
 
 
+def _sigmoid64(x: torch.Tensor) -> torch.Tensor:
+    """scene.py:31-38: 1 / (1 + exp(-x)) for x >= 0, exp(x) / (1 + exp(x))
+    otherwise -- both are exp(-|x|) and one division (float64)."""
+    e = torch.exp(-x.abs())
+    return torch.where(x >= 0, 1.0 / (1.0 + e), e / (1.0 + e))
+
+
+def activate(position, log_scale, rotation, color, opacity_logit):
+    """scene.py:103-126: raw channels -> activated (position, scale, unit
+    quaternion, color, opacity) in float64 (torch, on the inputs' device).
+    Raises ValidationError naming the channel / index for non-finite values
+    or zero-norm quaternions."""
+    arrays = {}
+    for name, v in (("position", position), ("log_scale", log_scale), ("rotation", rotation), ("color", color),
+                    ("opacity_logit", opacity_logit)):
+        t = v if torch.is_tensor(v) else torch.as_tensor(np.asarray(v, dtype=np.float64))
+        t = t.to(torch.float64)
+        bad = ~torch.isfinite(t)
+        if bool(bad.any()):
+            raise ValidationError(name, int(torch.nonzero(bad.reshape(t.shape[0], -1).any(1))[0, 0])
+                                  if t.dim() else 0, "non-finite value")
+        arrays[name] = t
+    qn = torch.linalg.vector_norm(arrays["rotation"], dim=-1)
+    if bool((qn == 0).any()):
+        raise ValidationError("rotation", int(torch.nonzero(qn == 0).reshape(-1)[0]), "zero-norm quaternion")
+    return (arrays["position"], torch.exp(arrays["log_scale"]), arrays["rotation"] / qn[..., None],
+            _sigmoid64(arrays["color"]), _sigmoid64(arrays["opacity_logit"]))
+
+
 def pack_rows(position, log_scale, rotation, color, opacity_logit, device=None) -> torch.Tensor:
     """Raw channels (numpy or torch, any float dtype) -> (N, 16) float32 rows."""
     chans = {"position": position, "log_scale": log_scale, "rotation": rotation, "color": color,
