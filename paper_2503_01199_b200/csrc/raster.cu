@@ -326,6 +326,11 @@ raster_fwd_kernel(FwdParams p)
 // in a 16-bit float: IEEE binary16 (__half ops round once per op, like
 // numpy's float16) or, as a variant the reference does not have (SURVEY
 // 8(f) rank 4), bfloat16.
+SB_INLINE __half __low2half_t(__half2 v) { return __low2half(v); }
+SB_INLINE __half __high2half_t(__half2 v) { return __high2half(v); }
+SB_INLINE __nv_bfloat16 __low2half_t(__nv_bfloat162 v) { return __low2bfloat16(v); }
+SB_INLINE __nv_bfloat16 __high2half_t(__nv_bfloat162 v) { return __high2bfloat16(v); }
+
 template <typename T> struct Half16;
 template <> struct Half16<__half> {
     static SB_INLINE __half from(float f) { return __float2half_rn(f); }
@@ -418,6 +423,121 @@ raster_fwd_half_kernel(FwdParams p)
             p.out_T[pix] = O::to(T[i]);
             p.out_frags[pix] = frags[i];
             p.out_last[pix] = last[i];
+        }
+    }
+}
+
+// The same 16-bit blending state with pixel pairs packed in half2 /
+// bfloat162 registers: every op still rounds each element once (HMUL2 /
+// HADD2 / HSUB2 are element-wise IEEE ops, no fusion), so the results are
+// bit-identical to the scalar kernel above; a pixel that does not blend
+// gets alpha 0 (w = T 0 = 0, rgb + 0 = rgb, T (1 - 0) = T exactly).
+template <typename H> struct Half16x2;
+template <> struct Half16x2<__half> {
+    using T2 = __half2;
+    static SB_INLINE T2 pack(float a, float b) { return __floats2half2_rn(a, b); }
+    static SB_INLINE T2 bcast(__half h) { return __half2half2(h); }
+};
+template <> struct Half16x2<__nv_bfloat16> {
+    using T2 = __nv_bfloat162;
+    static SB_INLINE T2 pack(float a, float b) { return __floats2bfloat162_rn(a, b); }
+    static SB_INLINE T2 bcast(__nv_bfloat16 h) { return __bfloat162bfloat162(h); }
+};
+
+template <typename H>
+__global__ void __launch_bounds__(kThreads)
+raster_fwd_half2_kernel(FwdParams p)
+{
+    sb_pdl_begin();
+    using O = Half16<H>;
+    using P = Half16x2<H>;
+    using H2 = typename P::T2;
+    __shared__ SRec slabs[kWarpsPerBlock][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    SRec* slab = slabs[warp];
+    const H2 amin = P::bcast(O::from(p.amin)), amax = P::bcast(O::from(p.amax));
+    const H2 tstop = P::bcast(O::from(p.tstop)), one = P::bcast(O::from(1.0f)), zero = P::bcast(O::from(0.0f));
+    for (int q = next_tile(p.tile_counter, lane, p.ntiles); q < p.ntiles;
+         q = next_tile(p.tile_counter, lane, p.ntiles)) {
+        const int t = p.offsets[p.ntiles + 1 + q];
+        const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
+        const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
+        const float px = (float)pxi, py0 = (float)py0i;
+        H2 vmask[2], T[2], rgb[2][3];
+        int frags[4], last[4];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const bool v0 = pxi < p.W && py0i + 2 * h < p.H, v1 = pxi < p.W && py0i + 2 * h + 1 < p.H;
+            vmask[h] = P::pack(v0 ? 1.0f : 0.0f, v1 ? 1.0f : 0.0f);
+            T[h] = one;
+            rgb[h][0] = rgb[h][1] = rgb[h][2] = zero;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) frags[i] = last[i] = 0;
+        const int beg = p.offsets[t], n = p.offsets[t + 1] - beg;
+        Prefetch pf;
+        if (n > 0) prefetch_chunk(pf, p.recs, p.prims, beg, 0, min(32, n), lane);
+        bool done = false;
+        for (int k0 = 0; k0 < n && !done; k0 += 32) {
+            const int cnt = min(32, n - k0);
+            __syncwarp();
+            commit_chunk<false>(slab, pf, cnt, lane);
+            unsigned todo = chunk_mask(pf, cnt, lane, x0, y0, p.W, p.H, p.amin);
+            __syncwarp();
+            if (k0 + 32 < n) prefetch_chunk(pf, p.recs, p.prims, beg, k0 + 32, min(32, n - k0 - 32), lane);
+            while (todo) {
+                const int j = __ffs(todo) - 1;
+                todo &= todo - 1;
+                // live: some valid pixel with T >= t_stop (the scalar kernel's test)
+                const H2 l0 = __hmul2(vmask[0], __hge2(T[0], tstop)), l1 = __hmul2(vmask[1], __hge2(T[1], tstop));
+                const H2 lv = __hadd2(l0, l1);
+                const bool live = O::to(__low2half_t(lv)) + O::to(__high2half_t(lv)) > 0.0f;
+                if (!__any_sync(0xffffffffu, live)) {
+                    done = true;
+                    break;
+                }
+                const SRec r = slab_get<false>(slab, j);
+                float G[4], dx, dy;
+                lane_G(r, px, py0, G, dx, dy);
+                const H2 o = P::bcast(O::from(r.o));
+                const H2 cr = P::bcast(O::from(r.r)), cg = P::bcast(O::from(r.g)), cb = P::bcast(O::from(r.bl));
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    H2 alpha = __hmin2(__hmul2(o, P::pack(G[2 * h], G[2 * h + 1])), amax);
+                    // blend where valid && T >= t_stop && alpha >= alpha_min
+                    const H2 c2 = __hmul2(__hmul2(vmask[h], __hge2(T[h], tstop)), __hge2(alpha, amin));
+                    const H2 a_eff = __hmul2(alpha, c2);
+                    const H2 w = __hmul2(T[h], a_eff);
+                    rgb[h][0] = __hadd2(rgb[h][0], __hmul2(w, cr));
+                    rgb[h][1] = __hadd2(rgb[h][1], __hmul2(w, cg));
+                    rgb[h][2] = __hadd2(rgb[h][2], __hmul2(w, cb));
+                    T[h] = __hmul2(T[h], __hsub2(one, a_eff));
+                    const bool b0 = O::to(__low2half_t(c2)) != 0.0f, b1 = O::to(__high2half_t(c2)) != 0.0f;
+                    frags[2 * h] += b0;
+                    frags[2 * h + 1] += b1;
+                    last[2 * h] = b0 ? k0 + j + 1 : last[2 * h];
+                    last[2 * h + 1] = b1 ? k0 + j + 1 : last[2 * h + 1];
+                }
+            }
+        }
+        const H2 bg[3] = {P::bcast(O::from(p.bg[0])), P::bcast(O::from(p.bg[1])), P::bcast(O::from(p.bg[2]))};
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            H2 outc[3];
+#pragma unroll
+            for (int ch = 0; ch < 3; ch++) outc[ch] = __hadd2(rgb[h][ch], __hmul2(T[h], bg[ch]));
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const int i = 2 * h + e;
+                if (!(pxi < p.W && py0i + i < p.H)) continue;
+                const size_t pix = (size_t)(py0i + i) * p.W + pxi;
+#pragma unroll
+                for (int ch = 0; ch < 3; ch++)
+                    p.out_color[3 * pix + ch] = O::to(e ? __high2half_t(outc[ch]) : __low2half_t(outc[ch]));
+                p.out_T[pix] = O::to(e ? __high2half_t(T[h]) : __low2half_t(T[h]));
+                p.out_frags[pix] = frags[i];
+                p.out_last[pix] = last[i];
+            }
         }
     }
 }
@@ -1230,8 +1350,14 @@ void sb_launch_raster_fwd(const RasterRec* recs, const RasterRow* rows, const in
     const int want = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const int blocks = min(want, sm_count() * 8);
     if (!blocks) return;
-    if (cfg.half_state == 2) sb_launch(raster_fwd_half_kernel<__nv_bfloat16>, blocks, kThreads, 0, stream, p);
-    else if (cfg.half_state) sb_launch(raster_fwd_half_kernel<__half>, blocks, kThreads, 0, stream, p);
+    // 16-bit blending state: pixel pairs packed (half2 / bfloat162) unless
+    // SB_HALF_SCALAR=1 selects the scalar kernel (bit-identical; A/B)
+    const char* hs = getenv("SB_HALF_SCALAR");
+    const bool scalar16 = hs && hs[0] == '1';
+    if (cfg.half_state == 2 && scalar16) sb_launch(raster_fwd_half_kernel<__nv_bfloat16>, blocks, kThreads, 0, stream, p);
+    else if (cfg.half_state == 2) sb_launch(raster_fwd_half2_kernel<__nv_bfloat16>, blocks, kThreads, 0, stream, p);
+    else if (cfg.half_state && scalar16) sb_launch(raster_fwd_half_kernel<__half>, blocks, kThreads, 0, stream, p);
+    else if (cfg.half_state) sb_launch(raster_fwd_half2_kernel<__half>, blocks, kThreads, 0, stream, p);
     else if (rows && staging_mode() != 0) {
         TmaFwdParams tp;
         tp.f = p;
