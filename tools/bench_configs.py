@@ -97,7 +97,11 @@ def config_A(steps=200):
     lrs = sb.LearningRates().at(0.0, position_scale=3.2)
     for _ in range(5):
         iteration(scene, state, views[0], targets[0], lrs)
-    ms, wall = device_time(lambda: [iteration(scene, state, views[0], targets[0], lrs) for _ in range(steps)])
+    def run():
+        for _ in range(steps):      # (contexts not retained: no allocator growth inside the timed loop)
+            iteration(scene, state, views[0], targets[0], lrs)
+
+    ms, wall = device_time(run)
     stages, ctx = stage_times(scene, state, views, targets, lrs)
     line("A", "10K Gaussians, 128x128, full training iteration", steps / (ms / 1e3), "iters/s", ms,
          {"steps": steps, "wall_ms": wall, "stages_ms": stages, "P_pairs": ctx.n_pairs,
