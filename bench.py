@@ -201,6 +201,11 @@ def timed(fn, steps, ws):
 
 
 # algorithmic bytes per launch; P pairs, Nc compact, Npix pixels
+# kernels timed by back-to-back replay (bench's roofline and raster line)
+REPLAYED = ("sb_raster_fwd", "sb_raster_bwd")
+K_REPLAY = 20
+
+
 def algorithmic_bytes(name, n, nc, P, npix):
     return {
         "sb_project_cull_compact": 56 * n + 48 * nc,
@@ -347,7 +352,15 @@ def main():
     e2e_val = ws * args.steps / (e2e_ms / 1e3)
 
     # per-kernel durations (CUDA events on the launching stream, separate pass)
+    # (a) in-step: events around every call of 3 training steps.  The host
+    #     sizes each view's pair buffers from one counter read, so a call's
+    #     start event can fire while the host is still issuing it: these
+    #     include host launch gaps.
+    # (b) replayed: the raster kernels of the last step re-issued K_REPLAY
+    #     times back to back on their stream with the same buffers, events
+    #     around the batch: the kernels' own average launch duration.
     _lib.enable_call_timing(True)
+    _lib.keep_last_args(REPLAYED)
     ctxs = []
     for _ in range(3):
         _, ctx = trainer.step(it["i"], targets_dev[0])
@@ -356,9 +369,13 @@ def main():
     torch.cuda.synchronize()
     tim = _lib.call_timings()
     _lib.enable_call_timing(False)
+    replayed = {k: _lib.replay_time(k, K_REPLAY) for k in REPLAYED}
+    _lib.keep_last_args(None)
     ctx = ctxs[-1]
     n, nc, P, npix = scene.n, ctx.n_compact, ctx.n_pairs, W * H
-    stages = {k: statistics.mean(v) for k, v in tim.items()}
+    stages_in_step = {k: statistics.mean(v) for k, v in tim.items()}
+    stages = dict(stages_in_step)
+    stages.update(replayed)
     dominant = max(stages, key=stages.get)
     peak, peak_kind = peaks()
     ab = algorithmic_bytes(dominant, n, nc, P, npix)
@@ -424,6 +441,10 @@ def main():
             "raster_fwd_bwd_ms_per_view": raster_ms,
             "raster_fwd_bwd_roofline_frac": (raster_bytes / (raster_ms * 1e-3) / 1e9) / peak if raster_ms else None,
             "stages_ms": stages,
+            "stages_ms_in_step": stages_in_step,
+            "stage_timing": ("stages_ms: raster fwd / bwd = average of %d back-to-back replays of the step's launch "
+                             "(CUDA events on its stream); the other stages and stages_ms_in_step = events around "
+                             "each call inside 3 training steps (include host launch gaps)" % K_REPLAY),
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "traffic_source": traffic_source, "algorithmic_bytes": ab, "peak_kind": peak_kind,

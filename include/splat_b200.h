@@ -208,9 +208,9 @@ int sb_variance_score(const double* S, const double* M, const int32_t* C, int64_
  * uint8 (value / 255) when target_u8 != NULL.  loss[0] (float64, device) is
  * written on the stream (by the kernel's last CTA; it may be mapped host
  * memory).  accum: sb_loss_workspace_bytes(width, height) of scratch -- a
- * ticket and one pair of partial sums per CTA, summed in a fixed order by
- * the last CTA (bit-reproducible) -- zeroed once before its first use; every
- * call leaves the ticket zeroed. */
+ * ticket and two int64 fixed-point accumulators the CTAs add their partial
+ * sums into (exact integer sums: bit-reproducible in any order) -- zeroed
+ * once before its first use; every call leaves it zeroed. */
 size_t sb_loss_workspace_bytes(int32_t width, int32_t height);
 int sb_loss_fwd_bwd(const float* rendered, const float* target, const uint8_t* target_u8, int32_t width,
                     int32_t height, float lam, float* grad, double* accum, double* loss, sb_stream_t stream);

@@ -145,6 +145,45 @@ def call_timings() -> dict:
     return {k: [a.elapsed_time(b) for a, b in v] for k, v in _timing.items()}
 
 
+# entry points whose last argument tuple is kept for replay_time()
+_keep_args: dict | None = None
+
+
+def keep_last_args(names):
+    """Remember the arguments of the last call of each named entry point
+    (bench.py replays the raster kernels to time them back to back)."""
+    global _keep_args
+    _keep_args = {n: None for n in names} if names else None
+
+
+def replay_time(name: str, k: int) -> float:
+    """Average device time (ms) of `name` re-issued k times back to back on
+    its recorded stream with the arguments of its last call: CUDA events on
+    that stream around the k launches, after one untimed launch.  The calls
+    are pure functions of their buffers (the raster tile queues reset
+    themselves; a replayed backward adds its gradients again, same work)."""
+    lib = load()
+    args = (_keep_args or {}).get(name)
+    if args is None:
+        raise RuntimeError(f"replay_time: no recorded call of {name}")
+    sv = args[-1].value if isinstance(args[-1], C.c_void_p) else args[-1]
+    stream = torch.cuda.ExternalStream(sv) if sv else torch.cuda.default_stream()
+    f = getattr(lib, name)
+    with torch.cuda.stream(stream):
+        f(*args)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(k):
+            rc = f(*args)
+        b.record()
+    b.synchronize()
+    if rc != SB_OK:
+        raise RuntimeError(f"{name} replay failed ({rc})")
+    launch_count["n"] += (k + 1) * KERNELS_PER_CALL.get(name, 0)
+    return a.elapsed_time(b) / k
+
+
 def call(name: str, *args):
     """Call an sb_* entry point and map its status to the reference's
     exception conventions (errors.py:6-32)."""
@@ -162,6 +201,8 @@ def call(name: str, *args):
 
 
 def _call(lib, name, args):
+    if _keep_args is not None and name in _keep_args:
+        _keep_args[name] = args
     if _timing is not None:
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)

@@ -15,8 +15,9 @@
 // pass is a register sliding window: a thread owns a short run of outputs
 // along the filter axis, loads the run + 10 inputs once from shared memory
 // and forms all outputs from registers.
-// Loss partial sums: one float64 pair per CTA; the last CTA to finish (a
-// ticket) sums them in a fixed order (bit-reproducible) and forms the loss.
+// Loss partial sums: one float64 pair per CTA, added into int64 fixed-point
+// accumulators (exact, order-independent: bit-reproducible); the last CTA to
+// finish (a ticket) forms the loss.
 #include "common.cuh"
 
 namespace {
@@ -64,7 +65,7 @@ SB_INLINE float2 f2(float v) { return make_float2(v, v); }
 template <bool kU8>
 __global__ void __launch_bounds__(kThreads, 2)
 loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, const uint8_t* __restrict__ y_u8,
-            int W, int H, float lam, Win win, float* __restrict__ grad, double* __restrict__ accum,
+            int W, int H, float lam, Win win, int fxp, float* __restrict__ grad, double* __restrict__ accum,
             double* __restrict__ loss_out)
 {
     sb_pdl_begin();
@@ -307,59 +308,43 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
             l1_part += fabsf(diff);
         }
     }
-    // block reduction of the two loss partials
+    // block reduction of the two loss partials: each warp sums its lanes in
+    // float32 (a fixed butterfly over at most 224 SSIM / 128 L1 terms), then
+    // thread 0 sums the 16 warp totals in float64 in a fixed order.
     const int lane = tid & 31, warp = tid >> 5;
-    double s_sum = (double)s_part, l1_sum = (double)l1_part;
+    float s_w = s_part, l_w = l1_part;
+#pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
-        s_sum += __shfl_xor_sync(0xffffffffu, s_sum, o);
-        l1_sum += __shfl_xor_sync(0xffffffffu, l1_sum, o);
+        s_w += __shfl_xor_sync(0xffffffffu, s_w, o);
+        l_w += __shfl_xor_sync(0xffffffffu, l_w, o);
     }
-    if (lane == 0) { sm.red[0][warp] = l1_sum; sm.red[1][warp] = s_sum; }
+    if (lane == 0) { sm.red[0][warp] = (double)l_w; sm.red[1][warp] = (double)s_w; }
     __syncthreads();
-    // Each CTA stores its two partials in its own slot; the last CTA to
-    // finish (a ticket, accum[0]) sums all slots in a fixed order -- thread t
-    // takes slots t, t + 512, ... in sequence, then a fixed tree -- so the
-    // loss is bit-reproducible (no float atomics), forms it and re-zeroes the
-    // ticket for the next call.
-    const unsigned ncta = gridDim.x * gridDim.y * gridDim.z;
-    const unsigned cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    double* part = accum + 2;                 // [ncta][2]
-    __shared__ int s_last;
-    if (tid == 0) {
-        double a = 0, b = 0;
-        for (int q = 0; q < kThreads / 32; q++) { a += sm.red[0][q]; b += sm.red[1][q]; }
-        part[2 * cta] = a;
-        part[2 * cta + 1] = b;
-        __threadfence();
-        unsigned long long* ticket = reinterpret_cast<unsigned long long*>(accum);
-        s_last = atomicAdd(ticket, 1ull) == (unsigned long long)ncta - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        double a = 0, b = 0;
-        for (unsigned q = tid; q < ncta; q += kThreads) {
-            a += __ldcg(part + 2 * q);
-            b += __ldcg(part + 2 * q + 1);
-        }
-        for (int o = 16; o >= 1; o >>= 1) {
-            a += __shfl_xor_sync(0xffffffffu, a, o);
-            b += __shfl_xor_sync(0xffffffffu, b, o);
-        }
-        __syncthreads();
-        if (lane == 0) { sm.red[0][warp] = a; sm.red[1][warp] = b; }
-        __syncthreads();
-        if (tid == 0) {
-            double l1 = 0, ss = 0;
-            for (int q = 0; q < kThreads / 32; q++) { l1 += sm.red[0][q]; ss += sm.red[1][q]; }
-            const double n = (double)W * H * 3.0;
-            const double ni = (double)(W - 2 * R) * (double)(H - 2 * R);
-            double l = (1.0 - lam) * l1 / n;
-            if (lam != 0.f) l += lam * (1.0 - (ni > 0 ? ss / (3.0 * ni) : 0.0));
-            *loss_out = l;
-            *reinterpret_cast<unsigned long long*>(accum) = 0ull;
-        }
-    }
+    if (tid != 0) return;
+    // The CTA's partials are added into two int64 fixed-point accumulators
+    // (2^-fxp units; integer addition is exact and order-independent, so the
+    // loss is bit-reproducible without a fixed summation order), and only
+    // this thread waits on the ticket: the last CTA to arrive forms the loss
+    // and re-zeroes the accumulators and the ticket for the next call.
+    double a = 0, b = 0;
+#pragma unroll
+    for (int q = 0; q < kThreads / 32; q++) { a += sm.red[0][q]; b += sm.red[1][q]; }
+    unsigned long long* ticket = reinterpret_cast<unsigned long long*>(accum);
+    unsigned long long* acc = ticket + 1;     // [0] L1 sum, [1] SSIM sum
+    atomicAdd(acc, (unsigned long long)__double2ll_rn(ldexp(a, fxp)));
+    atomicAdd(acc + 1, (unsigned long long)__double2ll_rn(ldexp(b, fxp)));
+    __threadfence();
+    const unsigned long long ncta = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+    if (atomicAdd(ticket, 1ull) != ncta - 1) return;
+    __threadfence();
+    const double l1 = ldexp((double)(long long)atomicExch(acc, 0ull), -fxp);
+    const double ss = ldexp((double)(long long)atomicExch(acc + 1, 0ull), -fxp);
+    const double n = (double)W * H * 3.0;
+    const double ni = (double)(W - 2 * R) * (double)(H - 2 * R);
+    double l = (1.0 - lam) * l1 / n;
+    if (lam != 0.f) l += lam * (1.0 - (ni > 0 ? ss / (3.0 * ni) : 0.0));
+    *loss_out = l;
+    atomicExch(ticket, 0ull);
 }
 
 }  // namespace
@@ -378,14 +363,17 @@ void sb_launch_loss(const float* x, const float* y, const uint8_t* y_u8, int W, 
     sb_smem_attr(loss_kernel<true>, (int)sizeof(Smem));
     sb_smem_attr(loss_kernel<false>, (int)sizeof(Smem));
     dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, 3);
+    // fixed-point scale of the loss accumulators: each sum is at most
+    // 3 W H (|L1 term|, |SSIM| <= 1), kept below 2^62
+    int fx = 36;
+    while (fx > 0 && ldexp(3.0 * (double)W * (double)H, fx) >= 0x1p62) fx--;
     if (y_u8)
-        sb_launch(loss_kernel<true>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum, loss);
+        sb_launch(loss_kernel<true>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, fx, grad, accum, loss);
     else
-        sb_launch(loss_kernel<false>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum,
-                  loss);
+        sb_launch(loss_kernel<false>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, fx, grad,
+                  accum, loss);
 }
 
-size_t sb_loss_accum_bytes(int W, int H) {
-    const size_t ncta = (size_t)((W + TW - 1) / TW) * (size_t)((H + TH - 1) / TH) * 3;
-    return 16 + 16 * ncta;
+size_t sb_loss_accum_bytes(int, int) {
+    return 32;   // ticket + two int64 fixed-point sums (+ pad)
 }
