@@ -15,6 +15,9 @@ from .errors import ShapeMismatchError, ValidationError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsplat_b200.so")
+# A/B experiments only: load another build of the same library (tools/ab.sh)
+if os.environ.get("SB_LIB_VARIANT"):
+    LIB_PATH = os.path.abspath(os.environ["SB_LIB_VARIANT"])
 
 SB_OK, SB_EINVAL, SB_ECUDA, SB_EWORKSPACE, SB_ENODEVICE = 0, -1, -2, -3, -4
 
