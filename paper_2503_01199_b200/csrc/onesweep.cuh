@@ -115,6 +115,10 @@ pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem<K>& sm = *reinterpret_cast<Smem<K>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // persistent CTAs: tiles drawn in ticket order until the (possibly
+    // device-side) count is covered; a look-back only waits on lower
+    // tickets, all held by running CTAs
+    for (;;) {
     if (threadIdx.x == 0) {
         sm.bid = (int)atomicAdd(ticket, 1u);
         sm.n = n_dev ? min(*n_dev, n_cap) : n_cap;
@@ -123,6 +127,7 @@ pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
     __syncthreads();
     const int bid = sm.bid, n = sm.n;
     const int tile_base = bid * kTile;
+    if (tile_base >= n && bid > 0) return;
     const int wbase = tile_base + warp * kWarpKeys;
     K k[kItems];
     uint32_t v[kItems], dr[kItems];   // dr = digit << 16 | rank within the warp (0xffffffff: none)
@@ -180,32 +185,11 @@ pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
         __syncthreads();
     }
     const uint32_t local_off = sm.block_off[d] - cnt;
-    // decoupled look-back for this digit
-    uint32_t prefix = 0;
-    if (bid > 0) {
-        // walk back 16 tiles per round trip (independent loads in flight);
-        // stop at the first not-ready entry and re-poll from there
-        int j = bid - 1;
-        bool done = false;
-        while (!done) {
-            uint32_t sv[16];
-#pragma unroll
-            for (int q = 0; q < 16; q++) sv[q] = j - q >= 0 ? st[(size_t)(j - q) * 256 + d] : (uint32_t)(2u << 30);
-            int q = 0;
-            for (; q < 16; q++) {
-                if ((sv[q] & (kFlagAgg | kFlagInc)) == 0) break;
-                prefix += sv[q] & kValMask;
-                if (sv[q] & kFlagInc) { done = true; break; }
-            }
-            j -= q;
-        }
-        st[(size_t)bid * 256 + d] = kFlagInc | (prefix + cnt);
-    }
     __syncthreads();
     sm.block_off[d] = local_off;
-    sm.global_off[d] = digit_base[d] + prefix;
     __syncthreads();
-    // stage in digit order (stable), then write digit-contiguous runs
+    // stage in digit order (stable) before the look-back, so the keys'
+    // registers are free for a wide look-back window
 #pragma unroll
     for (int j = 0; j < kItems; j++) {
         if (dr[j] == 0xffffffffu) continue;
@@ -214,6 +198,29 @@ pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
         sm.keys[pos] = k[j];
         sm.vals[pos] = v[j];
     }
+    // decoupled look-back for this digit: 64 predecessor tiles per round trip
+    // (independent loads in flight); stop at the first not-ready entry and
+    // re-poll from there
+    uint32_t prefix = 0;
+    if (bid > 0) {
+        constexpr int kLB = 64;
+        int j = bid - 1;
+        bool done = false;
+        while (!done) {
+            uint32_t sv[kLB];
+#pragma unroll
+            for (int q = 0; q < kLB; q++) sv[q] = j - q >= 0 ? st[(size_t)(j - q) * 256 + d] : (uint32_t)(2u << 30);
+            int q = 0;
+            for (; q < kLB; q++) {
+                if ((sv[q] & (kFlagAgg | kFlagInc)) == 0) break;
+                prefix += sv[q] & kValMask;
+                if (sv[q] & kFlagInc) { done = true; break; }
+            }
+            j -= q;
+        }
+        st[(size_t)bid * 256 + d] = kFlagInc | (prefix + cnt);
+    }
+    sm.global_off[d] = digit_base[d] + prefix;
     __syncthreads();
     const int tn = max(0, min(kTile, n - tile_base));
     for (int i = threadIdx.x; i < tn; i += kThreads) {
@@ -222,6 +229,9 @@ pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
         const uint32_t g = sm.global_off[dd] + (uint32_t)i - sm.block_off[dd];
         if (kout) kout[g] = key;
         vout[g] = sm.vals[i];
+    }
+    if (tile_base + kTile >= n) return;   // the last tile: no more tickets are needed
+    __syncthreads();                      // shared memory is reused by the next tile
     }
 }
 
@@ -251,6 +261,8 @@ int sort(K* keys, uint32_t* vals, K* k_alt, uint32_t* v_alt, const int* n_dev, i
     sb_launch(hist_kernel<K>, hb, kThreads, 0, stream, keys, n_dev, n_cap, passes, hist);
     sb_launch(scan_hist_kernel, 1, 256, 0, stream, hist, passes);
     int flip = 0;
+    // persistent pass grid: the resident CTAs, at most one per tile
+    const int grid = min(tiles, sb_resident_blocks(pass_kernel<K>, kThreads, sizeof(Smem<K>)));
     for (int p = 0; p < passes; p++) {
         cudaMemsetAsync(status, 0, (size_t)tiles * 256 * sizeof(uint32_t) + sizeof(unsigned), stream);
         const K* ki = flip ? k_alt : keys;
@@ -258,7 +270,7 @@ int sort(K* keys, uint32_t* vals, K* k_alt, uint32_t* v_alt, const int* n_dev, i
         K* ko = flip ? keys : k_alt;
         uint32_t* vo = flip ? vals : v_alt;
         const bool last = p == passes - 1;
-        sb_launch(pass_kernel<K>, tiles, kThreads, sizeof(Smem<K>), stream, ki, (p == 0 && iota) ? nullptr : vi,
+        sb_launch(pass_kernel<K>, grid, kThreads, sizeof(Smem<K>), stream, ki, (p == 0 && iota) ? nullptr : vi,
                   (last && !keep_keys) ? nullptr : ko, vo, n_dev, n_cap, 8 * p, hist + 256 * p, status, ticket);
         flip ^= 1;
     }

@@ -555,7 +555,10 @@ struct BwdParams {
     const float* T_final;   // (H, W)
     const int32_t* last;    // (H, W)
     sb_screen_grad* grads;  // (N_c,) compact, zeroed
-    sb_screen_grad* pair_rows;  // deterministic mode: (P,) one row per tile-list entry, zeroed
+    sb_screen_grad* pair_rows;  // deterministic mode: rows of the contributing (primitive, tile) entries, appended
+    unsigned long long* det_keys;   // deterministic mode: per appended row, slot << tile_bits | tile
+    int* det_count;             // deterministic mode: rows appended so far (zeroed before the launch)
+    int tile_bits;
 };
 
 SB_INLINE float warp_tree_f(float v) {
@@ -633,7 +636,6 @@ struct BwdWarpSmem {
     float2 pairs[kPairCh * kBatch * 32];
     int slot[kBatch];
     int count[kBatch];
-    int pos[kBatch];        // tile-list position of the entry (deterministic mode)
 };
 
 // reduction.py:35-58 over one row of 32 lane values held in registers:
@@ -713,12 +715,13 @@ SB_INLINE float2 row_tree2(float2 v[32]) {
 // reference (backward.py:254-255 sums float64 f and f^2 of the same f) --
 // never a densification candidate.  (The S row itself carries fl(uG^2)
 // 2^64 / o^2, whose float32 rounding would leave an ulp-level residue.)
-// Deterministic mode: the (primitive, tile) row goes to its own slot of the
-// per-entry buffer (tile-list position) with plain stores; a later ordered
-// per-primitive reduction (det_reduce_kernel) sums the rows in tile order.
+// Deterministic mode: the (primitive, tile) row is appended (plain stores,
+// every field written once) with its key (compact slot, tile-list
+// position); a stable sort of the keys groups each primitive's rows in tile
+// order and det_reduce_kernel sums them in a fixed order.
 template <class WS>
 SB_INLINE void emit_row(const WS& ws, int c, int b, float out, sb_screen_grad* pair_rows) {
-    sb_screen_grad* gr = pair_rows + ws.pos[b];
+    sb_screen_grad* gr = pair_rows + b;
     if (c < 9) {
         reinterpret_cast<float*>(gr)[c] = out;
         if (c == 5) {
@@ -748,8 +751,20 @@ SB_INLINE void emit(const WS& ws, int c, int b, float out, sb_screen_grad* grads
 
 template <bool kDet, class WS>
 SB_INLINE void flush_batch(WS& ws, int nb, int lane, int conic_tree, sb_screen_grad* grads,
-                           sb_screen_grad* pair_rows) {
+                           sb_screen_grad* pair_rows, unsigned long long* det_keys = nullptr,
+                           int* det_count = nullptr, int tile_bits = 0, int tile = 0) {
     __syncwarp();
+    if (kDet) {   // append the batch's rows: one reservation per flush
+        int base = 0;
+        if (lane == 0) base = atomicAdd(det_count, nb);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        // key (slot, tile): a primitive has at most one entry per tile, and
+        // the tile lists are concatenated in tile order, so tile order is
+        // the entries' list (np.add.at) order
+        if (lane < nb)
+            det_keys[base + lane] = ((unsigned long long)(uint32_t)ws.slot[lane] << tile_bits) | (uint32_t)tile;
+        pair_rows += base;
+    }
     if (lane < kRowCh * nb) {
         const int c = lane / nb, b = lane - c * nb;
         float v[32];
@@ -906,21 +921,22 @@ raster_bwd_kernel(BwdParams p)
                 if (lane == 0) {
                     ws.slot[nb] = r.slot;
                     ws.count[nb] = C;
-                    if (kDet) ws.pos[nb] = beg + k;
                 }
                 // next slot nb: float rows rotated by 4 nb, pair rows by 2 nb
                 ++nb;
                 pc_off = nb * 32 + ((lane + 4 * nb) & 31);
                 pp_off = nb * 32 + ((lane + 2 * nb) & 31);
                 if (nb == kBatch) {
-                    flush_batch<kDet>(ws, nb, lane, p.conic_tree, p.grads, p.pair_rows);
+                    flush_batch<kDet>(ws, nb, lane, p.conic_tree, p.grads, p.pair_rows, p.det_keys, p.det_count,
+                                      p.tile_bits, t);
                     nb = 0;
                     pc_off = lane;
                     pp_off = lane;
                 }
             }
         }
-        if (nb) flush_batch<kDet>(ws, nb, lane, p.conic_tree, p.grads, p.pair_rows);
+        if (nb) flush_batch<kDet>(ws, nb, lane, p.conic_tree, p.grads, p.pair_rows, p.det_keys, p.det_count,
+                                  p.tile_bits, t);
     }
 }
 
@@ -1371,26 +1387,28 @@ void sb_launch_raster_fwd(const RasterRec* recs, const RasterRow* rows, const in
 
 // ---- deterministic backward: ordered per-primitive reduction -------------
 // (backward.py:261-270: np.add.at scatters each tile's per-primitive values
-// in tile order.)  The raster backward wrote one sb_screen_grad row per
-// tile-list entry; the entries are grouped by compact slot with a stable
-// radix sort of the slots (values = entry positions, so each group stays in
-// tile order), and each primitive's rows are summed in a fixed order (four
-// interleaved tile-order partial sums, then a fixed butterfly) -- float32
-// channels in float32 like the reference's g_screen, S / M in float64, C in
-// integers.  No atomics: bit-reproducible for identical inputs.
-size_t sb_sort_u32_ws(int n_cap, int bits);
-int sb_launch_sort_u32_iota(uint32_t*, uint32_t*, uint32_t*, uint32_t*, const int*, int, int, void*, cudaStream_t);
+// in tile order.)  The raster backward appended one sb_screen_grad row per
+// CONTRIBUTING (primitive, tile) entry -- about 12% of the tile-list
+// entries at config B -- keyed by (compact slot, tile-list position); a
+// stable radix sort of the keys groups each primitive's rows in tile order,
+// and each primitive's rows are summed in a fixed order (four interleaved
+// partial sums, then a fixed butterfly) -- float32 channels in float32 like
+// the reference's g_screen, S / M in float64, C in integers.  No float
+// atomics: bit-reproducible for identical inputs.
+size_t sb_sort_u64_ws(int n, int bits);
+int sb_launch_sort_u64_dev(unsigned long long* keys, uint32_t* vals, unsigned long long* keys_alt, uint32_t* vals_alt,
+                           const int* n_dev, int n_cap, int bits, void* ws, cudaStream_t stream);
 
 namespace {
-__global__ void det_segments_kernel(const uint32_t* __restrict__ keys, const int32_t* __restrict__ n_dev,
-                                    int32_t* __restrict__ start, int32_t* __restrict__ end)
+__global__ void det_segments_kernel(const unsigned long long* __restrict__ keys, const int32_t* __restrict__ n_dev,
+                                    int tile_bits, int32_t* __restrict__ start, int32_t* __restrict__ end)
 {
     sb_pdl_begin();
-    const int P = *n_dev;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
-        const uint32_t k = keys[i];
-        if (i == 0 || keys[i - 1] != k) start[k] = i;
-        if (i == P - 1 || keys[i + 1] != k) end[k] = i + 1;
+    const int Q = *n_dev;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += gridDim.x * blockDim.x) {
+        const uint32_t k = (uint32_t)(keys[i] >> tile_bits);
+        if (i == 0 || (uint32_t)(keys[i - 1] >> tile_bits) != k) start[k] = i;
+        if (i == Q - 1 || (uint32_t)(keys[i + 1] >> tile_bits) != k) end[k] = i + 1;
     }
 }
 
@@ -1449,45 +1467,53 @@ static int bits_for(long long n) {
     return b;
 }
 
+// rows and keys sized for every tile-list entry (an upper bound on the
+// contributing ones); nothing of that size is cleared per call
 size_t sb_det_workspace_bytes(long long n_pairs, long long n_compact) {
     const size_t P = (size_t)(n_pairs > 0 ? n_pairs : 1), nc = (size_t)(n_compact > 0 ? n_compact : 1);
-    return align256(P * sizeof(sb_screen_grad)) + 4 * align256(P * 4) + 2 * align256(nc * 4) +
-           align256(sb_sort_u32_ws((int)P, bits_for((long long)nc)));
+    const int bits = 32 + bits_for((long long)nc);   // tile bits <= 32 (the sort workspace only grows with passes)
+    return align256(P * sizeof(sb_screen_grad)) + 2 * align256(P * 8) + 2 * align256(P * 4) + 2 * align256(nc * 4) +
+           256 + align256(sb_sort_u64_ws((int)P, bits));
 }
 
-// deterministic backward: rows per tile-list entry, grouped by slot (stable
-// sort), reduced in tile order into p.grads (every compact slot written)
-static void raster_bwd_det(BwdParams p, int want, const int32_t* n_pairs_dev, const int32_t* prims, long long n_pairs,
-                           long long n_compact, void* ws, cudaStream_t stream)
+// deterministic backward: appended rows of the contributing entries, grouped
+// by slot in tile order (stable sort of (slot, position) keys), reduced in a
+// fixed order into p.grads (every compact slot written)
+static void raster_bwd_det(BwdParams p, int want, long long n_pairs, long long n_compact, void* ws,
+                           cudaStream_t stream)
 {
     const size_t P = (size_t)(n_pairs > 0 ? n_pairs : 1), nc = (size_t)(n_compact > 0 ? n_compact : 1);
+    const int tbits = bits_for((long long)p.ntiles), bits = tbits + bits_for((long long)nc);
     char* w = static_cast<char*>(ws);
     sb_screen_grad* pair_rows = reinterpret_cast<sb_screen_grad*>(w); w += align256(P * sizeof(sb_screen_grad));
-    uint32_t* keys = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
-    uint32_t* keys_alt = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(w); w += align256(P * 8);
+    unsigned long long* keys_alt = reinterpret_cast<unsigned long long*>(w); w += align256(P * 8);
     uint32_t* vals = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
     uint32_t* vals_alt = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
     int32_t* start = reinterpret_cast<int32_t*>(w); w += align256(nc * 4);
     int32_t* end = reinterpret_cast<int32_t*>(w); w += align256(nc * 4);
+    int* count = reinterpret_cast<int*>(w); w += 256;
     void* sort_ws = w;
-    if (n_pairs > 0) cudaMemsetAsync(pair_rows, 0, (size_t)n_pairs * sizeof(sb_screen_grad), stream);
+    cudaMemsetAsync(count, 0, sizeof(int), stream);
     cudaMemsetAsync(start, 0, nc * 4, stream);
     cudaMemsetAsync(end, 0, nc * 4, stream);
     p.pair_rows = pair_rows;
+    p.det_keys = keys;
+    p.det_count = count;
+    p.tile_bits = tbits;
     const int smem = (int)sizeof(BwdWarpSmem) * kBwdWarps;
     sb_smem_attr(raster_bwd_kernel<true>, smem);
     sb_launch(raster_bwd_kernel<true>, min(want, sm_count() * 6), kBwdWarps * 32, smem, stream, p);
     if (n_compact <= 0) return;
     if (n_pairs > 0) {
-        cudaMemcpyAsync(keys, prims, (size_t)n_pairs * 4, cudaMemcpyDeviceToDevice, stream);
-        const int flip = sb_launch_sort_u32_iota(keys, vals, keys_alt, vals_alt, n_pairs_dev, (int)n_pairs,
-                                                 bits_for(n_compact), sort_ws, stream);
+        const int flip = sb_launch_sort_u64_dev(keys, vals, keys_alt, vals_alt, count, (int)n_pairs, bits, sort_ws,
+                                                stream);
         if (flip) {
             keys = keys_alt;
             vals = vals_alt;
         }
         sb_launch(det_segments_kernel, min((int)((n_pairs + 255) / 256), sm_count() * 8), 256, 0, stream, keys,
-                  n_pairs_dev, start, end);
+                  count, tbits, start, end);
     }
     sb_launch(det_reduce_kernel, (int)((n_compact * kDetLanes + 255) / 256), 256, 0, stream, pair_rows, vals, start,
               end, (int)n_compact, p.grads);
@@ -1506,10 +1532,11 @@ void sb_launch_raster_bwd(const RasterRec* recs, const RasterRow* rows, const in
     p.conic_tree = cfg.conic_reduce == 1;
     p.tile_counter = tile_counter;
     p.dL_dI = dL_dI; p.T_final = T_final; p.last = last; p.grads = grads; p.pair_rows = nullptr;
+    p.det_keys = nullptr; p.det_count = nullptr; p.tile_bits = 0;
     const int want = (ntiles + kBwdWarps - 1) / kBwdWarps;
     if (!want) return;
     if (det_ws) {
-        raster_bwd_det(p, want, offsets + ntiles, prims, n_pairs, n_compact, det_ws, stream);
+        raster_bwd_det(p, want, n_pairs, n_compact, det_ws, stream);
         return;
     }
     const int mode = rows ? staging_mode() : 0;

@@ -21,6 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--res", default="1920x1080")
 ap.add_argument("--iters", type=int, default=2)
+ap.add_argument("--deterministic", action="store_true")
 a = ap.parse_args()
 W, H = (int(v) for v in a.res.split("x"))
 arr = scaled_scene_arrays(a.n, 7, (W, H))
@@ -32,7 +33,7 @@ cam = camera_ring(SyntheticSceneSpec(n_gaussians=a.n, n_views=1, view_resolution
 target = torch.rand(H, W, 3, device="cuda", generator=torch.Generator("cuda").manual_seed(0))
 lrs = sb.LearningRates().at(0.0, 3.2)
 for _ in range(a.iters):
-    out, ctx = sb.forward(scene, cam)
+    out, ctx = sb.forward(scene, cam, sb.RasterConfig(deterministic=a.deterministic))
     loss, dI = sb.loss_and_grad(out.color, target, 0.2, return_tensor=True)
     res = sb.backward(scene, ctx, dI)
     sb.adam_step(scene, res.grads, state, res.cluster_mask, lrs)
