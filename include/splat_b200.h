@@ -192,6 +192,13 @@ int sb_raster_bwd(const void* recs, const void* raster_rows, const int32_t* tile
 int sb_chain_projection_bwd(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
                             const int32_t* cluster_offset, const void* recs, const sb_screen_grad* sgrad,
                             float* grads, double* S, double* M, int32_t* C, sb_stream_t stream);
+/* The same chain ADDED into grads (rows of culled clusters untouched): a
+ * multi-view optimiser step (config D; train.py:95-104 summed over views)
+ * accumulates every view's rows in place. */
+int sb_chain_projection_bwd_accumulate(const float* params, int64_t n, const sb_camera* cam,
+                                       const sb_raster_cfg* cfg, const int32_t* cluster_offset, const void* recs,
+                                       const sb_screen_grad* sgrad, float* grads, double* S, double* M, int32_t* C,
+                                       sb_stream_t stream);
 
 /* ---- optimiser / densification ------------------------------------------- */
 /* optim.py:69-98: Adam (0.9, 0.999, 1e-15) on rows of true-masked clusters;

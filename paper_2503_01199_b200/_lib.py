@@ -49,6 +49,7 @@ SIGNATURES = {
     "sb_raster_bwd_workspace_bytes": ([I32, I64, I64], SZ),
     "sb_raster_bwd": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, I64, I64, VP, SZ, VP], C.c_int),
     "sb_chain_projection_bwd": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP], C.c_int),
+    "sb_chain_projection_bwd_accumulate": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP], C.c_int),
     "sb_adam_sparse": ([VP, VP, VP, VP, VP, VP, I64, VP, VP], C.c_int),
     "sb_variance_score": ([VP, VP, VP, I64, VP, VP], C.c_int),
     "sb_lane_reduce": ([VP, I64, C.c_int, VP, VP, VP], C.c_int),
@@ -127,7 +128,7 @@ def ptr(t: torch.Tensor | None):
 KERNELS_PER_CALL = {
     "sb_morton_keys": 3, "sb_morton_encode": 1, "sb_permute_rows": 1, "sb_project_cull_compact": 1, "sb_bin_prepare": 3,
     "sb_bin_finish": 2, "sb_raster_fwd": 1, "sb_raster_bwd": 1, "sb_radix_sort_pairs_u64": 10,
-    "sb_chain_projection_bwd": 1, "sb_adam_sparse": 1, "sb_build_clusters": 1, "sb_cull_clusters": 1, "sb_variance_score": 1, "sb_lane_reduce": 1,
+    "sb_chain_projection_bwd": 1, "sb_chain_projection_bwd_accumulate": 1, "sb_adam_sparse": 1, "sb_build_clusters": 1, "sb_cull_clusters": 1, "sb_variance_score": 1, "sb_lane_reduce": 1,
     "sb_loss_fwd_bwd": 1,
 }
 launch_count = {"n": 0}

@@ -110,11 +110,13 @@ class BackwardResult:
 
 
 def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | None = None,
-             trace=None, grads_out: torch.Tensor | None = None) -> BackwardResult:
+             trace=None, grads_out: torch.Tensor | None = None, accumulate: bool = False) -> BackwardResult:
     """backward.py:205-279.  dL_dI is (H, W, 3) (any float dtype / device;
     cast to float32 on the scene's device).  grads_out: optional preallocated
     float32 rows (>= N, 16), e.g. padded for a reduce-scatter; the gradient
-    rows are its first N rows."""
+    rows are its first N rows.  accumulate=True (needs grads_out) ADDS this
+    view's rows into grads_out (rows of culled clusters untouched): a
+    multi-view step sums its views in place (sb_chain_projection_bwd_accumulate)."""
     if trace is not None:
         raise ValueError("per-fragment traces are a CPU-oracle debug feature")
     if ctx.generation != scene.generation:
@@ -160,6 +162,8 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
               C.byref(cam_s), C.byref(cfg_s), _lib.ptr(dI), _lib.ptr(T_final), _lib.ptr(last),
               _lib.ptr(sgrad), 0 if prezeroed else ctx.n_compact, ctx.n_pairs, ctx.n_compact, _lib.ptr(ws_r),
               ws_r.numel(), stream)
+    if accumulate and grads_out is None:
+        raise ValueError("accumulate=True needs grads_out (the running sum)")
     if grads_out is None:
         grads = torch.empty((n, 16), dtype=torch.float32, device=dev)
     else:
@@ -168,7 +172,8 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
             raise ShapeMismatchError(f"grads_out {tuple(grads_out.shape)} {grads_out.dtype} must be contiguous "
                                      f"float32 (>= {n}, 16) on {scene.data.device}")
         grads = grads_out[:n]
-    _lib.call("sb_chain_projection_bwd", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s),
+    _lib.call("sb_chain_projection_bwd_accumulate" if accumulate else "sb_chain_projection_bwd",
+              _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s),
               _lib.ptr(ctx.cluster_offset), _lib.ptr(ctx.recs), _lib.ptr(sgrad), _lib.ptr(grads), _lib.ptr(stats.S),
               _lib.ptr(stats.M), _lib.ptr(stats.C), stream)
     return BackwardResult(grads=SceneGrads(grads), stats=stats, cluster_mask=ctx.cluster_vis.view(torch.bool))

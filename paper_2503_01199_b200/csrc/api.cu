@@ -31,8 +31,7 @@ void sb_launch_raster_bwd(const RasterRec*, const RasterRow*, const int32_t*, co
 size_t sb_det_workspace_bytes(long long n_pairs, long long n_compact);
 void sb_launch_lane_reduce(const float*, int, int, float*, double*, cudaStream_t);
 void sb_launch_chain(const float*, int, const CamDev&, const int32_t*, const RasterRec*, const sb_screen_grad*, float*,
-                     double*,
-                     double*, int32_t*, cudaStream_t);
+                     double*, double*, int32_t*, int, cudaStream_t);
 void sb_launch_adam(float*, const float*, float*, float*, int32_t*, const uint8_t*, int, const double[5],
                     cudaStream_t);
 void sb_launch_loss(const float*, const float*, const uint8_t*, int, int, float, float*, double*, double*,
@@ -286,8 +285,19 @@ int sb_chain_projection_bwd(const float* params, int64_t n, const sb_camera* cam
     if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
     const CamDev d = make_cam(cam, cfg);
     sb_launch_chain(params, (int)n, d, cluster_offset, static_cast<const RasterRec*>(recs), sgrad, grads, S_, M_, C_,
-                    S(stream));
+                    0, S(stream));
     return check_launch("sb_chain_projection_bwd");
+}
+
+int sb_chain_projection_bwd_accumulate(const float* params, int64_t n, const sb_camera* cam, const sb_raster_cfg* cfg,
+                                       const int32_t* cluster_offset, const void* recs, const sb_screen_grad* sgrad,
+                                       float* grads, double* S_, double* M_, int32_t* C_, sb_stream_t stream) {
+    if (int r = check_cam(cam)) return r;
+    if (n < 0 || n > INT32_MAX) return fail(SB_EINVAL, "n out of range");
+    const CamDev d = make_cam(cam, cfg);
+    sb_launch_chain(params, (int)n, d, cluster_offset, static_cast<const RasterRec*>(recs), sgrad, grads, S_, M_, C_,
+                    1, S(stream));
+    return check_launch("sb_chain_projection_bwd_accumulate");
 }
 
 int sb_adam_sparse(float* params, const float* grads, float* m, float* v, int32_t* step, const uint8_t* cluster_mask,

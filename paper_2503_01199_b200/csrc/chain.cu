@@ -23,6 +23,9 @@ SB_INLINE void rotmat_grad_to_quat(const double d[3][3], const double q[4], doub
                     y * d[1][2]) + x * d[2][0]) + y * d[2][1]);
 }
 
+// kAcc: grads += this view's rows (rows of culled clusters, all zero, are
+// not touched) -- a multi-view step sums its views in place
+template <bool kAcc>
 __global__ void __launch_bounds__(256, 2)
 chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t* __restrict__ cluster_offset,
              const RasterRec* __restrict__ recs, const sb_screen_grad* __restrict__ sg, float4* __restrict__ grads,
@@ -177,6 +180,15 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
         }
     }
     float4* dst = grads + (size_t)g * 4;
+    if (kAcc) {
+        if (off < 0) return;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const float4 a = dst[k];
+            dst[k] = make_float4(a.x + out[4 * k], a.y + out[4 * k + 1], a.z + out[4 * k + 2], a.w + out[4 * k + 3]);
+        }
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < 4; k++) dst[k] = make_float4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
 }
@@ -247,11 +259,15 @@ __global__ void variance_kernel(const double* __restrict__ S, const double* __re
 
 void sb_launch_chain(const float* params, int n, const CamDev& cam, const int32_t* cluster_offset,
                      const RasterRec* recs, const sb_screen_grad* sg, float* grads, double* S, double* M, int32_t* C,
-                     cudaStream_t stream)
+                     int accumulate, cudaStream_t stream)
 {
     if (n <= 0) return;
-    sb_launch(chain_kernel, (n + 255) / 256, 256, 0, stream, reinterpret_cast<const float4*>(params), n, cam,
-              cluster_offset, recs, sg, reinterpret_cast<float4*>(grads), S, M, C);
+    if (accumulate)
+        sb_launch(chain_kernel<true>, (n + 255) / 256, 256, 0, stream, reinterpret_cast<const float4*>(params), n, cam,
+                  cluster_offset, recs, sg, reinterpret_cast<float4*>(grads), S, M, C);
+    else
+        sb_launch(chain_kernel<false>, (n + 255) / 256, 256, 0, stream, reinterpret_cast<const float4*>(params), n,
+                  cam, cluster_offset, recs, sg, reinterpret_cast<float4*>(grads), S, M, C);
 }
 
 void sb_launch_adam(float* params, const float* grads, float* m, float* v, int32_t* step, const uint8_t* mask,

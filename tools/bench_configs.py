@@ -158,18 +158,13 @@ def config_D(steps=10):
     n = 1_000_000
     scene, state, views, targets = make(n, (1920, 1080), 8)
     lrs = sb.LearningRates().at(0.0, position_scale=3.2)
-    acc = torch.zeros((n, 16), dtype=torch.float32, device=DEV)
+    batch = [(views[v], targets[v]) for v in range(8)]
 
     def step():
-        acc.zero_()
-        mask = None
-        for v in range(8):
-            out, ctx = sb.forward(scene, views[v])
-            loss, dI = sb.loss_and_grad(out.color, targets[v], 0.2, return_tensor=True)
-            res = sb.backward(scene, ctx, dI)
-            acc.add_(res.grads.packed)
-            mask = res.cluster_mask.clone() if mask is None else mask | res.cluster_mask
-        sb.adam_step(scene, sb.SceneGrads(acc), state, mask, lrs)
+        # the library's multi-view step: each view's chain adds its rows into
+        # one running sum (sb_chain_projection_bwd_accumulate), masks OR-ed,
+        # one Adam step; the losses stay on the device (no per-step sync)
+        sb.multiview_step(scene, state, batch, lrs, return_tensor=True)
 
     for _ in range(3):
         step()
