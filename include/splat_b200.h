@@ -210,6 +210,29 @@ int sb_adam_sparse(float* params, const float* grads, float* m, float* v, int32_
 int sb_variance_score(const double* S, const double* M, const int32_t* C, int64_t n, double* out,
                       sb_stream_t stream);
 
+/* densify.py:66-84 select_and_grow on the device: the top k rows by (score
+ * desc, index asc) with score > 0 (k = min(max(budget - n, 0), n), HOST),
+ * split when max(exp(log_scale)) > split_threshold.  Writes flags[n] (0, 1
+ * clone, 2 split), clone_idx / split_idx (ascending, capacity k each) and
+ * counts[2] = (clones, splits) on the device. */
+size_t sb_densify_workspace_bytes(int64_t n, int64_t n_virtual);
+int sb_densify_select(const double* scores, const float* params, int64_t n, int64_t k, double split_threshold,
+                      uint8_t* flags, int32_t* clone_idx, int32_t* split_idx, int32_t* counts, void* ws,
+                      size_t ws_bytes, sb_stream_t stream);
+/* densify.py:87-157 apply_growth + prune in one ordered compaction: the rows
+ * not split, then the clones, the + children and the - children (+-0.5
+ * sigma_max along the principal axis, log_scale - log 1.6), kept when
+ * sigmoid(opacity_logit) >= prune_threshold, into params_out (capacity
+ * n + n_clone + 2 n_split rows); every extra e (n_extras <= 16, row_bytes[e]
+ * bytes per row) is copied for kept original rows and zero for new rows.
+ * n_out[0] (device) = rows written.  ws: sb_densify_workspace_bytes(n,
+ * n + n_clone + 2 n_split). */
+int sb_densify_apply(const float* params, int64_t n, const uint8_t* flags, const int32_t* clone_idx, int64_t n_clone,
+                     const int32_t* split_idx, int64_t n_split, double prune_threshold, int32_t n_extras,
+                     const void* const* extra_src, void* const* extra_dst, const int32_t* extra_row_bytes,
+                     float* params_out, int32_t* n_out, void* ws, size_t ws_bytes, sb_stream_t stream);
+
+
 /* metrics.py:118-132 loss_and_grad, fused: (1 - lam) L1 + lam (1 - SSIM)
  * over (H, W, 3) float32 images and dL/d rendered.  target is float32, or
  * uint8 (value / 255) when target_u8 != NULL.  loss[0] (float64, device) is

@@ -52,6 +52,9 @@ SIGNATURES = {
     "sb_chain_projection_bwd_accumulate": ([VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP], C.c_int),
     "sb_adam_sparse": ([VP, VP, VP, VP, VP, VP, I64, VP, VP], C.c_int),
     "sb_variance_score": ([VP, VP, VP, I64, VP, VP], C.c_int),
+    "sb_densify_workspace_bytes": ([I64, I64], SZ),
+    "sb_densify_select": ([VP, VP, I64, I64, C.c_double, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
+    "sb_densify_apply": ([VP, I64, VP, VP, I64, VP, I64, C.c_double, I32, VP, VP, VP, VP, VP, VP, SZ, VP], C.c_int),
     "sb_lane_reduce": ([VP, I64, C.c_int, VP, VP, VP], C.c_int),
     "sb_loss_workspace_bytes": ([I32, I32], SZ),
     "sb_loss_fwd_bwd": ([VP, VP, VP, I32, I32, C.c_float, VP, VP, VP, VP], C.c_int),
@@ -129,6 +132,7 @@ KERNELS_PER_CALL = {
     "sb_morton_keys": 3, "sb_morton_encode": 1, "sb_permute_rows": 1, "sb_project_cull_compact": 1, "sb_bin_prepare": 3,
     "sb_bin_finish": 2, "sb_raster_fwd": 1, "sb_raster_bwd": 1, "sb_radix_sort_pairs_u64": 10,
     "sb_chain_projection_bwd": 1, "sb_chain_projection_bwd_accumulate": 1, "sb_adam_sparse": 1, "sb_build_clusters": 1, "sb_cull_clusters": 1, "sb_variance_score": 1, "sb_lane_reduce": 1,
+    "sb_densify_select": 14, "sb_densify_apply": 3,
     "sb_loss_fwd_bwd": 1,
 }
 launch_count = {"n": 0}

@@ -36,6 +36,13 @@ void sb_launch_adam(float*, const float*, float*, float*, int32_t*, const uint8_
                     cudaStream_t);
 void sb_launch_loss(const float*, const float*, const uint8_t*, int, int, float, float*, double*, double*,
                     cudaStream_t);
+size_t sb_densify_select_ws(long long n);
+void sb_launch_densify_select(const double*, const float*, int, int, double, uint8_t*, int32_t*, int32_t*, int32_t*,
+                              void*, cudaStream_t);
+size_t sb_densify_apply_ws(long long n, long long nv);
+int sb_densify_max_extras();
+void sb_launch_densify_apply(const float*, int, const uint8_t*, const int32_t*, int, const int32_t*, int, double, int,
+                             const void* const*, void* const*, const int32_t*, float*, int32_t*, void*, cudaStream_t);
 size_t sb_loss_accum_bytes(int W, int H);
 void sb_launch_variance(const double*, const double*, const int32_t*, int, double*, cudaStream_t);
 void sb_launch_bounds(const float*, int, float*, double*, cudaStream_t);
@@ -349,3 +356,36 @@ int sb_lane_reduce(const float* values, int64_t groups, int mode, float* out_f, 
 }
 
 }  // extern "C"
+
+// ---- densification (densify.py:66-157) ---------------------------------------
+size_t sb_densify_workspace_bytes(int64_t n, int64_t n_virtual) {
+    const size_t a = sb_densify_select_ws((long long)n), b = sb_densify_apply_ws((long long)n, (long long)n_virtual);
+    return (a > b ? a : b) + 256;
+}
+
+int sb_densify_select(const double* scores, const float* params, int64_t n, int64_t k, double split_threshold,
+                      uint8_t* flags, int32_t* clone_idx, int32_t* split_idx, int32_t* counts, void* ws,
+                      size_t ws_bytes, sb_stream_t stream) {
+    if (n < 0 || n > INT32_MAX / 2) return fail(SB_EINVAL, "n out of range");
+    if (k < 0 || k > n) return fail(SB_EINVAL, "k out of range [0, n]");
+    if (ws_bytes < sb_densify_workspace_bytes(n, n)) return fail(SB_EWORKSPACE, "densify workspace too small");
+    sb_launch_densify_select(scores, params, (int)n, (int)k, split_threshold, flags, clone_idx, split_idx, counts, ws,
+                             S(stream));
+    return check_launch("sb_densify_select");
+}
+
+int sb_densify_apply(const float* params, int64_t n, const uint8_t* flags, const int32_t* clone_idx, int64_t n_clone,
+                     const int32_t* split_idx, int64_t n_split, double prune_threshold, int32_t n_extras,
+                     const void* const* extra_src, void* const* extra_dst, const int32_t* extra_row_bytes,
+                     float* params_out, int32_t* n_out, void* ws, size_t ws_bytes, sb_stream_t stream) {
+    if (n < 0 || n_clone < 0 || n_split < 0 || n + n_clone + 2 * n_split > INT32_MAX / 2)
+        return fail(SB_EINVAL, "row counts out of range");
+    if (n_extras < 0 || n_extras > sb_densify_max_extras()) return fail(SB_EINVAL, "too many extras for one call");
+    for (int e = 0; e < n_extras; e++)
+        if (extra_row_bytes[e] <= 0) return fail(SB_EINVAL, "extra row bytes must be positive");
+    if (ws_bytes < sb_densify_workspace_bytes(n, n + n_clone + 2 * n_split))
+        return fail(SB_EWORKSPACE, "densify workspace too small");
+    sb_launch_densify_apply(params, (int)n, flags, clone_idx, (int)n_clone, split_idx, (int)n_split, prune_threshold,
+                            n_extras, extra_src, extra_dst, extra_row_bytes, params_out, n_out, ws, S(stream));
+    return check_launch("sb_densify_apply");
+}

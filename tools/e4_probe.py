@@ -22,3 +22,15 @@ def errs(c):
 fast = np.array([errs(cfg) for _ in range(40)])
 print("fast max per slice", fast.max(0)); print("fast median", np.median(fast, 0))
 print("det", errs(dataclasses.replace(cfg, deterministic=True)))
+
+# fast (atomic order) vs the fixed-order backward, floored relative over all channels
+def grads(c):
+    out, ctx = sb.forward(scene, cam, c)
+    return sb.backward(scene, ctx, torch.from_numpy(d[f"{prefix}dL_dI"]), sb.DensifyStats.zeros(scene.n)).grads.packed.double().cpu().numpy()
+det = grads(dataclasses.replace(cfg, deterministic=True))
+rel = []
+for _ in range(40):
+    f = grads(cfg)
+    den = np.maximum(np.abs(det), 1e-3 * np.abs(det).max(axis=0, keepdims=True))
+    rel.append(float((np.abs(f - det) / np.maximum(den, 1e-30)).max()))
+print("fast vs det floored rel: median %.2e max %.2e" % (np.median(rel), max(rel)))
