@@ -229,12 +229,15 @@ def _call(lib, name, args):
 
 
 # ---------------------------------------------------------------------------
-# workspace arena: one growable byte buffer per (purpose, device)
+# workspace arena: one growable byte buffer per (purpose, device, stream)
 _arena: dict = {}
 
 
 def workspace(purpose: str, nbytes: int, device) -> torch.Tensor:
-    key = (purpose, str(device))
+    """Per (purpose, device, current stream): the self-resetting workspaces
+    (tile queues, look-back words, bin counts, loss ticket, screen-gradient
+    rows) must not be shared by work in flight on two streams at once."""
+    key = (purpose, str(device), torch.cuda.current_stream(device).cuda_stream)
     buf = _arena.get(key)
     if buf is None or buf.numel() < nbytes:
         # zero-filled once: the raster tile queues expect a zeroed workspace

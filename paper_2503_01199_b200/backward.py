@@ -19,7 +19,7 @@ import torch
 
 from . import _lib
 from .errors import ShapeMismatchError, StaleSceneError
-from .forward import SGRAD_BYTES, RenderContext, _sgrad_clean
+from .forward import SGRAD_BYTES, RenderContext, _sgrad_clean, _stream_key
 from .scene import CHANNEL_COLS, RAW_CHANNELS, SceneSoA
 
 GRAD_CHANNELS = RAW_CHANNELS
@@ -110,11 +110,14 @@ class BackwardResult:
 
 
 def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | None = None,
-             trace=None, grads_out: torch.Tensor | None = None, accumulate: bool = False) -> BackwardResult:
+             trace=None, grads_out: torch.Tensor | None = None, accumulate: bool = False,
+             chain_after: torch.cuda.Event | None = None) -> BackwardResult:
     """backward.py:205-279.  dL_dI is (H, W, 3) (any float dtype / device;
     cast to float32 on the scene's device).  grads_out: optional preallocated
     float32 rows (>= N, 16), e.g. padded for a reduce-scatter; the gradient
-    rows are its first N rows.  accumulate=True (needs grads_out) ADDS this
+    rows are its first N rows.  chain_after: the projection chain (which
+    writes grads_out and the statistics) waits for this event -- views on
+    two streams serialise only their chains.  accumulate=True (needs grads_out) ADDS this
     view's rows into grads_out (rows of culled clusters untouched): a
     multi-view step sums its views in place (sb_chain_projection_bwd_accumulate)."""
     if trace is not None:
@@ -152,8 +155,8 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
     sgrad = _lib.workspace("sgrad", nc * SGRAD_BYTES, dev)
     # rows already zeroed by this context's forward (project kernel), unless
     # another forward or backward has used the workspace since
-    prezeroed = ctx.token != 0 and _sgrad_clean.get(str(dev)) == ctx.token
-    _sgrad_clean.pop(str(dev), None)
+    prezeroed = ctx.token != 0 and _sgrad_clean.get(_stream_key(dev)) == ctx.token
+    _sgrad_clean.pop(_stream_key(dev), None)
     det = int(bool(ctx.config.deterministic))
     ws_r = _lib.workspace("raster_bwd",
                           _lib.load().sb_raster_bwd_workspace_bytes(det, ctx.n_pairs, ctx.n_compact), dev)
@@ -172,6 +175,8 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
             raise ShapeMismatchError(f"grads_out {tuple(grads_out.shape)} {grads_out.dtype} must be contiguous "
                                      f"float32 (>= {n}, 16) on {scene.data.device}")
         grads = grads_out[:n]
+    if chain_after is not None:
+        torch.cuda.current_stream(dev).wait_event(chain_after)
     _lib.call("sb_chain_projection_bwd_accumulate" if accumulate else "sb_chain_projection_bwd",
               _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s),
               _lib.ptr(ctx.cluster_offset), _lib.ptr(ctx.recs), _lib.ptr(sgrad), _lib.ptr(grads), _lib.ptr(stats.S),

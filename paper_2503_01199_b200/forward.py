@@ -159,12 +159,18 @@ _sgrad_clean: dict = {}
 _ctx_tokens = itertools.count(1)
 
 
+def _stream_key(dev):
+    """(device, current stream): per-stream host state (counter mirror,
+    clean screen-gradient workspace)."""
+    return (str(dev), torch.cuda.current_stream(dev).cuda_stream)
+
+
 def _pinned_counters(dev):
     """Pinned host mirror of the counters and its device address (one per
-    device; the forward reads it before returning, so it is never in flight
-    twice).  The bin scan kernel writes it directly when the buffer is
-    mapped (address not None); otherwise it is filled by a copy."""
-    key = str(dev)
+    device and stream; the forward reads it before returning, so it is never
+    in flight twice).  The bin scan kernel writes it directly when the
+    buffer is mapped (address not None); otherwise it is filled by a copy."""
+    key = _stream_key(dev)
     if key not in _pinned:
         host = torch.zeros(8, dtype=torch.int32, pin_memory=True)
         addr = C.c_void_p()
@@ -215,7 +221,7 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
     tile_offsets = tile_buf[: ntiles + 1]
     ws = _lib.workspace("project", lib.sb_project_workspace_bytes(n), dev)
     sgrad = _lib.workspace("sgrad", max(n, 1) * SGRAD_BYTES, dev) if zero_sgrad else None
-    _sgrad_clean.pop(str(dev), None)
+    _sgrad_clean.pop(_stream_key(dev), None)
     _lib.call("sb_project_cull_compact", _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s), _lib.ptr(recs),
               _lib.ptr(cmap), _lib.ptr(coff), _lib.ptr(cvis), _lib.ptr(counters),
               _lib.ptr(sgrad) if sgrad is not None else None, _lib.ptr(rows), _lib.ptr(caabb), _lib.ptr(ccull),
@@ -269,7 +275,7 @@ def _launch_forward(scene: SceneSoA, camera: CameraView, config: RasterConfig, h
                         n_degenerate=ndeg, half=half)
     if sgrad is not None:
         ctx.token = next(_ctx_tokens)
-        _sgrad_clean[str(dev)] = ctx.token
+        _sgrad_clean[_stream_key(dev)] = ctx.token
     return out, ctx
 
 

@@ -154,7 +154,7 @@ def config_C(epochs=2):
           "stages_ms": stages, "P_pairs": ctx.n_pairs, "n_compact": ctx.n_compact})
 
 
-def config_D(steps=10):
+def config_D(steps=10, streams=int(os.environ.get("SB_VIEW_STREAMS", "2"))):
     n = 1_000_000
     scene, state, views, targets = make(n, (1920, 1080), 8)
     lrs = sb.LearningRates().at(0.0, position_scale=3.2)
@@ -164,14 +164,14 @@ def config_D(steps=10):
         # the library's multi-view step: each view's chain adds its rows into
         # one running sum (sb_chain_projection_bwd_accumulate), masks OR-ed,
         # one Adam step; the losses stay on the device (no per-step sync)
-        sb.multiview_step(scene, state, batch, lrs, return_tensor=True)
+        sb.multiview_step(scene, state, batch, lrs, return_tensor=True, streams=streams)
 
     for _ in range(3):
         step()
     ms, wall = device_time(lambda: [step() for _ in range(steps)])
     line("D", "1M Gaussians, 1920x1080, 8 views per optimiser step on 1 GPU (grads summed, one Adam step)",
          8 * steps / (ms / 1e3), "views/s", ms,
-         {"steps": steps, "steps_per_s": steps / (ms / 1e3), "wall_ms": wall,
+         {"steps": steps, "steps_per_s": steps / (ms / 1e3), "wall_ms": wall, "view_streams": streams,
           "note": "N=1 point of the view-sharded run; N=2/4/8 add one all-reduce per step (bench.py --gpus N)"})
 
 
