@@ -3,15 +3,15 @@
 # training step, the deterministic backward (sort + ordered reduction) and
 # the TMA staging variants (run under gpurun, 1 GPU):   bash tools/sanitize.sh
 # Full summaries are printed (the judge reads them from profiles/).
-sel="seeded_vs_oracle and 50000 or degenerate or bin_tiles_api or fused_loss or morton or half or densify or deterministic_backward or empty"
+sel="seeded_vs_oracle and 50000 or degenerate or bin_tiles_api or fused_loss or morton or half or densify or deterministic_backward or empty or native_densify"
 run() {   # tool, selection, [env]
   echo "=== compute-sanitizer --tool $1 ($3) :: -k \"$2\""
   env $3 compute-sanitizer --tool $1 --print-limit 5 python -m pytest tests/test_gpu_parity.py -m gpu -q \
       -p no:cacheprovider -k "$2" 2>&1 | grep -E "ERROR SUMMARY|RACECHECK SUMMARY|passed|failed|error" | tail -4
 }
 run memcheck "$sel" ""
-run racecheck "seeded_vs_oracle and 50000 or degenerate or deterministic_backward" ""
-run synccheck "seeded_vs_oracle and 50000 or degenerate or deterministic_backward" ""
+run racecheck "seeded_vs_oracle and 50000 or degenerate or deterministic_backward or native_densify" ""
+run synccheck "seeded_vs_oracle and 50000 or degenerate or deterministic_backward or native_densify" ""
 run initcheck "seeded_vs_oracle and 50000" ""
 run memcheck "seeded_vs_oracle and 50000" "SB_RASTER_STAGING=g4"
 run racecheck "seeded_vs_oracle and 50000" "SB_RASTER_STAGING=tma"
