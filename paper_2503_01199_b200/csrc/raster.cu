@@ -258,11 +258,13 @@ raster_fwd_kernel(FwdParams p)
         // out-of-image pixels start terminated (T = 0 < t_stop): they never
         // blend and are never written
         float T[4], rgb[4][3];
+        float2 rg[4];
         int frags[4], last[4];
 #pragma unroll
         for (int i = 0; i < 4; i++) {
             T[i] = (pxi < p.W && py0i + i < p.H) ? 1.0f : 0.0f;
             rgb[i][0] = rgb[i][1] = rgb[i][2] = 0.0f;
+            rg[i] = make_float2(0.0f, 0.0f);
             frags[i] = 0;
             last[i] = 0;
         }
@@ -297,8 +299,8 @@ raster_fwd_kernel(FwdParams p)
                         // T (which decides termination / frag counts) keeps
                         // numpy's rounding; the colour sum may fuse
                         const float w = T[i] * alpha;
-                        rgb[i][0] = fmaf(w, r.r, rgb[i][0]);
-                        rgb[i][1] = fmaf(w, r.g, rgb[i][1]);
+                        // (r, g) as one f32x2 FMA with w broadcast
+                        rg[i] = __ffma2_rn(make_float2(w, w), make_float2(r.r, r.g), rg[i]);
                         rgb[i][2] = fmaf(w, r.bl, rgb[i][2]);
                         T[i] = FMUL(T[i], FSUB(1.0f, alpha));
                         frags[i]++;
@@ -311,8 +313,8 @@ raster_fwd_kernel(FwdParams p)
         for (int i = 0; i < 4; i++) {
             if (!(pxi < p.W && py0i + i < p.H)) continue;
             const size_t pix = (size_t)(py0i + i) * p.W + pxi;
-            p.out_color[3 * pix + 0] = FADD(rgb[i][0], FMUL(T[i], p.bg[0]));
-            p.out_color[3 * pix + 1] = FADD(rgb[i][1], FMUL(T[i], p.bg[1]));
+            p.out_color[3 * pix + 0] = FADD(rg[i].x, FMUL(T[i], p.bg[0]));
+            p.out_color[3 * pix + 1] = FADD(rg[i].y, FMUL(T[i], p.bg[1]));
             p.out_color[3 * pix + 2] = FADD(rgb[i][2], FMUL(T[i], p.bg[2]));
             p.out_T[pix] = T[i];
             p.out_frags[pix] = frags[i];
