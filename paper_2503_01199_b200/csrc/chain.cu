@@ -180,17 +180,17 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
         }
     }
     float4* dst = grads + (size_t)g * 4;
-    if (kAcc) {
+    if constexpr (kAcc) {
         if (off < 0) return;
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             const float4 a = dst[k];
             dst[k] = make_float4(a.x + out[4 * k], a.y + out[4 * k + 1], a.z + out[4 * k + 2], a.w + out[4 * k + 3]);
         }
-        return;
-    }
+    } else {
 #pragma unroll
-    for (int k = 0; k < 4; k++) dst[k] = make_float4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+        for (int k = 0; k < 4; k++) dst[k] = make_float4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+    }
 }
 
 // optim.py:69-98: rows of true-masked clusters, per-row step counters.
