@@ -8,8 +8,10 @@ seed 7, footprints shrunk by (N/512)^(1/3) per SURVEY 8(d)), Morton-sorted,
 1920x1080 views on the reference's camera ring.  One step = one full training
 iteration per GPU: project + cluster cull + compact + bin + per-tile sort +
 raster forward + L1/D-SSIM loss + raster backward + projection chain +
-(one NCCL all-reduce of the gradient rows and cluster masks when N > 1;
-densification statistics stay rank-local until read) + cluster-sparse Adam.
+cluster-sparse Adam (N > 1: the gradient rows and cluster masks are
+all-reduced over NCCL in four cluster-aligned chunks, each overlapping the
+next chunk's chain and the previous chunk's Adam; densification statistics
+stay rank-local until read).
 Each rank rasterises its own view against replicated Gaussians (weak scaling).
 
 `value`  whole-job views/s with inputs resident in HBM, device-timed with CUDA
@@ -169,13 +171,16 @@ class Trainer:
             res = sb.backward(self.scene, ctx, dI, sb.DensifyStats.from_scene(self.scene), grads_out=gbuf)
             self.vp.zero1_step(self.scene, gbuf, res.cluster_mask, self.state, self.lrs)
             return loss, ctx
-        res = sb.backward(self.scene, ctx, dI, sb.DensifyStats.from_scene(self.scene))
-        mask = res.cluster_mask
         if self.ws > 1:
             # sum the views' grads over ranks, OR the masks --
-            # one all-reduce of the gradient rows (mask in a padding column)
-            mask = self.vp.reduce_grads(res.grads.packed, mask)
-        sb.adam_step(self.scene, res.grads, self.state, mask, self.lrs)
+            # the gradient rows (mask in a padding column) all-reduced in
+            # cluster-aligned chunks, each under the next chunk's chain and
+            # the previous chunk's Adam step
+            self.vp.overlapped_step(self.scene, ctx, dI, self.state, self.lrs,
+                                    sb.DensifyStats.from_scene(self.scene), chunks=4)
+            return loss, ctx
+        res = sb.backward(self.scene, ctx, dI, sb.DensifyStats.from_scene(self.scene))
+        sb.adam_step(self.scene, res.grads, self.state, res.cluster_mask, self.lrs)
         return loss, ctx
 
 
@@ -457,7 +462,7 @@ def main():
         if consistency is not None:
             line["rank_consistency"] = consistency
             line["config"]["optimizer_step"] = "zero1 (reduce-scatter, sharded Adam, all-gather)" if args.zero1 \
-                else "all-reduce of the gradient rows, replicated Adam"
+                else "all-reduce of the gradient rows in 4 chunks overlapped with the chain and Adam, replicated Adam"
         print(json.dumps(line))
     if ws > 1:
         dist.barrier()

@@ -19,6 +19,7 @@ import torch
 
 from . import _lib
 from .errors import ShapeMismatchError, StaleSceneError
+from .ccc import CLUSTER_SIZE
 from .forward import SGRAD_BYTES, RenderContext, _sgrad_clean, _stream_key
 from .scene import CHANNEL_COLS, RAW_CHANNELS, SceneSoA
 
@@ -111,11 +112,14 @@ class BackwardResult:
 
 def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | None = None,
              trace=None, grads_out: torch.Tensor | None = None, accumulate: bool = False,
-             chain_after: torch.cuda.Event | None = None) -> BackwardResult:
+             chain_after: torch.cuda.Event | None = None, chain_chunks=None) -> BackwardResult:
     """backward.py:205-279.  dL_dI is (H, W, 3) (any float dtype / device;
     cast to float32 on the scene's device).  grads_out: optional preallocated
     float32 rows (>= N, 16), e.g. padded for a reduce-scatter; the gradient
-    rows are its first N rows.  chain_after: the projection chain (which
+    rows are its first N rows.  chain_chunks(chain, grads): runs the
+    projection chain itself as chain(r0, r1) over cluster-aligned row ranges
+    (ViewParallel.overlapped_step interleaves them with the gradient
+    all-reduce).  chain_after: the projection chain (which
     writes grads_out and the statistics) waits for this event -- views on
     two streams serialise only their chains.  accumulate=True (needs grads_out) ADDS this
     view's rows into grads_out (rows of culled clusters untouched): a
@@ -177,8 +181,25 @@ def backward(scene: SceneSoA, ctx: RenderContext, dL_dI, stats: DensifyStats | N
         grads = grads_out[:n]
     if chain_after is not None:
         torch.cuda.current_stream(dev).wait_event(chain_after)
-    _lib.call("sb_chain_projection_bwd_accumulate" if accumulate else "sb_chain_projection_bwd",
-              _lib.ptr(scene.data), n, C.byref(cam_s), C.byref(cfg_s),
-              _lib.ptr(ctx.cluster_offset), _lib.ptr(ctx.recs), _lib.ptr(sgrad), _lib.ptr(grads), _lib.ptr(stats.S),
-              _lib.ptr(stats.M), _lib.ptr(stats.C), stream)
+    name = "sb_chain_projection_bwd_accumulate" if accumulate else "sb_chain_projection_bwd"
+
+    def chain(r0: int, r1: int):
+        """The chain on scene rows [r0, r1) (r0 cluster-aligned): row-offset
+        views of the parameters, cluster offsets, gradients and statistics."""
+        m = r1 - r0
+        if m <= 0:
+            return
+        f4, f8, i4 = 16 * 4, 8, 4
+        _lib.call(name, C.c_void_p(scene.data.data_ptr() + r0 * f4), m, C.byref(cam_s), C.byref(cfg_s),
+                  C.c_void_p(ctx.cluster_offset.data_ptr() + (r0 // CLUSTER_SIZE) * i4), _lib.ptr(ctx.recs),
+                  _lib.ptr(sgrad), C.c_void_p(grads.data_ptr() + r0 * f4),
+                  C.c_void_p(stats.S.data_ptr() + r0 * f8), C.c_void_p(stats.M.data_ptr() + r0 * f8),
+                  C.c_void_p(stats.C.data_ptr() + r0 * i4), stream)
+
+    if chain_chunks is None:
+        chain(0, n)
+    else:
+        # the caller's schedule: chain_chunks(chain, grads) runs the chain
+        # over row ranges, e.g. interleaved with gradient exchanges
+        chain_chunks(chain, grads)
     return BackwardResult(grads=SceneGrads(grads), stats=stats, cluster_mask=ctx.cluster_vis.view(torch.bool))

@@ -179,6 +179,10 @@ chain_kernel(const float4* __restrict__ params, int n, CamDev cam, const int32_t
             stat_C[g] = C0 + s.C;
         }
     }
+    // padding column 14 of a visible cluster's first row carries the
+    // cluster mask (1.0): a gradient exchange reduces it with the rows
+    // (parallel.py: OR = sum > 0); Adam never reads columns 14-15
+    if (off >= 0 && (g % SB_CLUSTER_SIZE) == 0) out[14] = 1.0f;
     float4* dst = grads + (size_t)g * 4;
     if constexpr (kAcc) {
         if (off < 0) return;

@@ -17,7 +17,10 @@ OR-ed masks, then a single adam_step -- the SURVEY 8(e) definition.
 Works with any torch.distributed backend (NCCL over NVLink on the GPU box,
 gloo for the CPU tests).
 
-The training step uses the leaner pair reduce_grads / reduce_stats:
+The training step uses the leaner pair reduce_grads / reduce_stats (or
+overlapped_step, which splits the gradient exchange into cluster-aligned
+row chunks so each chunk's all-reduce runs under the next chunk's chain and
+the previous chunk's Adam):
   - per step ONE all-reduce of the (N, 16) float32 gradient rows, with the
     cluster mask riding in padding column 14 of each cluster's first row
     (the chain writes zeros there and Adam never reads columns 14-15);
@@ -116,6 +119,51 @@ class ViewParallel:
             full = torch.empty((per * self.world, width), dtype=t.dtype, device=t.device)
             dist.all_gather_into_tensor(full, send, group=self.group)
             t.copy_(full[:n])
+
+    # ---- all-reduce overlapped with the chain and Adam -----------------------
+    def chunk_bounds(self, n: int, chunks: int) -> list:
+        """Cluster-aligned row ranges [r0, r1) covering n rows."""
+        k = (n + CLUSTER_SIZE - 1) // CLUSTER_SIZE
+        per = max(1, (k + chunks - 1) // chunks) * CLUSTER_SIZE
+        return [(r0, min(r0 + per, n)) for r0 in range(0, n, per)]
+
+    def overlapped_step(self, scene, ctx, dL_dI, state, lrs: dict, stats=None, chunks: int = 4):
+        """One data-parallel training step after the forward: raster backward,
+        then per cluster-aligned row chunk the projection chain, an ASYNC
+        all-reduce of that chunk's gradient rows (the cluster mask rides in
+        padding column 14, which the chain sets to 1.0 on a visible
+        cluster's first row) and, once its reduction has landed, that chunk's
+        sparse Adam step.  The collective of chunk c overlaps the chain of
+        chunk c + 1 and the Adam of chunk c - 1 (NCCL runs on its own
+        stream).  Same sums and the same Adam arithmetic as backward +
+        reduce_grads + adam_step; on one rank it is exactly that."""
+        from .backward import SceneGrads, backward
+        from .optim import adam_step
+        n = scene.n
+        key = ("rows", n, str(scene.device))
+        if key not in self._bufs:
+            self._bufs = {k: v for k, v in self._bufs.items() if k[1] == n}
+            self._bufs[key] = torch.empty((max(n, 1), 16), dtype=torch.float32, device=scene.device)
+        g = self._bufs[key]
+        bounds = self.chunk_bounds(n, chunks)
+        works = []
+
+        def schedule(chain, grads):
+            for r0, r1 in bounds:
+                chain(r0, r1)
+                if self.world > 1:
+                    works.append(dist.all_reduce(grads[r0:r1], group=self.group, async_op=True))
+
+        res = backward(scene, ctx, dL_dI, stats, grads_out=g, chain_chunks=schedule)
+        for i, (r0, r1) in enumerate(bounds):
+            sub = g[r0:r1]
+            if self.world > 1:
+                works[i].wait()
+                mask = sub[::CLUSTER_SIZE, MASK_COL] > 0
+            else:
+                mask = res.cluster_mask[r0 // CLUSTER_SIZE:(r1 + CLUSTER_SIZE - 1) // CLUSTER_SIZE]
+            adam_step(scene, SceneGrads(sub), state, mask, lrs, rows=(r0, r1))
+        return res
 
     def views_for_step(self, step: int, n_views: int, views_per_rank: int = 1) -> list:
         """Indices of the views this rank renders at `step` (round robin)."""

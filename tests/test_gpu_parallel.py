@@ -84,3 +84,60 @@ def test_view_parallel_train_two_ranks_zero1():
         assert np.array_equal(res[True][r]["m"], res[False][r]["m"])
         assert np.array_equal(res[True][r]["step"], res[False][r]["step"])
     assert res[True][0]["losses"] == res[False][0]["losses"]
+
+
+def _overlap_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2503_01199_b200 as sb
+        from paper_2503_01199_b200.parallel import ViewParallel
+        from paper_2503_01199_b200.synthetic import SyntheticSceneSpec, camera_ring, random_scene_arrays
+        spec = SyntheticSceneSpec(n_gaussians=3000, n_views=4, view_resolution=(96, 72), seed=4)
+        arrays = random_scene_arrays(spec)
+        cams = camera_ring(spec)
+        cfg = sb.RasterConfig(deterministic=True)
+        rng = np.random.default_rng(7)
+        targets = [torch.from_numpy(rng.uniform(0, 1, (72, 96, 3))).float().cuda() for _ in cams]
+        lrs = sb.LearningRates().at(0.0, position_scale=1.0)
+        vp = ViewParallel()
+        got = {}
+        for mode in ("plain", "overlap"):
+            scene = sb.SceneSoA(*[arrays[k] for k in G.CH], device="cuda")
+            sb.morton_sort(scene)
+            state = sb.AdamState(scene)
+            stats = sb.DensifyStats.zeros(scene.n).attach(scene) or sb.DensifyStats.from_scene(scene)
+            for step in range(3):
+                v = (2 * step + rank) % len(cams)
+                out_, ctx = sb.forward(scene, cams[v], cfg)
+                _, dI = sb.loss_and_grad(out_.color, targets[v], 0.2, return_tensor=True)
+                st = sb.DensifyStats.from_scene(scene)
+                if mode == "plain":
+                    res = sb.backward(scene, ctx, dI, st)
+                    mask = vp.reduce_grads(res.grads.packed, res.cluster_mask)
+                    sb.adam_step(scene, res.grads, state, mask, lrs)
+                else:
+                    vp.overlapped_step(scene, ctx, dI, state, lrs, st, chunks=3)
+            torch.cuda.synchronize()
+            got[mode] = (scene.data.cpu().numpy(), state.m_rows.cpu().numpy(), state.step.cpu().numpy())
+        out[rank] = got
+    finally:
+        dist.destroy_process_group()
+
+
+def test_overlapped_step_matches_plain_two_ranks():
+    """ViewParallel.overlapped_step (chunked async all-reduce interleaved
+    with the chain and Adam) == backward + reduce_grads + adam_step, bit for
+    bit, on two ranks (fixed-order backward so runs are comparable), and the
+    ranks stay identical."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_overlap_worker, args=(world, _free_port(), out), nprocs=world, join=True,
+                       start_method="spawn")
+    a, b = out[0], out[1]
+    for x, y in zip(a["plain"], a["overlap"]):
+        assert np.array_equal(x, y)
+    for x, y in zip(a["overlap"], b["overlap"]):
+        assert np.array_equal(x, y)
