@@ -496,6 +496,35 @@ SB_INLINE uint32_t sb_lookback_exclusive(unsigned long long* status, int bid, ui
     return excl;
 }
 
+// The two halves of sb_lookback_warp, so a block can publish its aggregate
+// as soon as it is known and look back later (lane 0 publishes).
+SB_INLINE void sb_publish_aggregate(unsigned long long* status, int bid, uint32_t agg) {
+    if ((threadIdx.x & 31) == 0) atomicExch(&status[bid], ((bid == 0 ? 2ull : 1ull) << 32) | agg);
+}
+SB_INLINE uint32_t sb_lookback_published(unsigned long long* status, int bid, uint32_t agg) {
+    const int lane = threadIdx.x & 31;
+    if (bid == 0) return 0;
+    uint32_t excl = 0;
+    int j = bid - 1;
+    while (true) {
+        const int idx = j - lane;
+        const unsigned long long s = idx >= 0 ? atomicAdd(&status[idx], 0ull) : (2ull << 32);
+        const uint32_t flag = (uint32_t)(s >> 32), val = (uint32_t)s;
+        const unsigned unready = __ballot_sync(0xffffffffu, flag == 0);
+        const unsigned inc = __ballot_sync(0xffffffffu, flag == 2);
+        const int first_unready = unready ? __ffs(unready) - 1 : 32;
+        const int first_inc = inc ? __ffs(inc) - 1 : 32;
+        if (first_inc < first_unready) {
+            excl += __reduce_add_sync(0xffffffffu, lane <= first_inc ? val : 0u);
+            break;
+        }
+        excl += __reduce_add_sync(0xffffffffu, lane < first_unready ? val : 0u);
+        j -= first_unready;
+    }
+    if (lane == 0) atomicExch(&status[bid], (2ull << 32) | (excl + agg));
+    return excl;
+}
+
 // Warp-cooperative decoupled look-back (all 32 lanes of ONE warp per block,
 // blocks in ticket order): each round trip inspects 32 predecessors; the
 // prefix is complete once an inclusive entry precedes the first not-ready one.

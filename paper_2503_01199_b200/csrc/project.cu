@@ -59,6 +59,39 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
         bool any_in = false;
         double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
         int ndeg = 0;
+        const bool need_box = use_culling || aabb_out || cull_out;
+        // pass 1 (cheap): the cluster AABB p -+ 3 * max(exp(log_scale)) in
+        // float64 (ccc.py:125-130) and its frustum test, so a cluster that is
+        // inside -- visible whatever its members' in_image (ccc.py:149-164)
+        // -- publishes its look-back aggregate before it projects, and the
+        // clusters after it rarely wait
+        bool inside = true;
+        if (need_box) {
+#pragma unroll 1
+            for (int j = 0; j < 4; j++) {
+                const int g = cl * SB_CLUSTER_SIZE + j * 32 + lane;
+                if (g < n) {
+                    const float4 v0 = __ldg(params + (size_t)g * 4), v1 = __ldg(params + (size_t)g * 4 + 1);
+                    const float p3[6] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y};
+                    sb_member_reach(p3, lo, hi);
+                }
+            }
+            for (int k = 0; k < 3; k++) {
+                lo[k] = warp_min_d(lo[k]);
+                hi[k] = warp_max_d(hi[k]);
+            }
+            inside = sb_aabb_in_frustum(lo, hi, cam.planes);
+            if (lane == 0) {
+                if (aabb_out)
+                    for (int k = 0; k < 3; k++) {
+                        aabb_out[6 * cl + k] = lo[k];
+                        aabb_out[6 * cl + 3 + k] = hi[k];
+                    }
+                if (cull_out) cull_out[cl] = inside ? 1 : 0;
+            }
+        }
+        const bool early = !use_culling || inside;   // visible regardless of in_image
+        if (early) sb_publish_aggregate(status, cl, 1u);
         __syncwarp();   // the previous cluster's records have been copied out
 #pragma unroll 1
         for (int j = 0; j < 4; j++) {
@@ -75,48 +108,23 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
                     p[4 * k] = v.x; p[4 * k + 1] = v.y; p[4 * k + 2] = v.z; p[4 * k + 3] = v.w;
                 }
                 ProjOut o;
-                double s64[3];
-                sb_project(p, cam, o, s64);
+                sb_project(p, cam, o);
                 r.x = o.x; r.y = o.y; r.a = o.ca; r.b = o.cb; r.c = o.cc; r.o = o.op;
                 r.r = o.col[0]; r.g = o.col[1]; r.bl = o.col[2]; r.depth = o.depth; r.radius = o.radius;
                 any_in |= o.in_image;
                 ndeg += o.degenerate ? 1 : 0;
-                // cluster AABB: p -+ 3 * max(exp(log_scale)) in float64 (ccc.py:125-130)
-                const double m = fmax(fmax(s64[0], s64[1]), s64[2]);
-                const double reach = DMUL(3.0, m);
-                for (int k = 0; k < 3; k++) {
-                    lo[k] = fmin(lo[k], DSUB((double)p[k], reach));
-                    hi[k] = fmax(hi[k], DADD((double)p[k], reach));
-                }
                 // flags: bit0 valid, bit1 in_image (tile hits: binning.cu)
                 r.flags = (o.valid ? 1u : 0u) | (o.in_image ? 2u : 0u);
             }
             st[slot] = r;
         }
         // cluster visibility (p-vertex test, einsum order (c0 n0 + c2 n2) + c1 n1)
-        bool vis = true;
         const bool any_ii = __any_sync(0xffffffffu, any_in);
-        if (use_culling || aabb_out || cull_out) {
-            for (int k = 0; k < 3; k++) {
-                lo[k] = warp_min_d(lo[k]);
-                hi[k] = warp_max_d(hi[k]);
-            }
-            const bool inside = sb_aabb_in_frustum(lo, hi, cam.planes);
-            if (use_culling) vis = inside || any_ii;
-            // optional outputs: the cluster's AABB (build_clusters, ccc.py:112-131)
-            // and the pure frustum test (cull_clusters, ccc.py:134-146)
-            if (lane == 0) {
-                if (aabb_out)
-                    for (int k = 0; k < 3; k++) {
-                        aabb_out[6 * cl + k] = lo[k];
-                        aabb_out[6 * cl + 3 + k] = hi[k];
-                    }
-                if (cull_out) cull_out[cl] = inside ? 1 : 0;
-            }
-        }
+        const bool vis = early || any_ii;
+        if (!early) sb_publish_aggregate(status, cl, vis ? 1u : 0u);
         const int nd = __reduce_add_sync(0xffffffffu, ndeg);
         if (lane == 0 && nd) atomicAdd(ticket + 2, (unsigned)nd);
-        const uint32_t before = sb_lookback_warp(status, cl, vis ? 1u : 0u);
+        const uint32_t before = sb_lookback_published(status, cl, vis ? 1u : 0u);
         if (lane == 0) {
             cluster_vis[cl] = vis ? 1 : 0;
             cluster_offset[cl] = vis ? (int32_t)(before * SB_CLUSTER_SIZE) : -1;
