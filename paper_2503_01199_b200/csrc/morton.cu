@@ -216,13 +216,3 @@ int sb_launch_sort_u64_dev(unsigned long long* keys, uint32_t* vals, unsigned lo
                                               true, ws, stream);
 }
 
-// u32 keys (the deterministic backward groups tile-list entries by compact
-// slot): n_dev (device int, nullable) bounds the count below n_cap
-size_t sb_sort_u32_ws(int n_cap, int bits) { return onesweep::workspace_bytes(n_cap, (bits + 7) / 8); }
-
-int sb_launch_sort_u32_iota(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, const int* n_dev,
-                            int n_cap, int bits, void* ws, cudaStream_t stream)
-{
-    return onesweep::sort<uint32_t>(keys, vals, keys_alt, vals_alt, n_dev, n_cap, (bits + 7) / 8, true, true, ws,
-                                    stream);
-}
