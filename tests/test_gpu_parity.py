@@ -776,3 +776,47 @@ def test_multiview_step_streams_bit_identical():
             assert torch.equal(x, y), k
         assert runs[1][7] == runs[k][7]
     assert not torch.equal(runs[1][0], sb.SceneSoA(*[arrays[c] for c in G.CH], device="cuda").data)
+
+
+def _ref_make_camera(sb, resolution=(32, 32), eye=(0.6, 0.4, -2.5), target=(0, 0, 0), focal=40.0, near=0.1,
+                     far=50.0):
+    """The reference suite's camera helper (pkg/tests/conftest.py:8-17)."""
+    W, H = resolution
+    return sb.CameraView(sb.look_at(eye, target), (focal, focal), ((W - 1) / 2.0, (H - 1) / 2.0), resolution, near,
+                         far)
+
+
+def _ref_make_scene(sb, n, rng, extent=0.3, scale_range=(0.08, 0.2), opacity_range=(-0.5, 1.0)):
+    """The reference suite's random scene (pkg/tests/conftest.py:20-29)."""
+    return sb.SceneSoA(rng.uniform(-extent, extent, (n, 3)), np.log(rng.uniform(*scale_range, (n, 3))),
+                       rng.normal(size=(n, 4)), rng.uniform(-1.0, 1.0, (n, 3)), rng.uniform(*opacity_range, n),
+                       device="cuda")
+
+
+def test_criteria_06_07_culling_and_resort_invisible():
+    """The reference's acceptance criterion 6 (test_acceptance.py:257-272):
+    20 random scene / camera pairs (generated as the reference does), cluster
+    culling on vs off give identical colour, transmittance and fragment
+    counts; and criterion 7's invariance (test_acceptance.py:296-300): a
+    Morton re-sort never changes the render."""
+    sb = _sb()
+    culled_any = False
+    for trial in range(20):
+        rng = np.random.default_rng(trial + 400)
+        scene = _ref_make_scene(sb, int(rng.integers(100, 400)), rng, extent=2.5)
+        sb.morton_sort(scene)
+        eye = (float(rng.uniform(-2, 2)), float(rng.uniform(-1, 1)), float(rng.uniform(-5, -2.5)))
+        cam = _ref_make_camera(sb, (64, 48), eye=eye, target=tuple(rng.uniform(-0.3, 0.3, 3)))
+        on, ctx = sb.forward(scene, cam, sb.RasterConfig(use_culling=True))
+        off, _ = sb.forward(scene, cam, sb.RasterConfig(use_culling=False))
+        culled_any |= ctx.culled_clusters > 0
+        assert torch.equal(on.color, off.color), trial
+        assert torch.equal(on.transmittance, off.transmittance), trial
+        assert torch.equal(on.frag_count, off.frag_count), trial
+    scene = _ref_make_scene(sb, 60, np.random.default_rng(5))
+    cam = _ref_make_camera(sb, (48, 48))
+    before, _ = sb.forward(scene, cam)
+    before = before.color.clone()
+    sb.morton_sort(scene)
+    after, _ = sb.forward(scene, cam)
+    assert torch.equal(before, after.color)
