@@ -820,3 +820,26 @@ def test_criteria_06_07_culling_and_resort_invisible():
     sb.morton_sort(scene)
     after, _ = sb.forward(scene, cam)
     assert torch.equal(before, after.color)
+
+
+def test_criterion_05_exp_aligned_reduce_device():
+    """The reference's acceptance criterion 5 (test_acceptance.py:234-254) on
+    the device reduction the backward uses: 10^5 random 32-sets in
+    [2^-10, 2^10] within 32 * 2^(e_max - 23) of the exact sum (the device
+    rounds the exact integer sum once to float32, inside that bound); an
+    all-equal set and one-hot sets exact."""
+    sb = _sb()
+    rng = np.random.default_rng(13)
+    n = 100_000
+    v = (2.0 ** rng.uniform(-10, 10, (n, 32)) * rng.choice([-1.0, 1.0], (n, 32))).astype(np.float32)
+    got = sb.exp_aligned_reduce(torch.from_numpy(v)).double().cpu().numpy()
+    v64 = v.astype(np.float64)
+    exact = v64.sum(axis=1)
+    e_max = np.floor(np.log2(np.abs(v64).max(axis=1)))
+    bound = 32 * 2.0 ** (e_max - 23)
+    assert np.all(np.abs(got - exact) <= bound)
+    assert float(sb.exp_aligned_reduce(torch.ones(32))) == 32.0
+    xs = (rng.normal(size=1000) * 2.0 ** rng.integers(-10, 11, 1000)).astype(np.float32)
+    one = np.zeros((1000, 32), np.float32)
+    one[np.arange(1000), rng.integers(0, 32, 1000)] = xs
+    assert np.array_equal(sb.exp_aligned_reduce(torch.from_numpy(one)).cpu().numpy(), xs)
