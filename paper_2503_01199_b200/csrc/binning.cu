@@ -872,15 +872,21 @@ __device__ void st_emit(StSmem& sm, SlotOf&& slot_of, int E, int st, int st_x, c
         const unsigned lt = (1u << lane) - 1u;
         const int R = ((n + NW - 1) / NW + 31) & ~31;
         const int e_beg = min(n, warp * R), e_end = min(n, e_beg + R);
-        int cnt = 0;   // lane j: this warp's count for tile j
+        // lane j: this warp's count for tile j.  Per 32 entries each lane
+        // spreads its 16-bit mask into four words of 8-bit fields (nibble n
+        // -> bytes: (n * 0x204081) & 0x01010101) and four warp sums add them
+        // (each field <= 32: no carries); lane j takes its field
+        int cnt = 0;
+        const int wsel = lane >> 2, fsh = 8 * (lane & 3);
         for (int e0 = e_beg; e0 < e_end; e0 += 32) {
             const int e = e0 + lane;
             const uint32_t m = e < e_end ? sm.mask[e] : 0u;
-#pragma unroll
-            for (int j = 0; j < kST * kST; j++) {
-                const int c = __popc(__ballot_sync(0xffffffffu, (m >> j) & 1u));
-                if (lane == j) cnt += c;
-            }
+            const uint32_t s0 = __reduce_add_sync(0xffffffffu, ((m & 0xfu) * 0x204081u) & 0x01010101u);
+            const uint32_t s1 = __reduce_add_sync(0xffffffffu, (((m >> 4) & 0xfu) * 0x204081u) & 0x01010101u);
+            const uint32_t s2 = __reduce_add_sync(0xffffffffu, (((m >> 8) & 0xfu) * 0x204081u) & 0x01010101u);
+            const uint32_t s3 = __reduce_add_sync(0xffffffffu, (((m >> 12) & 0xfu) * 0x204081u) & 0x01010101u);
+            const uint32_t w = wsel == 0 ? s0 : wsel == 1 ? s1 : wsel == 2 ? s2 : s3;
+            cnt += (int)((w >> fsh) & 0xffu);
         }
         if (lane < kST * kST) sm.tot[warp][lane] = cnt;
         __syncthreads();
