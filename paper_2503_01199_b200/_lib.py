@@ -102,9 +102,15 @@ def exported_symbols():
     return sorted(SIGNATURES)
 
 
+_have_cuda = False
+
+
 def require_cuda(t: torch.Tensor | None = None):
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2503_01199_b200 needs a CUDA device (B200, sm_100a); none is available")
+    global _have_cuda
+    if not _have_cuda:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2503_01199_b200 needs a CUDA device (B200, sm_100a); none is available")
+        _have_cuda = True
     if t is not None and not t.is_cuda:
         raise ValueError("expected a CUDA tensor")
 
@@ -114,10 +120,35 @@ def require_cuda(t: torch.Tensor | None = None):
 _stream_device: dict = {}
 
 
+def device_index(device=None) -> int:
+    if isinstance(device, torch.device):
+        return device.index if device.index is not None else torch._C._cuda_getDevice()
+    if device is None:
+        return torch._C._cuda_getDevice()
+    if isinstance(device, int):
+        return device
+    return device_index(torch.device(device))
+
+
+_cuda_ready = False
+
+
+def raw_stream(device=None) -> tuple:
+    """(device index, current stream handle) without constructing a
+    torch.cuda.Stream (the per-call host cost of torch.cuda.current_stream
+    is a visible share of a small-scene iteration)."""
+    global _cuda_ready
+    if not _cuda_ready:
+        torch.cuda.init()
+        _cuda_ready = True
+    idx = device_index(device)
+    return idx, torch._C._cuda_getCurrentRawStream(idx)
+
+
 def stream_ptr(device=None) -> int:
-    s = torch.cuda.current_stream(device)
-    _stream_device[s.cuda_stream] = s.device.index
-    return s.cuda_stream
+    idx, s = raw_stream(device)
+    _stream_device[s] = idx
+    return s
 
 
 def ptr(t: torch.Tensor | None):
@@ -237,7 +268,7 @@ def workspace(purpose: str, nbytes: int, device) -> torch.Tensor:
     """Per (purpose, device, current stream): the self-resetting workspaces
     (tile queues, look-back words, bin counts, loss ticket, screen-gradient
     rows) must not be shared by work in flight on two streams at once."""
-    key = (purpose, str(device), torch.cuda.current_stream(device).cuda_stream)
+    key = (purpose,) + raw_stream(device)
     buf = _arena.get(key)
     if buf is None or buf.numel() < nbytes:
         # zero-filled once: the raster tile queues expect a zeroed workspace

@@ -64,6 +64,19 @@ class CameraView:
         return frustum_planes(self)
 
     def struct(self) -> SbCamera:
+        """The C-ABI struct, rebuilt only when a field changed (the frustum
+        planes cost ~50 us of numpy per build; callers pass the struct by
+        reference and the library copies it at launch)."""
+        key = (self.world_to_camera.tobytes(), self.focal.tobytes(), self.principal_point.tobytes(),
+               self.resolution, self.near, self.far)
+        cached = self.__dict__.get("_struct_cache")
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        s = self._build_struct()
+        self.__dict__["_struct_cache"] = (key, s)
+        return s
+
+    def _build_struct(self) -> SbCamera:
         s = SbCamera()
         s.w2c[:] = [float(v) for v in self.world_to_camera.reshape(16)]
         s.fx, s.fy = float(self.focal[0]), float(self.focal[1])

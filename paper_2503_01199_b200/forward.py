@@ -162,7 +162,7 @@ _ctx_tokens = itertools.count(1)
 def _stream_key(dev):
     """(device, current stream): per-stream host state (counter mirror,
     clean screen-gradient workspace)."""
-    return (str(dev), torch.cuda.current_stream(dev).cuda_stream)
+    return _lib.raw_stream(dev)
 
 
 def _pinned_counters(dev):
