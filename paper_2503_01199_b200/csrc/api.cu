@@ -275,6 +275,8 @@ int sb_raster_bwd(const void* recs, const void* raster_rows, const int32_t* tile
     if (ws_bytes < sb_raster_bwd_workspace_bytes(det, n_pairs, n_compact))
         return fail(SB_EWORKSPACE, "raster backward workspace too small");
     const CamDev d = make_cam(cam, cfg);
+    if (det && (long long)d.tiles_x * d.tiles_y > (1ll << 20))
+        return fail(SB_EINVAL, "the deterministic backward supports tile grids up to 2^20 tiles");
     // (the deterministic reduction writes every compact row itself)
     if (n_cap > 0 && !det) cudaMemsetAsync(sgrad, 0, sizeof(sb_screen_grad) * (size_t)n_cap, S(stream));
     void* det_ws = det ? static_cast<char*>(ws) + sb_raster_workspace_bytes() : nullptr;

@@ -207,6 +207,15 @@ int sb_launch_sort_u64(unsigned long long* keys, uint32_t* vals, unsigned long l
                                               ws, stream);
 }
 
+// u32 keys with given values and a device-side count (the deterministic
+// backward's slot keys over the rows' tile-list positions)
+int sb_launch_sort_u32_dev(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, const int* n_dev,
+                           int n_cap, int bits, void* ws, cudaStream_t stream)
+{
+    return onesweep::sort<uint32_t>(keys, vals, keys_alt, vals_alt, n_dev, n_cap, (bits + 7) / 8, true, false, ws,
+                                    stream);
+}
+
 // u64 keys with a device-side count (the deterministic backward's
 // (slot, position) keys): n_dev bounds the count below n_cap, values iota
 int sb_launch_sort_u64_dev(unsigned long long* keys, uint32_t* vals, unsigned long long* keys_alt, uint32_t* vals_alt,

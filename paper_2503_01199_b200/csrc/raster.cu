@@ -557,10 +557,12 @@ struct BwdParams {
     const float* T_final;   // (H, W)
     const int32_t* last;    // (H, W)
     sb_screen_grad* grads;  // (N_c,) compact, zeroed
-    sb_screen_grad* pair_rows;  // deterministic mode: rows of the contributing (primitive, tile) entries, appended
-    unsigned long long* det_keys;   // deterministic mode: per appended row, slot << tile_bits | tile
-    int* det_count;             // deterministic mode: rows appended so far (zeroed before the launch)
-    int tile_bits;
+    // deterministic mode: the contributing (primitive, tile) rows of tile t
+    // are written at tile-list positions [offsets[t], offsets[t] + cnt[t]) in
+    // the tile's (fixed) processing order, with their compact slots
+    sb_screen_grad* pair_rows;
+    uint32_t* det_keys;
+    int32_t* det_tile_cnt;
 };
 
 SB_INLINE float warp_tree_f(float v) {
@@ -717,10 +719,11 @@ SB_INLINE float2 row_tree2(float2 v[32]) {
 // reference (backward.py:254-255 sums float64 f and f^2 of the same f) --
 // never a densification candidate.  (The S row itself carries fl(uG^2)
 // 2^64 / o^2, whose float32 rounding would leave an ulp-level residue.)
-// Deterministic mode: the (primitive, tile) row is appended (plain stores,
-// every field written once) with its key (compact slot, tile-list
-// position); a stable sort of the keys groups each primitive's rows in tile
-// order and det_reduce_kernel sums them in a fixed order.
+// Deterministic mode: the (primitive, tile) row is stored (plain stores,
+// every field written once) at a tile-list position of its tile, with its
+// compact slot as the key; the tiles' rows, concatenated in tile order and
+// stably sorted by slot, give each primitive's rows in tile order, which
+// det_reduce_kernel sums in a fixed order.
 template <class WS>
 SB_INLINE void emit_row(const WS& ws, int c, int b, float out, sb_screen_grad* pair_rows) {
     sb_screen_grad* gr = pair_rows + b;
@@ -753,19 +756,11 @@ SB_INLINE void emit(const WS& ws, int c, int b, float out, sb_screen_grad* grads
 
 template <bool kDet, class WS>
 SB_INLINE void flush_batch(WS& ws, int nb, int lane, int conic_tree, sb_screen_grad* grads,
-                           sb_screen_grad* pair_rows, unsigned long long* det_keys = nullptr,
-                           int* det_count = nullptr, int tile_bits = 0, int tile = 0) {
+                           sb_screen_grad* pair_rows, uint32_t* det_keys = nullptr, int det_pos = 0) {
     __syncwarp();
-    if (kDet) {   // append the batch's rows: one reservation per flush
-        int base = 0;
-        if (lane == 0) base = atomicAdd(det_count, nb);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        // key (slot, tile): a primitive has at most one entry per tile, and
-        // the tile lists are concatenated in tile order, so tile order is
-        // the entries' list (np.add.at) order
-        if (lane < nb)
-            det_keys[base + lane] = ((unsigned long long)(uint32_t)ws.slot[lane] << tile_bits) | (uint32_t)tile;
-        pair_rows += base;
+    if (kDet) {   // the batch's rows at the tile's next positions (det_pos)
+        if (lane < nb) det_keys[det_pos + lane] = (uint32_t)ws.slot[lane];
+        pair_rows += det_pos;
     }
     if (lane < kRowCh * nb) {
         const int c = lane / nb, b = lane - c * nb;
@@ -808,10 +803,14 @@ raster_bwd_kernel(BwdParams p)
          q = next_tile(p.tile_counter, lane, p.ntiles)) {
         const int t = p.offsets[p.ntiles + 1 + q];   // heavy-first schedule (binning scan)
         const int beg = p.offsets[t];
-        if (p.offsets[t + 1] == beg) continue;
+        if (p.offsets[t + 1] == beg) {
+            if (kDet && lane == 0) p.det_tile_cnt[t] = 0;
+            continue;
+        }
         const int x0 = (t % p.tiles_x) * SB_TILE_W, y0 = (t / p.tiles_x) * SB_TILE_H;
         const int pxi = x0 + (lane & 15), py0i = y0 + 4 * (lane >> 4);
         const float px = (float)pxi, py0 = (float)py0i;
+        int run = 0;   // deterministic mode: rows stored for this tile so far
         // per pixel: T (recovered back to front), dI, and Sd = dI . suffix where
         // suffix = sum_{j>k} w_j c_j + T_final bg (backward.py:155-159), so
         // dL/dalpha = T (dI . c) - Sd / (1 - alpha).  Pixel pairs (0,1) and
@@ -929,16 +928,16 @@ raster_bwd_kernel(BwdParams p)
                 pc_off = nb * 32 + ((lane + 4 * nb) & 31);
                 pp_off = nb * 32 + ((lane + 2 * nb) & 31);
                 if (nb == kBatch) {
-                    flush_batch<kDet>(ws, nb, lane, p.conic_tree, p.grads, p.pair_rows, p.det_keys, p.det_count,
-                                      p.tile_bits, t);
+                    flush_batch<kDet>(ws, nb, lane, p.conic_tree, p.grads, p.pair_rows, p.det_keys, beg + run);
+                    run += nb;
                     nb = 0;
                     pc_off = lane;
                     pp_off = lane;
                 }
             }
         }
-        if (nb) flush_batch<kDet>(ws, nb, lane, p.conic_tree, p.grads, p.pair_rows, p.det_keys, p.det_count,
-                                  p.tile_bits, t);
+        if (nb) flush_batch<kDet>(ws, nb, lane, p.conic_tree, p.grads, p.pair_rows, p.det_keys, beg + run);
+        if (kDet && lane == 0) p.det_tile_cnt[t] = run + nb;
     }
 }
 
@@ -1389,31 +1388,107 @@ void sb_launch_raster_fwd(const RasterRec* recs, const RasterRow* rows, const in
 
 // ---- deterministic backward: ordered per-primitive reduction -------------
 // (backward.py:261-270: np.add.at scatters each tile's per-primitive values
-// in tile order.)  The raster backward appended one sb_screen_grad row per
+// in tile order.)  The raster backward stores one sb_screen_grad row per
 // CONTRIBUTING (primitive, tile) entry -- about 12% of the tile-list
-// entries at config B -- keyed by (compact slot, tile-list position); a
-// stable radix sort of the keys groups each primitive's rows in tile order,
-// and each primitive's rows are summed in a fixed order (four interleaved
-// partial sums, then a fixed butterfly) -- float32 channels in float32 like
-// the reference's g_screen, S / M in float64, C in integers.  No float
-// atomics: bit-reproducible for identical inputs.
+// entries at config B -- at the tile's own list positions, in the tile's
+// fixed processing order, with the compact slot as its key.  The tiles' key
+// runs are concatenated in tile order (a scan over the tiles' row counts), a
+// stable radix sort by slot then lists each primitive's rows in tile order
+// (a primitive has at most one entry per tile), and each primitive's rows
+// are summed in a fixed order (four interleaved partial sums, then a fixed
+// butterfly) -- float32 channels in float32 like the reference's g_screen,
+// S / M in float64, C in integers.  No float atomics: bit-reproducible for
+// identical inputs.
 size_t sb_sort_u64_ws(int n, int bits);
-int sb_launch_sort_u64_dev(unsigned long long* keys, uint32_t* vals, unsigned long long* keys_alt, uint32_t* vals_alt,
-                           const int* n_dev, int n_cap, int bits, void* ws, cudaStream_t stream);
+int sb_launch_sort_u32_dev(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, const int* n_dev,
+                           int n_cap, int bits, void* ws, cudaStream_t stream);
 
 namespace {
-__global__ void det_segments_kernel(const unsigned long long* __restrict__ keys, const int32_t* __restrict__ n_dev,
-                                    int tile_bits, int32_t* __restrict__ start, int32_t* __restrict__ end)
+constexpr int kDetMaxTiles = 1 << 20;   // tile grids up to 1M tiles (16384 x 8192 pixels)
+constexpr int kDetScanThreads = 1024;
+
+// exclusive scan of the tiles' row counts (one CTA; rounds of 8
+// consecutive tiles per thread, read as two 16-byte loads) and their total
+__global__ void __launch_bounds__(kDetScanThreads)
+det_tile_scan_kernel(const int32_t* __restrict__ cnt, int ntiles, int32_t* __restrict__ base,
+                     int32_t* __restrict__ total)
+{
+    sb_pdl_begin();
+    constexpr int PER = 8;
+    __shared__ int32_t s_warp[kDetScanThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int carry = 0;
+    for (int r0 = 0; r0 < ntiles; r0 += PER * kDetScanThreads) {
+        const int t0 = r0 + PER * tid;
+        int v[PER];
+        if (t0 + PER <= ntiles) {
+            const int4 a = *reinterpret_cast<const int4*>(cnt + t0), b = *reinterpret_cast<const int4*>(cnt + t0 + 4);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < PER; q++) v[q] = t0 + q < ntiles ? cnt[t0 + q] : 0;
+        }
+        int sum = 0;
+#pragma unroll
+        for (int q = 0; q < PER; q++) sum += v[q];
+        int x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        const int wsum = lane < kDetScanThreads / 32 ? s_warp[lane] : 0;
+        int wincl = wsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, wincl, o);
+            if (lane >= o) wincl += y;
+        }
+        const int before = __shfl_sync(0xffffffffu, wincl - wsum, warp);   // warps before this one
+        const int round = __shfl_sync(0xffffffffu, wincl, 31);
+        int run = carry + before + x - sum;
+#pragma unroll
+        for (int q = 0; q < PER; q++)
+            if (t0 + q < ntiles) {
+                base[t0 + q] = run;
+                run += v[q];
+            }
+        carry += round;
+        __syncthreads();   // s_warp is rewritten by the next round
+    }
+    if (tid == 0) *total = carry;
+}
+
+// the tiles' key runs concatenated in tile order; values = the rows'
+// tile-list positions
+__global__ void det_compact_kernel(const int32_t* __restrict__ offsets, const int32_t* __restrict__ cnt,
+                                   const int32_t* __restrict__ base, const uint32_t* __restrict__ keys_at, int ntiles,
+                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ vals)
+{
+    sb_pdl_begin();
+    const int lane = threadIdx.x & 31;
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += (gridDim.x * blockDim.x) >> 5) {
+        const int c = cnt[t], off = offsets[t], b = base[t];
+        for (int k = lane; k < c; k += 32) {
+            keys[b + k] = keys_at[off + k];
+            vals[b + k] = (uint32_t)(off + k);
+        }
+    }
+}
+
+__global__ void det_segments_kernel(const uint32_t* __restrict__ keys, const int32_t* __restrict__ n_dev,
+                                    int32_t* __restrict__ start, int32_t* __restrict__ end)
 {
     sb_pdl_begin();
     const int Q = *n_dev;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += gridDim.x * blockDim.x) {
-        const uint32_t k = (uint32_t)(keys[i] >> tile_bits);
-        if (i == 0 || (uint32_t)(keys[i - 1] >> tile_bits) != k) start[k] = i;
-        if (i == Q - 1 || (uint32_t)(keys[i + 1] >> tile_bits) != k) end[k] = i + 1;
+        const uint32_t k = keys[i];
+        if (i == 0 || keys[i - 1] != k) start[k] = i;
+        if (i == Q - 1 || keys[i + 1] != k) end[k] = i + 1;
     }
 }
-
 // four lanes per primitive: lane j sums the primitive's rows j, j + 4, ...
 // in tile order, then a fixed two-step butterfly -- a fixed order, so the
 // result is bit-reproducible, with four independent load chains per primitive
@@ -1469,53 +1544,59 @@ static int bits_for(long long n) {
     return b;
 }
 
-// rows and keys sized for every tile-list entry (an upper bound on the
-// contributing ones); nothing of that size is cleared per call
+// rows and slot keys at every tile-list position (an upper bound on the
+// contributing ones), the concatenated keys / values with their sort
+// buffers, per-slot segments and per-tile counts; nothing of size P is
+// cleared per call
 size_t sb_det_workspace_bytes(long long n_pairs, long long n_compact) {
     const size_t P = (size_t)(n_pairs > 0 ? n_pairs : 1), nc = (size_t)(n_compact > 0 ? n_compact : 1);
-    const int bits = 32 + bits_for((long long)nc);   // tile bits <= 32 (the sort workspace only grows with passes)
-    return align256(P * sizeof(sb_screen_grad)) + 2 * align256(P * 8) + 2 * align256(P * 4) + 2 * align256(nc * 4) +
-           256 + align256(sb_sort_u64_ws((int)P, bits));
+    return align256(P * sizeof(sb_screen_grad)) + 5 * align256(P * 4) + 2 * align256(nc * 4) +
+           2 * align256((size_t)kDetMaxTiles * 4) + 256 + align256(sb_sort_u64_ws((int)P, bits_for((long long)nc)));
 }
 
-// deterministic backward: appended rows of the contributing entries, grouped
-// by slot in tile order (stable sort of (slot, position) keys), reduced in a
-// fixed order into p.grads (every compact slot written)
+// deterministic backward: rows at tile-list positions, concatenated in tile
+// order, stably sorted by slot, reduced in a fixed order into p.grads (every
+// compact slot written)
 static void raster_bwd_det(BwdParams p, int want, long long n_pairs, long long n_compact, void* ws,
                            cudaStream_t stream)
 {
     const size_t P = (size_t)(n_pairs > 0 ? n_pairs : 1), nc = (size_t)(n_compact > 0 ? n_compact : 1);
-    const int tbits = bits_for((long long)p.ntiles), bits = tbits + bits_for((long long)nc);
+    const int bits = bits_for((long long)nc);
     char* w = static_cast<char*>(ws);
     sb_screen_grad* pair_rows = reinterpret_cast<sb_screen_grad*>(w); w += align256(P * sizeof(sb_screen_grad));
-    unsigned long long* keys = reinterpret_cast<unsigned long long*>(w); w += align256(P * 8);
-    unsigned long long* keys_alt = reinterpret_cast<unsigned long long*>(w); w += align256(P * 8);
+    uint32_t* keys_at = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
+    uint32_t* keys_alt = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
     uint32_t* vals = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
     uint32_t* vals_alt = reinterpret_cast<uint32_t*>(w); w += align256(P * 4);
     int32_t* start = reinterpret_cast<int32_t*>(w); w += align256(nc * 4);
     int32_t* end = reinterpret_cast<int32_t*>(w); w += align256(nc * 4);
+    int32_t* tile_cnt = reinterpret_cast<int32_t*>(w); w += align256((size_t)kDetMaxTiles * 4);
+    int32_t* tile_base = reinterpret_cast<int32_t*>(w); w += align256((size_t)kDetMaxTiles * 4);
     int* count = reinterpret_cast<int*>(w); w += 256;
     void* sort_ws = w;
-    cudaMemsetAsync(count, 0, sizeof(int), stream);
     cudaMemsetAsync(start, 0, nc * 4, stream);
     cudaMemsetAsync(end, 0, nc * 4, stream);
     p.pair_rows = pair_rows;
-    p.det_keys = keys;
-    p.det_count = count;
-    p.tile_bits = tbits;
+    p.det_keys = keys_at;
+    p.det_tile_cnt = tile_cnt;
     const int smem = (int)sizeof(BwdWarpSmem) * kBwdWarps;
     sb_smem_attr(raster_bwd_kernel<true>, smem);
     sb_launch(raster_bwd_kernel<true>, min(want, sm_count() * 6), kBwdWarps * 32, smem, stream, p);
     if (n_compact <= 0) return;
     if (n_pairs > 0) {
-        const int flip = sb_launch_sort_u64_dev(keys, vals, keys_alt, vals_alt, count, (int)n_pairs, bits, sort_ws,
+        sb_launch(det_tile_scan_kernel, 1, kDetScanThreads, 0, stream, (const int32_t*)tile_cnt, p.ntiles, tile_base,
+                  count);
+        sb_launch(det_compact_kernel, min((p.ntiles + 7) / 8, sm_count() * 8), 256, 0, stream, p.offsets,
+                  (const int32_t*)tile_cnt, (const int32_t*)tile_base, (const uint32_t*)keys_at, p.ntiles, keys, vals);
+        const int flip = sb_launch_sort_u32_dev(keys, vals, keys_alt, vals_alt, count, (int)n_pairs, bits, sort_ws,
                                                 stream);
         if (flip) {
             keys = keys_alt;
             vals = vals_alt;
         }
-        sb_launch(det_segments_kernel, min((int)((n_pairs + 255) / 256), sm_count() * 8), 256, 0, stream, keys,
-                  count, tbits, start, end);
+        sb_launch(det_segments_kernel, min((int)((n_pairs + 255) / 256), sm_count() * 8), 256, 0, stream,
+                  (const uint32_t*)keys, (const int32_t*)count, start, end);
     }
     sb_launch(det_reduce_kernel, (int)((n_compact * kDetLanes + 255) / 256), 256, 0, stream, pair_rows, vals, start,
               end, (int)n_compact, p.grads);
@@ -1534,7 +1615,7 @@ void sb_launch_raster_bwd(const RasterRec* recs, const RasterRow* rows, const in
     p.conic_tree = cfg.conic_reduce == 1;
     p.tile_counter = tile_counter;
     p.dL_dI = dL_dI; p.T_final = T_final; p.last = last; p.grads = grads; p.pair_rows = nullptr;
-    p.det_keys = nullptr; p.det_count = nullptr; p.tile_bits = 0;
+    p.det_keys = nullptr; p.det_tile_cnt = nullptr;
     const int want = (ntiles + kBwdWarps - 1) / kBwdWarps;
     if (!want) return;
     if (det_ws) {
