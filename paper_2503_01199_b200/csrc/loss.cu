@@ -88,6 +88,24 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
         constexpr int NROW = (IH + kThreads / 32 - 1) / (kThreads / 32);   // 4 rows per warp
         const int warp = tid >> 5, lane = tid & 31;
         float2 v[NROW][NCH];
+        // interior tiles (the whole halo inside the image; 88% at 1080p):
+        // no per-element bounds tests
+        const bool interior = ox >= 2 * R && oy >= 2 * R && ox - 2 * R + IW <= W && oy - 2 * R + IH <= H;
+        if (interior) {
+            const int base = ((oy - 2 * R) * W + ox - 2 * R + lane) * 3 + ch;
+#pragma unroll
+            for (int q = 0; q < NROW; q++) {
+                const int r = warp + q * (kThreads / 32);
+#pragma unroll
+                for (int k = 0; k < NCH; k++) {
+                    v[q][k] = make_float2(0.f, 0.f);
+                    if (r < IH && 32 * k + lane < IW) {
+                        const int idx = base + (r * W + 32 * k) * 3;
+                        v[q][k] = make_float2(x_img[idx], load_y<kU8>(y_img, y_u8, idx));
+                    }
+                }
+            }
+        } else {
 #pragma unroll
         for (int q = 0; q < NROW; q++) {
             const int r = warp + q * (kThreads / 32);
@@ -103,6 +121,7 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
                     v[q][k] = make_float2(x_img[idx], load_y<kU8>(y_img, y_u8, idx));
                 }
             }
+        }
         }
 #pragma unroll
         for (int q = 0; q < NROW; q++) {
