@@ -9,6 +9,8 @@ python tools/bench_configs.py A C D E > gpurun_out/${tag}_configs.jsonl 2> gpuru
 python tools/stage_timing.py --deterministic > gpurun_out/${tag}_det_stage_timing.json 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/${tag}_launches.csv python tools/profile_step.py --iters 5 > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_det_launches.csv \
+    python tools/profile_step.py --iters 3 --deterministic > /dev/null 2>&1
 for c in C E; do
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_${c}_launches.csv \
       python tools/config_step.py $c > /dev/null 2>&1
