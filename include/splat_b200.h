@@ -173,11 +173,13 @@ int sb_raster_fwd(const void* recs, const void* raster_rows, const int32_t* tile
  * cfg->deterministic = 0: one float atomic per (primitive, tile, channel)
  * into sgrad; rows [0, n_cap) of sgrad are zeroed first, n_cap = 0
  * accumulates into sgrad as given (rows zeroed by sb_project_cull_compact's
- * sgrad_zero).  cfg->deterministic = 1: no atomics -- one row per tile-list
- * entry, grouped by primitive with a stable radix sort and summed in tile
- * order (the reference's np.add.at order, backward.py:261-270); every row
- * [0, n_compact) of sgrad is written; n_pairs = P and n_compact = N_c of the
- * forward size the workspace.  ws: sb_raster_bwd_workspace_bytes(...); its
+ * sgrad_zero).  cfg->deterministic = 1: no atomics -- one row per
+ * contributing tile-list entry, stored at its tile's list positions,
+ * grouped by primitive with a stable radix sort over the tiles' rows in tile
+ * order and summed in tile order (the reference's np.add.at order,
+ * backward.py:261-270); every row [0, n_compact) of sgrad is written; n_pairs
+ * = P and n_compact = N_c of the forward size the workspace; tile grids above
+ * 2^20 tiles return SB_EINVAL.  ws: sb_raster_bwd_workspace_bytes(...); its
  * first sb_raster_workspace_bytes() are the tile queue (zero once). */
 size_t sb_raster_bwd_workspace_bytes(int32_t deterministic, int64_t n_pairs, int64_t n_compact);
 int sb_raster_bwd(const void* recs, const void* raster_rows, const int32_t* tile_offsets, const int32_t* tile_prims,
