@@ -242,7 +242,9 @@ struct FwdParams {
     int32_t* out_last;  // (H, W): 1 + list position of the last contributing fragment
 };
 
-__global__ void __launch_bounds__(kThreads)
+// 8 CTAs x 4 warps per SM: 64 registers (70 unbounded; 4 B of spill) for
+// 32 resident warps instead of 28 (r02h: 169.1 -> 165.4 us)
+__global__ void __launch_bounds__(kThreads, 8)
 raster_fwd_kernel(FwdParams p)
 {
     sb_pdl_begin();

