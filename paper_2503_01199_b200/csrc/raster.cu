@@ -281,16 +281,7 @@ raster_fwd_kernel(FwdParams p)
             unsigned todo = chunk_mask(pf, cnt, lane, x0, y0, p.W, p.H, p.amin);
             __syncwarp();
             if (k0 + 32 < n) prefetch_chunk(pf, p.recs, p.prims, beg, k0 + 32, min(32, n - k0 - 32), lane);
-            while (todo) {
-                const int j = __ffs(todo) - 1;
-                todo &= todo - 1;
-                const bool live = fmaxf(fmaxf(T[0], T[1]), fmaxf(T[2], T[3])) >= p.tstop;
-                if (!__any_sync(0xffffffffu, live)) {
-                    done = true;
-                    break;
-                }
-                // (no per-lane skip: a terminated lane's pixels fail the
-                // T >= t_stop test below, and SIMT runs the body anyway)
+            const auto visit = [&](int j) {
                 const SRec r = slab_get<false>(slab, j);
                 float araw[4], dx, dy;
                 lane_alpha_raw(r, px, py0, araw, dx, dy);
@@ -309,6 +300,24 @@ raster_fwd_kernel(FwdParams p)
                         last[i] = k0 + j + 1;
                     }
                 }
+            };
+            // one termination vote per two entries: a warp whose pixels all
+            // terminated on the first runs the second as a no-op (every pixel
+            // tests T >= t_stop itself; no per-lane skip: SIMT runs the body
+            // anyway)
+            while (todo) {
+                const bool live = fmaxf(fmaxf(T[0], T[1]), fmaxf(T[2], T[3])) >= p.tstop;
+                if (!__any_sync(0xffffffffu, live)) {
+                    done = true;
+                    break;
+                }
+                const int j = __ffs(todo) - 1;
+                todo &= todo - 1;
+                visit(j);
+                if (!todo) break;
+                const int j2 = __ffs(todo) - 1;
+                todo &= todo - 1;
+                visit(j2);
             }
         }
 #pragma unroll
