@@ -240,9 +240,12 @@ int sb_densify_apply(const float* params, int64_t n, const uint8_t* flags, const
  * uint8 (value / 255) when target_u8 != NULL.  loss[0] (float64, device) is
  * written on the stream (by the kernel's last CTA; it may be mapped host
  * memory).  accum: sb_loss_workspace_bytes(width, height) of scratch -- a
- * ticket and two int64 fixed-point accumulators the CTAs add their partial
- * sums into (exact integer sums: bit-reproducible in any order) -- zeroed
- * once before its first use; every call leaves it zeroed. */
+ * ticket and the int64 fixed-point accumulators the CTAs add their partial
+ * sums into (exact integer sums: bit-reproducible in any order; NaN / inf
+ * inputs propagate to the loss as in float arithmetic) -- zeroed once before
+ * its first use; every call leaves them zeroed and stores the call's sum of
+ * squared errors sum((rendered - target)^2) as a float64 in accum[9]
+ * (metrics.py psnr's numerator), valid until the next call. */
 size_t sb_loss_workspace_bytes(int32_t width, int32_t height);
 int sb_loss_fwd_bwd(const float* rendered, const float* target, const uint8_t* target_u8, int32_t width,
                     int32_t height, float lam, float* grad, double* accum, double* loss, sb_stream_t stream);

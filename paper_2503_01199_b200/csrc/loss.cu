@@ -15,9 +15,10 @@
 // pass is a register sliding window: a thread owns a short run of outputs
 // along the filter axis, loads the run + 10 inputs once from shared memory
 // and forms all outputs from registers.
-// Loss partial sums: one float64 pair per CTA, added into int64 fixed-point
-// accumulators (exact, order-independent: bit-reproducible); the last CTA to
-// finish (a ticket) forms the loss.
+// Loss partial sums: one float64 triple per CTA (L1, SSIM, squared error),
+// added into int64 fixed-point accumulators (exact, order-independent:
+// bit-reproducible; non-finite partials propagate through flags); the last
+// CTA to finish (a ticket) forms the loss and the call's squared-error sum.
 #include "common.cuh"
 
 namespace {
@@ -43,7 +44,7 @@ struct Smem {
         struct { float2 m01[FH][VW]; float2 m23[FH][VW]; float m4[FH][VW]; } vm;   // vertical moments
         struct { float2 a01[TH][FW]; float a2[TH][FW]; } av;                       // adjoint vertical pass
     } b;
-    double red[2][kThreads / 32];
+    double red[3][kThreads / 32];
 };
 
 template <bool kU8>
@@ -65,7 +66,7 @@ SB_INLINE float2 f2(float v) { return make_float2(v, v); }
 template <bool kU8>
 __global__ void __launch_bounds__(kThreads, 2)
 loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, const uint8_t* __restrict__ y_u8,
-            int W, int H, float lam, Win win, int fxp, float* __restrict__ grad, double* __restrict__ accum,
+            int W, int H, float lam, Win win, float* __restrict__ grad, double* __restrict__ accum,
             double* __restrict__ loss_out)
 {
     sb_pdl_begin();
@@ -141,8 +142,8 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
         fx[o] = xy.x;
         fy[o] = xy.y;
     }
-    // per-thread partials in float32 (at most 7 / 4 terms), reduced in float64
-    float s_part = 0.0f, l1_part = 0.0f;
+    // per-thread partials in float32 (at most 7 / 4 / 4 terms), reduced in float64
+    float s_part = 0.0f, l1_part = 0.0f, l2_part = 0.0f;
 
     // (2) vertical moments on rows [oy-5, oy+TH+5): column c, runs of 7 rows
     {
@@ -322,9 +323,10 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
             const float xv = fx[o], yv = fy[o];
             const float g_ssim = t01[o].x + t01[o].y * yv + t2[o] * (2.f * xv);
             const float diff = xv - yv;
-            const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
+            const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : diff * 0.f);   // np.sign (NaN stays NaN)
             grad[idx] = sgn * l1_scale - ssim_scale * g_ssim;
             l1_part += fabsf(diff);
+            l2_part = fmaf(diff, diff, l2_part);
         }
     }
     // block reduction of the two loss partials: each warp sums its lanes in
@@ -332,38 +334,78 @@ loss_kernel(const float* __restrict__ x_img, const float* __restrict__ y_img, co
     // thread 0 sums the 16 warp totals in float64 in a fixed order.
     const int lane = tid & 31, warp = tid >> 5;
     float s_w = s_part, l_w = l1_part;
+    double q_w = (double)l2_part;    // squared errors in float64 past the thread (psnr)
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
         s_w += __shfl_xor_sync(0xffffffffu, s_w, o);
         l_w += __shfl_xor_sync(0xffffffffu, l_w, o);
+        q_w += __shfl_xor_sync(0xffffffffu, q_w, o);
     }
-    if (lane == 0) { sm.red[0][warp] = (double)l_w; sm.red[1][warp] = (double)s_w; }
+    if (lane == 0) { sm.red[0][warp] = (double)l_w; sm.red[1][warp] = (double)s_w; sm.red[2][warp] = q_w; }
     __syncthreads();
     if (tid != 0) return;
-    // The CTA's partials are added into two int64 fixed-point accumulators
-    // (2^-fxp units; integer addition is exact and order-independent, so the
-    // loss is bit-reproducible without a fixed summation order), and only
-    // this thread waits on the ticket: the last CTA to arrive forms the loss
-    // and re-zeroes the accumulators and the ticket for the next call.
-    double a = 0, b = 0;
+    // The CTA's partials go into int64 fixed-point accumulators (integer
+    // addition is exact and order-independent, so the loss is
+    // bit-reproducible without a fixed summation order): L1 and SSIM in
+    // 2^-30 units, the squared error as a 2^-20 part plus its 2^-50
+    // remainder (psnr needs its small sums to full precision).  Only this
+    // thread waits on the ticket: the last CTA to arrive forms the loss and
+    // re-zeroes the accumulators and the ticket for the next call.  A partial
+    // too large for its accumulator's share of the int64 range (|x - y|
+    // beyond ~300, far outside image values) goes into a float64 sum
+    // instead (order-dependent; empty for image-range inputs), and
+    // non-finite partials set flags, so NaN / +inf / -inf reach the loss as
+    // in float arithmetic (the divergence guard, train.py:100).
+    double part[3] = {0, 0, 0};
 #pragma unroll
-    for (int q = 0; q < kThreads / 32; q++) { a += sm.red[0][q]; b += sm.red[1][q]; }
-    unsigned long long* ticket = reinterpret_cast<unsigned long long*>(accum);
-    unsigned long long* acc = ticket + 1;     // [0] L1 sum, [1] SSIM sum
-    atomicAdd(acc, (unsigned long long)__double2ll_rn(ldexp(a, fxp)));
-    atomicAdd(acc + 1, (unsigned long long)__double2ll_rn(ldexp(b, fxp)));
+    for (int q = 0; q < kThreads / 32; q++) { part[0] += sm.red[0][q]; part[1] += sm.red[1][q]; part[2] += sm.red[2][q]; }
+    unsigned long long* acw = reinterpret_cast<unsigned long long*>(accum);
+    // [0] ticket, [1] L1, [2] SSIM, [3] squared error 2^-20 part, [4] its
+    // 2^-50 remainder, [5..7] float64 sums of oversized partials, [8] flags,
+    // [9] the call's squared-error sum (result)
+    const double ncta_d = (double)gridDim.x * gridDim.y * gridDim.z;
+    unsigned long long flags = 0;
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        const double v = part[q];
+        if (isnan(v)) { flags |= 1ull << q; continue; }
+        if (isinf(v)) { flags |= 1ull << (v > 0 ? 3 + q : 6 + q); continue; }
+        const int sc = q < 2 ? 30 : 20;
+        if (fabs(v) * ncta_d >= ldexp(1.0, 62 - sc)) {      // could overflow the shared int64 sum
+            atomicAdd(reinterpret_cast<double*>(acw + 5 + q), v);
+            continue;
+        }
+        const long long hi = __double2ll_rn(ldexp(v, sc));
+        atomicAdd(acw + 1 + q, (unsigned long long)hi);
+        if (q == 2) atomicAdd(acw + 4, (unsigned long long)__double2ll_rn(ldexp(v - ldexp((double)hi, -sc), 50)));
+    }
+    if (flags) atomicOr(acw + 8, flags);
     __threadfence();
-    const unsigned long long ncta = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
-    if (atomicAdd(ticket, 1ull) != ncta - 1) return;
+    if (atomicAdd(acw, 1ull) != (unsigned long long)ncta_d - 1) return;
     __threadfence();
-    const double l1 = ldexp((double)(long long)atomicExch(acc, 0ull), -fxp);
-    const double ss = ldexp((double)(long long)atomicExch(acc + 1, 0ull), -fxp);
+    const unsigned long long fl = atomicExch(acw + 8, 0ull);
+    double sum[3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        const int sc = q < 2 ? 30 : 20;
+        double v = ldexp((double)(long long)atomicExch(acw + 1 + q, 0ull), -sc);
+        if (q == 2) v += ldexp((double)(long long)atomicExch(acw + 4, 0ull), -50);
+        v += __longlong_as_double((long long)atomicExch(acw + 5 + q, 0ull));
+        const bool pinf = (fl >> (3 + q)) & 1, ninf = (fl >> (6 + q)) & 1;
+        if (pinf) v = ninf ? __longlong_as_double(0x7ff8000000000000ll) : __longlong_as_double(0x7ff0000000000000ll);
+        else if (ninf) v = __longlong_as_double((long long)0xfff0000000000000ull);
+        if ((fl >> q) & 1) v = __longlong_as_double(0x7ff8000000000000ll);
+        sum[q] = v;
+    }
+    // the call's sum of squared errors (metrics.py psnr's numerator) stays
+    // in accum[9] until the next call
+    accum[9] = sum[2];
     const double n = (double)W * H * 3.0;
     const double ni = (double)(W - 2 * R) * (double)(H - 2 * R);
-    double l = (1.0 - lam) * l1 / n;
-    if (lam != 0.f) l += lam * (1.0 - (ni > 0 ? ss / (3.0 * ni) : 0.0));
+    double l = (1.0 - lam) * sum[0] / n;
+    if (lam != 0.f) l += lam * (1.0 - (ni > 0 ? sum[1] / (3.0 * ni) : 0.0));
     *loss_out = l;
-    atomicExch(ticket, 0ull);
+    atomicExch(acw, 0ull);
 }
 
 }  // namespace
@@ -382,17 +424,13 @@ void sb_launch_loss(const float* x, const float* y, const uint8_t* y_u8, int W, 
     sb_smem_attr(loss_kernel<true>, (int)sizeof(Smem));
     sb_smem_attr(loss_kernel<false>, (int)sizeof(Smem));
     dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, 3);
-    // fixed-point scale of the loss accumulators: each sum is at most
-    // 3 W H (|L1 term|, |SSIM| <= 1), kept below 2^62
-    int fx = 36;
-    while (fx > 0 && ldexp(3.0 * (double)W * (double)H, fx) >= 0x1p62) fx--;
     if (y_u8)
-        sb_launch(loss_kernel<true>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, fx, grad, accum, loss);
+        sb_launch(loss_kernel<true>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad, accum, loss);
     else
-        sb_launch(loss_kernel<false>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, fx, grad,
+        sb_launch(loss_kernel<false>, grid, kThreads, sizeof(Smem), stream, x, y, y_u8, W, H, lam, win, grad,
                   accum, loss);
 }
 
 size_t sb_loss_accum_bytes(int, int) {
-    return 32;   // ticket + two int64 fixed-point sums (+ pad)
+    return 128;   // ticket, fixed-point / float64 sums, flags, the last call's squared-error sum
 }

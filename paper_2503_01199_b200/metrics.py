@@ -95,14 +95,18 @@ def psnr(a, b) -> float:
     return math.inf if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
 
 
-def loss_and_grad(rendered: torch.Tensor, target, lam: float, return_tensor: bool = False, loss_out=None):
+def loss_and_grad(rendered: torch.Tensor, target, lam: float, return_tensor: bool = False, loss_out=None,
+                  sse_out=None):
     """(loss, dL/d rendered) for (H, W, 3) images (metrics.py:118-132), fused
     kernel.  `target` may be float (any dtype) or uint8 (value / 255).  With
     return_tensor=True the loss stays a 0-d float64 device tensor (no sync).
     `loss_out`: a 1-element float64 tensor in pinned host memory that the
     kernel writes directly (mapped, zero-copy; no device-to-host copy in the
     stream) -- valid once the stream has reached this point; returned as the
-    loss tensor with return_tensor=True."""
+    loss tensor with return_tensor=True.  `sse_out`: a 1-element float64
+    device tensor that receives the call's sum of squared errors
+    sum((rendered - target)^2) in float64 (psnr's numerator, formed by the
+    same kernel; a device-to-device copy, no host sync)."""
     import ctypes as C
     from . import _lib
     from .errors import ShapeMismatchError
@@ -134,6 +138,8 @@ def loss_and_grad(rendered: torch.Tensor, target, lam: float, return_tensor: boo
         out_ptr = _lib.ptr(out)
     _lib.call("sb_loss_fwd_bwd", _lib.ptr(x), _lib.ptr(y), _lib.ptr(y8), W, H, float(lam), _lib.ptr(grad),
               _lib.ptr(acc), out_ptr, C.c_void_p(_lib.stream_ptr(x.device)))
+    if sse_out is not None:
+        sse_out.copy_(acc[72:80].view(torch.float64))
     if loss_out is not None and out is not loss_out:
         loss_out.copy_(out, non_blocking=True)   # not mappable: an async copy instead
         out = loss_out

@@ -432,6 +432,55 @@ def test_fused_loss_sizes_vs_torch(W, H):
     assert (grad.double().cpu() - g_ref).abs().max().item() <= 1e-4 * g_ref.abs().max().item()
     loss_b, grad_b = sb.loss_and_grad(x, y, 0.2)
     assert loss_b == loss and torch.equal(grad_b, grad)
+    # the same kernel's sum of squared errors (train()'s per-view PSNR)
+    sse = torch.full((1,), -1.0, dtype=torch.float64, device="cuda")
+    sb.loss_and_grad(x, y, 0.2, sse_out=sse)
+    ref = ((xd - yd) ** 2).sum().item()
+    assert abs(sse.item() - ref) <= 1e-8 * ref   # float32 per-thread partials (4 terms)
+    mse = ref / xd.numel()
+    assert abs(10 * np.log10(1 / (sse.item() / xd.numel())) - sb.psnr(x, y)) <= 1e-8 * abs(10 * np.log10(1 / mse))
+
+
+def test_fused_loss_nonfinite_and_wide_range():
+    """metrics.py:118-132 in float64: a NaN in the target makes the loss NaN
+    and an inf makes it non-finite (the divergence guard, train.py:100);
+    0-255-valued float images (far outside [0, 1]) give the float64 loss."""
+    sb = _sb()
+    from paper_2503_01199_b200.metrics import _chw, _ssim_terms
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.rand((1080, 1920, 3), device="cuda", generator=g)
+    y = torch.rand((1080, 1920, 3), device="cuda", generator=g)
+    for bad, check in ((float("nan"), np.isnan), (float("inf"), lambda v: not np.isfinite(v))):
+        yb = y.clone()
+        yb[7, 11, 1] = bad
+        loss, grad = sb.loss_and_grad(x, yb, 0.2)
+        assert check(loss), (bad, loss)
+        loss1, _ = sb.loss_and_grad(x, yb, 0.0)
+        assert check(loss1), (bad, loss1)
+        l_ok, _ = sb.loss_and_grad(x, y, 0.2)     # the workspace is clean again
+        assert np.isfinite(l_ok)
+    xs, ys = x * 255.0, y * 255.0
+    loss, _ = sb.loss_and_grad(xs, ys, 0.2)
+    xd, yd = xs.double().cpu(), ys.double().cpu()
+    vals, _ = _ssim_terms(_chw(xd), _chw(yd), False)
+    l_ref = 0.8 * (xd - yd).abs().mean().item() + 0.2 * (1.0 - vals.mean().item())
+    assert abs(loss - l_ref) <= 1e-5 * abs(l_ref)
+
+
+def test_train_divergence_guard():
+    """test_train.py:96-104: a NaN in the target raises TrainingDiverged in
+    epoch 1."""
+    sb = _sb()
+    d = G.load("golden_A.npz")
+    sc = G.scene(d)
+    scene = sb.SceneSoA(*[sc[k] for k in G.CH], device="cuda")
+    cam = sb.CameraView.from_any(G.camera(d))
+    W, H = cam.resolution
+    bad = np.zeros((H, W, 3))
+    bad[0, 0, 0] = np.nan
+    with pytest.raises(sb.TrainingDiverged) as e:
+        sb.train(sb.TrainConfig(epochs=1), scene, [(cam, bad)])
+    assert e.value.epoch == 1
 
 
 @pytest.mark.parametrize("fname,prefix", [("golden_A.npz", ""), ("golden_edge.npz", "e1_")])
