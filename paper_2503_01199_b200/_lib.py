@@ -122,9 +122,9 @@ _stream_device: dict = {}
 
 def device_index(device=None) -> int:
     if isinstance(device, torch.device):
-        return device.index if device.index is not None else torch._C._cuda_getDevice()
+        return device.index if device.index is not None else torch.cuda.current_device()
     if device is None:
-        return torch._C._cuda_getDevice()
+        return torch.cuda.current_device()
     if isinstance(device, int):
         return device
     return device_index(torch.device(device))
@@ -133,16 +133,22 @@ def device_index(device=None) -> int:
 _cuda_ready = False
 
 
+_raw_current = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def raw_stream(device=None) -> tuple:
     """(device index, current stream handle) without constructing a
     torch.cuda.Stream (the per-call host cost of torch.cuda.current_stream
-    is a visible share of a small-scene iteration)."""
+    is a visible share of a small-scene iteration); torch builds without the
+    raw accessor take the public path."""
     global _cuda_ready
     if not _cuda_ready:
         torch.cuda.init()
         _cuda_ready = True
     idx = device_index(device)
-    return idx, torch._C._cuda_getCurrentRawStream(idx)
+    if _raw_current is None:
+        return idx, torch.cuda.current_stream(idx).cuda_stream
+    return idx, _raw_current(idx)
 
 
 def stream_ptr(device=None) -> int:
