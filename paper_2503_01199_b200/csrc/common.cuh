@@ -417,6 +417,12 @@ SB_INLINE bool sb_disc_hits(float cx, float cy, float r, int tx, int ty, int W, 
     return DADD(DMUL(dx, dx), DMUL(dy, dy)) <= (double)rr;
 }
 
+// sb_disc_hits out of line: the float64 fallback is rarely taken, and
+// inlined its row-invariant float64 terms are hoisted into every row's setup
+static __device__ __noinline__ bool sb_disc_hits_slow(float cx, float cy, float r, int tx, int ty, int W, int H) {
+    return sb_disc_hits(cx, cy, r, tx, ty, W, H);
+}
+
 // The same decision with a float32 filter.  Each float32 difference of an
 // integer <= W (or H) and cx (cy) is within E = (|cx| + |cy| + W + H) 2^-23
 // of the exact one, so |q32 - Q64| <= 2 (dx + dy + E) E + 2^-22 (q + rr).
@@ -460,7 +466,7 @@ SB_INLINE int sb_row_hits(float cx, float cy, float r, int ty, int tx0, int tx1,
         const float m = fmaf(e2, dx, fmaf(q, 2.384185791e-7f * kInfl, mrow));
         if (q < rr - m) return true;
         if (q > rr + m) return false;
-        return sb_disc_hits(cx, cy, r, tx, ty, W, H);
+        return sb_disc_hits_slow(cx, cy, r, tx, ty, W, H);
     };
     a = tx0;
     while (a <= tx1 && !hit(a)) a++;
