@@ -88,20 +88,17 @@ SB_INLINE float rcp_approx(float x) {
     return y;
 }
 
-// The 16-byte chunks of record l sit XOR-swizzled by (l >> 1) & 3, so the
-// 32 lanes' 128-bit stores in commit_chunk (64-byte record stride) hit every
-// bank group of a quarter warp once instead of four times.
-// (The backward, bound by shared memory, uses it; the issue-bound forwards
-// keep the plain layout, whose 3 extra wavefronts per chunk cost less than
-// the swizzle arithmetic per fragment.)
-template <bool kSwz>
-SB_INLINE int slab_swizzle(int l) { return kSwz ? (l >> 1) & 3 : 0; }
-
+// The 32-record warp slab is stored part-major (float4 part p of record j
+// at float4 index 32 p + j): a chunk commit writes 32 consecutive float4s
+// per part (conflict-free), and a fragment's broadcast read is four LDS.128
+// at one uniform base (16 j) with immediate part offsets (r02: records
+// contiguous, XOR-swizzled in the backward, whose read side paid the swizzle
+// arithmetic per fragment).  kSwz is kept for the call sites; both layouts
+// are now the same.
 template <bool kSwz>
 SB_INLINE SRec slab_get(const SRec* slab, int j) {
-    const float4* b = reinterpret_cast<const float4*>(slab + j);
-    const int sw = slab_swizzle<kSwz>(j);
-    const float4 c0 = b[0 ^ sw], c1 = b[1 ^ sw], c2 = b[2 ^ sw], c3 = b[3 ^ sw];
+    const float4* b = reinterpret_cast<const float4*>(slab) + j;
+    const float4 c0 = b[0], c1 = b[32], c2 = b[64], c3 = b[96];
     SRec r;
     r.x = c0.x; r.y = c0.y; r.A = c0.z; r.B = c0.w;
     r.Cq = c1.x; r.o = c1.y; r.r = c1.z; r.g = c1.w;
@@ -114,14 +111,13 @@ template <bool kSwz>
 SB_INLINE void commit_chunk(SRec* slab, const Prefetch& pf, int cnt, int lane) {
     if (lane < cnt) {
         const float A = kHalfLog2e * pf.a.z, B = kLog2e * pf.a.w, Cq = kHalfLog2e * pf.b.x;
-        float4* d = reinterpret_cast<float4*>(slab + lane);
-        const int sw = slab_swizzle<kSwz>(lane);
-        d[0 ^ sw] = make_float4(pf.a.x, pf.a.y, A, B);
-        d[1 ^ sw] = make_float4(Cq, pf.b.y, pf.b.z, pf.b.w);
+        float4* d = reinterpret_cast<float4*>(slab) + lane;
+        d[0] = make_float4(pf.a.x, pf.a.y, A, B);
+        d[32] = make_float4(Cq, pf.b.y, pf.b.z, pf.b.w);
         const float io = rcp_approx(pf.b.y), io32 = io * 4294967296.0f;
         // (finite even for opacities far below any alpha_min: 0 * s2io = 0)
-        d[2 ^ sw] = make_float4(pf.bl, __log2f(pf.b.y), io, fminf(io32 * io32, 3.0e38f));
-        d[3 ^ sw] = make_float4(pf.a.z, pf.a.w, pf.b.x, __int_as_float(pf.slot));
+        d[64] = make_float4(pf.bl, __log2f(pf.b.y), io, fminf(io32 * io32, 3.0e38f));
+        d[96] = make_float4(pf.a.z, pf.a.w, pf.b.x, __int_as_float(pf.slot));
     }
 }
 
