@@ -738,6 +738,35 @@ def test_deterministic_backward(fname, prefix):
     assert l1 == l2 and torch.equal(g1, g2)
 
 
+def test_deterministic_backward_config_b():
+    """The deterministic backward at the benchmarked size (config B: 1M
+    Gaussians, 1080p, 16,200 tiles -- several rounds of the tile scan, 13.7M
+    tile-list positions): two runs bit-identical in gradients and S / M / C,
+    C equal to the fast path's integer counts, gradients within float-atomic
+    order noise of the fast path."""
+    sb = _sb()
+    from paper_2503_01199_b200.synthetic import SyntheticSceneSpec, camera_ring, scaled_scene_arrays
+    n, res = 1_000_000, (1920, 1080)
+    arr = scaled_scene_arrays(n, 7, res)
+    scene = sb.SceneSoA(*[arr[k] for k in G.CH], device="cuda")
+    sb.morton_sort(scene)
+    cam = camera_ring(SyntheticSceneSpec(n_gaussians=n, n_views=1, view_resolution=res, seed=7))[0]
+    g = torch.Generator(device="cuda").manual_seed(3)
+    target = torch.rand((res[1], res[0], 3), device="cuda", generator=g)
+    runs = {}
+    for name, det in (("d1", True), ("d2", True), ("fast", False)):
+        out, ctx = sb.forward(scene, cam, sb.RasterConfig(deterministic=det))
+        _, dI = sb.loss_and_grad(out.color, target, 0.2, return_tensor=True)
+        st = sb.DensifyStats.zeros(scene.n, scene.device)
+        r = sb.backward(scene, ctx, dI, st)
+        runs[name] = (r.grads.packed.clone(), st.S.clone(), st.M.clone(), st.C.clone())
+    assert ctx.camera.tiles[0] * ctx.camera.tiles[1] > 8 * 1024
+    assert all(torch.equal(a, b) for a, b in zip(runs["d1"], runs["d2"]))
+    assert torch.equal(runs["d1"][3], runs["fast"][3])
+    gd, gf = runs["d1"][0], runs["fast"][0]
+    assert ((gd - gf).abs().max() / gf.abs().max()).item() <= 1e-5
+
+
 def test_deterministic_training_checkpoints(tmp_path):
     """The reference's acceptance criterion 12 (test_acceptance.py:397-418)
     through the device path: two seeded deterministic train() runs with
