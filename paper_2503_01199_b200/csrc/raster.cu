@@ -494,17 +494,7 @@ raster_fwd_half2_kernel(FwdParams p)
             unsigned todo = chunk_mask(pf, cnt, lane, x0, y0, p.W, p.H, p.amin);
             __syncwarp();
             if (k0 + 32 < n) prefetch_chunk(pf, p.recs, p.prims, beg, k0 + 32, min(32, n - k0 - 32), lane);
-            while (todo) {
-                const int j = __ffs(todo) - 1;
-                todo &= todo - 1;
-                // live: some valid pixel with T >= t_stop (the scalar kernel's test)
-                const H2 l0 = __hmul2(vmask[0], __hge2(T[0], tstop)), l1 = __hmul2(vmask[1], __hge2(T[1], tstop));
-                const H2 lv = __hadd2(l0, l1);
-                const bool live = O::to(__low2half_t(lv)) + O::to(__high2half_t(lv)) > 0.0f;
-                if (!__any_sync(0xffffffffu, live)) {
-                    done = true;
-                    break;
-                }
+            const auto visit = [&](int j) {
                 const SRec r = slab_get<false>(slab, j);
                 float G[4], dx, dy;
                 lane_G(r, px, py0, G, dx, dy);
@@ -527,6 +517,25 @@ raster_fwd_half2_kernel(FwdParams p)
                     last[2 * h] = b0 ? k0 + j + 1 : last[2 * h];
                     last[2 * h + 1] = b1 ? k0 + j + 1 : last[2 * h + 1];
                 }
+            };
+            // one termination vote per two entries, as the fp32 forward (a
+            // terminated pixel's blend test fails, so the second is a no-op)
+            while (todo) {
+                // live: some valid pixel with T >= t_stop (the scalar kernel's test)
+                const H2 l0 = __hmul2(vmask[0], __hge2(T[0], tstop)), l1 = __hmul2(vmask[1], __hge2(T[1], tstop));
+                const H2 lv = __hadd2(l0, l1);
+                const bool live = O::to(__low2half_t(lv)) + O::to(__high2half_t(lv)) > 0.0f;
+                if (!__any_sync(0xffffffffu, live)) {
+                    done = true;
+                    break;
+                }
+                const int j = __ffs(todo) - 1;
+                todo &= todo - 1;
+                visit(j);
+                if (!todo) break;
+                const int j2 = __ffs(todo) - 1;
+                todo &= todo - 1;
+                visit(j2);
             }
         }
         const H2 bg[3] = {P::bcast(O::from(p.bg[0])), P::bcast(O::from(p.bg[1])), P::bcast(O::from(p.bg[2]))};
