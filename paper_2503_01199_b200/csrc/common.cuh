@@ -297,12 +297,14 @@ struct ProjOut {
 // The backward chain only needs them to float32 accuracy (gradient
 // tolerance), so it uses the float32 forms.
 template <bool kExact = true>
-SB_INLINE void sb_project(const float* __restrict__ p, const CamDev& cam, ProjOut& o, double* s64 = nullptr) {
-    // activations in float64, then rounded (projection.py:134-138)
+SB_INLINE void sb_project(const float* __restrict__ p, const CamDev& cam, ProjOut& o, double* s64 = nullptr,
+                          const double* s_in = nullptr) {
+    // activations in float64, then rounded (projection.py:134-138); s_in:
+    // exp(log_scale) already formed by the caller (the same float64 values)
     float pos[3] = {p[0], p[1], p[2]};
     if (kExact) {
         for (int k = 0; k < 3; k++) {
-            const double e = exp((double)p[SB_COL_LS + k]);
+            const double e = s_in ? s_in[k] : exp((double)p[SB_COL_LS + k]);
             if (s64) s64[k] = e;
             o.s[k] = (float)e;
         }
@@ -580,9 +582,10 @@ SB_INLINE bool sb_aabb_in_frustum(const double lo[3], const double hi[3], const 
 
 // ccc.py:125-130: one member's contribution to its cluster's AABB,
 // p -+ 3 * max(exp(log_scale)) in float64 (scene.scales() is float64)
-SB_INLINE void sb_member_reach(const float* p, double lo[3], double hi[3]) {
-    const double m = fmax(fmax(exp((double)p[SB_COL_LS]), exp((double)p[SB_COL_LS + 1])),
-                          exp((double)p[SB_COL_LS + 2]));
+SB_INLINE void sb_member_reach(const float* p, double lo[3], double hi[3], double* s_out = nullptr) {
+    const double e0 = exp((double)p[SB_COL_LS]), e1 = exp((double)p[SB_COL_LS + 1]), e2 = exp((double)p[SB_COL_LS + 2]);
+    if (s_out) { s_out[0] = e0; s_out[1] = e1; s_out[2] = e2; }
+    const double m = fmax(fmax(e0, e1), e2);
     const double reach = DMUL(3.0, m);
     for (int k = 0; k < 3; k++) {
         lo[k] = fmin(lo[k], DSUB((double)p[k], reach));

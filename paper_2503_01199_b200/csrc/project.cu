@@ -22,6 +22,7 @@ constexpr int kThreads = kWarps * 32;
 
 struct WarpStage {
     RasterRec rec[SB_CLUSTER_SIZE];
+    double scale[3][SB_CLUSTER_SIZE];   // pass 1's exp(log_scale), reused by the projection
 };
 
 SB_INLINE double warp_min_d(double v) {
@@ -73,7 +74,12 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
                 if (g < n) {
                     const float4 v0 = __ldg(params + (size_t)g * 4), v1 = __ldg(params + (size_t)g * 4 + 1);
                     const float p3[6] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y};
-                    sb_member_reach(p3, lo, hi);
+                    double e[3];
+                    sb_member_reach(p3, lo, hi, e);
+                    const int slot = j * 32 + lane;
+                    stage[warp].scale[0][slot] = e[0];
+                    stage[warp].scale[1][slot] = e[1];
+                    stage[warp].scale[2][slot] = e[2];
                 }
             }
             for (int k = 0; k < 3; k++) {
@@ -108,7 +114,13 @@ project_cull_compact_kernel(const float4* __restrict__ params, int n, int n_clus
                     p[4 * k] = v.x; p[4 * k + 1] = v.y; p[4 * k + 2] = v.z; p[4 * k + 3] = v.w;
                 }
                 ProjOut o;
-                sb_project(p, cam, o);
+                if (need_box) {
+                    const double sc[3] = {stage[warp].scale[0][slot], stage[warp].scale[1][slot],
+                                          stage[warp].scale[2][slot]};
+                    sb_project(p, cam, o, nullptr, sc);
+                } else {
+                    sb_project(p, cam, o);
+                }
                 r.x = o.x; r.y = o.y; r.a = o.ca; r.b = o.cb; r.c = o.cc; r.o = o.op;
                 r.r = o.col[0]; r.g = o.col[1]; r.bl = o.col[2]; r.depth = o.depth; r.radius = o.radius;
                 any_in |= o.in_image;
