@@ -467,6 +467,29 @@ def test_fused_loss_nonfinite_and_wide_range():
     assert abs(loss - l_ref) <= 1e-5 * abs(l_ref)
 
 
+def test_train_epoch_psnr_from_loss_kernel():
+    """train()'s per-view PSNR comes from the loss kernel's squared-error sum
+    (no host sync per view): with zero learning rates the epoch row equals
+    metrics.psnr / loss_and_grad of the rendered image (train.py:107-121)."""
+    sb = _sb()
+    d = G.load("golden_A.npz")
+    sc = G.scene(d)
+    scene = sb.SceneSoA(*[sc[k] for k in G.CH], device="cuda")
+    sb.morton_sort(scene)
+    cam = sb.CameraView.from_any(G.camera(d))
+    W, H = cam.resolution
+    target = np.random.default_rng(4).uniform(0.0, 1.0, (H, W, 3))
+    out, _ = sb.forward(scene, cam)
+    ref_psnr = sb.psnr(out.color, torch.from_numpy(target).float().cuda())
+    ref_loss, _ = sb.loss_and_grad(out.color, torch.from_numpy(target).float().cuda(), 0.2)
+    lrs = sb.LearningRates(position=1e-30, position_final=1e-30, log_scale=0.0, rotation=0.0, color=0.0,
+                           opacity_logit=0.0)
+    r = sb.train(sb.TrainConfig(epochs=1, lrs=lrs), scene, [(cam, target)])
+    row = r.metrics[0]
+    assert abs(row.psnr - ref_psnr) <= 1e-8 * abs(ref_psnr)
+    assert row.loss == ref_loss
+
+
 def test_train_divergence_guard():
     """test_train.py:96-104: a NaN in the target raises TrainingDiverged in
     epoch 1."""
